@@ -1,0 +1,372 @@
+"""Python access to the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Imported only by tests/, __graft_entry__.smoke() (as the checker) and
+bench.py's cpu_baseline / ``--impl reference`` legs.  The product package
+(paper_1810_02612_b200) never imports this module.
+
+Two backends:
+  * ``Oracle``  -- oracle/liboracle.so, the C restatement (ltlg_oracle.c) of
+    the reference labeling path, each function citing the reference file:line.
+  * ``RefCore`` -- oracle/_ref/libltlgrid_ref.so, the UNMODIFIED reference core
+    compiled from /root/reference by oracle/Makefile, behind ref_shim.cpp.
+
+Plus numpy restatements of the reference test-input generators
+(SplitMix64 ``random_rows`` of test_label.cpp:29-40, ``to_csr`` of
+label.cpp:42-57) so fixtures can be regenerated bit-exactly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libltlgrid_ref.so")
+
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+# ---------------------------------------------------------------------------
+# SplitMix64 (rng.hpp:10-34), vectorised
+# ---------------------------------------------------------------------------
+
+class SplitMix64:
+    """Stateful SplitMix64 identical to ltlgrid::SplitMix64 (rng.hpp:10-29)."""
+
+    def __init__(self, seed: int):
+        self.state = np.uint64(seed & 0xFFFFFFFFFFFFFFFF)
+
+    def next_block(self, n: int) -> np.ndarray:
+        with np.errstate(over="ignore"):
+            k = np.arange(1, n + 1, dtype=np.uint64)
+            z = self.state + k * _GOLDEN
+            self.state = np.uint64(self.state + np.uint64(n) * _GOLDEN)
+            z = (z ^ (z >> np.uint64(30))) * _M1
+            z = (z ^ (z >> np.uint64(27))) * _M2
+            return z ^ (z >> np.uint64(31))
+
+    def next(self) -> int:
+        return int(self.next_block(1)[0])
+
+    def uniform_block(self, n: int) -> np.ndarray:
+        """SplitMix64::uniform (rng.hpp:21): (next >> 11) * 2^-53."""
+        return (self.next_block(n) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+    def below(self, n: int) -> int:
+        return self.next() % n if n else 0
+
+
+def mix_seed(seed: int, stream: int) -> int:
+    """mix_seed, rng.hpp:31-34."""
+    with np.errstate(over="ignore"):
+        s = np.uint64(seed) ^ (np.uint64(stream) * _GOLDEN + np.uint64(0x2545F4914F6CDD1D))
+    return SplitMix64(int(s)).next()
+
+
+def random_rows(rng: SplitMix64, rows: int, cols: int, density: float) -> np.ndarray:
+    """random_rows of test_label.cpp:29-40: row-major Bernoulli(density)."""
+    return (rng.uniform_block(rows * cols) < density).reshape(rows, cols)
+
+
+def to_csr(dense: np.ndarray):
+    """to_csr, label.cpp:42-57 (ascending set bits per row via collect)."""
+    dense = np.asarray(dense, dtype=bool)
+    rows = dense.shape[0]
+    counts = dense.sum(axis=1).astype(np.uint64)
+    offsets = np.zeros(rows + 1, dtype=np.uint64)
+    np.cumsum(counts, out=offsets[1:])
+    indices = np.nonzero(dense)[1].astype(np.uint32)
+    return offsets, indices
+
+
+def bits_to_words(bits: np.ndarray) -> np.ndarray:
+    """Bool [n, cells] -> u64 words [n, ceil(cells/64)], LE bit i = cell i
+    (OccupancyBitset layout, grid.hpp:93-125)."""
+    bits = np.atleast_2d(np.asarray(bits, dtype=bool))
+    n, cells = bits.shape
+    nw = (cells + 63) // 64
+    padded = np.zeros((n, nw * 64), dtype=bool)
+    padded[:, :cells] = bits
+    by = np.packbits(padded.reshape(n, nw * 8, 8), axis=2, bitorder="little").reshape(n, nw * 8)
+    return np.ascontiguousarray(by).view(np.uint64).reshape(n, nw)
+
+
+def words_to_bits(words: np.ndarray, cells: int) -> np.ndarray:
+    words = np.atleast_2d(np.ascontiguousarray(words, dtype=np.uint64))
+    by = words.view(np.uint8)
+    return np.unpackbits(by, axis=1, bitorder="little")[:, :cells].astype(bool)
+
+
+def labels_dense(words: np.ndarray, rows: int, props: int) -> np.ndarray:
+    """LabelMatrix words (label.hpp:61-92) -> bool [rows, props]."""
+    if props == 0:
+        return np.zeros((rows, 0), dtype=bool)
+    wpr = (props + 63) // 64
+    w = np.asarray(words, dtype=np.uint64).reshape(rows, wpr)
+    return words_to_bits(w, wpr * 64)[:, :props]
+
+
+def dense_label(dense_rows: np.ndarray, dense_cols: np.ndarray) -> np.ndarray:
+    """oracles::label_triple_loop (tests/support/oracles.hpp:203-216) as a
+    boolean matrix product."""
+    m = np.asarray(dense_rows, dtype=np.int64)
+    p = np.asarray(dense_cols, dtype=np.int64)
+    if p.shape[0] == 0:
+        return np.zeros((m.shape[0], 0), dtype=bool)
+    return (m @ p.T) > 0
+
+
+def labels_to_words(dense: np.ndarray) -> np.ndarray:
+    rows, props = dense.shape
+    wpr = (props + 63) // 64
+    if wpr == 0:
+        return np.zeros(0, dtype=np.uint64)
+    padded = np.zeros((rows, wpr * 64), dtype=bool)
+    padded[:, :props] = dense
+    return bits_to_words(padded).reshape(-1)
+
+
+# ---------------------------------------------------------------------------
+# ctypes backends
+# ---------------------------------------------------------------------------
+
+def _p(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct)) if a is not None else None
+
+
+def build_oracle() -> None:
+    subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
+
+
+class OracleError(ValueError):
+    pass
+
+
+class Oracle:
+    """oracle/liboracle.so -- the C restatement."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            build_oracle()
+        L = C.CDLL(path)
+        u64, u32, i32 = C.c_uint64, C.c_uint32, C.c_int
+        P64, P32 = C.POINTER(u64), C.POINTER(u32)
+        L.oracle_label_all.argtypes = [u64, u64, P64, P32, u64, i32, P64, i32, P64, C.c_char_p, C.c_size_t]
+        L.oracle_label_all.restype = i32
+        L.oracle_validate_csr.argtypes = [u64, u64, P64, u64, P32, u64, C.c_char_p, C.c_size_t]
+        L.oracle_validate_csr.restype = i32
+        L.oracle_label_edge_counting.argtypes = [P32, u64, P64, P64]
+        L.oracle_label_edge_counting.restype = i32
+        L.oracle_z_index_of_cells.argtypes = [i32, i32, P64]
+        L.oracle_z_index_of_cells.restype = u64
+        L.oracle_z_index.argtypes = [i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.oracle_z_index.restype = u64
+        L.oracle_z_index_tree_descent.argtypes = L.oracle_z_index.argtypes
+        L.oracle_z_index_tree_descent.restype = u64
+        L.oracle_mix_seed.argtypes = [u64, u64]
+        L.oracle_mix_seed.restype = u64
+        L.oracle_effective_workers.argtypes = [i32, u64]
+        L.oracle_effective_workers.restype = i32
+        d = C.c_double
+        L.oracle_resample.argtypes = [i32, d, d, d, d, i32, d, d, d, d, d, d, d, d, i32, P64, i32, P64]
+        L.oracle_resample.restype = None
+        self.lib = L
+
+    def label_all(self, rows, cols, offsets, indices, cells, props, colwords, workers=0):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        indices = np.ascontiguousarray(indices, dtype=np.uint32)
+        colwords = np.ascontiguousarray(colwords, dtype=np.uint64).reshape(-1)
+        if colwords.size == 0:
+            colwords = np.zeros(1, dtype=np.uint64)
+        if indices.size == 0:
+            indices = np.zeros(1, dtype=np.uint32)
+        wpr = (props + 63) // 64 if 0 <= props <= 64 else 1
+        out = np.zeros(max(rows * wpr, 1), dtype=np.uint64)
+        err = C.create_string_buffer(256)
+        rc = self.lib.oracle_label_all(rows, cols, _p(offsets, C.c_uint64), _p(indices, C.c_uint32),
+                                       cells, props, _p(colwords, C.c_uint64), workers,
+                                       _p(out, C.c_uint64), err, 256)
+        if rc:
+            raise OracleError(err.value.decode())
+        return out[: rows * wpr]
+
+    def validate_csr(self, rows, cols, offsets, indices):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        indices = np.ascontiguousarray(indices, dtype=np.uint32)
+        err = C.create_string_buffer(256)
+        rc = self.lib.oracle_validate_csr(rows, cols, _p(offsets, C.c_uint64), offsets.size,
+                                          _p(indices, C.c_uint32), indices.size, err, 256)
+        return None if rc == 0 else err.value.decode()
+
+    def label_edge_counting(self, row, column_words):
+        row = np.ascontiguousarray(row, dtype=np.uint32)
+        col = np.ascontiguousarray(column_words, dtype=np.uint64)
+        ex = C.c_uint64(0)
+        hit = self.lib.oracle_label_edge_counting(_p(row, C.c_uint32), row.size, _p(col, C.c_uint64), C.byref(ex))
+        return bool(hit), ex.value
+
+    def z_index_of_cells(self, k, depth, cells):
+        c = np.ascontiguousarray(cells, dtype=np.uint64)
+        return self.lib.oracle_z_index_of_cells(k, depth, _p(c, C.c_uint64))
+
+    def _zcall(self, fn, k, depth, lo, hi, p):
+        a = [np.ascontiguousarray(x, dtype=np.float64) for x in (lo, hi, p)]
+        r = fn(k, depth, *[_p(x, C.c_double) for x in a])
+        if r == 0xFFFFFFFFFFFFFFFF:
+            raise IndexError("point outside workspace bounds")
+        return r
+
+    def z_index(self, k, depth, lo, hi, p):
+        return self._zcall(self.lib.oracle_z_index, k, depth, lo, hi, p)
+
+    def z_index_tree_descent(self, k, depth, lo, hi, p):
+        return self._zcall(self.lib.oracle_z_index_tree_descent, k, depth, lo, hi, p)
+
+    def mix_seed(self, seed, stream):
+        return self.lib.oracle_mix_seed(seed, stream)
+
+    def effective_workers(self, workers, items):
+        return self.lib.oracle_effective_workers(workers, items)
+
+    def resample(self, vgrid, wgrid, pose, props, world_cols, outside=0):
+        """vgrid/wgrid = (depth, lo0, hi0, lo1, hi1); pose = (dx, dy, cos, sin)."""
+        dv = vgrid[0]
+        vwords = ((1 << dv) + 63) // 64
+        out = np.zeros(max(vwords * props, 1), dtype=np.uint64)
+        wc = np.ascontiguousarray(world_cols, dtype=np.uint64).reshape(-1)
+        self.lib.oracle_resample(*vgrid, *wgrid, *pose, props, _p(wc, C.c_uint64), int(outside),
+                                 _p(out, C.c_uint64))
+        return out[: vwords * props]
+
+
+class RefCore:
+    """oracle/_ref/libltlgrid_ref.so -- the unmodified reference core."""
+
+    @staticmethod
+    def available(path: str = REF_SO) -> bool:
+        return os.path.exists(path)
+
+    def __init__(self, path: str = REF_SO):
+        L = C.CDLL(path)
+        u64, u32, i32 = C.c_uint64, C.c_uint32, C.c_int
+        P64, P32 = C.POINTER(u64), C.POINTER(u32)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_hardware_concurrency.restype = i32
+        L.ref_csr_create.argtypes = [u64, u64, P64, P32]
+        L.ref_csr_create.restype = C.c_void_p
+        L.ref_csr_free.argtypes = [C.c_void_p]
+        L.ref_props_create.argtypes = [u64, i32, P64]
+        L.ref_props_create.restype = C.c_void_p
+        L.ref_props_free.argtypes = [C.c_void_p]
+        L.ref_time_label_ms.argtypes = [C.c_void_p, C.c_void_p, i32, i32, P64]
+        L.ref_time_label_ms.restype = C.c_double
+        L.ref_label_all.argtypes = [u64, u64, P64, P32, u64, i32, P64, i32, P64]
+        L.ref_label_all.restype = i32
+        L.ref_csr_validate.argtypes = [u64, u64, P64, u64, P32, u64]
+        L.ref_csr_validate.restype = i32
+        L.ref_label_edge_counting.argtypes = [P32, u64, u64, P64, P64]
+        L.ref_label_edge_counting.restype = i32
+        L.ref_csr_save.argtypes = [C.c_char_p, u64, u64, P64, P32]
+        L.ref_csr_save.restype = i32
+        L.ref_csr_load.argtypes = [C.c_char_p, P64, P64, P64, P32]
+        L.ref_csr_load.restype = C.c_int64
+        L.ref_label_save.argtypes = [C.c_char_p, u64, i32, P64]
+        L.ref_label_save.restype = i32
+        L.ref_z_index.argtypes = [i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.ref_z_index.restype = u64
+        L.ref_save_bitset.argtypes = [C.c_char_p, i32, i32, P64]
+        L.ref_save_bitset.restype = i32
+        self.lib = L
+
+    def error(self) -> str:
+        return self.lib.ref_last_error().decode()
+
+    def hardware_concurrency(self) -> int:
+        return self.lib.ref_hardware_concurrency()
+
+    def label_all(self, rows, cols, offsets, indices, cells, props, colwords, workers=0):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        indices = np.ascontiguousarray(indices, dtype=np.uint32)
+        if indices.size == 0:
+            indices = np.zeros(1, dtype=np.uint32)
+        colwords = np.ascontiguousarray(colwords, dtype=np.uint64).reshape(-1)
+        if colwords.size == 0:
+            colwords = np.zeros(1, dtype=np.uint64)
+        wpr = (props + 63) // 64 if 0 <= props <= 64 else 1
+        out = np.zeros(max(rows * wpr, 1), dtype=np.uint64)
+        rc = self.lib.ref_label_all(rows, cols, _p(offsets, C.c_uint64), _p(indices, C.c_uint32), cells,
+                                    props, _p(colwords, C.c_uint64), workers, _p(out, C.c_uint64))
+        if rc:
+            raise OracleError(self.error())
+        return out[: rows * wpr]
+
+    def validate_csr(self, rows, cols, offsets, indices):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        indices = np.ascontiguousarray(indices, dtype=np.uint32)
+        ind = indices if indices.size else np.zeros(1, dtype=np.uint32)
+        rc = self.lib.ref_csr_validate(rows, cols, _p(offsets, C.c_uint64), offsets.size,
+                                       _p(ind, C.c_uint32), indices.size)
+        return None if rc == 0 else self.error()
+
+    def label_edge_counting(self, row, cells, column_words):
+        row = np.ascontiguousarray(row, dtype=np.uint32)
+        col = np.ascontiguousarray(column_words, dtype=np.uint64)
+        ex = C.c_uint64(0)
+        hit = self.lib.ref_label_edge_counting(_p(row, C.c_uint32), row.size, cells, _p(col, C.c_uint64), C.byref(ex))
+        return bool(hit), ex.value
+
+    def z_index(self, k, depth, lo, hi, p):
+        a = [np.ascontiguousarray(x, dtype=np.float64) for x in (lo, hi, p)]
+        r = self.lib.ref_z_index(k, depth, *[_p(x, C.c_double) for x in a])
+        if r == 0xFFFFFFFFFFFFFFFF:
+            raise IndexError(self.error())
+        return r
+
+    def csr_save(self, path, rows, cols, offsets, indices):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        indices = np.ascontiguousarray(indices, dtype=np.uint32)
+        if indices.size == 0:
+            indices = np.zeros(1, dtype=np.uint32)
+        if self.lib.ref_csr_save(path.encode(), rows, cols, _p(offsets, C.c_uint64), _p(indices, C.c_uint32)):
+            raise OracleError(self.error())
+
+    def label_save(self, path, rows, props, words):
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        if words.size == 0:
+            words = np.zeros(1, dtype=np.uint64)
+        if self.lib.ref_label_save(path.encode(), rows, props, _p(words, C.c_uint64)):
+            raise OracleError(self.error())
+
+    def save_bitset(self, path, k, depth, words):
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        if self.lib.ref_save_bitset(path.encode(), k, depth, _p(words, C.c_uint64)):
+            raise OracleError(self.error())
+
+    # timing handles (bench cpu_baseline / --impl reference)
+    def csr_handle(self, rows, cols, offsets, indices):
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        indices = np.ascontiguousarray(indices, dtype=np.uint32)
+        if indices.size == 0:
+            indices = np.zeros(1, dtype=np.uint32)
+        return self.lib.ref_csr_create(rows, cols, _p(offsets, C.c_uint64), _p(indices, C.c_uint32))
+
+    def props_handle(self, cells, props, colwords):
+        colwords = np.ascontiguousarray(colwords, dtype=np.uint64).reshape(-1)
+        h = self.lib.ref_props_create(cells, props, _p(colwords, C.c_uint64))
+        if not h:
+            raise OracleError(self.error())
+        return h
+
+    def time_label_ms(self, m, p, workers=0, repeats=2, out=None):
+        return self.lib.ref_time_label_ms(m, p, workers, repeats, _p(out, C.c_uint64) if out is not None else None)
+
+    def free(self, m=None, p=None):
+        if m:
+            self.lib.ref_csr_free(m)
+        if p:
+            self.lib.ref_props_free(p)

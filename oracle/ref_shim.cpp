@@ -1,0 +1,245 @@
+// ref_shim.cpp -- extern "C" access to the UNMODIFIED reference core.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile together with the
+// reference sources where they lie under /root/reference/proj/core/src
+// (nothing is copied into this repo) into oracle/_ref/libltlgrid_ref.so.
+// Used to (a) generate tests/golden fixtures, (b) validate the C restatement
+// in oracle/ltlg_oracle.c, and (c) time the reference CPU path
+// (bench.py --impl reference, cpu_baseline kind "reference").
+//
+// Every entry point builds the reference's own value types and calls the
+// reference's own functions: ltlgrid::label_all (label.cpp:150-189),
+// CsrBoolMatrix::validate/save/load (label.cpp:16-40, 251-298),
+// LabelMatrix::save/load (label.cpp:300-326), z_index (grid.cpp:108-117),
+// save_bitset (grid.cpp:370-390).
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <limits>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ltlgrid/grid.hpp"
+#include "ltlgrid/label.hpp"
+#include "ltlgrid/rng.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e) {
+    g_err = e.what();
+    return 1;
+}
+
+ltlgrid::DensePropMatrix make_props(std::uint64_t cells, int props, const std::uint64_t* colwords) {
+    const std::uint64_t wpc = (cells + 63) / 64;
+    std::vector<ltlgrid::OccupancyBitset> cols;
+    cols.reserve(static_cast<std::size_t>(props));
+    for (int j = 0; j < props; ++j) {
+        std::vector<std::uint64_t> w(colwords + static_cast<std::uint64_t>(j) * wpc,
+                                     colwords + static_cast<std::uint64_t>(j + 1) * wpc);
+        cols.push_back(ltlgrid::OccupancyBitset::from_words(cells, std::move(w)));
+    }
+    return ltlgrid::DensePropMatrix(cells, std::move(cols));
+}
+
+void export_labels(const ltlgrid::LabelMatrix& l, std::uint64_t* out) {
+    const int wpr = (l.props() + 63) / 64;
+    std::memset(out, 0, l.rows() * static_cast<std::uint64_t>(wpr) * sizeof(std::uint64_t));
+    for (std::uint64_t i = 0; i < l.rows(); ++i) {
+        for (int j = 0; j < l.props(); ++j) {
+            if (l.get(i, j)) {
+                const std::uint64_t bit = i * static_cast<std::uint64_t>(wpr) * 64 + j;
+                out[bit >> 6] |= std::uint64_t{1} << (bit & 63);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// SplitMix64 stream straight from rng.hpp:10-29 (pins the numpy restatement).
+void ref_splitmix_block(std::uint64_t seed, std::uint64_t n, std::uint64_t* out, double* uni) {
+    ltlgrid::SplitMix64 a(seed), b(seed);
+    for (std::uint64_t i = 0; i < n; ++i) {
+        out[i] = a.next();
+        uni[i] = b.uniform();
+    }
+}
+
+std::uint64_t ref_mix_seed(std::uint64_t seed, std::uint64_t stream) { return ltlgrid::mix_seed(seed, stream); }
+
+int ref_hardware_concurrency() { return static_cast<int>(std::thread::hardware_concurrency()); }
+
+// Opaque reference CsrBoolMatrix, built once so timing excludes the copy.
+void* ref_csr_create(std::uint64_t rows, std::uint64_t cols, const std::uint64_t* offsets,
+                     const std::uint32_t* indices) {
+    auto* m = new ltlgrid::CsrBoolMatrix;
+    m->rows = rows;
+    m->cols = cols;
+    m->row_offsets.assign(offsets, offsets + rows + 1);
+    m->col_indices.assign(indices, indices + offsets[rows]);
+    return m;
+}
+
+void ref_csr_free(void* m) { delete static_cast<ltlgrid::CsrBoolMatrix*>(m); }
+
+int ref_csr_validate(std::uint64_t rows, std::uint64_t cols, const std::uint64_t* offsets,
+                     std::uint64_t n_offsets, const std::uint32_t* indices, std::uint64_t nnz) {
+    try {
+        ltlgrid::CsrBoolMatrix m;
+        m.rows = rows;
+        m.cols = cols;
+        m.row_offsets.assign(offsets, offsets + n_offsets);
+        m.col_indices.assign(indices, indices + nnz);
+        m.validate();
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+void* ref_props_create(std::uint64_t cells, int props, const std::uint64_t* colwords) {
+    try {
+        return new ltlgrid::DensePropMatrix(make_props(cells, props, colwords));
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+void ref_props_free(void* p) { delete static_cast<ltlgrid::DensePropMatrix*>(p); }
+
+// Mirrors time_label_ms (scenario.cpp:154-165): best of `repeats` timed
+// label_all calls; labels of the last call exported into out (may be null).
+double ref_time_label_ms(void* m, void* p, int workers, int repeats, std::uint64_t* out) {
+    try {
+        const auto& mm = *static_cast<ltlgrid::CsrBoolMatrix*>(m);
+        const auto& pp = *static_cast<ltlgrid::DensePropMatrix*>(p);
+        double best = std::numeric_limits<double>::infinity();
+        ltlgrid::LabelMatrix l;
+        for (int r = 0; r < (repeats < 1 ? 1 : repeats); ++r) {
+            const auto t0 = std::chrono::steady_clock::now();
+            l = ltlgrid::label_all(mm, pp, workers);
+            const auto t1 = std::chrono::steady_clock::now();
+            const double ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+            if (ms < best) best = ms;
+        }
+        if (out) export_labels(l, out);
+        return best;
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1.0;
+    }
+}
+
+// One-shot label_all over raw arrays (for goldens / small parity checks).
+int ref_label_all(std::uint64_t rows, std::uint64_t cols, const std::uint64_t* offsets,
+                  const std::uint32_t* indices, std::uint64_t cells, int props,
+                  const std::uint64_t* colwords, int workers, std::uint64_t* out) {
+    try {
+        ltlgrid::CsrBoolMatrix m;
+        m.rows = rows;
+        m.cols = cols;
+        m.row_offsets.assign(offsets, offsets + rows + 1);
+        m.col_indices.assign(indices, indices + offsets[rows]);
+        auto p = make_props(cells, props, colwords);
+        auto l = ltlgrid::label_all(m, p, workers);
+        export_labels(l, out);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_label_edge_counting(const std::uint32_t* row, std::uint64_t n, std::uint64_t cells,
+                            const std::uint64_t* column, std::uint64_t* examined) {
+    std::vector<std::uint64_t> w(column, column + (cells + 63) / 64);
+    auto col = ltlgrid::OccupancyBitset::from_words(cells, std::move(w));
+    auto [hit, e] = ltlgrid::label_edge_counting({row, n}, col);
+    *examined = e;
+    return hit ? 1 : 0;
+}
+
+int ref_csr_save(const char* path, std::uint64_t rows, std::uint64_t cols,
+                 const std::uint64_t* offsets, const std::uint32_t* indices) {
+    try {
+        ltlgrid::CsrBoolMatrix m;
+        m.rows = rows;
+        m.cols = cols;
+        m.row_offsets.assign(offsets, offsets + rows + 1);
+        m.col_indices.assign(indices, indices + offsets[rows]);
+        m.save(path);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// Loads a CSB1 file; returns nnz (or -1) and fills the caller's buffers
+// when they are non-null (call twice: sizes, then data).
+std::int64_t ref_csr_load(const char* path, std::uint64_t* rows, std::uint64_t* cols,
+                          std::uint64_t* offsets, std::uint32_t* indices) {
+    try {
+        auto m = ltlgrid::CsrBoolMatrix::load(path);
+        *rows = m.rows;
+        *cols = m.cols;
+        if (offsets) std::memcpy(offsets, m.row_offsets.data(), m.row_offsets.size() * 8);
+        if (indices) std::memcpy(indices, m.col_indices.data(), m.col_indices.size() * 4);
+        return static_cast<std::int64_t>(m.nnz());
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1;
+    }
+}
+
+int ref_label_save(const char* path, std::uint64_t rows, int props, const std::uint64_t* words) {
+    try {
+        ltlgrid::LabelMatrix l(rows, props);
+        const int wpr = (props + 63) / 64;
+        for (std::uint64_t i = 0; i < rows; ++i)
+            for (int j = 0; j < props; ++j) {
+                const std::uint64_t bit = i * static_cast<std::uint64_t>(wpr) * 64 + j;
+                if ((words[bit >> 6] >> (bit & 63)) & 1u) l.set(i, j);
+            }
+        l.save(path);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+std::uint64_t ref_z_index(int k, int depth, const double* lo, const double* hi, const double* p) {
+    try {
+        std::vector<std::pair<double, double>> b;
+        for (int i = 0; i < k; ++i) b.emplace_back(lo[i], hi[i]);
+        ltlgrid::GridSpec g(std::move(b), depth);
+        return ltlgrid::z_index({p, static_cast<std::size_t>(k)}, g);
+    } catch (const std::exception& e) {
+        fail(e);
+        return ~std::uint64_t{0};
+    }
+}
+
+int ref_save_bitset(const char* path, int k, int depth, const std::uint64_t* words) {
+    try {
+        std::vector<std::pair<double, double>> b;
+        for (int i = 0; i < k; ++i) b.emplace_back(0.0, 1.0);
+        ltlgrid::GridSpec g(std::move(b), depth);
+        const std::uint64_t bits = std::uint64_t{1} << depth;
+        std::vector<std::uint64_t> w(words, words + (bits + 63) / 64);
+        ltlgrid::save_bitset(path, ltlgrid::OccupancyBitset::from_words(bits, std::move(w)), g);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+}  // extern "C"
