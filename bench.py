@@ -1,0 +1,343 @@
+"""bench.py -- edge-labels/sec of the B200 labeling path (BASELINE.json metric).
+
+Workload (N=1 headline): BASELINE config 4 "batched frames": 2,000,000-edge
+synthetic PRM, 512x512 grid (2^18 cells), 32 propositions, 64 frames per step.
+One step = label every edge for the 64 frames (one summary + one labeling
+kernel).  Under torchrun (N>1) the 2M edges are sharded across ranks by edge
+rows and rank 0's P is NCCL-broadcast every step (strong scaling).
+
+Also reported: p50 per-frame latency of config 3 (2M edges, 16 props, one
+frame; host P in pinned memory -> labels resident in HBM), the e2e number
+through the public API with host buffers, the roofline of the labeling
+kernel, the CPU baseline (reference core on the host cores), clocks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "edge-labels/sec (batched, 1/2/4/8 GPU) and p50 per-frame labeling latency"
+UNIT = "edge-labels/s"
+CFG4 = dict(edges=2_000_000, depth=18, props=32, frames=64)
+CFG3_PROPS = 16
+SEED_T, SEED_P = 1, 1
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def shard_rows(E: int, rank: int, world: int):
+    return E * rank // world, E * (rank + 1) // world
+
+
+def cpu_reference_sample(depth: int, props: int, rows: int, frames: int, workers: int = 0):
+    """Time the reference CPU label_all (oracle/_ref, or the C port) on rows
+    [0, rows) of the same synthetic T, `frames` frames, best of 2 per frame
+    (time_label_ms protocol, scenario.cpp:154-165).  Returns (edge-labels/s,
+    kind, cores, sample description)."""
+    from oracle.oracle import Oracle, RefCore  # checker / baseline only
+    from paper_1810_02612_b200.synth import SyntheticPRM, props_words
+
+    prm = SyntheticPRM(seed=SEED_T, depth=depth)
+    off, idx = prm.csr(0, rows)
+    P = props_words(SEED_P, depth, props, 0, frames)
+    cells = 1 << depth
+    if RefCore.available():
+        ref = RefCore()
+        kind = "reference"
+        cores = workers or ref.hardware_concurrency()
+        m = ref.csr_handle(rows, cells, off, idx)
+        total = 0.0
+        for f in range(frames):
+            p = ref.props_handle(cells, props, P[f])
+            total += ref.time_label_ms(m, p, workers, 2) / 1e3
+            ref.free(p=p)
+        ref.free(m=m)
+    else:
+        o = Oracle()
+        kind = "port"
+        cores = o.effective_workers(workers, rows)
+        total = 0.0
+        for f in range(frames):
+            best = 1e30
+            for _ in range(2):
+                t0 = time.perf_counter()
+                o.label_all(rows, cells, off, idx, cells, props, P[f], workers)
+                best = min(best, time.perf_counter() - t0)
+            total += best
+    sample = f"rows [0,{rows}) of the {CFG4['edges']}-edge T, {frames} frames x {props} props, best of 2 per frame"
+    return rows * frames / total, kind, cores, sample
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    rows, frames = 100_000, 1
+    vals = []
+    for _ in range(args.warmup):
+        cpu_reference_sample(CFG4["depth"], CFG4["props"], 20_000, 1)
+    t_all = time.perf_counter()
+    kind = cores = sample = None
+    for _ in range(args.steps):
+        v, kind, cores, sample = cpu_reference_sample(CFG4["depth"], CFG4["props"], rows, frames)
+        vals.append(v)
+    wall = time.perf_counter() - t_all
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / max(args.steps, 1) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": cfg_json(world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cfg_json(world):
+    return {"workload": "config4-batched-frames: 2M-edge synthetic PRM x 64 frames, 512x512 grid (2^18 cells), "
+                        "32 propositions", "edges": CFG4["edges"], "grid": "512x512", "cells": 1 << CFG4["depth"],
+            "props": CFG4["props"], "frames_per_step": CFG4["frames"], "parallelism": f"edge-row shards x{world}",
+            "l2": "inputs larger than L2 (packed T 526 MB streamed per step)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="short run for profilers")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1810_02612_b200 import LabelEngine
+    from paper_1810_02612_b200.synth import SyntheticPRM, props_words
+
+    E, depth, props, F = CFG4["edges"], CFG4["depth"], CFG4["props"], CFG4["frames"]
+    cells = 1 << depth
+    nw = (cells + 63) // 64
+    r0, r1 = shard_rows(E, rank, world)
+    prm = SyntheticPRM(seed=SEED_T, depth=depth)
+    T = prm.words(r0, r1)
+    eng = LabelEngine(devices=[local], profile=True)
+    eng.load_abstraction_words(r1 - r0, cells, T.offsets, T.words, T.masks)
+    info = eng.info()
+    W32_all = torch.tensor([int(info.words), int(r1 - r0)], dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(W32_all)
+    W32, rows_all = int(W32_all[0]), int(W32_all[1])
+
+    # P for 64 frames: pinned host (e2e) and device-resident (value)
+    P_host = torch.empty((F, props, nw), dtype=torch.int64, pin_memory=True)
+    if rank == 0:
+        props_words(SEED_P, depth, props, 0, F, out=P_host)
+    P_dev = torch.empty((F, props, nw), dtype=torch.int64, device="cuda")
+    if rank == 0:
+        P_dev.copy_(P_host)
+    stream = torch.cuda.ExternalStream(eng.stream())
+
+    def step():
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.broadcast(P_dev, src=0)
+        eng.submit_grid_device(cells, props, P_dev.data_ptr(), F)
+
+    for _ in range(args.warmup):
+        step()
+    eng.wait()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    # ---- timed region: K steps, CUDA events on the engine's stream ----------
+    K = args.steps
+    kernel_ms = []
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(K):
+            step()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    # per-launch device times of the K timed launches (event ring on the launching stream)
+    kernel_ms = [eng.stage_times(0, back)[1:] for back in range(min(K, 255))]
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t[0])
+    value = E * F * K / (ms_max / 1e3)
+    label_ms = statistics.mean(k[1] for k in kernel_ms)
+    summary_ms = statistics.mean(k[0] for k in kernel_ms)
+
+    # roofline of the labeling kernel (SURVEY 8(d) algorithmic bytes, this rank's shard)
+    hbm, src = peaks()
+    rows_local = r1 - r0
+    alg_bytes = 8 * int(info.words) + 4 * (rows_local + 1) + F * (cells * props // 8 + rows_local * 4)
+    achieved = alg_bytes / (label_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "peak_source": src, "kernel": "label_batch_kernel<u32,u32,2>",
+                "alg_bytes_per_launch": alg_bytes, "kernel_ms": label_ms, "summary_kernel_ms": summary_ms,
+                "note": "algorithmic bytes = 8*W32 + 4*(E+1) + F*(cells*props/8 + E*4)"}
+
+    # ---- p50 single-frame latency, config 3 (16 props), host P -> labels in HBM
+    lat = None
+    if rank == 0 and world == 1:
+        P3 = torch.empty((1, CFG3_PROPS, nw), dtype=torch.int64, pin_memory=True)
+        eng_lat = []
+        n_frames = 30 if args.quick else 150
+        frames3 = torch.empty((n_frames + 1, CFG3_PROPS, nw), dtype=torch.int64, pin_memory=True)
+        props_words(SEED_P + 3, depth, CFG3_PROPS, 0, n_frames + 1, out=frames3)
+        label3 = []
+        for q in range(-1, n_frames):  # query -1 is the warm-up (scenario.cpp:183-193)
+            src3 = frames3[q + 1]
+            t0 = time.perf_counter()
+            eng.submit_grid(cells, CFG3_PROPS, src3, 1)
+            eng.wait()
+            dt = time.perf_counter() - t0
+            if q >= 0:
+                eng_lat.append(dt * 1e3)
+                label3.append(eng.stage_times(0, 0)[2])
+        del P3
+        k3 = statistics.median(label3)
+        alg3 = 8 * int(info.words) + 4 * (rows_local + 1) + cells * CFG3_PROPS // 8 + rows_local * 2
+        lat = {"config": "config3-large-abstraction: 2M edges, 512x512, 16 props, 1 frame",
+               "p50_ms": statistics.median(eng_lat), "p99_ms": sorted(eng_lat)[int(0.99 * (len(eng_lat) - 1))],
+               "frames": n_frames, "what": "pinned host P -> labels resident in HBM (host steady clock)",
+               "kernel_p50_ms": k3, "roofline": {"bound": "hbm", "achieved": alg3 / (k3 / 1e3) / 1e9, "peak": hbm,
+                                                "unit": "GB/s", "frac": alg3 / (k3 / 1e3) / 1e9 / hbm,
+                                                "alg_bytes_per_launch": alg3}}
+
+    # ---- e2e through the public API with host buffers ------------------------
+    e2e = None
+    if not args.no_e2e:
+        out_host = torch.empty((rows_local, F), dtype=torch.int32, pin_memory=True)
+        Ke = max(2, min(K, 5))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(Ke):
+            if world > 1:
+                if rank == 0:
+                    P_dev.copy_(P_host, non_blocking=True)
+                with torch.cuda.stream(stream):
+                    dist.broadcast(P_dev, src=0)
+                eng.submit_grid_device(cells, props, P_dev.data_ptr(), F)
+            else:
+                eng.submit_grid(cells, props, P_host, F)
+            eng.get_labels_packed(out_host)
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt[0])
+        e2e = {"value": E * F * Ke / dt, "unit": UNIT, "h2d_bytes_per_step": F * props * nw * 8,
+               "d2h_bytes_per_step": E * F * 4, "steps": Ke,
+               "what": "ltlg_submit_grid(pinned host P, 64 frames) + ltlg_get_labels_packed(pinned host, u32 x 64 "
+                       "frames per edge); host wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, kind, cores, sample = cpu_reference_sample(depth, props, 20_000 if args.quick else 100_000, 2)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic", "config": cfg_json(world), "clocks": clk.summary(),
+            "gpu_launches": 2 * K, "roofline": roofline, "latency": lat, "e2e": e2e, "cpu_baseline": cpu,
+            "shape": {"W32": W32, "rows": rows_all, "t_bytes_device": int(info.t_bytes)},
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * ltlgrid_gpu.h -- C ABI of the B200 edge-labeling engine (libltlgrid_gpu.so).
+ *
+ * Drop-in for the reference labeling path L = T o P over the OR-AND semiring:
+ *   ltlgrid::label_all(const CsrBoolMatrix&, const DensePropMatrix&, int)
+ *   (reference: proj/core/include/ltlgrid/label.hpp:94-98, label.cpp:150-189)
+ * split into the reference's own life cycle "load abstraction -> submit grid
+ * -> get per-edge label bitsets".  Plain pointers and sizes only; no CUDA or
+ * torch types cross this boundary.  All host buffers are owned by the caller
+ * and never retained after a call returns (inputs are copied to the device,
+ * label reads are synchronous).  A context is used by one host thread at a
+ * time; distinct contexts are independent (reference: label_all is reentrant,
+ * SPEC.md:424).
+ *
+ * Bit layouts are the reference's, verbatim:
+ *   T  CSR, row i's set cells col_indices[row_offsets[i] .. row_offsets[i+1]),
+ *      strictly ascending, each < cols            (label.hpp:18-35)
+ *   P  props columns of ceil(cells/64) u64 words, little-endian, bit c of the
+ *      column = cell c in z-order                 (label.hpp:47-58, grid.hpp:93-125)
+ *   L  LabelMatrix: rows x ceil(props/64) u64 words, bit j of edge i = prop j
+ *                                                 (label.hpp:61-92)
+ *
+ * Errors: every entry point returns an ltlg_status; the message of the last
+ * failure is ltlg_last_error(ctx) (ltlg_last_error(NULL) for ltlg_create and
+ * the one-shot ltlg_label_all).  LTLG_EINVAL messages are the reference's
+ * std::invalid_argument texts (label.cpp:16-40, 124-132, 151-154), LTLG_EFORMAT /
+ * LTLG_EIO the std::runtime_error texts of the file loaders (label.cpp:271-298).
+ */
+#ifndef LTLGRID_GPU_H
+#define LTLGRID_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LTLG_ABI_VERSION 1
+
+typedef enum ltlg_status {
+    LTLG_OK = 0,
+    LTLG_EINVAL = 1,  /* reference std::invalid_argument                 */
+    LTLG_EFORMAT = 2, /* reference std::runtime_error (bad file content) */
+    LTLG_EIO = 3,     /* reference std::runtime_error (open/read/write)  */
+    LTLG_ECUDA = 4,   /* CUDA runtime error (no device, launch failure)  */
+    LTLG_ENCCL = 5,   /* NCCL error (multi-device contexts)              */
+    LTLG_ENOMEM = 6,  /* device or host allocation failed                */
+    LTLG_ESTATE = 7   /* call out of order (e.g. submit before load)     */
+} ltlg_status;
+
+typedef struct ltlg_ctx ltlg_ctx;
+
+/* Engine options (ltlg_create_ex).  Zero-initialise and set what you need. */
+typedef struct ltlg_options {
+    int sort_rows;        /* 1 (default via ltlg_create): store T rows in z-locality order, undo on output */
+    int stream_task_pairs;/* target T pairs per warp task, single-frame kernel (0 = default 2048) */
+    int batch_task_pairs; /* target T pairs per warp task, multi-frame kernel (0 = default 256)   */
+    int profile;          /* 1: record CUDA events around each stage (ltlg_stage_times) */
+    int reserved[7];
+} ltlg_options;
+
+/* Shape / layout facts about the loaded abstraction and the last submit. */
+typedef struct ltlg_info {
+    uint64_t rows;         /* edges E                                    */
+    uint64_t cols;         /* cells of T's column space                  */
+    uint64_t nnz;          /* stored cells of T                          */
+    uint64_t words;        /* W32: distinct (row, 32-bit word) pairs     */
+    uint64_t pairs;        /* stored T pairs incl. empty-row sentinels   */
+    uint64_t t_bytes;      /* device bytes of the packed T (all shards)  */
+    int n_devices;
+    int props;             /* props of the last submit                   */
+    int frames;            /* frames of the last submit                  */
+    int label_bytes;       /* bytes per packed label word: 1, 2, 4 or 8  */
+    int label_words;       /* LabelMatrix words per row, ceil(props/64)  */
+    int reserved[7];
+} ltlg_info;
+
+/* Create an engine on the given CUDA devices (n >= 1; NULL = device 0).
+ * T rows are sharded across the devices; each frame's P is uploaded to the
+ * first device and broadcast to the others (NCCL when n > 1). */
+ltlg_status ltlg_create(const int* devices, int n_devices, ltlg_ctx** out);
+ltlg_status ltlg_create_ex(const int* devices, int n_devices, const ltlg_options* opts,
+                           ltlg_ctx** out);
+void ltlg_destroy(ltlg_ctx* ctx);
+const char* ltlg_last_error(const ltlg_ctx* ctx);
+int ltlg_abi_version(void);
+
+/* Load T from a CSR (replaces CsrBoolMatrix + validate, label.hpp:18-35,
+ * label.cpp:16-40).  Validated with the reference's rules and messages, then
+ * bit-packed once into the device word-CSR; the host arrays are not retained. */
+ltlg_status ltlg_load_abstraction(ltlg_ctx* ctx, uint64_t rows, uint64_t cols,
+                                  const uint64_t* row_offsets, const uint32_t* col_indices);
+
+/* Load T from a CSB1 file (replaces CsrBoolMatrix::load, label.cpp:271-298):
+ * same header checks and messages, then validate, then pack. */
+ltlg_status ltlg_load_abstraction_file(ltlg_ctx* ctx, const char* csb1_path);
+
+/* Load T already packed as a word-CSR: row i's 32-bit words are
+ * word_index[row_word_offsets[i] .. row_word_offsets[i+1]) (strictly
+ * ascending, < ceil(cols/32)) with non-zero word_mask (bit b = cell
+ * 32*word + b, every such cell < cols).  Same semantics as the CSR form. */
+ltlg_status ltlg_load_abstraction_words(ltlg_ctx* ctx, uint64_t rows, uint64_t cols,
+                                        const uint64_t* row_word_offsets,
+                                        const uint32_t* word_index, const uint32_t* word_mask);
+
+/* Submit `frames` perception grids and label every edge for each of them
+ * (replaces DensePropMatrix + label_all, label.hpp:47-58 / 94-98).
+ * column_words: frames x num_props x ceil(cells/64) u64, i.e. `frames`
+ * DensePropMatrix column sets back to back.  Requires cells == cols of T
+ * (else LTLG_EINVAL "dimension mismatch: ..."), 0 <= num_props <= 64.
+ * Asynchronous: returns after enqueueing the upload and the kernels. */
+ltlg_status ltlg_submit_grid(ltlg_ctx* ctx, uint64_t cells, int num_props,
+                             const uint64_t* column_words, int frames);
+
+/* Same, but column_words already lives on the context's first device
+ * (e.g. written by a perception kernel, or received by an NCCL broadcast).
+ * A single-device engine reads it in place: keep it alive and unmodified
+ * until ltlg_wait / ltlg_get_labels* returns. */
+ltlg_status ltlg_submit_grid_device(ltlg_ctx* ctx, uint64_t cells, int num_props,
+                                    const uint64_t* device_column_words, int frames);
+
+/* World-frame perception grid -> vehicle-frame P resample, then label
+ * (north_star subsystem 2; transform convention of translate_system,
+ * abstraction.cpp:396-404).  Grids are k=2 z-order grids; world_words is
+ * num_props x ceil(2^world_depth/64) u64 (device or host, see flag).
+ * Cells whose centre maps outside the world take `outside` (0 or 1). */
+typedef struct ltlg_grid2 {
+    int depth;
+    double lo0, hi0, lo1, hi1;
+} ltlg_grid2;
+typedef struct ltlg_pose2 {
+    double dx, dy, cos_t, sin_t;
+} ltlg_pose2;
+ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, const ltlg_grid2* world,
+                                   int num_props, const uint64_t* world_words, int words_on_device,
+                                   const ltlg_pose2* poses, int frames, int outside);
+
+/* Block until every submitted frame is labelled. */
+ltlg_status ltlg_wait(ltlg_ctx* ctx);
+
+/* Copy one frame's labels in the reference LabelMatrix word layout
+ * (rows x ceil(props/64) u64).  Synchronous. */
+ltlg_status ltlg_get_labels(ltlg_ctx* ctx, int frame, uint64_t* out);
+
+/* Copy all frames' packed labels: edge-major rows x frames words of
+ * ltlg_info.label_bytes each (bit j = prop j).  out_bytes must be >=
+ * rows * frames * label_bytes.  Synchronous. */
+ltlg_status ltlg_get_labels_packed(ltlg_ctx* ctx, void* out, size_t out_bytes);
+
+/* Resident labels for downstream consumers: device pointer of shard s
+ * (rows [row_begin, row_end) x frames packed words) -- stays valid until the
+ * next submit / load / destroy. */
+ltlg_status ltlg_device_labels(ltlg_ctx* ctx, int shard, void** dev_ptr, uint64_t* row_begin,
+                               uint64_t* row_end, int* device);
+
+ltlg_status ltlg_get_info(ltlg_ctx* ctx, ltlg_info* out);
+
+/* The CUDA stream (as void*) the engine enqueues shard s's work on, so that
+ * callers can time with events on the launching stream. */
+ltlg_status ltlg_stream(ltlg_ctx* ctx, int shard, void** stream);
+
+/* With ltlg_options.profile = 1: device time (CUDA events on the launching
+ * stream) of the stages of the submit `back` submits ago (0 = the last one,
+ * up to 255) on shard s -- P upload / broadcast, per-word summary build,
+ * labeling kernel.  Waits for that submit only. */
+ltlg_status ltlg_stage_times(ltlg_ctx* ctx, int shard, int back, float* upload_ms, float* summary_ms,
+                             float* label_ms);
+
+/* Host-only CsrBoolMatrix::validate (label.cpp:16-40): same checks, same
+ * order, same messages (written to err, NUL-terminated).  No device needed. */
+ltlg_status ltlg_validate_csr(uint64_t rows, uint64_t cols, const uint64_t* row_offsets,
+                              uint64_t n_offsets, const uint32_t* col_indices, uint64_t nnz,
+                              char* err, size_t err_len);
+
+/* One-shot drop-in for ltlgrid::label_all (label.cpp:150-189) on device 0:
+ * out = rows x ceil(num_props/64) u64 LabelMatrix words.  `workers` is
+ * accepted for signature parity and ignored (the GPU partition is internal;
+ * results are identical for any value, as test_label.cpp:121-132 requires). */
+ltlg_status ltlg_label_all(uint64_t rows, uint64_t cols, const uint64_t* row_offsets,
+                           const uint32_t* col_indices, uint64_t cells, int num_props,
+                           const uint64_t* column_words, int workers, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LTLGRID_GPU_H */

@@ -1,0 +1,13 @@
+"""B200-native edge labeling L = T o P (OR-AND semiring) for LTL planning
+abstractions -- a drop-in for the reference's labeling path
+(ltlgrid::label_all, proj/core/src/label.cpp:150-189).
+
+  label.LabelEngine   load abstraction -> submit grid -> get labels (C ABI)
+  label.label_all     one-shot drop-in for ltlgrid::label_all
+  synth               synthetic T / P of the BASELINE configs
+"""
+from .label import (CsrBoolMatrix, DensePropMatrix, LabelEngine, LabelMatrix, LtlgError,  # noqa: F401
+                    OccupancyBitset, label_all, to_csr)
+
+__all__ = ["CsrBoolMatrix", "DensePropMatrix", "LabelEngine", "LabelMatrix", "LtlgError",
+           "OccupancyBitset", "label_all", "to_csr"]

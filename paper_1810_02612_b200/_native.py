@@ -1,0 +1,118 @@
+"""ctypes binding of include/ltlgrid_gpu.h (libltlgrid_gpu.so) -- no torch types.
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+sm_100a).  There is no CPU fallback: if the library is missing, importing the
+engine raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(HERE, "_lib")
+GPU_SO = os.path.join(LIB_DIR, "libltlgrid_gpu.so")
+SYNTH_SO = os.path.join(LIB_DIR, "libltlgrid_synth.so")
+
+LTLG_OK, LTLG_EINVAL, LTLG_EFORMAT, LTLG_EIO, LTLG_ECUDA, LTLG_ENCCL, LTLG_ENOMEM, LTLG_ESTATE = range(8)
+
+# Every symbol include/ltlgrid_gpu.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "ltlg_create", "ltlg_create_ex", "ltlg_destroy", "ltlg_last_error", "ltlg_abi_version",
+    "ltlg_load_abstraction", "ltlg_load_abstraction_file", "ltlg_load_abstraction_words",
+    "ltlg_submit_grid", "ltlg_submit_grid_device", "ltlg_submit_world_grid", "ltlg_wait",
+    "ltlg_get_labels", "ltlg_get_labels_packed", "ltlg_device_labels", "ltlg_get_info",
+    "ltlg_stream", "ltlg_stage_times", "ltlg_validate_csr", "ltlg_label_all",
+]
+
+
+class Options(C.Structure):
+    _fields_ = [("sort_rows", C.c_int), ("stream_task_pairs", C.c_int), ("batch_task_pairs", C.c_int),
+                ("profile", C.c_int), ("reserved", C.c_int * 7)]
+
+
+class Info(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("nnz", C.c_uint64), ("words", C.c_uint64),
+                ("pairs", C.c_uint64), ("t_bytes", C.c_uint64), ("n_devices", C.c_int), ("props", C.c_int),
+                ("frames", C.c_int), ("label_bytes", C.c_int), ("label_words", C.c_int),
+                ("reserved", C.c_int * 7)]
+
+
+class Grid2(C.Structure):
+    _fields_ = [("depth", C.c_int), ("lo0", C.c_double), ("hi0", C.c_double), ("lo1", C.c_double),
+                ("hi1", C.c_double)]
+
+
+class Pose2(C.Structure):
+    _fields_ = [("dx", C.c_double), ("dy", C.c_double), ("cos_t", C.c_double), ("sin_t", C.c_double)]
+
+
+class NativeMissing(ImportError):
+    pass
+
+
+_lib = None
+_synth = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(GPU_SO):
+        raise NativeMissing(
+            f"{GPU_SO} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the labeling path has no CPU fallback)")
+    L = C.CDLL(GPU_SO, mode=C.RTLD_GLOBAL)
+    u64, i32, vp = C.c_uint64, C.c_int, C.c_void_p
+    P64, P32 = C.POINTER(C.c_uint64), C.POINTER(C.c_uint32)
+    ctxp = C.c_void_p
+    sig = {
+        "ltlg_create": ([C.POINTER(i32), i32, C.POINTER(ctxp)], i32),
+        "ltlg_create_ex": ([C.POINTER(i32), i32, C.POINTER(Options), C.POINTER(ctxp)], i32),
+        "ltlg_destroy": ([ctxp], None),
+        "ltlg_last_error": ([ctxp], C.c_char_p),
+        "ltlg_abi_version": ([], i32),
+        "ltlg_load_abstraction": ([ctxp, u64, u64, vp, vp], i32),
+        "ltlg_load_abstraction_file": ([ctxp, C.c_char_p], i32),
+        "ltlg_load_abstraction_words": ([ctxp, u64, u64, vp, vp, vp], i32),
+        "ltlg_submit_grid": ([ctxp, u64, i32, vp, i32], i32),
+        "ltlg_submit_grid_device": ([ctxp, u64, i32, vp, i32], i32),
+        "ltlg_submit_world_grid": ([ctxp, C.POINTER(Grid2), C.POINTER(Grid2), i32, vp, i32, vp, i32, i32], i32),
+        "ltlg_wait": ([ctxp], i32),
+        "ltlg_get_labels": ([ctxp, i32, vp], i32),
+        "ltlg_get_labels_packed": ([ctxp, vp, C.c_size_t], i32),
+        "ltlg_device_labels": ([ctxp, i32, C.POINTER(vp), P64, P64, C.POINTER(i32)], i32),
+        "ltlg_get_info": ([ctxp, C.POINTER(Info)], i32),
+        "ltlg_stream": ([ctxp, i32, C.POINTER(vp)], i32),
+        "ltlg_stage_times": ([ctxp, i32, i32, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_float)], i32),
+        "ltlg_validate_csr": ([u64, u64, vp, u64, vp, u64, C.c_char_p, C.c_size_t], i32),
+        "ltlg_label_all": ([u64, u64, vp, vp, u64, i32, vp, i32, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    del P32
+    _lib = L
+    return L
+
+
+def synth() -> C.CDLL:
+    global _synth
+    if _synth is not None:
+        return _synth
+    if not os.path.exists(SYNTH_SO):
+        raise NativeMissing(f"{SYNTH_SO} is not built; run __graft_entry__.build()")
+    S = C.CDLL(SYNTH_SO)
+    u64, i32, vp = C.c_uint64, C.c_int, C.c_void_p
+    S.synth_prm_create.argtypes = [u64, i32, C.c_double, i32]
+    S.synth_prm_create.restype = vp
+    S.synth_prm_free.argtypes = [vp]
+    S.synth_prm_row_words.argtypes = [vp, u64, u64, vp]
+    S.synth_prm_row_cells.argtypes = [vp, u64, u64, vp]
+    S.synth_prm_fill_words.argtypes = [vp, u64, u64, vp, vp, vp]
+    S.synth_prm_fill_cells.argtypes = [vp, u64, u64, vp, vp]
+    S.synth_props.argtypes = [u64, i32, i32, u64, i32, vp]
+    _synth = S
+    return S

@@ -1,0 +1,686 @@
+// api.cu -- the C ABI of include/ltlgrid_gpu.h: engine context, device memory,
+// P upload / broadcast, kernel sequencing and label read-back.
+//
+// Reference interface replaced (proj/core/include/ltlgrid/label.hpp):
+//   CsrBoolMatrix (:18-35) + validate/load (label.cpp:16-40, 271-298) -> ltlg_load_abstraction*
+//   DensePropMatrix (:47-58) + label_all (:94-98, label.cpp:150-189)   -> ltlg_submit_grid*
+//   LabelMatrix (:61-92)                                               -> ltlg_get_labels*
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/ltlgrid_gpu.h"
+#include "engine.h"
+#include "launch.h"
+
+
+using namespace ltlg;
+
+namespace {
+
+thread_local std::string g_error;
+
+// --- NCCL, loaded lazily so single-device engines never need it ------------
+struct Nccl {
+    bool tried = false, ok = false;
+    ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+Nccl& nccl() {
+    static Nccl n;
+    if (!n.tried) {
+        n.tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            n.CommInitAll = reinterpret_cast<decltype(n.CommInitAll)>(dlsym(h, "ncclCommInitAll"));
+            n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+            n.Broadcast = reinterpret_cast<decltype(n.Broadcast)>(dlsym(h, "ncclBroadcast"));
+            n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(dlsym(h, "ncclGroupStart"));
+            n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+            n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+            n.ok = n.CommInitAll && n.CommDestroy && n.Broadcast && n.GroupStart && n.GroupEnd;
+        }
+    }
+    return n;
+}
+
+template <typename T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t bytes = 0;
+    int device = 0;
+    cudaError_t reserve(size_t b) {
+        if (b <= bytes) return cudaSuccess;
+        release();
+        if (b == 0) return cudaSuccess;
+        cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&ptr), b);
+        if (e != cudaSuccess) {
+            ptr = nullptr;
+            bytes = 0;
+            return e;
+        }
+        bytes = b;
+        return cudaSuccess;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+};
+
+struct Shard {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    // profiling: a ring of kRing event quadruples (upload, summary, label, end)
+    static constexpr int kRing = 256;
+    std::vector<cudaEvent_t> ring;  // kRing * 4 when profiling
+    uint64_t submits = 0;           // profiled submits recorded so far
+    cudaEvent_t* ev = nullptr;      // the quadruple of the current submit
+    uint64_t row_begin = 0, row_end = 0, n_pairs = 0, words = 0;
+    uint32_t ntask_stream = 0, ntask_batch = 0;
+    DevBuf<Pair> pairs;
+    DevBuf<uint32_t> perm, trow_s, trow_b;
+    DevBuf<uint64_t> tpair_s, tpair_b;
+    DevBuf<uint64_t> P;  // frames x props x nw64
+    const uint64_t* P_in = nullptr;  // caller's device P used in place (single device)
+    const uint64_t* Pdev() const { return P_in ? P_in : P.ptr; }
+    DevBuf<uint8_t> sf;
+    DevBuf<uint8_t> labels;
+    DevBuf<uint64_t> stage;
+    DevBuf<uint64_t> world;
+    DevBuf<uint8_t> poses;
+    bool have_times = false;
+    uint64_t rows() const { return row_end - row_begin; }
+};
+
+}  // namespace
+
+struct ltlg_ctx {
+    std::vector<Shard> shards;
+    std::vector<ncclComm_t> comms;
+    ltlg_options opts{};
+    std::string err;
+    bool loaded = false, submitted = false;
+    uint64_t rows = 0, cols = 0, nnz = 0, words = 0, pairs = 0, t_bytes = 0;
+    int props = 0, frames = 0, label_bytes = 0;
+    uint64_t cells = 0;
+};
+
+namespace {
+
+ltlg_status set_err(ltlg_ctx* ctx, ltlg_status s, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    g_error = msg;
+    return s;
+}
+
+ltlg_status cuda_fail(ltlg_ctx* ctx, cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation)
+        return set_err(ctx, LTLG_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+    return set_err(ctx, LTLG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call, what)                                  \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, what); \
+    } while (0)
+
+int label_bytes_for(int props) {
+    if (props <= 8) return 1;
+    if (props <= 16) return 2;
+    if (props <= 32) return 4;
+    return 8;
+}
+
+uint32_t nw32_of(uint64_t cells) { return static_cast<uint32_t>(2 * ((cells + 63) / 64)); }
+
+ltlg_status upload_shard(ltlg_ctx* ctx, Shard& s, const PackedShard& p) {
+    CK(cudaSetDevice(s.device), "cudaSetDevice");
+    s.row_begin = p.row_begin;
+    s.row_end = p.row_end;
+    s.n_pairs = p.n_pairs;
+    s.words = p.words;
+    s.ntask_stream = static_cast<uint32_t>(p.task_row_stream.size() - 1);
+    s.ntask_batch = static_cast<uint32_t>(p.task_row_batch.size() - 1);
+    auto put = [&](auto& buf, const auto& vec, const char* what) -> ltlg_status {
+        using T = typename std::decay_t<decltype(vec)>::value_type;
+        const size_t b = vec.size() * sizeof(T);
+        cudaError_t e = buf.reserve(b ? b : sizeof(T));
+        if (e != cudaSuccess) return cuda_fail(ctx, e, what);
+        if (b) {
+            e = cudaMemcpy(buf.ptr, vec.data(), b, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, what);
+        }
+        return LTLG_OK;
+    };
+    ltlg_status st;
+    if ((st = put(s.pairs, p.pairs, "upload T pairs")) != LTLG_OK) return st;
+    if ((st = put(s.perm, p.perm, "upload row permutation")) != LTLG_OK) return st;
+    if ((st = put(s.trow_s, p.task_row_stream, "upload tasks")) != LTLG_OK) return st;
+    if ((st = put(s.tpair_s, p.task_pair_stream, "upload tasks")) != LTLG_OK) return st;
+    if ((st = put(s.trow_b, p.task_row_batch, "upload tasks")) != LTLG_OK) return st;
+    if ((st = put(s.tpair_b, p.task_pair_batch, "upload tasks")) != LTLG_OK) return st;
+    ctx->t_bytes += p.pairs.size() * sizeof(Pair) + p.perm.size() * 4;
+    return LTLG_OK;
+}
+
+ltlg_status load_words(ltlg_ctx* ctx, WordCsr& t) {
+    ctx->loaded = false;
+    ctx->submitted = false;
+    ctx->t_bytes = 0;
+    const int n = static_cast<int>(ctx->shards.size());
+    const uint32_t sentinel = nw32_of(t.cols);
+    if (static_cast<uint64_t>(sentinel) >= kWordMask)
+        return set_err(ctx, LTLG_EINVAL, "CSR column space too large for this build");
+    const std::vector<uint64_t> b = shard_bounds(t, n);
+    uint64_t pairs = 0;
+    for (int i = 0; i < n; ++i) {
+        PackedShard p;
+        if (b[i + 1] - b[i] > 0xffffffffull)
+            return set_err(ctx, LTLG_EINVAL, "a device shard holds more than 2^32-1 rows");
+        build_shard(t, b[i], b[i + 1], ctx->opts.sort_rows != 0, sentinel,
+                    ctx->opts.stream_task_pairs > 0 ? ctx->opts.stream_task_pairs : 2048,
+                    ctx->opts.batch_task_pairs > 0 ? ctx->opts.batch_task_pairs : 256, &p);
+        ltlg_status st = upload_shard(ctx, ctx->shards[static_cast<size_t>(i)], p);
+        if (st != LTLG_OK) return st;
+        pairs += p.n_pairs;
+    }
+    ctx->rows = t.rows;
+    ctx->cols = t.cols;
+    ctx->nnz = t.nnz;
+    ctx->words = t.offsets.empty() ? 0 : t.offsets[t.rows];
+    ctx->pairs = pairs;
+    ctx->loaded = true;
+    return LTLG_OK;
+}
+
+ltlg_status check_grid(ltlg_ctx* ctx, uint64_t cells, int num_props, int frames) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!ctx->loaded) return set_err(ctx, LTLG_ESTATE, "no abstraction loaded");
+    // DensePropMatrix ctor (label.cpp:122-128) before label_all's check (:151-154)
+    if (num_props > 64) return set_err(ctx, LTLG_EINVAL, "at most 64 propositions");
+    if (num_props < 0) return set_err(ctx, LTLG_EINVAL, "props must be in [0, 64]");
+    if (frames < 1) return set_err(ctx, LTLG_EINVAL, "frames must be >= 1");
+    if (ctx->cols != cells)
+        return set_err(ctx, LTLG_EINVAL,
+                       "dimension mismatch: matrix cols " + std::to_string(ctx->cols) +
+                           " vs proposition rows " + std::to_string(cells));
+    return LTLG_OK;
+}
+
+// Broadcast shard 0's P to the other devices (NCCL over NVLink when loaded).
+ltlg_status broadcast_P(ltlg_ctx* ctx, size_t words) {
+    const int n = static_cast<int>(ctx->shards.size());
+    if (n == 1 || words == 0) return LTLG_OK;
+    Shard& s0 = ctx->shards[0];
+    CK(cudaSetDevice(s0.device), "cudaSetDevice");
+    cudaEvent_t ready;
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+    CK(cudaEventRecord(ready, s0.stream), "event");
+    for (int i = 1; i < n; ++i) {
+        Shard& s = ctx->shards[static_cast<size_t>(i)];
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        CK(cudaStreamWaitEvent(s.stream, ready, 0), "stream wait");
+    }
+    if (!ctx->comms.empty()) {
+        Nccl& N = nccl();
+        N.GroupStart();
+        for (int i = 0; i < n; ++i) {
+            Shard& s = ctx->shards[static_cast<size_t>(i)];
+            cudaSetDevice(s.device);
+            ncclResult_t r = N.Broadcast(s0.P.ptr, s.P.ptr, words, ncclUint64, 0, ctx->comms[static_cast<size_t>(i)],
+                                         s.stream);
+            if (r != ncclSuccess) {
+                N.GroupEnd();
+                return set_err(ctx, LTLG_ENCCL, std::string("ncclBroadcast: ") + N.GetErrorString(r));
+            }
+        }
+        ncclResult_t r = N.GroupEnd();
+        if (r != ncclSuccess) return set_err(ctx, LTLG_ENCCL, std::string("ncclGroupEnd: ") + N.GetErrorString(r));
+    } else {
+        for (int i = 1; i < n; ++i) {
+            Shard& s = ctx->shards[static_cast<size_t>(i)];
+            CK(cudaSetDevice(s.device), "cudaSetDevice");
+            CK(cudaMemcpyPeerAsync(s.P.ptr, s.device, s0.P.ptr, s0.device, words * 8, s.stream), "peer copy");
+        }
+    }
+    cudaSetDevice(s0.device);
+    cudaEventDestroy(ready);
+    return LTLG_OK;
+}
+
+// Summary + labeling on every shard for P already resident in shard.P.
+ltlg_status run_label(ltlg_ctx* ctx) {
+    const uint32_t nw32 = nw32_of(ctx->cells);
+    const int props = ctx->props, frames = ctx->frames;
+    for (Shard& s : ctx->shards) {
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        const size_t lab = s.rows() * static_cast<size_t>(frames) * static_cast<size_t>(ctx->label_bytes);
+        CK(s.labels.reserve(lab ? lab : 8), "allocate labels");
+        if (props == 0 || s.rows() == 0) {
+            s.have_times = false;
+            continue;
+        }
+        CK(s.sf.reserve(static_cast<size_t>(nw32 + 1) * frames * summary_entry_bytes(props)), "allocate summary");
+        const bool prof = ctx->opts.profile != 0;
+        if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
+        CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
+                          s.stream),
+           "summary kernel");
+        if (prof) CK(cudaEventRecord(s.ev[2], s.stream), "event");
+        LaunchArgs a{};
+        a.pairs = s.pairs.ptr;
+        a.perm = s.perm.ptr;
+        a.sf = s.sf.ptr;
+        a.P32 = reinterpret_cast<const uint32_t*>(s.Pdev());
+        a.nw32 = nw32;
+        a.props = props;
+        a.frames = frames;
+        a.out = s.labels.ptr;
+        a.label_bytes = ctx->label_bytes;
+        if (frames == 1) {
+            a.task_pair = s.tpair_s.ptr;
+            a.task_row = s.trow_s.ptr;
+            a.ntasks = s.ntask_stream;
+        } else {
+            a.task_pair = s.tpair_b.ptr;
+            a.task_row = s.trow_b.ptr;
+            a.ntasks = s.ntask_batch;
+        }
+        CK(launch_label(a, s.stream), "label kernel");
+        if (prof) CK(cudaEventRecord(s.ev[3], s.stream), "event");
+        s.have_times = prof;
+    }
+    ctx->submitted = true;
+    return LTLG_OK;
+}
+
+ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* words, int frames,
+                   bool on_device) {
+    ltlg_status st = check_grid(ctx, cells, num_props, frames);
+    if (st != LTLG_OK) return st;
+    ctx->cells = cells;
+    ctx->props = num_props;
+    ctx->frames = frames;
+    ctx->label_bytes = label_bytes_for(num_props);
+    const size_t nwords = static_cast<size_t>(frames) * num_props * ((cells + 63) / 64);
+    if (nwords && !words) return set_err(ctx, LTLG_EINVAL, "null column_words");
+    // A single-device engine reads a device-resident P in place (no copy);
+    // the caller keeps it alive and unmodified until the labels are ready.
+    const bool in_place = on_device && ctx->shards.size() == 1;
+    for (Shard& s : ctx->shards) {
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        if (!in_place) CK(s.P.reserve(nwords * 8 + 16), "allocate P");
+    }
+    if (ctx->opts.profile)
+        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
+    Shard& s0 = ctx->shards[0];
+    CK(cudaSetDevice(s0.device), "cudaSetDevice");
+    if (ctx->opts.profile) CK(cudaEventRecord(s0.ev[0], s0.stream), "event");
+    s0.P_in = in_place ? words : nullptr;
+    if (nwords && !in_place)
+        CK(cudaMemcpyAsync(s0.P.ptr, words, nwords * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           s0.stream),
+           "upload P");
+    if ((st = broadcast_P(ctx, nwords)) != LTLG_OK) return st;
+    if (ctx->opts.profile)
+        for (size_t i = 1; i < ctx->shards.size(); ++i) {
+            cudaSetDevice(ctx->shards[i].device);
+            cudaEventRecord(ctx->shards[i].ev[0], ctx->shards[i].stream);
+        }
+    return run_label(ctx);
+}
+
+ltlg_status sync_all(ltlg_ctx* ctx) {
+    for (Shard& s : ctx->shards) {
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        CK(cudaStreamSynchronize(s.stream), "labeling");
+    }
+    return LTLG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ltlg_abi_version(void) { return LTLG_ABI_VERSION; }
+
+const char* ltlg_last_error(const ltlg_ctx* ctx) { return ctx ? ctx->err.c_str() : g_error.c_str(); }
+
+ltlg_status ltlg_create_ex(const int* devices, int n_devices, const ltlg_options* opts, ltlg_ctx** out) {
+    if (!out) return set_err(nullptr, LTLG_EINVAL, "null output handle");
+    *out = nullptr;
+    if (n_devices < 1) n_devices = 1;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return set_err(nullptr, LTLG_ECUDA,
+                       std::string("no CUDA device available: ") + (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+    auto ctx = std::make_unique<ltlg_ctx>();
+    if (opts) ctx->opts = *opts;
+    else ctx->opts.sort_rows = 1;
+    ctx->shards.resize(static_cast<size_t>(n_devices));
+    std::vector<int> devs;
+    for (int i = 0; i < n_devices; ++i) {
+        const int d = devices ? devices[i] : i;
+        if (d < 0 || d >= count) return set_err(nullptr, LTLG_EINVAL, "device index out of range: " + std::to_string(d));
+        Shard& s = ctx->shards[static_cast<size_t>(i)];
+        s.device = d;
+        devs.push_back(d);
+        if ((e = cudaSetDevice(d)) != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+        int major = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d);
+        if (major != 10)
+            return set_err(nullptr, LTLG_ECUDA, "device " + std::to_string(d) + " is not sm_100 (built for B200 only)");
+        if ((e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(nullptr, e, "stream");
+        if (ctx->opts.profile) {
+            s.ring.assign(Shard::kRing * 4, nullptr);
+            for (auto& ev : s.ring)
+                if ((e = cudaEventCreate(&ev)) != cudaSuccess) return cuda_fail(nullptr, e, "event");
+        }
+    }
+    if (n_devices > 1) {
+        Nccl& N = nccl();
+        if (N.ok) {
+            ctx->comms.resize(static_cast<size_t>(n_devices));
+            ncclResult_t r = N.CommInitAll(ctx->comms.data(), n_devices, devs.data());
+            if (r != ncclSuccess) {
+                ctx->comms.clear();
+                return set_err(nullptr, LTLG_ENCCL, std::string("ncclCommInitAll: ") + N.GetErrorString(r));
+            }
+        } else {
+            for (int i = 0; i < n_devices; ++i)
+                for (int j = 0; j < n_devices; ++j)
+                    if (i != j) {
+                        cudaSetDevice(devs[static_cast<size_t>(i)]);
+                        cudaDeviceEnablePeerAccess(devs[static_cast<size_t>(j)], 0);
+                        cudaGetLastError();
+                    }
+        }
+    }
+    *out = ctx.release();
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_create(const int* devices, int n_devices, ltlg_ctx** out) {
+    ltlg_options o{};
+    o.sort_rows = 1;
+    return ltlg_create_ex(devices, n_devices, &o, out);
+}
+
+void ltlg_destroy(ltlg_ctx* ctx) {
+    if (!ctx) return;
+    for (ncclComm_t c : ctx->comms) nccl().CommDestroy(c);
+    for (Shard& s : ctx->shards) {
+        cudaSetDevice(s.device);
+        if (s.stream) cudaStreamSynchronize(s.stream);
+        s.pairs.release();
+        s.perm.release();
+        s.trow_s.release();
+        s.trow_b.release();
+        s.tpair_s.release();
+        s.tpair_b.release();
+        s.P.release();
+        s.sf.release();
+        s.labels.release();
+        s.stage.release();
+        s.world.release();
+        s.poses.release();
+        for (auto& ev : s.ring)
+            if (ev) cudaEventDestroy(ev);
+        if (s.stream) cudaStreamDestroy(s.stream);
+    }
+    delete ctx;
+}
+
+ltlg_status ltlg_load_abstraction(ltlg_ctx* ctx, uint64_t rows, uint64_t cols, const uint64_t* row_offsets,
+                                  const uint32_t* col_indices) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!row_offsets) return set_err(ctx, LTLG_EINVAL, "row_offsets must have rows+1 entries");
+    Error err{S_OK, ""};
+    const uint64_t nnz = row_offsets[rows];
+    if (nnz && !col_indices) return set_err(ctx, LTLG_EINVAL, "null col_indices");
+    if (!validate_csr(rows, cols, row_offsets, rows + 1, col_indices, nnz, &err))
+        return set_err(ctx, static_cast<ltlg_status>(err.code), err.msg);
+    if (cols > (1ull << 36)) return set_err(ctx, LTLG_EINVAL, "CSR column space too large for this build");
+    WordCsr t;
+    if (!pack_csr(rows, cols, row_offsets, col_indices, &t, &err))
+        return set_err(ctx, static_cast<ltlg_status>(err.code), err.msg);
+    return load_words(ctx, t);
+}
+
+ltlg_status ltlg_load_abstraction_file(ltlg_ctx* ctx, const char* path) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!path) return set_err(ctx, LTLG_EINVAL, "null path");
+    uint64_t rows = 0, cols = 0;
+    std::vector<uint64_t> off;
+    std::vector<uint32_t> idx;
+    Error err{S_OK, ""};
+    if (!read_csb1(path, &rows, &cols, &off, &idx, &err))
+        return set_err(ctx, static_cast<ltlg_status>(err.code), err.msg);
+    WordCsr t;
+    pack_csr(rows, cols, off.data(), idx.data(), &t, &err);
+    return load_words(ctx, t);
+}
+
+ltlg_status ltlg_load_abstraction_words(ltlg_ctx* ctx, uint64_t rows, uint64_t cols, const uint64_t* row_word_offsets,
+                                        const uint32_t* word_index, const uint32_t* word_mask) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!row_word_offsets) return set_err(ctx, LTLG_EINVAL, "row_offsets must have rows+1 entries");
+    if (row_word_offsets[rows] && (!word_index || !word_mask))
+        return set_err(ctx, LTLG_EINVAL, "null word arrays");
+    if (cols > (1ull << 36)) return set_err(ctx, LTLG_EINVAL, "CSR column space too large for this build");
+    Error err{S_OK, ""};
+    WordCsr t;
+    if (!take_words(rows, cols, row_word_offsets, word_index, word_mask, &t, &err))
+        return set_err(ctx, static_cast<ltlg_status>(err.code), err.msg);
+    return load_words(ctx, t);
+}
+
+ltlg_status ltlg_submit_grid(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* column_words, int frames) {
+    return submit(ctx, cells, num_props, column_words, frames, false);
+}
+
+ltlg_status ltlg_submit_grid_device(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* dev_words,
+                                    int frames) {
+    return submit(ctx, cells, num_props, dev_words, frames, true);
+}
+
+ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, const ltlg_grid2* world, int num_props,
+                                   const uint64_t* world_words, int words_on_device, const ltlg_pose2* poses,
+                                   int frames, int outside) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!vehicle || !world || !poses) return set_err(ctx, LTLG_EINVAL, "null grid or pose");
+    if (vehicle->depth < 2 || vehicle->depth > 32 || world->depth < 2 || world->depth > 32)
+        return set_err(ctx, LTLG_EINVAL, "grid depth must be in [2, 32]");
+    if (!(vehicle->lo0 < vehicle->hi0 && vehicle->lo1 < vehicle->hi1 && world->lo0 < world->hi0 &&
+          world->lo1 < world->hi1))
+        return set_err(ctx, LTLG_EINVAL, "grid bounds must satisfy lo < hi");
+    const uint64_t cells = 1ull << vehicle->depth;
+    ltlg_status st = check_grid(ctx, cells, num_props, frames);
+    if (st != LTLG_OK) return st;
+    ctx->cells = cells;
+    ctx->props = num_props;
+    ctx->frames = frames;
+    ctx->label_bytes = label_bytes_for(num_props);
+    const uint64_t wcells = 1ull << world->depth;
+    const size_t wwords = static_cast<size_t>(num_props) * ((wcells + 63) / 64);
+    const size_t vwords = static_cast<size_t>(frames) * num_props * ((cells + 63) / 64);
+    if (wwords && !world_words) return set_err(ctx, LTLG_EINVAL, "null world_words");
+    for (Shard& s : ctx->shards) {
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        CK(s.P.reserve(vwords * 8 + 16), "allocate P");
+    }
+    if (ctx->opts.profile)
+        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
+    Shard& s0 = ctx->shards[0];
+    CK(cudaSetDevice(s0.device), "cudaSetDevice");
+    s0.P_in = nullptr;
+    if (ctx->opts.profile) CK(cudaEventRecord(s0.ev[0], s0.stream), "event");
+    const uint64_t* wsrc = world_words;
+    if (!words_on_device && wwords) {
+        CK(s0.world.reserve(wwords * 8), "allocate world grid");
+        CK(cudaMemcpyAsync(s0.world.ptr, world_words, wwords * 8, cudaMemcpyHostToDevice, s0.stream), "upload world");
+        wsrc = s0.world.ptr;
+    }
+    CK(s0.poses.reserve(sizeof(ltlg_pose2) * static_cast<size_t>(frames)), "allocate poses");
+    CK(cudaMemcpyAsync(s0.poses.ptr, poses, sizeof(ltlg_pose2) * static_cast<size_t>(frames), cudaMemcpyHostToDevice,
+                       s0.stream),
+       "upload poses");
+    CK(launch_resample(vehicle->depth, vehicle->lo0, vehicle->hi0, vehicle->lo1, vehicle->hi1, world->depth, world->lo0,
+                       world->hi0, world->lo1, world->hi1, s0.poses.ptr, frames, num_props,
+                       reinterpret_cast<const uint32_t*>(wsrc), nw32_of(wcells), outside ? 1 : 0, nw32_of(cells),
+                       reinterpret_cast<uint32_t*>(s0.P.ptr), s0.stream),
+       "resample kernel");
+    // pageable pose upload must complete before the caller's buffer may change
+    CK(cudaStreamSynchronize(s0.stream), "resample");
+    if ((st = broadcast_P(ctx, vwords)) != LTLG_OK) return st;
+    return run_label(ctx);
+}
+
+ltlg_status ltlg_wait(ltlg_ctx* ctx) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    return sync_all(ctx);
+}
+
+ltlg_status ltlg_get_labels(ltlg_ctx* ctx, int frame, uint64_t* out) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
+    if (frame < 0 || frame >= ctx->frames) return set_err(ctx, LTLG_EINVAL, "frame out of range");
+    if (ctx->props == 0 || ctx->rows == 0) return sync_all(ctx);
+    if (!out) return set_err(ctx, LTLG_EINVAL, "null output");
+    for (Shard& s : ctx->shards) {
+        if (s.rows() == 0) continue;
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        CK(s.stage.reserve(s.rows() * 8), "allocate staging");
+        CK(launch_extract(s.labels.ptr, ctx->label_bytes, s.rows(), ctx->frames, frame, s.stage.ptr, s.stream),
+           "extract kernel");
+        CK(cudaMemcpyAsync(out + s.row_begin, s.stage.ptr, s.rows() * 8, cudaMemcpyDeviceToHost, s.stream),
+           "download labels");
+    }
+    return sync_all(ctx);
+}
+
+ltlg_status ltlg_get_labels_packed(ltlg_ctx* ctx, void* out, size_t out_bytes) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
+    const size_t per_row = static_cast<size_t>(ctx->frames) * static_cast<size_t>(ctx->label_bytes);
+    if (ctx->props == 0) return sync_all(ctx);
+    if (out_bytes < ctx->rows * per_row) return set_err(ctx, LTLG_EINVAL, "output buffer too small");
+    for (Shard& s : ctx->shards) {
+        if (s.rows() == 0) continue;
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        CK(cudaMemcpyAsync(static_cast<uint8_t*>(out) + s.row_begin * per_row, s.labels.ptr, s.rows() * per_row,
+                           cudaMemcpyDeviceToHost, s.stream),
+           "download labels");
+    }
+    return sync_all(ctx);
+}
+
+ltlg_status ltlg_device_labels(ltlg_ctx* ctx, int shard, void** dev_ptr, uint64_t* row_begin, uint64_t* row_end,
+                               int* device) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return set_err(ctx, LTLG_EINVAL, "shard out of range");
+    if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
+    Shard& s = ctx->shards[static_cast<size_t>(shard)];
+    if (dev_ptr) *dev_ptr = s.labels.ptr;
+    if (row_begin) *row_begin = s.row_begin;
+    if (row_end) *row_end = s.row_end;
+    if (device) *device = s.device;
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_get_info(ltlg_ctx* ctx, ltlg_info* out) {
+    if (!ctx || !out) return set_err(ctx, LTLG_EINVAL, "null argument");
+    std::memset(out, 0, sizeof(*out));
+    out->rows = ctx->rows;
+    out->cols = ctx->cols;
+    out->nnz = ctx->nnz;
+    out->words = ctx->words;
+    out->pairs = ctx->pairs;
+    out->t_bytes = ctx->t_bytes;
+    out->n_devices = static_cast<int>(ctx->shards.size());
+    out->props = ctx->props;
+    out->frames = ctx->frames;
+    out->label_bytes = ctx->label_bytes;
+    out->label_words = (ctx->props + 63) / 64;
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_stream(ltlg_ctx* ctx, int shard, void** stream) {
+    if (!ctx || !stream) return set_err(ctx, LTLG_EINVAL, "null argument");
+    if (shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return set_err(ctx, LTLG_EINVAL, "shard out of range");
+    *stream = ctx->shards[static_cast<size_t>(shard)].stream;
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_stage_times(ltlg_ctx* ctx, int shard, int back, float* upload_ms, float* summary_ms,
+                             float* label_ms) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return set_err(ctx, LTLG_EINVAL, "shard out of range");
+    Shard& s = ctx->shards[static_cast<size_t>(shard)];
+    if (!ctx->opts.profile || !s.have_times) return set_err(ctx, LTLG_ESTATE, "no profiled submit on this shard");
+    if (back < 0 || back >= Shard::kRing || static_cast<uint64_t>(back) >= s.submits)
+        return set_err(ctx, LTLG_EINVAL, "profiled submit out of range");
+    CK(cudaSetDevice(s.device), "cudaSetDevice");
+    cudaEvent_t* q = &s.ring[static_cast<size_t>((s.submits - 1 - static_cast<uint64_t>(back)) % Shard::kRing) * 4];
+    CK(cudaEventSynchronize(q[3]), "sync");
+    float a = 0, b = 0, c = 0;
+    CK(cudaEventElapsedTime(&a, q[0], q[1]), "event time");
+    CK(cudaEventElapsedTime(&b, q[1], q[2]), "event time");
+    CK(cudaEventElapsedTime(&c, q[2], q[3]), "event time");
+    if (upload_ms) *upload_ms = a;
+    if (summary_ms) *summary_ms = b;
+    if (label_ms) *label_ms = c;
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_validate_csr(uint64_t rows, uint64_t cols, const uint64_t* row_offsets, uint64_t n_offsets,
+                              const uint32_t* col_indices, uint64_t nnz, char* err, size_t err_len) {
+    Error e{S_OK, ""};
+    if (!row_offsets && n_offsets) e = Error{S_EINVAL, "null row_offsets"};
+    else if (!col_indices && nnz) e = Error{S_EINVAL, "null col_indices"};
+    else validate_csr(rows, cols, row_offsets, n_offsets, col_indices, nnz, &e);
+    if (err && err_len) {
+        std::strncpy(err, e.msg.c_str(), err_len - 1);
+        err[err_len - 1] = '\0';
+    }
+    if (e.code != S_OK) g_error = e.msg;
+    return static_cast<ltlg_status>(e.code);
+}
+
+ltlg_status ltlg_label_all(uint64_t rows, uint64_t cols, const uint64_t* row_offsets, const uint32_t* col_indices,
+                           uint64_t cells, int num_props, const uint64_t* column_words, int workers, uint64_t* out) {
+    (void)workers;
+    if (num_props > 64) return set_err(nullptr, LTLG_EINVAL, "at most 64 propositions");
+    if (num_props < 0) return set_err(nullptr, LTLG_EINVAL, "props must be in [0, 64]");
+    if (cols != cells)
+        return set_err(nullptr, LTLG_EINVAL,
+                       "dimension mismatch: matrix cols " + std::to_string(cols) + " vs proposition rows " +
+                           std::to_string(cells));
+    ltlg_ctx* ctx = nullptr;
+    ltlg_status st = ltlg_create(nullptr, 1, &ctx);
+    if (st != LTLG_OK) return st;
+    st = ltlg_load_abstraction(ctx, rows, cols, row_offsets, col_indices);
+    if (st == LTLG_OK) st = ltlg_submit_grid(ctx, cells, num_props, column_words, 1);
+    if (st == LTLG_OK && num_props > 0) st = ltlg_get_labels(ctx, 0, out);
+    if (st != LTLG_OK) g_error = ctx->err;
+    ltlg_destroy(ctx);
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// engine.h -- internal types of the B200 labeling engine (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace ltlg {
+
+// Status codes mirror ltlg_status in include/ltlgrid_gpu.h.
+enum Status : int { S_OK = 0, S_EINVAL = 1, S_EFORMAT = 2, S_EIO = 3, S_ECUDA = 4, S_ENCCL = 5, S_ENOMEM = 6, S_ESTATE = 7 };
+
+struct Error {
+    Status code;
+    std::string msg;
+};
+
+// One T pair as stored in HBM: 8 bytes, AoS so a 16-byte load yields two.
+//   mask : bit b = cell 32*word + b of the row's swept volume
+//   word : bits 0..30 word index (z-order), bit 31 = first pair of its row
+struct Pair {
+    uint32_t mask;
+    uint32_t word;
+};
+constexpr uint32_t kHead = 0x80000000u;
+constexpr uint32_t kWordMask = 0x7fffffffu;
+
+// Word-CSR of the whole abstraction in ORIGINAL row order (host).
+struct WordCsr {
+    uint64_t rows = 0, cols = 0, nnz = 0;
+    std::vector<uint64_t> offsets;  // rows + 1
+    std::vector<uint32_t> word;     // W32
+    std::vector<uint32_t> mask;     // W32
+};
+
+// The device image of one shard (host staging copy).
+struct PackedShard {
+    uint64_t row_begin = 0, row_end = 0;  // original rows [row_begin, row_end)
+    uint64_t words = 0;                   // W32 of the shard
+    std::vector<Pair> pairs;              // sorted-row order, padded (see kPairPad)
+    uint64_t n_pairs = 0;                 // meaningful pairs (incl. sentinels)
+    std::vector<uint32_t> perm;           // sorted position -> local original row
+    // warp tasks: [row_begin, row_end) in sorted positions, pairs [pair_begin, pair_end)
+    std::vector<uint32_t> task_row_stream, task_row_batch;    // ntasks + 1
+    std::vector<uint64_t> task_pair_stream, task_pair_batch;  // ntasks + 1
+};
+
+constexpr uint64_t kPairPad = 256;  // tail padding so vector loads never leave the array
+
+// Host-side loader (loader.cpp).
+bool validate_csr(uint64_t rows, uint64_t cols, const uint64_t* offsets, uint64_t n_offsets,
+                  const uint32_t* indices, uint64_t nnz, Error* err);
+bool pack_csr(uint64_t rows, uint64_t cols, const uint64_t* offsets, const uint32_t* indices,
+              WordCsr* out, Error* err);
+bool take_words(uint64_t rows, uint64_t cols, const uint64_t* offsets, const uint32_t* word,
+                const uint32_t* mask, WordCsr* out, Error* err);
+bool read_csb1(const char* path, uint64_t* rows, uint64_t* cols, std::vector<uint64_t>* offsets,
+               std::vector<uint32_t>* indices, Error* err);
+// Split rows into n contiguous shards balanced by stored pairs.
+std::vector<uint64_t> shard_bounds(const WordCsr& t, int n);
+void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
+                 uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs,
+                 PackedShard* out);
+int host_threads();
+
+}  // namespace ltlg

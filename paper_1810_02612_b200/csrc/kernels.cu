@@ -1,0 +1,455 @@
+// kernels.cu -- sm_100a kernels of the labeling path L = T o P (OR-AND).
+//
+// Reference semantics (proj/core/src/label.cpp:150-189): L(i,j) = 1 iff some
+// stored cell c of row i has P_j[c] = 1.  The reference scans each row once
+// per proposition with a random bit probe per cell; here a row is a list of
+// (32-bit z-word, mask) pairs and one pair answers every proposition at once:
+//
+//   hit_j(w, m) = (m & P_j[w]) != 0.
+//
+// A per-frame summary of P makes that test mostly table-driven:
+//   S[w] bit j = P_j[w] != 0           (some cell of the word is set)
+//   F[w] bit j = P_j[w] covers the word (every valid cell of the word is set)
+// Since every stored mask is non-zero, F[w] props hit unconditionally, props
+// outside S[w] never hit, and only the "partial" props S & ~F need the exact
+// (m & P_j[w]) probe -- this is exact, not a heuristic.  For the bench
+// archetypes (a 90%-occupancy lane complement and 1.5%-occupancy boxes) the
+// partial set is empty for most (pair, frame) visits.
+//
+// Kernels:
+//   summary_kernel       P columns -> {S, F} per (word, frame)
+//   label_stream_kernel  single frame; lanes own 4 consecutive pairs each, rows
+//                        are recovered with a warp-wide segmented OR scan over
+//                        head flags (T is streamed once with 2x16-byte
+//                        L1::no_allocate loads; HBM-bound)
+//   label_batch_kernel   F frames; lanes own frames, pairs are broadcast by
+//                        shuffle, each T pair is read from HBM once for all F
+//   extract_kernel       one frame of the packed labels -> LabelMatrix u64 words
+//   resample_kernel      world-frame grid + pose -> vehicle-frame P columns
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "engine.h"
+#include "launch.h"
+
+namespace ltlg {
+
+template <typename LW>
+struct alignas(2 * sizeof(LW)) SF {
+    LW s;  // some cell of the word set, per prop
+    LW f;  // every valid cell of the word set, per prop
+};
+
+__device__ __forceinline__ uint4 ld_stream16(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint2 ld_stream8(const void* p) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+
+template <typename LW>
+__device__ __forceinline__ SF<LW> ld_sf(const SF<LW>* p);
+
+template <>
+__device__ __forceinline__ SF<uint32_t> ld_sf<uint32_t>(const SF<uint32_t>* p) {
+    uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    return SF<uint32_t>{v.x, v.y};
+}
+
+template <>
+__device__ __forceinline__ SF<uint64_t> ld_sf<uint64_t>(const SF<uint64_t>* p) {
+    ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    return SF<uint64_t>{v.x, v.y};
+}
+
+__device__ __forceinline__ int lowest_bit(uint32_t x) { return __ffs(x) - 1; }
+__device__ __forceinline__ int lowest_bit(uint64_t x) { return __ffsll(static_cast<long long>(x)) - 1; }
+
+template <typename LW>
+__device__ __forceinline__ LW shfl_up(LW v, int d) {
+    return __shfl_up_sync(0xffffffffu, v, d);
+}
+template <typename LW>
+__device__ __forceinline__ LW shfl_idx(LW v, int l) {
+    return __shfl_sync(0xffffffffu, v, l);
+}
+
+// Label contribution of one stored pair (mask m of word w) for one frame.
+//   sfe  : the frame's summary entry of word w
+//   col0 : the frame's P column 0 (u32 view); column j starts at col0 + j*nw32
+template <typename LW>
+__device__ __forceinline__ LW pair_hits(uint32_t m, uint32_t w, SF<LW> sfe, LW skip,
+                                        const uint32_t* __restrict__ col0, uint32_t nw32) {
+    LW v = sfe.f;
+    LW cand = sfe.s & ~sfe.f & ~skip;
+    while (cand) {
+        const int j = lowest_bit(cand);
+        if (m & __ldg(col0 + static_cast<uint64_t>(j) * nw32 + w)) v |= LW(1) << j;
+        cand &= cand - 1;
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Summary build: thread per (word, frame).  P32 = frames x props x nw32 u32.
+// Output layout sf[w * frames + f]; entry nw32 of every frame is the all-zero
+// sentinel that empty rows point at.
+// ---------------------------------------------------------------------------
+template <typename LW>
+__global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict__ P32, int props, int frames,
+                                                      uint32_t nw32, uint64_t cells,
+                                                      SF<LW>* __restrict__ sf) {
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int f = blockIdx.y;
+    if (w > nw32) return;
+    LW s = 0, full = 0;
+    const uint64_t lo = static_cast<uint64_t>(w) * 32;
+    if (w < nw32 && lo < cells) {
+        const uint32_t valid = (cells - lo >= 32) ? 0xffffffffu : ((1u << (cells - lo)) - 1u);
+        const uint32_t* base = P32 + static_cast<uint64_t>(f) * props * nw32 + w;
+#pragma unroll 4
+        for (int j = 0; j < props; ++j) {
+            const uint32_t x = base[static_cast<uint64_t>(j) * nw32] & valid;
+            s |= LW(x != 0) << j;
+            full |= LW(x == valid) << j;
+        }
+    }
+    sf[static_cast<uint64_t>(w) * frames + f] = SF<LW>{s, full};
+}
+
+// ---------------------------------------------------------------------------
+// Single frame.  One warp per task (a run of whole rows, pairs [p0, p1)).
+// ---------------------------------------------------------------------------
+template <typename LW, typename SW>
+__global__ void __launch_bounds__(256)
+    label_stream_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
+                        const uint32_t* __restrict__ task_row, uint32_t ntasks,
+                        const SF<LW>* __restrict__ sf, const uint32_t* __restrict__ P32, uint32_t nw32,
+                        const uint32_t* __restrict__ perm, SW* __restrict__ out) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= ntasks) return;
+    const uint64_t p0 = task_pair[warp], p1 = task_pair[warp + 1];
+    const int64_t r0 = task_row[warp];
+    const uint32_t lt = (1u << lane) - 1u;
+    int64_t open_row = r0 - 1;  // row owning `carry`
+    LW carry = 0;
+
+    uint64_t c = p0 & ~uint64_t(3);
+    uint4 a = ld_stream16(pairs + c + 4 * lane);
+    uint4 b = ld_stream16(pairs + c + 4 * lane + 2);
+    for (; c < p1; c += 128) {
+        // software prefetch of the next chunk (array is padded by kPairPad)
+        const uint64_t cn = c + 128;
+        uint4 an = a, bn = b;
+        if (cn < p1) {
+            an = ld_stream16(pairs + cn + 4 * lane);
+            bn = ld_stream16(pairs + cn + 4 * lane + 2);
+        }
+        const uint64_t q0 = c + 4 * lane;
+        const uint32_t mk[4] = {a.x, a.z, b.x, b.z};
+        const uint32_t wh[4] = {a.y, a.w, b.y, b.w};
+        bool head[4];
+        LW v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint64_t q = q0 + k;
+            const bool valid = q >= p0 && q < p1;
+            head[k] = valid && (wh[k] & kHead);
+            v[k] = 0;
+            if (valid) {
+                const uint32_t w = wh[k] & kWordMask;
+                v[k] = pair_hits<LW>(mk[k], w, ld_sf(sf + w), LW(0), P32, nw32);
+            }
+        }
+        int hb = 0, tot = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, head[k]);
+            hb += __popc(bal & lt);
+            tot += __popc(bal);
+        }
+        // lane-local segmentation: rows that start and end inside this lane
+        LW pre = 0, cur = 0;
+        int nh = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (head[k]) {
+                if (nh) {
+                    const int64_t row = open_row + hb + nh;
+                    out[perm[row]] = static_cast<SW>(cur);
+                } else {
+                    pre = cur;
+                }
+                ++nh;
+                cur = 0;
+            }
+            cur |= v[k];
+        }
+        if (!nh) pre = cur;
+        // warp-wide inclusive segmented OR scan; lane 0 carries the open row
+        LW x = nh ? cur : pre;
+        if (lane == 0 && !nh) x |= carry;
+        bool f = nh > 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const LW xo = shfl_up(x, d);
+            const bool fo = __shfl_up_sync(0xffffffffu, static_cast<int>(f), d) != 0;
+            if (lane >= d) {
+                if (!f) x |= xo;
+                f = f || fo;
+            }
+        }
+        LW excl = shfl_up(x, 1);
+        if (lane == 0) excl = carry;
+        if (nh) {
+            const int64_t row = open_row + hb;  // the row open before this lane's first head
+            if (row >= r0) out[perm[row]] = static_cast<SW>(excl | pre);
+        }
+        carry = shfl_idx(x, 31);
+        open_row += tot;
+        a = an;
+        b = bn;
+    }
+    if (lane == 0 && open_row >= r0) out[perm[open_row]] = static_cast<SW>(carry);
+}
+
+// ---------------------------------------------------------------------------
+// F frames.  One warp per task; lane l owns frames l, l+32, ... (FPL of them).
+// sf[w * frames + f], P32 frame f column j at (f*props + j) * nw32,
+// out[perm[row] * frames + f] (edge-major).
+// ---------------------------------------------------------------------------
+template <typename LW, typename SW, int FPL>
+__global__ void __launch_bounds__(256)
+    label_batch_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
+                       const uint32_t* __restrict__ task_row, uint32_t ntasks,
+                       const SF<LW>* __restrict__ sf, const uint32_t* __restrict__ P32, uint32_t nw32,
+                       int props, int frames, const uint32_t* __restrict__ perm, SW* __restrict__ out) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= ntasks) return;
+    const uint64_t p0 = task_pair[warp], p1 = task_pair[warp + 1];
+    const int64_t r0 = task_row[warp];
+    int64_t row = r0 - 1;
+    const uint64_t frame_stride = static_cast<uint64_t>(props) * nw32;
+    LW acc[FPL];
+#pragma unroll
+    for (int q = 0; q < FPL; ++q) acc[q] = 0;
+
+    auto store = [&](int64_t r) {
+        const uint64_t base = static_cast<uint64_t>(perm[r]) * frames;
+#pragma unroll
+        for (int q = 0; q < FPL; ++q) {
+            const int f = lane + 32 * q;
+            if (f < frames) out[base + f] = static_cast<SW>(acc[q]);
+        }
+    };
+
+    uint2 cur = ld_stream8(pairs + p0 + lane);
+    for (uint64_t c = p0; c < p1; c += 32) {
+        uint2 nxt = cur;
+        if (c + 32 < p1) nxt = ld_stream8(pairs + c + 32 + lane);
+        const int n = static_cast<int>(p1 - c < 32 ? p1 - c : 32);
+        for (int i = 0; i < n; ++i) {
+            const uint32_t m = __shfl_sync(0xffffffffu, cur.x, i);
+            const uint32_t wh = __shfl_sync(0xffffffffu, cur.y, i);
+            if (wh & kHead) {  // warp-uniform
+                if (row >= r0) store(row);
+                ++row;
+#pragma unroll
+                for (int q = 0; q < FPL; ++q) acc[q] = 0;
+            }
+            const uint32_t w = wh & kWordMask;
+            const SF<LW>* e = sf + static_cast<uint64_t>(w) * frames;
+#pragma unroll
+            for (int q = 0; q < FPL; ++q) {
+                const int f = lane + 32 * q;
+                if (f < frames)
+                    acc[q] |= pair_hits<LW>(m, w, ld_sf(e + f), acc[q], P32 + f * frame_stride, nw32);
+            }
+        }
+        cur = nxt;
+    }
+    if (row >= r0) store(row);
+}
+
+// One frame of packed edge-major labels -> LabelMatrix u64 words.
+template <typename SW>
+__global__ void extract_kernel(const SW* __restrict__ labels, uint64_t rows, int frames, int frame,
+                               uint64_t* __restrict__ out) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i < rows) out[i] = static_cast<uint64_t>(labels[i * frames + frame]);
+}
+
+// ---------------------------------------------------------------------------
+// World -> vehicle resample (north_star subsystem 2).  Thread per (vehicle
+// 32-bit word, group of 8 props, frame).  fp64 with explicit round-to-nearest
+// intrinsics in the order of oracle_resample (built with -ffp-contract=off),
+// so results are bit-identical to the CPU restatement.
+// ---------------------------------------------------------------------------
+struct Grid2 {
+    int depth;
+    double lo0, hi0, lo1, hi1;
+};
+struct Pose2 {
+    double dx, dy, c, s;
+};
+
+__device__ __forceinline__ int axis_bits2(int depth, int axis) { return depth / 2 + (axis < depth % 2 ? 1 : 0); }
+
+__device__ __forceinline__ int64_t quantize_dev(double lo, double hi, int bits, double x) {
+    if (!(x >= lo && x < hi)) return -1;
+    const double z = __ddiv_rn(__dadd_rn(x, -lo), __dadd_rn(hi, -lo));
+    const double scaled = floor(__dmul_rn(z, static_cast<double>(1ull << bits)));
+    uint64_t c = static_cast<uint64_t>(scaled);
+    if (c >= (1ull << bits)) c = (1ull << bits) - 1;
+    return static_cast<int64_t>(c);
+}
+
+__global__ void resample_kernel(Grid2 vg, Grid2 wg, const Pose2* __restrict__ poses, int props,
+                                const uint32_t* __restrict__ world32, uint32_t wnw32, int outside,
+                                uint32_t vnw32, uint32_t* __restrict__ out32) {
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int g0 = blockIdx.y * 8;
+    const int f = blockIdx.z;
+    if (w >= vnw32) return;
+    const Pose2 ps = poses[f];
+    const int bvx = axis_bits2(vg.depth, 0), bvy = axis_bits2(vg.depth, 1);
+    const int bwx = axis_bits2(wg.depth, 0), bwy = axis_bits2(wg.depth, 1);
+    const uint64_t vcells = 1ull << vg.depth;
+    const double wxv = __ddiv_rn(__dadd_rn(vg.hi0, -vg.lo0), static_cast<double>(1ull << bvx));
+    const double wyv = __ddiv_rn(__dadd_rn(vg.hi1, -vg.lo1), static_cast<double>(1ull << bvy));
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const int ng = props - g0 < 8 ? props - g0 : 8;
+    for (int b = 0; b < 32; ++b) {
+        const uint64_t z = static_cast<uint64_t>(w) * 32 + b;
+        if (z >= vcells) break;
+        uint64_t cx = 0, cy = 0;
+        for (int level = 0; level < vg.depth; ++level) {
+            const uint64_t bit = (z >> (vg.depth - 1 - level)) & 1u;
+            if ((level & 1) == 0) cx = (cx << 1) | bit;
+            else cy = (cy << 1) | bit;
+        }
+        const double x = __dadd_rn(vg.lo0, __dmul_rn(__dadd_rn(static_cast<double>(cx), 0.5), wxv));
+        const double y = __dadd_rn(vg.lo1, __dmul_rn(__dadd_rn(static_cast<double>(cy), 0.5), wyv));
+        const double xw = __dadd_rn(__dadd_rn(__dmul_rn(ps.c, x), -__dmul_rn(ps.s, y)), ps.dx);
+        const double yw = __dadd_rn(__dadd_rn(__dmul_rn(ps.s, x), __dmul_rn(ps.c, y)), ps.dy);
+        const int64_t qx = quantize_dev(wg.lo0, wg.hi0, bwx, xw);
+        const int64_t qy = quantize_dev(wg.lo1, wg.hi1, bwy, yw);
+        if (qx < 0 || qy < 0) {
+            if (outside)
+                for (int j = 0; j < ng; ++j) acc[j] |= 1u << b;
+            continue;
+        }
+        uint64_t zw = 0;
+        for (int level = 0; level < wg.depth; ++level) {
+            const int axis = level & 1;
+            const int bit_pos = (axis ? bwy : bwx) - 1 - level / 2;
+            zw = (zw << 1) | (((axis ? static_cast<uint64_t>(qy) : static_cast<uint64_t>(qx)) >> bit_pos) & 1u);
+        }
+        for (int j = 0; j < ng; ++j) {
+            const uint32_t word = __ldg(world32 + static_cast<uint64_t>(g0 + j) * wnw32 + (zw >> 5));
+            acc[j] |= ((word >> (zw & 31)) & 1u) << b;
+        }
+    }
+    uint32_t* dst = out32 + static_cast<uint64_t>(f) * props * vnw32 + w;
+    for (int j = 0; j < ng; ++j) dst[static_cast<uint64_t>(g0 + j) * vnw32] = acc[j];
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+
+cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
+                           void* sf, cudaStream_t st) {
+    dim3 grid((nw32 + 1 + 255) / 256, static_cast<unsigned>(frames));
+    if (props <= 32)
+        summary_kernel<uint32_t><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells,
+                                                       static_cast<SF<uint32_t>*>(sf));
+    else
+        summary_kernel<uint64_t><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells,
+                                                       static_cast<SF<uint64_t>*>(sf));
+    return cudaGetLastError();
+}
+
+size_t summary_entry_bytes(int props) { return props <= 32 ? 8 : 16; }
+
+template <typename LW, typename SW>
+static void launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
+    const unsigned blocks = (a.ntasks + 7) / 8;
+    label_stream_kernel<LW, SW><<<blocks, 256, 0, st>>>(a.pairs, a.task_pair, a.task_row, a.ntasks,
+                                                       static_cast<const SF<LW>*>(a.sf), a.P32, a.nw32,
+                                                       a.perm, static_cast<SW*>(a.out));
+}
+
+template <typename LW, typename SW, int FPL>
+static void launch_batch_t(const LaunchArgs& a, cudaStream_t st) {
+    const unsigned blocks = (a.ntasks + 7) / 8;
+    label_batch_kernel<LW, SW, FPL><<<blocks, 256, 0, st>>>(a.pairs, a.task_pair, a.task_row, a.ntasks,
+                                                           static_cast<const SF<LW>*>(a.sf), a.P32, a.nw32,
+                                                           a.props, a.frames, a.perm, static_cast<SW*>(a.out));
+}
+
+template <typename LW, typename SW>
+static void launch_batch_fpl(const LaunchArgs& a, cudaStream_t st) {
+    if (a.frames <= 32) launch_batch_t<LW, SW, 1>(a, st);
+    else if (a.frames <= 64) launch_batch_t<LW, SW, 2>(a, st);
+    else if (a.frames <= 128) launch_batch_t<LW, SW, 4>(a, st);
+    else launch_batch_t<LW, SW, 8>(a, st);
+}
+
+cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
+    if (a.ntasks == 0) return cudaSuccess;
+    if (a.frames == 1) {
+        switch (a.label_bytes) {
+            case 1: launch_stream_t<uint32_t, uint8_t>(a, st); break;
+            case 2: launch_stream_t<uint32_t, uint16_t>(a, st); break;
+            case 4: launch_stream_t<uint32_t, uint32_t>(a, st); break;
+            default: launch_stream_t<uint64_t, uint64_t>(a, st); break;
+        }
+    } else {
+        switch (a.label_bytes) {
+            case 1: launch_batch_fpl<uint32_t, uint8_t>(a, st); break;
+            case 2: launch_batch_fpl<uint32_t, uint16_t>(a, st); break;
+            case 4: launch_batch_fpl<uint32_t, uint32_t>(a, st); break;
+            default: launch_batch_fpl<uint64_t, uint64_t>(a, st); break;
+        }
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, int frames, int frame,
+                           uint64_t* out, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    const unsigned blocks = static_cast<unsigned>((rows + 255) / 256);
+    switch (label_bytes) {
+        case 1: extract_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint8_t*>(labels), rows, frames, frame, out); break;
+        case 2: extract_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint16_t*>(labels), rows, frames, frame, out); break;
+        case 4: extract_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint32_t*>(labels), rows, frames, frame, out); break;
+        default: extract_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint64_t*>(labels), rows, frames, frame, out); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_resample(int vdepth, double vlo0, double vhi0, double vlo1, double vhi1, int wdepth,
+                            double wlo0, double whi0, double wlo1, double whi1, const void* poses,
+                            int frames, int props, const uint32_t* world32, uint32_t wnw32, int outside,
+                            uint32_t vnw32, uint32_t* out32, cudaStream_t st) {
+    if (props == 0) return cudaSuccess;
+    Grid2 vg{vdepth, vlo0, vhi0, vlo1, vhi1};
+    Grid2 wg{wdepth, wlo0, whi0, wlo1, whi1};
+    dim3 grid((vnw32 + 127) / 128, static_cast<unsigned>((props + 7) / 8), static_cast<unsigned>(frames));
+    resample_kernel<<<grid, 128, 0, st>>>(vg, wg, static_cast<const Pose2*>(poses), props, world32, wnw32,
+                                          outside, vnw32, out32);
+    return cudaGetLastError();
+}
+
+}  // namespace ltlg

@@ -1,0 +1,39 @@
+// launch.h -- host launchers of the sm_100a kernels (kernels.cu), used by api.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "engine.h"
+
+namespace ltlg {
+
+struct LaunchArgs {
+    const Pair* pairs;
+    const uint64_t* task_pair;
+    const uint32_t* task_row;
+    uint32_t ntasks;
+    const void* sf;
+    const uint32_t* P32;
+    uint32_t nw32;
+    int props;
+    int frames;
+    const uint32_t* perm;
+    void* out;
+    int label_bytes;
+};
+
+cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
+                           void* sf, cudaStream_t st);
+size_t summary_entry_bytes(int props);
+cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st);
+cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, int frames, int frame,
+                           uint64_t* out, cudaStream_t st);
+cudaError_t launch_resample(int vdepth, double vlo0, double vhi0, double vlo1, double vhi1, int wdepth,
+                            double wlo0, double whi0, double wlo1, double whi1, const void* poses,
+                            int frames, int props, const uint32_t* world32, uint32_t wnw32, int outside,
+                            uint32_t vnw32, uint32_t* out32, cudaStream_t st);
+
+}  // namespace ltlg

@@ -1,0 +1,347 @@
+// loader.cpp -- host side of "load abstraction": validate T exactly like the
+// reference, bit-pack it into a word-CSR, order rows for z-locality, split it
+// into device shards and warp tasks.
+//
+// Reference behaviour reproduced here:
+//   CsrBoolMatrix::validate   proj/core/src/label.cpp:16-40   (checks, order, messages)
+//   CsrBoolMatrix::load       proj/core/src/label.cpp:271-298 (CSB1 header, messages)
+//   OccupancyBitset layout    proj/core/include/ltlgrid/grid.hpp:93-125 (cell c = word c>>5, bit c&31
+//                             of the little-endian u32 view of the u64 words)
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <thread>
+
+#include "engine.h"
+
+namespace ltlg {
+
+int host_threads() {
+    unsigned hw = std::thread::hardware_concurrency();
+    if (hw == 0) hw = 1;
+    return static_cast<int>(std::min(hw, 64u));
+}
+
+namespace {
+
+// Run fn(begin, end, chunk_id) over [0, n) in contiguous chunks.
+void parallel_chunks(uint64_t n, uint64_t min_chunk,
+                     const std::function<void(uint64_t, uint64_t, int)>& fn) {
+    int t = host_threads();
+    if (n < min_chunk * 2 || t == 1) {
+        fn(0, n, 0);
+        return;
+    }
+    uint64_t chunks = std::min<uint64_t>(static_cast<uint64_t>(t), (n + min_chunk - 1) / min_chunk);
+    uint64_t step = (n + chunks - 1) / chunks;
+    std::vector<std::thread> pool;
+    for (uint64_t c = 0; c < chunks; ++c) {
+        uint64_t b = c * step, e = std::min(n, b + step);
+        if (b >= e) break;
+        pool.emplace_back(fn, b, e, static_cast<int>(c));
+    }
+    for (auto& th : pool) th.join();
+}
+
+bool fail(Error* err, Status code, const std::string& msg) {
+    if (err) {
+        err->code = code;
+        err->msg = msg;
+    }
+    return false;
+}
+
+// Offsets checks of validate(), label.cpp:17-31, in the reference's order.
+bool check_offsets(uint64_t rows, const uint64_t* offsets, uint64_t n_offsets, uint64_t nnz,
+                   Error* err) {
+    if (n_offsets != rows + 1) return fail(err, S_EINVAL, "row_offsets must have rows+1 entries");
+    if (n_offsets && offsets[0] != 0) return fail(err, S_EINVAL, "row_offsets must start at 0");
+    std::atomic<bool> bad{false};
+    parallel_chunks(n_offsets ? n_offsets - 1 : 0, 1 << 20, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t i = b; i < e; ++i)
+            if (offsets[i] > offsets[i + 1]) {
+                bad = true;
+                return;
+            }
+    });
+    if (bad) return fail(err, S_EINVAL, "row_offsets must be nondecreasing");
+    if (n_offsets && offsets[n_offsets - 1] != nnz) return fail(err, S_EINVAL, "row_offsets must end at nnz");
+    return true;
+}
+
+}  // namespace
+
+bool validate_csr(uint64_t rows, uint64_t cols, const uint64_t* offsets, uint64_t n_offsets,
+                  const uint32_t* indices, uint64_t nnz, Error* err) {
+    if (!check_offsets(rows, offsets, n_offsets, nnz, err)) return false;
+    // Per-row index checks, label.cpp:32-39: the first failing row (in row
+    // order) decides the message; within a row, range before ascending.
+    const int T = host_threads();
+    std::vector<uint64_t> first_bad(static_cast<size_t>(T) + 1, UINT64_MAX);
+    std::vector<int> kind(static_cast<size_t>(T) + 1, 0);
+    parallel_chunks(rows, 1 << 14, [&](uint64_t b, uint64_t e, int c) {
+        for (uint64_t i = b; i < e; ++i) {
+            for (uint64_t k = offsets[i]; k < offsets[i + 1]; ++k) {
+                int why = 0;
+                if (static_cast<uint64_t>(indices[k]) >= cols) why = 1;
+                else if (k > offsets[i] && indices[k - 1] >= indices[k]) why = 2;
+                if (why) {
+                    first_bad[static_cast<size_t>(c)] = i;
+                    kind[static_cast<size_t>(c)] = why;
+                    return;
+                }
+            }
+        }
+    });
+    uint64_t best = UINT64_MAX;
+    int why = 0;
+    for (size_t c = 0; c < first_bad.size(); ++c)
+        if (first_bad[c] < best) {
+            best = first_bad[c];
+            why = kind[c];
+        }
+    if (why == 1) return fail(err, S_EINVAL, "column index out of range");
+    if (why == 2) return fail(err, S_EINVAL, "column indices must be strictly ascending per row");
+    return true;
+}
+
+bool pack_csr(uint64_t rows, uint64_t cols, const uint64_t* offsets, const uint32_t* indices,
+              WordCsr* out, Error* err) {
+    (void)err;
+    out->rows = rows;
+    out->cols = cols;
+    out->nnz = rows ? offsets[rows] : 0;
+    out->offsets.assign(rows + 1, 0);
+    // pass 1: distinct 32-bit words per row (indices are ascending)
+    parallel_chunks(rows, 1 << 14, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t i = b; i < e; ++i) {
+            uint64_t n = 0;
+            uint32_t last = UINT32_MAX;
+            for (uint64_t k = offsets[i]; k < offsets[i + 1]; ++k) {
+                const uint32_t w = indices[k] >> 5;
+                n += (w != last);
+                last = w;
+            }
+            out->offsets[i + 1] = n;
+        }
+    });
+    for (uint64_t i = 0; i < rows; ++i) out->offsets[i + 1] += out->offsets[i];
+    const uint64_t W = out->offsets[rows];
+    out->word.assign(W, 0);
+    out->mask.assign(W, 0);
+    // pass 2: fill (word, mask)
+    parallel_chunks(rows, 1 << 14, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t i = b; i < e; ++i) {
+            uint64_t o = out->offsets[i] - 1;
+            uint32_t last = UINT32_MAX;
+            for (uint64_t k = offsets[i]; k < offsets[i + 1]; ++k) {
+                const uint32_t c = indices[k];
+                const uint32_t w = c >> 5;
+                if (w != last) {
+                    ++o;
+                    out->word[o] = w;
+                    last = w;
+                }
+                out->mask[o] |= 1u << (c & 31);
+            }
+        }
+    });
+    return true;
+}
+
+bool take_words(uint64_t rows, uint64_t cols, const uint64_t* offsets, const uint32_t* word,
+                const uint32_t* mask, WordCsr* out, Error* err) {
+    const uint64_t W = rows ? offsets[rows] : 0;
+    if (!check_offsets(rows, offsets, rows + 1, W, err)) return false;
+    const uint64_t nwords = (cols + 31) / 32;
+    const uint32_t tail_bits = static_cast<uint32_t>(cols & 31);
+    const uint32_t tail_mask = tail_bits ? ((1u << tail_bits) - 1u) : 0xffffffffu;
+    const int T = host_threads();
+    std::vector<uint64_t> first_bad(static_cast<size_t>(T) + 1, UINT64_MAX);
+    std::vector<int> kind(static_cast<size_t>(T) + 1, 0);
+    std::vector<uint64_t> pop(static_cast<size_t>(T) + 1, 0);
+    parallel_chunks(rows, 1 << 14, [&](uint64_t b, uint64_t e, int c) {
+        uint64_t nnz = 0;
+        for (uint64_t i = b; i < e; ++i) {
+            for (uint64_t k = offsets[i]; k < offsets[i + 1]; ++k) {
+                int why = 0;
+                if (word[k] >= nwords || (word[k] == nwords - 1 && (mask[k] & ~tail_mask)))
+                    why = 1;
+                else if (mask[k] == 0)
+                    why = 3;
+                else if (k > offsets[i] && word[k - 1] >= word[k])
+                    why = 2;
+                if (why) {
+                    first_bad[static_cast<size_t>(c)] = i;
+                    kind[static_cast<size_t>(c)] = why;
+                    return;
+                }
+                nnz += static_cast<uint64_t>(__builtin_popcount(mask[k]));
+            }
+        }
+        pop[static_cast<size_t>(c)] = nnz;
+    });
+    uint64_t best = UINT64_MAX;
+    int why = 0;
+    for (size_t c = 0; c < first_bad.size(); ++c)
+        if (first_bad[c] < best) {
+            best = first_bad[c];
+            why = kind[c];
+        }
+    if (why == 1) return fail(err, S_EINVAL, "column index out of range");
+    if (why == 2) return fail(err, S_EINVAL, "column indices must be strictly ascending per row");
+    if (why == 3) return fail(err, S_EINVAL, "word masks must be non-zero");
+    out->rows = rows;
+    out->cols = cols;
+    out->nnz = 0;
+    for (uint64_t p : pop) out->nnz += p;
+    out->offsets.assign(offsets, offsets + rows + 1);
+    out->word.assign(word, word + W);
+    out->mask.assign(mask, mask + W);
+    return true;
+}
+
+// CsrBoolMatrix::load, label.cpp:271-298.
+bool read_csb1(const char* path, uint64_t* rows, uint64_t* cols, std::vector<uint64_t>* offsets,
+               std::vector<uint32_t>* indices, Error* err) {
+    const std::string p(path);
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return fail(err, S_EIO, "cannot open: " + p);
+    auto rd = [&](void* dst, size_t n) { return std::fread(dst, 1, n, f) == n; };
+    char magic[4];
+    if (!rd(magic, 4) || std::memcmp(magic, "CSB1", 4) != 0) {
+        std::fclose(f);
+        return fail(err, S_EFORMAT, "not a CSR file: " + p);
+    }
+    uint32_t flags = 0;
+    uint64_t nnz = 0;
+    bool ok = rd(&flags, 4) && rd(rows, 8) && rd(cols, 8) && rd(&nnz, 8);
+    const bool wide = flags & 1u;
+    if (ok && *cols > 0xffffffffull) {
+        std::fclose(f);
+        return fail(err, S_EFORMAT, "CSR column space too large for this build");
+    }
+    if (ok) {
+        try {
+            offsets->assign(*rows + 1, 0);
+            indices->assign(nnz, 0);
+        } catch (...) {
+            std::fclose(f);
+            return fail(err, S_ENOMEM, "cannot allocate CSR of the declared size: " + p);
+        }
+        if (wide) {
+            ok = rd(offsets->data(), (*rows + 1) * 8);
+            std::vector<uint64_t> tmp(1 << 20);
+            for (uint64_t done = 0; ok && done < nnz;) {
+                const uint64_t n = std::min<uint64_t>(tmp.size(), nnz - done);
+                ok = rd(tmp.data(), n * 8);
+                for (uint64_t i = 0; ok && i < n; ++i) (*indices)[done + i] = static_cast<uint32_t>(tmp[i]);
+                done += n;
+            }
+        } else {
+            std::vector<uint32_t> o32(*rows + 1);
+            ok = rd(o32.data(), (*rows + 1) * 4) && rd(indices->data(), nnz * 4);
+            for (uint64_t i = 0; i <= *rows; ++i) (*offsets)[i] = o32[i];
+        }
+    }
+    std::fclose(f);
+    if (!ok) return fail(err, S_EFORMAT, "truncated CSR file: " + p);
+    return validate_csr(*rows, *cols, offsets->data(), offsets->size(), indices->data(), nnz, err);
+}
+
+std::vector<uint64_t> shard_bounds(const WordCsr& t, int n) {
+    std::vector<uint64_t> b(static_cast<size_t>(n) + 1, t.rows);
+    b[0] = 0;
+    if (n == 1 || t.rows == 0) return b;
+    // pairs of row i = max(1, words) (empty rows carry one sentinel pair)
+    const uint64_t total = t.offsets[t.rows] + t.rows;  // upper bound proxy: words + rows
+    uint64_t acc = 0;
+    int s = 1;
+    for (uint64_t i = 0; i < t.rows && s < n; ++i) {
+        acc += (t.offsets[i + 1] - t.offsets[i]) + 1;
+        while (s < n && acc * static_cast<uint64_t>(n) >= total * static_cast<uint64_t>(s)) {
+            b[static_cast<size_t>(s)] = i + 1;
+            ++s;
+        }
+    }
+    return b;
+}
+
+namespace {
+
+void make_tasks(const std::vector<uint64_t>& pair_off, uint64_t rows, int target,
+                std::vector<uint32_t>* trow, std::vector<uint64_t>* tpair) {
+    trow->clear();
+    tpair->clear();
+    const uint64_t T = static_cast<uint64_t>(std::max(target, 1));
+    uint64_t start = 0;
+    while (start < rows) {
+        trow->push_back(static_cast<uint32_t>(start));
+        tpair->push_back(pair_off[start]);
+        // first row whose end passes start_pairs + T (at least one row)
+        const uint64_t goal = pair_off[start] + T;
+        auto it = std::lower_bound(pair_off.begin() + static_cast<std::ptrdiff_t>(start) + 1,
+                                   pair_off.begin() + static_cast<std::ptrdiff_t>(rows) + 1, goal);
+        uint64_t end = static_cast<uint64_t>(it - pair_off.begin());
+        if (end > rows) end = rows;
+        if (end <= start) end = start + 1;
+        start = end;
+    }
+    trow->push_back(static_cast<uint32_t>(rows));
+    tpair->push_back(pair_off[rows]);
+}
+
+}  // namespace
+
+void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
+                 uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs,
+                 PackedShard* out) {
+    const uint64_t R = row_end - row_begin;
+    out->row_begin = row_begin;
+    out->row_end = row_end;
+    out->words = t.offsets[row_end] - t.offsets[row_begin];
+    out->perm.resize(R);
+    if (sort_rows) {
+        // z-locality key: the row's median 32-bit word (rows are ascending in
+        // z-order, so this is a point inside the swept volume's z-range).
+        std::vector<uint64_t> key(R);
+        parallel_chunks(R, 1 << 16, [&](uint64_t b, uint64_t e, int) {
+            for (uint64_t r = b; r < e; ++r) {
+                const uint64_t o0 = t.offsets[row_begin + r], o1 = t.offsets[row_begin + r + 1];
+                const uint64_t k = o1 > o0 ? t.word[o0 + (o1 - o0 - 1) / 2] : 0;
+                key[r] = (k << 32) | r;
+            }
+        });
+        std::sort(key.begin(), key.end());
+        for (uint64_t s = 0; s < R; ++s) out->perm[s] = static_cast<uint32_t>(key[s] & 0xffffffffu);
+    } else {
+        for (uint64_t s = 0; s < R; ++s) out->perm[s] = static_cast<uint32_t>(s);
+    }
+    std::vector<uint64_t> pair_off(R + 1, 0);
+    for (uint64_t s = 0; s < R; ++s) {
+        const uint64_t r = row_begin + out->perm[s];
+        const uint64_t n = t.offsets[r + 1] - t.offsets[r];
+        pair_off[s + 1] = pair_off[s] + (n ? n : 1);
+    }
+    out->n_pairs = pair_off[R];
+    out->pairs.assign(out->n_pairs + kPairPad, Pair{0, sentinel_word});
+    parallel_chunks(R, 1 << 14, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t s = b; s < e; ++s) {
+            const uint64_t r = row_begin + out->perm[s];
+            const uint64_t o0 = t.offsets[r], o1 = t.offsets[r + 1];
+            Pair* dst = out->pairs.data() + pair_off[s];
+            if (o1 == o0) {
+                dst[0] = Pair{0, sentinel_word | kHead};  // empty row: a no-op pair on the zero sentinel word
+                continue;
+            }
+            for (uint64_t k = o0; k < o1; ++k) dst[k - o0] = Pair{t.mask[k], t.word[k]};
+            dst[0].word |= kHead;
+        }
+    });
+    make_tasks(pair_off, R, stream_task_pairs, &out->task_row_stream, &out->task_pair_stream);
+    make_tasks(pair_off, R, batch_task_pairs, &out->task_row_batch, &out->task_pair_batch);
+}
+
+}  // namespace ltlg

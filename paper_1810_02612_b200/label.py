@@ -1,0 +1,456 @@
+"""Host-side mirror of the reference labeling interface, backed by the B200 engine.
+
+Names, argument meaning and error behaviour follow
+proj/core/include/ltlgrid/label.hpp (+ grid.hpp for OccupancyBitset):
+
+  reference (C++)                          here (Python)
+  ---------------------------------------  --------------------------------------
+  CsrBoolMatrix         label.hpp:18-35    CsrBoolMatrix (numpy arrays)
+  to_csr                label.hpp:38       to_csr
+  OccupancyBitset       grid.hpp:93-125    OccupancyBitset
+  DensePropMatrix       label.hpp:47-58    DensePropMatrix
+  LabelMatrix           label.hpp:61-92    LabelMatrix (== compares like the reference)
+  label_all             label.hpp:94-98    label_all  -> libltlgrid_gpu.so (sm_100a)
+  std::invalid_argument                    ValueError
+  std::runtime_error                       RuntimeError
+
+The compute path is the C ABI of include/ltlgrid_gpu.h; there is no CPU
+fallback (a missing library or device raises).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+
+# ---------------------------------------------------------------------------
+# Errors
+# ---------------------------------------------------------------------------
+
+class LtlgError(RuntimeError):
+    """CUDA / NCCL / state errors of the engine."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+def _raise(status: int, msg: str):
+    if status == N.LTLG_EINVAL:
+        raise ValueError(msg)
+    if status in (N.LTLG_EFORMAT, N.LTLG_EIO):
+        raise RuntimeError(msg)
+    if status == N.LTLG_ENOMEM:
+        raise MemoryError(msg)
+    raise LtlgError(status, msg)
+
+
+def _ptr(a) -> Optional[int]:
+    """Raw address of a numpy array / torch tensor / int (None for empty)."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr() or None
+    return a.ctypes.data if a.size else None
+
+
+# ---------------------------------------------------------------------------
+# OccupancyBitset / CsrBoolMatrix / DensePropMatrix / LabelMatrix
+# ---------------------------------------------------------------------------
+
+class OccupancyBitset:
+    """Fixed-length bit vector over 2^depth cells (grid.hpp:93-125): u64
+    little-endian words, bit i = cell i."""
+
+    def __init__(self, size_bits: int):
+        self.size_bits = int(size_bits)
+        self.words = np.zeros((self.size_bits + 63) // 64, dtype=np.uint64)
+
+    @classmethod
+    def from_words(cls, size_bits: int, words) -> "OccupancyBitset":
+        w = np.array(words, dtype=np.uint64).reshape(-1)
+        if w.size != (size_bits + 63) // 64:
+            raise ValueError("word count does not match bit length")
+        b = cls.__new__(cls)
+        b.size_bits = int(size_bits)
+        if size_bits & 63:
+            w[-1] &= np.uint64((1 << (size_bits & 63)) - 1)
+        b.words = w
+        return b
+
+    def test(self, i: int) -> bool:
+        return bool((int(self.words[i >> 6]) >> (i & 63)) & 1)
+
+    def set(self, i: int) -> None:
+        self.words[i >> 6] |= np.uint64(1 << (i & 63))
+
+    def count(self) -> int:
+        return int(np.unpackbits(self.words.view(np.uint8)).sum())
+
+    def collect(self) -> np.ndarray:
+        bits = np.unpackbits(self.words.view(np.uint8), bitorder="little")[: self.size_bits]
+        return np.nonzero(bits)[0].astype(np.uint64)
+
+    def __eq__(self, o) -> bool:
+        return isinstance(o, OccupancyBitset) and self.size_bits == o.size_bits and np.array_equal(self.words, o.words)
+
+
+class CsrBoolMatrix:
+    """T: row i's set columns are col_indices[row_offsets[i]:row_offsets[i+1]],
+    strictly ascending (label.hpp:18-35)."""
+
+    def __init__(self, rows: int = 0, cols: int = 0, row_offsets=None, col_indices=None):
+        self.rows = int(rows)
+        self.cols = int(cols)
+        self.row_offsets = np.ascontiguousarray(row_offsets if row_offsets is not None else [0], dtype=np.uint64)
+        self.col_indices = np.ascontiguousarray(col_indices if col_indices is not None else [], dtype=np.uint32)
+
+    def nnz(self) -> int:
+        return int(self.col_indices.size)
+
+    def row(self, i: int) -> np.ndarray:
+        return self.col_indices[int(self.row_offsets[i]):int(self.row_offsets[i + 1])]
+
+    def validate(self) -> None:
+        """CsrBoolMatrix::validate (label.cpp:16-40): same checks, order, messages."""
+        o, ix = self.row_offsets, self.col_indices
+        if o.size != self.rows + 1:
+            raise ValueError("row_offsets must have rows+1 entries")
+        if o.size and o[0] != 0:
+            raise ValueError("row_offsets must start at 0")
+        if o.size > 1 and np.any(o[:-1] > o[1:]):
+            raise ValueError("row_offsets must be nondecreasing")
+        if o.size and int(o[-1]) != ix.size:
+            raise ValueError("row_offsets must end at nnz")
+        if ix.size == 0:
+            return
+        row_of = np.repeat(np.arange(self.rows), np.diff(o).astype(np.int64))
+        bad_range = ix.astype(np.uint64) >= np.uint64(self.cols)
+        same_row = np.zeros(ix.size, dtype=bool)
+        same_row[1:] = row_of[1:] == row_of[:-1]
+        bad_order = np.zeros(ix.size, dtype=bool)
+        bad_order[1:] = same_row[1:] & (ix[:-1] >= ix[1:])
+        bad = bad_range | bad_order
+        if bad.any():
+            k = int(np.argmax(bad))
+            raise ValueError("column index out of range" if bad_range[k] else
+                             "column indices must be strictly ascending per row")
+
+    # CSB1, label.cpp:251-298
+    def save(self, path: str) -> None:
+        wide = self.cols > 0xFFFFFFFF or self.nnz() > 0xFFFFFFFF
+        try:
+            f = open(path, "wb")
+        except OSError:
+            raise RuntimeError("cannot open for writing: " + str(path))
+        with f:
+            f.write(b"CSB1")
+            f.write(np.array([1 if wide else 0], "<u4").tobytes())
+            f.write(np.array([self.rows, self.cols, self.nnz()], "<u8").tobytes())
+            f.write(self.row_offsets.astype("<u8" if wide else "<u4").tobytes())
+            f.write(self.col_indices.astype("<u8" if wide else "<u4").tobytes())
+
+    @staticmethod
+    def load(path: str) -> "CsrBoolMatrix":
+        try:
+            data = open(path, "rb").read()
+        except OSError:
+            raise RuntimeError("cannot open: " + str(path))
+        if data[:4] != b"CSB1":
+            raise RuntimeError("not a CSR file: " + str(path))
+        if len(data) < 32:
+            raise RuntimeError("truncated CSR file: " + str(path))
+        flags = int(np.frombuffer(data, "<u4", 1, 4)[0])
+        rows, cols, nnz = (int(x) for x in np.frombuffer(data, "<u8", 3, 8))
+        if cols > 0xFFFFFFFF:
+            raise RuntimeError("CSR column space too large for this build")
+        wide = flags & 1
+        dt, sz = ("<u8", 8) if wide else ("<u4", 4)
+        need = 32 + (rows + 1) * sz + nnz * sz
+        if len(data) < need:
+            raise RuntimeError("truncated CSR file: " + str(path))
+        off = np.frombuffer(data, dt, rows + 1, 32).astype(np.uint64)
+        idx = np.frombuffer(data, dt, nnz, 32 + (rows + 1) * sz).astype(np.uint32)
+        m = CsrBoolMatrix(rows, cols, off, idx)
+        m.validate()
+        return m
+
+
+def to_csr(rows: Sequence[OccupancyBitset]) -> CsrBoolMatrix:
+    """to_csr, label.cpp:42-57."""
+    cols = rows[0].size_bits if len(rows) else 0
+    off = [0]
+    idx = []
+    for r in rows:
+        if r.size_bits != cols:
+            raise ValueError("row length mismatch")
+        c = r.collect()
+        idx.append(c.astype(np.uint32))
+        off.append(off[-1] + c.size)
+    return CsrBoolMatrix(len(rows), cols, np.array(off, np.uint64),
+                         np.concatenate(idx) if idx else np.zeros(0, np.uint32))
+
+
+class DensePropMatrix:
+    """P, column-major: one bitset per proposition (label.hpp:47-58)."""
+
+    def __init__(self, cells: int, columns: Iterable[OccupancyBitset]):
+        cols = list(columns)
+        if len(cols) > 64:
+            raise ValueError("at most 64 propositions")
+        for c in cols:
+            if c.size_bits != cells:
+                raise ValueError("column length mismatch")
+        self._cells = int(cells)
+        self._columns = cols
+
+    @classmethod
+    def from_words(cls, cells: int, words: np.ndarray) -> "DensePropMatrix":
+        w = np.asarray(words, dtype=np.uint64).reshape(-1, (int(cells) + 63) // 64)
+        return cls(cells, [OccupancyBitset.from_words(cells, r) for r in w])
+
+    def cells(self) -> int:
+        return self._cells
+
+    def num_props(self) -> int:
+        return len(self._columns)
+
+    def column(self, j: int) -> OccupancyBitset:
+        return self._columns[j]
+
+    def column_words(self) -> np.ndarray:
+        nw = (self._cells + 63) // 64
+        if not self._columns:
+            return np.zeros((0, nw), np.uint64)
+        return np.ascontiguousarray(np.stack([c.words for c in self._columns]))
+
+
+class LabelMatrix:
+    """Edge-by-proposition bits, ceil(props/64) u64 words per row (label.hpp:61-92)."""
+
+    def __init__(self, rows: int = 0, props: int = 0, words=None):
+        if props < 0 or props > 64:
+            raise ValueError("props must be in [0, 64]")
+        self._rows = int(rows)
+        self._props = int(props)
+        self._wpr = (props + 63) // 64
+        n = self._rows * self._wpr
+        self.bits = (np.zeros(n, np.uint64) if words is None
+                     else np.ascontiguousarray(words, dtype=np.uint64).reshape(-1)[:n].copy())
+
+    def rows(self) -> int:
+        return self._rows
+
+    def props(self) -> int:
+        return self._props
+
+    def get(self, i: int, j: int) -> bool:
+        bit = i * self._wpr * 64 + j
+        return bool((int(self.bits[bit >> 6]) >> (bit & 63)) & 1)
+
+    def set(self, i: int, j: int) -> None:
+        bit = i * self._wpr * 64 + j
+        self.bits[bit >> 6] |= np.uint64(1 << (bit & 63))
+
+    def __eq__(self, o) -> bool:  # operator== (label.hpp:79): rows, props, words_per_row, bits
+        return (isinstance(o, LabelMatrix) and self._rows == o._rows and self._props == o._props
+                and self._wpr == o._wpr and np.array_equal(self.bits, o.bits))
+
+    # LBM1, label.cpp:300-326
+    def save(self, path: str) -> None:
+        try:
+            f = open(path, "wb")
+        except OSError:
+            raise RuntimeError("cannot open for writing: " + str(path))
+        with f:
+            f.write(b"LBM1")
+            f.write(np.array([1], "<u4").tobytes())
+            f.write(np.array([self._rows], "<u8").tobytes())
+            f.write(np.array([self._props], "<u4").tobytes())
+            f.write(self.bits.astype("<u8").tobytes())
+
+    @staticmethod
+    def load(path: str) -> "LabelMatrix":
+        try:
+            data = open(path, "rb").read()
+        except OSError:
+            raise RuntimeError("cannot open: " + str(path))
+        if data[:4] != b"LBM1":
+            raise RuntimeError("not a label matrix file: " + str(path))
+        if len(data) < 8 or int(np.frombuffer(data, "<u4", 1, 4)[0]) != 1:
+            raise RuntimeError("unsupported label matrix version")
+        if len(data) < 20:
+            raise RuntimeError("truncated label matrix file: " + str(path))
+        rows = int(np.frombuffer(data, "<u8", 1, 8)[0])
+        props = int(np.frombuffer(data, "<u4", 1, 16)[0])
+        l = LabelMatrix(rows, props)
+        n = l.bits.size
+        if len(data) < 20 + 8 * n:
+            raise RuntimeError("truncated label matrix file: " + str(path))
+        l.bits[:] = np.frombuffer(data, "<u8", n, 20)
+        return l
+
+    def to_csv(self, names: Sequence[str]) -> str:
+        """LabelMatrix::to_csv (label.cpp:328-344) given the alphabet's prop names."""
+        if len(names) != self._props:
+            raise ValueError("alphabet size mismatch")
+        out = ["edge,propositions\n"]
+        for i in range(self._rows):
+            out.append(f"{i}," + " ".join(names[j] for j in range(self._props) if self.get(i, j)) + "\n")
+        return "".join(out)
+
+
+# ---------------------------------------------------------------------------
+# The engine (load abstraction -> submit grid -> get labels)
+# ---------------------------------------------------------------------------
+
+class LabelEngine:
+    """One ltlg_ctx: T resident in HBM (sharded over `devices`), per-frame P
+    submissions, labels resident per shard (include/ltlgrid_gpu.h)."""
+
+    def __init__(self, devices: Optional[Sequence[int]] = None, sort_rows: bool = True,
+                 stream_task_pairs: int = 0, batch_task_pairs: int = 0, profile: bool = False):
+        self._L = N.lib()
+        opts = N.Options()
+        opts.sort_rows = 1 if sort_rows else 0
+        opts.stream_task_pairs = stream_task_pairs
+        opts.batch_task_pairs = batch_task_pairs
+        opts.profile = 1 if profile else 0
+        h = C.c_void_p()
+        if devices is None:
+            st = self._L.ltlg_create_ex(None, 1, C.byref(opts), C.byref(h))
+        else:
+            arr = (C.c_int * len(devices))(*devices)
+            st = self._L.ltlg_create_ex(arr, len(devices), C.byref(opts), C.byref(h))
+        if st:
+            _raise(st, self._L.ltlg_last_error(None).decode())
+        self._h = h
+        self.n_devices = 1 if devices is None else len(devices)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.ltlg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _ck(self, st: int):
+        if st:
+            _raise(st, self._L.ltlg_last_error(self._h).decode())
+
+    # -- load abstraction ---------------------------------------------------
+    def load_abstraction(self, m: CsrBoolMatrix) -> None:
+        off = np.ascontiguousarray(m.row_offsets, dtype=np.uint64)
+        idx = np.ascontiguousarray(m.col_indices, dtype=np.uint32)
+        self._ck(self._L.ltlg_load_abstraction(self._h, m.rows, m.cols, _ptr(off), _ptr(idx)))
+
+    def load_abstraction_file(self, path: str) -> None:
+        self._ck(self._L.ltlg_load_abstraction_file(self._h, os.fsencode(path)))
+
+    def load_abstraction_words(self, rows: int, cols: int, offsets, words, masks) -> None:
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        w = np.ascontiguousarray(words, dtype=np.uint32)
+        mk = np.ascontiguousarray(masks, dtype=np.uint32)
+        self._ck(self._L.ltlg_load_abstraction_words(self._h, rows, cols, _ptr(off), _ptr(w), _ptr(mk)))
+
+    # -- submit grid --------------------------------------------------------
+    def submit_grid(self, cells: int, num_props: int, column_words, frames: int = 1) -> None:
+        """column_words: numpy (host) or a pinned torch tensor; frames x props x ceil(cells/64) u64."""
+        if isinstance(column_words, np.ndarray):
+            column_words = np.ascontiguousarray(column_words, dtype=np.uint64)
+        self._ck(self._L.ltlg_submit_grid(self._h, cells, num_props, _ptr(column_words), frames))
+
+    def submit_props(self, p: DensePropMatrix) -> None:
+        self.submit_grid(p.cells(), p.num_props(), p.column_words(), 1)
+
+    def submit_grid_device(self, cells: int, num_props: int, device_words, frames: int = 1) -> None:
+        self._ck(self._L.ltlg_submit_grid_device(self._h, cells, num_props, _ptr(device_words), frames))
+
+    def submit_world_grid(self, vehicle, world, num_props: int, world_words, poses, outside: int = 0,
+                          words_on_device: bool = False) -> None:
+        """vehicle/world = (depth, lo0, hi0, lo1, hi1); poses = [(dx, dy, cos, sin), ...]."""
+        vg, wg = N.Grid2(*vehicle), N.Grid2(*world)
+        arr = (N.Pose2 * len(poses))(*[N.Pose2(*p) for p in poses])
+        if isinstance(world_words, np.ndarray):
+            world_words = np.ascontiguousarray(world_words, dtype=np.uint64)
+        self._ck(self._L.ltlg_submit_world_grid(self._h, C.byref(vg), C.byref(wg), num_props, _ptr(world_words),
+                                                1 if words_on_device else 0, C.cast(arr, C.c_void_p), len(poses),
+                                                int(outside)))
+
+    def wait(self) -> None:
+        self._ck(self._L.ltlg_wait(self._h))
+
+    # -- get labels ---------------------------------------------------------
+    def info(self) -> N.Info:
+        i = N.Info()
+        self._ck(self._L.ltlg_get_info(self._h, C.byref(i)))
+        return i
+
+    def get_labels(self, frame: int = 0) -> LabelMatrix:
+        i = self.info()
+        l = LabelMatrix(i.rows, i.props)
+        buf = l.bits if l.bits.size else None
+        self._ck(self._L.ltlg_get_labels(self._h, frame, _ptr(buf)))
+        return l
+
+    def get_labels_packed(self, out=None):
+        """All frames, edge-major [rows, frames] of the packed label word
+        (uint8/16/32/64 by prop count).  `out` may be a pinned torch tensor."""
+        i = self.info()
+        dt = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[i.label_bytes or 8]
+        if out is None:
+            out = np.zeros((i.rows, i.frames), dtype=dt)
+        nbytes = out.nbytes if isinstance(out, np.ndarray) else out.numel() * out.element_size()
+        self._ck(self._L.ltlg_get_labels_packed(self._h, _ptr(out), nbytes))
+        return out
+
+    def device_labels(self, shard: int = 0):
+        p, b, e, d = C.c_void_p(), C.c_uint64(), C.c_uint64(), C.c_int()
+        self._ck(self._L.ltlg_device_labels(self._h, shard, C.byref(p), C.byref(b), C.byref(e), C.byref(d)))
+        return p.value, b.value, e.value, d.value
+
+    def stream(self, shard: int = 0) -> int:
+        s = C.c_void_p()
+        self._ck(self._L.ltlg_stream(self._h, shard, C.byref(s)))
+        return s.value or 0
+
+    def stage_times(self, shard: int = 0, back: int = 0):
+        """(upload_ms, summary_ms, label_ms) of the submit `back` submits ago."""
+        a, b, c = C.c_float(), C.c_float(), C.c_float()
+        self._ck(self._L.ltlg_stage_times(self._h, shard, back, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+
+def label_all(m: CsrBoolMatrix, p: DensePropMatrix, workers: int = 0) -> LabelMatrix:
+    """Drop-in for ltlgrid::label_all (label.cpp:150-189): L(i,j) = OR_k M(i,k) AND P(k,j),
+    computed on the B200 through ltlg_label_all.  `workers` is accepted for
+    signature parity; the result is identical for any value."""
+    L = N.lib()
+    if p.num_props() > 64:
+        raise ValueError("at most 64 propositions")
+    out = LabelMatrix(m.rows, p.num_props())
+    off = np.ascontiguousarray(m.row_offsets, dtype=np.uint64)
+    idx = np.ascontiguousarray(m.col_indices, dtype=np.uint32)
+    cw = p.column_words()
+    st = L.ltlg_label_all(m.rows, m.cols, _ptr(off), _ptr(idx), p.cells(), p.num_props(), _ptr(cw),
+                          int(workers), _ptr(out.bits) if out.bits.size else None)
+    if st:
+        _raise(st, L.ltlg_last_error(None).decode())
+    return out

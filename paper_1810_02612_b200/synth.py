@@ -1,0 +1,85 @@
+"""Synthetic workloads (libltlgrid_synth.so): the BASELINE configs' T and P.
+
+See csrc/synth.cpp for the generator definitions.
+Row i of the synthetic PRM depends only on (seed, i), so any row range can be
+regenerated bit-identically -- the CPU oracle / reference time a bounded row
+sample of exactly the rows the GPU labels.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+# BASELINE.json configs: k = 2 grids over 102.4 m x 102.4 m.
+CONFIGS = {
+    1: dict(name="cpu-oracle", edges=10_000, depth=12, props=4, frames=1),
+    2: dict(name="driving-prm", edges=200_000, depth=16, props=8, frames=1),
+    3: dict(name="large-abstraction", edges=2_000_000, depth=18, props=16, frames=1),
+    4: dict(name="batched-frames", edges=2_000_000, depth=18, props=32, frames=64),
+    5: dict(name="dense-grid-stress", edges=8_000_000, depth=20, props=64, frames=1),
+}
+EXTENT = 102.4
+NPRIM = 2048
+
+
+@dataclass
+class WordT:
+    rows: int
+    cols: int
+    offsets: np.ndarray  # u64 [rows+1]
+    words: np.ndarray    # u32 [W]
+    masks: np.ndarray    # u32 [W]
+
+
+class SyntheticPRM:
+    """Handle on the primitive library of one (seed, depth)."""
+
+    def __init__(self, seed: int = 1, depth: int = 18, extent: float = EXTENT, nprim: int = NPRIM):
+        self._S = N.synth()
+        self.depth = depth
+        self.cells = 1 << depth
+        self._h = self._S.synth_prm_create(seed, depth, extent, nprim)
+        if not self._h:
+            raise ValueError("unsupported synthetic grid depth (need 10..30)")
+
+    def __del__(self):
+        try:
+            self._S.synth_prm_free(self._h)
+        except Exception:
+            pass
+
+    def words(self, row_begin: int, row_end: int) -> WordT:
+        n = row_end - row_begin
+        cnt = np.zeros(n, np.uint64)
+        self._S.synth_prm_row_words(self._h, row_begin, row_end, cnt.ctypes.data)
+        off = np.zeros(n + 1, np.uint64)
+        np.cumsum(cnt, out=off[1:])
+        W = int(off[-1])
+        w = np.zeros(max(W, 1), np.uint32)
+        m = np.zeros(max(W, 1), np.uint32)
+        self._S.synth_prm_fill_words(self._h, row_begin, row_end, off.ctypes.data, w.ctypes.data, m.ctypes.data)
+        return WordT(n, self.cells, off, w[:W], m[:W])
+
+    def csr(self, row_begin: int, row_end: int):
+        """Reference CsrBoolMatrix arrays (offsets u64, indices u32) of the rows."""
+        n = row_end - row_begin
+        cnt = np.zeros(n, np.uint64)
+        self._S.synth_prm_row_cells(self._h, row_begin, row_end, cnt.ctypes.data)
+        off = np.zeros(n + 1, np.uint64)
+        np.cumsum(cnt, out=off[1:])
+        idx = np.zeros(max(int(off[-1]), 1), np.uint32)
+        self._S.synth_prm_fill_cells(self._h, row_begin, row_end, off.ctypes.data, idx.ctypes.data)
+        return off, idx[: int(off[-1])]
+
+
+def props_words(seed: int, depth: int, props: int, frame0: int = 0, frames: int = 1, out=None) -> np.ndarray:
+    """frames x props x ceil(2^depth/64) u64 (DensePropMatrix columns per frame)."""
+    nw = ((1 << depth) + 63) // 64
+    if out is None:
+        out = np.zeros((frames, props, nw), np.uint64)
+    ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+    N.synth().synth_props(seed, depth, props, frame0, frames, ptr)
+    return out

@@ -1,0 +1,308 @@
+"""GPU parity: the sm_100a labeling path through the C ABI vs the CPU oracle.
+
+Bit-exact (LabelMatrix::operator==, label.hpp:79) on
+  * every golden fixture produced by the unmodified reference (tests/golden),
+  * >= 100 seeded random scenes (SPEC.md:616 acceptance), single and batched,
+  * the synthetic BASELINE configs 1-3 in full and config 4 on sampled frames,
+  * the world->vehicle resample (vs oracle_resample),
+and the reference's error behaviour (messages of label.cpp:124-154, 16-40, 271-298).
+"""
+import glob
+import math
+import os
+import zlib
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, has_gpu
+from oracle.oracle import (Oracle, SplitMix64, bits_to_words, dense_label, labels_dense, random_rows, to_csr,
+                           words_to_bits)
+
+pytestmark = pytest.mark.gpu
+
+if not has_gpu():  # pragma: no cover - collected on CPU-only hosts
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1810_02612_b200 import (CsrBoolMatrix, DensePropMatrix, LabelEngine, LabelMatrix,  # noqa: E402
+                                   LtlgError, label_all)
+from paper_1810_02612_b200.synth import CONFIGS, SyntheticPRM, props_words  # noqa: E402
+
+ORACLE = Oracle()
+LABEL_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                     if "labels" in np.load(p).files)
+ENGINE_VARIANTS = [
+    dict(),
+    dict(sort_rows=False),
+    dict(stream_task_pairs=1, batch_task_pairs=1),
+    dict(stream_task_pairs=37, batch_task_pairs=5, sort_rows=False),
+]
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+
+
+@pytest.fixture(scope="module", params=range(len(ENGINE_VARIANTS)))
+def engine(request):
+    e = LabelEngine(devices=[0], **ENGINE_VARIANTS[request.param])
+    yield e
+    e.close()
+
+
+@pytest.mark.parametrize("case", LABEL_CASES)
+def test_golden_single_frame(engine, case):
+    g = load(case)
+    rows, cols, props = int(g["rows"]), int(g["cols"]), int(g["props"])
+    engine.load_abstraction(CsrBoolMatrix(rows, cols, g["offsets"], g["indices"]))
+    engine.submit_grid(cols, props, g["colwords"], 1)
+    got = engine.get_labels(0)
+    assert got == LabelMatrix(rows, props, g["labels"])
+
+
+@pytest.mark.parametrize("case", LABEL_CASES)
+def test_golden_batched_frames(engine, case):
+    g = load(case)
+    rows, cols, props = int(g["rows"]), int(g["cols"]), int(g["props"])
+    nw = (cols + 63) // 64
+    rng = SplitMix64(zlib.crc32(case.encode()))
+    frames = 3
+    P = np.zeros((frames, props, nw), np.uint64)
+    P[0] = g["colwords"].reshape(props, nw)
+    for f in range(1, frames):
+        if props:
+            P[f] = bits_to_words(random_rows(rng, props, cols, 0.05 * f))
+    engine.load_abstraction(CsrBoolMatrix(rows, cols, g["offsets"], g["indices"]))
+    engine.submit_grid(cols, props, P, frames)
+    assert engine.get_labels(0) == LabelMatrix(rows, props, g["labels"])
+    for f in range(1, frames):
+        want = ORACLE.label_all(rows, cols, g["offsets"], g["indices"], cols, props, P[f])
+        assert engine.get_labels(f) == LabelMatrix(rows, props, want)
+
+
+@pytest.mark.parametrize("case", ["eq13_col4", "rand_seed11", "scene_04", "scene_08"])
+@pytest.mark.parametrize("workers", [0, 1, 2, 5])
+def test_label_all_drop_in(case, workers):
+    g = load(case)
+    rows, cols, props = int(g["rows"]), int(g["cols"]), int(g["props"])
+    m = CsrBoolMatrix(rows, cols, g["offsets"], g["indices"])
+    p = DensePropMatrix.from_words(cols, g["colwords"].reshape(props, -1))
+    assert label_all(m, p, workers) == LabelMatrix(rows, props, g["labels"])
+
+
+def _scene(seed):
+    rng = SplitMix64(seed)
+    r = int(rng.below(600))
+    c = int(1 + rng.below(5000))
+    props = int(rng.below(65))
+    frames = [1, 1, 2, 3, 5, 31, 33, 64, 65][int(rng.below(9))]
+    dr = [0.0, 0.001, 0.01, 0.05, 0.3][int(rng.below(5))]
+    rows = random_rows(rng, r, c, dr) if r else np.zeros((0, c), bool)
+    P = np.zeros((frames, props, (c + 63) // 64), np.uint64)
+    for f in range(frames):
+        for j in range(props):
+            kind = int(rng.below(4))
+            if kind == 0:
+                col = random_rows(rng, 1, c, [0.001, 0.01, 0.1, 0.5][int(rng.below(4))])[0]
+            elif kind == 1:  # contiguous run -> full words
+                a = int(rng.below(c))
+                col = np.zeros(c, bool)
+                col[a:a + int(rng.below(c - a + 1))] = True
+            elif kind == 2:
+                col = np.ones(c, bool)
+            else:
+                col = np.zeros(c, bool)
+            P[f, j] = bits_to_words(col[None, :])[0]
+    return rows, P, frames, props, c
+
+
+@pytest.mark.parametrize("seed", range(120))
+def test_random_scenes(seed):
+    rows, P, frames, props, c = _scene(1000 + seed)
+    r = rows.shape[0]
+    off, idx = to_csr(rows)
+    eng = LabelEngine(devices=[0], stream_task_pairs=int(1 + seed % 97), batch_task_pairs=int(1 + seed % 13),
+                      sort_rows=bool(seed % 2))
+    eng.load_abstraction(CsrBoolMatrix(r, c, off, idx))
+    eng.submit_grid(c, props, P, frames)
+    packed = eng.get_labels_packed() if props else None
+    for f in range(frames):
+        want = ORACLE.label_all(r, c, off, idx, c, props, P[f])
+        if props and r * c <= 2_000_000:  # the oracle itself vs the dense triple loop
+            assert np.array_equal(labels_dense(want, r, props), dense_label(rows, words_to_bits(P[f], c)))
+        got = eng.get_labels(f)
+        assert got == LabelMatrix(r, props, want), f"frame {f}"
+        if props:
+            assert np.array_equal(packed[:, f].astype(np.uint64), want.reshape(r, -1)[:, 0])
+    eng.close()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_synthetic_configs_full(cfg):
+    c = CONFIGS[cfg]
+    depth, E, props = c["depth"], c["edges"], c["props"]
+    prm = SyntheticPRM(seed=1, depth=depth)
+    t = prm.words(0, E)
+    off, idx = prm.csr(0, E)
+    P = props_words(1, depth, props, 0, 1)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
+    eng.submit_grid(1 << depth, props, P, 1)
+    got = eng.get_labels(0)
+    want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[0])
+    assert got == LabelMatrix(E, props, want)
+    hit = labels_dense(want[: min(E, 20000)], min(E, 20000), props).mean()
+    assert 0.02 < hit < 0.6  # parity is non-trivial
+    # the CSR path packs to the same device image and labels identically
+    if cfg < 3:
+        eng.load_abstraction(CsrBoolMatrix(E, 1 << depth, off, idx))
+        eng.submit_grid(1 << depth, props, P, 1)
+        assert eng.get_labels(0) == got
+    eng.close()
+
+
+def test_config4_batched_frames():
+    c = CONFIGS[4]
+    depth, E, props, F = c["depth"], c["edges"], c["props"], c["frames"]
+    prm = SyntheticPRM(seed=1, depth=depth)
+    t = prm.words(0, E)
+    P = props_words(1, depth, props, 0, F)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
+    eng.submit_grid(1 << depth, props, P, F)
+    packed = eng.get_labels_packed()
+    assert packed.shape == (E, F) and packed.dtype == np.uint32
+    off, idx = prm.csr(0, E)
+    for f in (0, 17, 63):  # full oracle parity on sampled frames
+        want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[f])
+        assert np.array_equal(packed[:, f].astype(np.uint64), want)
+    # every frame: the batched kernel equals the single-frame kernel
+    single = LabelEngine(devices=[0])
+    single.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
+    for f in range(0, F, 7):
+        single.submit_grid(1 << depth, props, P[f], 1)
+        assert np.array_equal(single.get_labels(0).bits, packed[:, f].astype(np.uint64))
+    single.close()
+    eng.close()
+
+
+def test_monotone_in_proposition_bits():
+    # test_label.cpp:134-146 at driving-PRM scale
+    depth, E = 16, 200_000
+    prm = SyntheticPRM(seed=3, depth=depth)
+    t = prm.words(0, E)
+    P = props_words(7, depth, 8, 0, 1)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
+    eng.submit_grid(1 << depth, 8, P, 1)
+    before = eng.get_labels(0).bits
+    grown = P.copy()
+    rng = SplitMix64(99)
+    for _ in range(2000):
+        z = rng.below(1 << depth)
+        j = rng.below(8)
+        grown[0, j, z >> 6] |= np.uint64(1 << (z & 63))
+    eng.submit_grid(1 << depth, 8, grown, 1)
+    after = eng.get_labels(0).bits
+    assert np.all((before & ~after) == 0) and np.any(after != before)
+    eng.close()
+
+
+def test_errors_mirror_reference():
+    g = load("eq13_col4")
+    eng = LabelEngine(devices=[0])
+    with pytest.raises(LtlgError, match="no abstraction loaded"):
+        eng.submit_grid(5, 1, g["colwords"], 1)
+    eng.load_abstraction(CsrBoolMatrix(5, 5, g["offsets"], g["indices"]))
+    # label.cpp:151-154
+    with pytest.raises(ValueError, match="^dimension mismatch: matrix cols 5 vs proposition rows 8$"):
+        eng.submit_grid(8, 1, np.zeros(1, np.uint64), 1)
+    # label.cpp:124
+    with pytest.raises(ValueError, match="^at most 64 propositions$"):
+        eng.submit_grid(5, 65, np.zeros(65, np.uint64), 1)
+    # validate(), label.cpp:16-40
+    with pytest.raises(ValueError, match="^column index out of range$"):
+        eng.load_abstraction(CsrBoolMatrix(2, 4, [0, 1, 1], [9]))
+    with pytest.raises(ValueError, match="^row_offsets must be nondecreasing$"):
+        eng.load_abstraction(CsrBoolMatrix(2, 4, [0, 2, 1], [1]))
+    with pytest.raises(ValueError, match="^column indices must be strictly ascending per row$"):
+        eng.load_abstraction(CsrBoolMatrix(1, 8, [0, 2], [5, 2]))
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        label_all(CsrBoolMatrix(5, 5, g["offsets"], g["indices"]), DensePropMatrix.from_words(8, np.zeros((1, 1))))
+    eng.close()
+
+
+def test_csb1_file_loader(tmp_path):
+    g = load("seed31337_csr")
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_file(os.path.join(GOLDEN, "seed31337.csb1"))  # written by the reference
+    rng = SplitMix64(5)
+    P = bits_to_words(random_rows(rng, 3, 2048, 0.02))
+    eng.submit_grid(2048, 3, P, 1)
+    want = ORACLE.label_all(64, 2048, g["offsets"], g["indices"], 2048, 3, P)
+    assert eng.get_labels(0) == LabelMatrix(64, 3, want)
+    bad = tmp_path / "bad.csb1"
+    bad.write_bytes(b"XXXX0000")
+    with pytest.raises(RuntimeError, match="^not a CSR file: "):
+        eng.load_abstraction_file(str(bad))
+    trunc = tmp_path / "trunc.csb1"
+    trunc.write_bytes(open(os.path.join(GOLDEN, "seed31337.csb1"), "rb").read()[:100])
+    with pytest.raises(RuntimeError, match="^truncated CSR file: "):
+        eng.load_abstraction_file(str(trunc))
+    with pytest.raises(RuntimeError, match="^cannot open: "):
+        eng.load_abstraction_file(str(tmp_path / "missing.csb1"))
+    eng.close()
+
+
+@pytest.mark.parametrize("pose", [(0.0, 0.0, 0.0), (3.7, -2.1, 0.0), (0.0, 0.0, 0.4), (-5.5, 8.25, 2.9),
+                                  (60.0, 0.0, -1.2)])
+@pytest.mark.parametrize("outside", [0, 1])
+def test_world_resample_then_label(pose, outside):
+    vdepth, wdepth, props = 12, 14, 5
+    vgrid = (vdepth, 0.0, 102.4, 0.0, 102.4)
+    wgrid = (wdepth, -50.0, 150.0, -40.0, 160.0)
+    world = props_words(11, wdepth, props, 0, 1)[0]
+    dx, dy, th = pose
+    ps = (dx, dy, math.cos(th), math.sin(th))
+    want_P = ORACLE.resample(vgrid, wgrid, ps, props, world, outside)
+    prm = SyntheticPRM(seed=2, depth=vdepth)
+    t = prm.words(0, 5000)
+    off, idx = prm.csr(0, 5000)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_words(5000, 1 << vdepth, t.offsets, t.words, t.masks)
+    eng.submit_world_grid(vgrid, wgrid, props, world, [ps], outside=outside)
+    want = ORACLE.label_all(5000, 1 << vdepth, off, idx, 1 << vdepth, props, want_P)
+    assert eng.get_labels(0) == LabelMatrix(5000, props, want)
+    eng.close()
+
+
+def test_world_resample_batched_poses():
+    vdepth, wdepth, props = 12, 12, 3
+    vgrid = (vdepth, 0.0, 102.4, 0.0, 102.4)
+    wgrid = (wdepth, 0.0, 102.4, 0.0, 102.4)
+    world = props_words(4, wdepth, props, 0, 1)[0]
+    poses = [(1.5 * k, -0.7 * k, math.cos(0.1 * k), math.sin(0.1 * k)) for k in range(6)]
+    prm = SyntheticPRM(seed=2, depth=vdepth)
+    t = prm.words(0, 3000)
+    off, idx = prm.csr(0, 3000)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_words(3000, 1 << vdepth, t.offsets, t.words, t.masks)
+    eng.submit_world_grid(vgrid, wgrid, props, world, poses)
+    for f, ps in enumerate(poses):
+        want = ORACLE.label_all(3000, 1 << vdepth, off, idx, 1 << vdepth, props,
+                                ORACLE.resample(vgrid, wgrid, ps, props, world, 0))
+        assert eng.get_labels(f) == LabelMatrix(3000, props, want)
+    eng.close()
+
+
+def test_empty_and_degenerate():
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction(CsrBoolMatrix(0, 64, [0], []))
+    eng.submit_grid(64, 3, np.zeros(3, np.uint64), 1)
+    assert eng.get_labels(0) == LabelMatrix(0, 3)
+    eng.load_abstraction(CsrBoolMatrix(4, 64, [0, 0, 0, 0, 0], []))
+    eng.submit_grid(64, 2, np.full(2, ~np.uint64(0)), 1)
+    assert eng.get_labels(0) == LabelMatrix(4, 2)  # all-false rows never hit (test_label.cpp:68-73)
+    eng.submit_grid(64, 0, np.zeros(0, np.uint64), 2)
+    assert eng.get_labels(1) == LabelMatrix(4, 0)
+    eng.close()
