@@ -35,10 +35,18 @@
 
 namespace ltlg {
 
+// Summary entry of one (32-bit word, frame):
+//   s, f  : the S / F prop masks above
+//   pa, pb: the P words (valid bits only) of the two lowest "partial" props
+//           (s & ~f), 0 when absent -- so the exact probe of up to two partial
+//           props is branch-free and needs no dependent gather.  Partial
+//           props beyond the second fall back to a gather of P (rare).
 template <typename LW>
-struct alignas(2 * sizeof(LW)) SF {
-    LW s;  // some cell of the word set, per prop
-    LW f;  // every valid cell of the word set, per prop
+struct alignas(16) SF {
+    LW s;
+    LW f;
+    uint32_t pa;
+    uint32_t pb;
 };
 
 __device__ __forceinline__ uint4 ld_stream16(const void* p) {
@@ -60,14 +68,15 @@ __device__ __forceinline__ SF<LW> ld_sf(const SF<LW>* p);
 
 template <>
 __device__ __forceinline__ SF<uint32_t> ld_sf<uint32_t>(const SF<uint32_t>* p) {
-    uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-    return SF<uint32_t>{v.x, v.y};
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    return SF<uint32_t>{v.x, v.y, v.z, v.w};
 }
 
 template <>
 __device__ __forceinline__ SF<uint64_t> ld_sf<uint64_t>(const SF<uint64_t>* p) {
-    ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
-    return SF<uint64_t>{v.x, v.y};
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(p) + 2);
+    return SF<uint64_t>{v.x, v.y, w.x, w.y};
 }
 
 __device__ __forceinline__ int lowest_bit(uint32_t x) { return __ffs(x) - 1; }
@@ -83,17 +92,24 @@ __device__ __forceinline__ LW shfl_idx(LW v, int l) {
 }
 
 // Label contribution of one stored pair (mask m of word w) for one frame.
-//   sfe  : the frame's summary entry of word w
+//   e    : the frame's summary entry of word w
+//   skip : props already known to hit (their probes are unnecessary)
 //   col0 : the frame's P column 0 (u32 view); column j starts at col0 + j*nw32
 template <typename LW>
-__device__ __forceinline__ LW pair_hits(uint32_t m, uint32_t w, SF<LW> sfe, LW skip,
+__device__ __forceinline__ LW pair_hits(uint32_t m, uint32_t w, const SF<LW>& e, LW skip,
                                         const uint32_t* __restrict__ col0, uint32_t nw32) {
-    LW v = sfe.f;
-    LW cand = sfe.s & ~sfe.f & ~skip;
-    while (cand) {
-        const int j = lowest_bit(cand);
+    const LW partial = e.s & ~e.f;
+    const LW abit = partial & (~partial + 1);
+    const LW rest = partial ^ abit;
+    const LW bbit = rest & (~rest + 1);
+    LW v = e.f;
+    v |= (m & e.pa) ? abit : LW(0);
+    v |= (m & e.pb) ? bbit : LW(0);
+    LW over = (rest ^ bbit) & ~skip;
+    while (over) {  // a third partial prop at this word/frame: exact probe
+        const int j = lowest_bit(over);
         if (m & __ldg(col0 + static_cast<uint64_t>(j) * nw32 + w)) v |= LW(1) << j;
-        cand &= cand - 1;
+        over &= over - 1;
     }
     return v;
 }
@@ -111,6 +127,8 @@ __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict
     const int f = blockIdx.y;
     if (w > nw32) return;
     LW s = 0, full = 0;
+    uint32_t pa = 0, pb = 0;
+    int np = 0;
     const uint64_t lo = static_cast<uint64_t>(w) * 32;
     if (w < nw32 && lo < cells) {
         const uint32_t valid = (cells - lo >= 32) ? 0xffffffffu : ((1u << (cells - lo)) - 1u);
@@ -120,9 +138,14 @@ __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict
             const uint32_t x = base[static_cast<uint64_t>(j) * nw32] & valid;
             s |= LW(x != 0) << j;
             full |= LW(x == valid) << j;
+            if (x != 0 && x != valid) {
+                if (np == 0) pa = x;
+                else if (np == 1) pb = x;
+                ++np;
+            }
         }
     }
-    sf[static_cast<uint64_t>(w) * frames + f] = SF<LW>{s, full};
+    sf[static_cast<uint64_t>(w) * frames + f] = SF<LW>{s, full, pa, pb};
 }
 
 // ---------------------------------------------------------------------------
@@ -137,38 +160,37 @@ __global__ void __launch_bounds__(256)
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= ntasks) return;
-    const uint64_t p0 = task_pair[warp], p1 = task_pair[warp + 1];
+    const uint64_t p0 = task_pair[warp];
+    const uint32_t lead = static_cast<uint32_t>(p0 & 3);              // pairs before p0 in the first chunk
+    const uint32_t end = lead + static_cast<uint32_t>(task_pair[warp + 1] - p0);  // task end, chunk-relative
+    const Pair* base = pairs + (p0 - lead);                             // 32-byte aligned
     const int64_t r0 = task_row[warp];
     const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t le = 0xffffffffu >> (31 - lane);
     int64_t open_row = r0 - 1;  // row owning `carry`
     LW carry = 0;
 
-    uint64_t c = p0 & ~uint64_t(3);
-    uint4 a = ld_stream16(pairs + c + 4 * lane);
-    uint4 b = ld_stream16(pairs + c + 4 * lane + 2);
-    for (; c < p1; c += 128) {
-        // software prefetch of the next chunk (array is padded by kPairPad)
-        const uint64_t cn = c + 128;
+    uint4 a = ld_stream16(base + 4 * lane);
+    uint4 b = ld_stream16(base + 4 * lane + 2);
+    for (uint32_t c = 0; c < end; c += 128) {
+        // software prefetch of the next chunk (the pair array is padded by kPairPad)
         uint4 an = a, bn = b;
-        if (cn < p1) {
-            an = ld_stream16(pairs + cn + 4 * lane);
-            bn = ld_stream16(pairs + cn + 4 * lane + 2);
+        if (c + 128 < end) {
+            an = ld_stream16(base + c + 128 + 4 * lane);
+            bn = ld_stream16(base + c + 128 + 4 * lane + 2);
         }
-        const uint64_t q0 = c + 4 * lane;
+        const uint32_t q0 = c + 4 * lane;
         const uint32_t mk[4] = {a.x, a.z, b.x, b.z};
         const uint32_t wh[4] = {a.y, a.w, b.y, b.w};
         bool head[4];
         LW v[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint64_t q = q0 + k;
-            const bool valid = q >= p0 && q < p1;
+            const bool valid = q0 + k >= lead && q0 + k < end;
             head[k] = valid && (wh[k] & kHead);
-            v[k] = 0;
-            if (valid) {
-                const uint32_t w = wh[k] & kWordMask;
-                v[k] = pair_hits<LW>(mk[k], w, ld_sf(sf + w), LW(0), P32, nw32);
-            }
+            const uint32_t w = valid ? (wh[k] & kWordMask) : nw32;  // invalid -> zero sentinel
+            const SF<LW> e = ld_sf(sf + w);
+            v[k] = pair_hits<LW>(mk[k], w, e, LW(0), P32, nw32);
         }
         int hb = 0, tot = 0;
 #pragma unroll
@@ -183,30 +205,24 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (head[k]) {
-                if (nh) {
-                    const int64_t row = open_row + hb + nh;
-                    out[perm[row]] = static_cast<SW>(cur);
-                } else {
-                    pre = cur;
-                }
+                if (nh) out[perm[open_row + hb + nh]] = static_cast<SW>(cur);
+                else pre = cur;
                 ++nh;
                 cur = 0;
             }
             cur |= v[k];
         }
         if (!nh) pre = cur;
-        // warp-wide inclusive segmented OR scan; lane 0 carries the open row
+        // warp-wide segmented inclusive OR scan; a segment starts at the last
+        // lane <= this one holding a head (lane 0 otherwise, carrying the open row)
+        const uint32_t hmask = __ballot_sync(0xffffffffu, nh > 0) & le;
+        const int seg = hmask ? 31 - __clz(hmask) : 0;
         LW x = nh ? cur : pre;
         if (lane == 0 && !nh) x |= carry;
-        bool f = nh > 0;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const LW xo = shfl_up(x, d);
-            const bool fo = __shfl_up_sync(0xffffffffu, static_cast<int>(f), d) != 0;
-            if (lane >= d) {
-                if (!f) x |= xo;
-                f = f || fo;
-            }
+            const LW y = shfl_up(x, d);
+            if (lane - d >= seg) x |= y;
         }
         LW excl = shfl_up(x, 1);
         if (lane == 0) excl = carry;
@@ -272,8 +288,10 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int q = 0; q < FPL; ++q) {
                 const int f = lane + 32 * q;
-                if (f < frames)
-                    acc[q] |= pair_hits<LW>(m, w, ld_sf(e + f), acc[q], P32 + f * frame_stride, nw32);
+                if (f < frames) {
+                    const SF<LW> x = ld_sf(e + f);
+                    acc[q] |= pair_hits<LW>(m, w, x, acc[q], P32 + f * frame_stride, nw32);
+                }
             }
         }
         cur = nxt;
@@ -380,7 +398,7 @@ cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t 
     return cudaGetLastError();
 }
 
-size_t summary_entry_bytes(int props) { return props <= 32 ? 8 : 16; }
+size_t summary_entry_bytes(int props) { return props <= 32 ? sizeof(SF<uint32_t>) : sizeof(SF<uint64_t>); }
 
 template <typename LW, typename SW>
 static void launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
