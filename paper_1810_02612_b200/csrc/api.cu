@@ -101,6 +101,8 @@ struct Shard {
     DevBuf<uint64_t> stage;
     DevBuf<uint64_t> world;
     DevBuf<uint8_t> poses;
+    DevBuf<uint32_t> ctr;  // persistent-kernel task counter
+    DevBuf<uint8_t> s_only;  // S-only summary of multi-frame submits
     bool have_times = false;
     uint64_t rows() const { return row_end - row_begin; }
 };
@@ -275,10 +277,13 @@ ltlg_status run_label(ltlg_ctx* ctx) {
             continue;
         }
         CK(s.sf.reserve(static_cast<size_t>(nw32 + 1) * frames * summary_entry_bytes(props)), "allocate summary");
+        CK(s.ctr.reserve(64), "allocate task counter");
+        if (frames > 1)
+            CK(s.s_only.reserve(static_cast<size_t>(nw32 + 1) * frames * (props <= 32 ? 4 : 8)), "allocate summary");
         const bool prof = ctx->opts.profile != 0;
         if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
         CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
-                          s.stream),
+                          frames > 1 ? s.s_only.ptr : nullptr, s.ctr.ptr, s.stream),
            "summary kernel");
         if (prof) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
@@ -291,6 +296,8 @@ ltlg_status run_label(ltlg_ctx* ctx) {
         a.frames = frames;
         a.out = s.labels.ptr;
         a.label_bytes = ctx->label_bytes;
+        a.task_ctr = s.ctr.ptr;
+        a.s_only = s.s_only.ptr;
         if (frames == 1) {
             a.task_pair = s.tpair_s.ptr;
             a.task_row = s.trow_s.ptr;
@@ -440,6 +447,8 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.stage.release();
         s.world.release();
         s.poses.release();
+        s.ctr.release();
+        s.s_only.release();
         for (auto& ev : s.ring)
             if (ev) cudaEventDestroy(ev);
         if (s.stream) cudaStreamDestroy(s.stream);

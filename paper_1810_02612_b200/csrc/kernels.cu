@@ -122,9 +122,11 @@ __device__ __forceinline__ LW pair_hits(uint32_t m, uint32_t w, const SF<LW>& e,
 template <typename LW>
 __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict__ P32, int props, int frames,
                                                       uint32_t nw32, uint64_t cells,
-                                                      SF<LW>* __restrict__ sf) {
+                                                      SF<LW>* __restrict__ sf, LW* __restrict__ s_only,
+                                                      uint32_t* __restrict__ task_ctr) {
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     const int f = blockIdx.y;
+    if (w == 0 && f == 0) *task_ctr = 0;  // the labeling kernel that follows pulls tasks from 0
     if (w > nw32) return;
     LW s = 0, full = 0;
     uint32_t pa = 0, pb = 0;
@@ -146,157 +148,239 @@ __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict
         }
     }
     sf[static_cast<uint64_t>(w) * frames + f] = SF<LW>{s, full, pa, pb};
+    if (s_only) s_only[static_cast<uint64_t>(w) * frames + f] = s;
 }
 
 // ---------------------------------------------------------------------------
-// Single frame.  One warp per task (a run of whole rows, pairs [p0, p1)).
+// TMA bulk copy + mbarrier helpers (sm_90+ PTX, used on sm_100a)
 // ---------------------------------------------------------------------------
-template <typename LW, typename SW>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Single frame.  Persistent: warps pull tasks (runs of whole rows, pairs
+// [p0, p1)) from an atomic counter.  With TAB_SMEM the frame's summary table
+// is TMA-bulk-copied once per CTA into shared memory (one CTA of 32 warps per
+// SM), so the per-pair gathers hit shared-memory banks instead of L1 tags.
+// ---------------------------------------------------------------------------
+template <typename LW, typename SW, bool TAB_SMEM>
+__global__ void __launch_bounds__(TAB_SMEM ? 1024 : 256)
     label_stream_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
-                        const uint32_t* __restrict__ task_row, uint32_t ntasks,
-                        const SF<LW>* __restrict__ sf, const uint32_t* __restrict__ P32, uint32_t nw32,
-                        const uint32_t* __restrict__ perm, SW* __restrict__ out) {
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                        const uint32_t* __restrict__ task_row, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
+                        const SF<LW>* __restrict__ sf, uint32_t tab_bytes, const uint32_t* __restrict__ P32,
+                        uint32_t nw32, const uint32_t* __restrict__ perm, SW* __restrict__ out) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ uint64_t tab_bar;
     const int lane = threadIdx.x & 31;
-    if (warp >= ntasks) return;
-    const uint64_t p0 = task_pair[warp];
-    const uint32_t lead = static_cast<uint32_t>(p0 & 3);              // pairs before p0 in the first chunk
-    const uint32_t end = lead + static_cast<uint32_t>(task_pair[warp + 1] - p0);  // task end, chunk-relative
-    const Pair* base = pairs + (p0 - lead);                             // 32-byte aligned
-    const int64_t r0 = task_row[warp];
+    const SF<LW>* tab = sf;
+    if constexpr (TAB_SMEM) {
+        if (threadIdx.x == 0) {
+            mbar_init(&tab_bar, 1);
+            mbar_expect_tx(&tab_bar, tab_bytes);
+            for (uint32_t o = 0; o < tab_bytes; o += 32768u) {
+                const uint32_t n = tab_bytes - o < 32768u ? tab_bytes - o : 32768u;
+                bulk_g2s(smem_raw + o, reinterpret_cast<const uint8_t*>(sf) + o, n, &tab_bar);
+            }
+        }
+        __syncthreads();
+        tab = reinterpret_cast<const SF<LW>*>(smem_raw);
+    }
+    bool tab_ready = !TAB_SMEM;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t le = 0xffffffffu >> (31 - lane);
-    int64_t open_row = r0 - 1;  // row owning `carry`
-    LW carry = 0;
 
-    uint4 a = ld_stream16(base + 4 * lane);
-    uint4 b = ld_stream16(base + 4 * lane + 2);
-    for (uint32_t c = 0; c < end; c += 128) {
-        // software prefetch of the next chunk (the pair array is padded by kPairPad)
-        uint4 an = a, bn = b;
-        if (c + 128 < end) {
-            an = ld_stream16(base + c + 128 + 4 * lane);
-            bn = ld_stream16(base + c + 128 + 4 * lane + 2);
-        }
-        const uint32_t q0 = c + 4 * lane;
-        const uint32_t mk[4] = {a.x, a.z, b.x, b.z};
-        const uint32_t wh[4] = {a.y, a.w, b.y, b.w};
-        bool head[4];
-        LW v[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const bool valid = q0 + k >= lead && q0 + k < end;
-            head[k] = valid && (wh[k] & kHead);
-            const uint32_t w = valid ? (wh[k] & kWordMask) : nw32;  // invalid -> zero sentinel
-            const SF<LW> e = ld_sf(sf + w);
-            v[k] = pair_hits<LW>(mk[k], w, e, LW(0), P32, nw32);
-        }
-        int hb = 0, tot = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t bal = __ballot_sync(0xffffffffu, head[k]);
-            hb += __popc(bal & lt);
-            tot += __popc(bal);
-        }
-        // lane-local segmentation: rows that start and end inside this lane
-        LW pre = 0, cur = 0;
-        int nh = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (head[k]) {
-                if (nh) out[perm[open_row + hb + nh]] = static_cast<SW>(cur);
-                else pre = cur;
-                ++nh;
-                cur = 0;
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(task_ctr, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntasks) break;
+        const uint64_t p0 = task_pair[t];
+        const uint32_t lead = static_cast<uint32_t>(p0 & 3);                        // pairs before p0
+        const uint32_t end = lead + static_cast<uint32_t>(task_pair[t + 1] - p0);   // chunk-relative end
+        const Pair* base = pairs + (p0 - lead);                                       // 32-byte aligned
+        const int64_t r0 = task_row[t];
+        int64_t open_row = r0 - 1;  // row owning `carry`
+        LW carry = 0;
+
+        uint4 a = ld_stream16(base + 4 * lane);
+        uint4 b = ld_stream16(base + 4 * lane + 2);
+        if constexpr (TAB_SMEM) {
+            if (!tab_ready) {
+                mbar_wait(&tab_bar, 0);
+                tab_ready = true;
             }
-            cur |= v[k];
         }
-        if (!nh) pre = cur;
-        // warp-wide segmented inclusive OR scan; a segment starts at the last
-        // lane <= this one holding a head (lane 0 otherwise, carrying the open row)
-        const uint32_t hmask = __ballot_sync(0xffffffffu, nh > 0) & le;
-        const int seg = hmask ? 31 - __clz(hmask) : 0;
-        LW x = nh ? cur : pre;
-        if (lane == 0 && !nh) x |= carry;
+        for (uint32_t c = 0; c < end; c += 128) {
+            // software prefetch of the next chunk (the pair array is padded by kPairPad)
+            uint4 an = a, bn = b;
+            if (c + 128 < end) {
+                an = ld_stream16(base + c + 128 + 4 * lane);
+                bn = ld_stream16(base + c + 128 + 4 * lane + 2);
+            }
+            const uint32_t q0 = c + 4 * lane;
+            const uint32_t mk[4] = {a.x, a.z, b.x, b.z};
+            const uint32_t wh[4] = {a.y, a.w, b.y, b.w};
+            bool head[4];
+            LW v[4];
+            const bool interior = c >= lead && c + 128 <= end;  // warp-uniform: every pair valid
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const LW y = shfl_up(x, d);
-            if (lane - d >= seg) x |= y;
+            for (int k = 0; k < 4; ++k) {
+                const bool valid = interior || (q0 + k >= lead && q0 + k < end);
+                head[k] = valid && (wh[k] & kHead);
+                const uint32_t w = valid ? (wh[k] & kWordMask) : nw32;  // invalid -> zero sentinel
+                SF<LW> e;
+                if constexpr (TAB_SMEM) e = tab[w];
+                else e = ld_sf(tab + w);
+                v[k] = pair_hits<LW>(mk[k], w, e, LW(0), P32, nw32);
+            }
+            int hb = 0, tot = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, head[k]);
+                hb += __popc(bal & lt);
+                tot += __popc(bal);
+            }
+            // lane-local segmentation: rows that start and end inside this lane
+            LW pre = 0, cur = 0;
+            int nh = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (head[k]) {
+                    if (nh) out[perm[open_row + hb + nh]] = static_cast<SW>(cur);
+                    else pre = cur;
+                    ++nh;
+                    cur = 0;
+                }
+                cur |= v[k];
+            }
+            if (!nh) pre = cur;
+            // warp-wide segmented inclusive OR scan; a segment starts at the last
+            // lane <= this one holding a head (lane 0 otherwise, carrying the open row)
+            const uint32_t hmask = __ballot_sync(0xffffffffu, nh > 0) & le;
+            const int seg = hmask ? 31 - __clz(hmask) : 0;
+            LW x = nh ? cur : pre;
+            if (lane == 0 && !nh) x |= carry;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const LW y = shfl_up(x, d);
+                if (lane - d >= seg) x |= y;
+            }
+            LW excl = shfl_up(x, 1);
+            if (lane == 0) excl = carry;
+            if (nh) {
+                const int64_t row = open_row + hb;  // the row open before this lane's first head
+                if (row >= r0) out[perm[row]] = static_cast<SW>(excl | pre);
+            }
+            carry = shfl_idx(x, 31);
+            open_row += tot;
+            a = an;
+            b = bn;
         }
-        LW excl = shfl_up(x, 1);
-        if (lane == 0) excl = carry;
-        if (nh) {
-            const int64_t row = open_row + hb;  // the row open before this lane's first head
-            if (row >= r0) out[perm[row]] = static_cast<SW>(excl | pre);
-        }
-        carry = shfl_idx(x, 31);
-        open_row += tot;
-        a = an;
-        b = bn;
+        if (lane == 0 && open_row >= r0) out[perm[open_row]] = static_cast<SW>(carry);
     }
-    if (lane == 0 && open_row >= r0) out[perm[open_row]] = static_cast<SW>(carry);
+    if constexpr (TAB_SMEM) {
+        if (!tab_ready) mbar_wait(&tab_bar, 0);  // never leave with a bulk copy in flight
+    }
 }
 
 // ---------------------------------------------------------------------------
-// F frames.  One warp per task; lane l owns frames l, l+32, ... (FPL of them).
-// sf[w * frames + f], P32 frame f column j at (f*props + j) * nw32,
-// out[perm[row] * frames + f] (edge-major).
+// F frames.  Persistent warps pull tasks; lane l owns frames l, l+32, ...
+// (FPL of them; FULL = every lane owns exactly FPL frames).  Each T pair is
+// read from HBM once for all F frames and broadcast by shuffle.
+//   sf[w * frames + f]  full summary entry (16 B for <= 32 props)
+//   s_only[w * frames + f]  the S mask alone: a pair whose mask covers the
+//                       whole word hits exactly the props set somewhere in
+//                       the word (warp-uniform fast path, 4 B per lookup)
+//   P32 frame f column j at (f*props + j) * nw32
+//   out[perm[row] * frames + f] (edge-major)
 // ---------------------------------------------------------------------------
-template <typename LW, typename SW, int FPL>
+template <typename LW, typename SW, int FPL, bool FULL>
 __global__ void __launch_bounds__(256)
     label_batch_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
-                       const uint32_t* __restrict__ task_row, uint32_t ntasks,
-                       const SF<LW>* __restrict__ sf, const uint32_t* __restrict__ P32, uint32_t nw32,
-                       int props, int frames, const uint32_t* __restrict__ perm, SW* __restrict__ out) {
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                       const uint32_t* __restrict__ task_row, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
+                       const SF<LW>* __restrict__ sf, const LW* __restrict__ s_only,
+                       const uint32_t* __restrict__ P32, uint32_t nw32, int props, int frames,
+                       const uint32_t* __restrict__ perm, SW* __restrict__ out) {
     const int lane = threadIdx.x & 31;
-    if (warp >= ntasks) return;
-    const uint64_t p0 = task_pair[warp], p1 = task_pair[warp + 1];
-    const int64_t r0 = task_row[warp];
-    int64_t row = r0 - 1;
     const uint64_t frame_stride = static_cast<uint64_t>(props) * nw32;
-    LW acc[FPL];
+    const SF<LW>* lane_sf = sf + lane;
+    const LW* lane_s = s_only + lane;
+    const uint32_t* lane_P = P32 + static_cast<uint64_t>(lane) * frame_stride;
+    bool fv[FPL];
 #pragma unroll
-    for (int q = 0; q < FPL; ++q) acc[q] = 0;
+    for (int q = 0; q < FPL; ++q) fv[q] = FULL || lane + 32 * q < frames;
 
-    auto store = [&](int64_t r) {
-        const uint64_t base = static_cast<uint64_t>(perm[r]) * frames;
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(task_ctr, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntasks) break;
+        const uint64_t p0 = task_pair[t], p1 = task_pair[t + 1];
+        const int64_t r0 = task_row[t];
+        int64_t row = r0 - 1;
+        LW acc[FPL];
 #pragma unroll
-        for (int q = 0; q < FPL; ++q) {
-            const int f = lane + 32 * q;
-            if (f < frames) out[base + f] = static_cast<SW>(acc[q]);
-        }
-    };
-
-    uint2 cur = ld_stream8(pairs + p0 + lane);
-    for (uint64_t c = p0; c < p1; c += 32) {
-        uint2 nxt = cur;
-        if (c + 32 < p1) nxt = ld_stream8(pairs + c + 32 + lane);
-        const int n = static_cast<int>(p1 - c < 32 ? p1 - c : 32);
-        for (int i = 0; i < n; ++i) {
-            const uint32_t m = __shfl_sync(0xffffffffu, cur.x, i);
-            const uint32_t wh = __shfl_sync(0xffffffffu, cur.y, i);
-            if (wh & kHead) {  // warp-uniform
-                if (row >= r0) store(row);
-                ++row;
+        for (int q = 0; q < FPL; ++q) acc[q] = 0;
+        auto store = [&](int64_t r) {
+            SW* o = out + static_cast<uint64_t>(perm[r]) * frames + lane;
 #pragma unroll
-                for (int q = 0; q < FPL; ++q) acc[q] = 0;
-            }
-            const uint32_t w = wh & kWordMask;
-            const SF<LW>* e = sf + static_cast<uint64_t>(w) * frames;
+            for (int q = 0; q < FPL; ++q)
+                if (fv[q]) o[32 * q] = static_cast<SW>(acc[q]);
+        };
+        uint2 cur = ld_stream8(pairs + p0 + lane);
+        for (uint64_t c = p0; c < p1; c += 32) {
+            uint2 nxt = cur;
+            if (c + 32 < p1) nxt = ld_stream8(pairs + c + 32 + lane);
+            const int n = static_cast<int>(p1 - c < 32 ? p1 - c : 32);
+            for (int i = 0; i < n; ++i) {
+                const uint32_t m = __shfl_sync(0xffffffffu, cur.x, i);
+                const uint32_t wh = __shfl_sync(0xffffffffu, cur.y, i);
+                if (wh & kHead) {  // warp-uniform
+                    if (row >= r0) store(row);
+                    ++row;
 #pragma unroll
-            for (int q = 0; q < FPL; ++q) {
-                const int f = lane + 32 * q;
-                if (f < frames) {
-                    const SF<LW> x = ld_sf(e + f);
-                    acc[q] |= pair_hits<LW>(m, w, x, acc[q], P32 + f * frame_stride, nw32);
+                    for (int q = 0; q < FPL; ++q) acc[q] = 0;
+                }
+                const uint32_t w = wh & kWordMask;
+                const uint32_t off = w * static_cast<uint32_t>(frames);
+                if (m == 0xffffffffu) {  // warp-uniform: the whole word is swept
+#pragma unroll
+                    for (int q = 0; q < FPL; ++q)
+                        if (fv[q]) acc[q] |= __ldg(lane_s + off + 32 * q);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < FPL; ++q)
+                        if (fv[q]) {
+                            const SF<LW> x = ld_sf(lane_sf + off + 32 * q);
+                            acc[q] |= pair_hits<LW>(m, w, x, acc[q], lane_P + 32 * q * frame_stride, nw32);
+                        }
                 }
             }
+            cur = nxt;
         }
-        cur = nxt;
+        if (row >= r0) store(row);
     }
-    if (row >= r0) store(row);
 }
 
 // One frame of packed edge-major labels -> LabelMatrix u64 words.
@@ -387,41 +471,83 @@ __global__ void resample_kernel(Grid2 vg, Grid2 wg, const Pose2* __restrict__ po
 // ---------------------------------------------------------------------------
 
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
-                           void* sf, cudaStream_t st) {
+                           void* sf, void* s_only, uint32_t* task_ctr, cudaStream_t st) {
     dim3 grid((nw32 + 1 + 255) / 256, static_cast<unsigned>(frames));
     if (props <= 32)
         summary_kernel<uint32_t><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells,
-                                                       static_cast<SF<uint32_t>*>(sf));
+                                                       static_cast<SF<uint32_t>*>(sf),
+                                                       static_cast<uint32_t*>(s_only), task_ctr);
     else
         summary_kernel<uint64_t><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells,
-                                                       static_cast<SF<uint64_t>*>(sf));
+                                                       static_cast<SF<uint64_t>*>(sf),
+                                                       static_cast<uint64_t*>(s_only), task_ctr);
     return cudaGetLastError();
 }
 
 size_t summary_entry_bytes(int props) { return props <= 32 ? sizeof(SF<uint32_t>) : sizeof(SF<uint64_t>); }
 
-template <typename LW, typename SW>
-static void launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
-    const unsigned blocks = (a.ntasks + 7) / 8;
-    label_stream_kernel<LW, SW><<<blocks, 256, 0, st>>>(a.pairs, a.task_pair, a.task_row, a.ntasks,
-                                                       static_cast<const SF<LW>*>(a.sf), a.P32, a.nw32,
-                                                       a.perm, static_cast<SW*>(a.out));
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
 }
 
-template <typename LW, typename SW, int FPL>
+constexpr uint32_t kMaxSmemTable = 200u * 1024u;
+
+template <typename LW, typename SW>
+static void launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
+    const uint32_t tab_bytes = (a.nw32 + 1) * static_cast<uint32_t>(sizeof(SF<LW>));
+    const auto* tab = static_cast<const SF<LW>*>(a.sf);
+    if (tab_bytes <= kMaxSmemTable) {
+        static uint64_t attr_set = 0;  // per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!(attr_set >> dev & 1u)) {
+            cudaFuncSetAttribute(label_stream_kernel<LW, SW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kMaxSmemTable));
+            attr_set |= 1ull << dev;
+        }
+        label_stream_kernel<LW, SW, true><<<sm_count(), 1024, tab_bytes, st>>>(
+            a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, tab, tab_bytes, a.P32, a.nw32, a.perm,
+            static_cast<SW*>(a.out));
+    } else {
+        static int per_sm = 0;
+        if (!per_sm) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, label_stream_kernel<LW, SW, false>, 256, 0);
+            if (per_sm <= 0) per_sm = 4;
+        }
+        label_stream_kernel<LW, SW, false><<<sm_count() * per_sm, 256, 0, st>>>(
+            a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, tab, tab_bytes, a.P32, a.nw32, a.perm,
+            static_cast<SW*>(a.out));
+    }
+}
+
+template <typename LW, typename SW, int FPL, bool FULL>
 static void launch_batch_t(const LaunchArgs& a, cudaStream_t st) {
-    const unsigned blocks = (a.ntasks + 7) / 8;
-    label_batch_kernel<LW, SW, FPL><<<blocks, 256, 0, st>>>(a.pairs, a.task_pair, a.task_row, a.ntasks,
-                                                           static_cast<const SF<LW>*>(a.sf), a.P32, a.nw32,
-                                                           a.props, a.frames, a.perm, static_cast<SW*>(a.out));
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, label_batch_kernel<LW, SW, FPL, FULL>, 256, 0);
+        if (per_sm <= 0) per_sm = 4;
+    }
+    label_batch_kernel<LW, SW, FPL, FULL><<<sm_count() * per_sm, 256, 0, st>>>(
+        a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, static_cast<const SF<LW>*>(a.sf),
+        static_cast<const LW*>(a.s_only), a.P32, a.nw32, a.props, a.frames, a.perm, static_cast<SW*>(a.out));
 }
 
 template <typename LW, typename SW>
 static void launch_batch_fpl(const LaunchArgs& a, cudaStream_t st) {
-    if (a.frames <= 32) launch_batch_t<LW, SW, 1>(a, st);
-    else if (a.frames <= 64) launch_batch_t<LW, SW, 2>(a, st);
-    else if (a.frames <= 128) launch_batch_t<LW, SW, 4>(a, st);
-    else launch_batch_t<LW, SW, 8>(a, st);
+    if (a.frames == 32) launch_batch_t<LW, SW, 1, true>(a, st);
+    else if (a.frames == 64) launch_batch_t<LW, SW, 2, true>(a, st);
+    else if (a.frames == 128) launch_batch_t<LW, SW, 4, true>(a, st);
+    else if (a.frames < 32) launch_batch_t<LW, SW, 1, false>(a, st);
+    else if (a.frames < 64) launch_batch_t<LW, SW, 2, false>(a, st);
+    else if (a.frames < 128) launch_batch_t<LW, SW, 4, false>(a, st);
+    else launch_batch_t<LW, SW, 8, false>(a, st);
 }
 
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {

@@ -23,10 +23,12 @@ struct LaunchArgs {
     const uint32_t* perm;
     void* out;
     int label_bytes;
+    uint32_t* task_ctr;  // device counter, reset by the summary kernel
+    const void* s_only;  // S-only summary (multi-frame kernel)
 };
 
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
-                           void* sf, cudaStream_t st);
+                           void* sf, void* s_only, uint32_t* task_ctr, cudaStream_t st);
 size_t summary_entry_bytes(int props);
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st);
 cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, int frames, int frame,
