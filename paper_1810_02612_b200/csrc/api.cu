@@ -103,6 +103,7 @@ struct Shard {
     DevBuf<uint8_t> poses;
     DevBuf<uint32_t> ctr;  // persistent-kernel task counter
     DevBuf<uint8_t> s_only;  // S-only summary of multi-frame submits
+    DevBuf<uint8_t> split;   // single-frame shared-memory split table
     bool have_times = false;
     uint64_t rows() const { return row_end - row_begin; }
 };
@@ -280,10 +281,13 @@ ltlg_status run_label(ltlg_ctx* ctx) {
         CK(s.ctr.reserve(64), "allocate task counter");
         if (frames > 1)
             CK(s.s_only.reserve(static_cast<size_t>(nw32 + 1) * frames * (props <= 32 ? 4 : 8)), "allocate summary");
+        const bool use_split = frames == 1 && stream_table_mode(props, nw32) >= 4;
+        if (use_split) CK(s.split.reserve(split_table_bytes(props, nw32)), "allocate summary");
         const bool prof = ctx->opts.profile != 0;
         if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
         CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
-                          frames > 1 ? s.s_only.ptr : nullptr, s.ctr.ptr, s.stream),
+                          frames > 1 ? s.s_only.ptr : nullptr, s.ctr.ptr, use_split ? s.split.ptr : nullptr,
+                          s.stream),
            "summary kernel");
         if (prof) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
@@ -298,6 +302,7 @@ ltlg_status run_label(ltlg_ctx* ctx) {
         a.label_bytes = ctx->label_bytes;
         a.task_ctr = s.ctr.ptr;
         a.s_only = s.s_only.ptr;
+        a.split = s.split.ptr;
         if (frames == 1) {
             a.task_pair = s.tpair_s.ptr;
             a.task_row = s.trow_s.ptr;
@@ -449,6 +454,7 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.poses.release();
         s.ctr.release();
         s.s_only.release();
+        s.split.release();
         for (auto& ev : s.ring)
             if (ev) cudaEventDestroy(ev);
         if (s.stream) cudaStreamDestroy(s.stream);

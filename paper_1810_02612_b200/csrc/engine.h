@@ -45,7 +45,7 @@ struct PackedShard {
     std::vector<uint64_t> task_pair_stream, task_pair_batch;  // ntasks + 1
 };
 
-constexpr uint64_t kPairPad = 256;  // tail padding so vector loads never leave the array
+constexpr uint64_t kPairPad = 512;  // tail padding so vector loads never leave the array
 
 // Host-side loader (loader.cpp).
 bool validate_csr(uint64_t rows, uint64_t cols, const uint64_t* offsets, uint64_t n_offsets,

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "engine.h"
 #include "launch.h"
@@ -123,7 +124,8 @@ template <typename LW>
 __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict__ P32, int props, int frames,
                                                       uint32_t nw32, uint64_t cells,
                                                       SF<LW>* __restrict__ sf, LW* __restrict__ s_only,
-                                                      uint32_t* __restrict__ task_ctr) {
+                                                      uint32_t* __restrict__ task_ctr, uint8_t* __restrict__ split,
+                                                      int split_mb) {
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     const int f = blockIdx.y;
     if (w == 0 && f == 0) *task_ctr = 0;  // the labeling kernel that follows pulls tasks from 0
@@ -149,6 +151,12 @@ __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict
     }
     sf[static_cast<uint64_t>(w) * frames + f] = SF<LW>{s, full, pa, pb};
     if (s_only) s_only[static_cast<uint64_t>(w) * frames + f] = s;
+    if (split) {  // single frame, shared-memory split layout: M[w] then X[w] = {pa, pb}
+        if (split_mb == 4) reinterpret_cast<uint32_t*>(split)[w] = static_cast<uint32_t>(s) | (static_cast<uint32_t>(full) << 16);
+        else reinterpret_cast<uint2*>(split)[w] = make_uint2(static_cast<uint32_t>(s), static_cast<uint32_t>(full));
+        const uint32_t xoff = (static_cast<uint32_t>(split_mb) * (nw32 + 1) + 15u) & ~15u;
+        reinterpret_cast<uint2*>(split + xoff)[w] = make_uint2(pa, pb);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -171,11 +179,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-            smem_u32(bar)),
-        "r"(phase)
-        : "memory");
+    // bounded: a bulk copy that can never complete traps instead of hanging the GPU
+    for (uint32_t spin = 0;; ++spin) {
+        uint32_t done;
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+        if (done) return;
+        if (spin > (1u << 22)) __trap();
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -184,16 +198,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // is TMA-bulk-copied once per CTA into shared memory (one CTA of 32 warps per
 // SM), so the per-pair gathers hit shared-memory banks instead of L1 tags.
 // ---------------------------------------------------------------------------
-template <typename LW, typename SW, bool TAB_SMEM>
-__global__ void __launch_bounds__(TAB_SMEM ? 1024 : 256)
+template <typename LW, typename SW, int TAB, int K>
+__global__ void __launch_bounds__(TAB ? 1024 : 256)
     label_stream_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
                         const uint32_t* __restrict__ task_row, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
                         const SF<LW>* __restrict__ sf, uint32_t tab_bytes, const uint32_t* __restrict__ P32,
                         uint32_t nw32, const uint32_t* __restrict__ perm, SW* __restrict__ out) {
+    constexpr uint32_t CH = 32 * K;         // pairs per warp chunk
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ uint64_t tab_bar;
     const int lane = threadIdx.x & 31;
     const SF<LW>* tab = sf;
+    constexpr bool TAB_SMEM = TAB != 0;
+    constexpr bool SPLIT = TAB == 4 || TAB == 8;
+    const uint8_t* xtab = nullptr;  // split mode: {Pa, Pb} table after the M table
     if constexpr (TAB_SMEM) {
         if (threadIdx.x == 0) {
             mbar_init(&tab_bar, 1);
@@ -205,9 +223,9 @@ __global__ void __launch_bounds__(TAB_SMEM ? 1024 : 256)
         }
         __syncthreads();
         tab = reinterpret_cast<const SF<LW>*>(smem_raw);
+        if constexpr (SPLIT) xtab = smem_raw + ((static_cast<uint32_t>(TAB) * (nw32 + 1) + 15u) & ~15u);
     }
-    bool tab_ready = !TAB_SMEM;
-    const uint32_t lt = (1u << lane) - 1u;
+    bool tab_ready = TAB == 0;
     const uint32_t le = 0xffffffffu >> (31 - lane);
 
     for (;;) {
@@ -218,68 +236,91 @@ __global__ void __launch_bounds__(TAB_SMEM ? 1024 : 256)
         const uint64_t p0 = task_pair[t];
         const uint32_t lead = static_cast<uint32_t>(p0 & 3);                        // pairs before p0
         const uint32_t end = lead + static_cast<uint32_t>(task_pair[t + 1] - p0);   // chunk-relative end
-        const Pair* base = pairs + (p0 - lead);                                       // 32-byte aligned
-        const int64_t r0 = task_row[t];
-        int64_t open_row = r0 - 1;  // row owning `carry`
+        const uint4* base = reinterpret_cast<const uint4*>(pairs + (p0 - lead));     // 32-byte aligned
+        const int32_t r0 = static_cast<int32_t>(task_row[t]);
+        int32_t open_row = r0 - 1;  // row owning `carry`
         LW carry = 0;
 
-        uint4 a = ld_stream16(base + 4 * lane);
-        uint4 b = ld_stream16(base + 4 * lane + 2);
+        uint4 cur[K / 2], nxt[K / 2];
+#pragma unroll
+        for (int h = 0; h < K / 2; ++h) cur[h] = ld_stream16(base + (K / 2) * lane + h);
         if constexpr (TAB_SMEM) {
             if (!tab_ready) {
                 mbar_wait(&tab_bar, 0);
                 tab_ready = true;
             }
         }
-        for (uint32_t c = 0; c < end; c += 128) {
+        for (uint32_t c = 0; c < end; c += CH) {
             // software prefetch of the next chunk (the pair array is padded by kPairPad)
-            uint4 an = a, bn = b;
-            if (c + 128 < end) {
-                an = ld_stream16(base + c + 128 + 4 * lane);
-                bn = ld_stream16(base + c + 128 + 4 * lane + 2);
-            }
-            const uint32_t q0 = c + 4 * lane;
-            const uint32_t mk[4] = {a.x, a.z, b.x, b.z};
-            const uint32_t wh[4] = {a.y, a.w, b.y, b.w};
-            bool head[4];
-            LW v[4];
-            const bool interior = c >= lead && c + 128 <= end;  // warp-uniform: every pair valid
+            if (c + CH < end) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+                for (int h = 0; h < K / 2; ++h) nxt[h] = ld_stream16(base + (c + CH) / 2 + (K / 2) * lane + h);
+            }
+            const uint32_t q0 = c + K * lane;
+            const bool interior = c >= lead && c + CH <= end;  // warp-uniform: every pair valid
+            uint32_t heads = 0;  // bit k: pair k opens a row
+            LW v[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const uint32_t mk = (k & 1) ? cur[k / 2].z : cur[k / 2].x;
+                const uint32_t wh = (k & 1) ? cur[k / 2].w : cur[k / 2].y;
                 const bool valid = interior || (q0 + k >= lead && q0 + k < end);
-                head[k] = valid && (wh[k] & kHead);
-                const uint32_t w = valid ? (wh[k] & kWordMask) : nw32;  // invalid -> zero sentinel
-                SF<LW> e;
-                if constexpr (TAB_SMEM) e = tab[w];
-                else e = ld_sf(tab + w);
-                v[k] = pair_hits<LW>(mk[k], w, e, LW(0), P32, nw32);
-            }
-            int hb = 0, tot = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t bal = __ballot_sync(0xffffffffu, head[k]);
-                hb += __popc(bal & lt);
-                tot += __popc(bal);
-            }
-            // lane-local segmentation: rows that start and end inside this lane
-            LW pre = 0, cur = 0;
-            int nh = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (head[k]) {
-                    if (nh) out[perm[open_row + hb + nh]] = static_cast<SW>(cur);
-                    else pre = cur;
-                    ++nh;
-                    cur = 0;
+                heads |= static_cast<uint32_t>(valid && (wh & kHead)) << k;
+                const uint32_t w = valid ? (wh & kWordMask) : nw32;  // invalid -> zero sentinel
+                if constexpr (SPLIT) {
+                    LW S, F;
+                    if constexpr (TAB == 4) {
+                        const uint32_t e = reinterpret_cast<const uint32_t*>(smem_raw)[w];
+                        S = e & 0xffffu;
+                        F = e >> 16;
+                    } else {
+                        const uint2 e = reinterpret_cast<const uint2*>(smem_raw)[w];
+                        S = e.x;
+                        F = e.y;
+                    }
+                    const LW partial = S & ~F;
+                    LW vv = F;
+                    if (partial) {
+                        const uint2 x = reinterpret_cast<const uint2*>(xtab)[w];
+                        vv = pair_hits<LW>(mk, w, SF<LW>{S, F, x.x, x.y}, LW(0), P32, nw32);
+                    }
+                    v[k] = vv;
+                } else {
+                    SF<LW> e;
+                    if constexpr (TAB_SMEM) e = tab[w];
+                    else e = ld_sf(tab + w);
+                    v[k] = pair_hits<LW>(mk, w, e, LW(0), P32, nw32);
                 }
-                cur |= v[k];
             }
-            if (!nh) pre = cur;
+            // rows opened in lower lanes (exclusive prefix of head counts)
+            const int nh = __popc(heads);
+            int incl = nh;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += y;
+            }
+            const int hb = incl - nh;
+            const int tot = __shfl_sync(0xffffffffu, incl, 31);
+            // lane-local segmentation: rows that start and end inside this lane
+            LW pre = 0, cur_or = 0;
+            int seen = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (heads >> k & 1u) {
+                    if (seen) out[perm[open_row + hb + seen]] = static_cast<SW>(cur_or);
+                    else pre = cur_or;
+                    ++seen;
+                    cur_or = 0;
+                }
+                cur_or |= v[k];
+            }
+            if (!nh) pre = cur_or;
             // warp-wide segmented inclusive OR scan; a segment starts at the last
             // lane <= this one holding a head (lane 0 otherwise, carrying the open row)
             const uint32_t hmask = __ballot_sync(0xffffffffu, nh > 0) & le;
             const int seg = hmask ? 31 - __clz(hmask) : 0;
-            LW x = nh ? cur : pre;
+            LW x = nh ? cur_or : pre;
             if (lane == 0 && !nh) x |= carry;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -289,13 +330,13 @@ __global__ void __launch_bounds__(TAB_SMEM ? 1024 : 256)
             LW excl = shfl_up(x, 1);
             if (lane == 0) excl = carry;
             if (nh) {
-                const int64_t row = open_row + hb;  // the row open before this lane's first head
+                const int32_t row = open_row + hb;  // the row open before this lane's first head
                 if (row >= r0) out[perm[row]] = static_cast<SW>(excl | pre);
             }
             carry = shfl_idx(x, 31);
             open_row += tot;
-            a = an;
-            b = bn;
+#pragma unroll
+            for (int h = 0; h < K / 2; ++h) cur[h] = nxt[h];
         }
         if (lane == 0 && open_row >= r0) out[perm[open_row]] = static_cast<SW>(carry);
     }
@@ -470,17 +511,31 @@ __global__ void resample_kernel(Grid2 vg, Grid2 wg, const Pose2* __restrict__ po
 // Host launchers
 // ---------------------------------------------------------------------------
 
+// Single-frame shared-memory "split" table: M[w] (S|F<<16 in 4 B for <= 16
+// props, {S, F} in 8 B for <= 32) followed by X[w] = {pa, pb}; the wider M
+// halves the bank-conflict wavefronts of the per-pair gathers and X is only
+// read by lanes whose word has a partial prop.
+int split_entry_bytes(int props) { return props <= 16 ? 4 : props <= 32 ? 8 : 0; }
+size_t split_table_bytes(int props, uint32_t nw32) {
+    const int mb = split_entry_bytes(props);
+    if (!mb) return 0;
+    // both parts 16-byte aligned: the whole table is one set of TMA bulk copies
+    return ((static_cast<size_t>(mb) * (nw32 + 1) + 15u) & ~size_t(15)) + ((8u * (nw32 + 1) + 15u) & ~size_t(15));
+}
+
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
-                           void* sf, void* s_only, uint32_t* task_ctr, cudaStream_t st) {
+                           void* sf, void* s_only, uint32_t* task_ctr, void* split, cudaStream_t st) {
     dim3 grid((nw32 + 1 + 255) / 256, static_cast<unsigned>(frames));
+    const int mb = split_entry_bytes(props);
     if (props <= 32)
         summary_kernel<uint32_t><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells,
                                                        static_cast<SF<uint32_t>*>(sf),
-                                                       static_cast<uint32_t*>(s_only), task_ctr);
+                                                       static_cast<uint32_t*>(s_only), task_ctr,
+                                                       static_cast<uint8_t*>(split), mb);
     else
         summary_kernel<uint64_t><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells,
                                                        static_cast<SF<uint64_t>*>(sf),
-                                                       static_cast<uint64_t*>(s_only), task_ctr);
+                                                       static_cast<uint64_t*>(s_only), task_ctr, nullptr, 0);
     return cudaGetLastError();
 }
 
@@ -499,32 +554,75 @@ static int sm_count() {
 
 constexpr uint32_t kMaxSmemTable = 200u * 1024u;
 
-template <typename LW, typename SW>
-static void launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
-    const uint32_t tab_bytes = (a.nw32 + 1) * static_cast<uint32_t>(sizeof(SF<LW>));
-    const auto* tab = static_cast<const SF<LW>*>(a.sf);
-    if (tab_bytes <= kMaxSmemTable) {
+// Dev knobs (A/B sweeps on the GPU box): LTLG_STREAM_TABLE=smem|global, LTLG_STREAM_K=4|8
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+template <typename LW, typename SW, int TAB, int K>
+static cudaError_t launch_stream_v(const LaunchArgs& a, uint32_t tab_bytes, const void* tab_src, cudaStream_t st) {
+    const auto* tab = static_cast<const SF<LW>*>(tab_src);
+    if constexpr (TAB != 0) {
         static uint64_t attr_set = 0;  // per device
         int dev = 0;
         cudaGetDevice(&dev);
         if (!(attr_set >> dev & 1u)) {
-            cudaFuncSetAttribute(label_stream_kernel<LW, SW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(label_stream_kernel<LW, SW, TAB, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kMaxSmemTable));
             attr_set |= 1ull << dev;
         }
-        label_stream_kernel<LW, SW, true><<<sm_count(), 1024, tab_bytes, st>>>(
+        if (tab_bytes % 16u) return cudaErrorInvalidValue;  // never launch an uncompletable TMA copy
+        label_stream_kernel<LW, SW, TAB, K><<<sm_count(), 1024, tab_bytes, st>>>(
             a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, tab, tab_bytes, a.P32, a.nw32, a.perm,
             static_cast<SW*>(a.out));
     } else {
         static int per_sm = 0;
         if (!per_sm) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, label_stream_kernel<LW, SW, false>, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, label_stream_kernel<LW, SW, 0, K>, 256, 0);
             if (per_sm <= 0) per_sm = 4;
         }
-        label_stream_kernel<LW, SW, false><<<sm_count() * per_sm, 256, 0, st>>>(
+        label_stream_kernel<LW, SW, 0, K><<<sm_count() * per_sm, 256, 0, st>>>(
             a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, tab, tab_bytes, a.P32, a.nw32, a.perm,
             static_cast<SW*>(a.out));
     }
+    return cudaSuccess;
+}
+
+// Which single-frame table layout a submit uses (the summary kernel must
+// write the split layout when this returns a split mode).
+int stream_table_mode(int props, uint32_t nw32) {
+    static const int want = env_int("LTLG_STREAM_TABLE", -1);  // dev knob: 0 global, 1 smem, 2 split
+    const size_t comb = static_cast<size_t>(nw32 + 1) * summary_entry_bytes(props);
+    const size_t split = split_table_bytes(props, nw32);
+    if (want == 0) return 0;
+    if (want == 1) return comb <= kMaxSmemTable ? 1 : 0;
+    if (split && split <= kMaxSmemTable) return split_entry_bytes(props);
+    return comb <= kMaxSmemTable ? 1 : 0;
+}
+
+template <typename LW, typename SW>
+static cudaError_t launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
+    static const int k = env_int("LTLG_STREAM_K", 4);
+    const int mode = stream_table_mode(a.props, a.nw32);
+    const uint32_t comb = (a.nw32 + 1) * static_cast<uint32_t>(sizeof(SF<LW>));
+    if (mode == 0) {
+        if (k == 8) return launch_stream_v<LW, SW, 0, 8>(a, comb, a.sf, st);
+        else return launch_stream_v<LW, SW, 0, 4>(a, comb, a.sf, st);
+    } else if (mode == 1) {
+        if (k == 8) return launch_stream_v<LW, SW, 1, 8>(a, comb, a.sf, st);
+        else return launch_stream_v<LW, SW, 1, 4>(a, comb, a.sf, st);
+    } else if constexpr (sizeof(LW) == 4) {
+        const uint32_t sb = static_cast<uint32_t>(split_table_bytes(a.props, a.nw32));
+        if (mode == 4) {
+            if (k == 8) return launch_stream_v<LW, SW, 4, 8>(a, sb, a.split, st);
+            else return launch_stream_v<LW, SW, 4, 4>(a, sb, a.split, st);
+        } else {
+            if (k == 8) return launch_stream_v<LW, SW, 8, 8>(a, sb, a.split, st);
+            else return launch_stream_v<LW, SW, 8, 4>(a, sb, a.split, st);
+        }
+    }
+    return cudaErrorInvalidValue;
 }
 
 template <typename LW, typename SW, int FPL, bool FULL>
@@ -552,12 +650,13 @@ static void launch_batch_fpl(const LaunchArgs& a, cudaStream_t st) {
 
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
     if (a.ntasks == 0) return cudaSuccess;
+    cudaError_t e = cudaSuccess;
     if (a.frames == 1) {
         switch (a.label_bytes) {
-            case 1: launch_stream_t<uint32_t, uint8_t>(a, st); break;
-            case 2: launch_stream_t<uint32_t, uint16_t>(a, st); break;
-            case 4: launch_stream_t<uint32_t, uint32_t>(a, st); break;
-            default: launch_stream_t<uint64_t, uint64_t>(a, st); break;
+            case 1: e = launch_stream_t<uint32_t, uint8_t>(a, st); break;
+            case 2: e = launch_stream_t<uint32_t, uint16_t>(a, st); break;
+            case 4: e = launch_stream_t<uint32_t, uint32_t>(a, st); break;
+            default: e = launch_stream_t<uint64_t, uint64_t>(a, st); break;
         }
     } else {
         switch (a.label_bytes) {
@@ -567,6 +666,7 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
             default: launch_batch_fpl<uint64_t, uint64_t>(a, st); break;
         }
     }
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
