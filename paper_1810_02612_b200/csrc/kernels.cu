@@ -603,7 +603,7 @@ int stream_table_mode(int props, uint32_t nw32) {
 
 template <typename LW, typename SW>
 static cudaError_t launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
-    static const int k = env_int("LTLG_STREAM_K", 4);
+    static const int k = env_int("LTLG_STREAM_K", 8);
     const int mode = stream_table_mode(a.props, a.nw32);
     const uint32_t comb = (a.nw32 + 1) * static_cast<uint32_t>(sizeof(SF<LW>));
     if (mode == 0) {
