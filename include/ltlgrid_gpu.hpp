@@ -1,0 +1,119 @@
+// ltlgrid_gpu.hpp -- header-only C++ drop-in over the C ABI (ltlgrid_gpu.h).
+//
+// For code written against the reference core (proj/core/include/ltlgrid/
+// label.hpp): include the reference header first, then this one, and switch
+//     ltlgrid::label_all(m, p, workers)        (label.hpp:94-98)
+// to
+//     ltlgrid::gpu::label_all(m, p, workers)
+// Same argument meaning, same exception types and messages
+// (std::invalid_argument for LTLG_EINVAL -- dimension mismatch label.cpp:151-154,
+// > 64 props label.cpp:124, malformed CSR label.cpp:16-40; std::runtime_error for
+// file / CUDA failures).  `workers` is accepted and ignored: the result is
+// identical for any value (test_label.cpp:121-132).
+//
+// ltlgrid::gpu::Engine keeps T resident in HBM across frames (the reference
+// re-reads its CSR on every call): load once, then submit per frame.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ltlgrid/label.hpp"  // the reference's CsrBoolMatrix / DensePropMatrix / LabelMatrix
+#include "ltlgrid_gpu.h"
+
+namespace ltlgrid {
+namespace gpu {
+
+[[noreturn]] inline void throw_status(ltlg_status s, const char* msg) {
+    if (s == LTLG_EINVAL) throw std::invalid_argument(msg);
+    if (s == LTLG_ENOMEM) throw std::bad_alloc();
+    throw std::runtime_error(msg);
+}
+
+inline void check(ltlg_status s, const ltlg_ctx* ctx) {
+    if (s != LTLG_OK) throw_status(s, ltlg_last_error(ctx));
+}
+
+// DensePropMatrix columns -> contiguous column-major words (label.hpp:47-58).
+template <class Dense>
+std::vector<std::uint64_t> column_words(const Dense& p) {
+    std::vector<std::uint64_t> w;
+    const std::uint64_t per = (p.cells() + 63) / 64;
+    w.reserve(per * static_cast<std::uint64_t>(p.num_props()));
+    for (int j = 0; j < p.num_props(); ++j) {
+        const auto col = p.column(j).words();
+        w.insert(w.end(), col.begin(), col.end());
+    }
+    return w;
+}
+
+// Reference LabelMatrix from LabelMatrix-layout words (label.hpp:61-92).
+template <class Labels>
+Labels to_label_matrix(std::uint64_t rows, int props, const std::vector<std::uint64_t>& words) {
+    Labels out(rows, props);
+    const int wpr = (props + 63) / 64;
+    for (std::uint64_t i = 0; i < rows; ++i)
+        for (int w = 0; w < wpr; ++w) {
+            std::uint64_t x = words[i * static_cast<std::uint64_t>(wpr) + static_cast<std::uint64_t>(w)];
+            while (x) {
+                const int b = __builtin_ctzll(x);
+                out.set(i, w * 64 + b);
+                x &= x - 1;
+            }
+        }
+    return out;
+}
+
+class Engine {
+public:
+    explicit Engine(const std::vector<int>& devices = {0}) {
+        check(ltlg_create(devices.data(), static_cast<int>(devices.size()), &ctx_), nullptr);
+    }
+    ~Engine() { ltlg_destroy(ctx_); }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    template <class Csr>
+    void load_abstraction(const Csr& m) {
+        check(ltlg_load_abstraction(ctx_, m.rows, m.cols, m.row_offsets.data(), m.col_indices.data()), ctx_);
+    }
+    void load_abstraction_file(const std::string& csb1_path) {
+        check(ltlg_load_abstraction_file(ctx_, csb1_path.c_str()), ctx_);
+    }
+    template <class Dense>
+    void submit(const Dense& p) {
+        const auto w = column_words(p);
+        check(ltlg_submit_grid(ctx_, p.cells(), p.num_props(), w.data(), 1), ctx_);
+    }
+    template <class Labels>
+    Labels labels(int frame = 0) {
+        ltlg_info info{};
+        check(ltlg_get_info(ctx_, &info), ctx_);
+        std::vector<std::uint64_t> words(info.rows * static_cast<std::uint64_t>(info.label_words));
+        check(ltlg_get_labels(ctx_, frame, words.empty() ? nullptr : words.data()), ctx_);
+        return to_label_matrix<Labels>(info.rows, info.props, words);
+    }
+    ltlg_ctx* handle() const { return ctx_; }
+
+private:
+    ltlg_ctx* ctx_ = nullptr;
+};
+
+// Drop-in for ltlgrid::label_all (label.cpp:150-189): same checks in the
+// reference's order (DensePropMatrix already enforced <= 64 props; then the
+// dimension check of label.cpp:151-154), same result bits.
+inline LabelMatrix label_all(const CsrBoolMatrix& m, const DensePropMatrix& p, int workers = 0) {
+    const auto w = column_words(p);
+    const int wpr = (p.num_props() + 63) / 64;
+    std::vector<std::uint64_t> words(m.rows * static_cast<std::uint64_t>(wpr));
+    const ltlg_status s =
+        ltlg_label_all(m.rows, m.cols, m.row_offsets.data(), m.col_indices.data(), p.cells(), p.num_props(),
+                       w.empty() ? nullptr : w.data(), workers, words.empty() ? nullptr : words.data());
+    if (s != LTLG_OK) throw_status(s, ltlg_last_error(nullptr));
+    return to_label_matrix<LabelMatrix>(m.rows, p.num_props(), words);
+}
+
+}  // namespace gpu
+}  // namespace ltlgrid

@@ -1,0 +1,95 @@
+// cpp_parity.cpp -- C++ parity driver (TEST INFRASTRUCTURE ONLY).
+//
+// Built by oracle/Makefile against the UNMODIFIED reference core and the
+// product's C++ shim (include/ltlgrid_gpu.hpp -> libltlgrid_gpu.so).  For the
+// reference's own test inputs (test_label.cpp:58-153) and seeded synthetic
+// scenes it runs ltlgrid::label_all (CPU, reference) and
+// ltlgrid::gpu::label_all (B200) and compares them with the reference's
+// LabelMatrix::operator== (label.hpp:79).  Needs a GPU to run; exits 0 iff
+// every case is bit-identical and the error behaviour matches.
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ltlgrid/label.hpp"
+#include "ltlgrid/rng.hpp"
+#include "ltlgrid_gpu.hpp"
+
+using namespace ltlgrid;
+
+static std::vector<OccupancyBitset> random_rows(SplitMix64& rng, std::uint64_t rows, std::uint64_t cols,
+                                                double density) {
+    std::vector<OccupancyBitset> out;
+    for (std::uint64_t i = 0; i < rows; ++i) {
+        OccupancyBitset r(cols);
+        for (std::uint64_t c = 0; c < cols; ++c)
+            if (rng.uniform() < density) r.set(c);
+        out.push_back(std::move(r));
+    }
+    return out;
+}
+
+static int failures = 0;
+static void expect(bool ok, const std::string& what) {
+    std::printf("%s %s\n", ok ? "ok  " : "FAIL", what.c_str());
+    if (!ok) ++failures;
+}
+
+int main() {
+    // Eq. 13 worked example (test_label.cpp:13-27, 87-99)
+    {
+        std::vector<OccupancyBitset> rows;
+        for (auto cols : std::vector<std::vector<int>>{{4}, {1, 2}, {0}, {2, 3}, {3}}) {
+            OccupancyBitset r(5);
+            for (int c : cols) r.set(static_cast<std::uint64_t>(c));
+            rows.push_back(r);
+        }
+        auto csr = to_csr(rows);
+        OccupancyBitset col(5);
+        col.set(4);
+        DensePropMatrix p(5, {col});
+        expect(gpu::label_all(csr, p) == label_all(csr, p), "eq13 x column{4}");
+        DensePropMatrix pz(5, {OccupancyBitset(5), OccupancyBitset(5)});
+        expect(gpu::label_all(csr, pz) == label_all(csr, pz), "eq13 x all-false");
+        bool threw = false;
+        try {
+            gpu::label_all(csr, DensePropMatrix(8, {OccupancyBitset(8)}));
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()) == "dimension mismatch: matrix cols 5 vs proposition rows 8";
+        }
+        expect(threw, "dimension mismatch -> std::invalid_argument, reference message");
+    }
+    // test_label.cpp:111-119 and :121-132
+    {
+        SplitMix64 rng(11);
+        auto rows = random_rows(rng, 1000, 4096, 1e-3);
+        auto cols = random_rows(rng, 3, 4096, 0.5);
+        auto csr = to_csr(rows);
+        DensePropMatrix p(4096, {cols[0], cols[1], cols[2]});
+        expect(gpu::label_all(csr, p) == label_all(csr, p), "seed 11: 1000x4096 @1e-3 x 3 @0.5");
+        SplitMix64 r2(77);
+        auto rows2 = random_rows(r2, 333, 1024, 0.01);
+        auto cols2 = random_rows(r2, 2, 1024, 0.4);
+        auto csr2 = to_csr(rows2);
+        DensePropMatrix p2(1024, {cols2[0], cols2[1]});
+        const auto ref = label_all(csr2, p2, 1);
+        for (int w : {1, 2, 5}) expect(gpu::label_all(csr2, p2, w) == ref, "seed 77 workers=" + std::to_string(w));
+    }
+    // resident engine across frames vs per-frame reference calls
+    {
+        SplitMix64 rng(2024);
+        auto rows = random_rows(rng, 700, 16384, 0.002);
+        auto csr = to_csr(rows);
+        gpu::Engine eng;
+        eng.load_abstraction(csr);
+        for (int f = 0; f < 5; ++f) {
+            auto cols = random_rows(rng, 20, 16384, 0.003 * (f + 1));
+            DensePropMatrix p(16384, cols);
+            eng.submit(p);
+            expect(eng.labels<LabelMatrix>() == label_all(csr, p), "engine frame " + std::to_string(f));
+        }
+    }
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
+    return failures ? 1 : 0;
+}

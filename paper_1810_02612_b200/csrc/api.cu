@@ -405,7 +405,10 @@ ltlg_status ltlg_create_ex(const int* devices, int n_devices, const ltlg_options
                 if ((e = cudaEventCreate(&ev)) != cudaSuccess) return cuda_fail(nullptr, e, "event");
         }
     }
-    if (n_devices > 1) {
+    bool distinct = true;  // a device listed twice = several shards on one GPU (tests, MIG-like splits)
+    for (int i = 0; i < n_devices; ++i)
+        for (int j = 0; j < i; ++j) distinct = distinct && devs[static_cast<size_t>(i)] != devs[static_cast<size_t>(j)];
+    if (n_devices > 1 && distinct) {
         Nccl& N = nccl();
         if (N.ok) {
             ctx->comms.resize(static_cast<size_t>(n_devices));

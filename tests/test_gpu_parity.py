@@ -306,3 +306,41 @@ def test_empty_and_degenerate():
     eng.submit_grid(64, 0, np.zeros(0, np.uint64), 2)
     assert eng.get_labels(1) == LabelMatrix(4, 0)
     eng.close()
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0], [0, 0, 0, 0, 0]])
+def test_sharded_engine_on_one_device(devices):
+    # several shards on one GPU exercise the multi-device code path (row
+    # sharding, P broadcast, per-shard labels, assembly) without NCCL.
+    depth, E, props, F = 14, 30_000, 12, 5
+    prm = SyntheticPRM(seed=9, depth=depth)
+    t = prm.words(0, E)
+    off, idx = prm.csr(0, E)
+    P = props_words(13, depth, props, 0, F)
+    eng = LabelEngine(devices=devices)
+    eng.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
+    eng.submit_grid(1 << depth, props, P, F)
+    packed = eng.get_labels_packed()
+    spans = [eng.device_labels(s)[1:3] for s in range(len(devices))]
+    assert spans[0][0] == 0 and spans[-1][1] == E
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    for f in range(F):
+        want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[f])
+        assert eng.get_labels(f) == LabelMatrix(E, props, want)
+        assert np.array_equal(packed[:, f].astype(np.uint64), want)
+    eng.submit_grid(1 << depth, props, P[2], 1)  # single-frame kernel on every shard
+    want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[2])
+    assert eng.get_labels(0) == LabelMatrix(E, props, want)
+    eng.close()
+
+
+def test_cpp_drop_in_parity():
+    # the reference core and include/ltlgrid_gpu.hpp compiled into one binary
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(GOLDEN), "..", "oracle", "_ref", "cpp_parity")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/cpp_parity not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASSED" in r.stdout
