@@ -90,7 +90,7 @@ struct Shard {
     cudaEvent_t* ev = nullptr;      // the quadruple of the current submit
     uint64_t row_begin = 0, row_end = 0, n_pairs = 0, words = 0;
     uint32_t ntask_stream = 0, ntask_batch = 0;
-    DevBuf<Pair> pairs;
+    DevBuf<Pair> pairs, pairs_s;  // plain (multi-frame) and single-frame layouts
     DevBuf<uint32_t> perm, trow_s, trow_b;
     DevBuf<uint64_t> tpair_s, tpair_b;
     DevBuf<uint64_t> P;  // frames x props x nw64
@@ -102,8 +102,7 @@ struct Shard {
     DevBuf<uint64_t> world;
     DevBuf<uint8_t> poses;
     DevBuf<uint32_t> ctr;  // persistent-kernel task counter
-    DevBuf<uint8_t> s_only;  // S-only summary of multi-frame submits
-    DevBuf<uint8_t> split;   // single-frame shared-memory split table
+    DevBuf<uint8_t> s_only;  // S mask per (word, frame)
     bool have_times = false;
     uint64_t rows() const { return row_end - row_begin; }
 };
@@ -171,12 +170,13 @@ ltlg_status upload_shard(ltlg_ctx* ctx, Shard& s, const PackedShard& p) {
     };
     ltlg_status st;
     if ((st = put(s.pairs, p.pairs, "upload T pairs")) != LTLG_OK) return st;
+    if ((st = put(s.pairs_s, p.pairs_stream, "upload T pairs")) != LTLG_OK) return st;
     if ((st = put(s.perm, p.perm, "upload row permutation")) != LTLG_OK) return st;
     if ((st = put(s.trow_s, p.task_row_stream, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.tpair_s, p.task_pair_stream, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.trow_b, p.task_row_batch, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.tpair_b, p.task_pair_batch, "upload tasks")) != LTLG_OK) return st;
-    ctx->t_bytes += p.pairs.size() * sizeof(Pair) + p.perm.size() * 4;
+    ctx->t_bytes += (p.pairs.size() + p.pairs_stream.size()) * sizeof(Pair) + p.perm.size() * 4;
     return LTLG_OK;
 }
 
@@ -277,17 +277,15 @@ ltlg_status run_label(ltlg_ctx* ctx) {
             s.have_times = false;
             continue;
         }
-        CK(s.sf.reserve(static_cast<size_t>(nw32 + 1) * frames * summary_entry_bytes(props)), "allocate summary");
+        CK(s.sf.reserve(frames == 1 && props <= 32 ? split_table_bytes(props, nw32)
+                                                   : static_cast<size_t>(nw32 + 1) * frames * summary_entry_bytes(props)),
+           "allocate summary");
         CK(s.ctr.reserve(64), "allocate task counter");
-        if (frames > 1)
-            CK(s.s_only.reserve(static_cast<size_t>(nw32 + 1) * frames * (props <= 32 ? 4 : 8)), "allocate summary");
-        const bool use_split = frames == 1 && stream_table_mode(props, nw32) >= 4;
-        if (use_split) CK(s.split.reserve(split_table_bytes(props, nw32)), "allocate summary");
+        CK(s.s_only.reserve(static_cast<size_t>(nw32 + 1) * frames * s_only_bytes(props)), "allocate summary");
         const bool prof = ctx->opts.profile != 0;
         if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
         CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
-                          frames > 1 ? s.s_only.ptr : nullptr, s.ctr.ptr, use_split ? s.split.ptr : nullptr,
-                          s.stream),
+                          s.s_only.ptr, s.ctr.ptr, s.stream),
            "summary kernel");
         if (prof) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
@@ -302,8 +300,8 @@ ltlg_status run_label(ltlg_ctx* ctx) {
         a.label_bytes = ctx->label_bytes;
         a.task_ctr = s.ctr.ptr;
         a.s_only = s.s_only.ptr;
-        a.split = s.split.ptr;
         if (frames == 1) {
+            a.pairs = s.pairs_s.ptr;
             a.task_pair = s.tpair_s.ptr;
             a.task_row = s.trow_s.ptr;
             a.ntasks = s.ntask_stream;
@@ -444,6 +442,7 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         cudaSetDevice(s.device);
         if (s.stream) cudaStreamSynchronize(s.stream);
         s.pairs.release();
+        s.pairs_s.release();
         s.perm.release();
         s.trow_s.release();
         s.trow_b.release();
@@ -457,7 +456,6 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.poses.release();
         s.ctr.release();
         s.s_only.release();
-        s.split.release();
         for (auto& ev : s.ring)
             if (ev) cudaEventDestroy(ev);
         if (s.stream) cudaStreamDestroy(s.stream);

@@ -38,6 +38,7 @@ struct PackedShard {
     uint64_t row_begin = 0, row_end = 0;  // original rows [row_begin, row_end)
     uint64_t words = 0;                   // W32 of the shard
     std::vector<Pair> pairs;              // sorted-row order, padded (see kPairPad)
+    std::vector<Pair> pairs_stream;       // the same pairs in the single-frame layout (see kStreamK)
     uint64_t n_pairs = 0;                 // meaningful pairs (incl. sentinels)
     std::vector<uint32_t> perm;           // sorted position -> local original row
     // warp tasks: [row_begin, row_end) in sorted positions, pairs [pair_begin, pair_end)
@@ -46,6 +47,17 @@ struct PackedShard {
 };
 
 constexpr uint64_t kPairPad = 512;  // tail padding so vector loads never leave the array
+
+// Single-frame layout.  The stream kernel gives each lane kStreamK consecutive
+// pairs of a warp chunk of 32*kStreamK pairs and reads them as 16-byte pieces.
+// So that those reads are coalesced (one 512-byte run per warp instruction
+// instead of 32 pieces at a 64-byte lane stride), every FULL chunk of a stream
+// task is stored piece-transposed: the piece holding pairs (K*l + 2h,
+// K*l + 2h + 1) of the chunk sits at piece h*32 + l.  A task's last, partial
+// chunk stays in plain order.  Tasks start on 16-byte boundaries (a task with
+// an odd pair count gets one no-op pair appended).
+constexpr int kStreamK = 8;
+constexpr uint64_t kStreamCH = 32 * kStreamK;
 
 // Host-side loader (loader.cpp).
 bool validate_csr(uint64_t rows, uint64_t cols, const uint64_t* offsets, uint64_t n_offsets,

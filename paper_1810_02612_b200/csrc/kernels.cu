@@ -7,21 +7,33 @@
 //
 //   hit_j(w, m) = (m & P_j[w]) != 0.
 //
-// A per-frame summary of P makes that test mostly table-driven:
+// A per-frame summary of P makes that test table-driven:
 //   S[w] bit j = P_j[w] != 0           (some cell of the word is set)
 //   F[w] bit j = P_j[w] covers the word (every valid cell of the word is set)
 // Since every stored mask is non-zero, F[w] props hit unconditionally, props
 // outside S[w] never hit, and only the "partial" props S & ~F need the exact
-// (m & P_j[w]) probe -- this is exact, not a heuristic.  For the bench
-// archetypes (a 90%-occupancy lane complement and 1.5%-occupancy boxes) the
-// partial set is empty for most (pair, frame) visits.
+// (m & P_j[w]) probe -- this is exact, not a heuristic.
+//
+// Summary entry of one (word, frame), 16 bytes, branch-free to evaluate:
+//   FMT 16 (props <= 16): {F | over<<31, Pa, Pb, Abit | Bbit<<16}
+//   FMT 32 (props <= 32): {F,            Pa, Pb, ia | ib<<8 | over<<16}
+//   (Pa, Pb = P words of the two lowest partial props a < b, 0 when absent;
+//    Abit/Bbit = their prop bits, ia/ib their indices; over = a third
+//    partial prop exists -> exact gather of P, rare)
+//   FMT 64 (props <= 64): SF<u64> {S, F, Pa, Pb} (32 bytes, pair_hits).
+// Evaluating an entry for mask m:  v = F | (m&Pa ? A : 0) | (m&Pb ? B : 0).
+// FMT 16 leaves flag/Bbit garbage in bits 16..31 of v; labels of <= 16 props
+// are stored as u8/u16, so the store truncates it away.
+// The S masks are also written on their own (s_only): the over path needs S,
+// and the multi-frame kernel uses it for full-mask pairs (hits == S).
 //
 // Kernels:
-//   summary_kernel       P columns -> {S, F} per (word, frame)
-//   label_stream_kernel  single frame; lanes own 4 consecutive pairs each, rows
+//   summary_kernel       P columns -> entries + S per (word, frame)
+//   label_stream_kernel  single frame; lanes own K consecutive pairs each, rows
 //                        are recovered with a warp-wide segmented OR scan over
-//                        head flags (T is streamed once with 2x16-byte
-//                        L1::no_allocate loads; HBM-bound)
+//                        head flags (T is streamed once with coalesced 16-byte
+//                        L1::no_allocate loads from its own row-order copy;
+//                        HBM-bound)
 //   label_batch_kernel   F frames; lanes own frames, pairs are broadcast by
 //                        shuffle, each T pair is read from HBM once for all F
 //   extract_kernel       one frame of the packed labels -> LabelMatrix u64 words
@@ -36,12 +48,6 @@
 
 namespace ltlg {
 
-// Summary entry of one (32-bit word, frame):
-//   s, f  : the S / F prop masks above
-//   pa, pb: the P words (valid bits only) of the two lowest "partial" props
-//           (s & ~f), 0 when absent -- so the exact probe of up to two partial
-//           props is branch-free and needs no dependent gather.  Partial
-//           props beyond the second fall back to a gather of P (rare).
 template <typename LW>
 struct alignas(16) SF {
     LW s;
@@ -49,6 +55,41 @@ struct alignas(16) SF {
     uint32_t pa;
     uint32_t pb;
 };
+
+template <int FMT>
+struct Fmt {
+    using LW = uint32_t;
+    using E = uint4;
+};
+template <>
+struct Fmt<64> {
+    using LW = uint64_t;
+    using E = SF<uint64_t>;
+};
+
+constexpr uint32_t kOver16 = 0x80000000u;
+constexpr uint32_t kOver32 = 0x10000u;
+
+int entry_format(int props) { return props <= 16 ? 16 : props <= 32 ? 32 : 64; }
+size_t summary_entry_bytes(int props) { return props <= 32 ? sizeof(uint4) : sizeof(SF<uint64_t>); }
+size_t s_only_bytes(int props) { return props <= 32 ? 4 : 8; }
+
+// Single-frame split table (FMT 16/32): M[w] (4 B: (16+ia) | (16+ib)<<5 |
+// partial<<10 | over<<11 | F<<16 for <= 16 props -- the labels accumulate in
+// the high half and are shifted down once per stored row; 8 B: {F, ia |
+// ib<<8 | partial<<16 | over<<17} for <= 32) followed, 16-byte aligned, by
+// X[w] = {Pa, Pb}.  Every
+// pair reads M; only lanes whose word has a partial prop read X, so the
+// random shared-memory gathers cost ~1.5 wavefronts per pair instead of the
+// ~11 of a 16-byte entry.
+__host__ __device__ __forceinline__ uint32_t split_x_offset(int fmt, uint32_t nw32) {
+    return ((fmt == 16 ? 4u : 8u) * (nw32 + 1) + 15u) & ~15u;
+}
+size_t split_table_bytes(int props, uint32_t nw32) {
+    const int fmt = entry_format(props);
+    if (fmt == 64) return 0;
+    return split_x_offset(fmt, nw32) + ((8u * (nw32 + 1) + 15u) & ~15u);
+}
 
 __device__ __forceinline__ uint4 ld_stream16(const void* p) {
     uint4 r;
@@ -64,17 +105,8 @@ __device__ __forceinline__ uint2 ld_stream8(const void* p) {
     return r;
 }
 
-template <typename LW>
-__device__ __forceinline__ SF<LW> ld_sf(const SF<LW>* p);
-
-template <>
-__device__ __forceinline__ SF<uint32_t> ld_sf<uint32_t>(const SF<uint32_t>* p) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
-    return SF<uint32_t>{v.x, v.y, v.z, v.w};
-}
-
-template <>
-__device__ __forceinline__ SF<uint64_t> ld_sf<uint64_t>(const SF<uint64_t>* p) {
+__device__ __forceinline__ uint4 ld_entry(const uint4* p) { return __ldg(p); }
+__device__ __forceinline__ SF<uint64_t> ld_entry(const SF<uint64_t>* p) {
     const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
     const uint2 w = __ldg(reinterpret_cast<const uint2*>(p) + 2);
     return SF<uint64_t>{v.x, v.y, w.x, w.y};
@@ -92,22 +124,13 @@ __device__ __forceinline__ LW shfl_idx(LW v, int l) {
     return __shfl_sync(0xffffffffu, v, l);
 }
 
-// Label contribution of one stored pair (mask m of word w) for one frame.
-//   e    : the frame's summary entry of word w
-//   skip : props already known to hit (their probes are unnecessary)
-//   col0 : the frame's P column 0 (u32 view); column j starts at col0 + j*nw32
+// Exact probe of the props in `over` (bit j = prop j) for mask m of word w:
+// gather P_j[w].  col0 = the frame's P column 0 (u32 view).
 template <typename LW>
-__device__ __forceinline__ LW pair_hits(uint32_t m, uint32_t w, const SF<LW>& e, LW skip,
-                                        const uint32_t* __restrict__ col0, uint32_t nw32) {
-    const LW partial = e.s & ~e.f;
-    const LW abit = partial & (~partial + 1);
-    const LW rest = partial ^ abit;
-    const LW bbit = rest & (~rest + 1);
-    LW v = e.f;
-    v |= (m & e.pa) ? abit : LW(0);
-    v |= (m & e.pb) ? bbit : LW(0);
-    LW over = (rest ^ bbit) & ~skip;
-    while (over) {  // a third partial prop at this word/frame: exact probe
+__device__ __forceinline__ LW probe_gather(uint32_t m, uint32_t w, LW over, const uint32_t* __restrict__ col0,
+                                        uint32_t nw32) {
+    LW v = 0;
+    while (over) {
         const int j = lowest_bit(over);
         if (m & __ldg(col0 + static_cast<uint64_t>(j) * nw32 + w)) v |= LW(1) << j;
         over &= over - 1;
@@ -115,23 +138,63 @@ __device__ __forceinline__ LW pair_hits(uint32_t m, uint32_t w, const SF<LW>& e,
     return v;
 }
 
+// Label contribution of one stored pair (mask m of word w) for one frame.
+//   e    : the frame's summary entry of word w
+//   sp   : the frame's S mask of word w (read only on the rare over path)
+//   skip : props already known to hit (their probes are unnecessary)
+template <int FMT>
+__device__ __forceinline__ typename Fmt<FMT>::LW probe(const typename Fmt<FMT>::E& e, uint32_t m, uint32_t w,
+                                                       const typename Fmt<FMT>::LW* sp,
+                                                       typename Fmt<FMT>::LW skip,
+                                                       const uint32_t* __restrict__ col0, uint32_t nw32) {
+    if constexpr (FMT == 16) {
+        uint32_t v = e.x;
+        if (m & e.y) v |= e.w;
+        if (m & e.z) v |= e.w >> 16;
+        if (e.x & kOver16) {
+            const uint32_t known = (e.x | e.w | (e.w >> 16)) & 0xffffu;
+            v |= probe_gather<uint32_t>(m, w, __ldg(sp) & ~known & ~skip, col0, nw32);
+        }
+        return v;
+    } else if constexpr (FMT == 32) {
+        const uint32_t abit = __funnelshift_l(0u, 1u, e.w);
+        const uint32_t bbit = __funnelshift_l(0u, 1u, e.w >> 8);
+        uint32_t v = e.x;
+        if (m & e.y) v |= abit;
+        if (m & e.z) v |= bbit;
+        if (e.w & kOver32) v |= probe_gather<uint32_t>(m, w, __ldg(sp) & ~(e.x | abit | bbit | skip), col0, nw32);
+        return v;
+    } else {
+        (void)sp;
+        const uint64_t partial = e.s & ~e.f;
+        const uint64_t abit = partial & (~partial + 1);
+        const uint64_t rest = partial ^ abit;
+        const uint64_t bbit = rest & (~rest + 1);
+        uint64_t v = e.f;
+        if (m & e.pa) v |= abit;
+        if (m & e.pb) v |= bbit;
+        const uint64_t over = (rest ^ bbit) & ~skip;
+        if (over) v |= probe_gather<uint64_t>(m, w, over, col0, nw32);
+        return v;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Summary build: thread per (word, frame).  P32 = frames x props x nw32 u32.
-// Output layout sf[w * frames + f]; entry nw32 of every frame is the all-zero
-// sentinel that empty rows point at.
+// Output index w * frames + f; entry nw32 of every frame is the all-zero
+// sentinel that empty rows and neutralised pairs point at.
 // ---------------------------------------------------------------------------
-template <typename LW>
+template <int FMT, bool SPLIT>
 __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict__ P32, int props, int frames,
-                                                      uint32_t nw32, uint64_t cells,
-                                                      SF<LW>* __restrict__ sf, LW* __restrict__ s_only,
-                                                      uint32_t* __restrict__ task_ctr, uint8_t* __restrict__ split,
-                                                      int split_mb) {
+                                                      uint32_t nw32, uint64_t cells, void* __restrict__ tab,
+                                                      void* __restrict__ s_only, uint32_t* __restrict__ task_ctr) {
+    using LW = typename Fmt<FMT>::LW;
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     const int f = blockIdx.y;
     if (w == 0 && f == 0) *task_ctr = 0;  // the labeling kernel that follows pulls tasks from 0
     if (w > nw32) return;
     LW s = 0, full = 0;
-    uint32_t pa = 0, pb = 0;
+    uint32_t pa = 0, pb = 0, ia = 0, ib = 0;
     int np = 0;
     const uint64_t lo = static_cast<uint64_t>(w) * 32;
     if (w < nw32 && lo < cells) {
@@ -143,20 +206,39 @@ __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict
             s |= LW(x != 0) << j;
             full |= LW(x == valid) << j;
             if (x != 0 && x != valid) {
-                if (np == 0) pa = x;
-                else if (np == 1) pb = x;
+                if (np == 0) {
+                    pa = x;
+                    ia = static_cast<uint32_t>(j);
+                } else if (np == 1) {
+                    pb = x;
+                    ib = static_cast<uint32_t>(j);
+                }
                 ++np;
             }
         }
     }
-    sf[static_cast<uint64_t>(w) * frames + f] = SF<LW>{s, full, pa, pb};
-    if (s_only) s_only[static_cast<uint64_t>(w) * frames + f] = s;
-    if (split) {  // single frame, shared-memory split layout: M[w] then X[w] = {pa, pb}
-        if (split_mb == 4) reinterpret_cast<uint32_t*>(split)[w] = static_cast<uint32_t>(s) | (static_cast<uint32_t>(full) << 16);
-        else reinterpret_cast<uint2*>(split)[w] = make_uint2(static_cast<uint32_t>(s), static_cast<uint32_t>(full));
-        const uint32_t xoff = (static_cast<uint32_t>(split_mb) * (nw32 + 1) + 15u) & ~15u;
-        reinterpret_cast<uint2*>(split + xoff)[w] = make_uint2(pa, pb);
+    const uint64_t idx = static_cast<uint64_t>(w) * frames + f;
+    const uint32_t over = np > 2 ? 1u : 0u;
+    if constexpr (SPLIT) {  // single frame: the stream kernel's M / X tables (see split_table_bytes)
+        static_assert(FMT != 64, "split tables hold <= 32 props");
+        const uint32_t part = np > 0 ? 1u : 0u;
+        uint8_t* base = static_cast<uint8_t*>(tab);
+        if constexpr (FMT == 16)  // F in the high half: the probe bits are 1 << (16 + ia) straight from M
+            reinterpret_cast<uint32_t*>(base)[w] =
+                (static_cast<uint32_t>(full) << 16) | (16u + ia) | ((16u + ib) << 5) | (part << 10) | (over << 11);
+        else
+            reinterpret_cast<uint2*>(base)[w] =
+                make_uint2(static_cast<uint32_t>(full), ia | (ib << 8) | (part << 16) | (over << 17));
+        reinterpret_cast<uint2*>(base + split_x_offset(FMT, nw32))[w] = make_uint2(pa, pb);
+    } else if constexpr (FMT == 16) {
+        const uint32_t ab = (np > 0 ? 1u << ia : 0u) | (np > 1 ? (1u << ib) << 16 : 0u);
+        static_cast<uint4*>(tab)[idx] = make_uint4(static_cast<uint32_t>(full) | (over << 31), pa, pb, ab);
+    } else if constexpr (FMT == 32) {
+        static_cast<uint4*>(tab)[idx] = make_uint4(static_cast<uint32_t>(full), pa, pb, ia | (ib << 8) | (over << 16));
+    } else {
+        static_cast<SF<uint64_t>*>(tab)[idx] = SF<uint64_t>{s, full, pa, pb};
     }
+    static_cast<LW*>(s_only)[idx] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -178,6 +260,38 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// HEAD flag (bit 31) of a pair's word field as 0/1, on the FMA pipe (the
+// ALU pipe is the single-frame kernel's bottleneck): hi32(wh * 2).
+__device__ __forceinline__ uint32_t head_bit(uint32_t wh) {
+    uint32_t r;
+    asm("mul.hi.u32 %0, %1, 2;" : "=r"(r) : "r"(wh));
+    return r;
+}
+// acc + b * 2^k on the FMA pipe
+__device__ __forceinline__ uint32_t mad_pow2(uint32_t b, uint32_t pow2, uint32_t acc) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(pow2), "r"(acc));
+    return r;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+    uint2 v;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+// {x, y} = smem[a] if c != 0, else unchanged (callers pre-zero)
+__device__ __forceinline__ void lds64_if(uint32_t c, uint32_t a, uint32_t& x, uint32_t& y) {
+    asm("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.v2.u32 {%0, %1}, [%3];\n}\n"
+        : "+r"(x), "+r"(y)
+        : "r"(c), "r"(a));
+}
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     // bounded: a bulk copy that can never complete traps instead of hanging the GPU
     for (uint32_t spin = 0;; ++spin) {
@@ -194,179 +308,472 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 // ---------------------------------------------------------------------------
 // Single frame.  Persistent: warps pull tasks (runs of whole rows, pairs
-// [p0, p1)) from an atomic counter.  With TAB_SMEM the frame's summary table
-// is TMA-bulk-copied once per CTA into shared memory (one CTA of 32 warps per
-// SM), so the per-pair gathers hit shared-memory banks instead of L1 tags.
+// [p0, p1)) from an atomic counter.  The frame's split table (M / X) is
+// TMA-bulk-copied once per CTA into shared memory when it fits (one CTA of
+// 32 warps per SM), else read through L1.
+//
+// A warp chunk is 32*K consecutive pairs, lane l owning pairs [K*l, K*l+K).
+// Row recovery: HEAD flags mark each row's first pair.  When every lane holds
+// at most one head (rows longer than K pairs -- the common case), a lane's
+// pairs split into `pre` (before its head: the row open from lower lanes)
+// and `post` (from its head on), computed with predicated ORs; the head
+// count prefix is one ballot, and the rows spanning lanes are closed by one
+// warp-wide segmented OR scan.  Chunks where some lane holds several heads
+// (short rows) take the general lane-local loop.
 // ---------------------------------------------------------------------------
-template <typename LW, typename SW, int TAB, int K>
-__global__ void __launch_bounds__(TAB ? 1024 : 256)
+
+// Per-kernel constants of the single-frame chunk processing.
+template <int FMT, typename SW, bool SMEM>
+struct StreamCtx {
+    using LW = typename Fmt<FMT>::LW;
+    using E = typename Fmt<FMT>::E;
+    static constexpr int kShift = FMT == 16 ? 16 : 0;  // label bits sit at [kShift, kShift + props) of v
+    const uint8_t* tab;     // split table (smem or global) / SF<u64> entries (FMT 64)
+    const uint8_t* xbytes;  // X part of the split table
+    uint32_t tab_s, x_s;    // the same as shared-memory addresses (SMEM)
+    const LW* s_only;
+    const uint32_t* P32;
+    uint32_t nw32;
+    SW* out;
+    int lane;
+    uint32_t lt, le;
+};
+
+// The row being assembled across chunks of one task.
+template <typename LW>
+struct RowState {
+    int32_t r0, r1;      // the task's rows [r0, r1): only these are stored
+    int32_t open_row;    // row owning `carry`
+    LW carry;
+};
+
+// One warp chunk held in cur (lane-contiguous K pairs).  `reload(h0, h1)` is
+// called once pieces [h0, h1) of cur are no longer needed (after each half),
+// so a caller can prefetch the next chunk in place.
+template <int FMT, typename SW, bool SMEM, int K, typename Reload>
+__device__ __forceinline__ void stream_chunk(const StreamCtx<FMT, SW, SMEM>& sc,
+                                             RowState<typename Fmt<FMT>::LW>& rs, uint4 (&cur)[K / 2],
+                                             Reload&& reload) {
+    using LW = typename Fmt<FMT>::LW;
+    using E = typename Fmt<FMT>::E;
+    constexpr int kShift = StreamCtx<FMT, SW, SMEM>::kShift;
+    const int lane = sc.lane;
+    uint32_t heads = 0;  // bit k: pair k opens a row
+    LW v[K];
+    if constexpr (FMT == 64) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint32_t mk = (k & 1) ? cur[k / 2].z : cur[k / 2].x;
+            const uint32_t wh = (k & 1) ? cur[k / 2].w : cur[k / 2].y;
+            heads |= (wh >> 31) << k;
+            const uint32_t w = wh & kWordMask;
+            v[k] = probe<FMT>(ld_entry(reinterpret_cast<const E*>(sc.tab) + w), mk, w, sc.s_only + w, LW(0), sc.P32,
+                              sc.nw32);
+            if (k == K / 2 - 1) reload(0, K / 4);
+        }
+        reload(K / 4, K / 2);
+    } else {
+        const uint32_t* mtab16 = reinterpret_cast<const uint32_t*>(sc.tab);
+        const uint2* mtab32 = reinterpret_cast<const uint2*>(sc.tab);
+        const uint2* xtab = reinterpret_cast<const uint2*>(sc.xbytes);
+        // straight-line per half: M gathers, predicated X gathers, probes;
+        // the rare third-partial-prop fix-up runs after each half
+        auto look = [&](int k, uint32_t& over) {
+            const uint32_t mk = (k & 1) ? cur[k / 2].z : cur[k / 2].x;
+            const uint32_t wh = (k & 1) ? cur[k / 2].w : cur[k / 2].y;
+            heads = mad_pow2(head_bit(wh), 1u << k, heads);
+            if constexpr (FMT == 16) {
+                // byte offsets straight from the pair's word field: the HEAD
+                // bit (31) shifts out (shared-memory tables are small); X is
+                // gathered only by lanes whose word has a partial prop (an
+                // unconditional gather saves ALU work but saturates the
+                // shared-memory pipe)
+                uint32_t mw;
+                uint2 x = make_uint2(0u, 0u);
+                if constexpr (SMEM) {
+                    mw = lds32(sc.tab_s + (wh << 2));
+                    lds64_if(mw & (1u << 10), sc.x_s + (wh << 3), x.x, x.y);
+                } else {
+                    mw = mtab16[wh & kWordMask];
+                    if (mw & (1u << 10)) x = xtab[wh & kWordMask];
+                }
+                uint32_t vv = mw;  // F<<16; bits < 16 are index/flag garbage, shifted out at the store
+                if (mk & x.x) vv |= __funnelshift_l(0u, 1u, mw);
+                if (mk & x.y) vv |= __funnelshift_l(0u, 1u, mw >> 5);
+                over |= mw & (1u << 11);
+                v[k] = vv;
+            } else {
+                const uint32_t w = wh & kWordMask;
+                const uint2 mw = mtab32[w];
+                uint2 x = make_uint2(0u, 0u);
+                if (mw.y & 0x10000u) x = xtab[w];
+                uint32_t vv = mw.x;
+                if (mk & x.x) vv |= __funnelshift_l(0u, 1u, mw.y);
+                if (mk & x.y) vv |= __funnelshift_l(0u, 1u, mw.y >> 8);
+                over |= mw.y & 0x20000u;
+                v[k] = vv;
+            }
+        };
+        auto fix = [&](int k) {  // a word with >= 3 partial props: exact gather of the rest
+            const uint32_t mk = (k & 1) ? cur[k / 2].z : cur[k / 2].x;
+            const uint32_t w = ((k & 1) ? cur[k / 2].w : cur[k / 2].y) & kWordMask;
+            uint32_t known, ov;
+            if constexpr (FMT == 16) {
+                const uint32_t mw = mtab16[w];
+                known = (mw >> 16) | (1u << ((mw & 31) - 16)) | (1u << ((mw >> 5 & 31) - 16));
+                ov = mw >> 11 & 1u;
+            } else {
+                const uint2 mw = mtab32[w];
+                known = mw.x | (1u << (mw.y & 31)) | (1u << (mw.y >> 8 & 31));
+                ov = mw.y >> 17 & 1u;
+            }
+            if (ov) v[k] |= probe_gather<uint32_t>(mk, w, sc.s_only[w] & ~known, sc.P32, sc.nw32) << kShift;
+        };
+        uint32_t ov_lo = 0, ov_hi = 0;
+#pragma unroll
+        for (int k = 0; k < K / 2; ++k) look(k, ov_lo);
+        if (ov_lo) {
+#pragma unroll
+            for (int k = 0; k < K / 2; ++k) fix(k);
+        }
+        reload(0, K / 4);
+#pragma unroll
+        for (int k = K / 2; k < K; ++k) look(k, ov_hi);
+        if (ov_hi) {
+#pragma unroll
+            for (int k = K / 2; k < K; ++k) fix(k);
+        }
+        reload(K / 4, K / 2);
+    }
+    SW* out = sc.out;
+    if (!__any_sync(0xffffffffu, (heads & (heads - 1)) != 0)) {
+        // ---- fast path: every lane holds at most one head ----------
+        const uint32_t hmask_all = __ballot_sync(0xffffffffu, heads != 0);
+        const int hb = __popc(hmask_all & sc.lt);  // rows opened in lower lanes
+        LW pre = 0, post = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if ((heads & ((2u << k) - 1u)) == 0) pre |= v[k];
+            else post |= v[k];
+        }
+        const uint32_t hm = hmask_all & sc.le;
+        const int seg = hm ? 31 - __clz(hm) : 0;
+        LW x = heads ? post : pre;
+        if (lane == 0 && !heads) x |= rs.carry;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const LW y = shfl_up(x, d);
+            if (lane - d >= seg) x |= y;
+        }
+        LW excl = shfl_up(x, 1);
+        if (lane == 0) excl = rs.carry;
+        if (heads) {
+            const int32_t row = rs.open_row + hb;  // the row open before this lane's head
+            if (row >= rs.r0 && row < rs.r1) out[row] = static_cast<SW>((excl | pre) >> kShift);
+        }
+        rs.carry = shfl_idx(x, 31);
+        rs.open_row += __popc(hmask_all);
+    } else {
+        // ---- general path: lanes may hold several heads -----------
+        const int nh = __popc(heads);
+        int incl = nh;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += y;
+        }
+        const int hb = incl - nh;
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        // lane-local segmentation: rows that start and end inside this lane
+        LW pre = 0, cur_or = 0;
+        int seen = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (heads >> k & 1u) {
+                if (seen) {
+                    const int32_t row = rs.open_row + hb + seen;
+                    if (row < rs.r1) out[row] = static_cast<SW>(cur_or >> kShift);
+                } else {
+                    pre = cur_or;
+                }
+                ++seen;
+                cur_or = 0;
+            }
+            cur_or |= v[k];
+        }
+        if (!nh) pre = cur_or;
+        const uint32_t hmask = __ballot_sync(0xffffffffu, nh > 0) & sc.le;
+        const int seg = hmask ? 31 - __clz(hmask) : 0;
+        LW x = nh ? cur_or : pre;
+        if (lane == 0 && !nh) x |= rs.carry;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const LW y = shfl_up(x, d);
+            if (lane - d >= seg) x |= y;
+        }
+        LW excl = shfl_up(x, 1);
+        if (lane == 0) excl = rs.carry;
+        if (nh) {
+            const int32_t row = rs.open_row + hb;  // the row open before this lane's first head
+            if (row >= rs.r0 && row < rs.r1) out[row] = static_cast<SW>((excl | pre) >> kShift);
+        }
+        rs.carry = shfl_idx(x, 31);
+        rs.open_row += tot;
+    }
+}
+
+template <int FMT, typename SW, bool SMEM>
+__device__ __forceinline__ void stream_close_task(const StreamCtx<FMT, SW, SMEM>& sc,
+                                                  const RowState<typename Fmt<FMT>::LW>& rs) {
+    if (sc.lane == 0 && rs.open_row >= rs.r0 && rs.open_row < rs.r1)
+        sc.out[rs.open_row] = static_cast<SW>(rs.carry >> StreamCtx<FMT, SW, SMEM>::kShift);
+}
+
+// Copies the split table into shared memory (thread 0 issues, all wait later).
+__device__ __forceinline__ void stage_table(uint8_t* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_expect_tx(bar, bytes);
+        for (uint32_t o = 0; o < bytes; o += 32768u) {
+            const uint32_t n = bytes - o < 32768u ? bytes - o : 32768u;
+            bulk_g2s(dst + o, static_cast<const uint8_t*>(src) + o, n, bar);
+        }
+    }
+    __syncthreads();
+}
+
+// Register-prefetch variant (tables in L1 / 64-prop entries, or A/B runs):
+// the next chunk is loaded in place (IP) half by half, or double-buffered.
+template <int FMT, typename SW, bool SMEM, int K, int NT, bool IP>
+__global__ void __launch_bounds__(NT)
     label_stream_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
                         const uint32_t* __restrict__ task_row, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
-                        const SF<LW>* __restrict__ sf, uint32_t tab_bytes, const uint32_t* __restrict__ P32,
-                        uint32_t nw32, const uint32_t* __restrict__ perm, SW* __restrict__ out) {
-    constexpr uint32_t CH = 32 * K;         // pairs per warp chunk
+                        const void* __restrict__ tab_g, uint32_t tab_bytes, const void* __restrict__ s_only_g,
+                        const uint32_t* __restrict__ P32, uint32_t nw32, SW* __restrict__ out) {
+    using LW = typename Fmt<FMT>::LW;
+    static_assert(!(SMEM && FMT == 64), "the 64-prop entry table is read through L1");
+    static_assert(K == kStreamK, "the HBM chunk layout is built for kStreamK pairs per lane");
+    constexpr uint32_t CH = 32 * K;  // pairs per warp chunk
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ uint64_t tab_bar;
     const int lane = threadIdx.x & 31;
-    const SF<LW>* tab = sf;
-    constexpr bool TAB_SMEM = TAB != 0;
-    constexpr bool SPLIT = TAB == 4 || TAB == 8;
-    const uint8_t* xtab = nullptr;  // split mode: {Pa, Pb} table after the M table
-    if constexpr (TAB_SMEM) {
-        if (threadIdx.x == 0) {
-            mbar_init(&tab_bar, 1);
-            mbar_expect_tx(&tab_bar, tab_bytes);
-            for (uint32_t o = 0; o < tab_bytes; o += 32768u) {
-                const uint32_t n = tab_bytes - o < 32768u ? tab_bytes - o : 32768u;
-                bulk_g2s(smem_raw + o, reinterpret_cast<const uint8_t*>(sf) + o, n, &tab_bar);
-            }
-        }
-        __syncthreads();
-        tab = reinterpret_cast<const SF<LW>*>(smem_raw);
-        if constexpr (SPLIT) xtab = smem_raw + ((static_cast<uint32_t>(TAB) * (nw32 + 1) + 15u) & ~15u);
+    const uint8_t* tab = static_cast<const uint8_t*>(tab_g);
+    if constexpr (SMEM) {
+        stage_table(smem_raw, tab_g, tab_bytes, &tab_bar);
+        tab = smem_raw;
     }
-    bool tab_ready = TAB == 0;
-    const uint32_t le = 0xffffffffu >> (31 - lane);
+    StreamCtx<FMT, SW, SMEM> sc{tab, tab + split_x_offset(FMT, nw32), SMEM ? smem_u32(tab) : 0u,
+                               SMEM ? smem_u32(tab) + split_x_offset(FMT, nw32) : 0u, static_cast<const LW*>(s_only_g),
+                               P32, nw32, out, lane, (1u << lane) - 1u, ((1u << lane) - 1u) | (1u << lane)};
+    bool tab_ready = !SMEM;
 
     for (;;) {
         uint32_t t = 0;
         if (lane == 0) t = atomicAdd(task_ctr, 1u);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= ntasks) break;
-        const uint64_t p0 = task_pair[t];
-        const uint32_t lead = static_cast<uint32_t>(p0 & 3);                        // pairs before p0
-        const uint32_t end = lead + static_cast<uint32_t>(task_pair[t + 1] - p0);   // chunk-relative end
-        const uint4* base = reinterpret_cast<const uint4*>(pairs + (p0 - lead));     // 32-byte aligned
-        const int32_t r0 = static_cast<int32_t>(task_row[t]);
-        int32_t open_row = r0 - 1;  // row owning `carry`
-        LW carry = 0;
-
-        uint4 cur[K / 2], nxt[K / 2];
+        const uint64_t p0 = task_pair[t];  // even: 16-byte aligned
+        const uint32_t end = static_cast<uint32_t>(task_pair[t + 1] - p0);
+        const uint4* base = reinterpret_cast<const uint4*>(pairs + p0);
+        // Rows [r0, r1) are this task's.  Pairs loaded past `end` (last chunk)
+        // belong to later rows: the pair at `end` is always a head (the next
+        // task's first row, or the head padding after the last task), so they
+        // are processed like any other pair and only the stores are
+        // restricted to [r0, r1).
+        RowState<LW> rs{static_cast<int32_t>(task_row[t]), static_cast<int32_t>(task_row[t + 1]),
+                        static_cast<int32_t>(task_row[t]) - 1, LW(0)};
+        // Full chunks are piece-transposed in HBM (kStreamK, engine.h), so
+        // piece h of lane l is at h*32 + l: each load is one coalesced
+        // 512-byte run.  The partial last chunk is in plain order.
+        auto load_chunk = [&](uint4 (&cur)[K / 2], uint32_t c, int h0, int h1) {
+            const uint4* q = base + c / 2;
+            if (c + CH <= end) {
 #pragma unroll
-        for (int h = 0; h < K / 2; ++h) cur[h] = ld_stream16(base + (K / 2) * lane + h);
-        if constexpr (TAB_SMEM) {
+                for (int h = h0; h < h1; ++h) cur[h] = ld_stream16(q + h * 32 + lane);
+            } else {
+#pragma unroll
+                for (int h = h0; h < h1; ++h) cur[h] = ld_stream16(q + (K / 2) * lane + h);
+            }
+        };
+        uint4 bufA[K / 2];
+        load_chunk(bufA, 0, 0, K / 2);
+        if constexpr (SMEM) {
             if (!tab_ready) {
                 mbar_wait(&tab_bar, 0);
                 tab_ready = true;
             }
         }
-        for (uint32_t c = 0; c < end; c += CH) {
-            // software prefetch of the next chunk (the pair array is padded by kPairPad)
-            if (c + CH < end) {
-#pragma unroll
-                for (int h = 0; h < K / 2; ++h) nxt[h] = ld_stream16(base + (c + CH) / 2 + (K / 2) * lane + h);
+        if constexpr (IP) {
+            for (uint32_t c = 0; c < end; c += CH) {
+                const bool more = c + CH < end;
+                stream_chunk<FMT, SW, SMEM, K>(sc, rs, bufA, [&](int h0, int h1) {
+                    if (more) load_chunk(bufA, c + CH, h0, h1);
+                });
             }
-            const uint32_t q0 = c + K * lane;
-            const bool interior = c >= lead && c + CH <= end;  // warp-uniform: every pair valid
-            uint32_t heads = 0;  // bit k: pair k opens a row
-            LW v[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const uint32_t mk = (k & 1) ? cur[k / 2].z : cur[k / 2].x;
-                const uint32_t wh = (k & 1) ? cur[k / 2].w : cur[k / 2].y;
-                const bool valid = interior || (q0 + k >= lead && q0 + k < end);
-                heads |= static_cast<uint32_t>(valid && (wh & kHead)) << k;
-                const uint32_t w = valid ? (wh & kWordMask) : nw32;  // invalid -> zero sentinel
-                if constexpr (SPLIT) {
-                    LW S, F;
-                    if constexpr (TAB == 4) {
-                        const uint32_t e = reinterpret_cast<const uint32_t*>(smem_raw)[w];
-                        S = e & 0xffffu;
-                        F = e >> 16;
-                    } else {
-                        const uint2 e = reinterpret_cast<const uint2*>(smem_raw)[w];
-                        S = e.x;
-                        F = e.y;
-                    }
-                    const LW partial = S & ~F;
-                    LW vv = F;
-                    if (partial) {
-                        const uint2 x = reinterpret_cast<const uint2*>(xtab)[w];
-                        vv = pair_hits<LW>(mk, w, SF<LW>{S, F, x.x, x.y}, LW(0), P32, nw32);
-                    }
-                    v[k] = vv;
-                } else {
-                    SF<LW> e;
-                    if constexpr (TAB_SMEM) e = tab[w];
-                    else e = ld_sf(tab + w);
-                    v[k] = pair_hits<LW>(mk, w, e, LW(0), P32, nw32);
-                }
+        } else {  // double-buffered: chunk c is processed while chunk c + CH is in flight
+            uint4 bufB[K / 2];
+            auto none = [](int, int) {};
+            for (uint32_t c = 0; c < end; c += 2 * CH) {
+                if (c + CH < end) load_chunk(bufB, c + CH, 0, K / 2);
+                stream_chunk<FMT, SW, SMEM, K>(sc, rs, bufA, none);
+                if (c + CH >= end) break;
+                if (c + 2 * CH < end) load_chunk(bufA, c + 2 * CH, 0, K / 2);
+                stream_chunk<FMT, SW, SMEM, K>(sc, rs, bufB, none);
             }
-            // rows opened in lower lanes (exclusive prefix of head counts)
-            const int nh = __popc(heads);
-            int incl = nh;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += y;
-            }
-            const int hb = incl - nh;
-            const int tot = __shfl_sync(0xffffffffu, incl, 31);
-            // lane-local segmentation: rows that start and end inside this lane
-            LW pre = 0, cur_or = 0;
-            int seen = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                if (heads >> k & 1u) {
-                    if (seen) out[perm[open_row + hb + seen]] = static_cast<SW>(cur_or);
-                    else pre = cur_or;
-                    ++seen;
-                    cur_or = 0;
-                }
-                cur_or |= v[k];
-            }
-            if (!nh) pre = cur_or;
-            // warp-wide segmented inclusive OR scan; a segment starts at the last
-            // lane <= this one holding a head (lane 0 otherwise, carrying the open row)
-            const uint32_t hmask = __ballot_sync(0xffffffffu, nh > 0) & le;
-            const int seg = hmask ? 31 - __clz(hmask) : 0;
-            LW x = nh ? cur_or : pre;
-            if (lane == 0 && !nh) x |= carry;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const LW y = shfl_up(x, d);
-                if (lane - d >= seg) x |= y;
-            }
-            LW excl = shfl_up(x, 1);
-            if (lane == 0) excl = carry;
-            if (nh) {
-                const int32_t row = open_row + hb;  // the row open before this lane's first head
-                if (row >= r0) out[perm[row]] = static_cast<SW>(excl | pre);
-            }
-            carry = shfl_idx(x, 31);
-            open_row += tot;
-#pragma unroll
-            for (int h = 0; h < K / 2; ++h) cur[h] = nxt[h];
         }
-        if (lane == 0 && open_row >= r0) out[perm[open_row]] = static_cast<SW>(carry);
+        stream_close_task(sc, rs);
     }
-    if constexpr (TAB_SMEM) {
+    if constexpr (SMEM) {
         if (!tab_ready) mbar_wait(&tab_bar, 0);  // never leave with a bulk copy in flight
     }
+}
+
+// TMA-ring variant (split table in shared memory): every warp streams its
+// chunks through a 2-slot ring of 32*K-pair buffers filled by
+// cp.async.bulk (TMA) with one mbarrier per slot.  A chunk is copied into
+// registers (4 conflict-free LDS.128 per lane) as soon as its slot lands and
+// the slot is refilled at once, so two chunks per warp (4 KB) are always in
+// flight independent of registers.  The chunk sequence runs across task
+// boundaries: the next task is claimed when the issue side reaches the end
+// of the current one.
+constexpr int kRingSlots = 2;
+size_t stream_ring_bytes(int warps) {
+    return static_cast<size_t>(warps) * kRingSlots * kStreamCH * sizeof(Pair) + static_cast<size_t>(warps) * kRingSlots * 8;
+}
+
+template <int FMT, typename SW, int NT>
+__global__ void __launch_bounds__(NT)
+    label_stream_tma_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
+                            const uint32_t* __restrict__ task_row, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
+                            const void* __restrict__ tab_g, uint32_t tab_bytes, const void* __restrict__ s_only_g,
+                            const uint32_t* __restrict__ P32, uint32_t nw32, SW* __restrict__ out) {
+    static_assert(FMT != 64, "split tables only");
+    using LW = typename Fmt<FMT>::LW;
+    constexpr int K = kStreamK;
+    constexpr uint32_t CH = kStreamCH;
+    constexpr uint32_t kSlotBytes = CH * sizeof(Pair);
+    constexpr int kWarps = NT / 32;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ uint64_t tab_bar;
+    __shared__ uint32_t sink;  // target of the never-relied-upon store that pins LDS completion
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    // layout: [table (tab_bytes, 16-aligned)] [rings: kWarps x kRingSlots x slot] [mbarriers]
+    const uint32_t ring_off = (tab_bytes + 127u) & ~127u;
+    uint8_t* ring = smem_raw + ring_off + static_cast<uint32_t>(warp) * kRingSlots * kSlotBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + ring_off + kWarps * kRingSlots * kSlotBytes) +
+                     warp * kRingSlots;
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < kRingSlots; ++q) mbar_init(&bars[q], 1);
+    }
+    stage_table(smem_raw, tab_g, tab_bytes, &tab_bar);  // includes __syncthreads (barrier inits visible)
+    const uint8_t* tab = smem_raw;
+    StreamCtx<FMT, SW, true> sc{tab, tab + split_x_offset(FMT, nw32), smem_u32(tab), smem_u32(tab) + split_x_offset(FMT, nw32),
+                               static_cast<const LW*>(s_only_g), P32, nw32, out, lane, (1u << lane) - 1u,
+                               ((1u << lane) - 1u) | (1u << lane)};
+
+    // ---- issue side (warp-uniform state; lane 0 issues the copies) --------
+    uint32_t it = 0;     // task of the next chunk to issue (>= ntasks: none)
+    uint64_t ip0 = 0;    // its first pair
+    uint32_t iend = 0;   // its pair count
+    uint32_t ic = 0;     // chunk offset of the next chunk to issue
+    auto claim = [&]() {
+        uint32_t tn = 0;
+        if (lane == 0) tn = atomicAdd(task_ctr, 1u);
+        it = __shfl_sync(0xffffffffu, tn, 0);
+        ic = 0;
+        if (it < ntasks) {
+            ip0 = task_pair[it];
+            iend = static_cast<uint32_t>(task_pair[it + 1] - ip0);
+        }
+    };
+    static_assert(kRingSlots == 2, "slot bookkeeping below is written for two slots");
+    uint32_t st0 = 0, sc0 = 0, st1 = 0, sc1 = 0;  // (task, chunk offset) held by slot 0 / 1
+    auto issue = [&](int q) {
+        if (q) {
+            st1 = it;
+            sc1 = ic;
+        } else {
+            st0 = it;
+            sc0 = ic;
+        }
+        if (it >= ntasks) return;
+        if (lane == 0) {
+            mbar_expect_tx(&bars[q], kSlotBytes);
+            bulk_g2s(ring + q * kSlotBytes, pairs + ip0 + ic, kSlotBytes, &bars[q]);  // may read past the task: padded
+        }
+        ic += CH;
+        if (ic >= iend) claim();
+    };
+    claim();
+#pragma unroll
+    for (int q = 0; q < kRingSlots; ++q) issue(q);
+    mbar_wait(&tab_bar, 0);
+
+    // ---- compute side -----------------------------------------------------
+    uint32_t ph = 0;               // bit q: parity to wait for on slot q
+    uint32_t ct = ~0u;             // task being assembled
+    uint32_t cend = 0;
+    RowState<LW> rs{0, 0, -1, LW(0)};
+    for (int q = 0;; q ^= 1) {
+        const uint32_t t = q ? st1 : st0;
+        if (t >= ntasks) break;
+        const uint32_t c = q ? sc1 : sc0;
+        if (t != ct) {  // first chunk of a new task
+            if (ct != ~0u) stream_close_task(sc, rs);
+            ct = t;
+            cend = static_cast<uint32_t>(task_pair[t + 1] - task_pair[t]);
+            rs = RowState<LW>{static_cast<int32_t>(task_row[t]), static_cast<int32_t>(task_row[t + 1]),
+                              static_cast<int32_t>(task_row[t]) - 1, LW(0)};
+        }
+        mbar_wait(&bars[q], ph >> q & 1u);
+        ph ^= 1u << q;
+        // piece-transposed full chunk: piece h of this lane at (h*32 + lane)*16,
+        // lane-consecutive and conflict-free; the plain partial last chunk at
+        // (K/2*lane + h)*16
+        const bool full = c + CH <= cend;
+        const uint8_t* lp = ring + q * kSlotBytes + lane * (full ? 16 : 8 * K);
+        const uint32_t step = full ? 512u : 16u;
+        uint4 cur[K / 2];
+#pragma unroll
+        for (int h = 0; h < K / 2; ++h) cur[h] = *reinterpret_cast<const uint4*>(lp + h * step);
+        // the slot may be refilled only after every lane's LDS has returned:
+        // consume the loaded registers (a compare the compiler cannot drop)
+        // before the warp barrier that precedes the refill
+        asm volatile("{\n .reg .pred p;\n setp.eq.u32 p, %0, %1;\n @p st.shared.u32 [%2], %0;\n}\n" ::"r"(cur[0].x),
+                     "r"(cur[K / 2 - 1].w), "r"(smem_u32(&sink)));
+        __syncwarp();
+        issue(q);
+        stream_chunk<FMT, SW, true, K>(sc, rs, cur, [](int, int) {});
+    }
+    if (ct != ~0u) stream_close_task(sc, rs);
 }
 
 // ---------------------------------------------------------------------------
 // F frames.  Persistent warps pull tasks; lane l owns frames l, l+32, ...
 // (FPL of them; FULL = every lane owns exactly FPL frames).  Each T pair is
 // read from HBM once for all F frames and broadcast by shuffle.
-//   sf[w * frames + f]  full summary entry (16 B for <= 32 props)
+//   tab[w * frames + f]     entry (16 B for <= 32 props)
 //   s_only[w * frames + f]  the S mask alone: a pair whose mask covers the
-//                       whole word hits exactly the props set somewhere in
-//                       the word (warp-uniform fast path, 4 B per lookup)
+//                           whole word hits exactly the props set somewhere in
+//                           the word (warp-uniform fast path, 4 B per lookup)
 //   P32 frame f column j at (f*props + j) * nw32
 //   out[perm[row] * frames + f] (edge-major)
 // ---------------------------------------------------------------------------
-template <typename LW, typename SW, int FPL, bool FULL>
+template <int FMT, typename SW, int FPL, bool FULL>
 __global__ void __launch_bounds__(256)
     label_batch_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
                        const uint32_t* __restrict__ task_row, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
-                       const SF<LW>* __restrict__ sf, const LW* __restrict__ s_only,
+                       const void* __restrict__ tab_g, const void* __restrict__ s_only_g,
                        const uint32_t* __restrict__ P32, uint32_t nw32, int props, int frames,
                        const uint32_t* __restrict__ perm, SW* __restrict__ out) {
+    using LW = typename Fmt<FMT>::LW;
+    using E = typename Fmt<FMT>::E;
     const int lane = threadIdx.x & 31;
     const uint64_t frame_stride = static_cast<uint64_t>(props) * nw32;
-    const SF<LW>* lane_sf = sf + lane;
-    const LW* lane_s = s_only + lane;
+    const E* lane_tab = static_cast<const E*>(tab_g) + lane;
+    const LW* lane_s = static_cast<const LW*>(s_only_g) + lane;
     const uint32_t* lane_P = P32 + static_cast<uint64_t>(lane) * frame_stride;
     bool fv[FPL];
 #pragma unroll
@@ -413,8 +820,9 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
                     for (int q = 0; q < FPL; ++q)
                         if (fv[q]) {
-                            const SF<LW> x = ld_sf(lane_sf + off + 32 * q);
-                            acc[q] |= pair_hits<LW>(m, w, x, acc[q], lane_P + 32 * q * frame_stride, nw32);
+                            const E e = ld_entry(lane_tab + off + 32 * q);
+                            acc[q] |= probe<FMT>(e, m, w, lane_s + off + 32 * q, acc[q],
+                                                 lane_P + 32 * q * frame_stride, nw32);
                         }
                 }
             }
@@ -507,39 +915,26 @@ __global__ void resample_kernel(Grid2 vg, Grid2 wg, const Pose2* __restrict__ po
     for (int j = 0; j < ng; ++j) dst[static_cast<uint64_t>(g0 + j) * vnw32] = acc[j];
 }
 
+
 // ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------
-
-// Single-frame shared-memory "split" table: M[w] (S|F<<16 in 4 B for <= 16
-// props, {S, F} in 8 B for <= 32) followed by X[w] = {pa, pb}; the wider M
-// halves the bank-conflict wavefronts of the per-pair gathers and X is only
-// read by lanes whose word has a partial prop.
-int split_entry_bytes(int props) { return props <= 16 ? 4 : props <= 32 ? 8 : 0; }
-size_t split_table_bytes(int props, uint32_t nw32) {
-    const int mb = split_entry_bytes(props);
-    if (!mb) return 0;
-    // both parts 16-byte aligned: the whole table is one set of TMA bulk copies
-    return ((static_cast<size_t>(mb) * (nw32 + 1) + 15u) & ~size_t(15)) + ((8u * (nw32 + 1) + 15u) & ~size_t(15));
-}
-
-cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
-                           void* sf, void* s_only, uint32_t* task_ctr, void* split, cudaStream_t st) {
+cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells, void* tab,
+                           void* s_only, uint32_t* task_ctr, cudaStream_t st) {
     dim3 grid((nw32 + 1 + 255) / 256, static_cast<unsigned>(frames));
-    const int mb = split_entry_bytes(props);
-    if (props <= 32)
-        summary_kernel<uint32_t><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells,
-                                                       static_cast<SF<uint32_t>*>(sf),
-                                                       static_cast<uint32_t*>(s_only), task_ctr,
-                                                       static_cast<uint8_t*>(split), mb);
+    const int fmt = entry_format(props);
+    if (frames == 1 && fmt == 16)
+        summary_kernel<16, true><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr);
+    else if (frames == 1 && fmt == 32)
+        summary_kernel<32, true><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr);
+    else if (fmt == 16)
+        summary_kernel<16, false><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr);
+    else if (fmt == 32)
+        summary_kernel<32, false><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr);
     else
-        summary_kernel<uint64_t><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells,
-                                                       static_cast<SF<uint64_t>*>(sf),
-                                                       static_cast<uint64_t*>(s_only), task_ctr, nullptr, 0);
+        summary_kernel<64, false><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr);
     return cudaGetLastError();
 }
-
-size_t summary_entry_bytes(int props) { return props <= 32 ? sizeof(SF<uint32_t>) : sizeof(SF<uint64_t>); }
 
 static int sm_count() {
     static int n = 0;
@@ -554,98 +949,107 @@ static int sm_count() {
 
 constexpr uint32_t kMaxSmemTable = 200u * 1024u;
 
-// Dev knobs (A/B sweeps on the GPU box): LTLG_STREAM_TABLE=smem|global, LTLG_STREAM_K=4|8
+// Dev knobs (A/B sweeps on the GPU box): LTLG_STREAM_TABLE=0 forces the global table
 static int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
     return v && *v ? atoi(v) : dflt;
 }
 
-template <typename LW, typename SW, int TAB, int K>
-static cudaError_t launch_stream_v(const LaunchArgs& a, uint32_t tab_bytes, const void* tab_src, cudaStream_t st) {
-    const auto* tab = static_cast<const SF<LW>*>(tab_src);
-    if constexpr (TAB != 0) {
+bool stream_table_in_smem(int props, uint32_t nw32) {
+    static const int want = env_int("LTLG_STREAM_TABLE", -1);
+    if (want == 0 || entry_format(props) == 64) return false;
+    return split_table_bytes(props, nw32) <= kMaxSmemTable;
+}
+
+template <int FMT, typename SW, bool SMEM, int K, int NT, bool IP = false>
+static cudaError_t launch_stream_v(const LaunchArgs& a, cudaStream_t st) {
+    const uint32_t tab_bytes = FMT == 64 ? (a.nw32 + 1) * static_cast<uint32_t>(summary_entry_bytes(a.props))
+                                         : static_cast<uint32_t>(split_table_bytes(a.props, a.nw32));
+    auto kern = label_stream_kernel<FMT, SW, SMEM, K, NT, IP>;
+    if constexpr (SMEM) {
         static uint64_t attr_set = 0;  // per device
         int dev = 0;
         cudaGetDevice(&dev);
         if (!(attr_set >> dev & 1u)) {
-            cudaFuncSetAttribute(label_stream_kernel<LW, SW, TAB, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kMaxSmemTable));
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaxSmemTable));
             attr_set |= 1ull << dev;
         }
-        if (tab_bytes % 16u) return cudaErrorInvalidValue;  // never launch an uncompletable TMA copy
-        label_stream_kernel<LW, SW, TAB, K><<<sm_count(), 1024, tab_bytes, st>>>(
-            a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, tab, tab_bytes, a.P32, a.nw32, a.perm,
-            static_cast<SW*>(a.out));
+        if (tab_bytes % 16u || tab_bytes > kMaxSmemTable) return cudaErrorInvalidValue;  // never launch an uncompletable TMA copy
+        kern<<<sm_count(), NT, tab_bytes, st>>>(a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, a.sf, tab_bytes,
+                                                a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out));
     } else {
         static int per_sm = 0;
         if (!per_sm) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, label_stream_kernel<LW, SW, 0, K>, 256, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, 0);
             if (per_sm <= 0) per_sm = 4;
         }
-        label_stream_kernel<LW, SW, 0, K><<<sm_count() * per_sm, 256, 0, st>>>(
-            a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, tab, tab_bytes, a.P32, a.nw32, a.perm,
-            static_cast<SW*>(a.out));
+        kern<<<sm_count() * per_sm, NT, 0, st>>>(a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, a.sf, tab_bytes,
+                                                 a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out));
     }
     return cudaSuccess;
 }
 
-// Which single-frame table layout a submit uses (the summary kernel must
-// write the split layout when this returns a split mode).
-int stream_table_mode(int props, uint32_t nw32) {
-    static const int want = env_int("LTLG_STREAM_TABLE", -1);  // dev knob: 0 global, 1 smem, 2 split
-    const size_t comb = static_cast<size_t>(nw32 + 1) * summary_entry_bytes(props);
-    const size_t split = split_table_bytes(props, nw32);
-    if (want == 0) return 0;
-    if (want == 1) return comb <= kMaxSmemTable ? 1 : 0;
-    if (split && split <= kMaxSmemTable) return split_entry_bytes(props);
-    return comb <= kMaxSmemTable ? 1 : 0;
+// Single-frame variant: LTLG_STREAM_CFG (dev knob for A/B sweeps) picks the
+// prefetch scheme of the shared-memory-table kernel:
+//   2 = double-buffered registers, 3 = in-place prefetch (default; fastest,
+//   ncu r02), 4 = TMA ring (needs table + rings in shared memory; it removes
+//   the load-latency stalls but spends more ALU-pipe issue, the bottleneck)
+constexpr uint32_t kMaxDynSmem = 227u * 1024u - 1024u;  // opt-in limit minus static shared memory
+template <int FMT, typename SW>
+static cudaError_t launch_stream_tma(const LaunchArgs& a, uint32_t tab_bytes, cudaStream_t st) {
+    constexpr int NT = 1024;
+    const uint32_t smem = ((tab_bytes + 127u) & ~127u) + static_cast<uint32_t>(stream_ring_bytes(NT / 32));
+    auto kern = label_stream_tma_kernel<FMT, SW, NT>;
+    static uint32_t attr_set[64] = {};  // per device: dynamic shared memory granted so far
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (tab_bytes % 16u || smem > kMaxDynSmem || dev >= 64) return cudaErrorInvalidValue;
+    if (attr_set[dev] < smem) {
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        attr_set[dev] = smem;
+    }
+    kern<<<sm_count(), NT, smem, st>>>(a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, a.sf, tab_bytes,
+                                       a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out));
+    return cudaSuccess;
 }
 
-template <typename LW, typename SW>
+template <int FMT, typename SW>
 static cudaError_t launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
-    static const int k = env_int("LTLG_STREAM_K", 8);
-    const int mode = stream_table_mode(a.props, a.nw32);
-    const uint32_t comb = (a.nw32 + 1) * static_cast<uint32_t>(sizeof(SF<LW>));
-    if (mode == 0) {
-        if (k == 8) return launch_stream_v<LW, SW, 0, 8>(a, comb, a.sf, st);
-        else return launch_stream_v<LW, SW, 0, 4>(a, comb, a.sf, st);
-    } else if (mode == 1) {
-        if (k == 8) return launch_stream_v<LW, SW, 1, 8>(a, comb, a.sf, st);
-        else return launch_stream_v<LW, SW, 1, 4>(a, comb, a.sf, st);
-    } else if constexpr (sizeof(LW) == 4) {
-        const uint32_t sb = static_cast<uint32_t>(split_table_bytes(a.props, a.nw32));
-        if (mode == 4) {
-            if (k == 8) return launch_stream_v<LW, SW, 4, 8>(a, sb, a.split, st);
-            else return launch_stream_v<LW, SW, 4, 4>(a, sb, a.split, st);
-        } else {
-            if (k == 8) return launch_stream_v<LW, SW, 8, 8>(a, sb, a.split, st);
-            else return launch_stream_v<LW, SW, 8, 4>(a, sb, a.split, st);
+    static const int cfg = env_int("LTLG_STREAM_CFG", 3);
+    if constexpr (FMT != 64) {
+        if (stream_table_in_smem(a.props, a.nw32)) {
+            const uint32_t tab_bytes = static_cast<uint32_t>(split_table_bytes(a.props, a.nw32));
+            const bool ring_fits = ((tab_bytes + 127u) & ~127u) + stream_ring_bytes(32) <= kMaxDynSmem;
+            if (cfg == 4 && ring_fits) return launch_stream_tma<FMT, SW>(a, tab_bytes, st);
+            if (cfg == 2) return launch_stream_v<FMT, SW, true, kStreamK, 1024>(a, st);
+            return launch_stream_v<FMT, SW, true, kStreamK, 1024, true>(a, st);
         }
     }
-    return cudaErrorInvalidValue;
+    return launch_stream_v<FMT, SW, false, kStreamK, 256, true>(a, st);
 }
 
-template <typename LW, typename SW, int FPL, bool FULL>
+template <int FMT, typename SW, int FPL, bool FULL>
 static void launch_batch_t(const LaunchArgs& a, cudaStream_t st) {
     static int per_sm = 0;
     if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, label_batch_kernel<LW, SW, FPL, FULL>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, label_batch_kernel<FMT, SW, FPL, FULL>, 256, 0);
         if (per_sm <= 0) per_sm = 4;
     }
-    label_batch_kernel<LW, SW, FPL, FULL><<<sm_count() * per_sm, 256, 0, st>>>(
-        a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, static_cast<const SF<LW>*>(a.sf),
-        static_cast<const LW*>(a.s_only), a.P32, a.nw32, a.props, a.frames, a.perm, static_cast<SW*>(a.out));
+    label_batch_kernel<FMT, SW, FPL, FULL><<<sm_count() * per_sm, 256, 0, st>>>(
+        a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, a.sf, a.s_only, a.P32, a.nw32, a.props, a.frames,
+        a.perm, static_cast<SW*>(a.out));
 }
 
-template <typename LW, typename SW>
+template <int FMT, typename SW>
 static void launch_batch_fpl(const LaunchArgs& a, cudaStream_t st) {
-    if (a.frames == 32) launch_batch_t<LW, SW, 1, true>(a, st);
-    else if (a.frames == 64) launch_batch_t<LW, SW, 2, true>(a, st);
-    else if (a.frames == 128) launch_batch_t<LW, SW, 4, true>(a, st);
-    else if (a.frames < 32) launch_batch_t<LW, SW, 1, false>(a, st);
-    else if (a.frames < 64) launch_batch_t<LW, SW, 2, false>(a, st);
-    else if (a.frames < 128) launch_batch_t<LW, SW, 4, false>(a, st);
-    else launch_batch_t<LW, SW, 8, false>(a, st);
+    if (a.frames == 32) launch_batch_t<FMT, SW, 1, true>(a, st);
+    else if (a.frames == 64) launch_batch_t<FMT, SW, 2, true>(a, st);
+    else if (a.frames == 128) launch_batch_t<FMT, SW, 4, true>(a, st);
+    else if (a.frames < 32) launch_batch_t<FMT, SW, 1, false>(a, st);
+    else if (a.frames < 64) launch_batch_t<FMT, SW, 2, false>(a, st);
+    else if (a.frames < 128) launch_batch_t<FMT, SW, 4, false>(a, st);
+    else launch_batch_t<FMT, SW, 8, false>(a, st);
 }
 
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
@@ -653,17 +1057,17 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
     cudaError_t e = cudaSuccess;
     if (a.frames == 1) {
         switch (a.label_bytes) {
-            case 1: e = launch_stream_t<uint32_t, uint8_t>(a, st); break;
-            case 2: e = launch_stream_t<uint32_t, uint16_t>(a, st); break;
-            case 4: e = launch_stream_t<uint32_t, uint32_t>(a, st); break;
-            default: e = launch_stream_t<uint64_t, uint64_t>(a, st); break;
+            case 1: e = launch_stream_t<16, uint8_t>(a, st); break;
+            case 2: e = launch_stream_t<16, uint16_t>(a, st); break;
+            case 4: e = launch_stream_t<32, uint32_t>(a, st); break;
+            default: e = launch_stream_t<64, uint64_t>(a, st); break;
         }
     } else {
         switch (a.label_bytes) {
-            case 1: launch_batch_fpl<uint32_t, uint8_t>(a, st); break;
-            case 2: launch_batch_fpl<uint32_t, uint16_t>(a, st); break;
-            case 4: launch_batch_fpl<uint32_t, uint32_t>(a, st); break;
-            default: launch_batch_fpl<uint64_t, uint64_t>(a, st); break;
+            case 1: launch_batch_fpl<16, uint8_t>(a, st); break;
+            case 2: launch_batch_fpl<16, uint16_t>(a, st); break;
+            case 4: launch_batch_fpl<32, uint32_t>(a, st); break;
+            default: launch_batch_fpl<64, uint64_t>(a, st); break;
         }
     }
     if (e != cudaSuccess) return e;

@@ -24,16 +24,16 @@ struct LaunchArgs {
     void* out;
     int label_bytes;
     uint32_t* task_ctr;  // device counter, reset by the summary kernel
-    const void* s_only;  // S-only summary (multi-frame kernel)
-    const void* split;   // single-frame split table (see stream_table_mode)
+    const void* s_only;  // S mask per (word, frame): over-path probes, full-mask pairs
 };
 
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
-                           void* sf, void* s_only, uint32_t* task_ctr, void* split, cudaStream_t st);
-int split_entry_bytes(int props);
-size_t split_table_bytes(int props, uint32_t nw32);
-int stream_table_mode(int props, uint32_t nw32);
+                           void* tab, void* s_only, uint32_t* task_ctr, cudaStream_t st);
+int entry_format(int props);
 size_t summary_entry_bytes(int props);
+size_t s_only_bytes(int props);
+size_t split_table_bytes(int props, uint32_t nw32);
+bool stream_table_in_smem(int props, uint32_t nw32);
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st);
 cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, int frames, int frame,
                            uint64_t* out, cudaStream_t st);

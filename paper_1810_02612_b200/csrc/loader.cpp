@@ -295,6 +295,55 @@ void make_tasks(const std::vector<uint64_t>& pair_off, uint64_t rows, int target
 
 }  // namespace
 
+// The single-frame copy of the pairs (see kStreamK in engine.h): rows in
+// their ORIGINAL order (the single-frame kernel reads the summary from shared
+// memory, so it gains nothing from z-locality and stores label i at row i
+// without a permutation gather), tasks re-based to even pair offsets, full
+// chunks piece-transposed.
+void build_stream_layout(const WordCsr& t, uint64_t row_begin, uint64_t row_end, uint32_t sentinel_word,
+                         int stream_task_pairs, PackedShard* out) {
+    const uint64_t R = row_end - row_begin;
+    std::vector<uint64_t> pair_off(R + 1, 0);
+    for (uint64_t r = 0; r < R; ++r) {
+        const uint64_t n = t.offsets[row_begin + r + 1] - t.offsets[row_begin + r];
+        pair_off[r + 1] = pair_off[r] + (n ? n : 1);
+    }
+    make_tasks(pair_off, R, stream_task_pairs, &out->task_row_stream, &out->task_pair_stream);
+    const size_t nt = out->task_row_stream.size() - 1;
+    std::vector<uint64_t> dst_off(nt + 1, 0);
+    for (size_t k = 0; k < nt; ++k) {
+        const uint64_t n = out->task_pair_stream[k + 1] - out->task_pair_stream[k];
+        dst_off[k + 1] = dst_off[k] + n + (n & 1);
+    }
+    out->pairs_stream.assign(dst_off[nt] + kPairPad, Pair{0, sentinel_word | kHead});
+    parallel_chunks(nt, 64, [&](uint64_t b, uint64_t e, int) {
+        std::vector<Pair> src;
+        for (uint64_t k = b; k < e; ++k) {
+            // the task's rows in plain order
+            src.clear();
+            for (uint64_t r = out->task_row_stream[k]; r < out->task_row_stream[k + 1]; ++r) {
+                const uint64_t o0 = t.offsets[row_begin + r], o1 = t.offsets[row_begin + r + 1];
+                if (o1 == o0) {
+                    src.push_back(Pair{0, sentinel_word | kHead});  // empty row: a no-op pair on the zero sentinel word
+                    continue;
+                }
+                for (uint64_t q = o0; q < o1; ++q) src.push_back(Pair{t.mask[q], t.word[q] | (q == o0 ? kHead : 0u)});
+            }
+            Pair* dst = out->pairs_stream.data() + dst_off[k];
+            const uint64_t n = src.size();
+            uint64_t c = 0;
+            for (; c + kStreamCH <= n; c += kStreamCH)  // full chunks: piece-transposed
+                for (uint64_t l = 0; l < 32; ++l)
+                    for (uint64_t h = 0; h < kStreamK / 2; ++h)
+                        for (uint64_t e2 = 0; e2 < 2; ++e2)
+                            dst[c + 2 * (h * 32 + l) + e2] = src[c + kStreamK * l + 2 * h + e2];
+            for (; c < n; ++c) dst[c] = src[c];           // last partial chunk: plain
+            if (n & 1) dst[n] = Pair{0, sentinel_word};   // no-op pair (no head) to an even count
+        }
+    });
+    out->task_pair_stream = dst_off;
+}
+
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
                  uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs,
                  PackedShard* out) {
@@ -326,7 +375,9 @@ void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool so
         pair_off[s + 1] = pair_off[s] + (n ? n : 1);
     }
     out->n_pairs = pair_off[R];
-    out->pairs.assign(out->n_pairs + kPairPad, Pair{0, sentinel_word});
+    // padding: no-op head pairs, so the pair after any task is a head (the
+    // single-frame kernel closes a task's last row on it)
+    out->pairs.assign(out->n_pairs + kPairPad, Pair{0, sentinel_word | kHead});
     parallel_chunks(R, 1 << 14, [&](uint64_t b, uint64_t e, int) {
         for (uint64_t s = b; s < e; ++s) {
             const uint64_t r = row_begin + out->perm[s];
@@ -340,8 +391,8 @@ void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool so
             dst[0].word |= kHead;
         }
     });
-    make_tasks(pair_off, R, stream_task_pairs, &out->task_row_stream, &out->task_pair_stream);
     make_tasks(pair_off, R, batch_task_pairs, &out->task_row_batch, &out->task_pair_batch);
+    build_stream_layout(t, row_begin, row_end, sentinel_word, stream_task_pairs, out);
 }
 
 }  // namespace ltlg
