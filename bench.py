@@ -46,28 +46,55 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+    """SM clock + throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line): NVML in-process every 5 ms, falling back
+    to nvidia-smi polling when NVML is unavailable."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    REASONS = {0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.sm, self.mx, self.reasons = [], [], set()
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            n = self._nvml
+            self.sm.append(float(n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)))
+            self.mx.append(float(n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM)))
+            r = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            self.reasons |= {name for bit, name in self.REASONS.items() if r & bit}
+            return
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5).stdout.strip()
+        if out:
+            r = [x.strip() for x in out.split(",")]
+            self.sm.append(float(r[0]))
+            self.mx.append(float(r[1]))
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            self.reasons |= {names[k] for k in range(4) if len(r) > 2 + k and r[2 + k] == "Active"}
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self._sample()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.005 if self._nvml is not None else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -77,16 +104,27 @@ class Clocks:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if not self.sm:  # a timed region shorter than one poll: take one sample now
+            try:
+                self._sample()
+            except Exception:
+                pass
 
     def summary(self):
-        if not self.rows:
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx), "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml" if self._nvml is not None else "nvidia-smi"}
+
+
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture summary (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
 
 
 def shard_rows(E: int, rank: int, world: int):
@@ -173,6 +211,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="short run for profilers")
+    ap.add_argument("--readback-chunks", type=int, default=8,
+                    help="ltlg_options.readback_chunks: row blocks whose label read-back overlaps labelling")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -197,7 +237,7 @@ def main():
     r0, r1 = shard_rows(E, rank, world)
     prm = SyntheticPRM(seed=SEED_T, depth=depth)
     T = prm.words(r0, r1)
-    eng = LabelEngine(devices=[local], profile=True)
+    eng = LabelEngine(devices=[local], profile=True, readback_chunks=args.readback_chunks)
     eng.load_abstraction_words(r1 - r0, cells, T.offsets, T.words, T.masks)
     info = eng.info()
     W32_all = torch.tensor([int(info.words), int(r1 - r0)], dtype=torch.int64, device="cuda")
@@ -259,10 +299,20 @@ def main():
     rows_local = r1 - r0
     alg_bytes = 8 * int(info.words) + 4 * (rows_local + 1) + F * (cells * props // 8 + rows_local * 4)
     achieved = alg_bytes / (label_ms / 1e3) / 1e9
+    traffic = ncu_traffic("label_batch_kernel")
+    sm_clk = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+    lop3 = float(info.words) * F * props  # one AND-OR per stored T word per prop per frame
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "peak_source": src, "kernel": "label_batch_kernel<u32,u32,2>",
+                "traffic": traffic, "peak_source": src, "kernel": "label_batch_kernel<32,u32,2,full>",
                 "alg_bytes_per_launch": alg_bytes, "kernel_ms": label_ms, "summary_kernel_ms": summary_ms,
-                "note": "algorithmic bytes = 8*W32 + 4*(E+1) + F*(cells*props/8 + E*4)"}
+                "note": "algorithmic bytes = 8*W32 + 4*(E+1) + F*(cells*props/8 + E*4); traffic = dram read+write "
+                        "bytes per launch from the committed ncu --set full capture (profiles/traffic.json). The "
+                        "multi-frame kernel is not HBM-bound: ncu shows the ALU pipe saturated (see int_ops)",
+                "int_ops": {"alg_and_or_per_launch": lop3, "achieved_per_s": lop3 / (label_ms / 1e3),
+                            "peak_per_s": 148 * 64 * sm_clk,
+                            "frac": lop3 / (label_ms / 1e3) / (148 * 64 * sm_clk),
+                            "note": "SURVEY 8(d) integer roofline W32*F*props AND-ORs at 64/clk/SM; > 1 because one "
+                                    "summary entry answers every prop of a (T word, frame) at once"}}
 
     # ---- p50 single-frame latency, config 3 (16 props), host P -> labels in HBM
     lat = None
@@ -290,13 +340,17 @@ def main():
                "frames": n_frames, "what": "pinned host P -> labels resident in HBM (host steady clock)",
                "kernel_p50_ms": k3, "roofline": {"bound": "hbm", "achieved": alg3 / (k3 / 1e3) / 1e9, "peak": hbm,
                                                 "unit": "GB/s", "frac": alg3 / (k3 / 1e3) / 1e9 / hbm,
-                                                "alg_bytes_per_launch": alg3}}
+                                                "alg_bytes_per_launch": alg3,
+                                                "traffic": ncu_traffic("label_stream_kernel"),
+                                                "kernel": "label_stream_kernel<16,u16,smem,8,1024,in-place>"}}
 
     # ---- e2e through the public API with host buffers ------------------------
     e2e = None
     if not args.no_e2e:
         out_host = torch.empty((rows_local, F), dtype=torch.int32, pin_memory=True)
         Ke = max(2, min(K, 5))
+        eng.submit_grid(cells, props, P_host, F) if world == 1 else None  # untimed warm-up of the host path
+        eng.get_labels_packed(out_host)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
@@ -318,7 +372,8 @@ def main():
         e2e = {"value": E * F * Ke / dt, "unit": UNIT, "h2d_bytes_per_step": F * props * nw * 8,
                "d2h_bytes_per_step": E * F * 4, "steps": Ke,
                "what": "ltlg_submit_grid(pinned host P, 64 frames) + ltlg_get_labels_packed(pinned host, u32 x 64 "
-                       "frames per edge); host wall clock"}
+                       "frames per edge); host wall clock; readback_chunks=%d (block c's labels copy back while "
+                       "later blocks are labelled)" % args.readback_chunks}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

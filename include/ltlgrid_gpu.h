@@ -57,7 +57,11 @@ typedef struct ltlg_options {
     int stream_task_pairs;/* target T pairs per warp task, single-frame kernel (0 = default 2048) */
     int batch_task_pairs; /* target T pairs per warp task, multi-frame kernel (0 = default 256)   */
     int profile;          /* 1: record CUDA events around each stage (ltlg_stage_times) */
-    int reserved[7];
+    int readback_chunks;  /* >1: split each shard's rows into this many blocks (<= 64); multi-frame
+                             submits of host-memory P label them with separate launches, so
+                             ltlg_get_labels_packed copies block c to the host while later blocks
+                             are still being labelled (0/1 = off) */
+    int reserved[6];
 } ltlg_options;
 
 /* Shape / layout facts about the loaded abstraction and the last submit. */

@@ -90,6 +90,11 @@ struct Shard {
     cudaEvent_t* ev = nullptr;      // the quadruple of the current submit
     uint64_t row_begin = 0, row_end = 0, n_pairs = 0, words = 0;
     uint32_t ntask_stream = 0, ntask_batch = 0;
+    std::vector<uint64_t> block_row;                           // read-back blocks (local rows)
+    std::vector<uint32_t> block_task_s, block_task_b;          // their first task, per layout
+    cudaStream_t copy_stream = nullptr;                        // label read-back
+    std::vector<cudaEvent_t> block_done;                       // per block, recorded after its launch
+    int blocks_last = 0;                                       // blocks labelled by the last submit
     DevBuf<Pair> pairs, pairs_s;  // plain (multi-frame) and single-frame layouts
     DevBuf<uint32_t> perm, trow_s, trow_b;
     DevBuf<uint64_t> tpair_s, tpair_b;
@@ -157,6 +162,16 @@ ltlg_status upload_shard(ltlg_ctx* ctx, Shard& s, const PackedShard& p) {
     s.words = p.words;
     s.ntask_stream = static_cast<uint32_t>(p.task_row_stream.size() - 1);
     s.ntask_batch = static_cast<uint32_t>(p.task_row_batch.size() - 1);
+    s.block_row = p.block_row;
+    s.block_task_s = p.block_task_stream;
+    s.block_task_b = p.block_task_batch;
+    const size_t nb = p.block_row.size() - 1;
+    while (s.block_done.size() < nb) {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+        s.block_done.push_back(ev);
+    }
+    if (!s.copy_stream) CK(cudaStreamCreateWithFlags(&s.copy_stream, cudaStreamNonBlocking), "stream");
     auto put = [&](auto& buf, const auto& vec, const char* what) -> ltlg_status {
         using T = typename std::decay_t<decltype(vec)>::value_type;
         const size_t b = vec.size() * sizeof(T);
@@ -196,7 +211,9 @@ ltlg_status load_words(ltlg_ctx* ctx, WordCsr& t) {
             return set_err(ctx, LTLG_EINVAL, "a device shard holds more than 2^32-1 rows");
         build_shard(t, b[i], b[i + 1], ctx->opts.sort_rows != 0, sentinel,
                     ctx->opts.stream_task_pairs > 0 ? ctx->opts.stream_task_pairs : 2048,
-                    ctx->opts.batch_task_pairs > 0 ? ctx->opts.batch_task_pairs : 256, &p);
+                    ctx->opts.batch_task_pairs > 0 ? ctx->opts.batch_task_pairs : 256,
+                    ctx->opts.readback_chunks > 1 ? (ctx->opts.readback_chunks < 64 ? ctx->opts.readback_chunks : 64) : 1,
+                    &p);
         ltlg_status st = upload_shard(ctx, ctx->shards[static_cast<size_t>(i)], p);
         if (st != LTLG_OK) return st;
         pairs += p.n_pairs;
@@ -266,7 +283,9 @@ ltlg_status broadcast_P(ltlg_ctx* ctx, size_t words) {
 }
 
 // Summary + labeling on every shard for P already resident in shard.P.
-ltlg_status run_label(ltlg_ctx* ctx) {
+// split: one launch per read-back block (submits whose labels are expected
+// to go back to the host: host-memory P); otherwise one launch.
+ltlg_status run_label(ltlg_ctx* ctx, bool split) {
     const uint32_t nw32 = nw32_of(ctx->cells);
     const int props = ctx->props, frames = ctx->frames;
     for (Shard& s : ctx->shards) {
@@ -275,17 +294,18 @@ ltlg_status run_label(ltlg_ctx* ctx) {
         CK(s.labels.reserve(lab ? lab : 8), "allocate labels");
         if (props == 0 || s.rows() == 0) {
             s.have_times = false;
+            s.blocks_last = 0;
             continue;
         }
         CK(s.sf.reserve(frames == 1 && props <= 32 ? split_table_bytes(props, nw32)
                                                    : static_cast<size_t>(nw32 + 1) * frames * summary_entry_bytes(props)),
            "allocate summary");
-        CK(s.ctr.reserve(64), "allocate task counter");
+        CK(s.ctr.reserve(64 * sizeof(uint32_t)), "allocate task counters");
         CK(s.s_only.reserve(static_cast<size_t>(nw32 + 1) * frames * s_only_bytes(props)), "allocate summary");
         const bool prof = ctx->opts.profile != 0;
         if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
         CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
-                          s.s_only.ptr, s.ctr.ptr, s.stream),
+                          s.s_only.ptr, s.ctr.ptr, static_cast<int>(s.block_row.size() - 1), s.stream),
            "summary kernel");
         if (prof) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
@@ -298,19 +318,24 @@ ltlg_status run_label(ltlg_ctx* ctx) {
         a.frames = frames;
         a.out = s.labels.ptr;
         a.label_bytes = ctx->label_bytes;
-        a.task_ctr = s.ctr.ptr;
         a.s_only = s.s_only.ptr;
-        if (frames == 1) {
-            a.pairs = s.pairs_s.ptr;
-            a.task_pair = s.tpair_s.ptr;
-            a.task_row = s.trow_s.ptr;
-            a.ntasks = s.ntask_stream;
-        } else {
-            a.task_pair = s.tpair_b.ptr;
-            a.task_row = s.trow_b.ptr;
-            a.ntasks = s.ntask_batch;
+        const bool single = frames == 1;
+        if (single) a.pairs = s.pairs_s.ptr;
+        a.task_pair = single ? s.tpair_s.ptr : s.tpair_b.ptr;
+        a.task_row = single ? s.trow_s.ptr : s.trow_b.ptr;
+        // one launch per read-back block for multi-frame submits (their labels are
+        // large: rows x frames words); a single frame's labels are small, so it
+        // runs as one launch over all tasks (tasks are listed block by block)
+        const std::vector<uint32_t>& bt = single ? s.block_task_s : s.block_task_b;
+        const int nb = single || !split ? 1 : static_cast<int>(bt.size() - 1);
+        for (int c = 0; c < nb; ++c) {
+            a.task_begin = bt[static_cast<size_t>(c)];
+            a.ntasks = nb == 1 ? bt.back() : bt[static_cast<size_t>(c) + 1];
+            a.task_ctr = s.ctr.ptr + c;
+            CK(launch_label(a, s.stream), "label kernel");
+            if (nb > 1) CK(cudaEventRecord(s.block_done[static_cast<size_t>(c)], s.stream), "event");
         }
-        CK(launch_label(a, s.stream), "label kernel");
+        s.blocks_last = nb;
         if (prof) CK(cudaEventRecord(s.ev[3], s.stream), "event");
         s.have_times = prof;
     }
@@ -351,7 +376,7 @@ ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t*
             cudaSetDevice(ctx->shards[i].device);
             cudaEventRecord(ctx->shards[i].ev[0], ctx->shards[i].stream);
         }
-    return run_label(ctx);
+    return run_label(ctx, !on_device);
 }
 
 ltlg_status sync_all(ltlg_ctx* ctx) {
@@ -458,6 +483,8 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.s_only.release();
         for (auto& ev : s.ring)
             if (ev) cudaEventDestroy(ev);
+        for (auto& ev : s.block_done) cudaEventDestroy(ev);
+        if (s.copy_stream) cudaStreamDestroy(s.copy_stream);
         if (s.stream) cudaStreamDestroy(s.stream);
     }
     delete ctx;
@@ -565,7 +592,7 @@ ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, con
     // pageable pose upload must complete before the caller's buffer may change
     CK(cudaStreamSynchronize(s0.stream), "resample");
     if ((st = broadcast_P(ctx, vwords)) != LTLG_OK) return st;
-    return run_label(ctx);
+    return run_label(ctx, !words_on_device);
 }
 
 ltlg_status ltlg_wait(ltlg_ctx* ctx) {
@@ -600,9 +627,28 @@ ltlg_status ltlg_get_labels_packed(ltlg_ctx* ctx, void* out, size_t out_bytes) {
     for (Shard& s : ctx->shards) {
         if (s.rows() == 0) continue;
         CK(cudaSetDevice(s.device), "cudaSetDevice");
-        CK(cudaMemcpyAsync(static_cast<uint8_t*>(out) + s.row_begin * per_row, s.labels.ptr, s.rows() * per_row,
-                           cudaMemcpyDeviceToHost, s.stream),
-           "download labels");
+        uint8_t* dst = static_cast<uint8_t*>(out) + s.row_begin * per_row;
+        if (s.blocks_last > 1) {
+            // block c goes back on the copy stream as soon as its launch is done,
+            // while the later blocks are still being labelled
+            for (int c = 0; c < s.blocks_last; ++c) {
+                const uint64_t r0 = s.block_row[static_cast<size_t>(c)], r1 = s.block_row[static_cast<size_t>(c) + 1];
+                if (r1 == r0) continue;
+                CK(cudaStreamWaitEvent(s.copy_stream, s.block_done[static_cast<size_t>(c)], 0), "stream wait");
+                CK(cudaMemcpyAsync(dst + r0 * per_row, s.labels.ptr + r0 * per_row, (r1 - r0) * per_row,
+                                   cudaMemcpyDeviceToHost, s.copy_stream),
+                   "download labels");
+            }
+        } else {
+            CK(cudaMemcpyAsync(dst, s.labels.ptr, s.rows() * per_row, cudaMemcpyDeviceToHost, s.stream),
+               "download labels");
+        }
+    }
+    for (Shard& s : ctx->shards) {
+        if (s.blocks_last > 1) {
+            CK(cudaSetDevice(s.device), "cudaSetDevice");
+            CK(cudaStreamSynchronize(s.copy_stream), "download labels");
+        }
     }
     return sync_all(ctx);
 }

@@ -44,6 +44,11 @@ struct PackedShard {
     // warp tasks: [row_begin, row_end) in sorted positions, pairs [pair_begin, pair_end)
     std::vector<uint32_t> task_row_stream, task_row_batch;    // ntasks + 1
     std::vector<uint64_t> task_pair_stream, task_pair_batch;  // ntasks + 1
+    // read-back blocks: rows [block_row[c], block_row[c+1]) (local, original
+    // order) are z-sorted only among themselves, so the tasks
+    // [block_task_*[c], block_task_*[c+1]) write exactly that row range
+    std::vector<uint64_t> block_row;
+    std::vector<uint32_t> block_task_stream, block_task_batch;
 };
 
 constexpr uint64_t kPairPad = 512;  // tail padding so vector loads never leave the array
@@ -71,7 +76,7 @@ bool read_csb1(const char* path, uint64_t* rows, uint64_t* cols, std::vector<uin
 // Split rows into n contiguous shards balanced by stored pairs.
 std::vector<uint64_t> shard_bounds(const WordCsr& t, int n);
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
-                 uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs,
+                 uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs, int blocks,
                  PackedShard* out);
 int host_threads();
 

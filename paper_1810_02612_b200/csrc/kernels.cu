@@ -138,6 +138,14 @@ __device__ __forceinline__ LW probe_gather(uint32_t m, uint32_t w, LW over, cons
     return v;
 }
 
+// Out-of-line copy for the multi-frame kernel's inner loop: inlining the
+// rare gather loop there costs more (code size, scheduling) than the call.
+template <typename LW>
+__device__ __noinline__ LW probe_gather_call(uint32_t m, uint32_t w, LW over, const uint32_t* __restrict__ col0,
+                                             uint32_t nw32) {
+    return probe_gather<LW>(m, w, over, col0, nw32);
+}
+
 // Label contribution of one stored pair (mask m of word w) for one frame.
 //   e    : the frame's summary entry of word w
 //   sp   : the frame's S mask of word w (read only on the rare over path)
@@ -153,7 +161,7 @@ __device__ __forceinline__ typename Fmt<FMT>::LW probe(const typename Fmt<FMT>::
         if (m & e.z) v |= e.w >> 16;
         if (e.x & kOver16) {
             const uint32_t known = (e.x | e.w | (e.w >> 16)) & 0xffffu;
-            v |= probe_gather<uint32_t>(m, w, __ldg(sp) & ~known & ~skip, col0, nw32);
+            v |= probe_gather_call<uint32_t>(m, w, __ldg(sp) & ~known & ~skip, col0, nw32);
         }
         return v;
     } else if constexpr (FMT == 32) {
@@ -162,7 +170,7 @@ __device__ __forceinline__ typename Fmt<FMT>::LW probe(const typename Fmt<FMT>::
         uint32_t v = e.x;
         if (m & e.y) v |= abit;
         if (m & e.z) v |= bbit;
-        if (e.w & kOver32) v |= probe_gather<uint32_t>(m, w, __ldg(sp) & ~(e.x | abit | bbit | skip), col0, nw32);
+        if (e.w & kOver32) v |= probe_gather_call<uint32_t>(m, w, __ldg(sp) & ~(e.x | abit | bbit | skip), col0, nw32);
         return v;
     } else {
         (void)sp;
@@ -174,7 +182,7 @@ __device__ __forceinline__ typename Fmt<FMT>::LW probe(const typename Fmt<FMT>::
         if (m & e.pa) v |= abit;
         if (m & e.pb) v |= bbit;
         const uint64_t over = (rest ^ bbit) & ~skip;
-        if (over) v |= probe_gather<uint64_t>(m, w, over, col0, nw32);
+        if (over) v |= probe_gather_call<uint64_t>(m, w, over, col0, nw32);
         return v;
     }
 }
@@ -187,11 +195,12 @@ __device__ __forceinline__ typename Fmt<FMT>::LW probe(const typename Fmt<FMT>::
 template <int FMT, bool SPLIT>
 __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict__ P32, int props, int frames,
                                                       uint32_t nw32, uint64_t cells, void* __restrict__ tab,
-                                                      void* __restrict__ s_only, uint32_t* __restrict__ task_ctr) {
+                                                      void* __restrict__ s_only, uint32_t* __restrict__ task_ctr,
+                                                      int nctr) {
     using LW = typename Fmt<FMT>::LW;
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     const int f = blockIdx.y;
-    if (w == 0 && f == 0) *task_ctr = 0;  // the labeling kernel that follows pulls tasks from 0
+    if (f == 0 && w < static_cast<uint32_t>(nctr)) task_ctr[w] = 0;  // the labeling launches that follow pull from 0
     if (w > nw32) return;
     LW s = 0, full = 0;
     uint32_t pa = 0, pb = 0, ia = 0, ib = 0;
@@ -547,9 +556,10 @@ __device__ __forceinline__ void stage_table(uint8_t* dst, const void* src, uint3
 template <int FMT, typename SW, bool SMEM, int K, int NT, bool IP>
 __global__ void __launch_bounds__(NT)
     label_stream_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
-                        const uint32_t* __restrict__ task_row, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
-                        const void* __restrict__ tab_g, uint32_t tab_bytes, const void* __restrict__ s_only_g,
-                        const uint32_t* __restrict__ P32, uint32_t nw32, SW* __restrict__ out) {
+                        const uint32_t* __restrict__ task_row, uint32_t task_begin, uint32_t ntasks,
+                        uint32_t* __restrict__ task_ctr, const void* __restrict__ tab_g, uint32_t tab_bytes,
+                        const void* __restrict__ s_only_g, const uint32_t* __restrict__ P32, uint32_t nw32,
+                        SW* __restrict__ out) {
     using LW = typename Fmt<FMT>::LW;
     static_assert(!(SMEM && FMT == 64), "the 64-prop entry table is read through L1");
     static_assert(K == kStreamK, "the HBM chunk layout is built for kStreamK pairs per lane");
@@ -569,7 +579,7 @@ __global__ void __launch_bounds__(NT)
 
     for (;;) {
         uint32_t t = 0;
-        if (lane == 0) t = atomicAdd(task_ctr, 1u);
+        if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= ntasks) break;
         const uint64_t p0 = task_pair[t];  // even: 16-byte aligned
@@ -644,9 +654,10 @@ size_t stream_ring_bytes(int warps) {
 template <int FMT, typename SW, int NT>
 __global__ void __launch_bounds__(NT)
     label_stream_tma_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
-                            const uint32_t* __restrict__ task_row, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
-                            const void* __restrict__ tab_g, uint32_t tab_bytes, const void* __restrict__ s_only_g,
-                            const uint32_t* __restrict__ P32, uint32_t nw32, SW* __restrict__ out) {
+                            const uint32_t* __restrict__ task_row, uint32_t task_begin, uint32_t ntasks,
+                            uint32_t* __restrict__ task_ctr, const void* __restrict__ tab_g, uint32_t tab_bytes,
+                            const void* __restrict__ s_only_g, const uint32_t* __restrict__ P32, uint32_t nw32,
+                            SW* __restrict__ out) {
     static_assert(FMT != 64, "split tables only");
     using LW = typename Fmt<FMT>::LW;
     constexpr int K = kStreamK;
@@ -680,7 +691,7 @@ __global__ void __launch_bounds__(NT)
     uint32_t ic = 0;     // chunk offset of the next chunk to issue
     auto claim = [&]() {
         uint32_t tn = 0;
-        if (lane == 0) tn = atomicAdd(task_ctr, 1u);
+        if (lane == 0) tn = task_begin + atomicAdd(task_ctr, 1u);
         it = __shfl_sync(0xffffffffu, tn, 0);
         ic = 0;
         if (it < ntasks) {
@@ -764,8 +775,8 @@ __global__ void __launch_bounds__(NT)
 template <int FMT, typename SW, int FPL, bool FULL>
 __global__ void __launch_bounds__(256)
     label_batch_kernel(const Pair* __restrict__ pairs, const uint64_t* __restrict__ task_pair,
-                       const uint32_t* __restrict__ task_row, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
-                       const void* __restrict__ tab_g, const void* __restrict__ s_only_g,
+                       const uint32_t* __restrict__ task_row, uint32_t task_begin, uint32_t ntasks,
+                       uint32_t* __restrict__ task_ctr, const void* __restrict__ tab_g, const void* __restrict__ s_only_g,
                        const uint32_t* __restrict__ P32, uint32_t nw32, int props, int frames,
                        const uint32_t* __restrict__ perm, SW* __restrict__ out) {
     using LW = typename Fmt<FMT>::LW;
@@ -781,7 +792,7 @@ __global__ void __launch_bounds__(256)
 
     for (;;) {
         uint32_t t = 0;
-        if (lane == 0) t = atomicAdd(task_ctr, 1u);
+        if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= ntasks) break;
         const uint64_t p0 = task_pair[t], p1 = task_pair[t + 1];
@@ -920,19 +931,20 @@ __global__ void resample_kernel(Grid2 vg, Grid2 wg, const Pose2* __restrict__ po
 // Host launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells, void* tab,
-                           void* s_only, uint32_t* task_ctr, cudaStream_t st) {
-    dim3 grid((nw32 + 1 + 255) / 256, static_cast<unsigned>(frames));
+                           void* s_only, uint32_t* task_ctr, int nctr, cudaStream_t st) {
+    const uint32_t nthreads = nw32 + 1 > static_cast<uint32_t>(nctr) ? nw32 + 1 : static_cast<uint32_t>(nctr);
+    dim3 grid((nthreads + 255) / 256, static_cast<unsigned>(frames));
     const int fmt = entry_format(props);
     if (frames == 1 && fmt == 16)
-        summary_kernel<16, true><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr);
+        summary_kernel<16, true><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr, nctr);
     else if (frames == 1 && fmt == 32)
-        summary_kernel<32, true><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr);
+        summary_kernel<32, true><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr, nctr);
     else if (fmt == 16)
-        summary_kernel<16, false><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr);
+        summary_kernel<16, false><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr, nctr);
     else if (fmt == 32)
-        summary_kernel<32, false><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr);
+        summary_kernel<32, false><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr, nctr);
     else
-        summary_kernel<64, false><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr);
+        summary_kernel<64, false><<<grid, 256, 0, st>>>(P32, props, frames, nw32, cells, tab, s_only, task_ctr, nctr);
     return cudaGetLastError();
 }
 
@@ -975,7 +987,7 @@ static cudaError_t launch_stream_v(const LaunchArgs& a, cudaStream_t st) {
             attr_set |= 1ull << dev;
         }
         if (tab_bytes % 16u || tab_bytes > kMaxSmemTable) return cudaErrorInvalidValue;  // never launch an uncompletable TMA copy
-        kern<<<sm_count(), NT, tab_bytes, st>>>(a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, a.sf, tab_bytes,
+        kern<<<sm_count(), NT, tab_bytes, st>>>(a.pairs, a.task_pair, a.task_row, a.task_begin, a.ntasks, a.task_ctr, a.sf, tab_bytes,
                                                 a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out));
     } else {
         static int per_sm = 0;
@@ -983,7 +995,7 @@ static cudaError_t launch_stream_v(const LaunchArgs& a, cudaStream_t st) {
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, 0);
             if (per_sm <= 0) per_sm = 4;
         }
-        kern<<<sm_count() * per_sm, NT, 0, st>>>(a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, a.sf, tab_bytes,
+        kern<<<sm_count() * per_sm, NT, 0, st>>>(a.pairs, a.task_pair, a.task_row, a.task_begin, a.ntasks, a.task_ctr, a.sf, tab_bytes,
                                                  a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out));
     }
     return cudaSuccess;
@@ -1009,7 +1021,7 @@ static cudaError_t launch_stream_tma(const LaunchArgs& a, uint32_t tab_bytes, cu
         if (e != cudaSuccess) return e;
         attr_set[dev] = smem;
     }
-    kern<<<sm_count(), NT, smem, st>>>(a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, a.sf, tab_bytes,
+    kern<<<sm_count(), NT, smem, st>>>(a.pairs, a.task_pair, a.task_row, a.task_begin, a.ntasks, a.task_ctr, a.sf, tab_bytes,
                                        a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out));
     return cudaSuccess;
 }
@@ -1037,7 +1049,7 @@ static void launch_batch_t(const LaunchArgs& a, cudaStream_t st) {
         if (per_sm <= 0) per_sm = 4;
     }
     label_batch_kernel<FMT, SW, FPL, FULL><<<sm_count() * per_sm, 256, 0, st>>>(
-        a.pairs, a.task_pair, a.task_row, a.ntasks, a.task_ctr, a.sf, a.s_only, a.P32, a.nw32, a.props, a.frames,
+        a.pairs, a.task_pair, a.task_row, a.task_begin, a.ntasks, a.task_ctr, a.sf, a.s_only, a.P32, a.nw32, a.props, a.frames,
         a.perm, static_cast<SW*>(a.out));
 }
 
@@ -1053,7 +1065,7 @@ static void launch_batch_fpl(const LaunchArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
-    if (a.ntasks == 0) return cudaSuccess;
+    if (a.ntasks <= a.task_begin) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     if (a.frames == 1) {
         switch (a.label_bytes) {

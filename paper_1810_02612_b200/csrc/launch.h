@@ -14,6 +14,7 @@ struct LaunchArgs {
     const Pair* pairs;
     const uint64_t* task_pair;
     const uint32_t* task_row;
+    uint32_t task_begin;  // tasks [task_begin, ntasks) of this launch
     uint32_t ntasks;
     const void* sf;
     const uint32_t* P32;
@@ -28,7 +29,7 @@ struct LaunchArgs {
 };
 
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
-                           void* tab, void* s_only, uint32_t* task_ctr, cudaStream_t st);
+                           void* tab, void* s_only, uint32_t* task_ctr, int nctr, cudaStream_t st);
 int entry_format(int props);
 size_t summary_entry_bytes(int props);
 size_t s_only_bytes(int props);

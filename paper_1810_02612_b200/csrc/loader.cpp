@@ -271,12 +271,10 @@ std::vector<uint64_t> shard_bounds(const WordCsr& t, int n) {
 
 namespace {
 
-void make_tasks(const std::vector<uint64_t>& pair_off, uint64_t rows, int target,
-                std::vector<uint32_t>* trow, std::vector<uint64_t>* tpair) {
-    trow->clear();
-    tpair->clear();
+// Tasks over rows [start, rows) appended to trow / tpair (no closing entry).
+void make_tasks_range(const std::vector<uint64_t>& pair_off, uint64_t start, uint64_t rows, int target,
+                      std::vector<uint32_t>* trow, std::vector<uint64_t>* tpair) {
     const uint64_t T = static_cast<uint64_t>(std::max(target, 1));
-    uint64_t start = 0;
     while (start < rows) {
         trow->push_back(static_cast<uint32_t>(start));
         tpair->push_back(pair_off[start]);
@@ -289,6 +287,21 @@ void make_tasks(const std::vector<uint64_t>& pair_off, uint64_t rows, int target
         if (end <= start) end = start + 1;
         start = end;
     }
+}
+
+// Tasks of every read-back block; block_task[c] = the block's first task.
+void make_tasks(const std::vector<uint64_t>& pair_off, const std::vector<uint64_t>& block_row, int target,
+                std::vector<uint32_t>* trow, std::vector<uint64_t>* tpair, std::vector<uint32_t>* block_task) {
+    trow->clear();
+    tpair->clear();
+    block_task->clear();
+    const size_t nb = block_row.size() - 1;
+    for (size_t c = 0; c < nb; ++c) {
+        block_task->push_back(static_cast<uint32_t>(trow->size()));
+        make_tasks_range(pair_off, block_row[c], block_row[c + 1], target, trow, tpair);
+    }
+    block_task->push_back(static_cast<uint32_t>(trow->size()));
+    const uint64_t rows = block_row[nb];
     trow->push_back(static_cast<uint32_t>(rows));
     tpair->push_back(pair_off[rows]);
 }
@@ -308,7 +321,8 @@ void build_stream_layout(const WordCsr& t, uint64_t row_begin, uint64_t row_end,
         const uint64_t n = t.offsets[row_begin + r + 1] - t.offsets[row_begin + r];
         pair_off[r + 1] = pair_off[r] + (n ? n : 1);
     }
-    make_tasks(pair_off, R, stream_task_pairs, &out->task_row_stream, &out->task_pair_stream);
+    make_tasks(pair_off, out->block_row, stream_task_pairs, &out->task_row_stream, &out->task_pair_stream,
+               &out->block_task_stream);
     const size_t nt = out->task_row_stream.size() - 1;
     std::vector<uint64_t> dst_off(nt + 1, 0);
     for (size_t k = 0; k < nt; ++k) {
@@ -345,16 +359,20 @@ void build_stream_layout(const WordCsr& t, uint64_t row_begin, uint64_t row_end,
 }
 
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
-                 uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs,
+                 uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs, int blocks,
                  PackedShard* out) {
     const uint64_t R = row_end - row_begin;
     out->row_begin = row_begin;
     out->row_end = row_end;
     out->words = t.offsets[row_end] - t.offsets[row_begin];
     out->perm.resize(R);
+    const uint64_t nb = static_cast<uint64_t>(std::max(1, blocks));
+    out->block_row.resize(nb + 1);
+    for (uint64_t c = 0; c <= nb; ++c) out->block_row[c] = R * c / nb;
     if (sort_rows) {
         // z-locality key: the row's median 32-bit word (rows are ascending in
-        // z-order, so this is a point inside the swept volume's z-range).
+        // z-order, so this is a point inside the swept volume's z-range);
+        // rows are sorted within their read-back block only.
         std::vector<uint64_t> key(R);
         parallel_chunks(R, 1 << 16, [&](uint64_t b, uint64_t e, int) {
             for (uint64_t r = b; r < e; ++r) {
@@ -363,7 +381,9 @@ void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool so
                 key[r] = (k << 32) | r;
             }
         });
-        std::sort(key.begin(), key.end());
+        for (uint64_t c = 0; c < nb; ++c)
+            std::sort(key.begin() + static_cast<std::ptrdiff_t>(out->block_row[c]),
+                      key.begin() + static_cast<std::ptrdiff_t>(out->block_row[c + 1]));
         for (uint64_t s = 0; s < R; ++s) out->perm[s] = static_cast<uint32_t>(key[s] & 0xffffffffu);
     } else {
         for (uint64_t s = 0; s < R; ++s) out->perm[s] = static_cast<uint32_t>(s);
@@ -391,7 +411,8 @@ void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool so
             dst[0].word |= kHead;
         }
     });
-    make_tasks(pair_off, R, batch_task_pairs, &out->task_row_batch, &out->task_pair_batch);
+    make_tasks(pair_off, out->block_row, batch_task_pairs, &out->task_row_batch, &out->task_pair_batch,
+               &out->block_task_batch);
     build_stream_layout(t, row_begin, row_end, sentinel_word, stream_task_pairs, out);
 }
 

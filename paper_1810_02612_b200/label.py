@@ -316,13 +316,15 @@ class LabelEngine:
     submissions, labels resident per shard (include/ltlgrid_gpu.h)."""
 
     def __init__(self, devices: Optional[Sequence[int]] = None, sort_rows: bool = True,
-                 stream_task_pairs: int = 0, batch_task_pairs: int = 0, profile: bool = False):
+                 stream_task_pairs: int = 0, batch_task_pairs: int = 0, profile: bool = False,
+                 readback_chunks: int = 0):
         self._L = N.lib()
         opts = N.Options()
         opts.sort_rows = 1 if sort_rows else 0
         opts.stream_task_pairs = stream_task_pairs
         opts.batch_task_pairs = batch_task_pairs
         opts.profile = 1 if profile else 0
+        opts.readback_chunks = readback_chunks
         h = C.c_void_p()
         if devices is None:
             st = self._L.ltlg_create_ex(None, 1, C.byref(opts), C.byref(h))

@@ -36,6 +36,8 @@ ENGINE_VARIANTS = [
     dict(sort_rows=False),
     dict(stream_task_pairs=1, batch_task_pairs=1),
     dict(stream_task_pairs=37, batch_task_pairs=5, sort_rows=False),
+    dict(readback_chunks=3),
+    dict(readback_chunks=7, stream_task_pairs=37, batch_task_pairs=5),
 ]
 
 
@@ -305,6 +307,31 @@ def test_empty_and_degenerate():
     assert eng.get_labels(0) == LabelMatrix(4, 2)  # all-false rows never hit (test_label.cpp:68-73)
     eng.submit_grid(64, 0, np.zeros(0, np.uint64), 2)
     assert eng.get_labels(1) == LabelMatrix(4, 0)
+    eng.close()
+
+
+@pytest.mark.parametrize("chunks", [2, 8])
+@pytest.mark.parametrize("devices", [[0], [0, 0, 0]])
+def test_chunked_readback(devices, chunks):
+    # readback_chunks: rows z-sorted within blocks, one launch per block, the
+    # label copy of block c overlapping the labelling of later blocks
+    depth, E, props, F = 16, 60_001, 20, 6
+    prm = SyntheticPRM(seed=21, depth=depth)
+    t = prm.words(0, E)
+    off, idx = prm.csr(0, E)
+    P = props_words(23, depth, props, 0, F)
+    eng = LabelEngine(devices=devices, readback_chunks=chunks)
+    eng.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
+    for rep in range(2):  # twice: the per-block task counters are reset per submit
+        eng.submit_grid(1 << depth, props, P, F)
+        packed = eng.get_labels_packed()
+        for f in range(F):
+            want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[f])
+            assert np.array_equal(packed[:, f].astype(np.uint64), want), (rep, f)
+    eng.submit_grid(1 << depth, props, P[4], 1)
+    want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[4])
+    assert np.array_equal(eng.get_labels_packed()[:, 0].astype(np.uint64), want)
+    assert eng.get_labels(0) == LabelMatrix(E, props, want)
     eng.close()
 
 
