@@ -14,7 +14,7 @@ python tools/bench_summary.py $out/${tag}_bench.json
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $out/${tag}_bench_ref.json 2> $out/${tag}_bench_ref.err; echo "ref rc=$?"; cat $out/${tag}_bench_ref.json
 # launch list (cold-cache, serialised): shares only
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/${tag}_launches.csv \
-    python bench.py --quick --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > $out/${tag}_ncu_bench.log 2>&1; echo "ncu launches rc=$?"
+    python bench.py --quick --steps 3 --warmup 3 --no-cpu-baseline > $out/${tag}_ncu_bench.log 2>&1; echo "ncu launches rc=$?"
 # full capture of the top kernels
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:label_batch_kernel -s 2 -c 1 \
     -o $out/${tag}_batch python bench.py --quick --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $out/${tag}_ncu_batch.log 2>&1; echo "ncu batch rc=$?"

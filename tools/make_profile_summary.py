@@ -1,0 +1,59 @@
+"""Write the committed evidence for one GPU pass: profiles/<name>_ncu_summary.md
+(launch list shares + key counters + SASS mix of both labeling kernels),
+<name>_bench.json, <name>_bench_ref.json, <name>_launches.csv, and update
+profiles/traffic.json (dram bytes per launch, read by bench.py).
+
+  python tools/make_profile_summary.py gpurun_out/r02 profiles/round1
+"""
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+src, dst = sys.argv[1], sys.argv[2]
+here = os.path.dirname(os.path.abspath(__file__))
+lines = []
+
+
+def run(*cmd):
+    return subprocess.run(list(cmd), capture_output=True, text=True).stdout
+
+
+lines.append(f"# {os.path.basename(dst)}: ncu evidence (`tools/gpu_full.sh`, one B200, `--clock-control none`)\n")
+lines.append("## Launch list of `python bench.py --quick --steps 3 --warmup 3 --no-cpu-baseline`")
+lines.append("(gpu__time_duration.sum; cold-cache and serialised, so compare shares, not absolutes)\n```")
+lines.append(run("python", os.path.join(here, "ncu_launches.py"), src + "_launches.csv").rstrip())
+lines.append("```")
+traffic_path = os.path.join(os.path.dirname(dst), "traffic.json")
+traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+for kind in ("batch", "stream"):
+    rep = f"{src}_{kind}.ncu-rep"
+    if not os.path.exists(rep):
+        continue
+    lines.append(f"\n## `ncu --set full`: {kind} labeling kernel\n```")
+    lines.append(run("python", os.path.join(here, "ncu_brief.py"), rep).rstrip())
+    raw = list(csv.reader(io.StringIO(run("ncu", "-i", rep, "--page", "raw", "--csv"))))
+    d = dict(zip(raw[0], raw[2]))
+    u = dict(zip(raw[0], raw[1]))
+    for k in ["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+              "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+              "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+              "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
+              "smsp__thread_inst_executed_per_inst_executed.ratio"]:
+        lines.append(f"  {k:60s} {d.get(k)}")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tb = sum(float(d[k]) * scale.get(u[k], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    name = d["Kernel Name"].split("<")[0].replace("void ", "").split("::")[-1]
+    traffic[name] = tb
+    lines.append(f"  dram read+write bytes per launch (traffic)                   {tb:.4g}")
+    lines.append(run("python", os.path.join(here, "ncu_sass.py"), rep, "12").rstrip())
+    lines.append("```")
+open(dst + "_ncu_summary.md", "w").write("\n".join(lines) + "\n")
+json.dump(traffic, open(traffic_path, "w"), indent=1)
+for suffix in ("_bench.json", "_bench_ref.json", "_launches.csv"):
+    if os.path.exists(src + suffix):
+        shutil.copy(src + suffix, dst + suffix)
+print("wrote", dst + "_ncu_summary.md", traffic)
