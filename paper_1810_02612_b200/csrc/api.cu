@@ -300,12 +300,12 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         CK(s.sf.reserve(frames == 1 && props <= 32 ? split_table_bytes(props, nw32)
                                                    : static_cast<size_t>(nw32 + 1) * frames * summary_entry_bytes(props)),
            "allocate summary");
-        CK(s.ctr.reserve(64 * sizeof(uint32_t)), "allocate task counters");
+        CK(s.ctr.reserve(64 * kCtrStride * sizeof(uint32_t)), "allocate task counters");
         CK(s.s_only.reserve(static_cast<size_t>(nw32 + 1) * frames * s_only_bytes(props)), "allocate summary");
         const bool prof = ctx->opts.profile != 0;
         if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
         CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
-                          s.s_only.ptr, s.ctr.ptr, static_cast<int>(s.block_row.size() - 1), s.stream),
+                          s.s_only.ptr, s.ctr.ptr, static_cast<int>((s.block_row.size() - 1) * kCtrStride), s.stream),
            "summary kernel");
         if (prof) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
@@ -331,7 +331,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         for (int c = 0; c < nb; ++c) {
             a.task_begin = bt[static_cast<size_t>(c)];
             a.ntasks = nb == 1 ? bt.back() : bt[static_cast<size_t>(c) + 1];
-            a.task_ctr = s.ctr.ptr + c;
+            a.task_ctr = s.ctr.ptr + static_cast<size_t>(c) * kCtrStride;
             CK(launch_label(a, s.stream), "label kernel");
             if (nb > 1) CK(cudaEventRecord(s.block_done[static_cast<size_t>(c)], s.stream), "event");
         }

@@ -106,6 +106,14 @@ __device__ __forceinline__ uint2 ld_stream8(const void* p) {
 }
 
 __device__ __forceinline__ uint4 ld_entry(const uint4* p) { return __ldg(p); }
+
+// base + idx elements as one IMAD.WIDE (FMA pipe) instead of 64-bit ALU adds
+template <typename T>
+__device__ __forceinline__ const T* index_wide(const T* base, uint32_t idx) {
+    uint64_t r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(idx), "n"(static_cast<int>(sizeof(T))), "l"(base));
+    return reinterpret_cast<const T*>(r);
+}
 __device__ __forceinline__ SF<uint64_t> ld_entry(const SF<uint64_t>* p) {
     const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
     const uint2 w = __ldg(reinterpret_cast<const uint2*>(p) + 2);
@@ -148,11 +156,12 @@ __device__ __noinline__ LW probe_gather_call(uint32_t m, uint32_t w, LW over, co
 
 // Label contribution of one stored pair (mask m of word w) for one frame.
 //   e    : the frame's summary entry of word w
-//   sp   : the frame's S mask of word w (read only on the rare over path)
+//   sp   : base + index of the frame's S mask of word w (read only on the
+//          rare over path, so its address is formed there)
 //   skip : props already known to hit (their probes are unnecessary)
 template <int FMT>
 __device__ __forceinline__ typename Fmt<FMT>::LW probe(const typename Fmt<FMT>::E& e, uint32_t m, uint32_t w,
-                                                       const typename Fmt<FMT>::LW* sp,
+                                                       const typename Fmt<FMT>::LW* s_base, uint32_t s_idx,
                                                        typename Fmt<FMT>::LW skip,
                                                        const uint32_t* __restrict__ col0, uint32_t nw32) {
     if constexpr (FMT == 16) {
@@ -161,7 +170,7 @@ __device__ __forceinline__ typename Fmt<FMT>::LW probe(const typename Fmt<FMT>::
         if (m & e.z) v |= e.w >> 16;
         if (e.x & kOver16) {
             const uint32_t known = (e.x | e.w | (e.w >> 16)) & 0xffffu;
-            v |= probe_gather_call<uint32_t>(m, w, __ldg(sp) & ~known & ~skip, col0, nw32);
+            v |= probe_gather_call<uint32_t>(m, w, __ldg(s_base + s_idx) & ~known & ~skip, col0, nw32);
         }
         return v;
     } else if constexpr (FMT == 32) {
@@ -170,10 +179,12 @@ __device__ __forceinline__ typename Fmt<FMT>::LW probe(const typename Fmt<FMT>::
         uint32_t v = e.x;
         if (m & e.y) v |= abit;
         if (m & e.z) v |= bbit;
-        if (e.w & kOver32) v |= probe_gather_call<uint32_t>(m, w, __ldg(sp) & ~(e.x | abit | bbit | skip), col0, nw32);
+        if (e.w & kOver32)
+            v |= probe_gather_call<uint32_t>(m, w, __ldg(s_base + s_idx) & ~(e.x | abit | bbit | skip), col0, nw32);
         return v;
     } else {
-        (void)sp;
+        (void)s_base;
+        (void)s_idx;
         const uint64_t partial = e.s & ~e.f;
         const uint64_t abit = partial & (~partial + 1);
         const uint64_t rest = partial ^ abit;
@@ -376,7 +387,7 @@ __device__ __forceinline__ void stream_chunk(const StreamCtx<FMT, SW, SMEM>& sc,
             const uint32_t wh = (k & 1) ? cur[k / 2].w : cur[k / 2].y;
             heads |= (wh >> 31) << k;
             const uint32_t w = wh & kWordMask;
-            v[k] = probe<FMT>(ld_entry(reinterpret_cast<const E*>(sc.tab) + w), mk, w, sc.s_only + w, LW(0), sc.P32,
+            v[k] = probe<FMT>(ld_entry(reinterpret_cast<const E*>(sc.tab) + w), mk, w, sc.s_only, w, LW(0), sc.P32,
                               sc.nw32);
             if (k == K / 2 - 1) reload(0, K / 4);
         }
@@ -807,36 +818,39 @@ __global__ void __launch_bounds__(256)
             for (int q = 0; q < FPL; ++q)
                 if (fv[q]) o[32 * q] = static_cast<SW>(acc[q]);
         };
+        // one pair (mask m, word field wh), broadcast to every lane
+        auto pair_step = [&](uint32_t m, uint32_t wh) {
+            if (wh & kHead) {  // warp-uniform
+                if (row >= r0) store(row);
+                ++row;
+#pragma unroll
+                for (int q = 0; q < FPL; ++q) acc[q] = 0;
+            }
+            const uint32_t w = wh & kWordMask;
+            const uint32_t off = w * static_cast<uint32_t>(frames);
+            if (m == 0xffffffffu) {  // warp-uniform: the whole word is swept
+                const LW* sp = index_wide(lane_s, off);
+#pragma unroll
+                for (int q = 0; q < FPL; ++q)
+                    if (fv[q]) acc[q] |= __ldg(sp + 32 * q);
+            } else {
+                const E* ep = index_wide(lane_tab, off);
+#pragma unroll
+                for (int q = 0; q < FPL; ++q)
+                    if (fv[q]) {
+                        const E e = ld_entry(ep + 32 * q);
+                        acc[q] |= probe<FMT>(e, m, w, lane_s, off + 32 * q, acc[q],
+                                             lane_P + 32 * q * frame_stride, nw32);
+                    }
+            }
+        };
         uint2 cur = ld_stream8(pairs + p0 + lane);
         for (uint64_t c = p0; c < p1; c += 32) {
             uint2 nxt = cur;
             if (c + 32 < p1) nxt = ld_stream8(pairs + c + 32 + lane);
             const int n = static_cast<int>(p1 - c < 32 ? p1 - c : 32);
-            for (int i = 0; i < n; ++i) {
-                const uint32_t m = __shfl_sync(0xffffffffu, cur.x, i);
-                const uint32_t wh = __shfl_sync(0xffffffffu, cur.y, i);
-                if (wh & kHead) {  // warp-uniform
-                    if (row >= r0) store(row);
-                    ++row;
-#pragma unroll
-                    for (int q = 0; q < FPL; ++q) acc[q] = 0;
-                }
-                const uint32_t w = wh & kWordMask;
-                const uint32_t off = w * static_cast<uint32_t>(frames);
-                if (m == 0xffffffffu) {  // warp-uniform: the whole word is swept
-#pragma unroll
-                    for (int q = 0; q < FPL; ++q)
-                        if (fv[q]) acc[q] |= __ldg(lane_s + off + 32 * q);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < FPL; ++q)
-                        if (fv[q]) {
-                            const E e = ld_entry(lane_tab + off + 32 * q);
-                            acc[q] |= probe<FMT>(e, m, w, lane_s + off + 32 * q, acc[q],
-                                                 lane_P + 32 * q * frame_stride, nw32);
-                        }
-                }
-            }
+            for (int i = 0; i < n; ++i)
+                pair_step(__shfl_sync(0xffffffffu, cur.x, i), __shfl_sync(0xffffffffu, cur.y, i));
             cur = nxt;
         }
         if (row >= r0) store(row);

@@ -10,6 +10,8 @@
 
 namespace ltlg {
 
+constexpr uint32_t kCtrStride = 256;  // task counters per launch (one per SM slice)
+
 struct LaunchArgs {
     const Pair* pairs;
     const uint64_t* task_pair;
@@ -24,7 +26,7 @@ struct LaunchArgs {
     const uint32_t* perm;
     void* out;
     int label_bytes;
-    uint32_t* task_ctr;  // device counter, reset by the summary kernel
+    uint32_t* task_ctr;  // this launch's kCtrStride device counters, reset by the summary kernel
     const void* s_only;  // S mask per (word, frame): over-path probes, full-mask pairs
 };
 
