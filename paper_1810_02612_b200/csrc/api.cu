@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -96,6 +97,9 @@ struct Shard {
     std::vector<cudaEvent_t> block_done;                       // per block, recorded after its launch
     int blocks_last = 0;                                       // blocks labelled by the last submit
     DevBuf<Pair> pairs, pairs_s;  // plain (multi-frame) and single-frame layouts
+    DevBuf<uint8_t> t64;          // single-frame 64-cell-word copy
+    DevBuf<uint64_t> tbyte64;
+    DevBuf<uint32_t> tn64;
     DevBuf<uint32_t> perm, trow_s, trow_b;
     DevBuf<uint64_t> tpair_s, tpair_b;
     DevBuf<uint64_t> P;  // frames x props x nw64
@@ -186,12 +190,15 @@ ltlg_status upload_shard(ltlg_ctx* ctx, Shard& s, const PackedShard& p) {
     ltlg_status st;
     if ((st = put(s.pairs, p.pairs, "upload T pairs")) != LTLG_OK) return st;
     if ((st = put(s.pairs_s, p.pairs_stream, "upload T pairs")) != LTLG_OK) return st;
+    if ((st = put(s.t64, p.stream64, "upload T pairs")) != LTLG_OK) return st;
+    if ((st = put(s.tbyte64, p.task_byte64, "upload tasks")) != LTLG_OK) return st;
+    if ((st = put(s.tn64, p.task_n64, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.perm, p.perm, "upload row permutation")) != LTLG_OK) return st;
     if ((st = put(s.trow_s, p.task_row_stream, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.tpair_s, p.task_pair_stream, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.trow_b, p.task_row_batch, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.tpair_b, p.task_pair_batch, "upload tasks")) != LTLG_OK) return st;
-    ctx->t_bytes += (p.pairs.size() + p.pairs_stream.size()) * sizeof(Pair) + p.perm.size() * 4;
+    ctx->t_bytes += (p.pairs.size() + p.pairs_stream.size()) * sizeof(Pair) + p.stream64.size() + p.perm.size() * 4;
     return LTLG_OK;
 }
 
@@ -297,16 +304,27 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
             s.blocks_last = 0;
             continue;
         }
-        CK(s.sf.reserve(frames == 1 && props <= 32 ? split_table_bytes(props, nw32)
-                                                   : static_cast<size_t>(nw32 + 1) * frames * summary_entry_bytes(props)),
+        const uint32_t nw64 = nw32 / 2;
+        // 64-cell-word single-frame path (dev knob LTLG_STREAM64=0 selects the 32-cell copy for A/B runs)
+        static const bool wide_ok = !getenv("LTLG_STREAM64") || atoi(getenv("LTLG_STREAM64")) != 0;
+        const bool wide = wide_ok && frames == 1 && props <= 32;
+        CK(s.sf.reserve(wide ? split64_table_bytes(props, nw64)
+                             : frames == 1 && props <= 32
+                                   ? split_table_bytes(props, nw32)
+                                   : static_cast<size_t>(nw32 + 1) * frames * summary_entry_bytes(props)),
            "allocate summary");
         CK(s.ctr.reserve(64 * kCtrStride * sizeof(uint32_t)), "allocate task counters");
         CK(s.s_only.reserve(static_cast<size_t>(nw32 + 1) * frames * s_only_bytes(props)), "allocate summary");
         const bool prof = ctx->opts.profile != 0;
         if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
-        CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
-                          s.s_only.ptr, s.ctr.ptr, static_cast<int>((s.block_row.size() - 1) * kCtrStride), s.stream),
-           "summary kernel");
+        const int nctr = static_cast<int>((s.block_row.size() - 1) * kCtrStride);
+        if (wide)
+            CK(launch_summary64(s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr, s.ctr.ptr, nctr, s.stream),
+               "summary kernel");
+        else
+            CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
+                              s.s_only.ptr, s.ctr.ptr, nctr, s.stream),
+               "summary kernel");
         if (prof) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
         a.pairs = s.pairs.ptr;
@@ -321,6 +339,12 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         a.s_only = s.s_only.ptr;
         const bool single = frames == 1;
         if (single) a.pairs = s.pairs_s.ptr;
+        if (wide) {
+            a.t64 = s.t64.ptr;
+            a.task_byte64 = s.tbyte64.ptr;
+            a.task_n64 = s.tn64.ptr;
+            a.nw64 = nw64;
+        }
         a.task_pair = single ? s.tpair_s.ptr : s.tpair_b.ptr;
         a.task_row = single ? s.trow_s.ptr : s.trow_b.ptr;
         // one launch per read-back block for multi-frame submits (their labels are
@@ -468,6 +492,9 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         if (s.stream) cudaStreamSynchronize(s.stream);
         s.pairs.release();
         s.pairs_s.release();
+        s.t64.release();
+        s.tbyte64.release();
+        s.tn64.release();
         s.perm.release();
         s.trow_s.release();
         s.trow_b.release();

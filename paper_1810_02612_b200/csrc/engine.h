@@ -39,6 +39,11 @@ struct PackedShard {
     uint64_t words = 0;                   // W32 of the shard
     std::vector<Pair> pairs;              // sorted-row order, padded (see kPairPad)
     std::vector<Pair> pairs_stream;       // the same pairs in the single-frame layout (see kStreamK)
+    // single-frame 64-cell-word copy (see kStreamK): per stream task, its bytes
+    // start at task_byte64[t] and hold task_n64[t] (mask64, word64) pairs
+    std::vector<uint8_t> stream64;
+    std::vector<uint64_t> task_byte64;    // ntasks + 1
+    std::vector<uint32_t> task_n64;       // ntasks
     uint64_t n_pairs = 0;                 // meaningful pairs (incl. sentinels)
     std::vector<uint32_t> perm;           // sorted position -> local original row
     // warp tasks: [row_begin, row_end) in sorted positions, pairs [pair_begin, pair_end)
@@ -63,6 +68,13 @@ constexpr uint64_t kPairPad = 512;  // tail padding so vector loads never leave 
 // an odd pair count gets one no-op pair appended).
 constexpr int kStreamK = 8;
 constexpr uint64_t kStreamCH = 32 * kStreamK;
+// The 64-cell-word single-frame copy uses the same chunking with 12-byte
+// pairs stored SoA per chunk: a full chunk is 2 KB of u64 masks (piece h*32+l
+// = masks of pairs K*l+2h, K*l+2h+1) then 1 KB of u32 word fields (piece
+// h*32+l = words of pairs K*l+4h .. K*l+4h+3); a partial last chunk of n
+// pairs is n masks then n words, each region padded to 16 bytes.
+constexpr uint64_t kChunk64Bytes = kStreamCH * 12;
+constexpr uint64_t kPad64Bytes = 4096;  // tail padding: lane-contiguous loads of a partial chunk stay inside
 
 // Host-side loader (loader.cpp).
 bool validate_csr(uint64_t rows, uint64_t cols, const uint64_t* offsets, uint64_t n_offsets,

@@ -85,6 +85,16 @@ size_t s_only_bytes(int props) { return props <= 32 ? 4 : 8; }
 __host__ __device__ __forceinline__ uint32_t split_x_offset(int fmt, uint32_t nw32) {
     return ((fmt == 16 ? 4u : 8u) * (nw32 + 1) + 15u) & ~15u;
 }
+// 64-cell-word split table: M[w64] as above, then (16-byte aligned) X[w64] =
+// {Pa lo, Pa hi, Pb lo, Pb hi}.
+__host__ __device__ __forceinline__ uint32_t split64_x_offset(int fmt, uint32_t nw64) {
+    return ((fmt == 16 ? 4u : 8u) * (nw64 + 1) + 15u) & ~15u;
+}
+size_t split64_table_bytes(int props, uint32_t nw64) {
+    const int fmt = entry_format(props);
+    if (fmt == 64) return 0;
+    return split64_x_offset(fmt, nw64) + 16u * (nw64 + 1);
+}
 size_t split_table_bytes(int props, uint32_t nw32) {
     const int fmt = entry_format(props);
     if (fmt == 64) return 0;
@@ -261,6 +271,51 @@ __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict
     static_cast<LW*>(s_only)[idx] = s;
 }
 
+// Single-frame summary over 64-cell words (P's own u64 column words): the
+// split table of split64_x_offset + S per word.  Thread per word.
+template <int FMT>
+__global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restrict__ P64, int props, uint32_t nw64,
+                                                        uint64_t cells, uint8_t* __restrict__ tab,
+                                                        uint32_t* __restrict__ s_only, uint32_t* __restrict__ task_ctr,
+                                                        int nctr) {
+    static_assert(FMT != 64, "split tables hold <= 32 props");
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w < static_cast<uint32_t>(nctr)) task_ctr[w] = 0;  // the labeling launches that follow pull from 0
+    if (w > nw64) return;
+    uint32_t s = 0, full = 0, ia = 0, ib = 0;
+    uint64_t pa = 0, pb = 0;
+    int np = 0;
+    const uint64_t lo = static_cast<uint64_t>(w) * 64;
+    if (w < nw64 && lo < cells) {
+        const uint64_t valid = (cells - lo >= 64) ? ~0ull : ((1ull << (cells - lo)) - 1ull);
+#pragma unroll 4
+        for (int j = 0; j < props; ++j) {
+            const uint64_t x = P64[static_cast<uint64_t>(j) * nw64 + w] & valid;
+            s |= static_cast<uint32_t>(x != 0) << j;
+            full |= static_cast<uint32_t>(x == valid) << j;
+            if (x != 0 && x != valid) {
+                if (np == 0) {
+                    pa = x;
+                    ia = static_cast<uint32_t>(j);
+                } else if (np == 1) {
+                    pb = x;
+                    ib = static_cast<uint32_t>(j);
+                }
+                ++np;
+            }
+        }
+    }
+    const uint32_t over = np > 2 ? 1u : 0u, part = np > 0 ? 1u : 0u;
+    if constexpr (FMT == 16)
+        reinterpret_cast<uint32_t*>(tab)[w] = (full << 16) | (16u + ia) | ((16u + ib) << 5) | (part << 10) | (over << 11);
+    else
+        reinterpret_cast<uint2*>(tab)[w] = make_uint2(full, ia | (ib << 8) | (part << 16) | (over << 17));
+    reinterpret_cast<uint4*>(tab + split64_x_offset(FMT, nw64))[w] =
+        make_uint4(static_cast<uint32_t>(pa), static_cast<uint32_t>(pa >> 32), static_cast<uint32_t>(pb),
+                   static_cast<uint32_t>(pb >> 32));
+    s_only[w] = s;
+}
+
 // ---------------------------------------------------------------------------
 // TMA bulk copy + mbarrier helpers (sm_90+ PTX, used on sm_100a)
 // ---------------------------------------------------------------------------
@@ -297,6 +352,12 @@ __device__ __forceinline__ uint2 lds64(uint32_t a) {
     uint2 v;
     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
     return v;
+}
+// x = smem[a] (16 B) if c != 0, else unchanged (callers pre-zero)
+__device__ __forceinline__ void lds128_if(uint32_t c, uint32_t a, uint4& x) {
+    asm("{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n @p ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n}\n"
+        : "+r"(x.x), "+r"(x.y), "+r"(x.z), "+r"(x.w)
+        : "r"(c), "r"(a));
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     uint32_t v;
@@ -366,6 +427,93 @@ struct RowState {
     int32_t open_row;    // row owning `carry`
     LW carry;
 };
+
+// Row recovery for one warp chunk: lane l's K consecutive pairs have label
+// contributions v[0..K) and HEAD bits `heads`; closes every row that ends in
+// the chunk (stores rows in [rs.r0, rs.r1) only) and carries the open row.
+template <int FMT, typename SW, bool SMEM, int K>
+__device__ __forceinline__ void segment_chunk(const StreamCtx<FMT, SW, SMEM>& sc,
+                                              RowState<typename Fmt<FMT>::LW>& rs, uint32_t heads,
+                                              const typename Fmt<FMT>::LW (&v)[K]) {
+    using LW = typename Fmt<FMT>::LW;
+    constexpr int kShift = StreamCtx<FMT, SW, SMEM>::kShift;
+    const int lane = sc.lane;
+    SW* out = sc.out;
+    if (!__any_sync(0xffffffffu, (heads & (heads - 1)) != 0)) {
+        // ---- fast path: every lane holds at most one head ----------
+        const uint32_t hmask_all = __ballot_sync(0xffffffffu, heads != 0);
+        const int hb = __popc(hmask_all & sc.lt);  // rows opened in lower lanes
+        LW pre = 0, post = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if ((heads & ((2u << k) - 1u)) == 0) pre |= v[k];
+            else post |= v[k];
+        }
+        const uint32_t hm = hmask_all & sc.le;
+        const int seg = hm ? 31 - __clz(hm) : 0;
+        LW x = heads ? post : pre;
+        if (lane == 0 && !heads) x |= rs.carry;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const LW y = shfl_up(x, d);
+            if (lane - d >= seg) x |= y;
+        }
+        LW excl = shfl_up(x, 1);
+        if (lane == 0) excl = rs.carry;
+        if (heads) {
+            const int32_t row = rs.open_row + hb;  // the row open before this lane's head
+            if (row >= rs.r0 && row < rs.r1) out[row] = static_cast<SW>((excl | pre) >> kShift);
+        }
+        rs.carry = shfl_idx(x, 31);
+        rs.open_row += __popc(hmask_all);
+    } else {
+        // ---- general path: lanes may hold several heads -----------
+        const int nh = __popc(heads);
+        int incl = nh;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += y;
+        }
+        const int hb = incl - nh;
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        // lane-local segmentation: rows that start and end inside this lane
+        LW pre = 0, cur_or = 0;
+        int seen = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (heads >> k & 1u) {
+                if (seen) {
+                    const int32_t row = rs.open_row + hb + seen;
+                    if (row < rs.r1) out[row] = static_cast<SW>(cur_or >> kShift);
+                } else {
+                    pre = cur_or;
+                }
+                ++seen;
+                cur_or = 0;
+            }
+            cur_or |= v[k];
+        }
+        if (!nh) pre = cur_or;
+        const uint32_t hmask = __ballot_sync(0xffffffffu, nh > 0) & sc.le;
+        const int seg = hmask ? 31 - __clz(hmask) : 0;
+        LW x = nh ? cur_or : pre;
+        if (lane == 0 && !nh) x |= rs.carry;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const LW y = shfl_up(x, d);
+            if (lane - d >= seg) x |= y;
+        }
+        LW excl = shfl_up(x, 1);
+        if (lane == 0) excl = rs.carry;
+        if (nh) {
+            const int32_t row = rs.open_row + hb;  // the row open before this lane's first head
+            if (row >= rs.r0 && row < rs.r1) out[row] = static_cast<SW>((excl | pre) >> kShift);
+        }
+        rs.carry = shfl_idx(x, 31);
+        rs.open_row += tot;
+    }
+}
 
 // One warp chunk held in cur (lane-contiguous K pairs).  `reload(h0, h1)` is
 // called once pieces [h0, h1) of cur are no longer needed (after each half),
@@ -465,81 +613,7 @@ __device__ __forceinline__ void stream_chunk(const StreamCtx<FMT, SW, SMEM>& sc,
         }
         reload(K / 4, K / 2);
     }
-    SW* out = sc.out;
-    if (!__any_sync(0xffffffffu, (heads & (heads - 1)) != 0)) {
-        // ---- fast path: every lane holds at most one head ----------
-        const uint32_t hmask_all = __ballot_sync(0xffffffffu, heads != 0);
-        const int hb = __popc(hmask_all & sc.lt);  // rows opened in lower lanes
-        LW pre = 0, post = 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if ((heads & ((2u << k) - 1u)) == 0) pre |= v[k];
-            else post |= v[k];
-        }
-        const uint32_t hm = hmask_all & sc.le;
-        const int seg = hm ? 31 - __clz(hm) : 0;
-        LW x = heads ? post : pre;
-        if (lane == 0 && !heads) x |= rs.carry;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const LW y = shfl_up(x, d);
-            if (lane - d >= seg) x |= y;
-        }
-        LW excl = shfl_up(x, 1);
-        if (lane == 0) excl = rs.carry;
-        if (heads) {
-            const int32_t row = rs.open_row + hb;  // the row open before this lane's head
-            if (row >= rs.r0 && row < rs.r1) out[row] = static_cast<SW>((excl | pre) >> kShift);
-        }
-        rs.carry = shfl_idx(x, 31);
-        rs.open_row += __popc(hmask_all);
-    } else {
-        // ---- general path: lanes may hold several heads -----------
-        const int nh = __popc(heads);
-        int incl = nh;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += y;
-        }
-        const int hb = incl - nh;
-        const int tot = __shfl_sync(0xffffffffu, incl, 31);
-        // lane-local segmentation: rows that start and end inside this lane
-        LW pre = 0, cur_or = 0;
-        int seen = 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (heads >> k & 1u) {
-                if (seen) {
-                    const int32_t row = rs.open_row + hb + seen;
-                    if (row < rs.r1) out[row] = static_cast<SW>(cur_or >> kShift);
-                } else {
-                    pre = cur_or;
-                }
-                ++seen;
-                cur_or = 0;
-            }
-            cur_or |= v[k];
-        }
-        if (!nh) pre = cur_or;
-        const uint32_t hmask = __ballot_sync(0xffffffffu, nh > 0) & sc.le;
-        const int seg = hmask ? 31 - __clz(hmask) : 0;
-        LW x = nh ? cur_or : pre;
-        if (lane == 0 && !nh) x |= rs.carry;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const LW y = shfl_up(x, d);
-            if (lane - d >= seg) x |= y;
-        }
-        LW excl = shfl_up(x, 1);
-        if (lane == 0) excl = rs.carry;
-        if (nh) {
-            const int32_t row = rs.open_row + hb;  // the row open before this lane's first head
-            if (row >= rs.r0 && row < rs.r1) out[row] = static_cast<SW>((excl | pre) >> kShift);
-        }
-        rs.carry = shfl_idx(x, 31);
-        rs.open_row += tot;
-    }
+    segment_chunk<FMT, SW, SMEM, K>(sc, rs, heads, v);
 }
 
 template <int FMT, typename SW, bool SMEM>
@@ -641,6 +715,182 @@ __global__ void __launch_bounds__(NT)
                 if (c + 2 * CH < end) load_chunk(bufA, c + 2 * CH, 0, K / 2);
                 stream_chunk<FMT, SW, SMEM, K>(sc, rs, bufB, none);
             }
+        }
+        stream_close_task(sc, rs);
+    }
+    if constexpr (SMEM) {
+        if (!tab_ready) mbar_wait(&tab_bar, 0);  // never leave with a bulk copy in flight
+    }
+}
+
+// 64-cell-word variant (<= 32 props): T from its 12-byte-pair SoA copy
+// (kChunk64Bytes, engine.h), one (mask64, word64) pair per swept 64-cell word
+// -- 41% fewer pairs per row than 32-cell words at 512^2 --
+// against the 64-cell split summary (summary64_kernel).  Same lane
+// ownership, in-place prefetch and row segmentation as label_stream_kernel.
+template <int FMT, typename SW, bool SMEM, int NT>
+__global__ void __launch_bounds__(NT)
+    label_stream64_kernel(const uint8_t* __restrict__ t64, const uint64_t* __restrict__ task_byte,
+                          const uint32_t* __restrict__ task_n, const uint32_t* __restrict__ task_row,
+                          uint32_t task_begin, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
+                          const void* __restrict__ tab_g, uint32_t tab_bytes, const uint32_t* __restrict__ s_only,
+                          const uint64_t* __restrict__ P64, uint32_t nw64, SW* __restrict__ out) {
+    static_assert(FMT != 64, "split tables hold <= 32 props");
+    using LW = uint32_t;
+    constexpr int K = kStreamK;
+    constexpr uint32_t CH = kStreamCH;
+    constexpr int kShift = FMT == 16 ? 16 : 0;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    __shared__ uint64_t tab_bar;
+    const int lane = threadIdx.x & 31;
+    const uint8_t* tab = static_cast<const uint8_t*>(tab_g);
+    if constexpr (SMEM) {
+        stage_table(smem_raw, tab_g, tab_bytes, &tab_bar);
+        tab = smem_raw;
+    }
+    const uint32_t xoff = split64_x_offset(FMT, nw64);
+    StreamCtx<FMT, SW, SMEM> sc{tab, tab + xoff, SMEM ? smem_u32(tab) : 0u, SMEM ? smem_u32(tab) + xoff : 0u, s_only,
+                               reinterpret_cast<const uint32_t*>(P64), nw64, out, lane, (1u << lane) - 1u,
+                               ((1u << lane) - 1u) | (1u << lane)};
+    const uint32_t* mtab16 = reinterpret_cast<const uint32_t*>(tab);
+    const uint2* mtab32 = reinterpret_cast<const uint2*>(tab);
+    const uint4* xtab = reinterpret_cast<const uint4*>(tab + xoff);
+    bool tab_ready = !SMEM;
+
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntasks) break;
+        const uint8_t* base = t64 + task_byte[t];
+        const uint32_t n = task_n[t];
+        const uint32_t nfull = n / CH;
+        const uint32_t part = n - nfull * CH;
+        const uint8_t* pm = base + static_cast<uint64_t>(nfull) * kChunk64Bytes;      // partial chunk masks
+        const uint8_t* pw = pm + ((8u * part + 15u) & ~15u);                            // and words
+        RowState<LW> rs{static_cast<int32_t>(task_row[t]), static_cast<int32_t>(task_row[t + 1]),
+                        static_cast<int32_t>(task_row[t]) - 1, LW(0)};
+        uint4 cm[K / 2], cw[K / 4];  // masks (2 per piece), word fields (4 per piece)
+        // pieces [h0, h1) of masks and [h0/2, h1/2) of words of chunk c
+        auto load = [&](uint32_t c, int h0, int h1) {
+            if (c + CH <= n) {  // full chunk: piece-transposed, coalesced
+                const uint8_t* q = base + static_cast<uint64_t>(c / CH) * kChunk64Bytes;
+#pragma unroll
+                for (int h = h0; h < h1; ++h) cm[h] = ld_stream16(q + (h * 32 + lane) * 16);
+#pragma unroll
+                for (int h = h0 / 2; h < h1 / 2; ++h) cw[h] = ld_stream16(q + 8 * CH + (h * 32 + lane) * 16);
+            } else {  // partial chunk: plain, lane-contiguous
+#pragma unroll
+                for (int h = h0; h < h1; ++h) cm[h] = ld_stream16(pm + lane * 64 + h * 16);
+#pragma unroll
+                for (int h = h0 / 2; h < h1 / 2; ++h) cw[h] = ld_stream16(pw + lane * 32 + h * 16);
+            }
+        };
+        load(0, 0, K / 2);
+        if constexpr (SMEM) {
+            if (!tab_ready) {
+                mbar_wait(&tab_bar, 0);
+                tab_ready = true;
+            }
+        }
+        for (uint32_t c = 0; c < n; c += CH) {
+            const bool more = c + CH < n;
+            if (c + CH > n) {  // partial chunk: pairs past n become no-op heads
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    if (static_cast<uint32_t>(K * lane + k) >= part) {
+                        if (k & 1) {
+                            cm[k / 2].z = 0;
+                            cm[k / 2].w = 0;
+                        } else {
+                            cm[k / 2].x = 0;
+                            cm[k / 2].y = 0;
+                        }
+                        const uint32_t sw = nw64 | kHead;
+                        switch (k & 3) {
+                            case 0: cw[k / 4].x = sw; break;
+                            case 1: cw[k / 4].y = sw; break;
+                            case 2: cw[k / 4].z = sw; break;
+                            default: cw[k / 4].w = sw; break;
+                        }
+                    }
+                }
+            }
+            uint32_t heads = 0;
+            LW v[K];
+            auto mlo = [&](int k) { return (k & 1) ? cm[k / 2].z : cm[k / 2].x; };
+            auto mhi = [&](int k) { return (k & 1) ? cm[k / 2].w : cm[k / 2].y; };
+            auto wfield = [&](int k) {
+                switch (k & 3) {
+                    case 0: return cw[k / 4].x;
+                    case 1: return cw[k / 4].y;
+                    case 2: return cw[k / 4].z;
+                    default: return cw[k / 4].w;
+                }
+            };
+            auto look = [&](int k, uint32_t& over) {
+                const uint32_t lo = mlo(k), hi = mhi(k), wh = wfield(k);
+                heads = mad_pow2(head_bit(wh), 1u << k, heads);
+                uint32_t mw, meta, f;
+                uint4 x = make_uint4(0u, 0u, 0u, 0u);
+                if constexpr (FMT == 16) {
+                    mw = SMEM ? lds32(sc.tab_s + (wh << 2)) : mtab16[wh & kWordMask];
+                    meta = mw;
+                    f = mw;
+                    if constexpr (SMEM) lds128_if(mw & (1u << 10), sc.x_s + (wh << 4), x);
+                    else if (mw & (1u << 10)) x = xtab[wh & kWordMask];
+                    over |= mw & (1u << 11);
+                } else {
+                    const uint2 m2 = mtab32[wh & kWordMask];
+                    f = m2.x;
+                    meta = m2.y;
+                    if (m2.y & 0x10000u) x = xtab[wh & kWordMask];
+                    over |= m2.y & 0x20000u;
+                }
+                uint32_t vv = f;
+                if ((lo & x.x) | (hi & x.y)) vv |= __funnelshift_l(0u, 1u, meta);
+                if ((lo & x.z) | (hi & x.w)) vv |= __funnelshift_l(0u, 1u, meta >> (FMT == 16 ? 5 : 8));
+                v[k] = vv;
+            };
+            auto fix = [&](int k) {  // a word with >= 3 partial props: exact gather of the rest
+                const uint32_t w = wfield(k) & kWordMask;
+                uint32_t known, ov;
+                if constexpr (FMT == 16) {
+                    const uint32_t mw = mtab16[w];
+                    known = (mw >> 16) | (1u << ((mw & 31) - 16)) | (1u << ((mw >> 5 & 31) - 16));
+                    ov = mw >> 11 & 1u;
+                } else {
+                    const uint2 mw = mtab32[w];
+                    known = mw.x | (1u << (mw.y & 31)) | (1u << (mw.y >> 8 & 31));
+                    ov = mw.y >> 17 & 1u;
+                }
+                if (ov) {
+                    const uint64_t m = (static_cast<uint64_t>(mhi(k)) << 32) | mlo(k);
+                    uint32_t rest = s_only[w] & ~known, hit = 0;
+                    while (rest) {
+                        const int j = __ffs(rest) - 1;
+                        if (m & __ldg(P64 + static_cast<uint64_t>(j) * nw64 + w)) hit |= 1u << j;
+                        rest &= rest - 1;
+                    }
+                    v[k] |= hit << kShift;
+                }
+            };
+            uint32_t ov_lo = 0, ov_hi = 0;
+#pragma unroll
+            for (int k = 0; k < K / 2; ++k) look(k, ov_lo);
+            if (ov_lo) {
+#pragma unroll
+                for (int k = 0; k < K / 2; ++k) fix(k);
+            }
+            if (more) load(c + CH, 0, K / 4);
+#pragma unroll
+            for (int k = K / 2; k < K; ++k) look(k, ov_hi);
+            if (ov_hi) {
+#pragma unroll
+                for (int k = K / 2; k < K; ++k) fix(k);
+            }
+            if (more) load(c + CH, K / 4, K / 2);
+            segment_chunk<FMT, SW, SMEM, K>(sc, rs, heads, v);
         }
         stream_close_task(sc, rs);
     }
@@ -962,6 +1212,19 @@ cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t 
     return cudaGetLastError();
 }
 
+cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
+                             uint32_t* task_ctr, int nctr, cudaStream_t st) {
+    const uint32_t nthreads = nw64 + 1 > static_cast<uint32_t>(nctr) ? nw64 + 1 : static_cast<uint32_t>(nctr);
+    const unsigned grid = (nthreads + 255) / 256;
+    if (entry_format(props) == 16)
+        summary64_kernel<16><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab),
+                                                   static_cast<uint32_t*>(s_only), task_ctr, nctr);
+    else
+        summary64_kernel<32><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab),
+                                                   static_cast<uint32_t*>(s_only), task_ctr, nctr);
+    return cudaGetLastError();
+}
+
 static int sm_count() {
     static int n = 0;
     if (!n) {
@@ -1055,6 +1318,48 @@ static cudaError_t launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
     return launch_stream_v<FMT, SW, false, kStreamK, 256, true>(a, st);
 }
 
+bool stream64_table_in_smem(int props, uint32_t nw64) {
+    static const int want = env_int("LTLG_STREAM_TABLE", -1);
+    if (want == 0 || entry_format(props) == 64) return false;
+    return split64_table_bytes(props, nw64) <= kMaxSmemTable;
+}
+
+template <int FMT, typename SW, bool SMEM, int NT>
+static cudaError_t launch_stream64_v(const LaunchArgs& a, cudaStream_t st) {
+    const uint32_t tab_bytes = static_cast<uint32_t>(split64_table_bytes(a.props, a.nw64));
+    auto kern = label_stream64_kernel<FMT, SW, SMEM, NT>;
+    const uint64_t* P64 = reinterpret_cast<const uint64_t*>(a.P32);
+    if constexpr (SMEM) {
+        static uint64_t attr_set = 0;  // per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!(attr_set >> dev & 1u)) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaxSmemTable));
+            attr_set |= 1ull << dev;
+        }
+        if (tab_bytes % 16u || tab_bytes > kMaxSmemTable) return cudaErrorInvalidValue;
+        kern<<<sm_count(), NT, tab_bytes, st>>>(a.t64, a.task_byte64, a.task_n64, a.task_row, a.task_begin, a.ntasks,
+                                                a.task_ctr, a.sf, tab_bytes, static_cast<const uint32_t*>(a.s_only), P64,
+                                                a.nw64, static_cast<SW*>(a.out));
+    } else {
+        static int per_sm = 0;
+        if (!per_sm) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, 0);
+            if (per_sm <= 0) per_sm = 4;
+        }
+        kern<<<sm_count() * per_sm, NT, 0, st>>>(a.t64, a.task_byte64, a.task_n64, a.task_row, a.task_begin, a.ntasks,
+                                                 a.task_ctr, a.sf, tab_bytes, static_cast<const uint32_t*>(a.s_only),
+                                                 P64, a.nw64, static_cast<SW*>(a.out));
+    }
+    return cudaSuccess;
+}
+
+template <int FMT, typename SW>
+static cudaError_t launch_stream64_t(const LaunchArgs& a, cudaStream_t st) {
+    if (stream64_table_in_smem(a.props, a.nw64)) return launch_stream64_v<FMT, SW, true, 1024>(a, st);
+    return launch_stream64_v<FMT, SW, false, 256>(a, st);
+}
+
 template <int FMT, typename SW, int FPL, bool FULL>
 static void launch_batch_t(const LaunchArgs& a, cudaStream_t st) {
     static int per_sm = 0;
@@ -1081,7 +1386,13 @@ static void launch_batch_fpl(const LaunchArgs& a, cudaStream_t st) {
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
     if (a.ntasks <= a.task_begin) return cudaSuccess;
     cudaError_t e = cudaSuccess;
-    if (a.frames == 1) {
+    if (a.frames == 1 && a.t64) {  // 64-cell-word single-frame path (<= 32 props)
+        switch (a.label_bytes) {
+            case 1: e = launch_stream64_t<16, uint8_t>(a, st); break;
+            case 2: e = launch_stream64_t<16, uint16_t>(a, st); break;
+            default: e = launch_stream64_t<32, uint32_t>(a, st); break;
+        }
+    } else if (a.frames == 1) {
         switch (a.label_bytes) {
             case 1: e = launch_stream_t<16, uint8_t>(a, st); break;
             case 2: e = launch_stream_t<16, uint16_t>(a, st); break;

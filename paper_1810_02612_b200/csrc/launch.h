@@ -28,6 +28,11 @@ struct LaunchArgs {
     int label_bytes;
     uint32_t* task_ctr;  // this launch's kCtrStride device counters, reset by the summary kernel
     const void* s_only;  // S mask per (word, frame): over-path probes, full-mask pairs
+    // 64-cell-word single-frame copy (null: use the 32-bit stream copy)
+    const uint8_t* t64;
+    const uint64_t* task_byte64;
+    const uint32_t* task_n64;
+    uint32_t nw64;
 };
 
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
@@ -36,6 +41,9 @@ int entry_format(int props);
 size_t summary_entry_bytes(int props);
 size_t s_only_bytes(int props);
 size_t split_table_bytes(int props, uint32_t nw32);
+size_t split64_table_bytes(int props, uint32_t nw64);
+cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
+                             uint32_t* task_ctr, int nctr, cudaStream_t st);
 bool stream_table_in_smem(int props, uint32_t nw32);
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st);
 cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, int frames, int frame,

@@ -358,6 +358,81 @@ void build_stream_layout(const WordCsr& t, uint64_t row_begin, uint64_t row_end,
     out->task_pair_stream = dst_off;
 }
 
+// The single-frame 64-cell-word copy (kChunk64Bytes, engine.h), over the
+// same tasks (row ranges) as the 32-bit stream copy.
+void build_stream64_layout(const WordCsr& t, uint64_t row_begin, uint32_t sentinel64, PackedShard* out) {
+    const size_t nt = out->task_row_stream.size() - 1;
+    std::vector<uint64_t> bytes(nt + 1, 0);
+    out->task_n64.assign(nt, 0);
+    // pass 1: pair counts
+    parallel_chunks(nt, 64, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t k = b; k < e; ++k) {
+            uint64_t n = 0;
+            for (uint64_t r = out->task_row_stream[k]; r < out->task_row_stream[k + 1]; ++r) {
+                const uint64_t o0 = t.offsets[row_begin + r], o1 = t.offsets[row_begin + r + 1];
+                uint64_t cnt = 0;
+                for (uint64_t q = o0; q < o1; ++q)
+                    if (q == o0 || (t.word[q] >> 1) != (t.word[q - 1] >> 1)) ++cnt;
+                n += cnt ? cnt : 1;
+            }
+            out->task_n64[k] = static_cast<uint32_t>(n);
+        }
+    });
+    for (size_t k = 0; k < nt; ++k) {
+        const uint64_t n = out->task_n64[k], full = n / kStreamCH, part = n % kStreamCH;
+        bytes[k + 1] = bytes[k] + full * kChunk64Bytes + ((8 * part + 15) & ~uint64_t(15)) + ((4 * part + 15) & ~uint64_t(15));
+    }
+    out->stream64.assign(bytes[nt] + kPad64Bytes, 0);
+    out->task_byte64 = bytes;
+    // pass 2: fill
+    parallel_chunks(nt, 64, [&](uint64_t b, uint64_t e, int) {
+        std::vector<uint64_t> mk;
+        std::vector<uint32_t> wd;
+        for (uint64_t k = b; k < e; ++k) {
+            mk.clear();
+            wd.clear();
+            for (uint64_t r = out->task_row_stream[k]; r < out->task_row_stream[k + 1]; ++r) {
+                const uint64_t o0 = t.offsets[row_begin + r], o1 = t.offsets[row_begin + r + 1];
+                if (o1 == o0) {  // empty row: a no-op pair on the zero sentinel word
+                    mk.push_back(0);
+                    wd.push_back(sentinel64 | kHead);
+                    continue;
+                }
+                for (uint64_t q = o0; q < o1; ++q) {
+                    const uint32_t w64 = t.word[q] >> 1;
+                    const uint64_t m = static_cast<uint64_t>(t.mask[q]) << (32 * (t.word[q] & 1));
+                    if (q > o0 && w64 == (wd.back() & kWordMask)) {
+                        mk.back() |= m;
+                    } else {
+                        mk.push_back(m);
+                        wd.push_back(w64 | (q == o0 ? kHead : 0u));
+                    }
+                }
+            }
+            uint8_t* dst = out->stream64.data() + bytes[k];
+            const uint64_t n = mk.size(), full = n / kStreamCH, part = n % kStreamCH;
+            for (uint64_t c = 0; c < full; ++c) {
+                uint64_t* dm = reinterpret_cast<uint64_t*>(dst + c * kChunk64Bytes);
+                uint32_t* dw = reinterpret_cast<uint32_t*>(dst + c * kChunk64Bytes + 8 * kStreamCH);
+                const uint64_t base = c * kStreamCH;
+                for (uint64_t l = 0; l < 32; ++l) {
+                    for (uint64_t h = 0; h < kStreamK / 2; ++h)
+                        for (uint64_t e2 = 0; e2 < 2; ++e2)
+                            dm[2 * (h * 32 + l) + e2] = mk[base + kStreamK * l + 2 * h + e2];
+                    for (uint64_t h = 0; h < kStreamK / 4; ++h)
+                        for (uint64_t e4 = 0; e4 < 4; ++e4)
+                            dw[4 * (h * 32 + l) + e4] = wd[base + kStreamK * l + 4 * h + e4];
+                }
+            }
+            if (part) {
+                uint8_t* pm = dst + full * kChunk64Bytes;
+                std::memcpy(pm, mk.data() + full * kStreamCH, 8 * part);
+                std::memcpy(pm + ((8 * part + 15) & ~uint64_t(15)), wd.data() + full * kStreamCH, 4 * part);
+            }
+        }
+    });
+}
+
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
                  uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs, int blocks,
                  PackedShard* out) {
@@ -414,6 +489,7 @@ void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool so
     make_tasks(pair_off, out->block_row, batch_task_pairs, &out->task_row_batch, &out->task_pair_batch,
                &out->block_task_batch);
     build_stream_layout(t, row_begin, row_end, sentinel_word, stream_task_pairs, out);
+    build_stream64_layout(t, row_begin, sentinel_word / 2, out);  // sentinel_word = nw32 = 2 * nw64
 }
 
 }  // namespace ltlg

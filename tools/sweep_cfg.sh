@@ -1,4 +1,5 @@
 #!/bin/bash
-# A/B sweep of the single-frame kernel configurations (dev helper, GPU box)
-for cfg in ${CFGS:-1 2 3 4 5}; do LTLG_STREAM_CFG=$cfg TAG=cfg$cfg python tools/sweep_stream.py; done
-for cfg in ${CFGS8:-1 3}; do PROPS=8 LTLG_STREAM_CFG=$cfg TAG=cfg$cfg python tools/sweep_stream.py; done
+# A/B sweep of the single-frame kernel variants (dev helper, GPU box)
+for v in ${VARIANTS:-"LTLG_STREAM64=1" "LTLG_STREAM64=0"}; do
+  for p in ${PROPS_LIST:-16 8}; do env $v PROPS=$p TAG="$v" python tools/sweep_stream.py; done
+done
