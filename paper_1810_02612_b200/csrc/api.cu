@@ -98,6 +98,8 @@ struct Shard {
     int blocks_last = 0;                                       // blocks labelled by the last submit
     DevBuf<Pair> pairs, pairs_s;  // plain (multi-frame) and single-frame layouts
     DevBuf<uint8_t> t64;          // single-frame 64-cell-word copy
+    DevBuf<uint64_t> mask_b64, tpair_b64, pb64;  // multi-frame 64-cell-word copy, its Pb table
+    DevBuf<uint32_t> word_b64;
     DevBuf<uint64_t> tbyte64;
     DevBuf<uint32_t> tn64;
     DevBuf<uint32_t> perm, trow_s, trow_b;
@@ -193,12 +195,16 @@ ltlg_status upload_shard(ltlg_ctx* ctx, Shard& s, const PackedShard& p) {
     if ((st = put(s.t64, p.stream64, "upload T pairs")) != LTLG_OK) return st;
     if ((st = put(s.tbyte64, p.task_byte64, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.tn64, p.task_n64, "upload tasks")) != LTLG_OK) return st;
+    if ((st = put(s.mask_b64, p.mask_b64, "upload T pairs")) != LTLG_OK) return st;
+    if ((st = put(s.word_b64, p.word_b64, "upload T pairs")) != LTLG_OK) return st;
+    if ((st = put(s.tpair_b64, p.task_pair_b64, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.perm, p.perm, "upload row permutation")) != LTLG_OK) return st;
     if ((st = put(s.trow_s, p.task_row_stream, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.tpair_s, p.task_pair_stream, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.trow_b, p.task_row_batch, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.tpair_b, p.task_pair_batch, "upload tasks")) != LTLG_OK) return st;
-    ctx->t_bytes += (p.pairs.size() + p.pairs_stream.size()) * sizeof(Pair) + p.stream64.size() + p.perm.size() * 4;
+    ctx->t_bytes += (p.pairs.size() + p.pairs_stream.size()) * sizeof(Pair) + p.stream64.size() + p.perm.size() * 4 +
+                    p.mask_b64.size() * 8 + p.word_b64.size() * 4;
     return LTLG_OK;
 }
 
@@ -308,7 +314,10 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // 64-cell-word single-frame path (dev knob LTLG_STREAM64=0 selects the 32-cell copy for A/B runs)
         static const bool wide_ok = !getenv("LTLG_STREAM64") || atoi(getenv("LTLG_STREAM64")) != 0;
         const bool wide = wide_ok && frames == 1 && props <= 32;
-        CK(s.sf.reserve(wide ? split64_table_bytes(props, nw64)
+        static const bool wide_b_ok = !getenv("LTLG_BATCH64") || atoi(getenv("LTLG_BATCH64")) != 0;
+        const bool wide_b = wide_b_ok && frames > 1 && props <= 32;  // 64-cell-word multi-frame path
+        CK(s.sf.reserve(wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32
+                        : wide ? split64_table_bytes(props, nw64)
                              : frames == 1 && props <= 32
                                    ? split_table_bytes(props, nw32)
                                    : static_cast<size_t>(nw32 + 1) * frames * summary_entry_bytes(props)),
@@ -320,6 +329,10 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         const int nctr = static_cast<int>((s.block_row.size() - 1) * kCtrStride);
         if (wide)
             CK(launch_summary64(s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr, s.ctr.ptr, nctr, s.stream),
+               "summary kernel");
+        else if (wide_b)
+            CK(launch_summary_b64(s.Pdev(), props, frames, nw64, ctx->cells, s.sf.ptr, nullptr, s.s_only.ptr,
+                                  s.ctr.ptr, nctr, s.stream),
                "summary kernel");
         else
             CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
@@ -339,6 +352,12 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         a.s_only = s.s_only.ptr;
         const bool single = frames == 1;
         if (single) a.pairs = s.pairs_s.ptr;
+        if (wide_b) {
+            a.mask_b64 = s.mask_b64.ptr;
+            a.word_b64 = s.word_b64.ptr;
+            a.task_pair_b64 = s.tpair_b64.ptr;
+            a.nw64 = nw64;
+        }
         if (wide) {
             a.t64 = s.t64.ptr;
             a.task_byte64 = s.tbyte64.ptr;
@@ -495,6 +514,10 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.t64.release();
         s.tbyte64.release();
         s.tn64.release();
+        s.mask_b64.release();
+        s.word_b64.release();
+        s.tpair_b64.release();
+        s.pb64.release();
         s.perm.release();
         s.trow_s.release();
         s.trow_b.release();

@@ -44,6 +44,11 @@ struct PackedShard {
     std::vector<uint8_t> stream64;
     std::vector<uint64_t> task_byte64;    // ntasks + 1
     std::vector<uint32_t> task_n64;       // ntasks
+    // multi-frame 64-cell-word copy: SoA arrays in the batch layout's row
+    // order; task t's pairs are [task_pair_b64[t], task_pair_b64[t+1])
+    std::vector<uint64_t> mask_b64;
+    std::vector<uint32_t> word_b64;
+    std::vector<uint64_t> task_pair_b64;  // ntasks + 1
     uint64_t n_pairs = 0;                 // meaningful pairs (incl. sentinels)
     std::vector<uint32_t> perm;           // sorted position -> local original row
     // warp tasks: [row_begin, row_end) in sorted positions, pairs [pair_begin, pair_end)

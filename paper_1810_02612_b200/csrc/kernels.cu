@@ -316,6 +316,52 @@ __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restri
     s_only[w] = s;
 }
 
+// Multi-frame summary over 64-cell words, thread per (word, frame), index
+// w * frames + f:
+//   tab  : 32-B entry {F, ia | ib<<8 | hasB<<16 | over<<17, Pa lo, Pa hi,
+//          Pb lo, Pb hi, S, 0} -- one 256-bit load, branch-free probes
+//   s_only: S (4 B; full-mask pairs read only this)
+constexpr uint32_t kHasB64 = 0x10000u, kOver64 = 0x20000u;
+__global__ void __launch_bounds__(256) summary_b64_kernel(const uint64_t* __restrict__ P64, int props, int frames,
+                                                          uint32_t nw64, uint64_t cells, uint4* __restrict__ tab,
+                                                          uint64_t* __restrict__ pbt, uint32_t* __restrict__ s_only,
+                                                          uint32_t* __restrict__ task_ctr, int nctr) {
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int f = blockIdx.y;
+    if (f == 0 && w < static_cast<uint32_t>(nctr)) task_ctr[w] = 0;
+    if (w > nw64) return;
+    uint32_t s = 0, full = 0, ia = 0, ib = 0;
+    uint64_t pa = 0, pb = 0;
+    int np = 0;
+    const uint64_t lo = static_cast<uint64_t>(w) * 64;
+    if (w < nw64 && lo < cells) {
+        const uint64_t valid = (cells - lo >= 64) ? ~0ull : ((1ull << (cells - lo)) - 1ull);
+        const uint64_t* base = P64 + static_cast<uint64_t>(f) * props * nw64 + w;
+#pragma unroll 4
+        for (int j = 0; j < props; ++j) {
+            const uint64_t x = base[static_cast<uint64_t>(j) * nw64] & valid;
+            s |= static_cast<uint32_t>(x != 0) << j;
+            full |= static_cast<uint32_t>(x == valid) << j;
+            if (x != 0 && x != valid) {
+                if (np == 0) {
+                    pa = x;
+                    ia = static_cast<uint32_t>(j);
+                } else if (np == 1) {
+                    pb = x;
+                    ib = static_cast<uint32_t>(j);
+                }
+                ++np;
+            }
+        }
+    }
+    const uint64_t idx = static_cast<uint64_t>(w) * frames + f;
+    (void)pbt;
+    tab[2 * idx] = make_uint4(full, ia | (ib << 8) | (np > 1 ? kHasB64 : 0u) | (np > 2 ? kOver64 : 0u),
+                              static_cast<uint32_t>(pa), static_cast<uint32_t>(pa >> 32));
+    tab[2 * idx + 1] = make_uint4(static_cast<uint32_t>(pb), static_cast<uint32_t>(pb >> 32), s, 0u);
+    s_only[idx] = s;
+}
+
 // ---------------------------------------------------------------------------
 // TMA bulk copy + mbarrier helpers (sm_90+ PTX, used on sm_100a)
 // ---------------------------------------------------------------------------
@@ -1360,6 +1406,148 @@ static cudaError_t launch_stream64_t(const LaunchArgs& a, cudaStream_t st) {
     return launch_stream64_v<FMT, SW, false, 256>(a, st);
 }
 
+// F frames over 64-cell words (<= 32 props): the batch kernel's structure on
+// the SoA (mask64, word64) copy and the summary_b64_kernel entries.
+struct E32 {
+    uint32_t f, meta, pa_lo, pa_hi, pb_lo, pb_hi, s, pad;
+};
+__device__ __forceinline__ E32 ld_entry32(const E32* p) {
+    E32 e;
+    asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(e.f), "=r"(e.meta), "=r"(e.pa_lo), "=r"(e.pa_hi), "=r"(e.pb_lo), "=r"(e.pb_hi), "=r"(e.s), "=r"(e.pad)
+        : "l"(p));
+    return e;
+}
+
+template <typename SW, int FPL, bool FULL>
+__global__ void __launch_bounds__(256)
+    label_batch64_kernel(const uint64_t* __restrict__ masks, const uint32_t* __restrict__ words,
+                         const uint64_t* __restrict__ task_pair, const uint32_t* __restrict__ task_row,
+                         uint32_t task_begin, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
+                         const uint4* __restrict__ tab, const uint64_t* __restrict__ pbt,
+                         const uint32_t* __restrict__ s_only, const uint64_t* __restrict__ P64, uint32_t nw64,
+                         int props, int frames, const uint32_t* __restrict__ perm, SW* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t frame_stride = static_cast<uint64_t>(props) * nw64;
+    const E32* lane_tab = reinterpret_cast<const E32*>(tab) + lane;
+    (void)pbt;
+    const uint32_t* lane_s = s_only + lane;
+    bool fv[FPL];
+#pragma unroll
+    for (int q = 0; q < FPL; ++q) fv[q] = FULL || lane + 32 * q < frames;
+
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntasks) break;
+        const uint64_t p0 = task_pair[t], p1 = task_pair[t + 1];
+        const int64_t r0 = task_row[t];
+        int64_t row = r0 - 1;
+        uint32_t acc[FPL];
+#pragma unroll
+        for (int q = 0; q < FPL; ++q) acc[q] = 0;
+        auto store = [&](int64_t r) {
+            SW* o = out + static_cast<uint64_t>(perm[r]) * frames + lane;
+#pragma unroll
+            for (int q = 0; q < FPL; ++q)
+                if (fv[q]) o[32 * q] = static_cast<SW>(acc[q]);
+        };
+        auto pair_step = [&](uint32_t mlo, uint32_t mhi, uint32_t wh) {
+            if (wh & kHead) {  // warp-uniform
+                if (row >= r0) store(row);
+                ++row;
+#pragma unroll
+                for (int q = 0; q < FPL; ++q) acc[q] = 0;
+            }
+            const uint32_t w = wh & kWordMask;
+            const uint32_t off = w * static_cast<uint32_t>(frames);
+            if ((mlo & mhi) == 0xffffffffu) {  // warp-uniform: the whole 64-cell word is swept
+                const uint32_t* sp = index_wide(lane_s, off);
+#pragma unroll
+                for (int q = 0; q < FPL; ++q)
+                    if (fv[q]) acc[q] |= __ldg(sp + 32 * q);
+                return;
+            }
+            const E32* ep = index_wide(lane_tab, off);
+#pragma unroll
+            for (int q = 0; q < FPL; ++q) {
+                if (!fv[q]) continue;
+                const E32 e = ld_entry32(ep + 32 * q);
+                uint32_t v = e.f;
+                if ((mlo & e.pa_lo) | (mhi & e.pa_hi)) v |= __funnelshift_l(0u, 1u, e.meta);
+                if ((mlo & e.pb_lo) | (mhi & e.pb_hi)) v |= __funnelshift_l(0u, 1u, e.meta >> 8);
+                {
+                    if (e.meta & kOver64) {  // a third partial prop: exact gather of the rest
+                        const uint32_t known = e.f | (1u << (e.meta & 31)) | (1u << (e.meta >> 8 & 31));
+                        uint32_t rest = e.s & ~known & ~acc[q];
+                        const uint64_t m = (static_cast<uint64_t>(mhi) << 32) | mlo;
+                        const uint64_t* col0 = P64 + static_cast<uint64_t>(lane + 32 * q) * frame_stride + w;
+                        while (rest) {
+                            const int j = __ffs(rest) - 1;
+                            if (m & __ldg(col0 + static_cast<uint64_t>(j) * nw64)) v |= 1u << j;
+                            rest &= rest - 1;
+                        }
+                    }
+                }
+                acc[q] |= v;
+            }
+        };
+        uint2 cm = __ldg(reinterpret_cast<const uint2*>(masks + p0 + lane));
+        uint32_t cw = __ldg(words + p0 + lane);
+        for (uint64_t c = p0; c < p1; c += 32) {
+            uint2 nm = cm;
+            uint32_t nwd = cw;
+            if (c + 32 < p1) {
+                nm = __ldg(reinterpret_cast<const uint2*>(masks + c + 32 + lane));
+                nwd = __ldg(words + c + 32 + lane);
+            }
+            const int n = static_cast<int>(p1 - c < 32 ? p1 - c : 32);
+            for (int i = 0; i < n; ++i)
+                pair_step(__shfl_sync(0xffffffffu, cm.x, i), __shfl_sync(0xffffffffu, cm.y, i),
+                          __shfl_sync(0xffffffffu, cw, i));
+            cm = nm;
+            cw = nwd;
+        }
+        if (row >= r0) store(row);
+    }
+}
+
+template <typename SW, int FPL, bool FULL>
+static void launch_batch64_t(const LaunchArgs& a, cudaStream_t st) {
+    static int per_sm = 0;
+    auto kern = label_batch64_kernel<SW, FPL, FULL>;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+        if (per_sm <= 0) per_sm = 4;
+    }
+    kern<<<sm_count() * per_sm, 256, 0, st>>>(a.mask_b64, a.word_b64, a.task_pair_b64, a.task_row, a.task_begin, a.ntasks,
+                                              a.task_ctr, static_cast<const uint4*>(a.sf), a.pb64,
+                                              static_cast<const uint32_t*>(a.s_only),
+                                              reinterpret_cast<const uint64_t*>(a.P32), a.nw64, a.props, a.frames,
+                                              a.perm, static_cast<SW*>(a.out));
+}
+
+template <typename SW>
+static void launch_batch64_fpl(const LaunchArgs& a, cudaStream_t st) {
+    if (a.frames == 32) launch_batch64_t<SW, 1, true>(a, st);
+    else if (a.frames == 64) launch_batch64_t<SW, 2, true>(a, st);
+    else if (a.frames == 128) launch_batch64_t<SW, 4, true>(a, st);
+    else if (a.frames < 32) launch_batch64_t<SW, 1, false>(a, st);
+    else if (a.frames < 64) launch_batch64_t<SW, 2, false>(a, st);
+    else if (a.frames < 128) launch_batch64_t<SW, 4, false>(a, st);
+    else launch_batch64_t<SW, 8, false>(a, st);
+}
+
+cudaError_t launch_summary_b64(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* tab,
+                               uint64_t* pbt, void* s_only, uint32_t* task_ctr, int nctr, cudaStream_t st) {
+    const uint32_t nthreads = nw64 + 1 > static_cast<uint32_t>(nctr) ? nw64 + 1 : static_cast<uint32_t>(nctr);
+    dim3 grid((nthreads + 255) / 256, static_cast<unsigned>(frames));
+    summary_b64_kernel<<<grid, 256, 0, st>>>(P64, props, frames, nw64, cells, static_cast<uint4*>(tab), pbt,
+                                             static_cast<uint32_t*>(s_only), task_ctr, nctr);
+    return cudaGetLastError();
+}
+
 template <int FMT, typename SW, int FPL, bool FULL>
 static void launch_batch_t(const LaunchArgs& a, cudaStream_t st) {
     static int per_sm = 0;
@@ -1398,6 +1586,12 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
             case 2: e = launch_stream_t<16, uint16_t>(a, st); break;
             case 4: e = launch_stream_t<32, uint32_t>(a, st); break;
             default: e = launch_stream_t<64, uint64_t>(a, st); break;
+        }
+    } else if (a.mask_b64) {  // 64-cell-word multi-frame path (<= 32 props)
+        switch (a.label_bytes) {
+            case 1: launch_batch64_fpl<uint8_t>(a, st); break;
+            case 2: launch_batch64_fpl<uint16_t>(a, st); break;
+            default: launch_batch64_fpl<uint32_t>(a, st); break;
         }
     } else {
         switch (a.label_bytes) {

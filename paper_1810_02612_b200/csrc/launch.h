@@ -33,6 +33,11 @@ struct LaunchArgs {
     const uint64_t* task_byte64;
     const uint32_t* task_n64;
     uint32_t nw64;
+    // 64-cell-word multi-frame copy (null: use the 32-bit pairs)
+    const uint64_t* mask_b64;
+    const uint32_t* word_b64;
+    const uint64_t* task_pair_b64;
+    const uint64_t* pb64;  // Pb table of summary_b64_kernel
 };
 
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
@@ -42,6 +47,8 @@ size_t summary_entry_bytes(int props);
 size_t s_only_bytes(int props);
 size_t split_table_bytes(int props, uint32_t nw32);
 size_t split64_table_bytes(int props, uint32_t nw64);
+cudaError_t launch_summary_b64(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* tab,
+                               uint64_t* pbt, void* s_only, uint32_t* task_ctr, int nctr, cudaStream_t st);
 cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
                              uint32_t* task_ctr, int nctr, cudaStream_t st);
 bool stream_table_in_smem(int props, uint32_t nw32);

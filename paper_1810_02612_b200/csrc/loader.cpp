@@ -433,6 +433,50 @@ void build_stream64_layout(const WordCsr& t, uint64_t row_begin, uint32_t sentin
     });
 }
 
+// The multi-frame 64-cell-word copy (SoA), rows in the batch layout's order.
+void build_batch64_layout(const WordCsr& t, uint64_t row_begin, uint32_t sentinel64, PackedShard* out) {
+    const uint64_t R = out->perm.size();
+    std::vector<uint64_t> off(R + 1, 0);
+    parallel_chunks(R, 1 << 14, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t s = b; s < e; ++s) {
+            const uint64_t r = row_begin + out->perm[s];
+            uint64_t cnt = 0;
+            for (uint64_t q = t.offsets[r]; q < t.offsets[r + 1]; ++q)
+                if (q == t.offsets[r] || (t.word[q] >> 1) != (t.word[q - 1] >> 1)) ++cnt;
+            off[s + 1] = cnt ? cnt : 1;
+        }
+    });
+    for (uint64_t s = 0; s < R; ++s) off[s + 1] += off[s];
+    constexpr uint64_t kPad = 64;  // lanes load up to 31 pairs past a task
+    out->mask_b64.assign(off[R] + kPad, 0);
+    out->word_b64.assign(off[R] + kPad, sentinel64 | kHead);
+    parallel_chunks(R, 1 << 14, [&](uint64_t b, uint64_t e, int) {
+        for (uint64_t s = b; s < e; ++s) {
+            const uint64_t r = row_begin + out->perm[s];
+            uint64_t o = off[s];
+            if (t.offsets[r + 1] == t.offsets[r]) {  // empty row: a no-op pair on the zero sentinel word
+                out->mask_b64[o] = 0;
+                out->word_b64[o] = sentinel64 | kHead;
+                continue;
+            }
+            for (uint64_t q = t.offsets[r]; q < t.offsets[r + 1]; ++q) {
+                const uint32_t w64 = t.word[q] >> 1;
+                const uint64_t m = static_cast<uint64_t>(t.mask[q]) << (32 * (t.word[q] & 1));
+                if (q > t.offsets[r] && w64 == (out->word_b64[o - 1] & kWordMask)) {
+                    out->mask_b64[o - 1] |= m;
+                } else {
+                    out->mask_b64[o] = m;
+                    out->word_b64[o] = w64 | (q == t.offsets[r] ? kHead : 0u);
+                    ++o;
+                }
+            }
+        }
+    });
+    const size_t nt = out->task_row_batch.size() - 1;
+    out->task_pair_b64.resize(nt + 1);
+    for (size_t k = 0; k <= nt; ++k) out->task_pair_b64[k] = off[out->task_row_batch[k]];
+}
+
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
                  uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs, int blocks,
                  PackedShard* out) {
@@ -490,6 +534,7 @@ void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool so
                &out->block_task_batch);
     build_stream_layout(t, row_begin, row_end, sentinel_word, stream_task_pairs, out);
     build_stream64_layout(t, row_begin, sentinel_word / 2, out);  // sentinel_word = nw32 = 2 * nw64
+    build_batch64_layout(t, row_begin, sentinel_word / 2, out);
 }
 
 }  // namespace ltlg
