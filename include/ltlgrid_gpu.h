@@ -97,7 +97,8 @@ ltlg_status ltlg_load_abstraction(ltlg_ctx* ctx, uint64_t rows, uint64_t cols,
                                   const uint64_t* row_offsets, const uint32_t* col_indices);
 
 /* Load T from a CSB1 file (replaces CsrBoolMatrix::load, label.cpp:271-298):
- * same header checks and messages, then validate, then pack. */
+ * same header checks and messages, then validate, then pack -- streamed, so
+ * the u32 index array (4 B per swept cell) is never held in host memory. */
 ltlg_status ltlg_load_abstraction_file(ltlg_ctx* ctx, const char* csb1_path);
 
 /* Load T already packed as a word-CSR: row i's 32-bit words are
@@ -139,6 +140,28 @@ typedef struct ltlg_pose2 {
 ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, const ltlg_grid2* world,
                                    int num_props, const uint64_t* world_words, int words_on_device,
                                    const ltlg_pose2* poses, int frames, int outside);
+
+/* Submit `frames` x num_props ZOBV proposition columns (load_bitset,
+ * grid.cpp:375-405; paths[f * num_props + j] = prop j of frame f), read
+ * straight into pinned staging memory and labelled like ltlg_submit_grid.
+ * Every column must be cols-of-T bits long (DensePropMatrix, label.cpp:125-127:
+ * "column length mismatch").  File errors: "cannot open: <path>" (EIO),
+ * "not a bitset file: <path>", "corrupt bitset header",
+ * "truncated bitset file: <path>" (EFORMAT).  Returns when the labels are ready. */
+ltlg_status ltlg_submit_grid_files(ltlg_ctx* ctx, const char* const* paths, int num_props, int frames);
+
+/* Write one frame's labels as an LBM1 file (LabelMatrix::save, label.cpp:300-309). */
+ltlg_status ltlg_save_labels(ltlg_ctx* ctx, int frame, const char* path);
+
+/* Host-only: stream-read, validate and pack a CSB1 file exactly as
+ * ltlg_load_abstraction_file does (CsrBoolMatrix::load + validate, label.cpp:
+ * 271-298 / 16-40: same checks, same order, same messages), reporting its
+ * shape.  The index array is never held whole.  No device needed. */
+ltlg_status ltlg_read_csb1_words(const char* path, uint64_t* rows, uint64_t* cols, uint64_t* nnz, uint64_t* words);
+
+/* Host-only: one ZOBV proposition column of `cells` bits into words_out
+ * (ceil(cells/64) u64), with the ltlg_submit_grid_files checks. */
+ltlg_status ltlg_read_zobv(const char* path, uint64_t cells, uint64_t* words_out);
 
 /* Block until every submitted frame is labelled. */
 ltlg_status ltlg_wait(ltlg_ctx* ctx);

@@ -335,6 +335,15 @@ class RefCore:
         if self.lib.ref_csr_save(path.encode(), rows, cols, _p(offsets, C.c_uint64), _p(indices, C.c_uint32)):
             raise OracleError(self.error())
 
+    def csr_load_shape(self, path):
+        """CsrBoolMatrix::load (label.cpp:271-298) -> (rows, cols, nnz); raises
+        OracleError with the reference's what() text."""
+        rows, cols = C.c_uint64(), C.c_uint64()
+        n = self.lib.ref_csr_load(path.encode(), C.byref(rows), C.byref(cols), None, None)
+        if n < 0:
+            raise OracleError(self.error())
+        return rows.value, cols.value, n
+
     def label_save(self, path, rows, props, words):
         words = np.ascontiguousarray(words, dtype=np.uint64)
         if words.size == 0:

@@ -23,6 +23,7 @@ EXPORTS = [
     "ltlg_submit_grid", "ltlg_submit_grid_device", "ltlg_submit_world_grid", "ltlg_wait",
     "ltlg_get_labels", "ltlg_get_labels_packed", "ltlg_device_labels", "ltlg_get_info",
     "ltlg_stream", "ltlg_stage_times", "ltlg_validate_csr", "ltlg_label_all",
+    "ltlg_submit_grid_files", "ltlg_save_labels", "ltlg_read_csb1_words", "ltlg_read_zobv",
 ]
 
 
@@ -88,6 +89,10 @@ def lib() -> C.CDLL:
         "ltlg_stage_times": ([ctxp, i32, i32, C.POINTER(C.c_float), C.POINTER(C.c_float), C.POINTER(C.c_float)], i32),
         "ltlg_validate_csr": ([u64, u64, vp, u64, vp, u64, C.c_char_p, C.c_size_t], i32),
         "ltlg_label_all": ([u64, u64, vp, vp, u64, i32, vp, i32, vp], i32),
+        "ltlg_submit_grid_files": ([ctxp, C.POINTER(C.c_char_p), i32, i32], i32),
+        "ltlg_save_labels": ([ctxp, i32, C.c_char_p], i32),
+        "ltlg_read_csb1_words": ([C.c_char_p, P64, P64, P64, P64], i32),
+        "ltlg_read_zobv": ([C.c_char_p, u64, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -559,14 +559,9 @@ ltlg_status ltlg_load_abstraction(ltlg_ctx* ctx, uint64_t rows, uint64_t cols, c
 ltlg_status ltlg_load_abstraction_file(ltlg_ctx* ctx, const char* path) {
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!path) return set_err(ctx, LTLG_EINVAL, "null path");
-    uint64_t rows = 0, cols = 0;
-    std::vector<uint64_t> off;
-    std::vector<uint32_t> idx;
     Error err{S_OK, ""};
-    if (!read_csb1(path, &rows, &cols, &off, &idx, &err))
-        return set_err(ctx, static_cast<ltlg_status>(err.code), err.msg);
     WordCsr t;
-    pack_csr(rows, cols, off.data(), idx.data(), &t, &err);
+    if (!read_csb1_words(path, &t, &err)) return set_err(ctx, static_cast<ltlg_status>(err.code), err.msg);
     return load_words(ctx, t);
 }
 
@@ -643,6 +638,73 @@ ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, con
     CK(cudaStreamSynchronize(s0.stream), "resample");
     if ((st = broadcast_P(ctx, vwords)) != LTLG_OK) return st;
     return run_label(ctx, !words_on_device);
+}
+
+ltlg_status ltlg_submit_grid_files(ltlg_ctx* ctx, const char* const* paths, int num_props, int frames) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!ctx->loaded) return set_err(ctx, LTLG_ESTATE, "no abstraction loaded");
+    if (num_props > 64) return set_err(ctx, LTLG_EINVAL, "at most 64 propositions");
+    if (num_props < 0) return set_err(ctx, LTLG_EINVAL, "props must be in [0, 64]");
+    if (frames < 1) return set_err(ctx, LTLG_EINVAL, "frames must be >= 1");
+    const size_t nw = (ctx->cols + 63) / 64;
+    const size_t n = static_cast<size_t>(frames) * static_cast<size_t>(num_props);
+    if (n && !paths) return set_err(ctx, LTLG_EINVAL, "null paths");
+    // read every column straight into one pinned staging buffer, then submit
+    uint64_t* staging = nullptr;
+    if (n) {
+        Shard& s0 = ctx->shards[0];
+        CK(cudaSetDevice(s0.device), "cudaSetDevice");
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&staging), n * nw * 8, cudaHostAllocDefault), "pinned staging");
+    }
+    std::unique_ptr<uint64_t, cudaError_t (*)(void*)> hold(staging, cudaFreeHost);
+    for (size_t i = 0; i < n; ++i) {
+        Error err{S_OK, ""};
+        if (!paths[i]) return set_err(ctx, LTLG_EINVAL, "null path");
+        if (!read_zobv(paths[i], ctx->cols, staging + i * nw, &err))
+            return set_err(ctx, static_cast<ltlg_status>(err.code), err.msg);
+    }
+    ltlg_status st = submit(ctx, ctx->cols, num_props, staging, frames, false);
+    if (st == LTLG_OK && n) st = sync_all(ctx);  // the staging buffer is freed on return
+    return st;
+}
+
+ltlg_status ltlg_save_labels(ltlg_ctx* ctx, int frame, const char* path) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!path) return set_err(ctx, LTLG_EINVAL, "null path");
+    if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
+    if (frame < 0 || frame >= ctx->frames) return set_err(ctx, LTLG_EINVAL, "frame out of range");
+    const int wpr = (ctx->props + 63) / 64;
+    std::vector<uint64_t> words(ctx->rows * static_cast<uint64_t>(wpr));
+    if (!words.empty()) {
+        ltlg_status st = ltlg_get_labels(ctx, frame, words.data());
+        if (st != LTLG_OK) return st;
+    } else {
+        ltlg_status st = sync_all(ctx);
+        if (st != LTLG_OK) return st;
+    }
+    Error err{S_OK, ""};
+    if (!write_lbm1(path, ctx->rows, ctx->props, words.data(), &err))
+        return set_err(ctx, static_cast<ltlg_status>(err.code), err.msg);
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_read_csb1_words(const char* path, uint64_t* rows, uint64_t* cols, uint64_t* nnz, uint64_t* words) {
+    if (!path) return set_err(nullptr, LTLG_EINVAL, "null path");
+    Error err{S_OK, ""};
+    WordCsr t;
+    if (!read_csb1_words(path, &t, &err)) return set_err(nullptr, static_cast<ltlg_status>(err.code), err.msg);
+    if (rows) *rows = t.rows;
+    if (cols) *cols = t.cols;
+    if (nnz) *nnz = t.nnz;
+    if (words) *words = t.offsets.empty() ? 0 : t.offsets[t.rows];
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_read_zobv(const char* path, uint64_t cells, uint64_t* words_out) {
+    if (!path || (!words_out && cells)) return set_err(nullptr, LTLG_EINVAL, "null argument");
+    Error err{S_OK, ""};
+    if (!read_zobv(path, cells, words_out, &err)) return set_err(nullptr, static_cast<ltlg_status>(err.code), err.msg);
+    return LTLG_OK;
 }
 
 ltlg_status ltlg_wait(ltlg_ctx* ctx) {

@@ -90,6 +90,14 @@ bool take_words(uint64_t rows, uint64_t cols, const uint64_t* offsets, const uin
                 const uint32_t* mask, WordCsr* out, Error* err);
 bool read_csb1(const char* path, uint64_t* rows, uint64_t* cols, std::vector<uint64_t>* offsets,
                std::vector<uint32_t>* indices, Error* err);
+// CsrBoolMatrix::load + validate + pack, streaming: the u32 index array is
+// never held whole (peak host memory = offsets + one chunk + the word-CSR).
+bool read_csb1_words(const char* path, WordCsr* out, Error* err);
+// load_bitset (grid.cpp:375-405) of one proposition column into dst
+// (ceil(cells/64) u64); the file's cell count must equal `cells`.
+bool read_zobv(const char* path, uint64_t cells, uint64_t* dst, Error* err);
+// LabelMatrix::save (label.cpp:300-309): LBM1 of rows x ceil(props/64) words.
+bool write_lbm1(const char* path, uint64_t rows, int props, const uint64_t* words, Error* err);
 // Split rows into n contiguous shards balanced by stored pairs.
 std::vector<uint64_t> shard_bounds(const WordCsr& t, int n);
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,

@@ -251,6 +251,165 @@ bool read_csb1(const char* path, uint64_t* rows, uint64_t* cols, std::vector<uin
     return validate_csr(*rows, *cols, offsets->data(), offsets->size(), indices->data(), nnz, err);
 }
 
+bool read_csb1_words(const char* path, WordCsr* out, Error* err) {
+    const std::string p(path);
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return fail(err, S_EIO, "cannot open: " + p);
+    struct Closer {
+        FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    auto rd = [&](void* dst, size_t n) { return std::fread(dst, 1, n, f) == n; };
+    char magic[4];
+    if (!rd(magic, 4) || std::memcmp(magic, "CSB1", 4) != 0) return fail(err, S_EFORMAT, "not a CSR file: " + p);
+    uint32_t flags = 0;
+    uint64_t rows = 0, cols = 0, nnz = 0;
+    // a header cut short reads as zeros in the reference's get_u* and is then
+    // reported as truncated (label.cpp:290)
+    const bool hdr = rd(&flags, 4) && rd(&rows, 8) && rd(&cols, 8) && rd(&nnz, 8);
+    const bool wide = flags & 1u;
+    if (hdr && cols > 0xffffffffull) return fail(err, S_EFORMAT, "CSR column space too large for this build");
+    const uint64_t isz = wide ? 8 : 4;
+    // truncation is checked before validation (label.cpp:290 then :296): the
+    // whole payload must be present
+    std::fseek(f, 0, SEEK_END);
+    const uint64_t fsize = static_cast<uint64_t>(std::ftell(f));
+    const long long data0 = 4 + 4 + 24;
+    if (!hdr || (rows + 1) > (UINT64_MAX / isz) ||
+        fsize < static_cast<uint64_t>(data0) + (rows + 1) * isz + nnz * isz)
+        return fail(err, S_EFORMAT, "truncated CSR file: " + p);
+    std::fseek(f, data0, SEEK_SET);
+    std::vector<uint64_t> offsets;
+    try {
+        offsets.assign(rows + 1, 0);
+    } catch (...) {
+        return fail(err, S_ENOMEM, "cannot allocate CSR of the declared size: " + p);
+    }
+    if (wide) {
+        if (!rd(offsets.data(), (rows + 1) * 8)) return fail(err, S_EFORMAT, "truncated CSR file: " + p);
+    } else {
+        std::vector<uint32_t> o32(rows + 1);
+        if (!rd(o32.data(), (rows + 1) * 4)) return fail(err, S_EFORMAT, "truncated CSR file: " + p);
+        for (uint64_t i = 0; i <= rows; ++i) offsets[i] = o32[i];
+    }
+    if (!check_offsets(rows, offsets.data(), rows + 1, nnz, err)) return false;
+    // stream the indices row range by row range: validate (first failing row
+    // in row order decides the message, label.cpp:32-39) and pack
+    out->rows = rows;
+    out->cols = cols;
+    out->nnz = nnz;
+    out->offsets.assign(rows + 1, 0);
+    out->word.clear();
+    out->mask.clear();
+    constexpr uint64_t kChunk = uint64_t(1) << 24;  // indices per read
+    std::vector<uint32_t> idx;
+    std::vector<uint64_t> tmp64;
+    for (uint64_t r0 = 0; r0 < rows;) {
+        uint64_t r1 = r0 + 1;
+        while (r1 < rows && offsets[r1 + 1] - offsets[r0] <= kChunk) ++r1;
+        const uint64_t k0 = offsets[r0], n = offsets[r1] - k0;
+        idx.resize(n);
+        if (wide) {
+            tmp64.resize(n);
+            if (n && !rd(tmp64.data(), n * 8)) return fail(err, S_EFORMAT, "truncated CSR file: " + p);
+            for (uint64_t i = 0; i < n; ++i) idx[i] = static_cast<uint32_t>(tmp64[i]);
+        } else if (n && !rd(idx.data(), n * 4)) {
+            return fail(err, S_EFORMAT, "truncated CSR file: " + p);
+        }
+        // rows [r0, r1): validate + count words, then fill
+        const uint64_t nr = r1 - r0;
+        std::vector<uint64_t> cnt(nr + 1, 0);
+        const int T = host_threads();
+        std::vector<uint64_t> first_bad(static_cast<size_t>(T) + 1, UINT64_MAX);
+        std::vector<int> kind(static_cast<size_t>(T) + 1, 0);
+        parallel_chunks(nr, 1 << 12, [&](uint64_t b, uint64_t e, int c) {
+            for (uint64_t i = b; i < e; ++i) {
+                uint64_t words = 0;
+                uint32_t last = UINT32_MAX;
+                for (uint64_t k = offsets[r0 + i] - k0; k < offsets[r0 + i + 1] - k0; ++k) {
+                    int why = 0;
+                    if (static_cast<uint64_t>(idx[k]) >= cols) why = 1;
+                    else if (k > offsets[r0 + i] - k0 && idx[k - 1] >= idx[k]) why = 2;
+                    if (why) {
+                        first_bad[static_cast<size_t>(c)] = i;
+                        kind[static_cast<size_t>(c)] = why;
+                        return;
+                    }
+                    const uint32_t w = idx[k] >> 5;
+                    words += (w != last);
+                    last = w;
+                }
+                cnt[i + 1] = words;
+            }
+        });
+        uint64_t best = UINT64_MAX;
+        int why = 0;
+        for (size_t c = 0; c < first_bad.size(); ++c)
+            if (first_bad[c] < best) {
+                best = first_bad[c];
+                why = kind[c];
+            }
+        if (why == 1) return fail(err, S_EINVAL, "column index out of range");
+        if (why == 2) return fail(err, S_EINVAL, "column indices must be strictly ascending per row");
+        for (uint64_t i = 0; i < nr; ++i) cnt[i + 1] += cnt[i];
+        const uint64_t w0 = out->word.size();
+        out->word.resize(w0 + cnt[nr], 0);
+        out->mask.resize(w0 + cnt[nr], 0);
+        for (uint64_t i = 0; i < nr; ++i) out->offsets[r0 + i + 1] = w0 + cnt[i + 1];
+        parallel_chunks(nr, 1 << 12, [&](uint64_t b, uint64_t e, int) {
+            for (uint64_t i = b; i < e; ++i) {
+                uint64_t o = w0 + cnt[i] - 1;
+                uint32_t last = UINT32_MAX;
+                for (uint64_t k = offsets[r0 + i] - k0; k < offsets[r0 + i + 1] - k0; ++k) {
+                    const uint32_t c = idx[k], w = c >> 5;
+                    if (w != last) {
+                        ++o;
+                        out->word[o] = w;
+                        last = w;
+                    }
+                    out->mask[o] |= 1u << (c & 31);
+                }
+            }
+        });
+        r0 = r1;
+    }
+    return true;
+}
+
+bool read_zobv(const char* path, uint64_t cells, uint64_t* dst, Error* err) {
+    const std::string p(path);
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return fail(err, S_EIO, "cannot open: " + p);
+    struct Closer {
+        FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    unsigned char header[16];
+    if (std::fread(header, 1, 16, f) != 16 || std::memcmp(header, "ZOBV", 4) != 0)
+        return fail(err, S_EFORMAT, "not a bitset file: " + p);
+    const int depth = header[5];
+    if (depth < 1 || depth > 63) return fail(err, S_EFORMAT, "corrupt bitset header");
+    const uint64_t size_bits = uint64_t(1) << depth, words = (size_bits + 63) / 64;
+    // DensePropMatrix(cells, columns): every column is `cells` long (label.cpp:125-127)
+    if (size_bits != cells) return fail(err, S_EINVAL, "column length mismatch");
+    if (std::fread(dst, 8, words, f) != words) return fail(err, S_EFORMAT, "truncated bitset file: " + p);
+    return true;  // 2^depth bits: no tail word to mask (from_words, grid.cpp:201-203)
+}
+
+bool write_lbm1(const char* path, uint64_t rows, int props, const uint64_t* words, Error* err) {
+    const std::string p(path);
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return fail(err, S_EIO, "cannot open for writing: " + p);
+    const uint32_t version = 1, pr = static_cast<uint32_t>(props);
+    const uint64_t n = rows * static_cast<uint64_t>((props + 63) / 64);
+    bool ok = std::fwrite("LBM1", 1, 4, f) == 4 && std::fwrite(&version, 4, 1, f) == 1 &&
+              std::fwrite(&rows, 8, 1, f) == 1 && std::fwrite(&pr, 4, 1, f) == 1 &&
+              (n == 0 || std::fwrite(words, 8, n, f) == n);
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) return fail(err, S_EIO, "write failed: " + p);
+    return true;
+}
+
 std::vector<uint64_t> shard_bounds(const WordCsr& t, int n) {
     std::vector<uint64_t> b(static_cast<size_t>(n) + 1, t.rows);
     b[0] = 0;

@@ -382,6 +382,16 @@ class LabelEngine:
     def submit_props(self, p: DensePropMatrix) -> None:
         self.submit_grid(p.cells(), p.num_props(), p.column_words(), 1)
 
+    def submit_grid_files(self, paths: Sequence[str], num_props: int, frames: int = 1) -> None:
+        """ZOBV proposition columns (paths[f * num_props + j]) -> labels
+        (load_bitset grid.cpp:375-405 + DensePropMatrix + label_all)."""
+        arr = (C.c_char_p * max(1, len(paths)))(*[os.fsencode(p) for p in paths])
+        self._ck(self._L.ltlg_submit_grid_files(self._h, arr, num_props, frames))
+
+    def save_labels(self, path: str, frame: int = 0) -> None:
+        """LBM1 file of one frame's labels (LabelMatrix::save, label.cpp:300-309)."""
+        self._ck(self._L.ltlg_save_labels(self._h, frame, os.fsencode(path)))
+
     def submit_grid_device(self, cells: int, num_props: int, device_words, frames: int = 1) -> None:
         self._ck(self._L.ltlg_submit_grid_device(self._h, cells, num_props, _ptr(device_words), frames))
 
@@ -438,6 +448,28 @@ class LabelEngine:
         a, b, c = C.c_float(), C.c_float(), C.c_float()
         self._ck(self._L.ltlg_stage_times(self._h, shard, back, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
+
+
+def read_csb1_shape(path: str):
+    """Host-only streaming CSB1 read + validate + pack (the loader of
+    ltlg_load_abstraction_file): (rows, cols, nnz, W32 words).  Raises like
+    CsrBoolMatrix::load (label.cpp:271-298)."""
+    L = N.lib()
+    r, c, n, w = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+    st = L.ltlg_read_csb1_words(os.fsencode(path), C.byref(r), C.byref(c), C.byref(n), C.byref(w))
+    if st:
+        _raise(st, L.ltlg_last_error(None).decode())
+    return r.value, c.value, n.value, w.value
+
+
+def read_zobv(path: str, cells: int) -> OccupancyBitset:
+    """One ZOBV column of `cells` bits (load_bitset, grid.cpp:375-405)."""
+    L = N.lib()
+    words = np.zeros((cells + 63) // 64, dtype=np.uint64)
+    st = L.ltlg_read_zobv(os.fsencode(path), cells, words.ctypes.data)
+    if st:
+        _raise(st, L.ltlg_last_error(None).decode())
+    return OccupancyBitset.from_words(cells, words)
 
 
 def label_all(m: CsrBoolMatrix, p: DensePropMatrix, workers: int = 0) -> LabelMatrix:

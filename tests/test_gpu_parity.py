@@ -371,3 +371,63 @@ def test_cpp_drop_in_parity():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASSED" in r.stdout
+
+
+def test_zobv_ingest_and_lbm1_dump(tmp_path):
+    # ZOBV proposition columns in (load_bitset, grid.cpp:375-405),
+    # LBM1 labels out (LabelMatrix::save, label.cpp:300-309), both byte-compatible
+    # with the reference's own writers.
+    from oracle.oracle import RefCore
+
+    if not RefCore.available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefCore()
+    depth, E, props, F = 12, 7_001, 5, 2
+    prm = SyntheticPRM(seed=31, depth=depth)
+    off, idx = prm.csr(0, E)
+    P = props_words(37, depth, props, 0, F)
+    paths = []
+    for f in range(F):
+        for j in range(props):
+            p = tmp_path / f"f{f}_p{j}.zobv"
+            ref.save_bitset(str(p), 2, depth, P[f, j])
+            paths.append(str(p))
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction(CsrBoolMatrix(E, 1 << depth, off, idx))
+    eng.submit_grid_files(paths, props, F)
+    for f in range(F):
+        want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[f])
+        assert eng.get_labels(f) == LabelMatrix(E, props, want)
+        ours, theirs = tmp_path / f"ours{f}.lbm", tmp_path / f"ref{f}.lbm"
+        eng.save_labels(str(ours), f)
+        ref.label_save(str(theirs), E, props, want)
+        assert ours.read_bytes() == theirs.read_bytes()
+    with pytest.raises(ValueError, match="column length mismatch"):
+        small = tmp_path / "small.zobv"
+        ref.save_bitset(str(small), 2, depth - 2, P[0, 0][: (1 << (depth - 2)) // 64])
+        eng.submit_grid_files([str(small)], 1, 1)
+    with pytest.raises(RuntimeError, match="cannot open"):
+        eng.submit_grid_files([str(tmp_path / "nope.zobv")], 1, 1)
+    eng.close()
+
+
+def test_csb1_streaming_load_large(tmp_path):
+    # the streaming CSB1 loader on a file with > 2^24 indices (several read
+    # chunks) labels exactly like the in-memory CSR path
+    from oracle.oracle import RefCore
+
+    if not RefCore.available():
+        pytest.skip("oracle/_ref not built")
+    depth, E, props = 16, 120_000, 9
+    prm = SyntheticPRM(seed=77, depth=depth)
+    off, idx = prm.csr(0, E)
+    assert idx.size > (1 << 24)
+    p = tmp_path / "big.csb1"
+    RefCore().csr_save(str(p), E, 1 << depth, off, idx)
+    P = props_words(3, depth, props, 0, 1)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_file(str(p))
+    eng.submit_grid(1 << depth, props, P[0], 1)
+    want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[0])
+    assert eng.get_labels(0) == LabelMatrix(E, props, want)
+    eng.close()
