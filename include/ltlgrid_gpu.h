@@ -163,6 +163,32 @@ ltlg_status ltlg_read_csb1_words(const char* path, uint64_t* rows, uint64_t* col
  * (ceil(cells/64) u64), with the ltlg_submit_grid_files checks. */
 ltlg_status ltlg_read_zobv(const char* path, uint64_t cells, uint64_t* words_out);
 
+/* k-D z-order grid (GridSpec, grid.hpp:22-57): axis a gets depth/k bits,
+ * the first depth%k axes one extra; bounds lo[a] < hi[a].  dims <= 4. */
+typedef struct ltlg_gridk {
+    int dims;
+    int depth;
+    double lo[4], hi[4];
+} ltlg_gridk;
+
+/* Rasterize axis-aligned boxes into z-ordered proposition columns on the GPU
+ * (rasterize_box, grid.cpp:260-344, one column = the union of its boxes):
+ * column c (of num_cols) is the union of boxes [box_offsets[c],
+ * box_offsets[c+1]); box b spans [box_lo[b*dims + a], box_hi[b*dims + a]] on
+ * axis a, cell ranges by overlap_cells (grid.cpp:49-61).  out_words =
+ * num_cols x ceil(2^depth/64) u64 (host).  Runs on `device`, synchronous.
+ * Errors: the GridSpec messages ("grid needs at least one axis", "grid depth
+ * must be in [k, 63]", "grid bounds must satisfy lo < hi"). */
+ltlg_status ltlg_rasterize_boxes(const ltlg_gridk* grid, int num_cols, const uint64_t* box_offsets,
+                                 const double* box_lo, const double* box_hi, int device, uint64_t* out_words);
+
+/* The same rasterization straight into the context's P (frames x num_props
+ * columns, column f*num_props + j), then labelling -- the frame's proposition
+ * volumes never touch host bitsets.  2^depth must equal cols
+ * of T.  Asynchronous like ltlg_submit_grid_device. */
+ltlg_status ltlg_submit_boxes(ltlg_ctx* ctx, const ltlg_gridk* grid, int num_props, int frames,
+                              const uint64_t* box_offsets, const double* box_lo, const double* box_hi);
+
 /* Block until every submitted frame is labelled. */
 ltlg_status ltlg_wait(ltlg_ctx* ctx);
 

@@ -279,6 +279,9 @@ class RefCore:
         L.ref_label_save.restype = i32
         L.ref_z_index.argtypes = [i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.ref_z_index.restype = u64
+        L.ref_rasterize_union.argtypes = [i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double), u64,
+                                          C.POINTER(C.c_double), C.POINTER(C.c_double), P64]
+        L.ref_rasterize_union.restype = i32
         L.ref_save_bitset.argtypes = [C.c_char_p, i32, i32, P64]
         L.ref_save_bitset.restype = i32
         self.lib = L
@@ -343,6 +346,23 @@ class RefCore:
         if n < 0:
             raise OracleError(self.error())
         return rows.value, cols.value, n
+
+    def rasterize_union(self, k, depth, lo, hi, box_lo, box_hi):
+        """OR of the reference's rasterize_box (grid.cpp:331-335) over boxes
+        (box_lo/box_hi: nboxes x k) of GridSpec(bounds, depth)."""
+        D = C.POINTER(C.c_double)
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        hi = np.ascontiguousarray(hi, dtype=np.float64)
+        blo = np.ascontiguousarray(box_lo, dtype=np.float64).reshape(-1)
+        bhi = np.ascontiguousarray(box_hi, dtype=np.float64).reshape(-1)
+        n = blo.size // k
+        if n == 0:
+            blo = bhi = np.zeros(1, dtype=np.float64)
+        out = np.zeros(((1 << depth) + 63) // 64, dtype=np.uint64)
+        if self.lib.ref_rasterize_union(k, depth, lo.ctypes.data_as(D), hi.ctypes.data_as(D), n,
+                                        blo.ctypes.data_as(D), bhi.ctypes.data_as(D), _p(out, C.c_uint64)):
+            raise OracleError(self.error())
+        return out
 
     def label_save(self, path, rows, props, words):
         words = np.ascontiguousarray(words, dtype=np.uint64)

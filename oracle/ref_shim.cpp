@@ -14,6 +14,7 @@
 // save_bitset (grid.cpp:370-390).
 #include <chrono>
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <limits>
@@ -236,6 +237,31 @@ int ref_save_bitset(const char* path, int k, int depth, const std::uint64_t* wor
         const std::uint64_t bits = std::uint64_t{1} << depth;
         std::vector<std::uint64_t> w(words, words + (bits + 63) / 64);
         ltlgrid::save_bitset(path, ltlgrid::OccupancyBitset::from_words(bits, std::move(w)), g);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// Union of rasterize_box (grid.cpp:331-335) over nboxes boxes of a k-D grid
+// (GridSpec(bounds, depth)) into out (ceil(2^depth / 64) u64 words).
+int ref_rasterize_union(int k, int depth, const double* lo, const double* hi, std::uint64_t nboxes,
+                        const double* blo, const double* bhi, std::uint64_t* out) {
+    try {
+        std::vector<std::pair<double, double>> bounds;
+        for (int a = 0; a < k; ++a) bounds.emplace_back(lo[a], hi[a]);
+        const ltlgrid::GridSpec g(bounds, depth);
+        const std::uint64_t words = (g.cell_count() + 63) / 64;
+        std::fill(out, out + words, 0);
+        for (std::uint64_t b = 0; b < nboxes; ++b) {
+            ltlgrid::Box box;
+            for (int a = 0; a < k; ++a) {
+                box.lo.push_back(blo[b * k + a]);
+                box.hi.push_back(bhi[b * k + a]);
+            }
+            const auto bits = ltlgrid::rasterize_box(box, g);
+            for (std::uint64_t w = 0; w < words; ++w) out[w] |= bits.words()[w];
+        }
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

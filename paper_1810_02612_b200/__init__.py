@@ -7,7 +7,7 @@ abstractions -- a drop-in for the reference's labeling path
   synth               synthetic T / P of the BASELINE configs
 """
 from .label import (CsrBoolMatrix, DensePropMatrix, LabelEngine, LabelMatrix, LtlgError,  # noqa: F401
-                    OccupancyBitset, label_all, read_csb1_shape, read_zobv, to_csr)
+                    OccupancyBitset, label_all, rasterize_boxes, read_csb1_shape, read_zobv, to_csr)
 
 __all__ = ["CsrBoolMatrix", "DensePropMatrix", "LabelEngine", "LabelMatrix", "LtlgError",
-           "OccupancyBitset", "label_all", "read_csb1_shape", "read_zobv", "to_csr"]
+           "OccupancyBitset", "label_all", "rasterize_boxes", "read_csb1_shape", "read_zobv", "to_csr"]

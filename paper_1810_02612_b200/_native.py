@@ -24,12 +24,17 @@ EXPORTS = [
     "ltlg_get_labels", "ltlg_get_labels_packed", "ltlg_device_labels", "ltlg_get_info",
     "ltlg_stream", "ltlg_stage_times", "ltlg_validate_csr", "ltlg_label_all",
     "ltlg_submit_grid_files", "ltlg_save_labels", "ltlg_read_csb1_words", "ltlg_read_zobv",
+    "ltlg_rasterize_boxes", "ltlg_submit_boxes",
 ]
 
 
 class Options(C.Structure):
     _fields_ = [("sort_rows", C.c_int), ("stream_task_pairs", C.c_int), ("batch_task_pairs", C.c_int),
                 ("profile", C.c_int), ("readback_chunks", C.c_int), ("reserved", C.c_int * 6)]
+
+
+class GridK(C.Structure):
+    _fields_ = [("dims", C.c_int), ("depth", C.c_int), ("lo", C.c_double * 4), ("hi", C.c_double * 4)]
 
 
 class Info(C.Structure):
@@ -93,6 +98,8 @@ def lib() -> C.CDLL:
         "ltlg_save_labels": ([ctxp, i32, C.c_char_p], i32),
         "ltlg_read_csb1_words": ([C.c_char_p, P64, P64, P64, P64], i32),
         "ltlg_read_zobv": ([C.c_char_p, u64, vp], i32),
+        "ltlg_rasterize_boxes": ([C.POINTER(GridK), i32, vp, vp, vp, i32, vp], i32),
+        "ltlg_submit_boxes": ([ctxp, C.POINTER(GridK), i32, i32, vp, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

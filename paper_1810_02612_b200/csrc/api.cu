@@ -9,6 +9,8 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -112,6 +114,8 @@ struct Shard {
     DevBuf<uint64_t> stage;
     DevBuf<uint64_t> world;
     DevBuf<uint8_t> poses;
+    DevBuf<uint64_t> poses_off;  // box offsets of ltlg_submit_boxes
+    DevBuf<uint8_t> box_rng;     // and their per-axis cell ranges
     DevBuf<uint32_t> ctr;  // persistent-kernel task counter
     DevBuf<uint8_t> s_only;  // S mask per (word, frame)
     bool have_times = false;
@@ -529,6 +533,8 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.stage.release();
         s.world.release();
         s.poses.release();
+        s.poses_off.release();
+        s.box_rng.release();
         s.ctr.release();
         s.s_only.release();
         for (auto& ev : s.ring)
@@ -705,6 +711,135 @@ ltlg_status ltlg_read_zobv(const char* path, uint64_t cells, uint64_t* words_out
     Error err{S_OK, ""};
     if (!read_zobv(path, cells, words_out, &err)) return set_err(nullptr, static_cast<ltlg_status>(err.code), err.msg);
     return LTLG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// GridSpec ctor checks (grid.cpp:18-33) + this build's limits.
+ltlg_status check_gridk(ltlg_ctx* ctx, const ltlg_gridk* g) {
+    if (!g) return set_err(ctx, LTLG_EINVAL, "null grid");
+    if (g->dims < 1) return set_err(ctx, LTLG_EINVAL, "grid needs at least one axis");
+    if (g->depth < g->dims || g->depth > 63) return set_err(ctx, LTLG_EINVAL, "grid depth must be in [k, 63]");
+    for (int a = 0; a < g->dims && a < 4; ++a)
+        if (!(g->lo[a] < g->hi[a])) return set_err(ctx, LTLG_EINVAL, "grid bounds must satisfy lo < hi");
+    if (g->dims > 4) return set_err(ctx, LTLG_EINVAL, "at most 4 grid axes in this build");
+    if (g->depth > 36) return set_err(ctx, LTLG_EINVAL, "grid depth > 36 not supported by this build");
+    return LTLG_OK;
+}
+
+// overlap_cells (grid.cpp:49-61) of every box on every axis -> int64 ranges
+// (first, last) x 4 per box; an empty overlap on any axis empties the box.
+std::vector<int64_t> box_ranges(const ltlg_gridk* g, uint64_t nboxes, const double* blo, const double* bhi) {
+    std::vector<int64_t> r(nboxes * 8, 0);
+    for (uint64_t b = 0; b < nboxes; ++b) {
+        bool empty = false;
+        for (int a = 0; a < 4; ++a) {
+            int64_t first = 0, last = 0;
+            if (a < g->dims) {
+                const int bits = g->depth / g->dims + (a < g->depth % g->dims ? 1 : 0);
+                const double lo = g->lo[a], hi = g->hi[a];
+                const double cells = static_cast<double>(uint64_t(1) << bits);
+                const double z_lo = (blo[b * g->dims + a] - lo) / (hi - lo) * cells;
+                const double z_hi = (bhi[b * g->dims + a] - lo) / (hi - lo) * cells;
+                first = static_cast<int64_t>(std::floor(z_lo));
+                last = static_cast<int64_t>(std::ceil(z_hi)) - 1;
+                first = std::max<int64_t>(first, 0);
+                last = std::min<int64_t>(last, static_cast<int64_t>(uint64_t(1) << bits) - 1);
+                if (first > last) empty = true;
+            }
+            r[b * 8 + 2 * a] = first;
+            r[b * 8 + 2 * a + 1] = last;
+        }
+        if (empty) {  // rasterize_box_impl returns early: no cells
+            r[b * 8] = 1;
+            r[b * 8 + 1] = 0;
+        }
+    }
+    return r;
+}
+
+// Upload ranges/offsets to `dev` scratch buffers and rasterize into out (device).
+ltlg_status rasterize_on(ltlg_ctx* ctx, const ltlg_gridk* g, int cols, const uint64_t* box_off, const double* blo,
+                         const double* bhi, DevBuf<uint64_t>& off_buf, DevBuf<uint8_t>& rng_buf, uint64_t* out,
+                         cudaStream_t st) {
+    const uint64_t nboxes = cols ? box_off[cols] : 0;
+    for (int c = 0; c < cols; ++c)
+        if (box_off[c] > box_off[c + 1]) return set_err(ctx, LTLG_EINVAL, "box_offsets must be nondecreasing");
+    const std::vector<int64_t> r = box_ranges(g, nboxes, blo, bhi);
+    CK(off_buf.reserve(static_cast<size_t>(cols + 1) * 8), "allocate boxes");
+    CK(rng_buf.reserve(r.empty() ? 8 : r.size() * 8), "allocate boxes");
+    CK(cudaMemcpyAsync(off_buf.ptr, box_off, static_cast<size_t>(cols + 1) * 8, cudaMemcpyHostToDevice, st), "upload boxes");
+    if (!r.empty())
+        CK(cudaMemcpyAsync(rng_buf.ptr, r.data(), r.size() * 8, cudaMemcpyHostToDevice, st), "upload boxes");
+    CK(launch_rasterize(g->dims, g->depth, cols, off_buf.ptr, reinterpret_cast<const int64_t*>(rng_buf.ptr), out, st),
+       "rasterize kernel");
+    // the pageable range upload must complete before r goes out of scope
+    CK(cudaStreamSynchronize(st), "rasterize");
+    return LTLG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ltlg_status ltlg_rasterize_boxes(const ltlg_gridk* grid, int num_cols, const uint64_t* box_offsets,
+                                 const double* box_lo, const double* box_hi, int device, uint64_t* out_words) {
+    ltlg_ctx* ctx = nullptr;
+    ltlg_status st = check_gridk(nullptr, grid);
+    if (st != LTLG_OK) return st;
+    if (num_cols < 0 || (num_cols && (!box_offsets || !out_words)))
+        return set_err(nullptr, LTLG_EINVAL, "null argument");
+    if (num_cols && box_offsets[num_cols] && (!box_lo || !box_hi)) return set_err(nullptr, LTLG_EINVAL, "null boxes");
+    const int devs[1] = {device};
+    if ((st = ltlg_create(devs, 1, &ctx)) != LTLG_OK) return st;
+    std::unique_ptr<ltlg_ctx, void (*)(ltlg_ctx*)> hold(ctx, ltlg_destroy);
+    Shard& s0 = ctx->shards[0];
+    const size_t nw = ((uint64_t(1) << grid->depth) + 63) / 64;
+    CK(s0.P.reserve(static_cast<size_t>(num_cols) * nw * 8 + 8), "allocate P");
+    st = rasterize_on(ctx, grid, num_cols, box_offsets, box_lo, box_hi, s0.poses_off, s0.box_rng, s0.P.ptr, s0.stream);
+    if (st != LTLG_OK) {
+        g_error = ctx->err;
+        return st;
+    }
+    if (num_cols) {
+        cudaError_t e = cudaMemcpy(out_words, s0.P.ptr, static_cast<size_t>(num_cols) * nw * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return cuda_fail(nullptr, e, "download P");
+    }
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_submit_boxes(ltlg_ctx* ctx, const ltlg_gridk* grid, int num_props, int frames,
+                              const uint64_t* box_offsets, const double* box_lo, const double* box_hi) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    ltlg_status st = check_gridk(ctx, grid);
+    if (st != LTLG_OK) return st;
+    const uint64_t cells = uint64_t(1) << grid->depth;
+    if ((st = check_grid(ctx, cells, num_props, frames)) != LTLG_OK) return st;
+    const int cols = frames * num_props;
+    if (cols && !box_offsets) return set_err(ctx, LTLG_EINVAL, "null box_offsets");
+    if (cols && box_offsets[cols] && (!box_lo || !box_hi)) return set_err(ctx, LTLG_EINVAL, "null boxes");
+    ctx->cells = cells;
+    ctx->props = num_props;
+    ctx->frames = frames;
+    ctx->label_bytes = label_bytes_for(num_props);
+    const size_t nwords = static_cast<size_t>(cols) * ((cells + 63) / 64);
+    for (Shard& s : ctx->shards) {
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        CK(s.P.reserve(nwords * 8 + 16), "allocate P");
+    }
+    if (ctx->opts.profile)
+        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
+    Shard& s0 = ctx->shards[0];
+    CK(cudaSetDevice(s0.device), "cudaSetDevice");
+    s0.P_in = nullptr;
+    if (ctx->opts.profile) CK(cudaEventRecord(s0.ev[0], s0.stream), "event");
+    if ((st = rasterize_on(ctx, grid, cols, box_offsets, box_lo, box_hi, s0.poses_off, s0.box_rng, s0.P.ptr, s0.stream)) !=
+        LTLG_OK)
+        return st;
+    if ((st = broadcast_P(ctx, nwords)) != LTLG_OK) return st;
+    return run_label(ctx, false);
 }
 
 ltlg_status ltlg_wait(ltlg_ctx* ctx) {

@@ -42,6 +42,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <vector>
 
 #include "engine.h"
 #include "launch.h"
@@ -1238,6 +1239,58 @@ __global__ void resample_kernel(Grid2 vg, Grid2 wg, const Pose2* __restrict__ po
 
 
 // ---------------------------------------------------------------------------
+// Box rasterization into z-ordered P (rasterize_box,
+// grid.cpp:260-344).  The host turns every box into integer per-axis cell
+// ranges [first, last] with the reference's overlap_cells (grid.cpp:49-61);
+// here a thread owns one 64-cell z-word of one (frame, prop) column and ORs
+// the boxes' cell masks.  Within a word the low 6 z-bits give every cell a
+// fixed per-axis offset, so the cells of axis a whose coordinate lies in
+// [first, last] form OR_v PAT[a][v] over the in-range offsets v; a box's
+// mask is the AND of its axes' masks.
+// ---------------------------------------------------------------------------
+struct RasterGeom {
+    int k;                 // axes (<= kMaxRasterAxes)
+    int depth;
+    uint32_t nvals[4];     // distinct within-word offsets per axis
+};
+__constant__ uint64_t c_raster_pat[4][64];  // [axis][offset] -> cells of the word with that offset
+__constant__ RasterGeom c_raster_geom;
+
+__global__ void __launch_bounds__(256) rasterize_kernel(uint32_t nw64, int cols_total, const uint64_t* __restrict__ box_off,
+                                                        const int64_t* __restrict__ ranges, uint64_t cells,
+                                                        uint64_t* __restrict__ out) {
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int col = blockIdx.y;  // frame * props + prop
+    if (w >= nw64 || col >= cols_total) return;
+    const RasterGeom& g = c_raster_geom;
+    // base coordinates of the word's first cell (de-interleave z = 64 w,
+    // level l = MSB first, axis l % k, axis bit bits_a - 1 - l / k)
+    int64_t base[4] = {0, 0, 0, 0};
+    const uint64_t z = static_cast<uint64_t>(w) << 6;
+    for (int l = 0; l < g.depth; ++l) {
+        const int a = l % g.k;
+        base[a] = (base[a] << 1) | static_cast<int64_t>((z >> (g.depth - 1 - l)) & 1u);
+    }
+    uint64_t m = 0;
+    for (uint64_t b = box_off[col]; b < box_off[col + 1]; ++b) {
+        const int64_t* r = ranges + b * 8;  // first/last per axis
+        uint64_t bm = ~0ull;
+        for (int a = 0; a < g.k; ++a) {
+            uint64_t am = 0;
+            for (uint32_t v = 0; v < g.nvals[a]; ++v) {
+                const int64_t c = base[a] + static_cast<int64_t>(v);
+                if (c >= r[2 * a] && c <= r[2 * a + 1]) am |= c_raster_pat[a][v];
+            }
+            bm &= am;
+        }
+        m |= bm;
+    }
+    const uint64_t lo = static_cast<uint64_t>(w) * 64;
+    if (cells - lo < 64) m &= (1ull << (cells - lo)) - 1ull;
+    out[static_cast<uint64_t>(col) * nw64 + w] = m;
+}
+
+// ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells, void* tab,
@@ -1615,6 +1668,44 @@ cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, i
         case 4: extract_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint32_t*>(labels), rows, frames, frame, out); break;
         default: extract_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint64_t*>(labels), rows, frames, frame, out); break;
     }
+    return cudaGetLastError();
+}
+
+// ranges: nboxes x (first, last) per axis (4 axes, int64), box_off: cols + 1
+cudaError_t launch_rasterize(int k, int depth, int cols_total, const uint64_t* box_off, const int64_t* ranges,
+                             uint64_t* out, cudaStream_t st) {
+    if (k < 1 || k > 4 || depth < k || depth > 36) return cudaErrorInvalidValue;
+    RasterGeom g{};
+    g.k = k;
+    g.depth = depth;
+    uint64_t pat[4][64] = {};
+    const int low = depth < 6 ? depth : 6;  // z-bits inside one 64-cell word
+    std::vector<int> bits(static_cast<size_t>(k));
+    for (int a = 0; a < k; ++a) bits[static_cast<size_t>(a)] = depth / k + (a < depth % k ? 1 : 0);
+    for (int a = 0; a < k; ++a) {
+        uint32_t nv = 1;
+        for (int p = 0; p < low; ++p)
+            if ((depth - 1 - p) % k == a) nv <<= 1;
+        g.nvals[a] = nv;
+    }
+    for (uint32_t b = 0; b < (1u << low); ++b) {
+        uint32_t off[4] = {0, 0, 0, 0};
+        for (int p = 0; p < low; ++p) {
+            if (!(b >> p & 1u)) continue;
+            const int l = depth - 1 - p, a = l % k, ab = bits[static_cast<size_t>(a)] - 1 - l / k;
+            off[a] |= 1u << ab;
+        }
+        for (int a = 0; a < k; ++a) pat[a][off[a]] |= 1ull << b;
+    }
+    cudaError_t e = cudaMemcpyToSymbolAsync(c_raster_pat, pat, sizeof(pat), 0, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyToSymbolAsync(c_raster_geom, &g, sizeof(g), 0, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    const uint64_t cells = 1ull << depth;
+    const uint32_t nw64 = static_cast<uint32_t>((cells + 63) / 64);
+    if (cols_total == 0) return cudaSuccess;
+    dim3 grid((nw64 + 255) / 256, static_cast<unsigned>(cols_total));
+    rasterize_kernel<<<grid, 256, 0, st>>>(nw64, cols_total, box_off, ranges, cells, out);
     return cudaGetLastError();
 }
 

@@ -388,6 +388,14 @@ class LabelEngine:
         arr = (C.c_char_p * max(1, len(paths)))(*[os.fsencode(p) for p in paths])
         self._ck(self._L.ltlg_submit_grid_files(self._h, arr, num_props, frames))
 
+    def submit_boxes(self, dims: int, depth: int, lo, hi, columns, num_props: int, frames: int = 1) -> None:
+        """Rasterize boxes into P on the GPU (column f * num_props + j = union
+        of columns[...] boxes) and label."""
+        g = _gridk(dims, depth, lo, hi)
+        off, blo, bhi = _boxes(columns)
+        self._ck(self._L.ltlg_submit_boxes(self._h, C.byref(g), num_props, frames, off.ctypes.data, blo.ctypes.data,
+                                           bhi.ctypes.data))
+
     def save_labels(self, path: str, frame: int = 0) -> None:
         """LBM1 file of one frame's labels (LabelMatrix::save, label.cpp:300-309)."""
         self._ck(self._L.ltlg_save_labels(self._h, frame, os.fsencode(path)))
@@ -448,6 +456,43 @@ class LabelEngine:
         a, b, c = C.c_float(), C.c_float(), C.c_float()
         self._ck(self._L.ltlg_stage_times(self._h, shard, back, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
+
+
+def _gridk(dims: int, depth: int, lo, hi) -> "N.GridK":
+    g = N.GridK()
+    g.dims, g.depth = dims, depth
+    for a in range(min(dims, 4)):
+        g.lo[a], g.hi[a] = float(lo[a]), float(hi[a])
+    return g
+
+
+def _boxes(columns):
+    """[[(lo, hi), ...] per column] -> (offsets u64, lo f64 flat, hi f64 flat)."""
+    off = np.zeros(len(columns) + 1, dtype=np.uint64)
+    lo, hi = [], []
+    for c, boxes in enumerate(columns):
+        for b_lo, b_hi in boxes:
+            lo.extend(b_lo)
+            hi.extend(b_hi)
+        off[c + 1] = off[c] + len(boxes)
+    lo = np.asarray(lo if lo else [0.0], dtype=np.float64)
+    hi = np.asarray(hi if hi else [0.0], dtype=np.float64)
+    return off, lo, hi
+
+
+def rasterize_boxes(dims: int, depth: int, lo, hi, columns, device: int = 0) -> np.ndarray:
+    """GPU rasterize_box (grid.cpp:260-344): column c = union of its boxes
+    [(box_lo, box_hi), ...] on the k-D z-order grid GridSpec(bounds, depth).
+    Returns [len(columns), ceil(2^depth/64)] u64 column words."""
+    L = N.lib()
+    g = _gridk(dims, depth, lo, hi)
+    off, blo, bhi = _boxes(columns)
+    out = np.zeros((max(1, len(columns)), ((1 << depth) + 63) // 64), dtype=np.uint64)
+    st = L.ltlg_rasterize_boxes(C.byref(g), len(columns), off.ctypes.data, blo.ctypes.data, bhi.ctypes.data, device,
+                                out.ctypes.data)
+    if st:
+        _raise(st, L.ltlg_last_error(None).decode())
+    return out[: len(columns)]
 
 
 def read_csb1_shape(path: str):

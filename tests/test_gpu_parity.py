@@ -431,3 +431,74 @@ def test_csb1_streaming_load_large(tmp_path):
     want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[0])
     assert eng.get_labels(0) == LabelMatrix(E, props, want)
     eng.close()
+
+
+RASTER_GRIDS = [(1, 9), (2, 6), (2, 7), (2, 12), (2, 13), (3, 9), (3, 14), (3, 21)]
+
+
+@pytest.mark.parametrize("k,depth", RASTER_GRIDS)
+def test_rasterize_boxes_vs_reference(k, depth):
+    # GPU rasterize_box == the reference's rasterize_box (grid.cpp:260-344),
+    # unions per column; boxes partly outside, degenerate (lo == hi), inverted, tiny.
+    from oracle.oracle import RefCore
+
+    if not RefCore.available():
+        pytest.skip("oracle/_ref not built")
+    from paper_1810_02612_b200 import rasterize_boxes
+
+    ref = RefCore()
+    rng = np.random.default_rng(1000 * k + depth)
+    lo = rng.uniform(-50, 0, size=k)
+    hi = lo + rng.uniform(10, 80, size=k)
+    columns = []
+    for c in range(7):
+        boxes = []
+        for _ in range(int(rng.integers(0, 6))):
+            a = rng.uniform(lo - 5, hi + 5)
+            b = a + rng.uniform(-2, 0.6, size=k) * (hi - lo)
+            kind = rng.integers(0, 4)
+            if kind == 0:
+                b = a.copy()  # degenerate: zero measure
+            boxes.append((a.tolist(), b.tolist()))
+        columns.append(boxes)
+    got = rasterize_boxes(k, depth, lo, hi, columns)
+    for c, boxes in enumerate(columns):
+        blo = np.array([b[0] for b in boxes]).reshape(-1, k) if boxes else np.zeros((0, k))
+        bhi = np.array([b[1] for b in boxes]).reshape(-1, k) if boxes else np.zeros((0, k))
+        want = ref.rasterize_union(k, depth, lo, hi, blo, bhi)
+        assert np.array_equal(got[c], want), (c, boxes)
+
+
+def test_submit_boxes_labels_and_errors():
+    from oracle.oracle import RefCore
+
+    if not RefCore.available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefCore()
+    depth, E, props, F = 14, 20_000, 6, 3
+    prm = SyntheticPRM(seed=5, depth=depth)
+    off, idx = prm.csr(0, E)
+    lo, hi = [0.0, 0.0], [102.4, 102.4]
+    rng = np.random.default_rng(9)
+    columns = []
+    for _ in range(F * props):
+        boxes = []
+        for _ in range(int(rng.integers(1, 7))):
+            c = rng.uniform(0, 102.4, size=2)
+            boxes.append(((c - 3).tolist(), (c + rng.uniform(0.1, 9, size=2)).tolist()))
+        columns.append(boxes)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction(CsrBoolMatrix(E, 1 << depth, off, idx))
+    eng.submit_boxes(2, depth, lo, hi, columns, props, F)
+    for f in range(F):
+        P = np.stack([ref.rasterize_union(2, depth, lo, hi, np.array([b[0] for b in columns[f * props + j]]),
+                                          np.array([b[1] for b in columns[f * props + j]])) for j in range(props)])
+        want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P)
+        assert eng.get_labels(f) == LabelMatrix(E, props, want)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        eng.submit_boxes(2, depth + 2, lo, hi, columns[:1], 1, 1)
+    with pytest.raises(ValueError, match="grid bounds must satisfy lo < hi"):
+        eng.submit_boxes(2, depth, [0.0, 5.0], [1.0, 5.0], columns[:1], 1, 1)
+    with pytest.raises(ValueError, match=r"grid depth must be in \[k, 63\]"):
+        eng.submit_boxes(3, 2, [0.0] * 3, [1.0] * 3, columns[:1], 1, 1)
+    eng.close()
