@@ -189,6 +189,21 @@ ltlg_status ltlg_rasterize_boxes(const ltlg_gridk* grid, int num_cols, const uin
 ltlg_status ltlg_submit_boxes(ltlg_ctx* ctx, const ltlg_gridk* grid, int num_props, int frames,
                               const uint64_t* box_offsets, const double* box_lo, const double* box_hi);
 
+/* Resident-label consumer: monitor transition guards
+ * (TransitionGuard {positive, negative}, buchi.hpp:16-26; admits(s) =
+ * (s & positive) == positive && (s & negative) == 0).  After every later
+ * submit the engine also computes, per (edge, frame), the u64 mask of
+ * admitted guards (bit t = guard t admits the edge's label) -- the edge test
+ * of build_product (planner.cpp:53-64; AND it with the live-target mask).
+ * n_guards in [0, 64]; 0 turns the consumer off. */
+ltlg_status ltlg_set_guards(ltlg_ctx* ctx, int n_guards, const uint64_t* positive, const uint64_t* negative);
+
+/* Copy one frame's admitted-guard masks (rows u64).  Synchronous. */
+ltlg_status ltlg_get_admitted(ltlg_ctx* ctx, int frame, uint64_t* out);
+
+/* Resident admitted-guard masks of shard s (rows x frames u64, edge-major). */
+ltlg_status ltlg_device_admitted(ltlg_ctx* ctx, int shard, void** dev_ptr);
+
 /* Block until every submitted frame is labelled. */
 ltlg_status ltlg_wait(ltlg_ctx* ctx);
 

@@ -282,6 +282,8 @@ class RefCore:
         L.ref_rasterize_union.argtypes = [i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double), u64,
                                           C.POINTER(C.c_double), C.POINTER(C.c_double), P64]
         L.ref_rasterize_union.restype = i32
+        L.ref_guard_admits.argtypes = [u64, P64, i32, P64, P64, P64]
+        L.ref_guard_admits.restype = None
         L.ref_save_bitset.argtypes = [C.c_char_p, i32, i32, P64]
         L.ref_save_bitset.restype = i32
         self.lib = L
@@ -363,6 +365,20 @@ class RefCore:
                                         blo.ctypes.data_as(D), bhi.ctypes.data_as(D), _p(out, C.c_uint64)):
             raise OracleError(self.error())
         return out
+
+    def guard_admits(self, labels, positive, negative):
+        """TransitionGuard::admits (buchi.hpp:20-22): bit t of out[i] = guard t
+        admits labels[i]."""
+        labels = np.ascontiguousarray(labels, dtype=np.uint64).reshape(-1)
+        pos = np.ascontiguousarray(positive, dtype=np.uint64)
+        neg = np.ascontiguousarray(negative, dtype=np.uint64)
+        out = np.zeros(max(1, labels.size), dtype=np.uint64)
+        lab = labels if labels.size else np.zeros(1, dtype=np.uint64)
+        g = max(1, pos.size)
+        self.lib.ref_guard_admits(labels.size, _p(lab, C.c_uint64), pos.size,
+                                  _p(pos if pos.size else np.zeros(g, np.uint64), C.c_uint64),
+                                  _p(neg if neg.size else np.zeros(g, np.uint64), C.c_uint64), _p(out, C.c_uint64))
+        return out[: labels.size]
 
     def label_save(self, path, rows, props, words):
         words = np.ascontiguousarray(words, dtype=np.uint64)

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "ltlgrid/grid.hpp"
+#include "ltlgrid/buchi.hpp"
 #include "ltlgrid/label.hpp"
 #include "ltlgrid/rng.hpp"
 
@@ -265,6 +266,24 @@ int ref_rasterize_union(int k, int depth, const double* lo, const double* hi, st
         return 0;
     } catch (const std::exception& e) {
         return fail(e);
+    }
+}
+
+// TransitionGuard::admits (buchi.hpp:20-22) of every (label, guard):
+// out[i] bit t = guard t admits labels[i].
+void ref_guard_admits(std::uint64_t n, const std::uint64_t* labels, int n_guards, const std::uint64_t* pos,
+                      const std::uint64_t* neg, std::uint64_t* out) {
+    for (std::uint64_t i = 0; i < n; ++i) {
+        ltlgrid::AlphabetSymbol sym;
+        sym.bits = labels[i];
+        std::uint64_t m = 0;
+        for (int t = 0; t < n_guards; ++t) {
+            ltlgrid::TransitionGuard g;
+            g.positive = pos[t];
+            g.negative = neg[t];
+            if (g.admits(sym)) m |= std::uint64_t{1} << t;
+        }
+        out[i] = m;
     }
 }
 

@@ -24,7 +24,7 @@ EXPORTS = [
     "ltlg_get_labels", "ltlg_get_labels_packed", "ltlg_device_labels", "ltlg_get_info",
     "ltlg_stream", "ltlg_stage_times", "ltlg_validate_csr", "ltlg_label_all",
     "ltlg_submit_grid_files", "ltlg_save_labels", "ltlg_read_csb1_words", "ltlg_read_zobv",
-    "ltlg_rasterize_boxes", "ltlg_submit_boxes",
+    "ltlg_rasterize_boxes", "ltlg_submit_boxes", "ltlg_set_guards", "ltlg_get_admitted", "ltlg_device_admitted",
 ]
 
 
@@ -100,6 +100,9 @@ def lib() -> C.CDLL:
         "ltlg_read_zobv": ([C.c_char_p, u64, vp], i32),
         "ltlg_rasterize_boxes": ([C.POINTER(GridK), i32, vp, vp, vp, i32, vp], i32),
         "ltlg_submit_boxes": ([ctxp, C.POINTER(GridK), i32, i32, vp, vp, vp], i32),
+        "ltlg_set_guards": ([ctxp, i32, vp, vp], i32),
+        "ltlg_get_admitted": ([ctxp, i32, vp], i32),
+        "ltlg_device_admitted": ([ctxp, i32, C.POINTER(vp)], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

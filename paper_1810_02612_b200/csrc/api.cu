@@ -115,6 +115,9 @@ struct Shard {
     DevBuf<uint64_t> world;
     DevBuf<uint8_t> poses;
     DevBuf<uint64_t> poses_off;  // box offsets of ltlg_submit_boxes
+    DevBuf<uint64_t> admitted;   // guard consumer: rows x frames admitted-guard masks
+    DevBuf<uint64_t> guard_lut;  // its byte lookup table (8 x 256)
+    uint64_t guard_lut_key = ~0ull;  // (guard epoch, props) the uploaded table is for
     DevBuf<uint8_t> box_rng;     // and their per-axis cell ranges
     DevBuf<uint32_t> ctr;  // persistent-kernel task counter
     DevBuf<uint8_t> s_only;  // S mask per (word, frame)
@@ -132,6 +135,8 @@ struct ltlg_ctx {
     bool loaded = false, submitted = false;
     uint64_t rows = 0, cols = 0, nnz = 0, words = 0, pairs = 0, t_bytes = 0;
     int props = 0, frames = 0, label_bytes = 0;
+    std::vector<uint64_t> guard_pos, guard_neg;  // monitor guards (ltlg_set_guards)
+    uint64_t guard_epoch = 0;                    // bumped by every ltlg_set_guards
     uint64_t cells = 0;
 };
 
@@ -300,6 +305,40 @@ ltlg_status broadcast_P(ltlg_ctx* ctx, size_t words) {
 }
 
 // Summary + labeling on every shard for P already resident in shard.P.
+// Resident-label consumer: admitted-guard masks of shard s for the current
+// submit (labels already enqueued on s.stream).
+ltlg_status run_guards(ltlg_ctx* ctx, Shard& s) {
+    const int props = ctx->props, frames = ctx->frames;
+    const int nbytes = ctx->label_bytes;
+    std::vector<uint64_t> lut(static_cast<size_t>(nbytes) * 256, 0);
+    uint64_t always = 0;
+    const size_t ng = ctx->guard_pos.size();
+    for (int j = 0; j < 64; ++j) {
+        uint64_t needs = 0, forbids = 0;  // guards with prop j positive / negative
+        for (size_t t = 0; t < ng; ++t) {
+            needs |= (ctx->guard_pos[t] >> j & 1u) << t;
+            forbids |= (ctx->guard_neg[t] >> j & 1u) << t;
+        }
+        if (j >= 8 * nbytes || j >= props) {  // the label never carries prop j
+            always |= needs;
+            continue;
+        }
+        for (int v = 0; v < 256; ++v) lut[static_cast<size_t>(j / 8) * 256 + v] |= (v >> (j % 8) & 1) ? forbids : needs;
+    }
+    const uint64_t all = ng >= 64 ? ~0ull : ((1ull << ng) - 1ull);
+    const uint64_t n = s.rows() * static_cast<uint64_t>(frames);
+    CK(s.admitted.reserve(n * 8), "allocate guards");
+    if (s.guard_lut_key != ctx->guard_epoch * 128 + static_cast<uint64_t>(props)) {  // (re)upload on change only
+        CK(s.guard_lut.reserve(8 * 256 * 8), "allocate guards");
+        CK(cudaMemcpyAsync(s.guard_lut.ptr, lut.data(), lut.size() * 8, cudaMemcpyHostToDevice, s.stream), "guards");
+        CK(cudaStreamSynchronize(s.stream), "guards");  // the pageable upload completes before lut goes away
+        s.guard_lut_key = ctx->guard_epoch * 128 + static_cast<uint64_t>(props);
+    }
+    CK(launch_guards(s.labels.ptr, nbytes, n, s.guard_lut.ptr, always, all, s.admitted.ptr, s.stream),
+       "guard kernel");
+    return LTLG_OK;
+}
+
 // split: one launch per read-back block (submits whose labels are expected
 // to go back to the host: host-memory P); otherwise one launch.
 ltlg_status run_label(ltlg_ctx* ctx, bool split) {
@@ -312,6 +351,11 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         if (props == 0 || s.rows() == 0) {
             s.have_times = false;
             s.blocks_last = 0;
+            if (s.rows() && !ctx->guard_pos.empty()) {  // no props: every label is empty
+                CK(cudaMemsetAsync(s.labels.ptr, 0, lab, s.stream), "labels");
+                const ltlg_status gst = run_guards(ctx, s);
+                if (gst != LTLG_OK) return gst;
+            }
             continue;
         }
         const uint32_t nw64 = nw32 / 2;
@@ -383,6 +427,10 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
             if (nb > 1) CK(cudaEventRecord(s.block_done[static_cast<size_t>(c)], s.stream), "event");
         }
         s.blocks_last = nb;
+        if (!ctx->guard_pos.empty()) {
+            const ltlg_status gst = run_guards(ctx, s);
+            if (gst != LTLG_OK) return gst;
+        }
         if (prof) CK(cudaEventRecord(s.ev[3], s.stream), "event");
         s.have_times = prof;
     }
@@ -534,6 +582,8 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.world.release();
         s.poses.release();
         s.poses_off.release();
+        s.admitted.release();
+        s.guard_lut.release();
         s.box_rng.release();
         s.ctr.release();
         s.s_only.release();
@@ -840,6 +890,41 @@ ltlg_status ltlg_submit_boxes(ltlg_ctx* ctx, const ltlg_gridk* grid, int num_pro
         return st;
     if ((st = broadcast_P(ctx, nwords)) != LTLG_OK) return st;
     return run_label(ctx, false);
+}
+
+ltlg_status ltlg_set_guards(ltlg_ctx* ctx, int n_guards, const uint64_t* positive, const uint64_t* negative) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (n_guards < 0 || n_guards > 64) return set_err(ctx, LTLG_EINVAL, "guards must be in [0, 64]");
+    if (n_guards && (!positive || !negative)) return set_err(ctx, LTLG_EINVAL, "null guards");
+    ctx->guard_pos.assign(positive, positive + n_guards);
+    ctx->guard_neg.assign(negative, negative + n_guards);
+    ++ctx->guard_epoch;
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_get_admitted(ltlg_ctx* ctx, int frame, uint64_t* out) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
+    if (ctx->guard_pos.empty()) return set_err(ctx, LTLG_ESTATE, "no guards set");
+    if (frame < 0 || frame >= ctx->frames) return set_err(ctx, LTLG_EINVAL, "frame out of range");
+    if (ctx->rows && !out) return set_err(ctx, LTLG_EINVAL, "null output");
+    for (Shard& s : ctx->shards) {
+        if (s.rows() == 0) continue;
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        // strided copy: frame `frame` of every edge (edge-major rows x frames)
+        CK(cudaMemcpy2DAsync(out + s.row_begin, 8, s.admitted.ptr + frame, static_cast<size_t>(ctx->frames) * 8, 8,
+                             s.rows(), cudaMemcpyDeviceToHost, s.stream),
+           "download admitted");
+    }
+    return sync_all(ctx);
+}
+
+ltlg_status ltlg_device_admitted(ltlg_ctx* ctx, int shard, void** dev_ptr) {
+    if (!ctx || !dev_ptr) return set_err(ctx, LTLG_EINVAL, "null argument");
+    if (shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return set_err(ctx, LTLG_EINVAL, "shard out of range");
+    if (!ctx->submitted || ctx->guard_pos.empty()) return set_err(ctx, LTLG_ESTATE, "no guarded submit");
+    *dev_ptr = ctx->shards[static_cast<size_t>(shard)].admitted.ptr;
+    return LTLG_OK;
 }
 
 ltlg_status ltlg_wait(ltlg_ctx* ctx) {

@@ -1239,6 +1239,35 @@ __global__ void resample_kernel(Grid2 vg, Grid2 wg, const Pose2* __restrict__ po
 
 
 // ---------------------------------------------------------------------------
+// Resident-label consumer: monitor transition guards
+// TransitionGuard::admits (buchi.hpp:20-22) evaluated over the resident
+// labels, as the per-(edge, frame) mask of admitted transitions that
+// build_product needs (planner.cpp:53-64).  Guard t is violated by a label L
+// iff some prop of positive[t] is absent or some prop of negative[t] present;
+// per label byte the violated set is a table lookup:
+//   violated(L) = always | OR_b lut[b][(L >> 8b) & 255]
+// (lut in shared memory: nbytes x 256 u64; `always` = guards needing a prop
+// the labels do not carry).
+// ---------------------------------------------------------------------------
+template <typename SW>
+__global__ void __launch_bounds__(256) guard_kernel(const SW* __restrict__ labels, uint64_t n,
+                                                    const uint64_t* __restrict__ lut, uint64_t always,
+                                                    uint64_t all_guards, uint64_t* __restrict__ admitted) {
+    constexpr int kBytes = sizeof(SW);
+    __shared__ uint64_t s_lut[kBytes * 256];
+    for (int i = threadIdx.x; i < kBytes * 256; i += blockDim.x) s_lut[i] = lut[i];
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t L = static_cast<uint64_t>(labels[i]);
+        uint64_t v = always;
+#pragma unroll
+        for (int b = 0; b < kBytes; ++b) v |= s_lut[b * 256 + ((L >> (8 * b)) & 255u)];
+        admitted[i] = ~v & all_guards;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Box rasterization into z-ordered P (rasterize_box,
 // grid.cpp:260-344).  The host turns every box into integer per-axis cell
 // ranges [first, last] with the reference's overlap_cells (grid.cpp:49-61);
@@ -1667,6 +1696,19 @@ cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, i
         case 2: extract_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint16_t*>(labels), rows, frames, frame, out); break;
         case 4: extract_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint32_t*>(labels), rows, frames, frame, out); break;
         default: extract_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint64_t*>(labels), rows, frames, frame, out); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_guards(const void* labels, int label_bytes, uint64_t n, const uint64_t* lut, uint64_t always,
+                          uint64_t all_guards, uint64_t* admitted, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148ull * 16));
+    switch (label_bytes) {
+        case 1: guard_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint8_t*>(labels), n, lut, always, all_guards, admitted); break;
+        case 2: guard_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint16_t*>(labels), n, lut, always, all_guards, admitted); break;
+        case 4: guard_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint32_t*>(labels), n, lut, always, all_guards, admitted); break;
+        default: guard_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint64_t*>(labels), n, lut, always, all_guards, admitted); break;
     }
     return cudaGetLastError();
 }

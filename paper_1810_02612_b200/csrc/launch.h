@@ -55,6 +55,8 @@ bool stream_table_in_smem(int props, uint32_t nw32);
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st);
 cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, int frames, int frame,
                            uint64_t* out, cudaStream_t st);
+cudaError_t launch_guards(const void* labels, int label_bytes, uint64_t n, const uint64_t* lut, uint64_t always,
+                          uint64_t all_guards, uint64_t* admitted, cudaStream_t st);
 cudaError_t launch_rasterize(int k, int depth, int cols_total, const uint64_t* box_off, const int64_t* ranges,
                              uint64_t* out, cudaStream_t st);
 cudaError_t launch_resample(int vdepth, double vlo0, double vhi0, double vlo1, double vhi1, int wdepth,

@@ -396,6 +396,23 @@ class LabelEngine:
         self._ck(self._L.ltlg_submit_boxes(self._h, C.byref(g), num_props, frames, off.ctypes.data, blo.ctypes.data,
                                            bhi.ctypes.data))
 
+    def set_guards(self, positive, negative) -> None:
+        """Monitor transition guards (TransitionGuard, buchi.hpp:16-26) whose
+        admitted-masks are computed over the resident labels after every
+        submit.  Empty lists turn the consumer off."""
+        pos = np.ascontiguousarray(positive, dtype=np.uint64)
+        neg = np.ascontiguousarray(negative, dtype=np.uint64)
+        if pos.shape != neg.shape:
+            raise ValueError("positive and negative guard lists differ in length")
+        self._ck(self._L.ltlg_set_guards(self._h, int(pos.size), pos.ctypes.data if pos.size else None,
+                                         neg.ctypes.data if neg.size else None))
+
+    def get_admitted(self, frame: int = 0) -> np.ndarray:
+        """u64 per edge: bit t = guard t admits the edge's label in `frame`."""
+        out = np.zeros(max(1, self.info().rows), dtype=np.uint64)
+        self._ck(self._L.ltlg_get_admitted(self._h, frame, out.ctypes.data))
+        return out[: self.info().rows]
+
     def save_labels(self, path: str, frame: int = 0) -> None:
         """LBM1 file of one frame's labels (LabelMatrix::save, label.cpp:300-309)."""
         self._ck(self._L.ltlg_save_labels(self._h, frame, os.fsencode(path)))

@@ -502,3 +502,39 @@ def test_submit_boxes_labels_and_errors():
     with pytest.raises(ValueError, match=r"grid depth must be in \[k, 63\]"):
         eng.submit_boxes(3, 2, [0.0] * 3, [1.0] * 3, columns[:1], 1, 1)
     eng.close()
+
+
+@pytest.mark.parametrize("props", [0, 5, 16, 32, 40])
+def test_guard_consumer_vs_reference(props):
+    # admitted-guard masks over the resident labels ==
+    # TransitionGuard::admits (buchi.hpp:20-22) of the oracle's labels.
+    from oracle.oracle import RefCore
+
+    if not RefCore.available():
+        pytest.skip("oracle/_ref not built")
+    ref = RefCore()
+    depth, E, F = 12, 9_000, 3
+    prm = SyntheticPRM(seed=19, depth=depth)
+    off, idx = prm.csr(0, E)
+    P = props_words(41, depth, props, 0, F) if props else np.zeros((F, 0, (1 << depth) // 64), np.uint64)
+    rng = np.random.default_rng(props)
+    ng = 64 if props == 16 else 13
+    pos = np.zeros(ng, dtype=np.uint64)
+    neg = np.zeros(ng, dtype=np.uint64)
+    for t in range(ng):  # guards over props 0..props+3 (some need props the labels do not carry)
+        for j in rng.choice(props + 4, size=int(rng.integers(0, 4)), replace=False):
+            if rng.integers(0, 2):
+                pos[t] |= np.uint64(1) << np.uint64(j)
+            else:
+                neg[t] |= np.uint64(1) << np.uint64(j)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction(CsrBoolMatrix(E, 1 << depth, off, idx))
+    eng.set_guards(pos, neg)
+    for frames in (1, F):  # single-frame and multi-frame kernels
+        eng.submit_grid(1 << depth, props, P[:frames], frames)
+        for f in range(frames):
+            labels = (ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[f]) if props
+                      else np.zeros(E, dtype=np.uint64))
+            want = ref.guard_admits(labels.reshape(E, -1)[:, 0], pos, neg)
+            assert np.array_equal(eng.get_admitted(f), want), (frames, f)
+    eng.close()
