@@ -299,11 +299,11 @@ def main():
     rows_local = r1 - r0
     alg_bytes = 8 * int(info.words) + 4 * (rows_local + 1) + F * (cells * props // 8 + rows_local * 4)
     achieved = alg_bytes / (label_ms / 1e3) / 1e9
-    traffic = ncu_traffic("label_batch_kernel")
+    traffic = ncu_traffic("label_batch64_kernel")
     sm_clk = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
     lop3 = float(info.words) * F * props  # one AND-OR per stored T word per prop per frame
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "peak_source": src, "kernel": "label_batch_kernel<32,u32,2,full>",
+                "traffic": traffic, "peak_source": src, "kernel": "label_batch64_kernel<u32,2,full>",
                 "alg_bytes_per_launch": alg_bytes, "kernel_ms": label_ms, "summary_kernel_ms": summary_ms,
                 "note": "algorithmic bytes = 8*W32 + 4*(E+1) + F*(cells*props/8 + E*4); traffic = dram read+write "
                         "bytes per launch from the committed ncu --set full capture (profiles/traffic.json). The "
@@ -341,8 +341,8 @@ def main():
                "kernel_p50_ms": k3, "roofline": {"bound": "hbm", "achieved": alg3 / (k3 / 1e3) / 1e9, "peak": hbm,
                                                 "unit": "GB/s", "frac": alg3 / (k3 / 1e3) / 1e9 / hbm,
                                                 "alg_bytes_per_launch": alg3,
-                                                "traffic": ncu_traffic("label_stream_kernel"),
-                                                "kernel": "label_stream_kernel<16,u16,smem,8,1024,in-place>"}}
+                                                "traffic": ncu_traffic("label_stream64_kernel"),
+                                                "kernel": "label_stream64_kernel<16,u16,smem,1024>"}}
 
     # ---- e2e through the public API with host buffers ------------------------
     e2e = None
