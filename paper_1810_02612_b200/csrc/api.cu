@@ -361,7 +361,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         const uint32_t nw64 = nw32 / 2;
         // 64-cell-word single-frame path (dev knob LTLG_STREAM64=0 selects the 32-cell copy for A/B runs)
         static const bool wide_ok = !getenv("LTLG_STREAM64") || atoi(getenv("LTLG_STREAM64")) != 0;
-        const bool wide = wide_ok && frames == 1 && props <= 32;
+        const bool wide = wide_ok && frames == 1;
         static const bool wide_b_ok = !getenv("LTLG_BATCH64") || atoi(getenv("LTLG_BATCH64")) != 0;
         const bool wide_b = wide_b_ok && frames > 1 && props <= 32;  // 64-cell-word multi-frame path
         CK(s.sf.reserve(wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32

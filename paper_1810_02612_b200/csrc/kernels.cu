@@ -86,15 +86,15 @@ size_t s_only_bytes(int props) { return props <= 32 ? 4 : 8; }
 __host__ __device__ __forceinline__ uint32_t split_x_offset(int fmt, uint32_t nw32) {
     return ((fmt == 16 ? 4u : 8u) * (nw32 + 1) + 15u) & ~15u;
 }
-// 64-cell-word split table: M[w64] as above, then (16-byte aligned) X[w64] =
+// 64-cell-word split table: M[w64] as above (FMT 64: 16 B {F lo, F hi,
+// ia | ib<<8 | partial<<16 | over<<17, 0}), then (16-byte aligned) X[w64] =
 // {Pa lo, Pa hi, Pb lo, Pb hi}.
+__host__ __device__ __forceinline__ uint32_t split64_m_bytes(int fmt) { return fmt == 16 ? 4u : fmt == 32 ? 8u : 16u; }
 __host__ __device__ __forceinline__ uint32_t split64_x_offset(int fmt, uint32_t nw64) {
-    return ((fmt == 16 ? 4u : 8u) * (nw64 + 1) + 15u) & ~15u;
+    return (split64_m_bytes(fmt) * (nw64 + 1) + 15u) & ~15u;
 }
 size_t split64_table_bytes(int props, uint32_t nw64) {
-    const int fmt = entry_format(props);
-    if (fmt == 64) return 0;
-    return split64_x_offset(fmt, nw64) + 16u * (nw64 + 1);
+    return split64_x_offset(entry_format(props), nw64) + 16u * (nw64 + 1);
 }
 size_t split_table_bytes(int props, uint32_t nw32) {
     const int fmt = entry_format(props);
@@ -277,13 +277,14 @@ __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict
 template <int FMT>
 __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restrict__ P64, int props, uint32_t nw64,
                                                         uint64_t cells, uint8_t* __restrict__ tab,
-                                                        uint32_t* __restrict__ s_only, uint32_t* __restrict__ task_ctr,
+                                                        void* __restrict__ s_only_g, uint32_t* __restrict__ task_ctr,
                                                         int nctr) {
-    static_assert(FMT != 64, "split tables hold <= 32 props");
+    using LW = typename Fmt<FMT>::LW;
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w < static_cast<uint32_t>(nctr)) task_ctr[w] = 0;  // the labeling launches that follow pull from 0
     if (w > nw64) return;
-    uint32_t s = 0, full = 0, ia = 0, ib = 0;
+    LW s = 0, full = 0;
+    uint32_t ia = 0, ib = 0;
     uint64_t pa = 0, pb = 0;
     int np = 0;
     const uint64_t lo = static_cast<uint64_t>(w) * 64;
@@ -292,8 +293,8 @@ __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restri
 #pragma unroll 4
         for (int j = 0; j < props; ++j) {
             const uint64_t x = P64[static_cast<uint64_t>(j) * nw64 + w] & valid;
-            s |= static_cast<uint32_t>(x != 0) << j;
-            full |= static_cast<uint32_t>(x == valid) << j;
+            s |= LW(x != 0) << j;
+            full |= LW(x == valid) << j;
             if (x != 0 && x != valid) {
                 if (np == 0) {
                     pa = x;
@@ -308,13 +309,17 @@ __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restri
     }
     const uint32_t over = np > 2 ? 1u : 0u, part = np > 0 ? 1u : 0u;
     if constexpr (FMT == 16)
-        reinterpret_cast<uint32_t*>(tab)[w] = (full << 16) | (16u + ia) | ((16u + ib) << 5) | (part << 10) | (over << 11);
+        reinterpret_cast<uint32_t*>(tab)[w] =
+            (static_cast<uint32_t>(full) << 16) | (16u + ia) | ((16u + ib) << 5) | (part << 10) | (over << 11);
+    else if constexpr (FMT == 32)
+        reinterpret_cast<uint2*>(tab)[w] = make_uint2(static_cast<uint32_t>(full), ia | (ib << 8) | (part << 16) | (over << 17));
     else
-        reinterpret_cast<uint2*>(tab)[w] = make_uint2(full, ia | (ib << 8) | (part << 16) | (over << 17));
+        reinterpret_cast<uint4*>(tab)[w] = make_uint4(static_cast<uint32_t>(full), static_cast<uint32_t>(full >> 32),
+                                                      ia | (ib << 8) | (part << 16) | (over << 17), 0u);
     reinterpret_cast<uint4*>(tab + split64_x_offset(FMT, nw64))[w] =
         make_uint4(static_cast<uint32_t>(pa), static_cast<uint32_t>(pa >> 32), static_cast<uint32_t>(pb),
                    static_cast<uint32_t>(pb >> 32));
-    s_only[w] = s;
+    static_cast<LW*>(s_only_g)[w] = s;
 }
 
 // Multi-frame summary over 64-cell words, thread per (word, frame), index
@@ -775,33 +780,40 @@ __global__ void __launch_bounds__(NT)
 // -- 41% fewer pairs per row than 32-cell words at 512^2 --
 // against the 64-cell split summary (summary64_kernel).  Same lane
 // ownership, in-place prefetch and row segmentation as label_stream_kernel.
-template <int FMT, typename SW, bool SMEM, int NT>
+// TABLOC: 0 = split table read through L1, 1 = all of it in shared memory,
+// 2 = M (every pair) in shared memory and X (partial-prop lanes only) through
+// L1 -- for grids whose full table exceeds shared memory.
+template <int FMT, typename SW, int TABLOC, int NT>
 __global__ void __launch_bounds__(NT)
     label_stream64_kernel(const uint8_t* __restrict__ t64, const uint64_t* __restrict__ task_byte,
                           const uint32_t* __restrict__ task_n, const uint32_t* __restrict__ task_row,
                           uint32_t task_begin, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
-                          const void* __restrict__ tab_g, uint32_t tab_bytes, const uint32_t* __restrict__ s_only,
+                          const void* __restrict__ tab_g, uint32_t tab_bytes, const void* __restrict__ s_only_g,
                           const uint64_t* __restrict__ P64, uint32_t nw64, SW* __restrict__ out) {
-    static_assert(FMT != 64, "split tables hold <= 32 props");
-    using LW = uint32_t;
+    constexpr bool SMEM = TABLOC != 0;   // M in shared memory
+    constexpr bool XSMEM = TABLOC == 1;  // X in shared memory
+    using LW = typename Fmt<FMT>::LW;
     constexpr int K = kStreamK;
     constexpr uint32_t CH = kStreamCH;
     constexpr int kShift = FMT == 16 ? 16 : 0;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     __shared__ uint64_t tab_bar;
     const int lane = threadIdx.x & 31;
+    const uint32_t xoff = split64_x_offset(FMT, nw64);
     const uint8_t* tab = static_cast<const uint8_t*>(tab_g);
+    const uint8_t* xg = static_cast<const uint8_t*>(tab_g) + xoff;  // X in global memory
     if constexpr (SMEM) {
-        stage_table(smem_raw, tab_g, tab_bytes, &tab_bar);
+        stage_table(smem_raw, tab_g, XSMEM ? tab_bytes : xoff, &tab_bar);
         tab = smem_raw;
     }
-    const uint32_t xoff = split64_x_offset(FMT, nw64);
-    StreamCtx<FMT, SW, SMEM> sc{tab, tab + xoff, SMEM ? smem_u32(tab) : 0u, SMEM ? smem_u32(tab) + xoff : 0u, s_only,
-                               reinterpret_cast<const uint32_t*>(P64), nw64, out, lane, (1u << lane) - 1u,
-                               ((1u << lane) - 1u) | (1u << lane)};
+    const LW* s_only = static_cast<const LW*>(s_only_g);
+    StreamCtx<FMT, SW, SMEM> sc{tab, XSMEM ? tab + xoff : xg, SMEM ? smem_u32(tab) : 0u,
+                               XSMEM ? smem_u32(tab) + xoff : 0u, s_only, reinterpret_cast<const uint32_t*>(P64), nw64,
+                               out, lane, (1u << lane) - 1u, ((1u << lane) - 1u) | (1u << lane)};
     const uint32_t* mtab16 = reinterpret_cast<const uint32_t*>(tab);
     const uint2* mtab32 = reinterpret_cast<const uint2*>(tab);
-    const uint4* xtab = reinterpret_cast<const uint4*>(tab + xoff);
+    const uint4* mtab64 = reinterpret_cast<const uint4*>(tab);
+    const uint4* xtab = reinterpret_cast<const uint4*>(XSMEM ? tab + xoff : xg);
     bool tab_ready = !SMEM;
 
     for (;;) {
@@ -878,45 +890,73 @@ __global__ void __launch_bounds__(NT)
             auto look = [&](int k, uint32_t& over) {
                 const uint32_t lo = mlo(k), hi = mhi(k), wh = wfield(k);
                 heads = mad_pow2(head_bit(wh), 1u << k, heads);
-                uint32_t mw, meta, f;
+                uint32_t meta, part;
+                LW f;
                 uint4 x = make_uint4(0u, 0u, 0u, 0u);
                 if constexpr (FMT == 16) {
-                    mw = SMEM ? lds32(sc.tab_s + (wh << 2)) : mtab16[wh & kWordMask];
+                    const uint32_t mw = SMEM ? lds32(sc.tab_s + (wh << 2)) : mtab16[wh & kWordMask];
                     meta = mw;
                     f = mw;
-                    if constexpr (SMEM) lds128_if(mw & (1u << 10), sc.x_s + (wh << 4), x);
-                    else if (mw & (1u << 10)) x = xtab[wh & kWordMask];
+                    part = mw & (1u << 10);
                     over |= mw & (1u << 11);
-                } else {
-                    const uint2 m2 = mtab32[wh & kWordMask];
+                } else if constexpr (FMT == 32) {
+                    const uint2 m2 = SMEM ? lds64(sc.tab_s + (wh << 3)) : mtab32[wh & kWordMask];
                     f = m2.x;
                     meta = m2.y;
-                    if (m2.y & 0x10000u) x = xtab[wh & kWordMask];
-                    over |= m2.y & 0x20000u;
+                    part = m2.y & 0x10000u;
+                    over |= (m2.y >> 1) & 0x10000u;
+                } else {
+                    uint4 m4;
+                    if constexpr (SMEM) {
+                        const uint32_t a = sc.tab_s + ((wh & kWordMask) << 4);
+                        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(m4.x), "=r"(m4.y), "=r"(m4.z), "=r"(m4.w) : "r"(a));
+                    } else {
+                        m4 = __ldg(mtab64 + (wh & kWordMask));
+                    }
+                    f = (static_cast<uint64_t>(m4.y) << 32) | m4.x;
+                    meta = m4.z;
+                    part = m4.z & 0x10000u;
+                    over |= (m4.z >> 1) & 0x10000u;
                 }
-                uint32_t vv = f;
-                if ((lo & x.x) | (hi & x.y)) vv |= __funnelshift_l(0u, 1u, meta);
-                if ((lo & x.z) | (hi & x.w)) vv |= __funnelshift_l(0u, 1u, meta >> (FMT == 16 ? 5 : 8));
+                if constexpr (XSMEM) {
+                    lds128_if(part, sc.x_s + ((wh & kWordMask) << 4), x);
+                } else {
+                    if (part) x = __ldg(xtab + (wh & kWordMask));
+                }
+                LW vv = f;  // FMT 16: F<<16; bits < 16 are index/flag garbage, shifted out at the store
+                if constexpr (FMT == 64) {
+                    if ((lo & x.x) | (hi & x.y)) vv |= LW(1) << (meta & 63);
+                    if ((lo & x.z) | (hi & x.w)) vv |= LW(1) << (meta >> 8 & 63);
+                } else {
+                    if ((lo & x.x) | (hi & x.y)) vv |= __funnelshift_l(0u, 1u, meta);
+                    if ((lo & x.z) | (hi & x.w)) vv |= __funnelshift_l(0u, 1u, meta >> (FMT == 16 ? 5 : 8));
+                }
                 v[k] = vv;
             };
             auto fix = [&](int k) {  // a word with >= 3 partial props: exact gather of the rest
                 const uint32_t w = wfield(k) & kWordMask;
-                uint32_t known, ov;
+                LW known;
+                uint32_t ov;
                 if constexpr (FMT == 16) {
                     const uint32_t mw = mtab16[w];
                     known = (mw >> 16) | (1u << ((mw & 31) - 16)) | (1u << ((mw >> 5 & 31) - 16));
                     ov = mw >> 11 & 1u;
-                } else {
+                } else if constexpr (FMT == 32) {
                     const uint2 mw = mtab32[w];
                     known = mw.x | (1u << (mw.y & 31)) | (1u << (mw.y >> 8 & 31));
                     ov = mw.y >> 17 & 1u;
+                } else {
+                    const uint4 mw = mtab64[w];
+                    known = ((static_cast<uint64_t>(mw.y) << 32) | mw.x) | (LW(1) << (mw.z & 63)) |
+                            (LW(1) << (mw.z >> 8 & 63));
+                    ov = mw.z >> 17 & 1u;
                 }
                 if (ov) {
                     const uint64_t m = (static_cast<uint64_t>(mhi(k)) << 32) | mlo(k);
-                    uint32_t rest = s_only[w] & ~known, hit = 0;
+                    LW rest = s_only[w] & ~known, hit = 0;
                     while (rest) {
-                        const int j = __ffs(rest) - 1;
-                        if (m & __ldg(P64 + static_cast<uint64_t>(j) * nw64 + w)) hit |= 1u << j;
+                        const int j = lowest_bit(rest);
+                        if (m & __ldg(P64 + static_cast<uint64_t>(j) * nw64 + w)) hit |= LW(1) << j;
                         rest &= rest - 1;
                     }
                     v[k] |= hit << kShift;
@@ -1344,12 +1384,11 @@ cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint
                              uint32_t* task_ctr, int nctr, cudaStream_t st) {
     const uint32_t nthreads = nw64 + 1 > static_cast<uint32_t>(nctr) ? nw64 + 1 : static_cast<uint32_t>(nctr);
     const unsigned grid = (nthreads + 255) / 256;
-    if (entry_format(props) == 16)
-        summary64_kernel<16><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab),
-                                                   static_cast<uint32_t*>(s_only), task_ctr, nctr);
-    else
-        summary64_kernel<32><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab),
-                                                   static_cast<uint32_t*>(s_only), task_ctr, nctr);
+    switch (entry_format(props)) {
+        case 16: summary64_kernel<16><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr); break;
+        case 32: summary64_kernel<32><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr); break;
+        default: summary64_kernel<64><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr); break;
+    }
     return cudaGetLastError();
 }
 
@@ -1446,18 +1485,23 @@ static cudaError_t launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
     return launch_stream_v<FMT, SW, false, kStreamK, 256, true>(a, st);
 }
 
-bool stream64_table_in_smem(int props, uint32_t nw64) {
+// Where the 64-cell single-frame kernel keeps its split table (TABLOC).
+int stream64_table_loc(int props, uint32_t nw64) {
     static const int want = env_int("LTLG_STREAM_TABLE", -1);
-    if (want == 0 || entry_format(props) == 64) return false;
-    return split64_table_bytes(props, nw64) <= kMaxSmemTable;
+    if (want == 0) return 0;
+    const int fmt = entry_format(props);
+    if (split64_table_bytes(props, nw64) <= kMaxSmemTable) return 1;
+    if (split64_x_offset(fmt, nw64) <= kMaxSmemTable) return 2;
+    return 0;
 }
 
-template <int FMT, typename SW, bool SMEM, int NT>
+template <int FMT, typename SW, int TABLOC, int NT>
 static cudaError_t launch_stream64_v(const LaunchArgs& a, cudaStream_t st) {
     const uint32_t tab_bytes = static_cast<uint32_t>(split64_table_bytes(a.props, a.nw64));
-    auto kern = label_stream64_kernel<FMT, SW, SMEM, NT>;
+    const uint32_t smem = TABLOC == 1 ? tab_bytes : TABLOC == 2 ? split64_x_offset(FMT, a.nw64) : 0u;
+    auto kern = label_stream64_kernel<FMT, SW, TABLOC, NT>;
     const uint64_t* P64 = reinterpret_cast<const uint64_t*>(a.P32);
-    if constexpr (SMEM) {
+    if constexpr (TABLOC != 0) {
         static uint64_t attr_set = 0;  // per device
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1465,10 +1509,9 @@ static cudaError_t launch_stream64_v(const LaunchArgs& a, cudaStream_t st) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaxSmemTable));
             attr_set |= 1ull << dev;
         }
-        if (tab_bytes % 16u || tab_bytes > kMaxSmemTable) return cudaErrorInvalidValue;
-        kern<<<sm_count(), NT, tab_bytes, st>>>(a.t64, a.task_byte64, a.task_n64, a.task_row, a.task_begin, a.ntasks,
-                                                a.task_ctr, a.sf, tab_bytes, static_cast<const uint32_t*>(a.s_only), P64,
-                                                a.nw64, static_cast<SW*>(a.out));
+        if (smem % 16u || smem > kMaxSmemTable) return cudaErrorInvalidValue;
+        kern<<<sm_count(), NT, smem, st>>>(a.t64, a.task_byte64, a.task_n64, a.task_row, a.task_begin, a.ntasks,
+                                           a.task_ctr, a.sf, tab_bytes, a.s_only, P64, a.nw64, static_cast<SW*>(a.out));
     } else {
         static int per_sm = 0;
         if (!per_sm) {
@@ -1476,20 +1519,22 @@ static cudaError_t launch_stream64_v(const LaunchArgs& a, cudaStream_t st) {
             if (per_sm <= 0) per_sm = 4;
         }
         kern<<<sm_count() * per_sm, NT, 0, st>>>(a.t64, a.task_byte64, a.task_n64, a.task_row, a.task_begin, a.ntasks,
-                                                 a.task_ctr, a.sf, tab_bytes, static_cast<const uint32_t*>(a.s_only),
-                                                 P64, a.nw64, static_cast<SW*>(a.out));
+                                                 a.task_ctr, a.sf, tab_bytes, a.s_only, P64, a.nw64,
+                                                 static_cast<SW*>(a.out));
     }
     return cudaSuccess;
 }
 
 template <int FMT, typename SW>
 static cudaError_t launch_stream64_t(const LaunchArgs& a, cudaStream_t st) {
-    if (stream64_table_in_smem(a.props, a.nw64)) return launch_stream64_v<FMT, SW, true, 1024>(a, st);
-    return launch_stream64_v<FMT, SW, false, 256>(a, st);
+    constexpr int NT = FMT == 64 ? 512 : 1024;  // u64 labels: 16 warps per SM keep every value in registers
+    switch (stream64_table_loc(a.props, a.nw64)) {
+        case 1: return launch_stream64_v<FMT, SW, 1, NT>(a, st);
+        case 2: return launch_stream64_v<FMT, SW, 2, NT>(a, st);
+        default: return launch_stream64_v<FMT, SW, 0, 256>(a, st);
+    }
 }
 
-// F frames over 64-cell words (<= 32 props): the batch kernel's structure on
-// the SoA (mask64, word64) copy and the summary_b64_kernel entries.
 struct E32 {
     uint32_t f, meta, pa_lo, pa_hi, pb_lo, pb_hi, s, pad;
 };
@@ -1660,7 +1705,8 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
         switch (a.label_bytes) {
             case 1: e = launch_stream64_t<16, uint8_t>(a, st); break;
             case 2: e = launch_stream64_t<16, uint16_t>(a, st); break;
-            default: e = launch_stream64_t<32, uint32_t>(a, st); break;
+            case 4: e = launch_stream64_t<32, uint32_t>(a, st); break;
+            default: e = launch_stream64_t<64, uint64_t>(a, st); break;
         }
     } else if (a.frames == 1) {
         switch (a.label_bytes) {

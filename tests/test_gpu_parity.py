@@ -538,3 +538,25 @@ def test_guard_consumer_vs_reference(props):
             want = ref.guard_admits(labels.reshape(E, -1)[:, 0], pos, neg)
             assert np.array_equal(eng.get_admitted(f), want), (frames, f)
     eng.close()
+
+
+def test_config5_dense_grid_slice():
+    # BASELINE config 5 (1024^2 grid, 64 props) on a 300k-row slice of the 8M-edge
+    # abstraction: the 64-prop entry format, the L1 (not shared-memory) summary path
+    # of the single-frame kernel and the 64-prop multi-frame kernel.
+    c = CONFIGS[5]
+    depth, props, E = c["depth"], c["props"], 300_000
+    prm = SyntheticPRM(seed=1, depth=depth)
+    t = prm.words(0, E)
+    off, idx = prm.csr(0, E)
+    P = props_words(1, depth, props, 0, 3)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
+    eng.submit_grid(1 << depth, props, P[0], 1)
+    want0 = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[0])
+    assert eng.get_labels(0) == LabelMatrix(E, props, want0)
+    eng.submit_grid(1 << depth, props, P, 3)
+    for f in range(3):
+        want = want0 if f == 0 else ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[f])
+        assert eng.get_labels(f) == LabelMatrix(E, props, want)
+    eng.close()
