@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <thread>
@@ -487,6 +488,14 @@ void build_stream_layout(const WordCsr& t, uint64_t row_begin, uint64_t row_end,
     for (size_t k = 0; k < nt; ++k) {
         const uint64_t n = out->task_pair_stream[k + 1] - out->task_pair_stream[k];
         dst_off[k + 1] = dst_off[k] + n + (n & 1);
+    }
+    // The 32-cell single-frame copy is only streamed by the A/B knob
+    // LTLG_STREAM64=0 (every prop count runs the 64-cell copy by default).
+    const char* knob = std::getenv("LTLG_STREAM64");
+    if (!knob || std::atoi(knob) != 0) {
+        out->pairs_stream.assign(kPairPad, Pair{0, sentinel_word | kHead});
+        out->task_pair_stream = dst_off;
+        return;
     }
     out->pairs_stream.assign(dst_off[nt] + kPairPad, Pair{0, sentinel_word | kHead});
     parallel_chunks(nt, 64, [&](uint64_t b, uint64_t e, int) {

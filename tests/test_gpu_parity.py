@@ -560,3 +560,20 @@ def test_config5_dense_grid_slice():
         want = want0 if f == 0 else ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[f])
         assert eng.get_labels(f) == LabelMatrix(E, props, want)
     eng.close()
+
+
+@pytest.mark.parametrize("knobs", [
+    {"LTLG_STREAM64": "0", "LTLG_BATCH64": "0"},                            # 32-cell kernels
+    {"LTLG_STREAM64": "0", "LTLG_STREAM_CFG": "2"},                         # double-buffered 32-cell
+    {"LTLG_STREAM64": "0", "LTLG_STREAM_CFG": "4"},                         # TMA-ring 32-cell
+    {"LTLG_STREAM_TABLE": "0"},                                             # summary through L1
+])
+def test_ab_variants_parity(knobs):
+    # the A/B kernel variants (env knobs, read once per process) stay bit-exact
+    import subprocess
+    import sys
+
+    env = dict(os.environ, **knobs)
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(GOLDEN), "..", "tools", "ab_parity.py")],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
