@@ -356,11 +356,11 @@ def main():
         t0 = time.perf_counter()
         for _ in range(Ke):
             if world > 1:
-                if rank == 0:
-                    P_dev.copy_(P_host, non_blocking=True)
-                with torch.cuda.stream(stream):
+                with torch.cuda.stream(stream):  # H2D on rank 0, NCCL broadcast, labelling: one stream
+                    if rank == 0:
+                        P_dev.copy_(P_host, non_blocking=True)
                     dist.broadcast(P_dev, src=0)
-                eng.submit_grid_device(cells, props, P_dev.data_ptr(), F)
+                eng.submit_grid_device(cells, props, P_dev.data_ptr(), F, readback=True)
             else:
                 eng.submit_grid(cells, props, P_host, F)
             eng.get_labels_packed(out_host)

@@ -125,6 +125,14 @@ ltlg_status ltlg_submit_grid(ltlg_ctx* ctx, uint64_t cells, int num_props,
 ltlg_status ltlg_submit_grid_device(ltlg_ctx* ctx, uint64_t cells, int num_props,
                                     const uint64_t* device_column_words, int frames);
 
+/* Same as ltlg_submit_grid_device; readback != 0 declares that the labels
+ * will be copied to the host (ltlg_get_labels_packed), so a multi-frame
+ * submit is labelled block by block (ltlg_options.readback_chunks) and the
+ * copy of block c overlaps the labelling of later blocks -- what
+ * ltlg_submit_grid does for host P. */
+ltlg_status ltlg_submit_grid_device_ex(ltlg_ctx* ctx, uint64_t cells, int num_props,
+                                       const uint64_t* device_column_words, int frames, int readback);
+
 /* World-frame perception grid -> vehicle-frame P resample, then label
  * (north_star subsystem 2; transform convention of translate_system,
  * abstraction.cpp:396-404).  Grids are k=2 z-order grids; world_words is

@@ -25,6 +25,7 @@ EXPORTS = [
     "ltlg_stream", "ltlg_stage_times", "ltlg_validate_csr", "ltlg_label_all",
     "ltlg_submit_grid_files", "ltlg_save_labels", "ltlg_read_csb1_words", "ltlg_read_zobv",
     "ltlg_rasterize_boxes", "ltlg_submit_boxes", "ltlg_set_guards", "ltlg_get_admitted", "ltlg_device_admitted",
+    "ltlg_submit_grid_device_ex",
 ]
 
 
@@ -84,6 +85,7 @@ def lib() -> C.CDLL:
         "ltlg_load_abstraction_words": ([ctxp, u64, u64, vp, vp, vp], i32),
         "ltlg_submit_grid": ([ctxp, u64, i32, vp, i32], i32),
         "ltlg_submit_grid_device": ([ctxp, u64, i32, vp, i32], i32),
+        "ltlg_submit_grid_device_ex": ([ctxp, u64, i32, vp, i32, i32], i32),
         "ltlg_submit_world_grid": ([ctxp, C.POINTER(Grid2), C.POINTER(Grid2), i32, vp, i32, vp, i32, i32], i32),
         "ltlg_wait": ([ctxp], i32),
         "ltlg_get_labels": ([ctxp, i32, vp], i32),

@@ -439,7 +439,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
 }
 
 ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* words, int frames,
-                   bool on_device) {
+                   bool on_device, bool readback) {
     ltlg_status st = check_grid(ctx, cells, num_props, frames);
     if (st != LTLG_OK) return st;
     ctx->cells = cells;
@@ -471,7 +471,7 @@ ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t*
             cudaSetDevice(ctx->shards[i].device);
             cudaEventRecord(ctx->shards[i].ev[0], ctx->shards[i].stream);
         }
-    return run_label(ctx, !on_device);
+    return run_label(ctx, readback);
 }
 
 ltlg_status sync_all(ltlg_ctx* ctx) {
@@ -636,12 +636,17 @@ ltlg_status ltlg_load_abstraction_words(ltlg_ctx* ctx, uint64_t rows, uint64_t c
 }
 
 ltlg_status ltlg_submit_grid(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* column_words, int frames) {
-    return submit(ctx, cells, num_props, column_words, frames, false);
+    return submit(ctx, cells, num_props, column_words, frames, false, true);
 }
 
 ltlg_status ltlg_submit_grid_device(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* dev_words,
                                     int frames) {
-    return submit(ctx, cells, num_props, dev_words, frames, true);
+    return submit(ctx, cells, num_props, dev_words, frames, true, false);
+}
+
+ltlg_status ltlg_submit_grid_device_ex(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* dev_words,
+                                       int frames, int readback) {
+    return submit(ctx, cells, num_props, dev_words, frames, true, readback != 0);
 }
 
 ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, const ltlg_grid2* world, int num_props,
@@ -719,7 +724,7 @@ ltlg_status ltlg_submit_grid_files(ltlg_ctx* ctx, const char* const* paths, int 
         if (!read_zobv(paths[i], ctx->cols, staging + i * nw, &err))
             return set_err(ctx, static_cast<ltlg_status>(err.code), err.msg);
     }
-    ltlg_status st = submit(ctx, ctx->cols, num_props, staging, frames, false);
+    ltlg_status st = submit(ctx, ctx->cols, num_props, staging, frames, false, true);
     if (st == LTLG_OK && n) st = sync_all(ctx);  // the staging buffer is freed on return
     return st;
 }

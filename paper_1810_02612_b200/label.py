@@ -417,8 +417,12 @@ class LabelEngine:
         """LBM1 file of one frame's labels (LabelMatrix::save, label.cpp:300-309)."""
         self._ck(self._L.ltlg_save_labels(self._h, frame, os.fsencode(path)))
 
-    def submit_grid_device(self, cells: int, num_props: int, device_words, frames: int = 1) -> None:
-        self._ck(self._L.ltlg_submit_grid_device(self._h, cells, num_props, _ptr(device_words), frames))
+    def submit_grid_device(self, cells: int, num_props: int, device_words, frames: int = 1,
+                           readback: bool = False) -> None:
+        """P already in HBM; readback=True declares a following host read of
+        the labels (block-wise labelling overlapped with the copy)."""
+        self._ck(self._L.ltlg_submit_grid_device_ex(self._h, cells, num_props, _ptr(device_words), frames,
+                                                    1 if readback else 0))
 
     def submit_world_grid(self, vehicle, world, num_props: int, world_words, poses, outside: int = 0,
                           words_on_device: bool = False) -> None:

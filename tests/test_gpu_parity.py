@@ -332,6 +332,15 @@ def test_chunked_readback(devices, chunks):
     want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[4])
     assert np.array_equal(eng.get_labels_packed()[:, 0].astype(np.uint64), want)
     assert eng.get_labels(0) == LabelMatrix(E, props, want)
+    # device-resident P declared for read-back (ltlg_submit_grid_device_ex)
+    import torch
+
+    Pd = torch.from_numpy(P.view(np.int64)).cuda()
+    eng.submit_grid_device(1 << depth, props, Pd.data_ptr(), F, readback=True)
+    packed = eng.get_labels_packed()
+    for f in range(F):
+        want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[f])
+        assert np.array_equal(packed[:, f].astype(np.uint64), want), f
     eng.close()
 
 
