@@ -89,12 +89,20 @@ __host__ __device__ __forceinline__ uint32_t split_x_offset(int fmt, uint32_t nw
 // 64-cell-word split table: M[w64] as above (FMT 64: 16 B {F lo, F hi,
 // ia | ib<<8 | partial<<16 | over<<17, 0}), then (16-byte aligned) X[w64] =
 // {Pa lo, Pa hi, Pb lo, Pb hi}.
-__host__ __device__ __forceinline__ uint32_t split64_m_bytes(int fmt) { return fmt == 16 ? 4u : fmt == 32 ? 8u : 16u; }
+// FMT 64 (33..64 props, u64 labels) keeps M as two arrays, F[w] (u64) then
+// meta[w] (u32: ia | ib<<6 | ic<<12 | id<<18 | partial<<24 | over<<25), and
+// X[w] = the P words of the four lowest partial props (32 B): with 64
+// props a 64-cell word has >= 3 partial props 1.7% of the time at 1024^2,
+// >= 5 only 0.02%.  12 B of M per word fit 1024^2 (196 KB) in shared memory.
+__host__ __device__ __forceinline__ uint32_t split64_m_bytes(int fmt) { return fmt == 16 ? 4u : fmt == 32 ? 8u : 12u; }
 __host__ __device__ __forceinline__ uint32_t split64_x_offset(int fmt, uint32_t nw64) {
     return (split64_m_bytes(fmt) * (nw64 + 1) + 15u) & ~15u;
 }
+__host__ __device__ __forceinline__ uint32_t split64_meta_offset(uint32_t nw64) { return 8u * (nw64 + 1); }
+__host__ __device__ __forceinline__ uint32_t split64_x_bytes(int fmt) { return fmt == 64 ? 32u : 16u; }
 size_t split64_table_bytes(int props, uint32_t nw64) {
-    return split64_x_offset(entry_format(props), nw64) + 16u * (nw64 + 1);
+    const int fmt = entry_format(props);
+    return split64_x_offset(fmt, nw64) + split64_x_bytes(fmt) * (nw64 + 1);
 }
 size_t split_table_bytes(int props, uint32_t nw32) {
     const int fmt = entry_format(props);
@@ -284,8 +292,8 @@ __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restri
     if (w < static_cast<uint32_t>(nctr)) task_ctr[w] = 0;  // the labeling launches that follow pull from 0
     if (w > nw64) return;
     LW s = 0, full = 0;
-    uint32_t ia = 0, ib = 0;
-    uint64_t pa = 0, pb = 0;
+    uint32_t ia = 0, ib = 0, ic = 0, id = 0;
+    uint64_t pa = 0, pb = 0, pc = 0, pd = 0;
     int np = 0;
     const uint64_t lo = static_cast<uint64_t>(w) * 64;
     if (w < nw64 && lo < cells) {
@@ -302,23 +310,35 @@ __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restri
                 } else if (np == 1) {
                     pb = x;
                     ib = static_cast<uint32_t>(j);
+                } else if (np == 2) {
+                    pc = x;
+                    ic = static_cast<uint32_t>(j);
+                } else if (np == 3) {
+                    pd = x;
+                    id = static_cast<uint32_t>(j);
                 }
                 ++np;
             }
         }
     }
-    const uint32_t over = np > 2 ? 1u : 0u, part = np > 0 ? 1u : 0u;
+    const uint32_t over = np > (FMT == 64 ? 4 : 2) ? 1u : 0u, part = np > 0 ? 1u : 0u;
     if constexpr (FMT == 16)
         reinterpret_cast<uint32_t*>(tab)[w] =
             (static_cast<uint32_t>(full) << 16) | (16u + ia) | ((16u + ib) << 5) | (part << 10) | (over << 11);
     else if constexpr (FMT == 32)
         reinterpret_cast<uint2*>(tab)[w] = make_uint2(static_cast<uint32_t>(full), ia | (ib << 8) | (part << 16) | (over << 17));
-    else
-        reinterpret_cast<uint4*>(tab)[w] = make_uint4(static_cast<uint32_t>(full), static_cast<uint32_t>(full >> 32),
-                                                      ia | (ib << 8) | (part << 16) | (over << 17), 0u);
-    reinterpret_cast<uint4*>(tab + split64_x_offset(FMT, nw64))[w] =
-        make_uint4(static_cast<uint32_t>(pa), static_cast<uint32_t>(pa >> 32), static_cast<uint32_t>(pb),
-                   static_cast<uint32_t>(pb >> 32));
+    else {
+        reinterpret_cast<uint64_t*>(tab)[w] = static_cast<uint64_t>(full);
+        reinterpret_cast<uint32_t*>(tab + split64_meta_offset(nw64))[w] =
+            ia | (ib << 6) | (ic << 12) | (id << 18) | (part << 24) | (over << 25);
+    }
+    uint4* x = reinterpret_cast<uint4*>(tab + split64_x_offset(FMT, nw64));
+    const uint32_t xs = split64_x_bytes(FMT) / 16;
+    x[xs * w] = make_uint4(static_cast<uint32_t>(pa), static_cast<uint32_t>(pa >> 32), static_cast<uint32_t>(pb),
+                           static_cast<uint32_t>(pb >> 32));
+    if (xs == 2)
+        x[xs * w + 1] = make_uint4(static_cast<uint32_t>(pc), static_cast<uint32_t>(pc >> 32), static_cast<uint32_t>(pd),
+                                   static_cast<uint32_t>(pd >> 32));
     static_cast<LW*>(s_only_g)[w] = s;
 }
 
@@ -812,7 +832,6 @@ __global__ void __launch_bounds__(NT)
                                out, lane, (1u << lane) - 1u, ((1u << lane) - 1u) | (1u << lane)};
     const uint32_t* mtab16 = reinterpret_cast<const uint32_t*>(tab);
     const uint2* mtab32 = reinterpret_cast<const uint2*>(tab);
-    const uint4* mtab64 = reinterpret_cast<const uint4*>(tab);
     const uint4* xtab = reinterpret_cast<const uint4*>(XSMEM ? tab + xoff : xg);
     bool tab_ready = !SMEM;
 
@@ -906,19 +925,29 @@ __global__ void __launch_bounds__(NT)
                     part = m2.y & 0x10000u;
                     over |= (m2.y >> 1) & 0x10000u;
                 } else {
-                    uint4 m4;
+                    const uint32_t wi = wh & kWordMask;
                     if constexpr (SMEM) {
-                        const uint32_t a = sc.tab_s + ((wh & kWordMask) << 4);
-                        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(m4.x), "=r"(m4.y), "=r"(m4.z), "=r"(m4.w) : "r"(a));
+                        const uint2 f2 = lds64(sc.tab_s + (wi << 3));
+                        f = (static_cast<uint64_t>(f2.y) << 32) | f2.x;
+                        meta = lds32(sc.tab_s + split64_meta_offset(nw64) + (wi << 2));
                     } else {
-                        m4 = __ldg(mtab64 + (wh & kWordMask));
+                        f = __ldg(reinterpret_cast<const uint64_t*>(tab) + wi);
+                        meta = __ldg(reinterpret_cast<const uint32_t*>(tab + split64_meta_offset(nw64)) + wi);
                     }
-                    f = (static_cast<uint64_t>(m4.y) << 32) | m4.x;
-                    meta = m4.z;
-                    part = m4.z & 0x10000u;
-                    over |= (m4.z >> 1) & 0x10000u;
+                    part = meta & (1u << 24);
+                    over |= (meta >> 9) & 0x10000u;  // bit 25 -> the shared over flag bit 16
                 }
-                if constexpr (XSMEM) {
+                uint4 x2 = make_uint4(0u, 0u, 0u, 0u);  // FMT 64: partial props c, d
+                if constexpr (FMT == 64) {
+                    const uint32_t wi = wh & kWordMask;
+                    if constexpr (XSMEM) {
+                        lds128_if(part, sc.x_s + (wi << 5), x);
+                        lds128_if(part, sc.x_s + (wi << 5) + 16, x2);
+                    } else if (part) {
+                        x = __ldg(xtab + 2 * wi);
+                        x2 = __ldg(xtab + 2 * wi + 1);
+                    }
+                } else if constexpr (XSMEM) {
                     lds128_if(part, sc.x_s + ((wh & kWordMask) << 4), x);
                 } else {
                     if (part) x = __ldg(xtab + (wh & kWordMask));
@@ -926,7 +955,9 @@ __global__ void __launch_bounds__(NT)
                 LW vv = f;  // FMT 16: F<<16; bits < 16 are index/flag garbage, shifted out at the store
                 if constexpr (FMT == 64) {
                     if ((lo & x.x) | (hi & x.y)) vv |= LW(1) << (meta & 63);
-                    if ((lo & x.z) | (hi & x.w)) vv |= LW(1) << (meta >> 8 & 63);
+                    if ((lo & x.z) | (hi & x.w)) vv |= LW(1) << (meta >> 6 & 63);
+                    if ((lo & x2.x) | (hi & x2.y)) vv |= LW(1) << (meta >> 12 & 63);
+                    if ((lo & x2.z) | (hi & x2.w)) vv |= LW(1) << (meta >> 18 & 63);
                 } else {
                     if ((lo & x.x) | (hi & x.y)) vv |= __funnelshift_l(0u, 1u, meta);
                     if ((lo & x.z) | (hi & x.w)) vv |= __funnelshift_l(0u, 1u, meta >> (FMT == 16 ? 5 : 8));
@@ -946,10 +977,10 @@ __global__ void __launch_bounds__(NT)
                     known = mw.x | (1u << (mw.y & 31)) | (1u << (mw.y >> 8 & 31));
                     ov = mw.y >> 17 & 1u;
                 } else {
-                    const uint4 mw = mtab64[w];
-                    known = ((static_cast<uint64_t>(mw.y) << 32) | mw.x) | (LW(1) << (mw.z & 63)) |
-                            (LW(1) << (mw.z >> 8 & 63));
-                    ov = mw.z >> 17 & 1u;
+                    const uint32_t mt = reinterpret_cast<const uint32_t*>(tab + split64_meta_offset(nw64))[w];
+                    known = reinterpret_cast<const uint64_t*>(tab)[w] | (LW(1) << (mt & 63)) | (LW(1) << (mt >> 6 & 63)) |
+                            (LW(1) << (mt >> 12 & 63)) | (LW(1) << (mt >> 18 & 63));
+                    ov = mt >> 25 & 1u;
                 }
                 if (ov) {
                     const uint64_t m = (static_cast<uint64_t>(mhi(k)) << 32) | mlo(k);
