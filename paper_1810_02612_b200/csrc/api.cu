@@ -339,6 +339,53 @@ ltlg_status run_guards(ltlg_ctx* ctx, Shard& s) {
     return LTLG_OK;
 }
 
+constexpr int kSmallFrames = 12;  // sweep_frames: per-frame single-frame launches win up to ~12 frames
+
+// Multi-frame submit of few frames: per frame, the 64-cell summary + one
+// single-frame launch writing labels[row * frames + f].
+ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
+    const int props = ctx->props, frames = ctx->frames;
+    CK(s.sf.reserve(split64_table_bytes(props, nw64)), "allocate summary");
+    CK(s.ctr.reserve(64 * kCtrStride * sizeof(uint32_t)), "allocate task counters");
+    CK(s.s_only.reserve(static_cast<size_t>(nw64 + 1) * s_only_bytes(props)), "allocate summary");
+    const bool prof = ctx->opts.profile != 0;
+    if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
+    const size_t pw = static_cast<size_t>(props) * nw64;  // u64 words of one frame's P
+    for (int f = 0; f < frames; ++f) {
+        CK(launch_summary64(s.Pdev() + f * pw, props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr, s.ctr.ptr,
+                            static_cast<int>(kCtrStride), s.stream),
+           "summary kernel");
+        if (prof && f == 0) CK(cudaEventRecord(s.ev[2], s.stream), "event");
+        LaunchArgs a{};
+        a.sf = s.sf.ptr;
+        a.P32 = reinterpret_cast<const uint32_t*>(s.Pdev() + f * pw);
+        a.nw32 = 2 * nw64;
+        a.props = props;
+        a.frames = 1;
+        a.out = s.labels.ptr + static_cast<size_t>(f) * static_cast<size_t>(ctx->label_bytes);
+        a.ostride = static_cast<uint32_t>(frames);
+        a.label_bytes = ctx->label_bytes;
+        a.s_only = s.s_only.ptr;
+        a.t64 = s.t64.ptr;
+        a.task_byte64 = s.tbyte64.ptr;
+        a.task_n64 = s.tn64.ptr;
+        a.nw64 = nw64;
+        a.task_row = s.trow_s.ptr;
+        a.task_begin = 0;
+        a.ntasks = s.block_task_s.back();
+        a.task_ctr = s.ctr.ptr;
+        CK(launch_label(a, s.stream), "label kernel");
+    }
+    s.blocks_last = 1;
+    if (!ctx->guard_pos.empty()) {
+        const ltlg_status gst = run_guards(ctx, s);
+        if (gst != LTLG_OK) return gst;
+    }
+    if (prof) CK(cudaEventRecord(s.ev[3], s.stream), "event");
+    s.have_times = prof;
+    return LTLG_OK;
+}
+
 // split: one launch per read-back block (submits whose labels are expected
 // to go back to the host: host-memory P); otherwise one launch.
 ltlg_status run_label(ltlg_ctx* ctx, bool split) {
@@ -362,6 +409,15 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // 64-cell-word single-frame path (dev knob LTLG_STREAM64=0 selects the 32-cell copy for A/B runs)
         static const bool wide_ok = !getenv("LTLG_STREAM64") || atoi(getenv("LTLG_STREAM64")) != 0;
         const bool wide = wide_ok && frames == 1;
+        // Few frames: the frame-per-lane multi-frame kernel would leave most
+        // lanes idle (its cost is ~flat for frames <= 32), so label frame by
+        // frame with the single-frame kernel, each launch writing one column
+        // of the edge-major labels.
+        if (wide_ok && frames > 1 && frames <= kSmallFrames) {
+            const ltlg_status fst = run_label_per_frame(ctx, s, nw64);
+            if (fst != LTLG_OK) return fst;
+            continue;
+        }
         static const bool wide_b_ok = !getenv("LTLG_BATCH64") || atoi(getenv("LTLG_BATCH64")) != 0;
         const bool wide_b = wide_b_ok && frames > 1 && props <= 32;  // 64-cell-word multi-frame path
         CK(s.sf.reserve(wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32

@@ -487,7 +487,8 @@ struct StreamCtx {
     const LW* s_only;
     const uint32_t* P32;
     uint32_t nw32;
-    SW* out;
+    SW* out;       // label of row r at out[r * ostride] (ostride = frames of the
+    uint32_t ostride;  // submit: one frame of an edge-major multi-frame buffer)
     int lane;
     uint32_t lt, le;
 };
@@ -534,7 +535,7 @@ __device__ __forceinline__ void segment_chunk(const StreamCtx<FMT, SW, SMEM>& sc
         if (lane == 0) excl = rs.carry;
         if (heads) {
             const int32_t row = rs.open_row + hb;  // the row open before this lane's head
-            if (row >= rs.r0 && row < rs.r1) out[row] = static_cast<SW>((excl | pre) >> kShift);
+            if (row >= rs.r0 && row < rs.r1) out[static_cast<uint64_t>(row) * sc.ostride] = static_cast<SW>((excl | pre) >> kShift);
         }
         rs.carry = shfl_idx(x, 31);
         rs.open_row += __popc(hmask_all);
@@ -557,7 +558,7 @@ __device__ __forceinline__ void segment_chunk(const StreamCtx<FMT, SW, SMEM>& sc
             if (heads >> k & 1u) {
                 if (seen) {
                     const int32_t row = rs.open_row + hb + seen;
-                    if (row < rs.r1) out[row] = static_cast<SW>(cur_or >> kShift);
+                    if (row < rs.r1) out[static_cast<uint64_t>(row) * sc.ostride] = static_cast<SW>(cur_or >> kShift);
                 } else {
                     pre = cur_or;
                 }
@@ -580,7 +581,7 @@ __device__ __forceinline__ void segment_chunk(const StreamCtx<FMT, SW, SMEM>& sc
         if (lane == 0) excl = rs.carry;
         if (nh) {
             const int32_t row = rs.open_row + hb;  // the row open before this lane's first head
-            if (row >= rs.r0 && row < rs.r1) out[row] = static_cast<SW>((excl | pre) >> kShift);
+            if (row >= rs.r0 && row < rs.r1) out[static_cast<uint64_t>(row) * sc.ostride] = static_cast<SW>((excl | pre) >> kShift);
         }
         rs.carry = shfl_idx(x, 31);
         rs.open_row += tot;
@@ -692,7 +693,8 @@ template <int FMT, typename SW, bool SMEM>
 __device__ __forceinline__ void stream_close_task(const StreamCtx<FMT, SW, SMEM>& sc,
                                                   const RowState<typename Fmt<FMT>::LW>& rs) {
     if (sc.lane == 0 && rs.open_row >= rs.r0 && rs.open_row < rs.r1)
-        sc.out[rs.open_row] = static_cast<SW>(rs.carry >> StreamCtx<FMT, SW, SMEM>::kShift);
+        sc.out[static_cast<uint64_t>(rs.open_row) * sc.ostride] =
+            static_cast<SW>(rs.carry >> StreamCtx<FMT, SW, SMEM>::kShift);
 }
 
 // Copies the split table into shared memory (thread 0 issues, all wait later).
@@ -716,7 +718,7 @@ __global__ void __launch_bounds__(NT)
                         const uint32_t* __restrict__ task_row, uint32_t task_begin, uint32_t ntasks,
                         uint32_t* __restrict__ task_ctr, const void* __restrict__ tab_g, uint32_t tab_bytes,
                         const void* __restrict__ s_only_g, const uint32_t* __restrict__ P32, uint32_t nw32,
-                        SW* __restrict__ out) {
+                        SW* __restrict__ out, uint32_t ostride) {
     using LW = typename Fmt<FMT>::LW;
     static_assert(!(SMEM && FMT == 64), "the 64-prop entry table is read through L1");
     static_assert(K == kStreamK, "the HBM chunk layout is built for kStreamK pairs per lane");
@@ -731,7 +733,7 @@ __global__ void __launch_bounds__(NT)
     }
     StreamCtx<FMT, SW, SMEM> sc{tab, tab + split_x_offset(FMT, nw32), SMEM ? smem_u32(tab) : 0u,
                                SMEM ? smem_u32(tab) + split_x_offset(FMT, nw32) : 0u, static_cast<const LW*>(s_only_g),
-                               P32, nw32, out, lane, (1u << lane) - 1u, ((1u << lane) - 1u) | (1u << lane)};
+                               P32, nw32, out, ostride, lane, (1u << lane) - 1u, ((1u << lane) - 1u) | (1u << lane)};
     bool tab_ready = !SMEM;
 
     for (;;) {
@@ -809,7 +811,7 @@ __global__ void __launch_bounds__(NT)
                           const uint32_t* __restrict__ task_n, const uint32_t* __restrict__ task_row,
                           uint32_t task_begin, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
                           const void* __restrict__ tab_g, uint32_t tab_bytes, const void* __restrict__ s_only_g,
-                          const uint64_t* __restrict__ P64, uint32_t nw64, SW* __restrict__ out) {
+                          const uint64_t* __restrict__ P64, uint32_t nw64, SW* __restrict__ out, uint32_t ostride) {
     constexpr bool SMEM = TABLOC != 0;   // M in shared memory
     constexpr bool XSMEM = TABLOC == 1;  // X in shared memory
     using LW = typename Fmt<FMT>::LW;
@@ -829,7 +831,7 @@ __global__ void __launch_bounds__(NT)
     const LW* s_only = static_cast<const LW*>(s_only_g);
     StreamCtx<FMT, SW, SMEM> sc{tab, XSMEM ? tab + xoff : xg, SMEM ? smem_u32(tab) : 0u,
                                XSMEM ? smem_u32(tab) + xoff : 0u, s_only, reinterpret_cast<const uint32_t*>(P64), nw64,
-                               out, lane, (1u << lane) - 1u, ((1u << lane) - 1u) | (1u << lane)};
+                               out, ostride, lane, (1u << lane) - 1u, ((1u << lane) - 1u) | (1u << lane)};
     const uint32_t* mtab16 = reinterpret_cast<const uint32_t*>(tab);
     const uint2* mtab32 = reinterpret_cast<const uint2*>(tab);
     const uint4* xtab = reinterpret_cast<const uint4*>(XSMEM ? tab + xoff : xg);
@@ -1036,7 +1038,7 @@ __global__ void __launch_bounds__(NT)
                             const uint32_t* __restrict__ task_row, uint32_t task_begin, uint32_t ntasks,
                             uint32_t* __restrict__ task_ctr, const void* __restrict__ tab_g, uint32_t tab_bytes,
                             const void* __restrict__ s_only_g, const uint32_t* __restrict__ P32, uint32_t nw32,
-                            SW* __restrict__ out) {
+                            SW* __restrict__ out, uint32_t ostride) {
     static_assert(FMT != 64, "split tables only");
     using LW = typename Fmt<FMT>::LW;
     constexpr int K = kStreamK;
@@ -1060,7 +1062,7 @@ __global__ void __launch_bounds__(NT)
     stage_table(smem_raw, tab_g, tab_bytes, &tab_bar);  // includes __syncthreads (barrier inits visible)
     const uint8_t* tab = smem_raw;
     StreamCtx<FMT, SW, true> sc{tab, tab + split_x_offset(FMT, nw32), smem_u32(tab), smem_u32(tab) + split_x_offset(FMT, nw32),
-                               static_cast<const LW*>(s_only_g), P32, nw32, out, lane, (1u << lane) - 1u,
+                               static_cast<const LW*>(s_only_g), P32, nw32, out, ostride, lane, (1u << lane) - 1u,
                                ((1u << lane) - 1u) | (1u << lane)};
 
     // ---- issue side (warp-uniform state; lane 0 issues the copies) --------
@@ -1463,7 +1465,7 @@ static cudaError_t launch_stream_v(const LaunchArgs& a, cudaStream_t st) {
         }
         if (tab_bytes % 16u || tab_bytes > kMaxSmemTable) return cudaErrorInvalidValue;  // never launch an uncompletable TMA copy
         kern<<<sm_count(), NT, tab_bytes, st>>>(a.pairs, a.task_pair, a.task_row, a.task_begin, a.ntasks, a.task_ctr, a.sf, tab_bytes,
-                                                a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out));
+                                                a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out), a.ostride ? a.ostride : 1u);
     } else {
         static int per_sm = 0;
         if (!per_sm) {
@@ -1471,7 +1473,7 @@ static cudaError_t launch_stream_v(const LaunchArgs& a, cudaStream_t st) {
             if (per_sm <= 0) per_sm = 4;
         }
         kern<<<sm_count() * per_sm, NT, 0, st>>>(a.pairs, a.task_pair, a.task_row, a.task_begin, a.ntasks, a.task_ctr, a.sf, tab_bytes,
-                                                 a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out));
+                                                 a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out), a.ostride ? a.ostride : 1u);
     }
     return cudaSuccess;
 }
@@ -1497,7 +1499,7 @@ static cudaError_t launch_stream_tma(const LaunchArgs& a, uint32_t tab_bytes, cu
         attr_set[dev] = smem;
     }
     kern<<<sm_count(), NT, smem, st>>>(a.pairs, a.task_pair, a.task_row, a.task_begin, a.ntasks, a.task_ctr, a.sf, tab_bytes,
-                                       a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out));
+                                       a.s_only, a.P32, a.nw32, static_cast<SW*>(a.out), a.ostride ? a.ostride : 1u);
     return cudaSuccess;
 }
 
@@ -1542,7 +1544,7 @@ static cudaError_t launch_stream64_v(const LaunchArgs& a, cudaStream_t st) {
         }
         if (smem % 16u || smem > kMaxSmemTable) return cudaErrorInvalidValue;
         kern<<<sm_count(), NT, smem, st>>>(a.t64, a.task_byte64, a.task_n64, a.task_row, a.task_begin, a.ntasks,
-                                           a.task_ctr, a.sf, tab_bytes, a.s_only, P64, a.nw64, static_cast<SW*>(a.out));
+                                           a.task_ctr, a.sf, tab_bytes, a.s_only, P64, a.nw64, static_cast<SW*>(a.out), a.ostride ? a.ostride : 1u);
     } else {
         static int per_sm = 0;
         if (!per_sm) {
@@ -1551,7 +1553,7 @@ static cudaError_t launch_stream64_v(const LaunchArgs& a, cudaStream_t st) {
         }
         kern<<<sm_count() * per_sm, NT, 0, st>>>(a.t64, a.task_byte64, a.task_n64, a.task_row, a.task_begin, a.ntasks,
                                                  a.task_ctr, a.sf, tab_bytes, a.s_only, P64, a.nw64,
-                                                 static_cast<SW*>(a.out));
+                                                 static_cast<SW*>(a.out), a.ostride ? a.ostride : 1u);
     }
     return cudaSuccess;
 }

@@ -26,6 +26,7 @@ struct LaunchArgs {
     const uint32_t* perm;
     void* out;
     int label_bytes;
+    uint32_t ostride;  // single-frame kernels: label of row r at out[r * ostride] (0 = 1)
     uint32_t* task_ctr;  // this launch's kCtrStride device counters, reset by the summary kernel
     const void* s_only;  // S mask per (word, frame): over-path probes, full-mask pairs
     // 64-cell-word single-frame copy (null: use the 32-bit stream copy)
