@@ -339,7 +339,7 @@ ltlg_status run_guards(ltlg_ctx* ctx, Shard& s) {
     return LTLG_OK;
 }
 
-constexpr int kSmallFrames = 12;  // sweep_frames: per-frame single-frame launches win up to ~12 frames
+constexpr int kSmallFrames = 16;  // sweep_frames: per-frame single-frame launches win up to ~16 frames
 
 // Multi-frame submit of few frames: per frame, the 64-cell summary + one
 // single-frame launch writing labels[row * frames + f].
@@ -420,7 +420,11 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         }
         static const bool wide_b_ok = !getenv("LTLG_BATCH64") || atoi(getenv("LTLG_BATCH64")) != 0;
         const bool wide_b = wide_b_ok && frames > 1 && props <= 32;  // 64-cell-word multi-frame path
-        CK(s.sf.reserve(wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32
+        // prop-lane kernel for <= 64 frames (dev knob LTLG_PROPLANE=0: the frame-per-lane kernel)
+        static const bool pl_ok = !getenv("LTLG_PROPLANE") || atoi(getenv("LTLG_PROPLANE")) != 0;
+        const bool pl = wide_b && pl_ok && frames <= 64;
+        CK(s.sf.reserve(pl ? pl_work_bytes(frames, nw64)
+                        : wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32
                         : wide ? split64_table_bytes(props, nw64)
                              : frames == 1 && props <= 32
                                    ? split_table_bytes(props, nw32)
@@ -433,6 +437,9 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         const int nctr = static_cast<int>((s.block_row.size() - 1) * kCtrStride);
         if (wide)
             CK(launch_summary64(s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr, s.ctr.ptr, nctr, s.stream),
+               "summary kernel");
+        else if (pl)
+            CK(launch_pl(s.Pdev(), props, frames, nw64, ctx->cells, s.sf.ptr, s.sf.bytes, s.ctr.ptr, nctr, s.stream),
                "summary kernel");
         else if (wide_b)
             CK(launch_summary_b64(s.Pdev(), props, frames, nw64, ctx->cells, s.sf.ptr, nullptr, s.s_only.ptr,
@@ -457,6 +464,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         const bool single = frames == 1;
         if (single) a.pairs = s.pairs_s.ptr;
         if (wide_b) {
+            a.prop_lane = pl ? 1 : 0;
             a.mask_b64 = s.mask_b64.ptr;
             a.word_b64 = s.word_b64.ptr;
             a.task_pair_b64 = s.tpair_b64.ptr;

@@ -1708,6 +1708,238 @@ cudaError_t launch_summary_b64(const uint64_t* P64, int props, int frames, uint3
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Prop-lane multi-frame path (<= 32 props, <= 64 frames): lane j owns
+// proposition j and a 64-bit mask over the frames.  Per 64-cell word w:
+//   ffr[w * 32 + j]  frames where P_j[w] covers the word  (hit for any mask)
+//   sfr[w * 32 + j]  frames where P_j[w] != 0            (hit for a full mask)
+//   rec[rec_se[w].x .. rec_se[w].y)  one record per partial (frame, prop):
+//        {P_j^f[w] lo, hi, byte offset of accumulator word (f>>5)*32 + j, 1 << (f & 31)}
+// A pair (m, w) ORs ffr into its lanes and probes the word's records with
+// all 32 lanes, OR-ing hits (j, f) into a per-warp shared-memory accumulator;
+// at each row end a 32x32 bit transpose turns the prop-major masks into the
+// frame-major labels (lane f holds frame f and f + 32).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) pl_summary_kernel(const uint64_t* __restrict__ P64, int props, int frames,
+                                                         uint32_t nw64, uint64_t cells, uint64_t* __restrict__ ffr,
+                                                         uint64_t* __restrict__ sfr, uint32_t* __restrict__ cnt,
+                                                         uint32_t* __restrict__ wcnt, uint32_t* __restrict__ task_ctr,
+                                                         int nctr) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (t < static_cast<uint64_t>(nctr)) task_ctr[t] = 0;
+    const uint32_t w = static_cast<uint32_t>(t >> 5), j = static_cast<uint32_t>(t & 31);
+    if (w > nw64) return;
+    uint64_t full = 0, any = 0;
+    uint32_t n = 0;
+    const uint64_t lo = static_cast<uint64_t>(w) * 64;
+    if (w < nw64 && lo < cells && j < static_cast<uint32_t>(props)) {
+        const uint64_t valid = (cells - lo >= 64) ? ~0ull : ((1ull << (cells - lo)) - 1ull);
+        const uint64_t* base = P64 + static_cast<uint64_t>(j) * nw64 + w;
+        for (int f = 0; f < frames; ++f) {
+            const uint64_t x = base[static_cast<uint64_t>(f) * props * nw64] & valid;
+            any |= static_cast<uint64_t>(x != 0) << f;
+            full |= static_cast<uint64_t>(x == valid) << f;
+            n += (x != 0 && x != valid);
+        }
+    }
+    ffr[t] = full;
+    sfr[t] = any;
+    cnt[t] = n;
+    if (n) atomicAdd(wcnt + w, n);
+}
+
+// rec_off = exclusive scan of wcnt (one CTA); cursor = rec_off
+__global__ void __launch_bounds__(1024) pl_scan_kernel(const uint32_t* __restrict__ wcnt, uint32_t n,
+                                                       uint2* __restrict__ rec_se, uint32_t* __restrict__ cursor) {
+    __shared__ uint32_t part[1024];
+    const uint32_t per = (n + 1023) / 1024, b = threadIdx.x * per, e = b + per < n ? b + per : n;
+    uint32_t sum = 0;
+    for (uint32_t i = b; i < e; ++i) sum += wcnt[i];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (uint32_t d = 1; d < 1024; d <<= 1) {
+        const uint32_t v = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t acc = part[threadIdx.x] - sum;
+    for (uint32_t i = b; i < e; ++i) {
+        rec_se[i] = make_uint2(acc, acc + wcnt[i]);
+        cursor[i] = acc;
+        acc += wcnt[i];
+    }
+}
+
+__global__ void __launch_bounds__(256) pl_fill_kernel(const uint64_t* __restrict__ P64, int props, int frames,
+                                                      uint32_t nw64, uint64_t cells, const uint32_t* __restrict__ cnt,
+                                                      uint32_t* __restrict__ cursor, uint4* __restrict__ rec) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint32_t w = static_cast<uint32_t>(t >> 5), j = static_cast<uint32_t>(t & 31);
+    if (w >= nw64) return;
+    const uint32_t n = cnt[t];
+    if (!n) return;
+    uint32_t pos = atomicAdd(cursor + w, n);  // record order within a word is irrelevant (OR)
+    const uint64_t lo = static_cast<uint64_t>(w) * 64;
+    const uint64_t valid = (cells - lo >= 64) ? ~0ull : ((1ull << (cells - lo)) - 1ull);
+    const uint64_t* base = P64 + static_cast<uint64_t>(j) * nw64 + w;
+    for (int f = 0; f < frames; ++f) {
+        const uint64_t x = base[static_cast<uint64_t>(f) * props * nw64] & valid;
+        if (x != 0 && x != valid)  // smem accumulator word (f >> 5) * 32 + j, bit f & 31
+            rec[pos++] = make_uint4(static_cast<uint32_t>(x), static_cast<uint32_t>(x >> 32),
+                                    4u * ((static_cast<uint32_t>(f) & 32u) | j), 1u << (f & 31));
+    }
+}
+
+// 32x32 bit transpose across the warp: in, lane l holds row l; out, lane l
+// holds column l (bit r = row r's bit l).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+    const uint32_t masks[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int d = 16 >> i;
+        const uint32_t m = masks[i];
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, d);
+        x = (lane & d) ? ((x & ~m) | ((y >> d) & m)) : ((x & m) | ((y << d) & ~m));
+    }
+    return x;
+}
+
+template <typename SW>
+__global__ void __launch_bounds__(256)
+    label_pl_kernel(const uint64_t* __restrict__ masks, const uint32_t* __restrict__ words,
+                    const uint64_t* __restrict__ task_pair, const uint32_t* __restrict__ task_row, uint32_t task_begin,
+                    uint32_t ntasks, uint32_t* __restrict__ task_ctr, const uint64_t* __restrict__ ffr,
+                    const uint64_t* __restrict__ sfr, const uint2* __restrict__ rec_se,
+                    const uint4* __restrict__ rec, int frames, const uint32_t* __restrict__ perm,
+                    SW* __restrict__ out) {
+    // per warp: partial-record hits by (frame half, prop) -- 32-bit words, so
+    // the OR is a native shared-memory atomic (64-bit ones are CAS loops)
+    __shared__ uint32_t s_acc[8][64];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint32_t* sacc = s_acc[wib];
+    const uint32_t sacc_s = smem_u32(sacc);
+    sacc[lane] = 0;
+    sacc[lane + 32] = 0;
+    __syncwarp();
+    const uint4* lane_rec = rec + lane;
+    const uint64_t* lane_ffr = ffr + lane;
+    const uint64_t* lane_sfr = sfr + lane;
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntasks) break;
+        const uint64_t p0 = task_pair[t], p1 = task_pair[t + 1];
+        const int64_t r0 = task_row[t];
+        int64_t row = r0 - 1;
+        uint64_t acc = 0;  // frames where prop `lane` hits the open row
+        auto store = [&](int64_t r) {
+            __syncwarp();
+            acc |= (static_cast<uint64_t>(sacc[lane + 32]) << 32) | sacc[lane];
+            sacc[lane] = 0;
+            sacc[lane + 32] = 0;
+            const uint32_t lo = transpose32(static_cast<uint32_t>(acc), lane);   // frame lane
+            const uint32_t hi = transpose32(static_cast<uint32_t>(acc >> 32), lane);  // frame lane + 32
+            SW* o = out + static_cast<uint64_t>(perm[r]) * frames;
+            if (lane < frames) o[lane] = static_cast<SW>(lo);
+            if (lane + 32 < frames) o[lane + 32] = static_cast<SW>(hi);
+            __syncwarp();
+        };
+        uint2 cm = __ldg(reinterpret_cast<const uint2*>(masks + p0 + lane));
+        uint32_t cw = __ldg(words + p0 + lane);
+        for (uint64_t c = p0; c < p1; c += 32) {
+            uint2 nm = cm;
+            uint32_t nwd = cw;
+            if (c + 32 < p1) {
+                nm = __ldg(reinterpret_cast<const uint2*>(masks + c + 32 + lane));
+                nwd = __ldg(words + c + 32 + lane);
+            }
+            const int n = static_cast<int>(p1 - c < 32 ? p1 - c : 32);
+            for (int i = 0; i < n; ++i) {
+                const uint32_t mlo = __shfl_sync(0xffffffffu, cm.x, i), mhi = __shfl_sync(0xffffffffu, cm.y, i);
+                const uint32_t wh = __shfl_sync(0xffffffffu, cw, i);
+                if (wh & kHead) {  // warp-uniform
+                    if (row >= r0) store(row);
+                    ++row;
+                    acc = 0;
+                }
+                const uint32_t w = wh & kWordMask;
+                if ((mlo & mhi) == 0xffffffffu) {  // the whole 64-cell word is swept: every nonzero frame hits
+                    acc |= __ldg(index_wide(lane_sfr, w * 32u));
+                    continue;
+                }
+                acc |= __ldg(index_wide(lane_ffr, w * 32u));
+                const uint2 se = __ldg(rec_se + w);  // uniform
+                // all lanes probe 32 records at a time (the array is padded, so
+                // reading past the word's last record is harmless)
+                for (uint32_t q = se.x; q < se.y; q += 32) {
+                    const uint4 r = __ldg(index_wide(lane_rec, q));
+                    const bool hit = (q + lane < se.y) && ((mlo & r.x) | (mhi & r.y));
+                    if (hit) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(sacc_s + r.z), "r"(r.w) : "memory");
+                }
+            }
+            cm = nm;
+            cw = nwd;
+        }
+        if (row >= r0) store(row);
+    }
+}
+
+cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* work,
+                      size_t work_bytes, uint32_t* task_ctr, int nctr, cudaStream_t st) {
+    if (props > 32 || frames > 64) return cudaErrorInvalidValue;
+    uint8_t* wb = static_cast<uint8_t*>(work);
+    const uint64_t nt = static_cast<uint64_t>(nw64 + 1) * 32;
+    uint64_t* ffr = reinterpret_cast<uint64_t*>(wb);
+    uint64_t* sfr = ffr + nt;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(sfr + nt);
+    uint32_t* wcnt = cnt + nt;
+    uint32_t* cursor = wcnt + (nw64 + 2);
+    uint2* rec_se = reinterpret_cast<uint2*>(wb + ((reinterpret_cast<uint8_t*>(cursor + (nw64 + 2)) - wb + 7u) & ~size_t(7)));
+    const size_t rec_at = ((reinterpret_cast<uint8_t*>(rec_se + (nw64 + 2)) - wb) + 15u) & ~size_t(15);
+    if (rec_at > work_bytes) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(wcnt, 0, (nw64 + 2) * 4, st);
+    if (e != cudaSuccess) return e;
+    const uint64_t nthreads = nt > static_cast<uint64_t>(nctr) ? nt : static_cast<uint64_t>(nctr);
+    pl_summary_kernel<<<static_cast<unsigned>((nthreads + 255) / 256), 256, 0, st>>>(P64, props, frames, nw64, cells,
+                                                                                    ffr, sfr, cnt, wcnt, task_ctr, nctr);
+    pl_scan_kernel<<<1, 1024, 0, st>>>(wcnt, nw64 + 1, rec_se, cursor);
+    pl_fill_kernel<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(
+        P64, props, frames, nw64, cells, cnt, cursor, reinterpret_cast<uint4*>(wb + rec_at));
+    return cudaGetLastError();
+}
+
+size_t pl_work_bytes(int frames, uint32_t nw64) {
+    const uint64_t nt = static_cast<uint64_t>(nw64 + 1) * 32;
+    const size_t head = ((nt * 16 + nt * 4 + 2 * (nw64 + 2) * 4 + 8 + (nw64 + 2) * 8) + 15u) & ~size_t(15);
+    // worst case: every (word, prop, frame) partial; + 32 records of padding
+    return head + (nt * static_cast<uint64_t>(frames) + 32) * 16;
+}
+
+template <typename SW>
+static void launch_pl_label(const LaunchArgs& a, cudaStream_t st) {
+    const uint64_t nt = static_cast<uint64_t>(a.nw64 + 1) * 32;
+    const uint8_t* wb = static_cast<const uint8_t*>(a.sf);
+    const uint64_t* ffr = reinterpret_cast<const uint64_t*>(wb);
+    const uint64_t* sfr = ffr + nt;
+    const uint32_t* cnt = reinterpret_cast<const uint32_t*>(sfr + nt);
+    const uint32_t* cursor = cnt + nt + (a.nw64 + 2);
+    const uint2* rec_se = reinterpret_cast<const uint2*>(
+        wb + ((reinterpret_cast<const uint8_t*>(cursor + (a.nw64 + 2)) - wb + 7u) & ~size_t(7)));
+    const size_t rec_at = ((reinterpret_cast<const uint8_t*>(rec_se + (a.nw64 + 2)) - wb) + 15u) & ~size_t(15);
+    static int per_sm = 0;
+    auto kern = label_pl_kernel<SW>;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+        if (per_sm <= 0) per_sm = 4;
+    }
+    kern<<<sm_count() * per_sm, 256, 0, st>>>(a.mask_b64, a.word_b64, a.task_pair_b64, a.task_row, a.task_begin,
+                                              a.ntasks, a.task_ctr, ffr, sfr, rec_se,
+                                              reinterpret_cast<const uint4*>(wb + rec_at), a.frames, a.perm,
+                                              static_cast<SW*>(a.out));
+}
+
 template <int FMT, typename SW, int FPL, bool FULL>
 static void launch_batch_t(const LaunchArgs& a, cudaStream_t st) {
     static int per_sm = 0;
@@ -1747,6 +1979,12 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
             case 2: e = launch_stream_t<16, uint16_t>(a, st); break;
             case 4: e = launch_stream_t<32, uint32_t>(a, st); break;
             default: e = launch_stream_t<64, uint64_t>(a, st); break;
+        }
+    } else if (a.mask_b64 && a.prop_lane) {  // prop-lane multi-frame path (<= 32 props, <= 64 frames)
+        switch (a.label_bytes) {
+            case 1: launch_pl_label<uint8_t>(a, st); break;
+            case 2: launch_pl_label<uint16_t>(a, st); break;
+            default: launch_pl_label<uint32_t>(a, st); break;
         }
     } else if (a.mask_b64) {  // 64-cell-word multi-frame path (<= 32 props)
         switch (a.label_bytes) {

@@ -39,6 +39,7 @@ struct LaunchArgs {
     const uint32_t* word_b64;
     const uint64_t* task_pair_b64;
     const uint64_t* pb64;  // Pb table of summary_b64_kernel
+    int prop_lane;         // multi-frame: the prop-lane kernel (sf = its launch_pl work buffer)
 };
 
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,
@@ -50,6 +51,9 @@ size_t split_table_bytes(int props, uint32_t nw32);
 size_t split64_table_bytes(int props, uint32_t nw64);
 cudaError_t launch_summary_b64(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* tab,
                                uint64_t* pbt, void* s_only, uint32_t* task_ctr, int nctr, cudaStream_t st);
+cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* work,
+                      size_t work_bytes, uint32_t* task_ctr, int nctr, cudaStream_t st);
+size_t pl_work_bytes(int frames, uint32_t nw64);
 cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
                              uint32_t* task_ctr, int nctr, cudaStream_t st);
 bool stream_table_in_smem(int props, uint32_t nw32);

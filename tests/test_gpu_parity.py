@@ -576,6 +576,7 @@ def test_config5_dense_grid_slice():
     {"LTLG_STREAM64": "0", "LTLG_STREAM_CFG": "2"},                         # double-buffered 32-cell
     {"LTLG_STREAM64": "0", "LTLG_STREAM_CFG": "4"},                         # TMA-ring 32-cell
     {"LTLG_STREAM_TABLE": "0"},                                             # summary through L1
+    {"LTLG_PROPLANE": "0"},                                                 # frame-per-lane 64-cell kernel
 ])
 def test_ab_variants_parity(knobs):
     # the A/B kernel variants (env knobs, read once per process) stay bit-exact
