@@ -301,15 +301,16 @@ def main():
     rows_local = r1 - r0
     alg_bytes = 8 * int(info.words) + 4 * (rows_local + 1) + F * (cells * props // 8 + rows_local * 4)
     achieved = alg_bytes / (label_ms / 1e3) / 1e9
-    traffic = ncu_traffic("label_batch64_kernel")
+    traffic = ncu_traffic("label_pl_kernel")
     sm_clk = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
     lop3 = float(info.words) * F * props  # one AND-OR per stored T word per prop per frame
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "peak_source": src, "kernel": "label_batch64_kernel<u32,2,full>",
+                "traffic": traffic, "peak_source": src, "kernel": "label_pl_kernel<u32> (prop-lane multi-frame)",
                 "alg_bytes_per_launch": alg_bytes, "kernel_ms": label_ms, "summary_kernel_ms": summary_ms,
                 "note": "algorithmic bytes = 8*W32 + 4*(E+1) + F*(cells*props/8 + E*4); traffic = dram read+write "
                         "bytes per launch from the committed ncu --set full capture (profiles/traffic.json). The "
-                        "multi-frame kernel is not HBM-bound: ncu shows the ALU pipe saturated (see int_ops)",
+                        "multi-frame kernel is not HBM-bound: ncu shows the L1TEX pipe (record gathers + shared-"
+                        "memory OR reductions) and issue saturated (see int_ops)",
                 "int_ops": {"alg_and_or_per_launch": lop3, "achieved_per_s": lop3 / (label_ms / 1e3),
                             "peak_per_s": 148 * 64 * sm_clk,
                             "frac": lop3 / (label_ms / 1e3) / (148 * 64 * sm_clk),
@@ -392,11 +393,12 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
 
     if rank == 0:
+        # gpu_launches: our kernels per step = pl_summary, pl_scan, pl_fill, label_pl
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32", "data": "synthetic", "config": cfg_json(world), "clocks": clk.summary(),
-            "gpu_launches": 2 * K, "roofline": roofline, "latency": lat, "e2e": e2e, "cpu_baseline": cpu,
+            "gpu_launches": 4 * K, "roofline": roofline, "latency": lat, "e2e": e2e, "cpu_baseline": cpu,
             "shape": {"W32": W32, "rows": rows_all, "t_bytes_device": int(info.t_bytes)},
         }
         print(json.dumps(line), flush=True)
