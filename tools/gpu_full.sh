@@ -16,7 +16,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $out/${tag}_
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/${tag}_launches.csv \
     python bench.py --quick --steps 3 --warmup 3 --no-cpu-baseline > $out/${tag}_ncu_bench.log 2>&1; echo "ncu launches rc=$?"
 # full capture of the top kernels
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:label_batch -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"label_pl|label_batch" -s 2 -c 1 \
     -o $out/${tag}_batch python bench.py --quick --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $out/${tag}_ncu_batch.log 2>&1; echo "ncu batch rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:label_stream -s 5 -c 1 \
     -o $out/${tag}_stream python tools/sweep_stream.py > $out/${tag}_ncu_stream.log 2>&1; echo "ncu stream rc=$?"
