@@ -1714,11 +1714,15 @@ cudaError_t launch_summary_b64(const uint64_t* P64, int props, int frames, uint3
 //   ffr[w * 32 + j]  frames where P_j[w] covers the word  (hit for any mask)
 //   sfr[w * 32 + j]  frames where P_j[w] != 0            (hit for a full mask)
 //   rec[rec_se[w].x .. rec_se[w].y)  one record per partial (frame, prop):
-//        {P_j^f[w] lo, hi, byte offset of accumulator word (f>>5)*32 + j, 1 << (f & 31)}
+//        {P_j^f[w] lo, hi, byte offset 4 f of frame f's accumulator, 1 << j}
+//        grouped by prop, so the 32 records one probe round reads mostly
+//        name distinct frames (distinct shared-memory words, no same-address
+//        serialisation of the ORs)
 // A pair (m, w) ORs ffr into its lanes and probes the word's records with
-// all 32 lanes, OR-ing hits (j, f) into a per-warp shared-memory accumulator;
-// at each row end a 32x32 bit transpose turns the prop-major masks into the
-// frame-major labels (lane f holds frame f and f + 32).
+// all 32 lanes, OR-ing hits (j, f) into a per-warp shared-memory label
+// accumulator acc[f] |= 1 << j; at each row end a 32x32 bit transpose turns
+// the prop-major ffr masks into frame-major ones (lane f holds frame f and
+// f + 32) and ORs in acc[f].
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) pl_summary_kernel(const uint64_t* __restrict__ P64, int props, int frames,
                                                          uint32_t nw64, uint64_t cells, uint64_t* __restrict__ ffr,
@@ -1785,9 +1789,9 @@ __global__ void __launch_bounds__(256) pl_fill_kernel(const uint64_t* __restrict
     const uint64_t* base = P64 + static_cast<uint64_t>(j) * nw64 + w;
     for (int f = 0; f < frames; ++f) {
         const uint64_t x = base[static_cast<uint64_t>(f) * props * nw64] & valid;
-        if (x != 0 && x != valid)  // smem accumulator word (f >> 5) * 32 + j, bit f & 31
+        if (x != 0 && x != valid)  // smem label accumulator word f, bit j
             rec[pos++] = make_uint4(static_cast<uint32_t>(x), static_cast<uint32_t>(x >> 32),
-                                    4u * ((static_cast<uint32_t>(f) & 32u) | j), 1u << (f & 31));
+                                    4u * static_cast<uint32_t>(f), 1u << j);
     }
 }
 
@@ -1813,8 +1817,8 @@ __global__ void __launch_bounds__(256)
                     const uint64_t* __restrict__ sfr, const uint2* __restrict__ rec_se,
                     const uint4* __restrict__ rec, int frames, const uint32_t* __restrict__ perm,
                     SW* __restrict__ out) {
-    // per warp: partial-record hits by (frame half, prop) -- 32-bit words, so
-    // the OR is a native shared-memory atomic (64-bit ones are CAS loops)
+    // per warp: partial-record hits, one 32-bit prop mask per frame (a native
+    // shared-memory OR; 64-bit ones are CAS loops)
     __shared__ uint32_t s_acc[8][64];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint32_t* sacc = s_acc[wib];
@@ -1833,14 +1837,13 @@ __global__ void __launch_bounds__(256)
         const uint64_t p0 = task_pair[t], p1 = task_pair[t + 1];
         const int64_t r0 = task_row[t];
         int64_t row = r0 - 1;
-        uint64_t acc = 0;  // frames where prop `lane` hits the open row
+        uint64_t acc = 0;  // frames where prop `lane` covers a swept word of the open row
         auto store = [&](int64_t r) {
             __syncwarp();
-            acc |= (static_cast<uint64_t>(sacc[lane + 32]) << 32) | sacc[lane];
+            const uint32_t lo = transpose32(static_cast<uint32_t>(acc), lane) | sacc[lane];  // frame lane
+            const uint32_t hi = transpose32(static_cast<uint32_t>(acc >> 32), lane) | sacc[lane + 32];  // frame lane + 32
             sacc[lane] = 0;
             sacc[lane + 32] = 0;
-            const uint32_t lo = transpose32(static_cast<uint32_t>(acc), lane);   // frame lane
-            const uint32_t hi = transpose32(static_cast<uint32_t>(acc >> 32), lane);  // frame lane + 32
             SW* o = out + static_cast<uint64_t>(perm[r]) * frames;
             if (lane < frames) o[lane] = static_cast<SW>(lo);
             if (lane + 32 < frames) o[lane + 32] = static_cast<SW>(hi);
@@ -1856,6 +1859,9 @@ __global__ void __launch_bounds__(256)
                 nwd = __ldg(words + c + 32 + lane);
             }
             const int n = static_cast<int>(p1 - c < 32 ? p1 - c : 32);
+            // lane i fetches the record range of pair i once per chunk (the
+            // words arrived with the previous chunk's prefetch)
+            const uint2 cse = __ldg(rec_se + (lane < n ? (cw & kWordMask) : 0u));
             for (int i = 0; i < n; ++i) {
                 const uint32_t mlo = __shfl_sync(0xffffffffu, cm.x, i), mhi = __shfl_sync(0xffffffffu, cm.y, i);
                 const uint32_t wh = __shfl_sync(0xffffffffu, cw, i);
@@ -1870,7 +1876,7 @@ __global__ void __launch_bounds__(256)
                     continue;
                 }
                 acc |= __ldg(index_wide(lane_ffr, w * 32u));
-                const uint2 se = __ldg(rec_se + w);  // uniform
+                const uint2 se = make_uint2(__shfl_sync(0xffffffffu, cse.x, i), __shfl_sync(0xffffffffu, cse.y, i));
                 // all lanes probe 32 records at a time (the array is padded, so
                 // reading past the word's last record is harmless)
                 for (uint32_t q = se.x; q < se.y; q += 32) {
