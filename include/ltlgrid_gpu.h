@@ -46,7 +46,8 @@ typedef enum ltlg_status {
     LTLG_ECUDA = 4,   /* CUDA runtime error (no device, launch failure)  */
     LTLG_ENCCL = 5,   /* NCCL error (multi-device contexts)              */
     LTLG_ENOMEM = 6,  /* device or host allocation failed                */
-    LTLG_ESTATE = 7   /* call out of order (e.g. submit before load)     */
+    LTLG_ESTATE = 7,  /* call out of order (e.g. submit before load)     */
+    LTLG_EDOMAIN = 8  /* reference std::domain_error                     */
 } ltlg_status;
 
 typedef struct ltlg_ctx ltlg_ctx;
@@ -256,6 +257,43 @@ ltlg_status ltlg_validate_csr(uint64_t rows, uint64_t cols, const uint64_t* row_
 ltlg_status ltlg_label_all(uint64_t rows, uint64_t cols, const uint64_t* row_offsets,
                            const uint32_t* col_indices, uint64_t cells, int num_props,
                            const uint64_t* column_words, int workers, uint64_t* out);
+
+/* ------------------------------------------------------------------------
+ * Swept-volume matrix on the GPU: the abstraction T itself.
+ * Replaces swept_volume_matrix (core/include/ltlgrid/label.hpp:42-43,
+ * core/src/label.cpp:75-116) = sweep_voxelize_indices per edge
+ * (abstraction.hpp:88-93, abstraction.cpp:172-221).
+ *
+ * grid: a 3-axis (x, y, tau) GridSpec, depth <= 32.  footprint: FootprintSpec
+ * (abstraction.hpp:58-62).  Edge e's trajectory is samples
+ * [sample_offsets[e], sample_offsets[e+1]), 5 doubles per sample in State5
+ * order (px, py, heading, speed, tau; abstraction.hpp:16-22).  Synchronous on
+ * `device`; the CSR stays resident there until copied out or loaded.
+ * Errors, in the reference's order: the GridSpec messages; LTLG_EINVAL
+ * "swept_volume_matrix supports depth <= 32"; LTLG_EINVAL "sweep_voxelize
+ * requires a 3-d (x, y, tau) grid" (when there are edges); per sample in
+ * (edge, sample) order: LTLG_EDOMAIN "trajectory exits workspace (time
+ * axis)", LTLG_EINVAL "footprint must be positive", LTLG_EDOMAIN
+ * "trajectory exits workspace (position)".
+ * ---------------------------------------------------------------------- */
+typedef struct ltlg_footprint {
+    double length, width, ref_offset;
+} ltlg_footprint;
+
+typedef struct ltlg_csr ltlg_csr;
+
+ltlg_status ltlg_swept_volume(const ltlg_gridk* grid, const ltlg_footprint* footprint, uint64_t num_edges,
+                              const uint64_t* sample_offsets, const double* samples, int device, ltlg_csr** out);
+uint64_t ltlg_csr_rows(const ltlg_csr* m);
+uint64_t ltlg_csr_cols(const ltlg_csr* m);
+uint64_t ltlg_csr_nnz(const ltlg_csr* m);
+/* Kernel time of the last ltlg_swept_volume in ms (both passes, CUDA events). */
+double ltlg_csr_build_ms(const ltlg_csr* m);
+/* Host copies: row_offsets (rows + 1 u64), col_indices (nnz u32); either may be NULL. */
+ltlg_status ltlg_csr_copy(const ltlg_csr* m, uint64_t* row_offsets, uint32_t* col_indices);
+/* ltlg_load_abstraction of the swept-volume matrix into an engine. */
+ltlg_status ltlg_load_csr(ltlg_ctx* ctx, const ltlg_csr* m);
+void ltlg_csr_free(ltlg_csr* m);
 
 #ifdef __cplusplus
 }

@@ -243,6 +243,38 @@ class Oracle:
                                  _p(out, C.c_uint64))
         return out[: vwords * props]
 
+    def swept_volume(self, depth, lo, hi, footprint, sample_off, samples):
+        """swept_volume_matrix restatement (oracle_swept_volume): returns
+        (row_offsets u64, cols u32); raises OracleError / DomainError."""
+        L = self.lib
+        d = C.c_double
+        L.oracle_swept_volume.argtypes = [C.c_int, C.POINTER(d), C.POINTER(d), d, d, d, C.c_uint64,
+                                          C.POINTER(C.c_uint64), C.POINTER(d), C.POINTER(C.c_uint64),
+                                          C.POINTER(C.c_uint32), C.c_uint64, C.c_char_p, C.c_size_t]
+        L.oracle_swept_volume.restype = C.c_int
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        hi = np.ascontiguousarray(hi, dtype=np.float64)
+        off = np.ascontiguousarray(sample_off, dtype=np.uint64)
+        smp = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1)
+        edges = off.size - 1
+        rows = np.zeros(edges + 1, dtype=np.uint64)
+        err = C.create_string_buffer(256)
+        args = (depth, _p(lo, d), _p(hi, d), *map(float, footprint), edges, _p(off, C.c_uint64), _p(smp, d),
+                _p(rows, C.c_uint64))
+        rc = L.oracle_swept_volume(*args, None, 0, err, 256)
+        if rc == 0:
+            cols = np.zeros(max(int(rows[-1]), 1), dtype=np.uint32)
+            rc = L.oracle_swept_volume(*args, _p(cols, C.c_uint32), cols.size, err, 256)
+        if rc == 3:
+            raise DomainError(err.value.decode())
+        if rc != 0:
+            raise OracleError(err.value.decode())
+        return rows, cols[: int(rows[-1])]
+
+
+class DomainError(ArithmeticError):
+    """The reference's std::domain_error."""
+
 
 class RefCore:
     """oracle/_ref/libltlgrid_ref.so -- the unmodified reference core."""
@@ -409,6 +441,55 @@ class RefCore:
 
     def time_label_ms(self, m, p, workers=0, repeats=2, out=None):
         return self.lib.ref_time_label_ms(m, p, workers, repeats, _p(out, C.c_uint64) if out is not None else None)
+
+    def abstraction(self, x=(0.0, 64.0), y=(0.0, 64.0), speed=(4.0, 8.0), tau=(0.2, 2.5), tau_limit=3.9,
+                    target_edges=50, seed=17):
+        """build_abstraction (Rect region) -> (sample_off u64, samples (n, 5) f64)."""
+        L = self.lib
+        d, u64 = C.c_double, C.c_uint64
+        L.ref_abstraction_create.argtypes = [d] * 9 + [u64, u64]
+        L.ref_abstraction_create.restype = C.c_void_p
+        L.ref_abstraction_sizes.argtypes = [C.c_void_p, C.POINTER(u64), C.POINTER(u64)]
+        L.ref_abstraction_export.argtypes = [C.c_void_p, C.POINTER(u64), C.POINTER(d)]
+        L.ref_abstraction_free.argtypes = [C.c_void_p]
+        h = L.ref_abstraction_create(*x, *y, *speed, *tau, tau_limit, target_edges, seed)
+        if not h:
+            raise RuntimeError(self.error())
+        try:
+            e, n = u64(0), u64(0)
+            L.ref_abstraction_sizes(h, C.byref(e), C.byref(n))
+            off = np.zeros(e.value + 1, dtype=np.uint64)
+            smp = np.zeros((max(n.value, 1), 5), dtype=np.float64)
+            L.ref_abstraction_export(h, _p(off, u64), _p(smp, d))
+            return off, smp[: n.value]
+        finally:
+            L.ref_abstraction_free(h)
+
+    def swept_volume(self, depth, lo, hi, footprint, sample_off, samples, workers=0):
+        """The reference swept_volume_matrix -> (row_offsets u64, cols u32)."""
+        L = self.lib
+        d, u64 = C.c_double, C.c_uint64
+        L.ref_swept_volume.argtypes = [C.c_int, C.POINTER(d), C.POINTER(d), d, d, d, u64, C.POINTER(u64),
+                                       C.POINTER(d), C.c_int, C.POINTER(u64), C.POINTER(C.c_uint32), u64]
+        L.ref_swept_volume.restype = C.c_int64
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        hi = np.ascontiguousarray(hi, dtype=np.float64)
+        off = np.ascontiguousarray(sample_off, dtype=np.uint64)
+        smp = np.ascontiguousarray(samples, dtype=np.float64).reshape(-1)
+        edges = off.size - 1
+        rows = np.zeros(edges + 1, dtype=np.uint64)
+        args = (depth, _p(lo, d), _p(hi, d), *map(float, footprint), edges, _p(off, u64), _p(smp, d), workers,
+                _p(rows, u64))
+        nnz = L.ref_swept_volume(*args, None, 0)
+        if nnz >= 0:
+            cols = np.zeros(max(nnz, 1), dtype=np.uint32)
+            nnz = L.ref_swept_volume(*args, _p(cols, C.c_uint32), cols.size)
+        if nnz < 0:
+            msg = self.error()
+            if msg.startswith("domain_error: "):
+                raise DomainError(msg[len("domain_error: "):])
+            raise OracleError(msg.split(": ", 1)[-1])
+        return rows, cols[:nnz]
 
     def free(self, m=None, p=None):
         if m:

@@ -17,11 +17,13 @@
 #include <algorithm>
 #include <cstring>
 #include <exception>
+#include <stdexcept>
 #include <limits>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "ltlgrid/abstraction.hpp"
 #include "ltlgrid/grid.hpp"
 #include "ltlgrid/buchi.hpp"
 #include "ltlgrid/label.hpp"
@@ -284,6 +286,98 @@ void ref_guard_admits(std::uint64_t n, const std::uint64_t* labels, int n_guards
             if (g.admits(sym)) m |= std::uint64_t{1} << t;
         }
         out[i] = m;
+    }
+}
+
+// build_abstraction (abstraction.cpp) with a Rect sampling region: the
+// trajectories of its edges, flattened for the swept-volume parity tests.
+// Returns a handle; ref_abstraction_sizes / _export read it out.
+void* ref_abstraction_create(double x_min, double x_max, double y_min, double y_max, double speed_min,
+                             double speed_max, double tau_min, double tau_max, double tau_limit,
+                             std::uint64_t target_edges, std::uint64_t seed) {
+    try {
+        ltlgrid::AbstractionConfig cfg;
+        cfg.region = ltlgrid::SampleRegion::Rect;
+        cfg.x_min = x_min;
+        cfg.x_max = x_max;
+        cfg.y_min = y_min;
+        cfg.y_max = y_max;
+        cfg.speed_min = speed_min;
+        cfg.speed_max = speed_max;
+        cfg.tau_min = tau_min;
+        cfg.tau_max = tau_max;
+        cfg.tau_limit = tau_limit;
+        cfg.target_edges = target_edges;
+        return new ltlgrid::TransitionSystem(ltlgrid::build_abstraction(cfg, seed));
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+void ref_abstraction_sizes(void* h, std::uint64_t* edges, std::uint64_t* samples) {
+    const auto* ts = static_cast<const ltlgrid::TransitionSystem*>(h);
+    *edges = ts->num_edges();
+    std::uint64_t n = 0;
+    for (const auto& tr : ts->trajectories) n += tr.samples.size();
+    *samples = n;
+}
+
+// sample_off (edges + 1), samples (5 doubles per State5: px, py, heading, speed, tau)
+void ref_abstraction_export(void* h, std::uint64_t* sample_off, double* samples) {
+    const auto* ts = static_cast<const ltlgrid::TransitionSystem*>(h);
+    std::uint64_t n = 0;
+    sample_off[0] = 0;
+    for (std::size_t e = 0; e < ts->num_edges(); ++e) {
+        for (const auto& s : ts->trajectories[e].samples) {
+            double* o = samples + 5 * n++;
+            o[0] = s.px;
+            o[1] = s.py;
+            o[2] = s.heading;
+            o[3] = s.speed;
+            o[4] = s.tau;
+        }
+        sample_off[e + 1] = n;
+    }
+}
+
+void ref_abstraction_free(void* h) { delete static_cast<ltlgrid::TransitionSystem*>(h); }
+
+// swept_volume_matrix (label.cpp:75-116) over edges whose trajectories are
+// the given samples, on a 3-d GridSpec(bounds, depth).  Writes row_offsets
+// (edges + 1) and, when cols_cap >= nnz, cols.  Returns nnz, or -1 (error in
+// ref_last_error, prefixed "invalid_argument: " / "domain_error: ").
+std::int64_t ref_swept_volume(int depth, const double* lo, const double* hi, double length, double width,
+                              double ref_offset, std::uint64_t edges, const std::uint64_t* sample_off,
+                              const double* samples, int workers, std::uint64_t* row_offsets, std::uint32_t* cols,
+                              std::uint64_t cols_cap) {
+    try {
+        ltlgrid::TransitionSystem ts;
+        ts.trajectories.resize(edges);
+        ts.edges.resize(edges);
+        for (std::uint64_t e = 0; e < edges; ++e) {
+            auto& tr = ts.trajectories[e];
+            for (std::uint64_t i = sample_off[e]; i < sample_off[e + 1]; ++i) {
+                const double* s = samples + 5 * i;
+                tr.samples.push_back(ltlgrid::State5{s[0], s[1], s[2], s[3], s[4]});
+            }
+        }
+        const ltlgrid::GridSpec g({{lo[0], hi[0]}, {lo[1], hi[1]}, {lo[2], hi[2]}}, depth);
+        ltlgrid::FootprintSpec f{length, width, ref_offset};
+        const auto csr = ltlgrid::swept_volume_matrix(ts, f, g, workers);
+        std::copy(csr.row_offsets.begin(), csr.row_offsets.end(), row_offsets);
+        if (cols && cols_cap >= csr.col_indices.size())
+            std::copy(csr.col_indices.begin(), csr.col_indices.end(), cols);
+        return static_cast<std::int64_t>(csr.col_indices.size());
+    } catch (const std::domain_error& e) {
+        g_err = std::string("domain_error: ") + e.what();
+        return -1;
+    } catch (const std::invalid_argument& e) {
+        g_err = std::string("invalid_argument: ") + e.what();
+        return -1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
     }
 }
 

@@ -6,8 +6,10 @@ abstractions -- a drop-in for the reference's labeling path
   label.label_all     one-shot drop-in for ltlgrid::label_all
   synth               synthetic T / P of the BASELINE configs
 """
-from .label import (CsrBoolMatrix, DensePropMatrix, LabelEngine, LabelMatrix, LtlgError,  # noqa: F401
-                    OccupancyBitset, label_all, rasterize_boxes, read_csb1_shape, read_zobv, to_csr)
+from .label import (CsrBoolMatrix, DensePropMatrix, DomainError, FootprintSpec, LabelEngine,  # noqa: F401
+                    LabelMatrix, LtlgError, OccupancyBitset, SweptVolume, label_all, rasterize_boxes,
+                    read_csb1_shape, read_zobv, swept_volume, swept_volume_matrix, to_csr)
 
-__all__ = ["CsrBoolMatrix", "DensePropMatrix", "LabelEngine", "LabelMatrix", "LtlgError",
-           "OccupancyBitset", "label_all", "rasterize_boxes", "read_csb1_shape", "read_zobv", "to_csr"]
+__all__ = ["CsrBoolMatrix", "DensePropMatrix", "DomainError", "FootprintSpec", "LabelEngine", "LabelMatrix",
+           "LtlgError", "OccupancyBitset", "SweptVolume", "label_all", "rasterize_boxes", "read_csb1_shape",
+           "read_zobv", "swept_volume", "swept_volume_matrix", "to_csr"]

@@ -14,7 +14,7 @@ LIB_DIR = os.path.join(HERE, "_lib")
 GPU_SO = os.path.join(LIB_DIR, "libltlgrid_gpu.so")
 SYNTH_SO = os.path.join(LIB_DIR, "libltlgrid_synth.so")
 
-LTLG_OK, LTLG_EINVAL, LTLG_EFORMAT, LTLG_EIO, LTLG_ECUDA, LTLG_ENCCL, LTLG_ENOMEM, LTLG_ESTATE = range(8)
+LTLG_OK, LTLG_EINVAL, LTLG_EFORMAT, LTLG_EIO, LTLG_ECUDA, LTLG_ENCCL, LTLG_ENOMEM, LTLG_ESTATE, LTLG_EDOMAIN = range(9)
 
 # Every symbol include/ltlgrid_gpu.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -26,6 +26,8 @@ EXPORTS = [
     "ltlg_submit_grid_files", "ltlg_save_labels", "ltlg_read_csb1_words", "ltlg_read_zobv",
     "ltlg_rasterize_boxes", "ltlg_submit_boxes", "ltlg_set_guards", "ltlg_get_admitted", "ltlg_device_admitted",
     "ltlg_submit_grid_device_ex",
+    "ltlg_swept_volume", "ltlg_csr_rows", "ltlg_csr_cols", "ltlg_csr_nnz", "ltlg_csr_build_ms", "ltlg_csr_copy",
+    "ltlg_load_csr", "ltlg_csr_free",
 ]
 
 
@@ -36,6 +38,10 @@ class Options(C.Structure):
 
 class GridK(C.Structure):
     _fields_ = [("dims", C.c_int), ("depth", C.c_int), ("lo", C.c_double * 4), ("hi", C.c_double * 4)]
+
+
+class Footprint(C.Structure):
+    _fields_ = [("length", C.c_double), ("width", C.c_double), ("ref_offset", C.c_double)]
 
 
 class Info(C.Structure):
@@ -105,6 +111,14 @@ def lib() -> C.CDLL:
         "ltlg_set_guards": ([ctxp, i32, vp, vp], i32),
         "ltlg_get_admitted": ([ctxp, i32, vp], i32),
         "ltlg_device_admitted": ([ctxp, i32, C.POINTER(vp)], i32),
+        "ltlg_swept_volume": ([C.POINTER(GridK), C.POINTER(Footprint), u64, vp, vp, i32, C.POINTER(vp)], i32),
+        "ltlg_csr_rows": ([vp], u64),
+        "ltlg_csr_cols": ([vp], u64),
+        "ltlg_csr_nnz": ([vp], u64),
+        "ltlg_csr_build_ms": ([vp], C.c_double),
+        "ltlg_csr_copy": ([vp, vp, vp], i32),
+        "ltlg_load_csr": ([ctxp, vp], i32),
+        "ltlg_csr_free": ([vp], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

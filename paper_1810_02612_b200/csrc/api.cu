@@ -1147,3 +1147,221 @@ ltlg_status ltlg_label_all(uint64_t rows, uint64_t cols, const uint64_t* row_off
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Swept-volume matrix: swept_volume_matrix, label.cpp:75-116.
+// ---------------------------------------------------------------------------
+struct ltlg_csr {
+    int device = 0;
+    uint64_t rows = 0, cols = 0, nnz = 0;
+    DevBuf<uint64_t> off;
+    DevBuf<uint32_t> idx;
+    double ms = 0;
+    ~ltlg_csr() {
+        off.release();
+        idx.release();
+    }
+};
+
+namespace {
+
+struct SweepScratch {
+    DevBuf<uint64_t> off_in, bsum;
+    DevBuf<double> samples;
+    DevBuf<uint32_t> row_cnt, over, ctr;
+    DevBuf<unsigned long long> err, gtab;
+    DevBuf<uint32_t> gkeys;
+    ~SweepScratch() {
+        off_in.release();
+        bsum.release();
+        samples.release();
+        row_cnt.release();
+        over.release();
+        ctr.release();
+        err.release();
+        gtab.release();
+        gkeys.release();
+    }
+};
+
+ltlg_status sweep_build(const ltlg_gridk* g, const ltlg_footprint* f, uint64_t edges, const uint64_t* sample_off,
+                        const double* samples, ltlg_csr* m) {
+    using namespace ltlg;
+    ltlg_ctx* const ctx = nullptr;  // errors go to the thread's last-error slot
+    const uint64_t nsamp = edges ? sample_off[edges] : 0;
+    SweepScratch s;
+    cudaStream_t st = nullptr;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    std::unique_ptr<CUstream_st, void (*)(cudaStream_t)> hold_st(st, [](cudaStream_t x) { cudaStreamDestroy(x); });
+    cudaEvent_t ev[4];
+    for (auto& e : ev) CK(cudaEventCreate(&e), "event");
+    struct EvFree {
+        cudaEvent_t* e;
+        ~EvFree() {
+            for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+        }
+    } ev_free{ev};
+    CK(s.off_in.reserve((edges + 1) * 8), "allocate sweep inputs");
+    CK(s.samples.reserve(std::max<uint64_t>(nsamp, 1) * 40), "allocate sweep inputs");
+    CK(s.row_cnt.reserve(std::max<uint64_t>(edges, 1) * 4), "allocate sweep scratch");
+    CK(s.over.reserve(std::max<uint64_t>(edges, 1) * 4), "allocate sweep scratch");
+    CK(s.ctr.reserve(16), "allocate sweep scratch");
+    CK(s.err.reserve(16), "allocate sweep scratch");
+    CK(s.bsum.reserve(((edges + 1023) / 1024 + 1) * 8), "allocate sweep scratch");
+    CK(m->off.reserve((edges + 1) * 8), "allocate CSR");
+    CK(cudaMemcpyAsync(s.off_in.ptr, sample_off, (edges + 1) * 8, cudaMemcpyHostToDevice, st), "upload trajectories");
+    if (nsamp) CK(cudaMemcpyAsync(s.samples.ptr, samples, nsamp * 40, cudaMemcpyHostToDevice, st), "upload trajectories");
+    const unsigned long long err_init[2] = {~0ull, 0ull};
+    CK(cudaMemcpyAsync(s.err.ptr, err_init, 16, cudaMemcpyHostToDevice, st), "upload");
+    CK(cudaMemsetAsync(s.ctr.ptr, 0, 16, st), "memset");
+
+    SweepParams p{};
+    for (int a = 0; a < 3; ++a) {
+        const int bits = g->depth / 3 + (a < g->depth % 3 ? 1 : 0);
+        p.lo[a] = g->lo[a];
+        p.hi[a] = g->hi[a];
+        p.ncell[a] = int64_t(1) << bits;
+        p.cells[a] = static_cast<double>(p.ncell[a]);
+        p.w[a] = (g->hi[a] - g->lo[a]) / p.cells[a];  // GridSpec::cell_width
+        p.zoff[a] = g->depth % 3 + 2 - a - 3 * (a < g->depth % 3 ? 1 : 0);
+    }
+    p.length = f->length;
+    p.width = f->width;
+    p.ref_offset = f->ref_offset;
+    p.edges = edges;
+    p.sample_off = s.off_in.ptr;
+    p.samples = s.samples.ptr;
+    p.err_key = s.err.ptr;
+    uint32_t* edge_ctr = s.ctr.ptr;
+    uint32_t* n_over = s.ctr.ptr + 1;
+
+    // pass 1: row sizes
+    CK(cudaEventRecord(ev[0], st), "event");
+    if (edges) CK(launch_sweep(0, p, edge_ctr, s.row_cnt.ptr, nullptr, nullptr, s.over.ptr, n_over, nullptr, nullptr,
+                               0, 0, st), "sweep count kernel");
+    unsigned long long err[2];
+    uint32_t nov = 0;
+    CK(cudaMemcpyAsync(err, s.err.ptr, 16, cudaMemcpyDeviceToHost, st), "download");
+    CK(cudaMemcpyAsync(&nov, n_over, 4, cudaMemcpyDeviceToHost, st), "download");
+    CK(cudaEventRecord(ev[1], st), "event");
+    CK(cudaStreamSynchronize(st), "sweep count");
+    if (err[0] != ~0ull) {
+        static const char* const msg[3] = {"trajectory exits workspace (time axis)", "footprint must be positive",
+                                           "trajectory exits workspace (position)"};
+        const int kind = static_cast<int>(err[0] & 3);
+        return set_err(nullptr, kind == 1 ? LTLG_EINVAL : LTLG_EDOMAIN, msg[kind]);
+    }
+    // rows past kSweepCap distinct cells: global-memory sets, grown until they fit
+    uint32_t glog2 = 15;
+    int gblocks = 0;
+    while (nov) {
+        gblocks = static_cast<int>(std::min<uint32_t>(nov, 148));
+        CK(s.gtab.reserve((static_cast<size_t>(gblocks) << glog2) * 8), "allocate sweep overflow sets");
+        CK(s.gkeys.reserve((static_cast<size_t>(gblocks) << (glog2 - 1)) * 4), "allocate sweep overflow sets");
+        CK(cudaMemsetAsync(edge_ctr, 0, 4, st), "memset");
+        CK(cudaMemsetAsync(s.err.ptr + 1, 0, 8, st), "memset");
+        CK(launch_sweep(2, p, edge_ctr, s.row_cnt.ptr, nullptr, nullptr, s.over.ptr, n_over, s.gtab.ptr, s.gkeys.ptr,
+                        glog2, gblocks, st), "sweep overflow count kernel");
+        CK(cudaMemcpyAsync(err, s.err.ptr, 16, cudaMemcpyDeviceToHost, st), "download");
+        CK(cudaStreamSynchronize(st), "sweep overflow count");
+        if (!err[1]) break;
+        if (glog2 >= 30) return set_err(nullptr, LTLG_ENOMEM, "swept-volume row too large");
+        glog2 += 2;
+    }
+    // row offsets, pass 2: rows
+    CK(cudaEventRecord(ev[2], st), "event");
+    CK(launch_scan_counts(s.row_cnt.ptr, edges, s.bsum.ptr, m->off.ptr, st), "scan kernel");
+    uint64_t nnz = 0;
+    CK(cudaMemcpyAsync(&nnz, m->off.ptr + edges, 8, cudaMemcpyDeviceToHost, st), "download");
+    CK(cudaStreamSynchronize(st), "scan");
+    CK(m->idx.reserve(std::max<uint64_t>(nnz, 1) * 4), "allocate CSR");
+    if (edges)
+        CK(launch_sweep(1, p, edge_ctr, s.row_cnt.ptr, m->off.ptr, m->idx.ptr, s.over.ptr, n_over, nullptr, nullptr,
+                        0, 0, st), "sweep fill kernel");
+    if (nov)
+        CK(launch_sweep(3, p, edge_ctr, s.row_cnt.ptr, m->off.ptr, m->idx.ptr, s.over.ptr, n_over, s.gtab.ptr,
+                        s.gkeys.ptr, glog2, gblocks, st), "sweep overflow fill kernel");
+    CK(cudaEventRecord(ev[3], st), "event");
+    CK(cudaStreamSynchronize(st), "sweep fill");
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[2], ev[3]);
+    m->ms = static_cast<double>(a) + b;
+    m->rows = edges;
+    m->cols = uint64_t(1) << g->depth;
+    m->nnz = nnz;
+    return LTLG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ltlg_status ltlg_swept_volume(const ltlg_gridk* grid, const ltlg_footprint* footprint, uint64_t num_edges,
+                              const uint64_t* sample_offsets, const double* samples, int device, ltlg_csr** out) {
+    if (!out) return set_err(nullptr, LTLG_EINVAL, "null argument");
+    *out = nullptr;
+    if (!grid || !footprint || (num_edges && !sample_offsets)) return set_err(nullptr, LTLG_EINVAL, "null argument");
+    // GridSpec ctor (grid.cpp:18-33), then swept_volume_matrix / sweep_collect
+    if (grid->dims < 1) return set_err(nullptr, LTLG_EINVAL, "grid needs at least one axis");
+    if (grid->depth < grid->dims || grid->depth > 63)
+        return set_err(nullptr, LTLG_EINVAL, "grid depth must be in [k, 63]");
+    if (grid->dims > 4) return set_err(nullptr, LTLG_EINVAL, "at most 4 grid axes in this build");
+    for (int a = 0; a < grid->dims; ++a)
+        if (!(grid->lo[a] < grid->hi[a])) return set_err(nullptr, LTLG_EINVAL, "grid bounds must satisfy lo < hi");
+    if (grid->depth > 32) return set_err(nullptr, LTLG_EINVAL, "swept_volume_matrix supports depth <= 32");
+    if (num_edges && grid->dims != 3)
+        return set_err(nullptr, LTLG_EINVAL, "sweep_voxelize requires a 3-d (x, y, tau) grid");
+    if (num_edges > 0xffffffffull) return set_err(nullptr, LTLG_EINVAL, "at most 2^32 - 1 edges in this build");
+    for (uint64_t e = 0; e < num_edges; ++e)
+        if (sample_offsets[e] > sample_offsets[e + 1])
+            return set_err(nullptr, LTLG_EINVAL, "sample_offsets must be nondecreasing");
+    if (num_edges && sample_offsets[num_edges] > sample_offsets[0] && !samples)
+        return set_err(nullptr, LTLG_EINVAL, "null samples");
+    if (num_edges && sample_offsets[0] != 0) return set_err(nullptr, LTLG_EINVAL, "sample_offsets[0] must be 0");
+    ltlg_ctx* const ctx = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return set_err(nullptr, LTLG_ECUDA, "no CUDA device");
+    if (device < 0 || device >= ndev) return set_err(nullptr, LTLG_EINVAL, "device out of range");
+    CK(cudaSetDevice(device), "cudaSetDevice");
+    std::unique_ptr<ltlg_csr> m(new (std::nothrow) ltlg_csr);
+    if (!m) return set_err(nullptr, LTLG_ENOMEM, "out of host memory");
+    m->device = device;
+    const ltlg_status st = sweep_build(grid, footprint, num_edges, sample_offsets, samples, m.get());
+    if (st != LTLG_OK) return st;
+    *out = m.release();
+    return LTLG_OK;
+}
+
+uint64_t ltlg_csr_rows(const ltlg_csr* m) { return m ? m->rows : 0; }
+uint64_t ltlg_csr_cols(const ltlg_csr* m) { return m ? m->cols : 0; }
+uint64_t ltlg_csr_nnz(const ltlg_csr* m) { return m ? m->nnz : 0; }
+double ltlg_csr_build_ms(const ltlg_csr* m) { return m ? m->ms : 0.0; }
+
+ltlg_status ltlg_csr_copy(const ltlg_csr* m, uint64_t* row_offsets, uint32_t* col_indices) {
+    if (!m) return set_err(nullptr, LTLG_EINVAL, "null csr");
+    ltlg_ctx* const ctx = nullptr;
+    CK(cudaSetDevice(m->device), "cudaSetDevice");
+    if (row_offsets) CK(cudaMemcpy(row_offsets, m->off.ptr, (m->rows + 1) * 8, cudaMemcpyDeviceToHost), "download CSR");
+    if (col_indices && m->nnz)
+        CK(cudaMemcpy(col_indices, m->idx.ptr, m->nnz * 4, cudaMemcpyDeviceToHost), "download CSR");
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_load_csr(ltlg_ctx* ctx, const ltlg_csr* m) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!m) return set_err(ctx, LTLG_EINVAL, "null csr");
+    std::vector<uint64_t> off(m->rows + 1);
+    std::vector<uint32_t> idx(std::max<uint64_t>(m->nnz, 1));
+    const ltlg_status st = ltlg_csr_copy(m, off.data(), idx.data());
+    if (st != LTLG_OK) return st;
+    return ltlg_load_abstraction(ctx, m->rows, m->cols, off.data(), idx.data());
+}
+
+void ltlg_csr_free(ltlg_csr* m) {
+    if (!m) return;
+    cudaSetDevice(m->device);
+    delete m;
+}
+
+}  // extern "C"

@@ -69,4 +69,27 @@ cudaError_t launch_resample(int vdepth, double vlo0, double vhi0, double vlo1, d
                             int frames, int props, const uint32_t* world32, uint32_t wnw32, int outside,
                             uint32_t vnw32, uint32_t* out32, cudaStream_t st);
 
+// swept-volume matrix (sweep.cu): 3-axis grid of depth <= 32, so every
+// z-order cell index fits in 32 bits
+constexpr int kSweepThreads = 128;
+constexpr uint32_t kSweepTable = 4096;             // shared-memory set slots per CTA
+constexpr uint32_t kSweepCap = kSweepTable / 2;    // distinct cells per row before overflow
+struct SweepParams {
+    double lo[3], hi[3];
+    double cells[3];  // cells per axis, as double (GridSpec::axis_cells)
+    double w[3];      // GridSpec::cell_width
+    int64_t ncell[3];
+    int zoff[3];      // ZScatter shift per axis
+    double length, width, ref_offset;  // FootprintSpec
+    uint64_t edges;
+    const uint64_t* sample_off;  // edges + 1
+    const double* samples;       // 5 doubles per State5
+    unsigned long long* err_key; // [0] min(sample * 4 + kind), [1] global-table overflows
+};
+size_t sweep_smem_bytes();
+cudaError_t launch_sweep(int mode, const SweepParams& p, uint32_t* edge_ctr, uint32_t* row_cnt, const uint64_t* row_off,
+                         uint32_t* cols, uint32_t* over_list, uint32_t* n_over, unsigned long long* gtab,
+                         uint32_t* gkeys, uint32_t glog2, int gblocks, cudaStream_t st);
+cudaError_t launch_scan_counts(const uint32_t* cnt, uint64_t n, uint64_t* bsum, uint64_t* off, cudaStream_t st);
+
 }  // namespace ltlg

@@ -40,9 +40,15 @@ class LtlgError(RuntimeError):
         self.status = status
 
 
+class DomainError(ArithmeticError):
+    """The reference's std::domain_error (e.g. a trajectory leaving the workspace)."""
+
+
 def _raise(status: int, msg: str):
     if status == N.LTLG_EINVAL:
         raise ValueError(msg)
+    if status == N.LTLG_EDOMAIN:
+        raise DomainError(msg)
     if status in (N.LTLG_EFORMAT, N.LTLG_EIO):
         raise RuntimeError(msg)
     if status == N.LTLG_ENOMEM:
@@ -358,6 +364,10 @@ class LabelEngine:
             _raise(st, self._L.ltlg_last_error(self._h).decode())
 
     # -- load abstraction ---------------------------------------------------
+    def load_swept_volume(self, sv: "SweptVolume") -> None:
+        """ltlg_load_csr: the GPU-built swept-volume matrix as this engine's T."""
+        self._ck(self._L.ltlg_load_csr(self._h, sv._h))
+
     def load_abstraction(self, m: CsrBoolMatrix) -> None:
         off = np.ascontiguousarray(m.row_offsets, dtype=np.uint64)
         idx = np.ascontiguousarray(m.col_indices, dtype=np.uint32)
@@ -514,6 +524,94 @@ def rasterize_boxes(dims: int, depth: int, lo, hi, columns, device: int = 0) -> 
     if st:
         _raise(st, L.ltlg_last_error(None).decode())
     return out[: len(columns)]
+
+
+class FootprintSpec:
+    """Rectangular footprint (abstraction.hpp:58-62); defaults are the reference's."""
+
+    def __init__(self, length: float = 4.6, width: float = 2.0, ref_offset: float = -1.4):
+        self.length, self.width, self.ref_offset = float(length), float(width), float(ref_offset)
+
+
+def _trajectories(trajectories):
+    """(sample_offsets u64 [E+1], samples f64 [S, 5]) from either that pair or
+    a sequence of per-edge [n_i, 5] State5 arrays (px, py, heading, speed, tau)."""
+    if isinstance(trajectories, tuple) and len(trajectories) == 2:
+        off, smp = (np.asarray(x) for x in trajectories)
+        if off.ndim == 1 and smp.ndim == 2 and smp.shape[1] == 5:
+            return (np.ascontiguousarray(off, dtype=np.uint64),
+                    np.ascontiguousarray(smp, dtype=np.float64))
+    rows = [np.asarray(t, dtype=np.float64).reshape(-1, 5) for t in trajectories]
+    off = np.zeros(len(rows) + 1, dtype=np.uint64)
+    if rows:
+        off[1:] = np.cumsum([r.shape[0] for r in rows])
+    smp = np.ascontiguousarray(np.concatenate(rows) if rows else np.zeros((0, 5)), dtype=np.float64)
+    return off, smp
+
+
+class SweptVolume:
+    """Device-resident swept-volume matrix built by ltlg_swept_volume."""
+
+    def __init__(self, handle, lib):
+        self._h, self._L = handle, lib
+        self.rows = int(lib.ltlg_csr_rows(handle))
+        self.cols = int(lib.ltlg_csr_cols(handle))
+        self.nnz = int(lib.ltlg_csr_nnz(handle))
+        self.build_ms = float(lib.ltlg_csr_build_ms(handle))
+
+    def to_csr(self) -> CsrBoolMatrix:
+        off = np.zeros(self.rows + 1, dtype=np.uint64)
+        idx = np.zeros(max(self.nnz, 1), dtype=np.uint32)
+        st = self._L.ltlg_csr_copy(self._h, off.ctypes.data, idx.ctypes.data)
+        if st:
+            _raise(st, self._L.ltlg_last_error(None).decode())
+        return CsrBoolMatrix(self.rows, self.cols, off, idx[: self.nnz])
+
+    def close(self):
+        if self._h:
+            self._L.ltlg_csr_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def swept_volume(trajectories, footprint: Optional[FootprintSpec] = None, bounds=((0.0, 72.0), (0.0, 72.0), (0.0, 7.2)),
+                 depth: int = 18, device: int = 0) -> SweptVolume:
+    """GPU swept_volume_matrix (label.cpp:75-116), result left on the device."""
+    L = N.lib()
+    f = footprint or FootprintSpec()
+    lo = [b[0] for b in bounds]
+    hi = [b[1] for b in bounds]
+    g = _gridk(len(bounds), depth, lo, hi) if len(bounds) <= 4 else None
+    if g is None:
+        raise ValueError("at most 4 grid axes in this build")
+    off, smp = _trajectories(trajectories)
+    fp = N.Footprint(f.length, f.width, f.ref_offset)
+    h = C.c_void_p()
+    st = L.ltlg_swept_volume(C.byref(g), C.byref(fp), off.size - 1, off.ctypes.data, smp.ctypes.data if smp.size else None,
+                             device, C.byref(h))
+    if st:
+        _raise(st, L.ltlg_last_error(None).decode())
+    return SweptVolume(h.value, L)
+
+
+def swept_volume_matrix(trajectories, footprint: Optional[FootprintSpec] = None,
+                        bounds=((0.0, 72.0), (0.0, 72.0), (0.0, 7.2)), depth: int = 18, workers: int = 0,
+                        device: int = 0) -> CsrBoolMatrix:
+    """Drop-in for ltlgrid::swept_volume_matrix (label.cpp:75-116): one CSR row
+    per edge trajectory, the sorted z-order cells its footprint sweeps on the
+    (x, y, tau) grid GridSpec(bounds, depth).  Built on the B200; `workers`
+    is accepted for signature parity."""
+    del workers
+    sv = swept_volume(trajectories, footprint, bounds, depth, device)
+    try:
+        return sv.to_csr()
+    finally:
+        sv.close()
 
 
 def read_csb1_shape(path: str):
