@@ -1166,24 +1166,31 @@ struct ltlg_csr {
 namespace {
 
 struct SweepScratch {
-    DevBuf<uint64_t> off_in, bsum;
+    DevBuf<uint64_t> off_in, bsum, stage_off;
     DevBuf<double> samples;
-    DevBuf<uint32_t> row_cnt, over, ctr;
+    DevBuf<uint32_t> row_cnt, over, ctr, stage, gkeys;
     DevBuf<unsigned long long> err, gtab;
-    DevBuf<uint32_t> gkeys;
     ~SweepScratch() {
         off_in.release();
         bsum.release();
+        stage_off.release();
         samples.release();
         row_cnt.release();
         over.release();
         ctr.release();
+        stage.release();
+        gkeys.release();
         err.release();
         gtab.release();
-        gkeys.release();
     }
 };
 
+// Pass 1 rasterizes every edge once into shared-memory sets and stages the
+// sorted rows (bump allocator); the exclusive scan of the row sizes gives
+// the offsets and a gather moves the rows into place.  Rows past kSweepCap
+// distinct cells take global-memory sets (count, then fill after the scan).
+// If the staging buffer runs out, the rows are rasterized again straight
+// into place (MODE 1).
 ltlg_status sweep_build(const ltlg_gridk* g, const ltlg_footprint* f, uint64_t edges, const uint64_t* sample_off,
                         const double* samples, ltlg_csr* m) {
     using namespace ltlg;
@@ -1201,18 +1208,26 @@ ltlg_status sweep_build(const ltlg_gridk* g, const ltlg_footprint* f, uint64_t e
             for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
         }
     } ev_free{ev};
+    const uint64_t ne = std::max<uint64_t>(edges, 1);
+    // staging: ~8 distinct cells per sample covers the driving configurations
+    // with room to spare; a shortfall only costs the MODE 1 rerun
+    // (test knob LTLG_SWEEP_STAGE: the staging capacity in cells)
+    const char* stage_env = getenv("LTLG_SWEEP_STAGE");
+    const uint64_t stage_cap = stage_env ? std::strtoull(stage_env, nullptr, 10) : nsamp * 8 + (uint64_t(1) << 20);
     CK(s.off_in.reserve((edges + 1) * 8), "allocate sweep inputs");
     CK(s.samples.reserve(std::max<uint64_t>(nsamp, 1) * 40), "allocate sweep inputs");
-    CK(s.row_cnt.reserve(std::max<uint64_t>(edges, 1) * 4), "allocate sweep scratch");
-    CK(s.over.reserve(std::max<uint64_t>(edges, 1) * 4), "allocate sweep scratch");
+    CK(s.row_cnt.reserve(ne * 4), "allocate sweep scratch");
+    CK(s.over.reserve(ne * 4), "allocate sweep scratch");
+    CK(s.stage_off.reserve(ne * 8), "allocate sweep scratch");
+    CK(s.stage.reserve(stage_cap * 4), "allocate sweep scratch");
     CK(s.ctr.reserve(16), "allocate sweep scratch");
-    CK(s.err.reserve(16), "allocate sweep scratch");
+    CK(s.err.reserve(24), "allocate sweep scratch");
     CK(s.bsum.reserve(((edges + 1023) / 1024 + 1) * 8), "allocate sweep scratch");
     CK(m->off.reserve((edges + 1) * 8), "allocate CSR");
     CK(cudaMemcpyAsync(s.off_in.ptr, sample_off, (edges + 1) * 8, cudaMemcpyHostToDevice, st), "upload trajectories");
     if (nsamp) CK(cudaMemcpyAsync(s.samples.ptr, samples, nsamp * 40, cudaMemcpyHostToDevice, st), "upload trajectories");
-    const unsigned long long err_init[2] = {~0ull, 0ull};
-    CK(cudaMemcpyAsync(s.err.ptr, err_init, 16, cudaMemcpyHostToDevice, st), "upload");
+    const unsigned long long err_init[3] = {~0ull, 0ull, 0ull};
+    CK(cudaMemcpyAsync(s.err.ptr, err_init, 24, cudaMemcpyHostToDevice, st), "upload");
     CK(cudaMemsetAsync(s.ctr.ptr, 0, 16, st), "memset");
 
     SweepParams p{};
@@ -1232,61 +1247,69 @@ ltlg_status sweep_build(const ltlg_gridk* g, const ltlg_footprint* f, uint64_t e
     p.sample_off = s.off_in.ptr;
     p.samples = s.samples.ptr;
     p.err_key = s.err.ptr;
-    uint32_t* edge_ctr = s.ctr.ptr;
-    uint32_t* n_over = s.ctr.ptr + 1;
+    SweepBufs b{};
+    b.edge_ctr = s.ctr.ptr;
+    b.n_over = s.ctr.ptr + 1;
+    b.row_cnt = s.row_cnt.ptr;
+    b.over_list = s.over.ptr;
+    b.stage = s.stage.ptr;
+    b.stage_cap = stage_cap;
+    b.bump = s.err.ptr + 2;
+    b.stage_off = s.stage_off.ptr;
 
-    // pass 1: row sizes
+    // pass 1: rasterize + stage every row
     CK(cudaEventRecord(ev[0], st), "event");
-    if (edges) CK(launch_sweep(0, p, edge_ctr, s.row_cnt.ptr, nullptr, nullptr, s.over.ptr, n_over, nullptr, nullptr,
-                               0, 0, st), "sweep count kernel");
-    unsigned long long err[2];
+    if (edges) CK(launch_sweep(2, false, p, b, 0, 0, st), "sweep kernel");
+    unsigned long long err[3];
     uint32_t nov = 0;
-    CK(cudaMemcpyAsync(err, s.err.ptr, 16, cudaMemcpyDeviceToHost, st), "download");
-    CK(cudaMemcpyAsync(&nov, n_over, 4, cudaMemcpyDeviceToHost, st), "download");
+    CK(cudaMemcpyAsync(err, s.err.ptr, 24, cudaMemcpyDeviceToHost, st), "download");
+    CK(cudaMemcpyAsync(&nov, b.n_over, 4, cudaMemcpyDeviceToHost, st), "download");
     CK(cudaEventRecord(ev[1], st), "event");
-    CK(cudaStreamSynchronize(st), "sweep count");
+    CK(cudaStreamSynchronize(st), "sweep");
     if (err[0] != ~0ull) {
         static const char* const msg[3] = {"trajectory exits workspace (time axis)", "footprint must be positive",
                                            "trajectory exits workspace (position)"};
         const int kind = static_cast<int>(err[0] & 3);
         return set_err(nullptr, kind == 1 ? LTLG_EINVAL : LTLG_EDOMAIN, msg[kind]);
     }
+    const bool staged = err[2] <= stage_cap;
     // rows past kSweepCap distinct cells: global-memory sets, grown until they fit
+    CK(cudaEventRecord(ev[2], st), "event");
     uint32_t glog2 = 15;
     int gblocks = 0;
     while (nov) {
         gblocks = static_cast<int>(std::min<uint32_t>(nov, 148));
         CK(s.gtab.reserve((static_cast<size_t>(gblocks) << glog2) * 8), "allocate sweep overflow sets");
         CK(s.gkeys.reserve((static_cast<size_t>(gblocks) << (glog2 - 1)) * 4), "allocate sweep overflow sets");
-        CK(cudaMemsetAsync(edge_ctr, 0, 4, st), "memset");
+        b.gtab = s.gtab.ptr;
+        b.gkeys = s.gkeys.ptr;
         CK(cudaMemsetAsync(s.err.ptr + 1, 0, 8, st), "memset");
-        CK(launch_sweep(2, p, edge_ctr, s.row_cnt.ptr, nullptr, nullptr, s.over.ptr, n_over, s.gtab.ptr, s.gkeys.ptr,
-                        glog2, gblocks, st), "sweep overflow count kernel");
+        CK(launch_sweep(0, true, p, b, glog2, gblocks, st), "sweep overflow count kernel");
         CK(cudaMemcpyAsync(err, s.err.ptr, 16, cudaMemcpyDeviceToHost, st), "download");
         CK(cudaStreamSynchronize(st), "sweep overflow count");
         if (!err[1]) break;
         if (glog2 >= 30) return set_err(nullptr, LTLG_ENOMEM, "swept-volume row too large");
         glog2 += 2;
     }
-    // row offsets, pass 2: rows
-    CK(cudaEventRecord(ev[2], st), "event");
+    // row offsets; rows into place
     CK(launch_scan_counts(s.row_cnt.ptr, edges, s.bsum.ptr, m->off.ptr, st), "scan kernel");
     uint64_t nnz = 0;
     CK(cudaMemcpyAsync(&nnz, m->off.ptr + edges, 8, cudaMemcpyDeviceToHost, st), "download");
     CK(cudaStreamSynchronize(st), "scan");
     CK(m->idx.reserve(std::max<uint64_t>(nnz, 1) * 4), "allocate CSR");
-    if (edges)
-        CK(launch_sweep(1, p, edge_ctr, s.row_cnt.ptr, m->off.ptr, m->idx.ptr, s.over.ptr, n_over, nullptr, nullptr,
-                        0, 0, st), "sweep fill kernel");
-    if (nov)
-        CK(launch_sweep(3, p, edge_ctr, s.row_cnt.ptr, m->off.ptr, m->idx.ptr, s.over.ptr, n_over, s.gtab.ptr,
-                        s.gkeys.ptr, glog2, gblocks, st), "sweep overflow fill kernel");
+    b.row_off = m->off.ptr;
+    b.cols = m->idx.ptr;
+    if (edges) {
+        if (staged) CK(launch_sweep_gather(edges, b, st), "sweep gather kernel");
+        else CK(launch_sweep(1, false, p, b, 0, 0, st), "sweep fill kernel");
+    }
+    if (nov) CK(launch_sweep(1, true, p, b, glog2, gblocks, st), "sweep overflow fill kernel");
     CK(cudaEventRecord(ev[3], st), "event");
     CK(cudaStreamSynchronize(st), "sweep fill");
-    float a = 0, b = 0;
-    cudaEventElapsedTime(&a, ev[0], ev[1]);
-    cudaEventElapsedTime(&b, ev[2], ev[3]);
-    m->ms = static_cast<double>(a) + b;
+    float t01 = 0, t23 = 0;
+    cudaEventElapsedTime(&t01, ev[0], ev[1]);
+    cudaEventElapsedTime(&t23, ev[2], ev[3]);
+    m->ms = static_cast<double>(t01) + t23;
     m->rows = edges;
     m->cols = uint64_t(1) << g->depth;
     m->nnz = nnz;

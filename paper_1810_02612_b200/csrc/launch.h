@@ -72,7 +72,7 @@ cudaError_t launch_resample(int vdepth, double vlo0, double vhi0, double vlo1, d
 // swept-volume matrix (sweep.cu): 3-axis grid of depth <= 32, so every
 // z-order cell index fits in 32 bits
 constexpr int kSweepThreads = 128;
-constexpr uint32_t kSweepTable = 4096;             // shared-memory set slots per CTA
+constexpr uint32_t kSweepTable = 2048;             // shared-memory set slots per CTA
 constexpr uint32_t kSweepCap = kSweepTable / 2;    // distinct cells per row before overflow
 struct SweepParams {
     double lo[3], hi[3];
@@ -86,10 +86,24 @@ struct SweepParams {
     const double* samples;       // 5 doubles per State5
     unsigned long long* err_key; // [0] min(sample * 4 + kind), [1] global-table overflows
 };
+struct SweepBufs {
+    uint32_t* edge_ctr;
+    uint32_t* row_cnt;
+    const uint64_t* row_off;
+    uint32_t* cols;
+    uint32_t* over_list;
+    uint32_t* n_over;
+    unsigned long long* gtab;
+    uint32_t* gkeys;
+    uint32_t* stage;           // staged rows (MODE 2)
+    uint64_t stage_cap;
+    unsigned long long* bump;  // staging allocator
+    uint64_t* stage_off;       // per edge
+};
 size_t sweep_smem_bytes();
-cudaError_t launch_sweep(int mode, const SweepParams& p, uint32_t* edge_ctr, uint32_t* row_cnt, const uint64_t* row_off,
-                         uint32_t* cols, uint32_t* over_list, uint32_t* n_over, unsigned long long* gtab,
-                         uint32_t* gkeys, uint32_t glog2, int gblocks, cudaStream_t st);
+cudaError_t launch_sweep(int mode, bool global, const SweepParams& p, const SweepBufs& b, uint32_t glog2,
+                         int gblocks, cudaStream_t st);
+cudaError_t launch_sweep_gather(uint64_t edges, const SweepBufs& b, cudaStream_t st);
 cudaError_t launch_scan_counts(const uint32_t* cnt, uint64_t n, uint64_t* bsum, uint64_t* off, cudaStream_t st);
 
 }  // namespace ltlg

@@ -100,102 +100,137 @@ __device__ void bitonic_sort(uint32_t* k, uint32_t n2) {
 
 }  // namespace
 
-// FILL = false: row sizes into row_cnt; true: rows into cols at row_off.
+// MODE 0: row sizes into row_cnt.  MODE 1: rows into cols at row_off.
+// MODE 2: rows into the staging buffer at a bump-allocated position
+// (stage_off[e]; ~0 if the row overflowed or the buffer ran out), sizes
+// into row_cnt -- one rasterization pass instead of count + fill.
 // GLOBAL = false: every edge, shared-memory sets (an overflowing edge is
 // listed in over_list and skipped); true: the over_list edges, global-memory
 // sets of 2^glog2 entries per CTA (an overflow there bumps err_key[1] and the
 // host retries with a larger table).
-template <bool FILL, bool GLOBAL>
-__global__ void __launch_bounds__(kSweepThreads)
-    sweep_kernel(SweepParams p, uint32_t* __restrict__ edge_ctr, uint32_t* __restrict__ row_cnt,
-                 const uint64_t* __restrict__ row_off, uint32_t* __restrict__ cols, uint32_t* __restrict__ over_list,
-                 uint32_t* __restrict__ n_over, unsigned long long* __restrict__ gtab, uint32_t* __restrict__ gkeys,
-                 uint32_t glog2) {
+template <int MODE, bool GLOBAL>
+__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(SweepParams p, SweepBufs b, uint32_t glog2) {
     extern __shared__ unsigned long long smem_tab[];
     __shared__ uint32_t s_edge, s_cnt, s_pos, s_bad;
-    constexpr bool kGlobal = GLOBAL;
-    const uint32_t hsize = kGlobal ? (1u << glog2) : kSweepTable;
-    const uint32_t cap = kGlobal ? hsize / 2 : kSweepCap;
-    unsigned long long* tab = kGlobal ? gtab + static_cast<size_t>(blockIdx.x) * hsize : smem_tab;
-    uint32_t* keys = kGlobal ? gkeys + static_cast<size_t>(blockIdx.x) * (hsize / 2)
-                             : reinterpret_cast<uint32_t*>(smem_tab + kSweepTable);
+    __shared__ unsigned long long s_stage;
+    const uint32_t hsize = GLOBAL ? (1u << glog2) : kSweepTable;
+    const uint32_t cap = GLOBAL ? hsize / 2 : kSweepCap;
+    unsigned long long* tab = GLOBAL ? b.gtab + static_cast<size_t>(blockIdx.x) * hsize : smem_tab;
+    uint32_t* keys = GLOBAL ? b.gkeys + static_cast<size_t>(blockIdx.x) * (hsize / 2)
+                            : reinterpret_cast<uint32_t*>(smem_tab + kSweepTable);
     for (uint32_t i = threadIdx.x; i < hsize; i += blockDim.x) tab[i] = 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const double half_x = p.w[0] / 2, half_y = p.w[1] / 2;
     for (uint32_t epoch = 1;; ++epoch) {
         __syncthreads();
         if (threadIdx.x == 0) {
-            const uint32_t k = atomicAdd(edge_ctr, 1u);
-            s_edge = kGlobal ? (k < *n_over ? over_list[k] : 0xffffffffu) : k;
+            const uint32_t k = atomicAdd(b.edge_ctr, 1u);
+            s_edge = GLOBAL ? (k < *b.n_over ? b.over_list[k] : 0xffffffffu) : k;
             s_cnt = 0;
             s_pos = 0;
             s_bad = 0;
         }
         __syncthreads();
         const uint32_t e = s_edge;
-        if (kGlobal ? e == 0xffffffffu : e >= p.edges) break;
+        if (GLOBAL ? e == 0xffffffffu : e >= p.edges) break;
         const uint64_t sb = p.sample_off[e], se = p.sample_off[e + 1];
-        for (uint64_t i = sb + warp; i < se; i += nwarps) {
-            const double* s5 = p.samples + 5 * i;
-            const double px = s5[0], py = s5[1], heading = s5[2], tau = s5[4];
-            // sweep_collect (abstraction.cpp:180-199): the checks, in order
-            if (!(tau >= p.lo[2] && tau < p.hi[2])) {
-                if (lane == 0 && !FILL) atomicMin(p.err_key, static_cast<unsigned long long>(i) * 4 + 0);
-                continue;
+        const bool report = MODE == 2 || (MODE == 0 && !GLOBAL);
+        // warp `warp` owns samples sb + warp + k * nwarps; lane k sets up the
+        // k-th of a batch of 32 of them (footprint, checks, cell ranges), then
+        // the warp walks the batch, lanes over each sample's candidate cells
+        for (uint64_t base = sb + warp; base < se; base += 32ull * nwarps) {
+            const uint64_t i = base + static_cast<uint64_t>(lane) * nwarps;
+            const uint64_t left = (se - base + nwarps - 1) / nwarps;
+            const uint32_t nb = left < 32 ? static_cast<uint32_t>(left) : 32u;
+            uint32_t n = 0, ny = 1, ct_bits = 0;
+            int64_t x0 = 0, y0 = 0;
+            double rcx = 0, rcy = 0, cs = 0, sn = 0, sep_x = 0, sep_y = 0, sep_l = 0, sep_w = 0;
+            if (i < se) {
+                const double* s5 = p.samples + 5 * i;
+                const double px = s5[0], py = s5[1], heading = s5[2], tau = s5[4];
+                // sweep_collect (abstraction.cpp:180-199): the checks, in order
+                if (!(tau >= p.lo[2] && tau < p.hi[2])) {
+                    if (report) atomicMin(p.err_key, static_cast<unsigned long long>(i) * 4 + 0);
+                } else if (p.length <= 0 || p.width <= 0) {  // footprint_polygon's check
+                    if (report) atomicMin(p.err_key, static_cast<unsigned long long>(i) * 4 + 1);
+                } else {
+                    // GridSpec::quantize (grid.cpp:35-47) of tau
+                    uint64_t ct = static_cast<uint64_t>(floor((tau - p.lo[2]) / (p.hi[2] - p.lo[2]) * p.cells[2]));
+                    if (ct >= static_cast<uint64_t>(p.ncell[2])) ct = p.ncell[2] - 1;
+                    ct_bits = scatter3(p, 2, ct);
+                    sincos(heading, &sn, &cs);
+                    rcx = px + p.ref_offset * cs;
+                    rcy = py + p.ref_offset * sn;
+                    const double hl = p.length / 2, hw = p.width / 2;
+                    const double ac = fabs(cs), as = fabs(sn);
+                    const double ext_x = hl * ac + hw * as;
+                    const double ext_y = hl * as + hw * ac;
+                    if (rcx - ext_x < p.lo[0] || rcx + ext_x > p.hi[0] || rcy - ext_y < p.lo[1] ||
+                        rcy + ext_y > p.hi[1]) {
+                        if (report) atomicMin(p.err_key, static_cast<unsigned long long>(i) * 4 + 2);
+                    } else {
+                        int64_t x1, y1;
+                        overlap_cells(p, 0, rcx - ext_x, rcx + ext_x, x0, x1);
+                        overlap_cells(p, 1, rcy - ext_y, rcy + ext_y, y0, y1);
+                        if (x1 >= x0 && y1 >= y0) {
+                            ny = static_cast<uint32_t>(y1 - y0 + 1);
+                            n = static_cast<uint32_t>(x1 - x0 + 1) * ny;
+                        }
+                        // rect_cell_overlap's right-hand sides (abstraction.cpp:
+                        // 163-168): functions of the sample only, hoisted
+                        sep_x = half_x + hl * ac + hw * as;
+                        sep_y = half_y + hl * as + hw * ac;
+                        sep_l = hl + half_x * ac + half_y * as;
+                        sep_w = hw + half_x * as + half_y * ac;
+                    }
+                }
             }
-            // GridSpec::quantize (grid.cpp:35-47) of tau
-            uint64_t ct = static_cast<uint64_t>(floor((tau - p.lo[2]) / (p.hi[2] - p.lo[2]) * p.cells[2]));
-            if (ct >= static_cast<uint64_t>(p.ncell[2])) ct = p.ncell[2] - 1;
-            const uint32_t ct_bits = scatter3(p, 2, ct);
-            if (p.length <= 0 || p.width <= 0) {  // footprint_polygon's check
-                if (lane == 0 && !FILL) atomicMin(p.err_key, static_cast<unsigned long long>(i) * 4 + 1);
-                continue;
-            }
-            double sn, cs;
-            sincos(heading, &sn, &cs);
-            const double rcx = px + p.ref_offset * cs, rcy = py + p.ref_offset * sn;
-            const double hl = p.length / 2, hw = p.width / 2;
-            const double ac = fabs(cs), as = fabs(sn);
-            const double ext_x = hl * ac + hw * as;
-            const double ext_y = hl * as + hw * ac;
-            if (rcx - ext_x < p.lo[0] || rcx + ext_x > p.hi[0] || rcy - ext_y < p.lo[1] || rcy + ext_y > p.hi[1]) {
-                if (lane == 0 && !FILL) atomicMin(p.err_key, static_cast<unsigned long long>(i) * 4 + 2);
-                continue;
-            }
-            int64_t x0, x1, y0, y1;
-            overlap_cells(p, 0, rcx - ext_x, rcx + ext_x, x0, x1);
-            overlap_cells(p, 1, rcy - ext_y, rcy + ext_y, y0, y1);
-            if (x1 < x0 || y1 < y0) continue;
-            const uint32_t ny = static_cast<uint32_t>(y1 - y0 + 1);
-            const uint32_t n = static_cast<uint32_t>(x1 - x0 + 1) * ny;
-            for (uint32_t t = lane; t < n; t += 32) {
-                const int64_t cx = x0 + t / ny, cy = y0 + t % ny;
-                const double ccx = p.lo[0] + (static_cast<double>(cx) + 0.5) * p.w[0];
-                const double ccy = p.lo[1] + (static_cast<double>(cy) + 0.5) * p.w[1];
-                // rect_cell_overlap (abstraction.cpp:156-170)
-                const double dx = ccx - rcx, dy = ccy - rcy;
-                if (fabs(dx) >= half_x + hl * ac + hw * as) continue;
-                if (fabs(dy) >= half_y + hl * as + hw * ac) continue;
-                if (fabs(dx * cs + dy * sn) >= hl + half_x * ac + half_y * as) continue;
-                if (fabs(-dx * sn + dy * cs) >= hw + half_x * as + half_y * ac) continue;
-                const uint32_t key = scatter3(p, 0, static_cast<uint64_t>(cx)) |
-                                     scatter3(p, 1, static_cast<uint64_t>(cy)) | ct_bits;
-                if (!s_bad && !set_insert(tab, hsize - 1, epoch, key, &s_cnt, cap)) s_bad = 1;
+            for (uint32_t k = 0; k < nb; ++k) {
+                const uint32_t nk = __shfl_sync(0xffffffffu, n, k);
+                if (!nk) continue;
+                const uint32_t nyk = __shfl_sync(0xffffffffu, ny, k);
+                const uint32_t ctk = __shfl_sync(0xffffffffu, ct_bits, k);
+                const int64_t x0k = __shfl_sync(0xffffffffu, x0, k), y0k = __shfl_sync(0xffffffffu, y0, k);
+                const double rcxk = __shfl_sync(0xffffffffu, rcx, k), rcyk = __shfl_sync(0xffffffffu, rcy, k);
+                const double csk = __shfl_sync(0xffffffffu, cs, k), snk = __shfl_sync(0xffffffffu, sn, k);
+                const double sxk = __shfl_sync(0xffffffffu, sep_x, k), syk = __shfl_sync(0xffffffffu, sep_y, k);
+                const double slk = __shfl_sync(0xffffffffu, sep_l, k), swk = __shfl_sync(0xffffffffu, sep_w, k);
+                for (uint32_t t = lane; t < nk; t += 32) {
+                    const int64_t cx = x0k + t / nyk, cy = y0k + t % nyk;
+                    const double ccx = p.lo[0] + (static_cast<double>(cx) + 0.5) * p.w[0];
+                    const double ccy = p.lo[1] + (static_cast<double>(cy) + 0.5) * p.w[1];
+                    // rect_cell_overlap (abstraction.cpp:156-170)
+                    const double dx = ccx - rcxk, dy = ccy - rcyk;
+                    if (fabs(dx) >= sxk) continue;
+                    if (fabs(dy) >= syk) continue;
+                    if (fabs(dx * csk + dy * snk) >= slk) continue;
+                    if (fabs(-dx * snk + dy * csk) >= swk) continue;
+                    const uint32_t key = scatter3(p, 0, static_cast<uint64_t>(cx)) |
+                                         scatter3(p, 1, static_cast<uint64_t>(cy)) | ctk;
+                    if (!s_bad && !set_insert(tab, hsize - 1, epoch, key, &s_cnt, cap)) s_bad = 1;
+                }
             }
         }
         __syncthreads();
         const uint32_t cnt = s_cnt;
-        if (!FILL) {
+        if (MODE == 0) {
             if (threadIdx.x == 0) {
-                row_cnt[e] = s_bad ? 0u : cnt;
+                b.row_cnt[e] = s_bad ? 0u : cnt;
                 if (s_bad) {
                     if (GLOBAL) atomicAdd(p.err_key + 1, 1ull);  // retry with a larger table
-                    else over_list[atomicAdd(n_over, 1u)] = e;
+                    else b.over_list[atomicAdd(b.n_over, 1u)] = e;
                 }
             }
             continue;
         }
-        if (s_bad) continue;  // shared-memory fill: a listed overflow edge
+        if (s_bad) {  // listed for the global-memory sets (MODE 2), or already listed (MODE 1)
+            if (MODE == 2 && threadIdx.x == 0) {
+                b.row_cnt[e] = 0;
+                b.stage_off[e] = ~0ull;
+                b.over_list[atomicAdd(b.n_over, 1u)] = e;
+            }
+            continue;
+        }
         // compact this edge's keys, sort them, write the row (sweep_voxelize_indices'
         // sort + unique, abstraction.cpp:214-221)
         for (uint32_t i = threadIdx.x; i < hsize; i += blockDim.x) {
@@ -204,12 +239,37 @@ __global__ void __launch_bounds__(kSweepThreads)
         }
         uint32_t n2 = 1;
         while (n2 < cnt) n2 <<= 1;
+        if (MODE == 2 && threadIdx.x == 0) {
+            const unsigned long long pos = atomicAdd(b.bump, static_cast<unsigned long long>(cnt));
+            s_stage = pos + cnt <= b.stage_cap ? pos : ~0ull;
+            b.row_cnt[e] = cnt;
+            b.stage_off[e] = s_stage;
+        }
         __syncthreads();
         for (uint32_t i = cnt + threadIdx.x; i < n2; i += blockDim.x) keys[i] = 0xffffffffu;
         __syncthreads();
         if (cnt > 1) bitonic_sort(keys, n2);
-        uint32_t* out = cols + row_off[e];
+        if (MODE == 2 && s_stage == ~0ull) continue;  // staging buffer full: the host reruns MODE 1
+        uint32_t* out = MODE == 2 ? b.stage + s_stage : b.cols + b.row_off[e];
         for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) out[i] = keys[i];
+    }
+}
+
+// staged rows -> their CSR positions (one warp per edge)
+__global__ void __launch_bounds__(256) sweep_gather_kernel(uint64_t edges, const uint32_t* __restrict__ row_cnt,
+                                                            const uint64_t* __restrict__ stage_off,
+                                                            const uint32_t* __restrict__ stage,
+                                                            const uint64_t* __restrict__ row_off,
+                                                            uint32_t* __restrict__ cols) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); e < edges; e += nw) {
+        const uint64_t so = stage_off[e];
+        if (so == ~0ull) continue;  // an overflow row: written by the global-memory pass
+        const uint32_t n = row_cnt[e];
+        const uint32_t* src = stage + so;
+        uint32_t* dst = cols + row_off[e];
+        for (uint32_t i = lane; i < n; i += 32) dst[i] = src[i];
     }
 }
 
@@ -280,23 +340,20 @@ __global__ void __launch_bounds__(1024) scan_apply(const uint32_t* __restrict__ 
 
 size_t sweep_smem_bytes() { return kSweepTable * sizeof(unsigned long long) + kSweepCap * sizeof(uint32_t); }
 
-cudaError_t launch_sweep(int mode, const SweepParams& p, uint32_t* edge_ctr, uint32_t* row_cnt, const uint64_t* row_off,
-                         uint32_t* cols, uint32_t* over_list, uint32_t* n_over, unsigned long long* gtab,
-                         uint32_t* gkeys, uint32_t glog2, int gblocks, cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(edge_ctr, 0, sizeof(uint32_t), st);
+cudaError_t launch_sweep(int mode, bool global, const SweepParams& p, const SweepBufs& b, uint32_t glog2,
+                         int gblocks, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(b.edge_ctr, 0, sizeof(uint32_t), st);
     if (e != cudaSuccess) return e;
+    if (global) {
+        auto gk = mode == 1 ? sweep_kernel<1, true> : sweep_kernel<0, true>;
+        gk<<<gblocks, kSweepThreads, 0, st>>>(p, b, glog2);
+        return cudaGetLastError();
+    }
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // mode bit 0: fill, bit 1: global-memory sets over the overflow list
-    if (mode & 2) {
-        auto gk = (mode & 1) ? sweep_kernel<true, true> : sweep_kernel<false, true>;
-        gk<<<gblocks, kSweepThreads, 0, st>>>(p, edge_ctr, row_cnt, row_off, cols, over_list, n_over, gtab, gkeys,
-                                             glog2);
-        return cudaGetLastError();
-    }
     const size_t smem = sweep_smem_bytes();
-    auto kern = (mode & 1) ? sweep_kernel<true, false> : sweep_kernel<false, false>;
+    auto kern = mode == 2 ? sweep_kernel<2, false> : mode == 1 ? sweep_kernel<1, false> : sweep_kernel<0, false>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -304,8 +361,18 @@ cudaError_t launch_sweep(int mode, const SweepParams& p, uint32_t* edge_ctr, uin
     if (per_sm <= 0) per_sm = 1;
     uint64_t blocks = static_cast<uint64_t>(sms) * per_sm;
     if (blocks > p.edges) blocks = p.edges ? p.edges : 1;
-    kern<<<static_cast<unsigned>(blocks), kSweepThreads, smem, st>>>(p, edge_ctr, row_cnt, row_off, cols, over_list,
-                                                                     n_over, gtab, gkeys, glog2);
+    kern<<<static_cast<unsigned>(blocks), kSweepThreads, smem, st>>>(p, b, glog2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_gather(uint64_t edges, const SweepBufs& b, cudaStream_t st) {
+    if (!edges) return cudaSuccess;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (edges + 7) / 8;
+    const unsigned blocks = static_cast<unsigned>(want < static_cast<uint64_t>(sms) * 8 ? want : sms * 8);
+    sweep_gather_kernel<<<blocks, 256, 0, st>>>(edges, b.row_cnt, b.stage_off, b.stage, b.row_off, b.cols);
     return cudaGetLastError();
 }
 

@@ -63,6 +63,16 @@ def test_sweep_overflow_rows_vs_oracle(oracle):
         _same(_gpu(off, smp, depth, lo, hi, fp), want)
 
 
+@pytest.mark.parametrize("stage", ["0", "5000"])
+def test_sweep_staging_shortfall_vs_oracle(oracle, monkeypatch, stage):
+    """A staging buffer too small for the rows: the rows are rasterized again
+    straight into place (MODE 1); overflow rows still take the global sets."""
+    monkeypatch.setenv("LTLG_SWEEP_STAGE", stage)
+    off, smp = random_motions(41, 300, empty_every=5)
+    for depth in (15, 24):
+        _same(_gpu(off, smp, depth), oracle.swept_volume(depth, (0, 0, 0), (64, 64, 4), FOOTPRINT, off, smp))
+
+
 def test_sweep_empty_inputs():
     off, smp = flatten([])
     rows, cols = _gpu(off, smp, 12)

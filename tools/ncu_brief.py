@@ -27,8 +27,8 @@ for r in src[2:]:
     for k in hs:
         if k.startswith("stall_") and "Not Issued" not in k:
             try:
-                c[k[6:]] += float(d[k])
-            except ValueError:
+                c[k[6:]] += float(d.get(k, 0) or 0)
+            except (ValueError, TypeError):
                 pass
 t = sum(c.values())
 print("  stalls: " + " ".join(f"{k}={100 * v / t:.1f}%" for k, v in c.most_common(9)))
