@@ -20,6 +20,8 @@
 #include <string>
 #include <vector>
 
+#include "ltlgrid/abstraction.hpp"  // TransitionSystem / FootprintSpec (swept_volume_matrix)
+#include "ltlgrid/grid.hpp"
 #include "ltlgrid/label.hpp"  // the reference's CsrBoolMatrix / DensePropMatrix / LabelMatrix
 #include "ltlgrid_gpu.h"
 
@@ -28,6 +30,7 @@ namespace gpu {
 
 [[noreturn]] inline void throw_status(ltlg_status s, const char* msg) {
     if (s == LTLG_EINVAL) throw std::invalid_argument(msg);
+    if (s == LTLG_EDOMAIN) throw std::domain_error(msg);
     if (s == LTLG_ENOMEM) throw std::bad_alloc();
     throw std::runtime_error(msg);
 }
@@ -113,6 +116,41 @@ inline LabelMatrix label_all(const CsrBoolMatrix& m, const DensePropMatrix& p, i
                        w.empty() ? nullptr : w.data(), workers, words.empty() ? nullptr : words.data());
     if (s != LTLG_OK) throw_status(s, ltlg_last_error(nullptr));
     return to_label_matrix<LabelMatrix>(m.rows, p.num_props(), words);
+}
+
+// Drop-in for ltlgrid::swept_volume_matrix (label.hpp:42-43, label.cpp:75-116):
+// the same CSR, built on the GPU; same exception types and messages.
+inline CsrBoolMatrix swept_volume_matrix(const TransitionSystem& s, const FootprintSpec& f, const GridSpec& g,
+                                         int workers = 0, int device = 0) {
+    (void)workers;
+    ltlg_gridk grid{};
+    grid.dims = g.dims();
+    grid.depth = g.depth();
+    for (int a = 0; a < g.dims() && a < 4; ++a) {
+        grid.lo[a] = g.lower(a);
+        grid.hi[a] = g.upper(a);
+    }
+    std::vector<std::uint64_t> off(s.num_edges() + 1, 0);
+    std::vector<double> samples;
+    for (std::size_t e = 0; e < s.num_edges(); ++e) {
+        for (const State5& x : s.trajectories[e].samples)
+            samples.insert(samples.end(), {x.px, x.py, x.heading, x.speed, x.tau});
+        off[e + 1] = samples.size() / 5;
+    }
+    const ltlg_footprint fp{f.length, f.width, f.ref_offset};
+    ltlg_csr* m = nullptr;
+    const ltlg_status st = ltlg_swept_volume(&grid, &fp, s.num_edges(), off.data(),
+                                             samples.empty() ? nullptr : samples.data(), device, &m);
+    if (st != LTLG_OK) throw_status(st, ltlg_last_error(nullptr));
+    CsrBoolMatrix out;
+    out.rows = ltlg_csr_rows(m);
+    out.cols = ltlg_csr_cols(m);
+    out.row_offsets.resize(out.rows + 1);
+    out.col_indices.resize(ltlg_csr_nnz(m));
+    const ltlg_status cs = ltlg_csr_copy(m, out.row_offsets.data(), out.col_indices.data());
+    ltlg_csr_free(m);
+    if (cs != LTLG_OK) throw_status(cs, ltlg_last_error(nullptr));
+    return out;
 }
 
 }  // namespace gpu

@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "ltlgrid/abstraction.hpp"
 #include "ltlgrid/label.hpp"
 #include "ltlgrid/rng.hpp"
 #include "ltlgrid_gpu.hpp"
@@ -89,6 +90,51 @@ int main() {
             eng.submit(p);
             expect(eng.labels<LabelMatrix>() == label_all(csr, p), "engine frame " + std::to_string(f));
         }
+    }
+    // swept_volume_matrix (label.cpp:75-116) vs ltlgrid::gpu::swept_volume_matrix on the
+    // reference's own build_abstraction output (test_label.cpp:212-235 configuration)
+    {
+        AbstractionConfig cfg;
+        cfg.region = SampleRegion::Rect;
+        cfg.x_min = 0;
+        cfg.x_max = 64;
+        cfg.y_min = 0;
+        cfg.y_max = 64;
+        cfg.speed_min = 4;
+        cfg.speed_max = 8;
+        cfg.tau_min = 0.2;
+        cfg.tau_max = 2.5;
+        cfg.tau_limit = 3.9;
+        for (std::uint64_t target : {50ull, 1500ull}) {
+            cfg.target_edges = target;
+            auto ts = build_abstraction(cfg, 17);
+            for (int depth : {9, 12, 18, 24}) {
+                GridSpec g({{0.0, 64.0}, {0.0, 64.0}, {0.0, 4.0}}, depth);
+                auto want = swept_volume_matrix(ts, cfg.footprint, g, 2);
+                auto got = gpu::swept_volume_matrix(ts, cfg.footprint, g, 2);
+                expect(got.rows == want.rows && got.cols == want.cols && got.row_offsets == want.row_offsets &&
+                           got.col_indices == want.col_indices,
+                       "swept_volume_matrix " + std::to_string(ts.num_edges()) + " edges, depth " +
+                           std::to_string(depth));
+            }
+        }
+        TransitionSystem bad;
+        bad.trajectories.resize(1);
+        bad.edges.resize(1);
+        bad.trajectories[0].samples = {State5{9.8, 5, 0, 0, 0.5}};
+        GridSpec g({{0.0, 10.0}, {0.0, 10.0}, {0.0, 1.0}}, 9);
+        std::string a, b;
+        try {
+            swept_volume_matrix(bad, FootprintSpec{2.0, 1.0, 0.0}, g, 1);
+        } catch (const std::domain_error& e) {
+            a = e.what();
+        }
+        try {
+            gpu::swept_volume_matrix(bad, FootprintSpec{2.0, 1.0, 0.0}, g, 1);
+        } catch (const std::domain_error& e) {
+            b = e.what();
+        }
+        expect(!a.empty() && a == b, "swept_volume_matrix leaving the workspace -> std::domain_error, same message");
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "PASSED", failures);
     return failures ? 1 : 0;
