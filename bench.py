@@ -325,7 +325,7 @@ def main():
         n_frames = 30 if args.quick else 150
         frames3 = torch.empty((n_frames + 1, CFG3_PROPS, nw), dtype=torch.int64, pin_memory=True)
         props_words(SEED_P + 3, depth, CFG3_PROPS, 0, n_frames + 1, out=frames3)
-        label3 = []
+        label3, stages3 = [], []
         for q in range(-1, n_frames):  # query -1 is the warm-up (scenario.cpp:183-193)
             src3 = frames3[q + 1]
             t0 = time.perf_counter()
@@ -334,14 +334,20 @@ def main():
             dt = time.perf_counter() - t0
             if q >= 0:
                 eng_lat.append(dt * 1e3)
-                label3.append(eng.stage_times(0, 0)[2])
+                st3 = eng.stage_times(0, 0)
+                label3.append(st3[2])
+                stages3.append(st3)
         del P3
         k3 = statistics.median(label3)
         alg3 = 8 * int(info.words) + 4 * (rows_local + 1) + cells * CFG3_PROPS // 8 + rows_local * 2
         lat = {"config": "config3-large-abstraction: 2M edges, 512x512, 16 props, 1 frame",
                "p50_ms": statistics.median(eng_lat), "p99_ms": sorted(eng_lat)[int(0.99 * (len(eng_lat) - 1))],
                "frames": n_frames, "what": "pinned host P -> labels resident in HBM (host steady clock)",
-               "kernel_p50_ms": k3, "roofline": {"bound": "hbm", "achieved": alg3 / (k3 / 1e3) / 1e9, "peak": hbm,
+               "kernel_p50_ms": k3,
+               "stages_p50_ms": {"upload": statistics.median(x[0] for x in stages3),
+                                 "summary": statistics.median(x[1] for x in stages3),
+                                 "label": k3},
+               "roofline": {"bound": "hbm", "achieved": alg3 / (k3 / 1e3) / 1e9, "peak": hbm,
                                                 "unit": "GB/s", "frac": alg3 / (k3 / 1e3) / 1e9 / hbm,
                                                 "alg_bytes_per_launch": alg3,
                                                 "traffic": ncu_traffic("label_stream64_kernel"),

@@ -287,59 +287,82 @@ __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restri
                                                         uint64_t cells, uint8_t* __restrict__ tab,
                                                         void* __restrict__ s_only_g, uint32_t* __restrict__ task_ctr,
                                                         int nctr) {
+    // CTA = 32 consecutive words x 8 warps: warp g reads props g, g+8, ...
+    // (coalesced 256-B rows of P), lane = word; the eight partial masks meet
+    // in shared memory and warp 0 assembles the entries (first <= 2 / 4
+    // partial props in prop order, as before)
     using LW = typename Fmt<FMT>::LW;
-    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w < static_cast<uint32_t>(nctr)) task_ctr[w] = 0;  // the labeling launches that follow pull from 0
-    if (w > nw64) return;
-    LW s = 0, full = 0;
-    uint32_t ia = 0, ib = 0, ic = 0, id = 0;
-    uint64_t pa = 0, pb = 0, pc = 0, pd = 0;
-    int np = 0;
+    __shared__ uint64_t s_pv[64][32];              // P value of (prop, word) when partial
+    __shared__ uint64_t s_any[8][32], s_full[8][32], s_part[8][32];
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < static_cast<uint32_t>(nctr)) task_ctr[t] = 0;  // the labeling launches that follow pull from 0
+    const uint32_t w = blockIdx.x * 32 + lane;
+    uint64_t any = 0, full = 0, part = 0;
     const uint64_t lo = static_cast<uint64_t>(w) * 64;
     if (w < nw64 && lo < cells) {
         const uint64_t valid = (cells - lo >= 64) ? ~0ull : ((1ull << (cells - lo)) - 1ull);
-#pragma unroll 4
-        for (int j = 0; j < props; ++j) {
-            const uint64_t x = P64[static_cast<uint64_t>(j) * nw64 + w] & valid;
-            s |= LW(x != 0) << j;
-            full |= LW(x == valid) << j;
-            if (x != 0 && x != valid) {
-                if (np == 0) {
-                    pa = x;
-                    ia = static_cast<uint32_t>(j);
-                } else if (np == 1) {
-                    pb = x;
-                    ib = static_cast<uint32_t>(j);
-                } else if (np == 2) {
-                    pc = x;
-                    ic = static_cast<uint32_t>(j);
-                } else if (np == 3) {
-                    pd = x;
-                    id = static_cast<uint32_t>(j);
-                }
-                ++np;
+        uint64_t x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // all loads in flight before any use
+            const int j = g + 8 * k;
+            x[k] = j < props ? __ldg(P64 + static_cast<uint64_t>(j) * nw64 + w) & valid : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int j = g + 8 * k;
+            any |= static_cast<uint64_t>(x[k] != 0) << j;
+            full |= static_cast<uint64_t>(j < props && x[k] == valid) << j;
+            if (x[k] != 0 && x[k] != valid) {
+                part |= 1ull << j;
+                s_pv[j][lane] = x[k];
             }
         }
     }
-    const uint32_t over = np > (FMT == 64 ? 4 : 2) ? 1u : 0u, part = np > 0 ? 1u : 0u;
-    if constexpr (FMT == 16)
-        reinterpret_cast<uint32_t*>(tab)[w] =
-            (static_cast<uint32_t>(full) << 16) | (16u + ia) | ((16u + ib) << 5) | (part << 10) | (over << 11);
-    else if constexpr (FMT == 32)
-        reinterpret_cast<uint2*>(tab)[w] = make_uint2(static_cast<uint32_t>(full), ia | (ib << 8) | (part << 16) | (over << 17));
-    else {
-        reinterpret_cast<uint64_t*>(tab)[w] = static_cast<uint64_t>(full);
-        reinterpret_cast<uint32_t*>(tab + split64_meta_offset(nw64))[w] =
-            ia | (ib << 6) | (ic << 12) | (id << 18) | (part << 24) | (over << 25);
+    s_any[g][lane] = any;
+    s_full[g][lane] = full;
+    s_part[g][lane] = part;
+    __syncthreads();
+    if (g != 0 || w > nw64) return;
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+        any |= s_any[k][lane];
+        full |= s_full[k][lane];
+        part |= s_part[k][lane];
     }
-    uint4* x = reinterpret_cast<uint4*>(tab + split64_x_offset(FMT, nw64));
+    uint32_t ix[4] = {0, 0, 0, 0};
+    uint64_t pv[4] = {0, 0, 0, 0};
+    const int np = __popcll(part);
+    uint64_t rest = part;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (rest) {
+            ix[k] = static_cast<uint32_t>(__ffsll(static_cast<long long>(rest)) - 1);
+            pv[k] = s_pv[ix[k]][lane];
+            rest &= rest - 1;
+        }
+    }
+    const uint32_t over = np > (FMT == 64 ? 4 : 2) ? 1u : 0u, haspart = np > 0 ? 1u : 0u;
+    const LW sm = static_cast<LW>(any), fm = static_cast<LW>(full);
+    if constexpr (FMT == 16)
+        reinterpret_cast<uint32_t*>(tab)[w] = (static_cast<uint32_t>(fm) << 16) | (16u + ix[0]) | ((16u + ix[1]) << 5) |
+                                              (haspart << 10) | (over << 11);
+    else if constexpr (FMT == 32)
+        reinterpret_cast<uint2*>(tab)[w] =
+            make_uint2(static_cast<uint32_t>(fm), ix[0] | (ix[1] << 8) | (haspart << 16) | (over << 17));
+    else {
+        reinterpret_cast<uint64_t*>(tab)[w] = static_cast<uint64_t>(fm);
+        reinterpret_cast<uint32_t*>(tab + split64_meta_offset(nw64))[w] =
+            ix[0] | (ix[1] << 6) | (ix[2] << 12) | (ix[3] << 18) | (haspart << 24) | (over << 25);
+    }
+    uint4* xo = reinterpret_cast<uint4*>(tab + split64_x_offset(FMT, nw64));
     const uint32_t xs = split64_x_bytes(FMT) / 16;
-    x[xs * w] = make_uint4(static_cast<uint32_t>(pa), static_cast<uint32_t>(pa >> 32), static_cast<uint32_t>(pb),
-                           static_cast<uint32_t>(pb >> 32));
+    xo[xs * w] = make_uint4(static_cast<uint32_t>(pv[0]), static_cast<uint32_t>(pv[0] >> 32),
+                            static_cast<uint32_t>(pv[1]), static_cast<uint32_t>(pv[1] >> 32));
     if (xs == 2)
-        x[xs * w + 1] = make_uint4(static_cast<uint32_t>(pc), static_cast<uint32_t>(pc >> 32), static_cast<uint32_t>(pd),
-                                   static_cast<uint32_t>(pd >> 32));
-    static_cast<LW*>(s_only_g)[w] = s;
+        xo[xs * w + 1] = make_uint4(static_cast<uint32_t>(pv[2]), static_cast<uint32_t>(pv[2] >> 32),
+                                    static_cast<uint32_t>(pv[3]), static_cast<uint32_t>(pv[3] >> 32));
+    static_cast<LW*>(s_only_g)[w] = sm;
 }
 
 // Multi-frame summary over 64-cell words, thread per (word, frame), index
@@ -1415,8 +1438,10 @@ cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t 
 
 cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
                              uint32_t* task_ctr, int nctr, cudaStream_t st) {
-    const uint32_t nthreads = nw64 + 1 > static_cast<uint32_t>(nctr) ? nw64 + 1 : static_cast<uint32_t>(nctr);
-    const unsigned grid = (nthreads + 255) / 256;
+    // 32 words per CTA (word nw64 is the zero sentinel entry); enough CTAs to
+    // reset the nctr task counters too
+    const uint32_t nblk_w = (nw64 + 1 + 31) / 32, nblk_c = (static_cast<uint32_t>(nctr) + 255) / 256;
+    const unsigned grid = nblk_w > nblk_c ? nblk_w : nblk_c;
     switch (entry_format(props)) {
         case 16: summary64_kernel<16><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr); break;
         case 32: summary64_kernel<32><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr); break;
