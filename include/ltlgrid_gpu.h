@@ -115,7 +115,10 @@ ltlg_status ltlg_load_abstraction_words(ltlg_ctx* ctx, uint64_t rows, uint64_t c
  * column_words: frames x num_props x ceil(cells/64) u64, i.e. `frames`
  * DensePropMatrix column sets back to back.  Requires cells == cols of T
  * (else LTLG_EINVAL "dimension mismatch: ..."), 0 <= num_props <= 64.
- * Asynchronous: returns after enqueueing the upload and the kernels. */
+ * Asynchronous: returns after enqueueing the upload and the kernels.  A
+ * pageable column_words may be reused at once; a pinned (page-locked) one
+ * must stay unmodified until ltlg_wait, as with cudaMemcpyAsync (one frame
+ * on one device reads it in place through the host mapping). */
 ltlg_status ltlg_submit_grid(ltlg_ctx* ctx, uint64_t cells, int num_props,
                              const uint64_t* column_words, int frames);
 

@@ -108,6 +108,9 @@ struct Shard {
     DevBuf<uint64_t> tpair_s, tpair_b;
     DevBuf<uint64_t> P;  // frames x props x nw64
     const uint64_t* P_in = nullptr;  // caller's device P used in place (single device)
+    // caller's pinned host P, device-mapped: the single-frame summary kernel
+    // reads it over PCIe and writes the device copy as it goes (no separate H2D)
+    const uint64_t* P_host = nullptr;
     const uint64_t* Pdev() const { return P_in ? P_in : P.ptr; }
     DevBuf<uint8_t> sf;
     DevBuf<uint8_t> labels;
@@ -353,7 +356,7 @@ ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
     const size_t pw = static_cast<size_t>(props) * nw64;  // u64 words of one frame's P
     for (int f = 0; f < frames; ++f) {
         CK(launch_summary64(s.Pdev() + f * pw, props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr, s.ctr.ptr,
-                            static_cast<int>(kCtrStride), s.stream),
+                            static_cast<int>(kCtrStride), s.stream, nullptr),
            "summary kernel");
         if (prof && f == 0) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
@@ -409,6 +412,12 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // 64-cell-word single-frame path (dev knob LTLG_STREAM64=0 selects the 32-cell copy for A/B runs)
         static const bool wide_ok = !getenv("LTLG_STREAM64") || atoi(getenv("LTLG_STREAM64")) != 0;
         const bool wide = wide_ok && frames == 1;
+        if (s.P_host && !wide) {  // the fused upload only exists on the single-frame 64-cell path
+            CK(cudaMemcpyAsync(s.P.ptr, s.P_host, static_cast<size_t>(frames) * props * nw64 * 8,
+                               cudaMemcpyHostToDevice, s.stream),
+               "upload P");
+            s.P_host = nullptr;
+        }
         // Few frames: the frame-per-lane multi-frame kernel would leave most
         // lanes idle (its cost is ~flat for frames <= 32), so label frame by
         // frame with the single-frame kernel, each launch writing one column
@@ -436,7 +445,8 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
         const int nctr = static_cast<int>((s.block_row.size() - 1) * kCtrStride);
         if (wide)
-            CK(launch_summary64(s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr, s.ctr.ptr, nctr, s.stream),
+            CK(launch_summary64(s.P_host ? s.P_host : s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr,
+                                s.ctr.ptr, nctr, s.stream, s.P_host ? s.P.ptr : nullptr),
                "summary kernel");
         else if (pl)
             CK(launch_pl(s.Pdev(), props, frames, nw64, ctx->cells, s.sf.ptr, s.sf.bytes, s.ctr.ptr, nctr, s.stream),
@@ -525,7 +535,20 @@ ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t*
     CK(cudaSetDevice(s0.device), "cudaSetDevice");
     if (ctx->opts.profile) CK(cudaEventRecord(s0.ev[0], s0.stream), "event");
     s0.P_in = in_place ? words : nullptr;
-    if (nwords && !in_place)
+    s0.P_host = nullptr;
+    // One frame from pinned host memory on one device: no copy-engine upload;
+    // the summary kernel reads P through the mapping and writes the device
+    // copy (dev knob LTLG_FUSED_UPLOAD=0 restores the cudaMemcpyAsync).
+    static const bool fuse_ok = !getenv("LTLG_FUSED_UPLOAD") || atoi(getenv("LTLG_FUSED_UPLOAD")) != 0;
+    if (fuse_ok && nwords && !on_device && frames == 1 && num_props <= 64 && ctx->shards.size() == 1) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, words) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer &&
+            static_cast<const uint64_t*>(pa.hostPointer) == words)
+            s0.P_host = static_cast<const uint64_t*>(pa.devicePointer);
+        else
+            cudaGetLastError();  // pageable memory: not an error, just no mapping
+    }
+    if (nwords && !in_place && !s0.P_host)
         CK(cudaMemcpyAsync(s0.P.ptr, words, nwords * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                            s0.stream),
            "upload P");

@@ -282,11 +282,19 @@ __global__ void __launch_bounds__(256) summary_kernel(const uint32_t* __restrict
 
 // Single-frame summary over 64-cell words (P's own u64 column words): the
 // split table of split64_x_offset + S per word.  Thread per word.
+// P may be host memory read through the mapping: a plain global load (the
+// read-only path is only a hint, but keep mapped reads on the ordinary path)
+__device__ __forceinline__ uint64_t ld_nc_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
 template <int FMT>
 __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restrict__ P64, int props, uint32_t nw64,
                                                         uint64_t cells, uint8_t* __restrict__ tab,
                                                         void* __restrict__ s_only_g, uint32_t* __restrict__ task_ctr,
-                                                        int nctr) {
+                                                        int nctr, uint64_t* __restrict__ P_copy) {
     // CTA = 32 consecutive words x 8 warps: warp g reads props g, g+8, ...
     // (coalesced 256-B rows of P), lane = word; the eight partial masks meet
     // in shared memory and warp 0 assembles the entries (first <= 2 / 4
@@ -306,8 +314,15 @@ __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restri
 #pragma unroll
         for (int k = 0; k < 8; ++k) {  // all loads in flight before any use
             const int j = g + 8 * k;
-            x[k] = j < props ? __ldg(P64 + static_cast<uint64_t>(j) * nw64 + w) & valid : 0;
+            x[k] = j < props ? ld_nc_u64(P64 + static_cast<uint64_t>(j) * nw64 + w) : 0;
         }
+        if (P_copy) {  // P arrived through the host mapping: keep the device copy
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (g + 8 * k < props) P_copy[static_cast<uint64_t>(g + 8 * k) * nw64 + w] = x[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] &= valid;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int j = g + 8 * k;
@@ -1437,15 +1452,15 @@ cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t 
 }
 
 cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
-                             uint32_t* task_ctr, int nctr, cudaStream_t st) {
+                             uint32_t* task_ctr, int nctr, cudaStream_t st, uint64_t* P_copy) {
     // 32 words per CTA (word nw64 is the zero sentinel entry); enough CTAs to
     // reset the nctr task counters too
     const uint32_t nblk_w = (nw64 + 1 + 31) / 32, nblk_c = (static_cast<uint32_t>(nctr) + 255) / 256;
     const unsigned grid = nblk_w > nblk_c ? nblk_w : nblk_c;
     switch (entry_format(props)) {
-        case 16: summary64_kernel<16><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr); break;
-        case 32: summary64_kernel<32><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr); break;
-        default: summary64_kernel<64><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr); break;
+        case 16: summary64_kernel<16><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr, P_copy); break;
+        case 32: summary64_kernel<32><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr, P_copy); break;
+        default: summary64_kernel<64><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr, P_copy); break;
     }
     return cudaGetLastError();
 }
