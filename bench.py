@@ -326,6 +326,9 @@ def main():
         frames3 = torch.empty((n_frames + 1, CFG3_PROPS, nw), dtype=torch.int64, pin_memory=True)
         props_words(SEED_P + 3, depth, CFG3_PROPS, 0, n_frames + 1, out=frames3)
         label3, stages3 = [], []
+        # host latency with the stage events off (no events between the
+        # kernels: the labeling kernel launches as a programmatic dependent)
+        eng.set_profiling(False)
         for q in range(-1, n_frames):  # query -1 is the warm-up (scenario.cpp:183-193)
             src3 = frames3[q + 1]
             t0 = time.perf_counter()
@@ -334,6 +337,12 @@ def main():
             dt = time.perf_counter() - t0
             if q >= 0:
                 eng_lat.append(dt * 1e3)
+        # then the per-stage device times of the same frames
+        eng.set_profiling(True)
+        for q in range(-1, n_frames):
+            eng.submit_grid(cells, CFG3_PROPS, frames3[q + 1], 1)
+            eng.wait()
+            if q >= 0:
                 st3 = eng.stage_times(0, 0)
                 label3.append(st3[2])
                 stages3.append(st3)

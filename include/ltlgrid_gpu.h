@@ -240,6 +240,11 @@ ltlg_status ltlg_get_info(ltlg_ctx* ctx, ltlg_info* out);
  * callers can time with events on the launching stream. */
 ltlg_status ltlg_stream(ltlg_ctx* ctx, int shard, void** stream);
 
+/* Turn the per-submit stage events (ltlg_stage_times) on or off.  Off, a
+ * single-frame submit launches its labeling kernel as a programmatic
+ * dependent of the summary kernel (no event between them). */
+ltlg_status ltlg_set_profiling(ltlg_ctx* ctx, int on);
+
 /* With ltlg_options.profile = 1: device time (CUDA events on the launching
  * stream) of the stages of the submit `back` submits ago (0 = the last one,
  * up to 255) on shard s -- P upload / broadcast, per-word summary build,

@@ -27,7 +27,7 @@ EXPORTS = [
     "ltlg_rasterize_boxes", "ltlg_submit_boxes", "ltlg_set_guards", "ltlg_get_admitted", "ltlg_device_admitted",
     "ltlg_submit_grid_device_ex",
     "ltlg_swept_volume", "ltlg_csr_rows", "ltlg_csr_cols", "ltlg_csr_nnz", "ltlg_csr_build_ms", "ltlg_csr_copy",
-    "ltlg_load_csr", "ltlg_csr_free",
+    "ltlg_load_csr", "ltlg_csr_free", "ltlg_set_profiling",
 ]
 
 
@@ -119,6 +119,7 @@ def lib() -> C.CDLL:
         "ltlg_csr_copy": ([vp, vp, vp], i32),
         "ltlg_load_csr": ([ctxp, vp], i32),
         "ltlg_csr_free": ([vp], None),
+        "ltlg_set_profiling": ([ctxp, i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

@@ -461,6 +461,10 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
                "summary kernel");
         if (prof) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
+        // single frame: the labeling kernel is a programmatic dependent of the
+        // summary kernel (not when profiling: the event between them would
+        // serialise the two anyway)
+        a.pdl = wide && !prof ? 1 : 0;
         a.pairs = s.pairs.ptr;
         a.perm = s.perm.ptr;
         a.sf = s.sf.ptr;
@@ -1111,6 +1115,22 @@ ltlg_status ltlg_stream(ltlg_ctx* ctx, int shard, void** stream) {
     if (!ctx || !stream) return set_err(ctx, LTLG_EINVAL, "null argument");
     if (shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return set_err(ctx, LTLG_EINVAL, "shard out of range");
     *stream = ctx->shards[static_cast<size_t>(shard)].stream;
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_set_profiling(ltlg_ctx* ctx, int on) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (on) {
+        for (Shard& s : ctx->shards) {
+            if (!s.ring.empty()) continue;
+            CK(cudaSetDevice(s.device), "cudaSetDevice");
+            s.ring.assign(Shard::kRing * 4, nullptr);
+            for (auto& ev : s.ring) CK(cudaEventCreate(&ev), "event");
+        }
+    } else {
+        for (Shard& s : ctx->shards) s.have_times = false;
+    }
+    ctx->opts.profile = on ? 1 : 0;
     return LTLG_OK;
 }
 

@@ -300,6 +300,9 @@ __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restri
     // in shared memory and warp 0 assembles the entries (first <= 2 / 4
     // partial props in prop order, as before)
     using LW = typename Fmt<FMT>::LW;
+    // let a programmatically dependent labeling launch get its CTAs resident;
+    // it waits for this grid's completion before touching our outputs
+    asm volatile("griddepcontrol.launch_dependents;");
     __shared__ uint64_t s_pv[64][32];              // P value of (prop, word) when partial
     __shared__ uint64_t s_any[8][32], s_full[8][32], s_part[8][32];
     const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
@@ -862,6 +865,9 @@ __global__ void __launch_bounds__(NT)
     const uint32_t xoff = split64_x_offset(FMT, nw64);
     const uint8_t* tab = static_cast<const uint8_t*>(tab_g);
     const uint8_t* xg = static_cast<const uint8_t*>(tab_g) + xoff;  // X in global memory
+    // launched as a programmatic dependent of the summary kernel: its table,
+    // S words and the reset task counter are ready after this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if constexpr (SMEM) {
         stage_table(smem_raw, tab_g, XSMEM ? tab_bytes : xoff, &tab_bar);
         tab = smem_raw;
@@ -1583,8 +1589,21 @@ static cudaError_t launch_stream64_v(const LaunchArgs& a, cudaStream_t st) {
             attr_set |= 1ull << dev;
         }
         if (smem % 16u || smem > kMaxSmemTable) return cudaErrorInvalidValue;
-        kern<<<sm_count(), NT, smem, st>>>(a.t64, a.task_byte64, a.task_n64, a.task_row, a.task_begin, a.ntasks,
-                                           a.task_ctr, a.sf, tab_bytes, a.s_only, P64, a.nw64, static_cast<SW*>(a.out), a.ostride ? a.ostride : 1u);
+        // programmatic dependent launch: the CTAs get resident while the
+        // summary kernel finishes; they wait on it (griddepcontrol.wait) first
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+        cfg.gridDim = dim3(static_cast<unsigned>(sm_count()));
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, a.t64, a.task_byte64, a.task_n64, a.task_row, a.task_begin, a.ntasks,
+                                  a.task_ctr, a.sf, tab_bytes, a.s_only, P64, a.nw64, static_cast<SW*>(a.out),
+                                  a.ostride ? a.ostride : 1u);
     } else {
         static int per_sm = 0;
         if (!per_sm) {

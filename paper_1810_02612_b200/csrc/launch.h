@@ -40,6 +40,7 @@ struct LaunchArgs {
     const uint64_t* task_pair_b64;
     const uint64_t* pb64;  // Pb table of summary_b64_kernel
     int prop_lane;         // multi-frame: the prop-lane kernel (sf = its launch_pl work buffer)
+    int pdl;               // single frame: launch as a programmatic dependent of the summary kernel
 };
 
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,

@@ -482,6 +482,10 @@ class LabelEngine:
         self._ck(self._L.ltlg_stream(self._h, shard, C.byref(s)))
         return s.value or 0
 
+    def set_profiling(self, on: bool) -> None:
+        """Per-submit stage events on/off (ltlg_set_profiling)."""
+        self._ck(self._L.ltlg_set_profiling(self._h, 1 if on else 0))
+
     def stage_times(self, shard: int = 0, back: int = 0):
         """(upload_ms, summary_ms, label_ms) of the submit `back` submits ago."""
         a, b, c = C.c_float(), C.c_float(), C.c_float()
