@@ -1619,11 +1619,23 @@ static cudaError_t launch_stream64_v(const LaunchArgs& a, cudaStream_t st) {
 
 template <int FMT, typename SW>
 static cudaError_t launch_stream64_t(const LaunchArgs& a, cudaStream_t st) {
-    constexpr int NT = FMT == 64 ? 512 : 1024;  // u64 labels: 16 warps per SM keep every value in registers
-    switch (stream64_table_loc(a.props, a.nw64)) {
-        case 1: return launch_stream64_v<FMT, SW, 1, NT>(a, st);
-        case 2: return launch_stream64_v<FMT, SW, 2, NT>(a, st);
-        default: return launch_stream64_v<FMT, SW, 0, 256>(a, st);
+    // u64 labels: 24 warps per SM at 75 registers (no spills); 32 warps would
+    // need <= 64 and spill (cfg-5 shard: 512 threads 0.373 of HBM, 768 0.417,
+    // 1024 0.380).  Dev knob LTLG_NT64 = 512 / 1024 for A/B runs.
+    if constexpr (FMT == 64) {
+        static const int nt64 = env_int("LTLG_NT64", 768);
+        const int loc = stream64_table_loc(a.props, a.nw64);
+        if (loc == 0) return launch_stream64_v<FMT, SW, 0, 256>(a, st);
+        if (nt64 == 512) return loc == 1 ? launch_stream64_v<FMT, SW, 1, 512>(a, st) : launch_stream64_v<FMT, SW, 2, 512>(a, st);
+        if (nt64 == 1024)
+            return loc == 1 ? launch_stream64_v<FMT, SW, 1, 1024>(a, st) : launch_stream64_v<FMT, SW, 2, 1024>(a, st);
+        return loc == 1 ? launch_stream64_v<FMT, SW, 1, 768>(a, st) : launch_stream64_v<FMT, SW, 2, 768>(a, st);
+    } else {
+        switch (stream64_table_loc(a.props, a.nw64)) {
+            case 1: return launch_stream64_v<FMT, SW, 1, 1024>(a, st);
+            case 2: return launch_stream64_v<FMT, SW, 2, 1024>(a, st);
+            default: return launch_stream64_v<FMT, SW, 0, 256>(a, st);
+        }
     }
 }
 

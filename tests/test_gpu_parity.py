@@ -607,6 +607,8 @@ def test_config5_dense_grid_slice():
     {"LTLG_STREAM64": "0", "LTLG_STREAM_CFG": "2"},                         # double-buffered 32-cell
     {"LTLG_STREAM64": "0", "LTLG_STREAM_CFG": "4"},                         # TMA-ring 32-cell
     {"LTLG_STREAM_TABLE": "0"},                                             # summary through L1
+    {"LTLG_NT64": "512"},                                                   # 64-prop kernel, 16 warps
+    {"LTLG_NT64": "1024"},                                                  # 64-prop kernel, 32 warps
     {"LTLG_PROPLANE": "0"},                                                 # frame-per-lane 64-cell kernel
 ])
 def test_ab_variants_parity(knobs):

@@ -16,7 +16,7 @@ from paper_1810_02612_b200.synth import SyntheticPRM, props_words  # noqa: E402
 O = Oracle()
 bad = 0
 for depth, E, props, F in [(12, 9_000, 4, 3), (14, 20_000, 16, 2), (16, 30_000, 32, 3), (14, 12_000, 64, 2),
-                           (14, 15_000, 20, 40), (13, 8_000, 7, 17)]:
+                           (14, 15_000, 20, 40), (13, 8_000, 7, 17), (20, 30_000, 64, 1), (20, 30_000, 40, 2)]:
     prm = SyntheticPRM(seed=depth + props, depth=depth)
     off, idx = prm.csr(0, E)
     t = prm.words(0, E)
