@@ -422,7 +422,9 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // lanes idle (its cost is ~flat for frames <= 32), so label frame by
         // frame with the single-frame kernel, each launch writing one column
         // of the edge-major labels.
-        if (wide_ok && frames > 1 && frames <= kSmallFrames) {
+        // (dev knob LTLG_SMALL_FRAMES: the per-frame cut-over, for A/B runs)
+        static const int small_frames = getenv("LTLG_SMALL_FRAMES") ? atoi(getenv("LTLG_SMALL_FRAMES")) : kSmallFrames;
+        if (wide_ok && frames > 1 && frames <= small_frames) {
             const ltlg_status fst = run_label_per_frame(ctx, s, nw64);
             if (fst != LTLG_OK) return fst;
             continue;
