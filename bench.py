@@ -127,6 +127,15 @@ def ncu_traffic(kernel: str):
         return None
 
 
+def ncu_limiter(kernel: str):
+    """Pipe utilisations of `kernel` from the committed ncu capture (profiles/limiters.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "limiters.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
 def shard_rows(E: int, rank: int, world: int):
     return E * rank // world, E * (rank + 1) // world
 
@@ -311,6 +320,7 @@ def main():
                         "bytes per launch from the committed ncu --set full capture (profiles/traffic.json). The "
                         "multi-frame kernel is not HBM-bound: ncu shows the L1TEX pipe (record gathers + shared-"
                         "memory OR reductions) and issue saturated (see int_ops)",
+                "limiter": ncu_limiter("label_pl_kernel"),
                 "int_ops": {"alg_and_or_per_launch": lop3, "achieved_per_s": lop3 / (label_ms / 1e3),
                             "peak_per_s": 148 * 64 * sm_clk,
                             "frac": lop3 / (label_ms / 1e3) / (148 * 64 * sm_clk),
@@ -360,6 +370,7 @@ def main():
                                                 "unit": "GB/s", "frac": alg3 / (k3 / 1e3) / 1e9 / hbm,
                                                 "alg_bytes_per_launch": alg3,
                                                 "traffic": ncu_traffic("label_stream64_kernel"),
+                                                "limiter": ncu_limiter("label_stream64_kernel"),
                                                 "kernel": "label_stream64_kernel<16,u16,smem,1024>"}}
 
     # ---- e2e through the public API with host buffers ------------------------

@@ -29,6 +29,8 @@ lines.append(run("python", os.path.join(here, "ncu_launches.py"), src + "_launch
 lines.append("```")
 traffic_path = os.path.join(os.path.dirname(dst), "traffic.json")
 traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+lim_path = os.path.join(os.path.dirname(dst), "limiters.json")
+limiters = json.load(open(lim_path)) if os.path.exists(lim_path) else {}
 for kind in ("batch", "stream"):
     rep = f"{src}_{kind}.ncu-rep"
     if not os.path.exists(rep):
@@ -48,11 +50,27 @@ for kind in ("batch", "stream"):
     tb = sum(float(d[k]) * scale.get(u[k], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     name = d["Kernel Name"].split("<")[0].replace("void ", "").split("::")[-1]
     traffic[name] = tb
+
+    def pct(k):
+        try:
+            return round(float(d[k]), 1)
+        except (KeyError, ValueError):
+            return None
+    # what binds the kernel, from the same capture (bench.py reports it next to the roofline)
+    limiters[name] = {
+        "l1tex_data_pipe_pct": pct("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+        "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+        "dram_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+        "alu_pipe_pct": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+        "warps_active_pct": pct("sm__warps_active.avg.pct_of_peak_sustained_active"),
+        "source": os.path.basename(dst) + "_ncu_summary.md",
+    }
     lines.append(f"  dram read+write bytes per launch (traffic)                   {tb:.4g}")
     lines.append(run("python", os.path.join(here, "ncu_sass.py"), rep, "12").rstrip())
     lines.append("```")
 open(dst + "_ncu_summary.md", "w").write("\n".join(lines) + "\n")
 json.dump(traffic, open(traffic_path, "w"), indent=1)
+json.dump(limiters, open(lim_path, "w"), indent=1)
 for suffix in ("_bench.json", "_bench_ref.json", "_launches.csv"):
     if os.path.exists(src + suffix):
         shutil.copy(src + suffix, dst + suffix)
