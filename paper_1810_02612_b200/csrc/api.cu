@@ -342,7 +342,7 @@ ltlg_status run_guards(ltlg_ctx* ctx, Shard& s) {
     return LTLG_OK;
 }
 
-constexpr int kSmallFrames = 16;  // sweep_frames: per-frame single-frame launches win up to ~16 frames
+constexpr int kSmallFrames = 16;  // sweep_frames: per-frame single-frame launches win up to ~16 frames (<= 16 props)
 
 // Multi-frame submit of few frames: per frame, the 64-cell summary + one
 // single-frame launch writing labels[row * frames + f].
@@ -422,8 +422,15 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // lanes idle (its cost is ~flat for frames <= 32), so label frame by
         // frame with the single-frame kernel, each launch writing one column
         // of the edge-major labels.
-        // (dev knob LTLG_SMALL_FRAMES: the per-frame cut-over, for A/B runs)
-        static const int small_frames = getenv("LTLG_SMALL_FRAMES") ? atoi(getenv("LTLG_SMALL_FRAMES")) : kSmallFrames;
+        // The cut-over follows the measured per-frame cost (sweep_frames.py,
+        // B200): ~0.09 ms/frame up to 16 props, 0.13 at 32, 0.28-0.31 at 33-64
+        // props, against the prop-lane kernel's ~1.4-2.8 ms fixed cost per
+        // pass.  (dev knob LTLG_SMALL_FRAMES: a fixed cut-over, for A/B runs)
+        static const int small_frames_env = getenv("LTLG_SMALL_FRAMES") ? atoi(getenv("LTLG_SMALL_FRAMES")) : -1;
+        const int small_frames = small_frames_env >= 0 ? small_frames_env
+                                 : props <= 16       ? kSmallFrames
+                                 : props <= 32       ? 14
+                                                     : 9;
         if (wide_ok && frames > 1 && frames <= small_frames) {
             const ltlg_status fst = run_label_per_frame(ctx, s, nw64);
             if (fst != LTLG_OK) return fst;
@@ -433,8 +440,9 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         const bool wide_b = wide_b_ok && frames > 1 && props <= 32;  // 64-cell-word multi-frame path
         // prop-lane kernel for <= 64 frames (dev knob LTLG_PROPLANE=0: the frame-per-lane kernel)
         static const bool pl_ok = !getenv("LTLG_PROPLANE") || atoi(getenv("LTLG_PROPLANE")) != 0;
-        const bool pl = wide_b && pl_ok && frames <= 64;
-        CK(s.sf.reserve(pl ? pl_work_bytes(frames, nw64)
+        // (<= 32 props: one prop per lane; 33..64: two)
+        const bool pl = wide_b_ok && pl_ok && frames > 1 && frames <= 64 && props <= 64;
+        CK(s.sf.reserve(pl ? pl_work_bytes(props, frames, nw64)
                         : wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32
                         : wide ? split64_table_bytes(props, nw64)
                              : frames == 1 && props <= 32
@@ -479,7 +487,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         a.s_only = s.s_only.ptr;
         const bool single = frames == 1;
         if (single) a.pairs = s.pairs_s.ptr;
-        if (wide_b) {
+        if (wide_b || pl) {
             a.prop_lane = pl ? 1 : 0;
             a.mask_b64 = s.mask_b64.ptr;
             a.word_b64 = s.word_b64.ptr;

@@ -1780,12 +1780,14 @@ cudaError_t launch_summary_b64(const uint64_t* P64, int props, int frames, uint3
 }
 
 // ---------------------------------------------------------------------------
-// Prop-lane multi-frame path (<= 32 props, <= 64 frames): lane j owns
-// proposition j and a 64-bit mask over the frames.  Per 64-cell word w:
-//   ffr[w * 32 + j]  frames where P_j[w] covers the word  (hit for any mask)
-//   sfr[w * 32 + j]  frames where P_j[w] != 0            (hit for a full mask)
+// Prop-lane multi-frame path (<= 64 props, <= 64 frames): lane l owns
+// propositions l and (PW = 2, > 32 props) l + 32, each with a 64-bit mask
+// over the frames.  Per 64-cell word w, with pw = 32 * PW prop slots:
+//   ffr[w * pw + j]  frames where P_j[w] covers the word  (hit for any mask)
+//   sfr[w * pw + j]  frames where P_j[w] != 0            (hit for a full mask)
 //   rec[rec_se[w].x .. rec_se[w].y)  one record per partial (frame, prop):
-//        {P_j^f[w] lo, hi, byte offset 4 f of frame f's accumulator, 1 << j}
+//        {P_j^f[w] lo, hi, byte offset of accumulator word f + 64 (j / 32),
+//         1 << (j % 32)}
 //        grouped by prop, so the 32 records one probe round reads mostly
 //        name distinct frames (distinct shared-memory words, no same-address
 //        serialisation of the ORs)
@@ -1799,10 +1801,10 @@ __global__ void __launch_bounds__(256) pl_summary_kernel(const uint64_t* __restr
                                                          uint32_t nw64, uint64_t cells, uint64_t* __restrict__ ffr,
                                                          uint64_t* __restrict__ sfr, uint32_t* __restrict__ cnt,
                                                          uint32_t* __restrict__ wcnt, uint32_t* __restrict__ task_ctr,
-                                                         int nctr) {
+                                                         int nctr, int pshift) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (t < static_cast<uint64_t>(nctr)) task_ctr[t] = 0;
-    const uint32_t w = static_cast<uint32_t>(t >> 5), j = static_cast<uint32_t>(t & 31);
+    const uint32_t w = static_cast<uint32_t>(t >> pshift), j = static_cast<uint32_t>(t & ((1u << pshift) - 1u));
     if (w > nw64) return;
     uint64_t full = 0, any = 0;
     uint32_t n = 0;
@@ -1848,9 +1850,9 @@ __global__ void __launch_bounds__(1024) pl_scan_kernel(const uint32_t* __restric
 
 __global__ void __launch_bounds__(256) pl_fill_kernel(const uint64_t* __restrict__ P64, int props, int frames,
                                                       uint32_t nw64, uint64_t cells, const uint32_t* __restrict__ cnt,
-                                                      uint32_t* __restrict__ cursor, uint4* __restrict__ rec) {
+                                                      uint32_t* __restrict__ cursor, uint4* __restrict__ rec, int pshift) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    const uint32_t w = static_cast<uint32_t>(t >> 5), j = static_cast<uint32_t>(t & 31);
+    const uint32_t w = static_cast<uint32_t>(t >> pshift), j = static_cast<uint32_t>(t & ((1u << pshift) - 1u));
     if (w >= nw64) return;
     const uint32_t n = cnt[t];
     if (!n) return;
@@ -1860,9 +1862,9 @@ __global__ void __launch_bounds__(256) pl_fill_kernel(const uint64_t* __restrict
     const uint64_t* base = P64 + static_cast<uint64_t>(j) * nw64 + w;
     for (int f = 0; f < frames; ++f) {
         const uint64_t x = base[static_cast<uint64_t>(f) * props * nw64] & valid;
-        if (x != 0 && x != valid)  // smem label accumulator word f, bit j
+        if (x != 0 && x != valid)  // smem label accumulator word f + 64 (j / 32), bit j % 32
             rec[pos++] = make_uint4(static_cast<uint32_t>(x), static_cast<uint32_t>(x >> 32),
-                                    4u * static_cast<uint32_t>(f), 1u << j);
+                                    4u * (static_cast<uint32_t>(f) + 64u * (j >> 5)), 1u << (j & 31));
     }
 }
 
@@ -1880,7 +1882,7 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
     return x;
 }
 
-template <typename SW>
+template <typename SW, int PW>
 __global__ void __launch_bounds__(256)
     label_pl_kernel(const uint64_t* __restrict__ masks, const uint32_t* __restrict__ words,
                     const uint64_t* __restrict__ task_pair, const uint32_t* __restrict__ task_row, uint32_t task_begin,
@@ -1890,16 +1892,18 @@ __global__ void __launch_bounds__(256)
                     SW* __restrict__ out) {
     // per warp: partial-record hits, one 32-bit prop mask per frame (a native
     // shared-memory OR; 64-bit ones are CAS loops)
-    __shared__ uint32_t s_acc[8][64];
+    // (PW = 2: words 64..127 hold props 32..63)
+    __shared__ uint32_t s_acc[8][64 * PW];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint32_t* sacc = s_acc[wib];
     const uint32_t sacc_s = smem_u32(sacc);
-    sacc[lane] = 0;
-    sacc[lane + 32] = 0;
+#pragma unroll
+    for (int k = 0; k < 2 * PW; ++k) sacc[lane + 32 * k] = 0;
     __syncwarp();
     const uint4* lane_rec = rec + lane;
     const uint64_t* lane_ffr = ffr + lane;
     const uint64_t* lane_sfr = sfr + lane;
+    constexpr uint32_t kPw = 32u * PW;  // prop slots per word in ffr / sfr
     for (;;) {
         uint32_t t = 0;
         if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
@@ -1908,16 +1912,24 @@ __global__ void __launch_bounds__(256)
         const uint64_t p0 = task_pair[t], p1 = task_pair[t + 1];
         const int64_t r0 = task_row[t];
         int64_t row = r0 - 1;
-        uint64_t acc = 0;  // frames where prop `lane` covers a swept word of the open row
+        uint64_t acc = 0;   // frames where prop `lane` covers a swept word of the open row
+        uint64_t acc2 = 0;  // (PW = 2) the same for prop lane + 32
         auto store = [&](int64_t r) {
             __syncwarp();
             const uint32_t lo = transpose32(static_cast<uint32_t>(acc), lane) | sacc[lane];  // frame lane
             const uint32_t hi = transpose32(static_cast<uint32_t>(acc >> 32), lane) | sacc[lane + 32];  // frame lane + 32
-            sacc[lane] = 0;
-            sacc[lane + 32] = 0;
             SW* o = out + static_cast<uint64_t>(perm[r]) * frames;
-            if (lane < frames) o[lane] = static_cast<SW>(lo);
-            if (lane + 32 < frames) o[lane + 32] = static_cast<SW>(hi);
+            if constexpr (PW == 2) {
+                const uint32_t lo2 = transpose32(static_cast<uint32_t>(acc2), lane) | sacc[lane + 64];
+                const uint32_t hi2 = transpose32(static_cast<uint32_t>(acc2 >> 32), lane) | sacc[lane + 96];
+                if (lane < frames) o[lane] = static_cast<SW>((static_cast<uint64_t>(lo2) << 32) | lo);
+                if (lane + 32 < frames) o[lane + 32] = static_cast<SW>((static_cast<uint64_t>(hi2) << 32) | hi);
+            } else {
+                if (lane < frames) o[lane] = static_cast<SW>(lo);
+                if (lane + 32 < frames) o[lane + 32] = static_cast<SW>(hi);
+            }
+#pragma unroll
+            for (int k = 0; k < 2 * PW; ++k) sacc[lane + 32 * k] = 0;
             __syncwarp();
         };
         uint2 cm = __ldg(reinterpret_cast<const uint2*>(masks + p0 + lane));
@@ -1940,13 +1952,16 @@ __global__ void __launch_bounds__(256)
                     if (row >= r0) store(row);
                     ++row;
                     acc = 0;
+                    acc2 = 0;
                 }
                 const uint32_t w = wh & kWordMask;
                 if ((mlo & mhi) == 0xffffffffu) {  // the whole 64-cell word is swept: every nonzero frame hits
-                    acc |= __ldg(index_wide(lane_sfr, w * 32u));
+                    acc |= __ldg(index_wide(lane_sfr, w * kPw));
+                    if constexpr (PW == 2) acc2 |= __ldg(index_wide(lane_sfr, w * kPw + 32u));
                     continue;
                 }
-                acc |= __ldg(index_wide(lane_ffr, w * 32u));
+                acc |= __ldg(index_wide(lane_ffr, w * kPw));
+                if constexpr (PW == 2) acc2 |= __ldg(index_wide(lane_ffr, w * kPw + 32u));
                 const uint2 se = make_uint2(__shfl_sync(0xffffffffu, cse.x, i), __shfl_sync(0xffffffffu, cse.y, i));
                 // all lanes probe 32 records at a time (the array is padded, so
                 // reading past the word's last record is harmless)
@@ -1963,57 +1978,68 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Byte layout of the prop-lane work buffer: summary masks (pw prop slots per
+// word), counts, record ranges, then the records (worst case: every (word,
+// prop, frame) partial) + 32 records of padding for the last probe round.
+struct PlLayout {
+    uint64_t nt;  // (nw64 + 1) * pw
+    size_t ffr, sfr, cnt, wcnt, cursor, rec_se, rec, total;
+    PlLayout(int props, int frames, uint32_t nw64) {
+        nt = static_cast<uint64_t>(nw64 + 1) * (props > 32 ? 64u : 32u);
+        auto up = [](size_t x, size_t a) { return (x + a - 1) & ~(a - 1); };
+        ffr = 0;
+        sfr = ffr + nt * 8;
+        cnt = sfr + nt * 8;
+        wcnt = cnt + nt * 4;
+        cursor = wcnt + (nw64 + 2) * 4;
+        rec_se = up(cursor + (nw64 + 2) * 4, 8);
+        rec = up(rec_se + (nw64 + 2) * 8, 16);
+        total = rec + (nt * static_cast<uint64_t>(frames) + 32) * 16;
+    }
+};
+
 cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* work,
                       size_t work_bytes, uint32_t* task_ctr, int nctr, cudaStream_t st) {
-    if (props > 32 || frames > 64) return cudaErrorInvalidValue;
+    if (props > 64 || frames > 64) return cudaErrorInvalidValue;
+    const int pshift = props > 32 ? 6 : 5;
+    const PlLayout L(props, frames, nw64);
+    if (L.total > work_bytes) return cudaErrorInvalidValue;
     uint8_t* wb = static_cast<uint8_t*>(work);
-    const uint64_t nt = static_cast<uint64_t>(nw64 + 1) * 32;
-    uint64_t* ffr = reinterpret_cast<uint64_t*>(wb);
-    uint64_t* sfr = ffr + nt;
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(sfr + nt);
-    uint32_t* wcnt = cnt + nt;
-    uint32_t* cursor = wcnt + (nw64 + 2);
-    uint2* rec_se = reinterpret_cast<uint2*>(wb + ((reinterpret_cast<uint8_t*>(cursor + (nw64 + 2)) - wb + 7u) & ~size_t(7)));
-    const size_t rec_at = ((reinterpret_cast<uint8_t*>(rec_se + (nw64 + 2)) - wb) + 15u) & ~size_t(15);
-    if (rec_at > work_bytes) return cudaErrorInvalidValue;
+    uint64_t* ffr = reinterpret_cast<uint64_t*>(wb + L.ffr);
+    uint64_t* sfr = reinterpret_cast<uint64_t*>(wb + L.sfr);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(wb + L.cnt);
+    uint32_t* wcnt = reinterpret_cast<uint32_t*>(wb + L.wcnt);
+    uint32_t* cursor = reinterpret_cast<uint32_t*>(wb + L.cursor);
+    uint2* rec_se = reinterpret_cast<uint2*>(wb + L.rec_se);
     cudaError_t e = cudaMemsetAsync(wcnt, 0, (nw64 + 2) * 4, st);
     if (e != cudaSuccess) return e;
+    const uint64_t nt = L.nt;
     const uint64_t nthreads = nt > static_cast<uint64_t>(nctr) ? nt : static_cast<uint64_t>(nctr);
-    pl_summary_kernel<<<static_cast<unsigned>((nthreads + 255) / 256), 256, 0, st>>>(P64, props, frames, nw64, cells,
-                                                                                    ffr, sfr, cnt, wcnt, task_ctr, nctr);
+    pl_summary_kernel<<<static_cast<unsigned>((nthreads + 255) / 256), 256, 0, st>>>(
+        P64, props, frames, nw64, cells, ffr, sfr, cnt, wcnt, task_ctr, nctr, pshift);
     pl_scan_kernel<<<1, 1024, 0, st>>>(wcnt, nw64 + 1, rec_se, cursor);
     pl_fill_kernel<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(
-        P64, props, frames, nw64, cells, cnt, cursor, reinterpret_cast<uint4*>(wb + rec_at));
+        P64, props, frames, nw64, cells, cnt, cursor, reinterpret_cast<uint4*>(wb + L.rec), pshift);
     return cudaGetLastError();
 }
 
-size_t pl_work_bytes(int frames, uint32_t nw64) {
-    const uint64_t nt = static_cast<uint64_t>(nw64 + 1) * 32;
-    const size_t head = ((nt * 16 + nt * 4 + 2 * (nw64 + 2) * 4 + 8 + (nw64 + 2) * 8) + 15u) & ~size_t(15);
-    // worst case: every (word, prop, frame) partial; + 32 records of padding
-    return head + (nt * static_cast<uint64_t>(frames) + 32) * 16;
-}
+size_t pl_work_bytes(int props, int frames, uint32_t nw64) { return PlLayout(props, frames, nw64).total; }
 
-template <typename SW>
+template <typename SW, int PW>
 static void launch_pl_label(const LaunchArgs& a, cudaStream_t st) {
-    const uint64_t nt = static_cast<uint64_t>(a.nw64 + 1) * 32;
+    const PlLayout L(a.props, a.frames, a.nw64);
     const uint8_t* wb = static_cast<const uint8_t*>(a.sf);
-    const uint64_t* ffr = reinterpret_cast<const uint64_t*>(wb);
-    const uint64_t* sfr = ffr + nt;
-    const uint32_t* cnt = reinterpret_cast<const uint32_t*>(sfr + nt);
-    const uint32_t* cursor = cnt + nt + (a.nw64 + 2);
-    const uint2* rec_se = reinterpret_cast<const uint2*>(
-        wb + ((reinterpret_cast<const uint8_t*>(cursor + (a.nw64 + 2)) - wb + 7u) & ~size_t(7)));
-    const size_t rec_at = ((reinterpret_cast<const uint8_t*>(rec_se + (a.nw64 + 2)) - wb) + 15u) & ~size_t(15);
     static int per_sm = 0;
-    auto kern = label_pl_kernel<SW>;
+    auto kern = label_pl_kernel<SW, PW>;
     if (!per_sm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
         if (per_sm <= 0) per_sm = 4;
     }
     kern<<<sm_count() * per_sm, 256, 0, st>>>(a.mask_b64, a.word_b64, a.task_pair_b64, a.task_row, a.task_begin,
-                                              a.ntasks, a.task_ctr, ffr, sfr, rec_se,
-                                              reinterpret_cast<const uint4*>(wb + rec_at), a.frames, a.perm,
+                                              a.ntasks, a.task_ctr, reinterpret_cast<const uint64_t*>(wb + L.ffr),
+                                              reinterpret_cast<const uint64_t*>(wb + L.sfr),
+                                              reinterpret_cast<const uint2*>(wb + L.rec_se),
+                                              reinterpret_cast<const uint4*>(wb + L.rec), a.frames, a.perm,
                                               static_cast<SW*>(a.out));
 }
 
@@ -2057,11 +2083,12 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
             case 4: e = launch_stream_t<32, uint32_t>(a, st); break;
             default: e = launch_stream_t<64, uint64_t>(a, st); break;
         }
-    } else if (a.mask_b64 && a.prop_lane) {  // prop-lane multi-frame path (<= 32 props, <= 64 frames)
+    } else if (a.mask_b64 && a.prop_lane) {  // prop-lane multi-frame path (<= 64 props, <= 64 frames)
         switch (a.label_bytes) {
-            case 1: launch_pl_label<uint8_t>(a, st); break;
-            case 2: launch_pl_label<uint16_t>(a, st); break;
-            default: launch_pl_label<uint32_t>(a, st); break;
+            case 1: launch_pl_label<uint8_t, 1>(a, st); break;
+            case 2: launch_pl_label<uint16_t, 1>(a, st); break;
+            case 4: launch_pl_label<uint32_t, 1>(a, st); break;
+            default: launch_pl_label<uint64_t, 2>(a, st); break;
         }
     } else if (a.mask_b64) {  // 64-cell-word multi-frame path (<= 32 props)
         switch (a.label_bytes) {

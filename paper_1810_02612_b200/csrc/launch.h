@@ -54,7 +54,7 @@ cudaError_t launch_summary_b64(const uint64_t* P64, int props, int frames, uint3
                                uint64_t* pbt, void* s_only, uint32_t* task_ctr, int nctr, cudaStream_t st);
 cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* work,
                       size_t work_bytes, uint32_t* task_ctr, int nctr, cudaStream_t st);
-size_t pl_work_bytes(int frames, uint32_t nw64);
+size_t pl_work_bytes(int props, int frames, uint32_t nw64);
 cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
                              uint32_t* task_ctr, int nctr, cudaStream_t st, uint64_t* P_copy);
 bool stream_table_in_smem(int props, uint32_t nw32);
