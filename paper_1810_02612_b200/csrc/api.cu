@@ -438,11 +438,12 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         }
         static const bool wide_b_ok = !getenv("LTLG_BATCH64") || atoi(getenv("LTLG_BATCH64")) != 0;
         const bool wide_b = wide_b_ok && frames > 1 && props <= 32;  // 64-cell-word multi-frame path
-        // prop-lane kernel for <= 64 frames (dev knob LTLG_PROPLANE=0: the frame-per-lane kernel)
+        // prop-lane kernel, in slices of <= 64 frames (dev knob LTLG_PROPLANE=0:
+        // the frame-per-lane kernels); <= 32 props: one prop per lane, 33..64: two
         static const bool pl_ok = !getenv("LTLG_PROPLANE") || atoi(getenv("LTLG_PROPLANE")) != 0;
-        // (<= 32 props: one prop per lane; 33..64: two)
-        const bool pl = wide_b_ok && pl_ok && frames > 1 && frames <= 64 && props <= 64;
-        CK(s.sf.reserve(pl ? pl_work_bytes(props, frames, nw64)
+        const bool pl = wide_b_ok && pl_ok && frames > 1 && props <= 64;
+        const int nslice = pl ? (frames + 63) / 64 : 1;
+        CK(s.sf.reserve(pl ? pl_work_bytes(props, std::min(frames, 64), nw64)
                         : wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32
                         : wide ? split64_table_bytes(props, nw64)
                              : frames == 1 && props <= 32
@@ -454,12 +455,16 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         const bool prof = ctx->opts.profile != 0;
         if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
         const int nctr = static_cast<int>((s.block_row.size() - 1) * kCtrStride);
+        for (int sl = 0; sl < nslice; ++sl) {  // (frame slices: prop-lane path only)
+        // balanced slices (65 frames -> 33 + 32, not 64 + 1)
+        const int f0 = frames * sl / nslice, nf = pl ? frames * (sl + 1) / nslice - f0 : frames;
         if (wide)
             CK(launch_summary64(s.P_host ? s.P_host : s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr,
                                 s.ctr.ptr, nctr, s.stream, s.P_host ? s.P.ptr : nullptr),
                "summary kernel");
         else if (pl)
-            CK(launch_pl(s.Pdev(), props, frames, nw64, ctx->cells, s.sf.ptr, s.sf.bytes, s.ctr.ptr, nctr, s.stream),
+            CK(launch_pl(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.sf.ptr,
+                         s.sf.bytes, s.ctr.ptr, nctr, s.stream),
                "summary kernel");
         else if (wide_b)
             CK(launch_summary_b64(s.Pdev(), props, frames, nw64, ctx->cells, s.sf.ptr, nullptr, s.s_only.ptr,
@@ -469,7 +474,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
             CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
                               s.s_only.ptr, s.ctr.ptr, nctr, s.stream),
                "summary kernel");
-        if (prof) CK(cudaEventRecord(s.ev[2], s.stream), "event");
+        if (prof && sl == 0) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
         // single frame: the labeling kernel is a programmatic dependent of the
         // summary kernel (not when profiling: the event between them would
@@ -481,8 +486,9 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         a.P32 = reinterpret_cast<const uint32_t*>(s.Pdev());
         a.nw32 = nw32;
         a.props = props;
-        a.frames = frames;
-        a.out = s.labels.ptr;
+        a.frames = nf;
+        a.out = static_cast<uint8_t*>(s.labels.ptr) + static_cast<size_t>(f0) * static_cast<size_t>(ctx->label_bytes);
+        if (nslice > 1) a.ostride = static_cast<uint32_t>(frames);
         a.label_bytes = ctx->label_bytes;
         a.s_only = s.s_only.ptr;
         const bool single = frames == 1;
@@ -512,9 +518,10 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
             a.ntasks = nb == 1 ? bt.back() : bt[static_cast<size_t>(c) + 1];
             a.task_ctr = s.ctr.ptr + static_cast<size_t>(c) * kCtrStride;
             CK(launch_label(a, s.stream), "label kernel");
-            if (nb > 1) CK(cudaEventRecord(s.block_done[static_cast<size_t>(c)], s.stream), "event");
+            if (nb > 1 && sl == nslice - 1) CK(cudaEventRecord(s.block_done[static_cast<size_t>(c)], s.stream), "event");
         }
         s.blocks_last = nb;
+        }  // frame slices
         if (!ctx->guard_pos.empty()) {
             const ltlg_status gst = run_guards(ctx, s);
             if (gst != LTLG_OK) return gst;

@@ -1889,7 +1889,7 @@ __global__ void __launch_bounds__(256)
                     uint32_t ntasks, uint32_t* __restrict__ task_ctr, const uint64_t* __restrict__ ffr,
                     const uint64_t* __restrict__ sfr, const uint2* __restrict__ rec_se,
                     const uint4* __restrict__ rec, int frames, const uint32_t* __restrict__ perm,
-                    SW* __restrict__ out) {
+                    SW* __restrict__ out, uint32_t ostride) {
     // per warp: partial-record hits, one 32-bit prop mask per frame (a native
     // shared-memory OR; 64-bit ones are CAS loops)
     // (PW = 2: words 64..127 hold props 32..63)
@@ -1918,7 +1918,7 @@ __global__ void __launch_bounds__(256)
             __syncwarp();
             const uint32_t lo = transpose32(static_cast<uint32_t>(acc), lane) | sacc[lane];  // frame lane
             const uint32_t hi = transpose32(static_cast<uint32_t>(acc >> 32), lane) | sacc[lane + 32];  // frame lane + 32
-            SW* o = out + static_cast<uint64_t>(perm[r]) * frames;
+            SW* o = out + static_cast<uint64_t>(perm[r]) * ostride;
             if constexpr (PW == 2) {
                 const uint32_t lo2 = transpose32(static_cast<uint32_t>(acc2), lane) | sacc[lane + 64];
                 const uint32_t hi2 = transpose32(static_cast<uint32_t>(acc2 >> 32), lane) | sacc[lane + 96];
@@ -2040,7 +2040,7 @@ static void launch_pl_label(const LaunchArgs& a, cudaStream_t st) {
                                               reinterpret_cast<const uint64_t*>(wb + L.sfr),
                                               reinterpret_cast<const uint2*>(wb + L.rec_se),
                                               reinterpret_cast<const uint4*>(wb + L.rec), a.frames, a.perm,
-                                              static_cast<SW*>(a.out));
+                                              static_cast<SW*>(a.out), a.ostride ? a.ostride : static_cast<uint32_t>(a.frames));
 }
 
 template <int FMT, typename SW, int FPL, bool FULL>
@@ -2069,7 +2069,14 @@ static void launch_batch_fpl(const LaunchArgs& a, cudaStream_t st) {
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
     if (a.ntasks <= a.task_begin) return cudaSuccess;
     cudaError_t e = cudaSuccess;
-    if (a.frames == 1 && a.t64) {  // 64-cell-word single-frame path (<= 32 props)
+    if (a.mask_b64 && a.prop_lane) {  // prop-lane multi-frame path (<= 64 props, a slice of <= 64 frames)
+        switch (a.label_bytes) {
+            case 1: launch_pl_label<uint8_t, 1>(a, st); break;
+            case 2: launch_pl_label<uint16_t, 1>(a, st); break;
+            case 4: launch_pl_label<uint32_t, 1>(a, st); break;
+            default: launch_pl_label<uint64_t, 2>(a, st); break;
+        }
+    } else if (a.frames == 1 && a.t64) {  // 64-cell-word single-frame path (<= 32 props)
         switch (a.label_bytes) {
             case 1: e = launch_stream64_t<16, uint8_t>(a, st); break;
             case 2: e = launch_stream64_t<16, uint16_t>(a, st); break;
@@ -2082,13 +2089,6 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
             case 2: e = launch_stream_t<16, uint16_t>(a, st); break;
             case 4: e = launch_stream_t<32, uint32_t>(a, st); break;
             default: e = launch_stream_t<64, uint64_t>(a, st); break;
-        }
-    } else if (a.mask_b64 && a.prop_lane) {  // prop-lane multi-frame path (<= 64 props, <= 64 frames)
-        switch (a.label_bytes) {
-            case 1: launch_pl_label<uint8_t, 1>(a, st); break;
-            case 2: launch_pl_label<uint16_t, 1>(a, st); break;
-            case 4: launch_pl_label<uint32_t, 1>(a, st); break;
-            default: launch_pl_label<uint64_t, 2>(a, st); break;
         }
     } else if (a.mask_b64) {  // 64-cell-word multi-frame path (<= 32 props)
         switch (a.label_bytes) {

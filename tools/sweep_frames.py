@@ -10,10 +10,11 @@ from paper_1810_02612_b200.synth import SyntheticPRM, props_words  # noqa: E402
 depth, E, props = 18, 2_000_000, int(os.environ.get("PROPS", "16"))
 prm = SyntheticPRM(1, depth)
 T = prm.words(0, E)
-P = props_words(4, depth, props, 0, 64)
+FR = [int(x) for x in os.environ.get("FRAMES", "1 2 4 8 16 32 64").split()]
+P = props_words(4, depth, props, 0, max(FR))
 eng = LabelEngine(devices=[0], profile=True)
 eng.load_abstraction_words(E, 1 << depth, T.offsets, T.words, T.masks)
-for frames in [int(x) for x in os.environ.get("FRAMES", "1 2 4 8 16 32 64").split()]:
+for frames in FR:
     ts = []
     for it in range(8):
         eng.submit_grid(1 << depth, props, P[:frames], frames)
