@@ -139,6 +139,29 @@ def test_random_scenes(seed):
     eng.close()
 
 
+@pytest.mark.parametrize("props", [5, 20, 40, 64])
+@pytest.mark.parametrize("frames", [65, 130])
+def test_many_frames_in_slices(props, frames):
+    """> 64 frames: the prop-lane kernel in balanced frame slices (two or
+    three passes), each writing its columns of the edge-major labels."""
+    rng = SplitMix64(props * 1000 + frames)
+    r, c = 700, 3001
+    rows = random_rows(rng, r, c, 0.01)
+    off, idx = to_csr(rows)
+    P = np.zeros((frames, props, (c + 63) // 64), np.uint64)
+    for f in range(frames):
+        P[f] = bits_to_words(random_rows(rng, props, c, [0.002, 0.05, 0.6][f % 3]))
+    P[::7, :, ::5] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction(CsrBoolMatrix(r, c, off, idx))
+    eng.submit_grid(c, props, P, frames)
+    packed = eng.get_labels_packed()
+    for f in range(frames):
+        want = ORACLE.label_all(r, c, off, idx, c, props, P[f])
+        assert np.array_equal(packed[:, f].astype(np.uint64), want.reshape(r, -1)[:, 0]), f"frame {f}"
+    eng.close()
+
+
 @pytest.mark.parametrize("props", [1, 7, 16, 17, 32, 33, 64])
 def test_pinned_single_frame_fused_upload(props):
     """One frame from pinned host memory: the summary kernel reads P through
