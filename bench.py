@@ -236,9 +236,17 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # (dev-only knobs for exercising the N > 1 path on one GPU: every rank on
+    # BENCH_FORCE_DEVICE, collectives over BENCH_DIST_BACKEND=gloo -- NCCL
+    # refuses two ranks on one device)
+    local = int(os.environ.get("BENCH_FORCE_DEVICE", local))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_1810_02612_b200 import LabelEngine
     from paper_1810_02612_b200.synth import SyntheticPRM, props_words
 
@@ -267,8 +275,13 @@ def main():
 
     def step():
         if world > 1:
-            with torch.cuda.stream(stream):
-                dist.broadcast(P_dev, src=0)
+            # the broadcast runs on torch's stream, ordered after the engine's
+            # previous labelling (which reads P_dev in place) and before the
+            # next one -- no tensor is ever recorded on the engine's stream
+            cur = torch.cuda.current_stream()
+            cur.wait_stream(stream)
+            dist.broadcast(P_dev, src=0)
+            stream.wait_stream(cur)
         eng.submit_grid_device(cells, props, P_dev.data_ptr(), F)
 
     for _ in range(args.warmup):
@@ -386,11 +399,13 @@ def main():
         Ke = max(2, min(K, 5))
 
         def e2e_step():
-            if world > 1:
-                with torch.cuda.stream(stream):  # H2D on rank 0, NCCL broadcast, labelling: one stream
-                    if rank == 0:
-                        P_dev.copy_(P_host, non_blocking=True)
-                    dist.broadcast(P_dev, src=0)
+            if world > 1:  # H2D on rank 0 + broadcast on torch's stream, then the engine's
+                cur = torch.cuda.current_stream()
+                cur.wait_stream(stream)
+                if rank == 0:
+                    P_dev.copy_(P_host, non_blocking=True)
+                dist.broadcast(P_dev, src=0)
+                stream.wait_stream(cur)
                 eng.submit_grid_device(cells, props, P_dev.data_ptr(), F, readback=True)
             else:
                 eng.submit_grid(cells, props, P_host, F)
@@ -428,9 +443,13 @@ def main():
             "shape": {"W32": W32, "rows": rows_all, "t_bytes_device": int(info.t_bytes)},
         }
         print(json.dumps(line), flush=True)
-    eng.close()
+    # collectives ran on the engine's stream: tear the process group down
+    # before the engine (and its stream) goes away
+    torch.cuda.synchronize()
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
+    eng.close()
 
 
 if __name__ == "__main__":
