@@ -424,6 +424,27 @@ def test_sharded_engine_on_one_device(devices):
     eng.close()
 
 
+def test_bench_two_ranks_on_one_gpu():
+    """bench.py's N > 1 path (rank shards, P broadcast each step, max-over-ranks
+    timing, teardown) under torchrun with two ranks sharing cuda:0 over gloo
+    (NCCL refuses two ranks on one device): it must finish cleanly and rank 0
+    must print one JSON line with n_gpus = 2."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(GOLDEN))
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo", BENCH_FORCE_DEVICE="0")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29633", "bench.py", "--gpus", "2",
+                        "--steps", "3", "--warmup", "3", "--quick", "--no-cpu-baseline"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
+    assert lines[0]["e2e"]["value"] > 0
+
+
 def test_cpp_drop_in_parity():
     # the reference core and include/ltlgrid_gpu.hpp compiled into one binary
     import subprocess
