@@ -201,6 +201,35 @@ ltlg_status ltlg_rasterize_boxes(const ltlg_gridk* grid, int num_cols, const uin
 ltlg_status ltlg_submit_boxes(ltlg_ctx* ctx, const ltlg_gridk* grid, int num_props, int frames,
                               const uint64_t* box_offsets, const double* box_lo, const double* box_hi);
 
+/* The reference benchmark's perception volumes on the GPU:
+ * generate_scenario (core/src/scenario.cpp:52-128, ScenarioConfig
+ * scenario.hpp:18-31) on a 3-axis (x, y, tau) grid.  Column 0 =
+ * moving_vehicle: the agents' anticipated swept boxes (SplitMix64 seeded by
+ * mix_seed(seed, query_index), rasterize_box per agent per time slab);
+ * column 1 = not_nominal_lane: every cell outside the circular lane tube.
+ * The per-agent geometry and the per-(x, y) lane test run on the host with
+ * the reference's own arithmetic (libm cos / sin / hypot); the cells are
+ * written on the GPU.  Errors: the GridSpec messages; LTLG_EINVAL "scenario
+ * needs a 3-d (x, y, tau) grid", "horizon exceeds the grid's tau extent";
+ * LTLG_EDOMAIN "agent radius collapsed to the loop centre", "agent outside
+ * workspace". */
+typedef struct ltlg_scenario {
+    double loop_cx, loop_cy, loop_radius, lane_width;
+    int agent_count;
+    double agent_speed_min, agent_speed_max, agent_length, agent_width, lateral_spread, horizon;
+    uint64_t seed;
+} ltlg_scenario;
+
+/* out_words = 2 x ceil(2^depth/64) u64 (host): moving_vehicle, not_nominal_lane. */
+ltlg_status ltlg_generate_scenario(const ltlg_scenario* cfg, const ltlg_gridk* grid, uint64_t query_index,
+                                   int device, uint64_t* out_words);
+
+/* `frames` scenario queries (query_index0 + f) straight into the context's P
+ * (frames x 2 props: moving_vehicle = prop 0, not_nominal_lane = prop 1),
+ * then labelling; 2^depth must equal cols of T.  Asynchronous. */
+ltlg_status ltlg_submit_scenario(ltlg_ctx* ctx, const ltlg_scenario* cfg, const ltlg_gridk* grid,
+                                 uint64_t query_index0, int frames);
+
 /* Resident-label consumer: monitor transition guards
  * (TransitionGuard {positive, negative}, buchi.hpp:16-26; admits(s) =
  * (s & positive) == positive && (s & negative) == 0).  After every later

@@ -491,6 +491,27 @@ class RefCore:
             raise OracleError(msg.split(": ", 1)[-1])
         return rows, cols[:nnz]
 
+    def generate_scenario(self, cfg, agent_count, seed, lo, hi, depth, query_index):
+        """generate_scenario -> (moving_vehicle words, not_nominal_lane words)."""
+        L = self.lib
+        d = C.c_double
+        L.ref_generate_scenario.argtypes = [C.POINTER(d), C.c_int, C.c_uint64, C.POINTER(d), C.POINTER(d), C.c_int,
+                                            C.c_uint64, C.POINTER(C.c_uint64)]
+        L.ref_generate_scenario.restype = C.c_int
+        c = np.ascontiguousarray(cfg, dtype=np.float64)
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        hi = np.ascontiguousarray(hi, dtype=np.float64)
+        nw = ((1 << depth) + 63) // 64
+        out = np.zeros(2 * nw, dtype=np.uint64)
+        rc = L.ref_generate_scenario(_p(c, d), agent_count, seed, _p(lo, d), _p(hi, d), depth, query_index,
+                                     _p(out, C.c_uint64))
+        if rc:
+            msg = self.error()
+            if msg.startswith("domain_error: "):
+                raise DomainError(msg[len("domain_error: "):])
+            raise OracleError(msg)
+        return out[:nw], out[nw:]
+
     def free(self, m=None, p=None):
         if m:
             self.lib.ref_csr_free(m)

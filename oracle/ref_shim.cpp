@@ -28,6 +28,7 @@
 #include "ltlgrid/buchi.hpp"
 #include "ltlgrid/label.hpp"
 #include "ltlgrid/rng.hpp"
+#include "ltlgrid/scenario.hpp"
 
 namespace {
 
@@ -378,6 +379,40 @@ std::int64_t ref_swept_volume(int depth, const double* lo, const double* hi, dou
     } catch (const std::exception& e) {
         g_err = e.what();
         return -1;
+    }
+}
+
+// generate_scenario (scenario.cpp:52-128) on GridSpec({{lo, hi} x 3}, depth):
+// out = 2 x ceil(2^depth / 64) words, moving_vehicle then not_nominal_lane.
+// cfg = {loop_cx, loop_cy, loop_radius, lane_width, agent_speed_min,
+// agent_speed_max, agent_length, agent_width, lateral_spread, horizon}.
+int ref_generate_scenario(const double* cfg, int agent_count, std::uint64_t seed, const double* lo, const double* hi,
+                          int depth, std::uint64_t query_index, std::uint64_t* out) {
+    try {
+        ltlgrid::ScenarioConfig c;
+        c.loop_cx = cfg[0];
+        c.loop_cy = cfg[1];
+        c.loop_radius = cfg[2];
+        c.lane_width = cfg[3];
+        c.agent_speed_min = cfg[4];
+        c.agent_speed_max = cfg[5];
+        c.agent_length = cfg[6];
+        c.agent_width = cfg[7];
+        c.lateral_spread = cfg[8];
+        c.horizon = cfg[9];
+        c.agent_count = agent_count;
+        c.seed = seed;
+        const ltlgrid::GridSpec g({{lo[0], hi[0]}, {lo[1], hi[1]}, {lo[2], hi[2]}}, depth);
+        const auto v = ltlgrid::generate_scenario(c, g, query_index);
+        const auto a = v.moving_vehicle.words(), b = v.not_nominal_lane.words();
+        std::copy(a.begin(), a.end(), out);
+        std::copy(b.begin(), b.end(), out + a.size());
+        return 0;
+    } catch (const std::domain_error& e) {
+        g_err = std::string("domain_error: ") + e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        return fail(e);
     }
 }
 

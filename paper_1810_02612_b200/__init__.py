@@ -7,9 +7,10 @@ abstractions -- a drop-in for the reference's labeling path
   synth               synthetic T / P of the BASELINE configs
 """
 from .label import (CsrBoolMatrix, DensePropMatrix, DomainError, FootprintSpec, LabelEngine,  # noqa: F401
-                    LabelMatrix, LtlgError, OccupancyBitset, SweptVolume, label_all, rasterize_boxes,
+                    LabelMatrix, LtlgError, OccupancyBitset, ScenarioConfig, SweptVolume, generate_scenario,
+                    label_all, rasterize_boxes,
                     read_csb1_shape, read_zobv, swept_volume, swept_volume_matrix, to_csr)
 
 __all__ = ["CsrBoolMatrix", "DensePropMatrix", "DomainError", "FootprintSpec", "LabelEngine", "LabelMatrix",
-           "LtlgError", "OccupancyBitset", "SweptVolume", "label_all", "rasterize_boxes", "read_csb1_shape",
+           "LtlgError", "OccupancyBitset", "ScenarioConfig", "SweptVolume", "generate_scenario", "label_all", "rasterize_boxes", "read_csb1_shape",
            "read_zobv", "swept_volume", "swept_volume_matrix", "to_csr"]

@@ -27,7 +27,7 @@ EXPORTS = [
     "ltlg_rasterize_boxes", "ltlg_submit_boxes", "ltlg_set_guards", "ltlg_get_admitted", "ltlg_device_admitted",
     "ltlg_submit_grid_device_ex",
     "ltlg_swept_volume", "ltlg_csr_rows", "ltlg_csr_cols", "ltlg_csr_nnz", "ltlg_csr_build_ms", "ltlg_csr_copy",
-    "ltlg_load_csr", "ltlg_csr_free", "ltlg_set_profiling",
+    "ltlg_load_csr", "ltlg_csr_free", "ltlg_set_profiling", "ltlg_generate_scenario", "ltlg_submit_scenario",
 ]
 
 
@@ -38,6 +38,13 @@ class Options(C.Structure):
 
 class GridK(C.Structure):
     _fields_ = [("dims", C.c_int), ("depth", C.c_int), ("lo", C.c_double * 4), ("hi", C.c_double * 4)]
+
+
+class Scenario(C.Structure):
+    _fields_ = [("loop_cx", C.c_double), ("loop_cy", C.c_double), ("loop_radius", C.c_double),
+                ("lane_width", C.c_double), ("agent_count", C.c_int), ("agent_speed_min", C.c_double),
+                ("agent_speed_max", C.c_double), ("agent_length", C.c_double), ("agent_width", C.c_double),
+                ("lateral_spread", C.c_double), ("horizon", C.c_double), ("seed", C.c_uint64)]
 
 
 class Footprint(C.Structure):
@@ -120,6 +127,8 @@ def lib() -> C.CDLL:
         "ltlg_load_csr": ([ctxp, vp], i32),
         "ltlg_csr_free": ([vp], None),
         "ltlg_set_profiling": ([ctxp, i32], i32),
+        "ltlg_generate_scenario": ([C.POINTER(Scenario), C.POINTER(GridK), u64, i32, vp], i32),
+        "ltlg_submit_scenario": ([ctxp, C.POINTER(Scenario), C.POINTER(GridK), u64, i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

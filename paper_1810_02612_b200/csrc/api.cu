@@ -120,6 +120,7 @@ struct Shard {
     DevBuf<uint64_t> poses_off;  // box offsets of ltlg_submit_boxes
     DevBuf<uint64_t> admitted;   // guard consumer: rows x frames admitted-guard masks
     DevBuf<uint64_t> guard_lut;  // its byte lookup table (8 x 256)
+    DevBuf<uint64_t> lane_flags;  // ltlg_submit_scenario: per-(x, y) not-nominal-lane flags
     uint64_t guard_lut_key = ~0ull;  // (guard epoch, props) the uploaded table is for
     DevBuf<uint8_t> box_rng;     // and their per-axis cell ranges
     DevBuf<uint32_t> ctr;  // persistent-kernel task counter
@@ -692,6 +693,7 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.poses_off.release();
         s.admitted.release();
         s.guard_lut.release();
+        s.lane_flags.release();
         s.box_rng.release();
         s.ctr.release();
         s.s_only.release();
@@ -1001,6 +1003,178 @@ ltlg_status ltlg_submit_boxes(ltlg_ctx* ctx, const ltlg_gridk* grid, int num_pro
     if ((st = rasterize_on(ctx, grid, cols, box_offsets, box_lo, box_hi, s0.poses_off, s0.box_rng, s0.P.ptr, s0.stream)) !=
         LTLG_OK)
         return st;
+    if ((st = broadcast_P(ctx, nwords)) != LTLG_OK) return st;
+    return run_label(ctx, false);
+}
+
+}  // extern "C"
+
+namespace {
+
+// SplitMix64 / mix_seed (rng.hpp:10-35)
+struct Splitmix {
+    uint64_t state;
+    uint64_t next() {
+        uint64_t z = (state += 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+    double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+};
+uint64_t mix_seed(uint64_t seed, uint64_t stream) {
+    Splitmix r{seed ^ (stream * 0x9e3779b97f4a7c15ull + 0x2545f4914f6cdd1dull)};
+    return r.next();
+}
+
+// generate_scenario's host geometry (scenario.cpp:52-128), the same double
+// operations in the same order: the agents' boxes of one query (3 lo + 3 hi
+// doubles each) and, if lane != nullptr, the per-(cx, cy) not-nominal flags
+// (bit cy * nx + cx).
+ltlg_status scenario_geometry(ltlg_ctx* ctx, const ltlg_scenario* c, const ltlg_gridk* g, uint64_t query,
+                              std::vector<double>* blo, std::vector<double>* bhi, std::vector<uint64_t>* lane) {
+    constexpr double kPi = 3.14159265358979323846;
+    if (g->dims != 3) return set_err(ctx, LTLG_EINVAL, "scenario needs a 3-d (x, y, tau) grid");
+    if (c->horizon > g->hi[2] - g->lo[2] + 1e-9)
+        return set_err(ctx, LTLG_EINVAL, "horizon exceeds the grid's tau extent");
+    int bits[3];
+    double w[3];
+    for (int a = 0; a < 3; ++a) {
+        bits[a] = g->depth / 3 + (a < g->depth % 3 ? 1 : 0);
+        w[a] = (g->hi[a] - g->lo[a]) / static_cast<double>(uint64_t(1) << bits[a]);  // GridSpec::cell_width
+    }
+    const uint64_t nx = uint64_t(1) << bits[0], ny = uint64_t(1) << bits[1], nt = uint64_t(1) << bits[2];
+    if (lane) {
+        lane->assign((nx * ny + 63) / 64, 0);
+        const double half_lane = c->lane_width / 2;
+        for (uint64_t cx = 0; cx < nx; ++cx) {
+            const double x = g->lo[0] + (static_cast<double>(cx) + 0.5) * w[0];
+            for (uint64_t cy = 0; cy < ny; ++cy) {
+                const double y = g->lo[1] + (static_cast<double>(cy) + 0.5) * w[1];
+                const double r = std::hypot(x - c->loop_cx, y - c->loop_cy);
+                if (std::abs(r - c->loop_radius) <= half_lane) continue;  // nominal lane
+                const uint64_t f = cy * nx + cx;
+                (*lane)[f >> 6] |= uint64_t(1) << (f & 63);
+            }
+        }
+    }
+    Splitmix rng{mix_seed(c->seed, query)};
+    const double w_tau = w[2];
+    for (int agent = 0; agent < c->agent_count; ++agent) {
+        const double angle0 = rng.uniform(0, 2 * kPi);
+        const double direction = rng.uniform() < 0.5 ? 1.0 : -1.0;
+        const double speed = rng.uniform(c->agent_speed_min, c->agent_speed_max);
+        const double radius = c->loop_radius + rng.uniform(-c->lateral_spread, c->lateral_spread);
+        if (radius <= 1.0) return set_err(ctx, LTLG_EDOMAIN, "agent radius collapsed to the loop centre");
+        const double omega = direction * speed / radius;
+        auto extent = [&](double tau, double& x_lo, double& x_hi, double& y_lo, double& y_hi) {
+            const double phi = angle0 + omega * tau;
+            const double px = c->loop_cx + radius * std::cos(phi);
+            const double py = c->loop_cy + radius * std::sin(phi);
+            const double heading = phi + direction * kPi / 2;
+            const double ext_x = c->agent_length / 2 * std::abs(std::cos(heading)) +
+                                 c->agent_width / 2 * std::abs(std::sin(heading));
+            const double ext_y = c->agent_length / 2 * std::abs(std::sin(heading)) +
+                                 c->agent_width / 2 * std::abs(std::cos(heading));
+            x_lo = px - ext_x;
+            x_hi = px + ext_x;
+            y_lo = py - ext_y;
+            y_hi = py + ext_y;
+        };
+        const auto slabs = static_cast<uint64_t>(std::min<double>(static_cast<double>(nt), std::ceil(c->horizon / w_tau)));
+        for (uint64_t ct = 0; ct < slabs; ++ct) {
+            const double tau_a = static_cast<double>(ct) * w_tau;
+            const double tau_b = tau_a + w_tau;
+            double ax0, ax1, ay0, ay1, bx0, bx1, by0, by1;
+            extent(tau_a, ax0, ax1, ay0, ay1);
+            extent(tau_b, bx0, bx1, by0, by1);
+            const double lo[3] = {std::min(ax0, bx0), std::min(ay0, by0),
+                                  g->lo[2] + (static_cast<double>(ct) + 0.25) * w_tau};
+            const double hi[3] = {std::max(ax1, bx1), std::max(ay1, by1),
+                                  g->lo[2] + (static_cast<double>(ct) + 0.75) * w_tau};
+            if (lo[0] < g->lo[0] || hi[0] > g->hi[0] || lo[1] < g->lo[1] || hi[1] > g->hi[1])
+                return set_err(ctx, LTLG_EDOMAIN, "agent outside workspace");
+            blo->insert(blo->end(), lo, lo + 3);
+            bhi->insert(bhi->end(), hi, hi + 3);
+        }
+    }
+    return LTLG_OK;
+}
+
+// frames scenario queries into P (device): column 2 f = moving_vehicle of
+// query q0 + f, column 2 f + 1 = not_nominal_lane.
+ltlg_status scenario_on(ltlg_ctx* ctx, const ltlg_scenario* c, const ltlg_gridk* g, uint64_t q0, int frames,
+                        Shard& s, uint64_t* P) {
+    std::vector<double> blo, bhi;
+    std::vector<uint64_t> lane, off(static_cast<size_t>(2 * frames) + 1, 0);
+    for (int f = 0; f < frames; ++f) {
+        const ltlg_status st = scenario_geometry(ctx, c, g, q0 + static_cast<uint64_t>(f), &blo, &bhi,
+                                                 f == 0 ? &lane : nullptr);
+        if (st != LTLG_OK) return st;
+        off[static_cast<size_t>(2 * f) + 1] = blo.size() / 3;  // moving_vehicle: this query's boxes
+        off[static_cast<size_t>(2 * f) + 2] = blo.size() / 3;  // not_nominal_lane: no boxes (lane kernel)
+    }
+    ltlg_status st = rasterize_on(ctx, g, 2 * frames, off.data(), blo.data(), bhi.data(), s.poses_off, s.box_rng, P,
+                                  s.stream);
+    if (st != LTLG_OK) return st;
+    CK(s.lane_flags.reserve(lane.size() * 8), "allocate lane flags");
+    CK(cudaMemcpyAsync(s.lane_flags.ptr, lane.data(), lane.size() * 8, cudaMemcpyHostToDevice, s.stream), "upload lane");
+    CK(launch_lane(g->depth, s.lane_flags.ptr, frames, 1, 2, P, s.stream), "lane kernel");
+    CK(cudaStreamSynchronize(s.stream), "scenario");  // the pageable lane flags are read before they go away
+    return LTLG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ltlg_status ltlg_generate_scenario(const ltlg_scenario* cfg, const ltlg_gridk* grid, uint64_t query_index,
+                                   int device, uint64_t* out_words) {
+    if (!cfg || !out_words) return set_err(nullptr, LTLG_EINVAL, "null argument");
+    ltlg_status st = check_gridk(nullptr, grid);
+    if (st != LTLG_OK) return st;
+    ltlg_ctx* ctx = nullptr;
+    const int devs[1] = {device};
+    if ((st = ltlg_create(devs, 1, &ctx)) != LTLG_OK) return st;
+    std::unique_ptr<ltlg_ctx, void (*)(ltlg_ctx*)> hold(ctx, ltlg_destroy);
+    Shard& s0 = ctx->shards[0];
+    const size_t nw = ((uint64_t(1) << grid->depth) + 63) / 64;
+    CK(s0.P.reserve(2 * nw * 8 + 8), "allocate P");
+    if ((st = scenario_on(ctx, cfg, grid, query_index, 1, s0, s0.P.ptr)) != LTLG_OK) {
+        g_error = ctx->err;
+        return st;
+    }
+    cudaError_t e = cudaMemcpy(out_words, s0.P.ptr, 2 * nw * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(nullptr, e, "download P");
+    return LTLG_OK;
+}
+
+ltlg_status ltlg_submit_scenario(ltlg_ctx* ctx, const ltlg_scenario* cfg, const ltlg_gridk* grid,
+                                 uint64_t query_index0, int frames) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!cfg) return set_err(ctx, LTLG_EINVAL, "null argument");
+    ltlg_status st = check_gridk(ctx, grid);
+    if (st != LTLG_OK) return st;
+    const uint64_t cells = uint64_t(1) << grid->depth;
+    if ((st = check_grid(ctx, cells, 2, frames)) != LTLG_OK) return st;
+    ctx->cells = cells;
+    ctx->props = 2;
+    ctx->frames = frames;
+    ctx->label_bytes = label_bytes_for(2);
+    const size_t nwords = static_cast<size_t>(frames) * 2 * ((cells + 63) / 64);
+    for (Shard& s : ctx->shards) {
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        CK(s.P.reserve(nwords * 8 + 16), "allocate P");
+    }
+    if (ctx->opts.profile)
+        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
+    Shard& s0 = ctx->shards[0];
+    CK(cudaSetDevice(s0.device), "cudaSetDevice");
+    s0.P_in = nullptr;
+    s0.P_host = nullptr;
+    if (ctx->opts.profile) CK(cudaEventRecord(s0.ev[0], s0.stream), "event");
+    if ((st = scenario_on(ctx, cfg, grid, query_index0, frames, s0, s0.P.ptr)) != LTLG_OK) return st;
     if ((st = broadcast_P(ctx, nwords)) != LTLG_OK) return st;
     return run_label(ctx, false);
 }

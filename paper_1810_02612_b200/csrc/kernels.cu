@@ -2135,6 +2135,48 @@ cudaError_t launch_guards(const void* labels, int label_bytes, uint64_t n, const
 }
 
 // ranges: nboxes x (first, last) per axis (4 axes, int64), box_off: cols + 1
+// generate_scenario's not_nominal_lane (scenario.cpp:59-76): a cell (cx, cy,
+// ct) is set iff flag bit cy * nx + cx is set (the host evaluates the lane
+// test per (cx, cy) with the reference's libm hypot); the same column goes to
+// ncols columns out + (col0 + c * col_step) * nw64.
+__device__ __forceinline__ uint64_t compact3(uint64_t x) {
+    x &= 0x1249249249249249ull;
+    x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ull;
+    x = (x ^ (x >> 4)) & 0x100f00f00f00f00full;
+    x = (x ^ (x >> 8)) & 0x1f0000ff0000ffull;
+    x = (x ^ (x >> 16)) & 0x1f00000000ffffull;
+    x = (x ^ (x >> 32)) & 0x1fffffull;
+    return x;
+}
+
+__global__ void __launch_bounds__(256) lane_kernel(uint32_t nw64, uint64_t cells, int off0, int off1, int bits0,
+                                                   const uint64_t* __restrict__ flags, int ncols, int col0,
+                                                   int col_step, uint64_t* __restrict__ out) {
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nw64) return;
+    uint64_t v = 0;
+    for (int b = 0; b < 64; ++b) {
+        const uint64_t i = static_cast<uint64_t>(w) * 64 + b;
+        if (i >= cells) break;
+        const uint64_t cx = compact3(i >> off0), cy = compact3(i >> off1);
+        const uint64_t f = (cy << bits0) | cx;
+        v |= ((flags[f >> 6] >> (f & 63)) & 1ull) << b;
+    }
+    for (int c = 0; c < ncols; ++c) out[static_cast<uint64_t>(col0 + c * col_step) * nw64 + w] = v;
+}
+
+cudaError_t launch_lane(int depth, const uint64_t* flags, int ncols, int col0, int col_step, uint64_t* out,
+                        cudaStream_t st) {
+    const uint64_t cells = uint64_t(1) << depth;
+    const uint32_t nw64 = static_cast<uint32_t>((cells + 63) / 64);
+    const int r = depth % 3;
+    auto off = [&](int a) { return r + 2 - a - 3 * (a < r ? 1 : 0); };
+    const int bits0 = depth / 3 + (0 < r ? 1 : 0);
+    lane_kernel<<<(nw64 + 255) / 256, 256, 0, st>>>(nw64, cells, off(0), off(1), bits0, flags, ncols, col0, col_step,
+                                                    out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_rasterize(int k, int depth, int cols_total, const uint64_t* box_off, const int64_t* ranges,
                              uint64_t* out, cudaStream_t st) {
     if (k < 1 || k > 4 || depth < k || depth > 36) return cudaErrorInvalidValue;

@@ -63,6 +63,8 @@ cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, i
                            uint64_t* out, cudaStream_t st);
 cudaError_t launch_guards(const void* labels, int label_bytes, uint64_t n, const uint64_t* lut, uint64_t always,
                           uint64_t all_guards, uint64_t* admitted, cudaStream_t st);
+cudaError_t launch_lane(int depth, const uint64_t* flags, int ncols, int col0, int col_step, uint64_t* out,
+                        cudaStream_t st);
 cudaError_t launch_rasterize(int k, int depth, int cols_total, const uint64_t* box_off, const int64_t* ranges,
                              uint64_t* out, cudaStream_t st);
 cudaError_t launch_resample(int vdepth, double vlo0, double vhi0, double vlo1, double vhi1, int wdepth,

@@ -364,6 +364,15 @@ class LabelEngine:
             _raise(st, self._L.ltlg_last_error(self._h).decode())
 
     # -- load abstraction ---------------------------------------------------
+    def submit_scenario(self, cfg: Optional["ScenarioConfig"] = None, bounds=None, depth: int = 21,
+                        query_index0: int = 0, frames: int = 1) -> None:
+        """ltlg_submit_scenario: `frames` generate_scenario queries straight into P
+        (prop 0 = moving_vehicle, prop 1 = not_nominal_lane), then labelling."""
+        bounds = bounds or DEFAULT_BENCH_BOUNDS
+        c = (cfg or ScenarioConfig())._c()
+        g = _gridk(len(bounds), depth, [b[0] for b in bounds], [b[1] for b in bounds])
+        self._ck(self._L.ltlg_submit_scenario(self._h, C.byref(c), C.byref(g), int(query_index0), frames))
+
     def load_swept_volume(self, sv: "SweptVolume") -> None:
         """ltlg_load_csr: the GPU-built swept-volume matrix as this engine's T."""
         self._ck(self._L.ltlg_load_csr(self._h, sv._h))
@@ -528,6 +537,43 @@ def rasterize_boxes(dims: int, depth: int, lo, hi, columns, device: int = 0) -> 
     if st:
         _raise(st, L.ltlg_last_error(None).decode())
     return out[: len(columns)]
+
+
+class ScenarioConfig:
+    """The reference benchmark scenario (ScenarioConfig, scenario.hpp:18-31); defaults are the reference's."""
+
+    def __init__(self, loop_cx=36.0, loop_cy=36.0, loop_radius=24.0, lane_width=4.2, agent_count=3,
+                 agent_speed_min=8.0, agent_speed_max=14.0, agent_length=4.6, agent_width=2.0, lateral_spread=3.5,
+                 horizon=7.2, seed=1):
+        self.loop_cx, self.loop_cy, self.loop_radius, self.lane_width = loop_cx, loop_cy, loop_radius, lane_width
+        self.agent_count = agent_count
+        self.agent_speed_min, self.agent_speed_max = agent_speed_min, agent_speed_max
+        self.agent_length, self.agent_width, self.lateral_spread = agent_length, agent_width, lateral_spread
+        self.horizon, self.seed = horizon, seed
+
+    def _c(self):
+        return N.Scenario(float(self.loop_cx), float(self.loop_cy), float(self.loop_radius), float(self.lane_width),
+                          int(self.agent_count), float(self.agent_speed_min), float(self.agent_speed_max),
+                          float(self.agent_length), float(self.agent_width), float(self.lateral_spread),
+                          float(self.horizon), int(self.seed))
+
+
+DEFAULT_BENCH_BOUNDS = ((0.0, 72.0), (0.0, 72.0), (0.0, 7.2))  # default_bench_grid (scenario.cpp:20-22)
+
+
+def generate_scenario(cfg: Optional[ScenarioConfig] = None, bounds=DEFAULT_BENCH_BOUNDS, depth: int = 21,
+                      query_index: int = 0, device: int = 0):
+    """GPU generate_scenario (scenario.cpp:52-128): (moving_vehicle, not_nominal_lane)
+    as OccupancyBitsets of the (x, y, tau) grid GridSpec(bounds, depth)."""
+    L = N.lib()
+    c = (cfg or ScenarioConfig())._c()
+    g = _gridk(len(bounds), depth, [b[0] for b in bounds], [b[1] for b in bounds])
+    nw = ((1 << depth) + 63) // 64
+    out = np.zeros(2 * nw, dtype=np.uint64)
+    st = L.ltlg_generate_scenario(C.byref(c), C.byref(g), int(query_index), device, out.ctypes.data)
+    if st:
+        _raise(st, L.ltlg_last_error(None).decode())
+    return (OccupancyBitset.from_words(1 << depth, out[:nw]), OccupancyBitset.from_words(1 << depth, out[nw:]))
 
 
 class FootprintSpec:
