@@ -465,6 +465,29 @@ class RefCore:
         finally:
             L.ref_abstraction_free(h)
 
+    def loop_abstraction(self, depth, target_edges, seed=1):
+        """The reference benchmark roadmap (loop_abstraction_config + build_abstraction)
+        -> (sample_off u64, samples (n, 5) f64)."""
+        L = self.lib
+        u64, d = C.c_uint64, C.c_double
+        L.ref_loop_abstraction_create.argtypes = [C.c_int, u64, u64]
+        L.ref_loop_abstraction_create.restype = C.c_void_p
+        L.ref_abstraction_sizes.argtypes = [C.c_void_p, C.POINTER(u64), C.POINTER(u64)]
+        L.ref_abstraction_export.argtypes = [C.c_void_p, C.POINTER(u64), C.POINTER(d)]
+        L.ref_abstraction_free.argtypes = [C.c_void_p]
+        h = L.ref_loop_abstraction_create(depth, target_edges, seed)
+        if not h:
+            raise RuntimeError(self.error())
+        try:
+            e, n = u64(0), u64(0)
+            L.ref_abstraction_sizes(h, C.byref(e), C.byref(n))
+            off = np.zeros(e.value + 1, dtype=np.uint64)
+            smp = np.zeros((max(n.value, 1), 5), dtype=np.float64)
+            L.ref_abstraction_export(h, _p(off, u64), _p(smp, d))
+            return off, smp[: n.value]
+        finally:
+            L.ref_abstraction_free(h)
+
     def swept_volume(self, depth, lo, hi, footprint, sample_off, samples, workers=0):
         """The reference swept_volume_matrix -> (row_offsets u64, cols u32)."""
         L = self.lib

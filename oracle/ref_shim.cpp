@@ -316,6 +316,21 @@ void* ref_abstraction_create(double x_min, double x_max, double y_min, double y_
     }
 }
 
+// The reference benchmark's roadmap: build_abstraction(loop_abstraction_config(
+// ScenarioConfig{}, default_bench_grid(depth), target_edges), seed)
+// (scenario.cpp:20-46, abstraction.cpp:299).
+void* ref_loop_abstraction_create(int depth, std::uint64_t target_edges, std::uint64_t seed) {
+    try {
+        const ltlgrid::ScenarioConfig cfg;
+        const ltlgrid::GridSpec g = ltlgrid::default_bench_grid(depth);
+        return new ltlgrid::TransitionSystem(
+            ltlgrid::build_abstraction(ltlgrid::loop_abstraction_config(cfg, g, target_edges), seed));
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
 void ref_abstraction_sizes(void* h, std::uint64_t* edges, std::uint64_t* samples) {
     const auto* ts = static_cast<const ltlgrid::TransitionSystem*>(h);
     *edges = ts->num_edges();
