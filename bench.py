@@ -220,6 +220,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="short run for profilers")
+    ap.add_argument("--dump-labels", default="", help="(tests) write a row sample of each rank's labels "
+                    "after the timed steps to <prefix>_rank<r>.npz")
     ap.add_argument("--readback-chunks", type=int, default=8,
                     help="ltlg_options.readback_chunks of the e2e engine: row blocks whose label read-back "
                          "overlaps labelling (the device-resident `value` engine uses one block: globally "
@@ -272,17 +274,41 @@ def main():
     if rank == 0:
         P_dev.copy_(P_host)
     stream = torch.cuda.ExternalStream(eng.stream())
+    # N > 1: P is double-buffered and the broadcast of step k+1's P runs on a
+    # comm stream while step k labels (overlap the broadcast of
+    # frame f+1 with the labelling of frame f, chained by events).  The
+    # broadcast into a buffer waits for the labelling that last read it; the
+    # labelling waits for its broadcast.  No tensor is recorded on the
+    # engine's stream.
+    P_bufs = [P_dev, P_dev.clone()] if world > 1 else [P_dev]
+    comm = torch.cuda.Stream() if world > 1 else None
+    ready = [None, None]  # broadcast into buffer b done (event on comm)
+    done = [None, None]   # labelling that read buffer b done (event on the engine stream)
+    nstep = [0]
+
+    def bcast(b):
+        with torch.cuda.stream(comm):
+            if done[b] is not None:
+                comm.wait_event(done[b])
+            dist.broadcast(P_bufs[b], src=0)
+            ev = torch.cuda.Event()
+            ev.record(comm)
+            ready[b] = ev
+
+    if world > 1:
+        bcast(0)
 
     def step():
+        b = nstep[0] % len(P_bufs)
+        nstep[0] += 1
         if world > 1:
-            # the broadcast runs on torch's stream, ordered after the engine's
-            # previous labelling (which reads P_dev in place) and before the
-            # next one -- no tensor is ever recorded on the engine's stream
-            cur = torch.cuda.current_stream()
-            cur.wait_stream(stream)
-            dist.broadcast(P_dev, src=0)
-            stream.wait_stream(cur)
-        eng.submit_grid_device(cells, props, P_dev.data_ptr(), F)
+            stream.wait_event(ready[b])
+        eng.submit_grid_device(cells, props, P_bufs[b].data_ptr(), F)
+        if world > 1:
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            done[b] = ev
+            bcast(1 - b)  # the next step's P, overlapped with this labelling
 
     for _ in range(args.warmup):
         step()
@@ -310,6 +336,10 @@ def main():
     ms = e0.elapsed_time(e1)
     # per-launch device times of the K timed launches (event ring on the launching stream)
     kernel_ms = [eng.stage_times(0, back)[1:] for back in range(min(K, 255))]
+    if args.dump_labels:
+        lab = eng.get_labels_packed()
+        pick = np.arange(0, r1 - r0, 997)
+        np.savez(f"{args.dump_labels}_rank{rank}.npz", rows=pick + r0, labels=lab[pick])
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -443,8 +473,7 @@ def main():
             "shape": {"W32": W32, "rows": rows_all, "t_bytes_device": int(info.t_bytes)},
         }
         print(json.dumps(line), flush=True)
-    # collectives ran on the engine's stream: tear the process group down
-    # before the engine (and its stream) goes away
+    # tear the process group down before the engine (and its stream) goes away
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

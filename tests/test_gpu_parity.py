@@ -424,7 +424,7 @@ def test_sharded_engine_on_one_device(devices):
     eng.close()
 
 
-def test_bench_two_ranks_on_one_gpu():
+def test_bench_two_ranks_on_one_gpu(tmp_path):
     """bench.py's N > 1 path (rank shards, P broadcast each step, max-over-ranks
     timing, teardown) under torchrun with two ranks sharing cuda:0 over gloo
     (NCCL refuses two ranks on one device): it must finish cleanly and rank 0
@@ -437,12 +437,29 @@ def test_bench_two_ranks_on_one_gpu():
     env = dict(os.environ, BENCH_DIST_BACKEND="gloo", BENCH_FORCE_DEVICE="0")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", "29633", "bench.py", "--gpus", "2",
-                        "--steps", "3", "--warmup", "3", "--quick", "--no-cpu-baseline"],
+                        "--steps", "3", "--warmup", "3", "--quick", "--no-cpu-baseline",
+                        "--dump-labels", os.path.join(str(tmp_path), "two")],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
     assert lines[0]["e2e"]["value"] > 0
+    # the two rank shards (double-buffered P broadcast overlapped with the
+    # labelling) label exactly like one rank over all edges
+    r1 = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--quick", "--no-cpu-baseline",
+                         "--no-e2e", "--dump-labels", os.path.join(str(tmp_path), "one")],
+                        cwd=root, capture_output=True, text=True, timeout=900)
+    assert r1.returncode == 0, r1.stderr[-3000:]
+    one = np.load(os.path.join(str(tmp_path), "one_rank0.npz"))
+    pos = {int(x): i for i, x in enumerate(one["rows"])}
+    checked = 0
+    for rank in (0, 1):
+        d = np.load(os.path.join(str(tmp_path), f"two_rank{rank}.npz"))
+        for row, lab in zip(d["rows"], d["labels"]):
+            if int(row) in pos:
+                assert np.array_equal(lab, one["labels"][pos[int(row)]]), (rank, int(row))
+                checked += 1
+    assert checked > 100
 
 
 def test_cpp_drop_in_parity():
