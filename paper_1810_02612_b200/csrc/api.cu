@@ -58,6 +58,24 @@ Nccl& nccl() {
     return n;
 }
 
+// Every entry point leaves the caller's current CUDA device as it found it
+// (the engine switches devices per shard).
+struct DeviceGuard {
+    int dev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&dev) != cudaSuccess) {
+            dev = -1;
+            cudaGetLastError();
+        }
+    }
+    ~DeviceGuard() {
+        int now = -1;
+        if (dev >= 0 && cudaGetDevice(&now) == cudaSuccess && now != dev) cudaSetDevice(dev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 template <typename T>
 struct DevBuf {
     T* ptr = nullptr;
@@ -600,6 +618,7 @@ int ltlg_abi_version(void) { return LTLG_ABI_VERSION; }
 const char* ltlg_last_error(const ltlg_ctx* ctx) { return ctx ? ctx->err.c_str() : g_error.c_str(); }
 
 ltlg_status ltlg_create_ex(const int* devices, int n_devices, const ltlg_options* opts, ltlg_ctx** out) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!out) return set_err(nullptr, LTLG_EINVAL, "null output handle");
     *out = nullptr;
     if (n_devices < 1) n_devices = 1;
@@ -665,6 +684,7 @@ ltlg_status ltlg_create(const int* devices, int n_devices, ltlg_ctx** out) {
 }
 
 void ltlg_destroy(ltlg_ctx* ctx) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return;
     for (ncclComm_t c : ctx->comms) nccl().CommDestroy(c);
     for (Shard& s : ctx->shards) {
@@ -708,6 +728,7 @@ void ltlg_destroy(ltlg_ctx* ctx) {
 
 ltlg_status ltlg_load_abstraction(ltlg_ctx* ctx, uint64_t rows, uint64_t cols, const uint64_t* row_offsets,
                                   const uint32_t* col_indices) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!row_offsets) return set_err(ctx, LTLG_EINVAL, "row_offsets must have rows+1 entries");
     Error err{S_OK, ""};
@@ -723,6 +744,7 @@ ltlg_status ltlg_load_abstraction(ltlg_ctx* ctx, uint64_t rows, uint64_t cols, c
 }
 
 ltlg_status ltlg_load_abstraction_file(ltlg_ctx* ctx, const char* path) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!path) return set_err(ctx, LTLG_EINVAL, "null path");
     Error err{S_OK, ""};
@@ -733,6 +755,7 @@ ltlg_status ltlg_load_abstraction_file(ltlg_ctx* ctx, const char* path) {
 
 ltlg_status ltlg_load_abstraction_words(ltlg_ctx* ctx, uint64_t rows, uint64_t cols, const uint64_t* row_word_offsets,
                                         const uint32_t* word_index, const uint32_t* word_mask) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!row_word_offsets) return set_err(ctx, LTLG_EINVAL, "row_offsets must have rows+1 entries");
     if (row_word_offsets[rows] && (!word_index || !word_mask))
@@ -746,22 +769,26 @@ ltlg_status ltlg_load_abstraction_words(ltlg_ctx* ctx, uint64_t rows, uint64_t c
 }
 
 ltlg_status ltlg_submit_grid(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* column_words, int frames) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     return submit(ctx, cells, num_props, column_words, frames, false, true);
 }
 
 ltlg_status ltlg_submit_grid_device(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* dev_words,
                                     int frames) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     return submit(ctx, cells, num_props, dev_words, frames, true, false);
 }
 
 ltlg_status ltlg_submit_grid_device_ex(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* dev_words,
                                        int frames, int readback) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     return submit(ctx, cells, num_props, dev_words, frames, true, readback != 0);
 }
 
 ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, const ltlg_grid2* world, int num_props,
                                    const uint64_t* world_words, int words_on_device, const ltlg_pose2* poses,
                                    int frames, int outside) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!vehicle || !world || !poses) return set_err(ctx, LTLG_EINVAL, "null grid or pose");
     if (vehicle->depth < 2 || vehicle->depth > 32 || world->depth < 2 || world->depth > 32)
@@ -812,6 +839,7 @@ ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, con
 }
 
 ltlg_status ltlg_submit_grid_files(ltlg_ctx* ctx, const char* const* paths, int num_props, int frames) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!ctx->loaded) return set_err(ctx, LTLG_ESTATE, "no abstraction loaded");
     if (num_props > 64) return set_err(ctx, LTLG_EINVAL, "at most 64 propositions");
@@ -840,6 +868,7 @@ ltlg_status ltlg_submit_grid_files(ltlg_ctx* ctx, const char* const* paths, int 
 }
 
 ltlg_status ltlg_save_labels(ltlg_ctx* ctx, int frame, const char* path) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!path) return set_err(ctx, LTLG_EINVAL, "null path");
     if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
@@ -951,6 +980,7 @@ extern "C" {
 
 ltlg_status ltlg_rasterize_boxes(const ltlg_gridk* grid, int num_cols, const uint64_t* box_offsets,
                                  const double* box_lo, const double* box_hi, int device, uint64_t* out_words) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     ltlg_ctx* ctx = nullptr;
     ltlg_status st = check_gridk(nullptr, grid);
     if (st != LTLG_OK) return st;
@@ -977,6 +1007,7 @@ ltlg_status ltlg_rasterize_boxes(const ltlg_gridk* grid, int num_cols, const uin
 
 ltlg_status ltlg_submit_boxes(ltlg_ctx* ctx, const ltlg_gridk* grid, int num_props, int frames,
                               const uint64_t* box_offsets, const double* box_lo, const double* box_hi) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     ltlg_status st = check_gridk(ctx, grid);
     if (st != LTLG_OK) return st;
@@ -1131,6 +1162,7 @@ extern "C" {
 
 ltlg_status ltlg_generate_scenario(const ltlg_scenario* cfg, const ltlg_gridk* grid, uint64_t query_index,
                                    int device, uint64_t* out_words) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!cfg || !out_words) return set_err(nullptr, LTLG_EINVAL, "null argument");
     ltlg_status st = check_gridk(nullptr, grid);
     if (st != LTLG_OK) return st;
@@ -1152,6 +1184,7 @@ ltlg_status ltlg_generate_scenario(const ltlg_scenario* cfg, const ltlg_gridk* g
 
 ltlg_status ltlg_submit_scenario(ltlg_ctx* ctx, const ltlg_scenario* cfg, const ltlg_gridk* grid,
                                  uint64_t query_index0, int frames) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!cfg) return set_err(ctx, LTLG_EINVAL, "null argument");
     ltlg_status st = check_gridk(ctx, grid);
@@ -1180,6 +1213,7 @@ ltlg_status ltlg_submit_scenario(ltlg_ctx* ctx, const ltlg_scenario* cfg, const 
 }
 
 ltlg_status ltlg_set_guards(ltlg_ctx* ctx, int n_guards, const uint64_t* positive, const uint64_t* negative) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (n_guards < 0 || n_guards > 64) return set_err(ctx, LTLG_EINVAL, "guards must be in [0, 64]");
     if (n_guards && (!positive || !negative)) return set_err(ctx, LTLG_EINVAL, "null guards");
@@ -1190,6 +1224,7 @@ ltlg_status ltlg_set_guards(ltlg_ctx* ctx, int n_guards, const uint64_t* positiv
 }
 
 ltlg_status ltlg_get_admitted(ltlg_ctx* ctx, int frame, uint64_t* out) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
     if (ctx->guard_pos.empty()) return set_err(ctx, LTLG_ESTATE, "no guards set");
@@ -1207,6 +1242,7 @@ ltlg_status ltlg_get_admitted(ltlg_ctx* ctx, int frame, uint64_t* out) {
 }
 
 ltlg_status ltlg_device_admitted(ltlg_ctx* ctx, int shard, void** dev_ptr) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx || !dev_ptr) return set_err(ctx, LTLG_EINVAL, "null argument");
     if (shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return set_err(ctx, LTLG_EINVAL, "shard out of range");
     if (!ctx->submitted || ctx->guard_pos.empty()) return set_err(ctx, LTLG_ESTATE, "no guarded submit");
@@ -1215,11 +1251,13 @@ ltlg_status ltlg_device_admitted(ltlg_ctx* ctx, int shard, void** dev_ptr) {
 }
 
 ltlg_status ltlg_wait(ltlg_ctx* ctx) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     return sync_all(ctx);
 }
 
 ltlg_status ltlg_get_labels(ltlg_ctx* ctx, int frame, uint64_t* out) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
     if (frame < 0 || frame >= ctx->frames) return set_err(ctx, LTLG_EINVAL, "frame out of range");
@@ -1238,6 +1276,7 @@ ltlg_status ltlg_get_labels(ltlg_ctx* ctx, int frame, uint64_t* out) {
 }
 
 ltlg_status ltlg_get_labels_packed(ltlg_ctx* ctx, void* out, size_t out_bytes) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
     const size_t per_row = static_cast<size_t>(ctx->frames) * static_cast<size_t>(ctx->label_bytes);
@@ -1274,6 +1313,7 @@ ltlg_status ltlg_get_labels_packed(ltlg_ctx* ctx, void* out, size_t out_bytes) {
 
 ltlg_status ltlg_device_labels(ltlg_ctx* ctx, int shard, void** dev_ptr, uint64_t* row_begin, uint64_t* row_end,
                                int* device) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return set_err(ctx, LTLG_EINVAL, "shard out of range");
     if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
@@ -1310,6 +1350,7 @@ ltlg_status ltlg_stream(ltlg_ctx* ctx, int shard, void** stream) {
 }
 
 ltlg_status ltlg_set_profiling(ltlg_ctx* ctx, int on) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (on) {
         for (Shard& s : ctx->shards) {
@@ -1327,6 +1368,7 @@ ltlg_status ltlg_set_profiling(ltlg_ctx* ctx, int on) {
 
 ltlg_status ltlg_stage_times(ltlg_ctx* ctx, int shard, int back, float* upload_ms, float* summary_ms,
                              float* label_ms) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (shard < 0 || shard >= static_cast<int>(ctx->shards.size())) return set_err(ctx, LTLG_EINVAL, "shard out of range");
     Shard& s = ctx->shards[static_cast<size_t>(shard)];
@@ -1362,6 +1404,7 @@ ltlg_status ltlg_validate_csr(uint64_t rows, uint64_t cols, const uint64_t* row_
 
 ltlg_status ltlg_label_all(uint64_t rows, uint64_t cols, const uint64_t* row_offsets, const uint32_t* col_indices,
                            uint64_t cells, int num_props, const uint64_t* column_words, int workers, uint64_t* out) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     (void)workers;
     if (num_props > 64) return set_err(nullptr, LTLG_EINVAL, "at most 64 propositions");
     if (num_props < 0) return set_err(nullptr, LTLG_EINVAL, "props must be in [0, 64]");
@@ -1556,6 +1599,7 @@ extern "C" {
 
 ltlg_status ltlg_swept_volume(const ltlg_gridk* grid, const ltlg_footprint* footprint, uint64_t num_edges,
                               const uint64_t* sample_offsets, const double* samples, int device, ltlg_csr** out) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!out) return set_err(nullptr, LTLG_EINVAL, "null argument");
     *out = nullptr;
     if (!grid || !footprint || (num_edges && !sample_offsets)) return set_err(nullptr, LTLG_EINVAL, "null argument");
@@ -1596,6 +1640,7 @@ uint64_t ltlg_csr_nnz(const ltlg_csr* m) { return m ? m->nnz : 0; }
 double ltlg_csr_build_ms(const ltlg_csr* m) { return m ? m->ms : 0.0; }
 
 ltlg_status ltlg_csr_copy(const ltlg_csr* m, uint64_t* row_offsets, uint32_t* col_indices) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!m) return set_err(nullptr, LTLG_EINVAL, "null csr");
     ltlg_ctx* const ctx = nullptr;
     CK(cudaSetDevice(m->device), "cudaSetDevice");
@@ -1606,6 +1651,7 @@ ltlg_status ltlg_csr_copy(const ltlg_csr* m, uint64_t* row_offsets, uint32_t* co
 }
 
 ltlg_status ltlg_load_csr(ltlg_ctx* ctx, const ltlg_csr* m) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
     if (!m) return set_err(ctx, LTLG_EINVAL, "null csr");
     std::vector<uint64_t> off(m->rows + 1);
@@ -1616,6 +1662,7 @@ ltlg_status ltlg_load_csr(ltlg_ctx* ctx, const ltlg_csr* m) {
 }
 
 void ltlg_csr_free(ltlg_csr* m) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!m) return;
     cudaSetDevice(m->device);
     delete m;
