@@ -460,7 +460,12 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // prop-lane kernel, in slices of <= 64 frames (dev knob LTLG_PROPLANE=0:
         // the frame-per-lane kernels); <= 32 props: one prop per lane, 33..64: two
         static const bool pl_ok = !getenv("LTLG_PROPLANE") || atoi(getenv("LTLG_PROPLANE")) != 0;
-        const bool pl = wide_b_ok && pl_ok && frames > 1 && props <= 64;
+        // (the record indices are 32-bit and the work buffer is sized for the
+        // worst case -- every (word, prop, frame) partial: huge grids take the
+        // frame-per-lane kernels instead)
+        const uint64_t pl_worst = static_cast<uint64_t>(nw64 + 1) * (props > 32 ? 64u : 32u) *
+                                  static_cast<uint64_t>(std::min(frames, 64));
+        const bool pl = wide_b_ok && pl_ok && frames > 1 && props <= 64 && pl_worst < (uint64_t(1) << 31);
         const int nslice = pl ? (frames + 63) / 64 : 1;
         CK(s.sf.reserve(pl ? pl_work_bytes(props, std::min(frames, 64), nw64)
                         : wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32
