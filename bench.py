@@ -390,6 +390,16 @@ def main():
             dt = time.perf_counter() - t0
             if q >= 0:
                 eng_lat.append(dt * 1e3)
+        # the same, with the labels read back into pinned host memory (both
+        # PCIe transfers inside the time, as the paper's timings are)
+        out3 = torch.empty((rows_local, 1), dtype=torch.int16, pin_memory=True)
+        host_lat = []
+        for q in range(-1, n_frames):
+            t0 = time.perf_counter()
+            eng.submit_grid(cells, CFG3_PROPS, frames3[q + 1], 1)
+            eng.get_labels_packed(out3)
+            if q >= 0:
+                host_lat.append((time.perf_counter() - t0) * 1e3)
         # then the per-stage device times of the same frames
         eng.set_profiling(True)
         for q in range(-1, n_frames):
@@ -406,6 +416,8 @@ def main():
                "p50_ms": statistics.median(eng_lat), "p99_ms": sorted(eng_lat)[int(0.99 * (len(eng_lat) - 1))],
                "frames": n_frames, "what": "pinned host P -> labels resident in HBM (host steady clock)",
                "kernel_p50_ms": k3,
+               "p50_to_host_ms": statistics.median(host_lat),
+               "to_host_what": "pinned host P -> labels (u16 per edge, 4 MB) back in pinned host memory",
                "stages_p50_ms": {"upload": statistics.median(x[0] for x in stages3),
                                  "summary": statistics.median(x[1] for x in stages3),
                                  "label": k3},
