@@ -1804,8 +1804,11 @@ __global__ void __launch_bounds__(256) pl_summary_kernel(const uint64_t* __restr
                                                          int nctr, int pshift) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (t < static_cast<uint64_t>(nctr)) task_ctr[t] = 0;
-    const uint32_t w = static_cast<uint32_t>(t >> pshift), j = static_cast<uint32_t>(t & ((1u << pshift) - 1u));
-    if (w > nw64) return;
+    // consecutive threads take consecutive words of one prop: coalesced rows of P
+    const uint64_t nwp = nw64 + 1;
+    const uint32_t j = static_cast<uint32_t>(t / nwp), w = static_cast<uint32_t>(t - static_cast<uint64_t>(j) * nwp);
+    if (j >= (1u << pshift)) return;
+    const uint64_t o = (static_cast<uint64_t>(w) << pshift) | j;  // ffr / sfr / cnt index
     uint64_t full = 0, any = 0;
     uint32_t n = 0;
     const uint64_t lo = static_cast<uint64_t>(w) * 64;
@@ -1819,9 +1822,9 @@ __global__ void __launch_bounds__(256) pl_summary_kernel(const uint64_t* __restr
             n += (x != 0 && x != valid);
         }
     }
-    ffr[t] = full;
-    sfr[t] = any;
-    cnt[t] = n;
+    ffr[o] = full;
+    sfr[o] = any;
+    cnt[o] = n;
     if (n) atomicAdd(wcnt + w, n);
 }
 
@@ -1852,9 +1855,10 @@ __global__ void __launch_bounds__(256) pl_fill_kernel(const uint64_t* __restrict
                                                       uint32_t nw64, uint64_t cells, const uint32_t* __restrict__ cnt,
                                                       uint32_t* __restrict__ cursor, uint4* __restrict__ rec, int pshift) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    const uint32_t w = static_cast<uint32_t>(t >> pshift), j = static_cast<uint32_t>(t & ((1u << pshift) - 1u));
-    if (w >= nw64) return;
-    const uint32_t n = cnt[t];
+    const uint64_t nwp = nw64 + 1;
+    const uint32_t j = static_cast<uint32_t>(t / nwp), w = static_cast<uint32_t>(t - static_cast<uint64_t>(j) * nwp);
+    if (j >= (1u << pshift) || w >= nw64) return;
+    const uint32_t n = cnt[(static_cast<uint64_t>(w) << pshift) | j];
     if (!n) return;
     uint32_t pos = atomicAdd(cursor + w, n);  // record order within a word is irrelevant (OR)
     const uint64_t lo = static_cast<uint64_t>(w) * 64;
