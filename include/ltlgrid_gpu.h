@@ -328,6 +328,10 @@ uint64_t ltlg_csr_nnz(const ltlg_csr* m);
 double ltlg_csr_build_ms(const ltlg_csr* m);
 /* Host copies: row_offsets (rows + 1 u64), col_indices (nnz u32); either may be NULL. */
 ltlg_status ltlg_csr_copy(const ltlg_csr* m, uint64_t* row_offsets, uint32_t* col_indices);
+/* CsrBoolMatrix::save (label.cpp:251-268): the matrix as a CSB1 file,
+ * byte-identical to the reference's.  LTLG_EIO "cannot open for writing:
+ * <path>" / "write failed: <path>". */
+ltlg_status ltlg_csr_save(const ltlg_csr* m, const char* path);
 /* ltlg_load_abstraction of the swept-volume matrix into an engine. */
 ltlg_status ltlg_load_csr(ltlg_ctx* ctx, const ltlg_csr* m);
 void ltlg_csr_free(ltlg_csr* m);

@@ -28,6 +28,7 @@ EXPORTS = [
     "ltlg_submit_grid_device_ex",
     "ltlg_swept_volume", "ltlg_csr_rows", "ltlg_csr_cols", "ltlg_csr_nnz", "ltlg_csr_build_ms", "ltlg_csr_copy",
     "ltlg_load_csr", "ltlg_csr_free", "ltlg_set_profiling", "ltlg_generate_scenario", "ltlg_submit_scenario",
+    "ltlg_csr_save",
 ]
 
 
@@ -126,6 +127,7 @@ def lib() -> C.CDLL:
         "ltlg_csr_copy": ([vp, vp, vp], i32),
         "ltlg_load_csr": ([ctxp, vp], i32),
         "ltlg_csr_free": ([vp], None),
+        "ltlg_csr_save": ([vp, C.c_char_p], i32),
         "ltlg_set_profiling": ([ctxp, i32], i32),
         "ltlg_generate_scenario": ([C.POINTER(Scenario), C.POINTER(GridK), u64, i32, vp], i32),
         "ltlg_submit_scenario": ([ctxp, C.POINTER(Scenario), C.POINTER(GridK), u64, i32], i32),

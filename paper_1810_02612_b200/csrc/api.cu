@@ -1655,6 +1655,21 @@ ltlg_status ltlg_csr_copy(const ltlg_csr* m, uint64_t* row_offsets, uint32_t* co
     return LTLG_OK;
 }
 
+ltlg_status ltlg_csr_save(const ltlg_csr* m, const char* path) {
+    DeviceGuard device_guard;
+    if (!m || !path) return set_err(nullptr, LTLG_EINVAL, "null argument");
+    std::vector<uint64_t> off(m->rows + 1);
+    std::vector<uint32_t> idx(std::max<uint64_t>(m->nnz, 1));
+    const ltlg_status st = ltlg_csr_copy(m, off.data(), idx.data());
+    if (st != LTLG_OK) return st;
+    Error e{S_OK, ""};
+    if (!write_csb1(path, m->rows, m->cols, off.data(), idx.data(), &e)) {
+        g_error = e.msg;
+        return static_cast<ltlg_status>(e.code);
+    }
+    return LTLG_OK;
+}
+
 ltlg_status ltlg_load_csr(ltlg_ctx* ctx, const ltlg_csr* m) {
     DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");

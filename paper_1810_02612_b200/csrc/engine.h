@@ -98,6 +98,9 @@ bool read_csb1_words(const char* path, WordCsr* out, Error* err);
 bool read_zobv(const char* path, uint64_t cells, uint64_t* dst, Error* err);
 // LabelMatrix::save (label.cpp:300-309): LBM1 of rows x ceil(props/64) words.
 bool write_lbm1(const char* path, uint64_t rows, int props, const uint64_t* words, Error* err);
+// CsrBoolMatrix::save (label.cpp:251-268): CSB1 of rows x cols.
+bool write_csb1(const char* path, uint64_t rows, uint64_t cols, const uint64_t* offsets, const uint32_t* indices,
+                Error* err);
 // Split rows into n contiguous shards balanced by stored pairs.
 std::vector<uint64_t> shard_bounds(const WordCsr& t, int n);
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,

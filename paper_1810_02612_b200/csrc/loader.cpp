@@ -411,6 +411,41 @@ bool write_lbm1(const char* path, uint64_t rows, int props, const uint64_t* word
     return true;
 }
 
+// CsrBoolMatrix::save (label.cpp:251-268): CSB1, little-endian, u32 fields
+// unless cols or nnz exceed 32 bits.
+bool write_csb1(const char* path, uint64_t rows, uint64_t cols, const uint64_t* offsets, const uint32_t* indices,
+                Error* err) {
+    const std::string p(path);
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return fail(err, S_EIO, "cannot open for writing: " + p);
+    const uint64_t nnz = offsets[rows];
+    const bool wide = cols > 0xffffffffull || nnz > 0xffffffffull;
+    const uint32_t flags = wide ? 1u : 0u;
+    bool ok = std::fwrite("CSB1", 1, 4, f) == 4 && std::fwrite(&flags, 4, 1, f) == 1 &&
+              std::fwrite(&rows, 8, 1, f) == 1 && std::fwrite(&cols, 8, 1, f) == 1 && std::fwrite(&nnz, 8, 1, f) == 1;
+    std::vector<uint32_t> buf;
+    if (ok && wide) {
+        ok = std::fwrite(offsets, 8, rows + 1, f) == rows + 1;
+        std::vector<uint64_t> w(1 << 16);
+        for (uint64_t i = 0; ok && i < nnz; i += w.size()) {
+            const uint64_t n = std::min<uint64_t>(w.size(), nnz - i);
+            for (uint64_t k = 0; k < n; ++k) w[k] = indices[i + k];
+            ok = std::fwrite(w.data(), 8, n, f) == n;
+        }
+    } else if (ok) {
+        buf.resize(1 << 16);
+        for (uint64_t i = 0; ok && i <= rows; i += buf.size()) {
+            const uint64_t n = std::min<uint64_t>(buf.size(), rows + 1 - i);
+            for (uint64_t k = 0; k < n; ++k) buf[k] = static_cast<uint32_t>(offsets[i + k]);
+            ok = std::fwrite(buf.data(), 4, n, f) == n;
+        }
+        ok = ok && (nnz == 0 || std::fwrite(indices, 4, nnz, f) == nnz);
+    }
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) return fail(err, S_EIO, "write failed: " + p);
+    return true;
+}
+
 std::vector<uint64_t> shard_bounds(const WordCsr& t, int n) {
     std::vector<uint64_t> b(static_cast<size_t>(n) + 1, t.rows);
     b[0] = 0;

@@ -617,6 +617,12 @@ class SweptVolume:
             _raise(st, self._L.ltlg_last_error(None).decode())
         return CsrBoolMatrix(self.rows, self.cols, off, idx[: self.nnz])
 
+    def save(self, path: str) -> None:
+        """CsrBoolMatrix::save (CSB1), byte-identical to the reference's file."""
+        st = self._L.ltlg_csr_save(self._h, os.fsencode(path))
+        if st:
+            _raise(st, self._L.ltlg_last_error(None).decode())
+
     def close(self):
         if self._h:
             self._L.ltlg_csr_free(self._h)

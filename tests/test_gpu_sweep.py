@@ -132,3 +132,25 @@ def test_sweep_reference_abstraction(refcore, oracle):
     off, smp = refcore.abstraction(target_edges=2000, seed=29)
     for depth in (12, 18, 24):
         _same(_gpu(off, smp, depth), oracle.swept_volume(depth, (0, 0, 0), (64, 64, 4), FOOTPRINT, off, smp))
+
+
+def test_sweep_saved_as_csb1_like_the_reference(refcore, tmp_path):
+    """ltlg_csr_save: the GPU-built matrix as CSB1, byte-identical to the
+    reference's CsrBoolMatrix::save of the same rows; and it loads back."""
+    from paper_1810_02612_b200 import FootprintSpec, LabelEngine, swept_volume
+
+    off, smp = refcore.abstraction(target_edges=400, seed=9)
+    sv = swept_volume((off, smp), FootprintSpec(*FOOTPRINT), ((0, 64), (0, 64), (0, 4)), 15)
+    m = sv.to_csr()
+    ours, theirs = tmp_path / "gpu.csb1", tmp_path / "ref.csb1"
+    sv.save(str(ours))
+    refcore.csr_save(str(theirs), m.rows, m.cols, m.row_offsets, m.col_indices)
+    assert ours.read_bytes() == theirs.read_bytes()
+    eng = LabelEngine()
+    eng.load_abstraction_file(str(ours))
+    assert eng.info().rows == m.rows
+    eng.close()
+    sv.close()
+    with pytest.raises(RuntimeError, match="cannot open for writing"):
+        sv2 = swept_volume((off, smp), FootprintSpec(*FOOTPRINT), ((0, 64), (0, 64), (0, 4)), 15)
+        sv2.save(str(tmp_path / "no" / "such" / "dir.csb1"))
