@@ -68,3 +68,53 @@ def test_host_validator_matches_reference_messages():
     idx = np.array([4, 1, 2], np.uint32)
     buf = C.create_string_buffer(256)
     assert L.ltlg_validate_csr(2, 5, off.ctypes.data, 3, idx.ctypes.data, 3, buf, 256) == N.LTLG_OK
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of the header's structs (sizes and field offsets)
+    equal what a C compiler lays out for include/ltlgrid_gpu.h."""
+    structs = {
+        "ltlg_options": (N.Options, ["sort_rows", "stream_task_pairs", "batch_task_pairs", "profile",
+                                     "readback_chunks", "reserved"]),
+        "ltlg_info": (N.Info, ["rows", "cols", "nnz", "words", "pairs", "t_bytes", "n_devices", "props", "frames",
+                               "label_bytes", "label_words", "reserved"]),
+        "ltlg_grid2": (N.Grid2, ["depth", "lo0", "hi0", "lo1", "hi1"]),
+        "ltlg_pose2": (N.Pose2, ["dx", "dy", "cos_t", "sin_t"]),
+        "ltlg_gridk": (N.GridK, ["dims", "depth", "lo", "hi"]),
+        "ltlg_footprint": (N.Footprint, ["length", "width", "ref_offset"]),
+        "ltlg_scenario": (N.Scenario, ["loop_cx", "loop_cy", "loop_radius", "lane_width", "agent_count",
+                                       "agent_speed_min", "agent_speed_max", "agent_length", "agent_width",
+                                       "lateral_spread", "horizon", "seed"]),
+    }
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', 'int main(void) {']
+    for cname, (_, fields) in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f in fields:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-o", str(exe), str(src)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        name, key, val = line.split()
+        got[(name, key)] = int(val)
+    for cname, (py, fields) in structs.items():
+        assert C.sizeof(py) == got[(cname, "size")], cname
+        for f in fields:
+            assert getattr(py, f).offset == got[(cname, f)], (cname, f)
+
+
+def test_trajectory_inputs_both_forms():
+    """swept_volume's trajectory argument: (sample_offsets, samples) or a list
+    of per-edge State5 arrays give the same flat arrays."""
+    from paper_1810_02612_b200.label import _trajectories
+
+    rows = [np.arange(10.0).reshape(2, 5), np.zeros((0, 5)), np.ones((3, 5))]
+    off, smp = _trajectories(rows)
+    assert off.tolist() == [0, 2, 2, 5] and smp.shape == (5, 5)
+    off2, smp2 = _trajectories((off, smp))
+    assert np.array_equal(off2, off) and np.array_equal(smp2, smp)
+    off3, smp3 = _trajectories([])
+    assert off3.tolist() == [0] and smp3.shape == (0, 5)
