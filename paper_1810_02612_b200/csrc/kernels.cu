@@ -1304,30 +1304,51 @@ __device__ __forceinline__ int64_t quantize_dev(double lo, double hi, int bits, 
     return static_cast<int64_t>(c);
 }
 
-__global__ void resample_kernel(Grid2 vg, Grid2 wg, const Pose2* __restrict__ poses, int props,
-                                const uint32_t* __restrict__ world32, uint32_t wnw32, int outside,
-                                uint32_t vnw32, uint32_t* __restrict__ out32) {
-    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-    const int g0 = blockIdx.y * 8;
-    const int f = blockIdx.z;
-    if (w >= vnw32) return;
+// 2-D z-order (de)interleave: bits of x at every second position
+__device__ __forceinline__ uint64_t compact1by1(uint64_t x) {
+    x &= 0x5555555555555555ull;
+    x = (x | (x >> 1)) & 0x3333333333333333ull;
+    x = (x | (x >> 2)) & 0x0f0f0f0f0f0f0f0full;
+    x = (x | (x >> 4)) & 0x00ff00ff00ff00ffull;
+    x = (x | (x >> 8)) & 0x0000ffff0000ffffull;
+    x = (x | (x >> 16)) & 0x00000000ffffffffull;
+    return x;
+}
+__device__ __forceinline__ uint64_t spread1by1(uint64_t x) {
+    x &= 0x00000000ffffffffull;
+    x = (x | (x << 16)) & 0x0000ffff0000ffffull;
+    x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
+    x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
+}
+
+// Thread per vehicle cell (blockIdx.y = frame): the cell's centre through
+// the pose into world coordinates (the oracle's fp64 operations, in order),
+// its world cell, then one ballot per proposition assembles the 32-cell word
+// (lane j keeps props j and j + 32 and writes them).  Axis 0 takes the
+// z-index bits from the top, round-robin (grid.cpp:108-126): x sits at the
+// positions of parity (depth - 1) & 1.
+__global__ void __launch_bounds__(256) resample_kernel(Grid2 vg, Grid2 wg, const Pose2* __restrict__ poses,
+                                                       int props, const uint32_t* __restrict__ world32,
+                                                       uint32_t wnw32, int outside, uint32_t vnw32,
+                                                       uint32_t* __restrict__ out32) {
+    const uint64_t z = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const int f = blockIdx.y, lane = threadIdx.x & 31;
+    const uint32_t w = static_cast<uint32_t>(z >> 5);
+    if (w >= vnw32) return;  // whole warps (vnw32 words of 32 cells)
     const Pose2 ps = poses[f];
     const int bvx = axis_bits2(vg.depth, 0), bvy = axis_bits2(vg.depth, 1);
     const int bwx = axis_bits2(wg.depth, 0), bwy = axis_bits2(wg.depth, 1);
-    const uint64_t vcells = 1ull << vg.depth;
-    const double wxv = __ddiv_rn(__dadd_rn(vg.hi0, -vg.lo0), static_cast<double>(1ull << bvx));
-    const double wyv = __ddiv_rn(__dadd_rn(vg.hi1, -vg.lo1), static_cast<double>(1ull << bvy));
-    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const int ng = props - g0 < 8 ? props - g0 : 8;
-    for (int b = 0; b < 32; ++b) {
-        const uint64_t z = static_cast<uint64_t>(w) * 32 + b;
-        if (z >= vcells) break;
-        uint64_t cx = 0, cy = 0;
-        for (int level = 0; level < vg.depth; ++level) {
-            const uint64_t bit = (z >> (vg.depth - 1 - level)) & 1u;
-            if ((level & 1) == 0) cx = (cx << 1) | bit;
-            else cy = (cy << 1) | bit;
-        }
+    const bool valid = z < (1ull << vg.depth);
+    bool in = false, out_all = false;
+    uint64_t zw = 0;
+    if (valid) {
+        const double wxv = __ddiv_rn(__dadd_rn(vg.hi0, -vg.lo0), static_cast<double>(1ull << bvx));
+        const double wyv = __ddiv_rn(__dadd_rn(vg.hi1, -vg.lo1), static_cast<double>(1ull << bvy));
+        const uint64_t cx = compact1by1(z >> ((vg.depth - 1) & 1)) & ((1ull << bvx) - 1);
+        const uint64_t cy = compact1by1(z >> (vg.depth & 1)) & ((1ull << bvy) - 1);
         const double x = __dadd_rn(vg.lo0, __dmul_rn(__dadd_rn(static_cast<double>(cx), 0.5), wxv));
         const double y = __dadd_rn(vg.lo1, __dmul_rn(__dadd_rn(static_cast<double>(cy), 0.5), wyv));
         const double xw = __dadd_rn(__dadd_rn(__dmul_rn(ps.c, x), -__dmul_rn(ps.s, y)), ps.dx);
@@ -1335,23 +1356,26 @@ __global__ void resample_kernel(Grid2 vg, Grid2 wg, const Pose2* __restrict__ po
         const int64_t qx = quantize_dev(wg.lo0, wg.hi0, bwx, xw);
         const int64_t qy = quantize_dev(wg.lo1, wg.hi1, bwy, yw);
         if (qx < 0 || qy < 0) {
-            if (outside)
-                for (int j = 0; j < ng; ++j) acc[j] |= 1u << b;
-            continue;
+            out_all = outside != 0;
+        } else {
+            in = true;
+            zw = (spread1by1(static_cast<uint64_t>(qx)) << ((wg.depth - 1) & 1)) |
+                 (spread1by1(static_cast<uint64_t>(qy)) << (wg.depth & 1));
         }
-        uint64_t zw = 0;
-        for (int level = 0; level < wg.depth; ++level) {
-            const int axis = level & 1;
-            const int bit_pos = (axis ? bwy : bwx) - 1 - level / 2;
-            zw = (zw << 1) | (((axis ? static_cast<uint64_t>(qy) : static_cast<uint64_t>(qx)) >> bit_pos) & 1u);
-        }
-        for (int j = 0; j < ng; ++j) {
-            const uint32_t word = __ldg(world32 + static_cast<uint64_t>(g0 + j) * wnw32 + (zw >> 5));
-            acc[j] |= ((word >> (zw & 31)) & 1u) << b;
+    }
+    uint32_t mine0 = 0, mine1 = 0;
+    const uint32_t* wsrc = world32 + (zw >> 5);
+    for (int j = 0; j < props; ++j) {
+        const bool bit = in ? ((__ldg(wsrc + static_cast<uint64_t>(j) * wnw32) >> (zw & 31)) & 1u) != 0 : out_all;
+        const uint32_t word = __ballot_sync(0xffffffffu, bit);
+        if ((j & 31) == lane) {
+            if (j < 32) mine0 = word;
+            else mine1 = word;
         }
     }
     uint32_t* dst = out32 + static_cast<uint64_t>(f) * props * vnw32 + w;
-    for (int j = 0; j < ng; ++j) dst[static_cast<uint64_t>(g0 + j) * vnw32] = acc[j];
+    if (lane < props) dst[static_cast<uint64_t>(lane) * vnw32] = mine0;
+    if (lane + 32 < props) dst[static_cast<uint64_t>(lane + 32) * vnw32] = mine1;
 }
 
 
@@ -2225,8 +2249,9 @@ cudaError_t launch_resample(int vdepth, double vlo0, double vhi0, double vlo1, d
     if (props == 0) return cudaSuccess;
     Grid2 vg{vdepth, vlo0, vhi0, vlo1, vhi1};
     Grid2 wg{wdepth, wlo0, whi0, wlo1, whi1};
-    dim3 grid((vnw32 + 127) / 128, static_cast<unsigned>((props + 7) / 8), static_cast<unsigned>(frames));
-    resample_kernel<<<grid, 128, 0, st>>>(vg, wg, static_cast<const Pose2*>(poses), props, world32, wnw32,
+    const uint64_t threads = static_cast<uint64_t>(vnw32) * 32;
+    dim3 grid(static_cast<unsigned>((threads + 255) / 256), static_cast<unsigned>(frames));
+    resample_kernel<<<grid, 256, 0, st>>>(vg, wg, static_cast<const Pose2*>(poses), props, world32, wnw32,
                                           outside, vnw32, out32);
     return cudaGetLastError();
 }
