@@ -253,8 +253,19 @@ ltlg_status load_words(ltlg_ctx* ctx, WordCsr& t) {
         PackedShard p;
         if (b[i + 1] - b[i] > 0xffffffffull)
             return set_err(ctx, LTLG_EINVAL, "a device shard holds more than 2^32-1 rows");
-        build_shard(t, b[i], b[i + 1], ctx->opts.sort_rows != 0, sentinel,
-                    ctx->opts.stream_task_pairs > 0 ? ctx->opts.stream_task_pairs : 2048,
+        // single-frame task size: 2048 32-cell pairs, but small abstractions get
+        // smaller tasks (down to one 256-pair chunk) so that every warp of the
+        // persistent grid has a task -- a lone warp streaming 2048 pairs is
+        // a ~20 us critical path (cfg 2: 200k edges)
+        int stream_pairs = ctx->opts.stream_task_pairs;
+        if (stream_pairs <= 0) {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->shards[static_cast<size_t>(i)].device);
+            const uint64_t words = t.offsets[b[i + 1]] - t.offsets[b[i]];
+            const uint64_t want = words / (static_cast<uint64_t>(sms) * 32ull);
+            stream_pairs = static_cast<int>(std::min<uint64_t>(2048, std::max<uint64_t>(256, want)));
+        }
+        build_shard(t, b[i], b[i + 1], ctx->opts.sort_rows != 0, sentinel, stream_pairs,
                     ctx->opts.batch_task_pairs > 0 ? ctx->opts.batch_task_pairs : 256,
                     ctx->opts.readback_chunks > 1 ? (ctx->opts.readback_chunks < 64 ? ctx->opts.readback_chunks : 64) : 1,
                     &p);
