@@ -881,10 +881,18 @@ __global__ void __launch_bounds__(NT)
     const uint4* xtab = reinterpret_cast<const uint4*>(XSMEM ? tab + xoff : xg);
     bool tab_ready = !SMEM;
 
+    // a warp's first task is static (task_begin + its global warp index), so
+    // its critical path starts without an atomic round trip; later tasks
+    // come from the counter, after the static ones
+    const uint32_t nwarps = gridDim.x * (NT / 32);
+    uint32_t t_static = task_begin + blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
     for (;;) {
-        uint32_t t = 0;
-        if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
-        t = __shfl_sync(0xffffffffu, t, 0);
+        uint32_t t = t_static;
+        if (t_static == ~0u) {
+            if (lane == 0) t = task_begin + nwarps + atomicAdd(task_ctr, 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+        }
+        t_static = ~0u;
         if (t >= ntasks) break;
         const uint8_t* base = t64 + task_byte[t];
         const uint32_t n = task_n[t];
