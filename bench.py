@@ -127,6 +127,17 @@ def ncu_traffic(kernel: str):
         return None
 
 
+def lop3_peak(sm_clk_hz: float) -> float:
+    """Integer roofline: the measured LOP3 throughput (tools/micro/lop3_peak.cu,
+    profiles/lop3_peak.json) at this run's SM clock, else 64 LOP3/clk/SM."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "lop3_peak.json")) as f:
+            d = json.load(f)
+        return d["lop3_per_clk_per_sm_at_max_clock"] * d["sms"] * sm_clk_hz
+    except Exception:
+        return 148 * 64 * sm_clk_hz
+
+
 def ncu_limiter(kernel: str):
     """Pipe utilisations of `kernel` from the committed ncu capture (profiles/limiters.json)."""
     try:
@@ -365,8 +376,11 @@ def main():
                         "memory OR reductions) and issue saturated (see int_ops)",
                 "limiter": ncu_limiter("label_pl_kernel"),
                 "int_ops": {"alg_and_or_per_launch": lop3, "achieved_per_s": lop3 / (label_ms / 1e3),
-                            "peak_per_s": 148 * 64 * sm_clk,
-                            "frac": lop3 / (label_ms / 1e3) / (148 * 64 * sm_clk),
+                            "peak_per_s": lop3_peak(sm_clk),
+                            "peak_source": "profiles/lop3_peak.json (tools/micro/lop3_peak.cu on this B200 model)"
+                            if os.path.exists(os.path.join(ROOT, "profiles", "lop3_peak.json"))
+                            else "assumed 64 LOP3/clk/SM",
+                            "frac": lop3 / (label_ms / 1e3) / lop3_peak(sm_clk),
                             "note": "SURVEY 8(d) integer roofline W32*F*props AND-ORs at 64/clk/SM; > 1 because one "
                                     "summary entry answers every prop of a (T word, frame) at once"}}
 
