@@ -381,7 +381,7 @@ def main():
                             if os.path.exists(os.path.join(ROOT, "profiles", "lop3_peak.json"))
                             else "assumed 64 LOP3/clk/SM",
                             "frac": lop3 / (label_ms / 1e3) / lop3_peak(sm_clk),
-                            "note": "SURVEY 8(d) integer roofline W32*F*props AND-ORs at 64/clk/SM; > 1 because one "
+                            "note": "SURVEY 8(d) integer roofline W32*F*props AND-ORs at the measured LOP3 rate; > 1 because one "
                                     "summary entry answers every prop of a (T word, frame) at once"}}
 
     # ---- p50 single-frame latency, config 3 (16 props), host P -> labels in HBM
