@@ -886,10 +886,13 @@ __global__ void __launch_bounds__(NT)
     // come from the counter, after the static ones
     const uint32_t nwarps = gridDim.x * (NT / 32);
     uint32_t t_static = task_begin + blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+    const bool dyn = task_begin + nwarps < ntasks;
     for (;;) {
         uint32_t t = t_static;
         if (t_static == ~0u) {
-            if (lane == 0) t = task_begin + nwarps + atomicAdd(task_ctr, 1u);
+            // every task static (small abstractions: one task per warp): no
+            // failing fetch, so no burst of same-address atomics at the end
+            if (lane == 0) t = dyn ? task_begin + nwarps + atomicAdd(task_ctr, 1u) : ntasks;
             t = __shfl_sync(0xffffffffu, t, 0);
         }
         t_static = ~0u;
