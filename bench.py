@@ -347,6 +347,11 @@ def main():
     ms = e0.elapsed_time(e1)
     # per-launch device times of the K timed launches (event ring on the launching stream)
     kernel_ms = [eng.stage_times(0, back)[1:] for back in range(min(K, 255))]
+    if not args.no_e2e:
+        # a row sample of these labels: the pipelined host-buffer (e2e) steps
+        # below must reproduce it exactly
+        pick = np.arange(0, r1 - r0, 997)
+        ref_lab = eng.get_labels_packed()[pick].view(np.int32)
     if args.dump_labels:
         lab = eng.get_labels_packed()
         pick = np.arange(0, r1 - r0, 997)
@@ -445,44 +450,66 @@ def main():
     # ---- e2e through the public API with host buffers ------------------------
     e2e = None
     if not args.no_e2e:
-        # host-buffer path: an engine whose rows are z-sorted within read-back
-        # blocks, so the 512 MB label copy overlaps the labelling of later blocks
+        # host-buffer path: engines whose rows are z-sorted within read-back
+        # blocks, so the 512 MB label copy overlaps the labelling of later
+        # blocks.  Two engines alternate steps (double buffering, as a
+        # streaming caller would): step k+1's P upload and labelling are
+        # submitted before step k's labels are read back, so the H2D and D2H
+        # directions of PCIe run at the same time.  Every step's P still
+        # crosses H2D and its labels D2H inside the timed region.
         eng.close()
-        eng = LabelEngine(devices=[local], readback_chunks=args.readback_chunks)
-        eng.load_abstraction_words(r1 - r0, cells, T.offsets, T.words, T.masks)
-        stream = torch.cuda.ExternalStream(eng.stream())
-        out_host = torch.empty((rows_local, F), dtype=torch.int32, pin_memory=True)
-        Ke = max(2, min(K, 5))
+        engs = []
+        for _ in range(2):
+            e = LabelEngine(devices=[local], readback_chunks=args.readback_chunks)
+            e.load_abstraction_words(r1 - r0, cells, T.offsets, T.words, T.masks)
+            engs.append(e)
+        eng = engs[0]
+        streams = [torch.cuda.ExternalStream(e.stream()) for e in engs]
+        outs = [torch.empty((rows_local, F), dtype=torch.int32, pin_memory=True) for _ in engs]
+        Pd = [P_dev, torch.empty_like(P_dev)] if world > 1 else None
+        Ke = max(2, min(K, 6))
 
-        def e2e_step():
+        def e2e_submit(k):
+            e, st = engs[k % 2], streams[k % 2]
             if world > 1:  # H2D on rank 0 + broadcast on torch's stream, then the engine's
                 cur = torch.cuda.current_stream()
-                cur.wait_stream(stream)
+                cur.wait_stream(st)  # the buffer's previous reader (step k-2) is done
                 if rank == 0:
-                    P_dev.copy_(P_host, non_blocking=True)
-                dist.broadcast(P_dev, src=0)
-                stream.wait_stream(cur)
-                eng.submit_grid_device(cells, props, P_dev.data_ptr(), F, readback=True)
+                    Pd[k % 2].copy_(P_host, non_blocking=True)
+                dist.broadcast(Pd[k % 2], src=0)
+                st.wait_stream(cur)
+                e.submit_grid_device(cells, props, Pd[k % 2].data_ptr(), F, readback=True)
             else:
-                eng.submit_grid(cells, props, P_host, F)
-            eng.get_labels_packed(out_host)
+                e.submit_grid(cells, props, P_host, F)
 
-        e2e_step()  # untimed warm-up of the host path
+        def e2e_run(n):
+            e2e_submit(0)
+            for k in range(n):
+                if k + 1 < n:
+                    e2e_submit(k + 1)
+                engs[k % 2].get_labels_packed(outs[k % 2])
+
+        e2e_run(2)  # untimed warm-up of the host path (both engines)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(Ke):
-            e2e_step()
+        e2e_run(Ke)
         dt = time.perf_counter() - t0
         tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt[0])
+        for o in outs:
+            if not np.array_equal(o.numpy()[pick], ref_lab):
+                raise RuntimeError("e2e: labels read back to host differ from the device-resident run")
+        for e in engs[1:]:
+            e.close()
         e2e = {"value": E * F * Ke / dt, "unit": UNIT, "h2d_bytes_per_step": F * props * nw * 8,
                "d2h_bytes_per_step": E * F * 4, "steps": Ke,
                "what": "ltlg_submit_grid(pinned host P, 64 frames) + ltlg_get_labels_packed(pinned host, u32 x 64 "
                        "frames per edge); host wall clock; readback_chunks=%d (block c's labels copy back while "
-                       "later blocks are labelled)" % args.readback_chunks}
+                       "later blocks are labelled); two engines alternate steps, so step k+1's upload and "
+                       "labelling overlap step k's read-back" % args.readback_chunks}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
