@@ -151,6 +151,33 @@ def shard_rows(E: int, rank: int, world: int):
     return E * rank // world, E * (rank + 1) // world
 
 
+def spatial_shard(offsets, words, masks, rank: int, world: int):
+    """Rank `rank`'s edge rows of T (word-CSR arrays): the rows sorted by their
+    median swept word (z-order, so a part is a compact region of the grid),
+    cut into `world` contiguous parts of that order balanced by stored words.
+    Rows are independent (label.cpp:179-186), so any partition labels the same
+    (test_label.cpp:121-132); a compact region keeps the prop-lane kernel's
+    summary reads in L1 (8 GPUs: 0.49 -> 0.40 ms per rank, DESIGN (e)).
+    Returns (row ids ascending, offsets, words, masks) of the part."""
+    off = np.asarray(offsets, dtype=np.int64)
+    E = len(off) - 1
+    if world == 1:
+        return np.arange(E, dtype=np.int64), offsets, words, masks
+    cnt = off[1:] - off[:-1]
+    med = np.asarray(words)[off[:-1] + cnt // 2] if len(words) else np.zeros(E, np.uint32)
+    order = np.argsort(med, kind="stable")
+    cum = np.cumsum(cnt[order])
+    total = int(cum[-1]) if E else 0
+    cut = np.searchsorted(cum, [total * r // world for r in range(1, world)], side="right")
+    bounds = np.concatenate([[0], cut, [E]])
+    ids = np.sort(order[bounds[rank]:bounds[rank + 1]])
+    c = cnt[ids]
+    so = np.zeros(len(ids) + 1, np.int64)
+    np.cumsum(c, out=so[1:])
+    idx = np.repeat(off[ids] - so[:-1], c) + np.arange(so[-1])
+    return ids, so.astype(np.uint64), np.asarray(words)[idx], np.asarray(masks)[idx]
+
+
 def cpu_reference_sample(depth: int, props: int, rows: int, frames: int, workers: int = 0):
     """Time the reference CPU label_all (oracle/_ref, or the C port) on rows
     [0, rows) of the same synthetic T, `frames` frames, best of 2 per frame
@@ -218,7 +245,7 @@ def run_reference(args, rank, world):
 def cfg_json(world):
     return {"workload": "config4-batched-frames: 2M-edge synthetic PRM x 64 frames, 512x512 grid (2^18 cells), "
                         "32 propositions", "edges": CFG4["edges"], "grid": "512x512", "cells": 1 << CFG4["depth"],
-            "props": CFG4["props"], "frames_per_step": CFG4["frames"], "parallelism": f"edge-row shards x{world}",
+            "props": CFG4["props"], "frames_per_step": CFG4["frames"], "parallelism": f"spatial edge-row shards x{world}" if world > 1 else "edge-row shards x1",
             "l2": "inputs larger than L2 (packed T 526 MB streamed per step)"}
 
 
@@ -266,13 +293,17 @@ def main():
     E, depth, props, F = CFG4["edges"], CFG4["depth"], CFG4["props"], CFG4["frames"]
     cells = 1 << depth
     nw = (cells + 63) // 64
-    r0, r1 = shard_rows(E, rank, world)
+    # N > 1: each rank holds a spatially compact, word-balanced part of the
+    # edge rows (spatial_shard); N = 1: all rows in their original order
     prm = SyntheticPRM(seed=SEED_T, depth=depth)
-    T = prm.words(r0, r1)
+    T = prm.words(0, E)
+    row_ids, T_off, T_words, T_masks = spatial_shard(T.offsets, T.words, T.masks, rank, world)
+    del T
+    rows_local = len(row_ids)
     eng = LabelEngine(devices=[local], profile=True)  # device-resident labels: one block, global z-sort
-    eng.load_abstraction_words(r1 - r0, cells, T.offsets, T.words, T.masks)
+    eng.load_abstraction_words(rows_local, cells, T_off, T_words, T_masks)
     info = eng.info()
-    W32_all = torch.tensor([int(info.words), int(r1 - r0)], dtype=torch.int64, device="cuda")
+    W32_all = torch.tensor([int(info.words), rows_local], dtype=torch.int64, device="cuda")
     if world > 1:
         dist.all_reduce(W32_all)
     W32, rows_all = int(W32_all[0]), int(W32_all[1])
@@ -350,12 +381,12 @@ def main():
     if not args.no_e2e:
         # a row sample of these labels: the pipelined host-buffer (e2e) steps
         # below must reproduce it exactly
-        pick = np.arange(0, r1 - r0, 997)
-        ref_lab = eng.get_labels_packed()[pick].view(np.int32)
+        pick_e2e = np.arange(0, rows_local, 997)
+        ref_lab = eng.get_labels_packed()[pick_e2e].view(np.int32)
     if args.dump_labels:
         lab = eng.get_labels_packed()
-        pick = np.arange(0, r1 - r0, 997)
-        np.savez(f"{args.dump_labels}_rank{rank}.npz", rows=pick + r0, labels=lab[pick])
+        pick = np.nonzero(row_ids % 997 == 0)[0]  # the same row ids whatever the sharding
+        np.savez(f"{args.dump_labels}_rank{rank}.npz", rows=row_ids[pick], labels=lab[pick])
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -366,7 +397,6 @@ def main():
 
     # roofline of the labeling kernel (SURVEY 8(d) algorithmic bytes, this rank's shard)
     hbm, src = peaks()
-    rows_local = r1 - r0
     alg_bytes = 8 * int(info.words) + 4 * (rows_local + 1) + F * (cells * props // 8 + rows_local * 4)
     achieved = alg_bytes / (label_ms / 1e3) / 1e9
     traffic = ncu_traffic("label_pl_kernel")
@@ -461,7 +491,7 @@ def main():
         engs = []
         for _ in range(2):
             e = LabelEngine(devices=[local], readback_chunks=args.readback_chunks)
-            e.load_abstraction_words(r1 - r0, cells, T.offsets, T.words, T.masks)
+            e.load_abstraction_words(rows_local, cells, T_off, T_words, T_masks)
             engs.append(e)
         eng = engs[0]
         streams = [torch.cuda.ExternalStream(e.stream()) for e in engs]
@@ -499,9 +529,13 @@ def main():
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt[0])
-        for o in outs:
-            if not np.array_equal(o.numpy()[pick], ref_lab):
-                raise RuntimeError("e2e: labels read back to host differ from the device-resident run")
+        for i, o in enumerate(outs):
+            got = o.numpy()[pick_e2e]
+            if not np.array_equal(got, ref_lab):
+                bad = np.nonzero((got != ref_lab).any(axis=1))[0]
+                raise RuntimeError(f"e2e: labels read back to host differ from the device-resident run (rank {rank}, "
+                                   f"engine {i}: {len(bad)} of {len(pick_e2e)} sampled rows, first {bad[:5].tolist()}; "
+                                   f"engines agree: {np.array_equal(outs[0].numpy(), outs[1].numpy())})")
         for e in engs[1:]:
             e.close()
         e2e = {"value": E * F * Ke / dt, "unit": UNIT, "h2d_bytes_per_step": F * props * nw * 8,

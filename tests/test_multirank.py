@@ -1,9 +1,9 @@
 """Multi-rank host logic of the N>1 bench path, on CPU with gloo (world size 2).
 
-bench.py under torchrun shards the abstraction's edge rows contiguously over
-ranks (bench.shard_rows), regenerates only its own rows (the synthetic PRM is
-row-addressable), receives each frame's P by a broadcast from rank 0 and labels
-its shard; the timing is the max over ranks.  Here the CPU oracle stands in for
+bench.py under torchrun gives each rank a spatially compact, word-balanced
+part of the abstraction's edge rows (bench.spatial_shard: rows sorted by median
+swept word, cut into contiguous parts of that order), receives each frame's P by
+a broadcast from rank 0 and labels its shard; the timing is the max over ranks.  Here the CPU oracle stands in for
 the per-rank GPU engine so the sharding / broadcast / reassembly logic is
 checked end to end against a single-process labeling.
 """
@@ -27,6 +27,15 @@ def _free_port():
     return p
 
 
+def _csr_rows(off, idx, rows):
+    """The CSR arrays of the given rows (in that order)."""
+    off = off.astype(np.int64)
+    cnt = off[rows + 1] - off[rows]
+    so = np.zeros(len(rows) + 1, np.int64)
+    np.cumsum(cnt, out=so[1:])
+    return so.astype(np.uint64), idx[np.repeat(off[rows] - so[:-1], cnt) + np.arange(so[-1])]
+
+
 def _worker(rank, world, port, out_dir):
     import sys
 
@@ -40,23 +49,28 @@ def _worker(rank, world, port, out_dir):
     E, depth, props, F = 9_001, 12, 6, 3
     cells = 1 << depth
     nw = (cells + 63) // 64
-    r0, r1 = bench.shard_rows(E, rank, world)
-    off, idx = SyntheticPRM(seed=5, depth=depth).csr(r0, r1)
+    prm = SyntheticPRM(seed=5, depth=depth)
+    T = prm.words(0, E)
+    ids = bench.spatial_shard(T.offsets, T.words, T.masks, rank, world)[0]
+    off, idx = _csr_rows(*prm.csr(0, E), ids)
     P = torch.zeros((F, props, nw), dtype=torch.int64)
     if rank == 0:
         props_words(3, depth, props, 0, F, out=P)
     dist.broadcast(P, src=0)
     o = Oracle()
-    labels = np.stack([o.label_all(r1 - r0, cells, off, idx, cells, props, P[f].numpy().view(np.uint64))
+    labels = np.stack([o.label_all(len(ids), cells, off, idx, cells, props, P[f].numpy().view(np.uint64))
                        for f in range(F)], axis=1)  # edge-major like get_labels_packed
     t = torch.tensor([float(rank + 1)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     sizes = [None] * world
-    dist.all_gather_object(sizes, (r0, r1, labels))
+    dist.all_gather_object(sizes, (ids, labels))
     if rank == 0:
         full = np.zeros((E, F), np.uint64)
-        for a, b, lab in sizes:
-            full[a:b] = lab
+        seen = np.zeros(E, np.int64)
+        for rows, lab in sizes:
+            full[rows] = lab
+            seen[rows] += 1
+        assert (seen == 1).all()  # the parts partition the rows
         np.save(os.path.join(out_dir, "sharded.npy"), full)
         np.save(os.path.join(out_dir, "tmax.npy"), t.numpy())
     dist.destroy_process_group()
@@ -87,6 +101,29 @@ def test_shard_rows_partition():
             assert spans[0][0] == 0 and spans[-1][1] == E
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+
+
+def test_spatial_shard_partition():
+    import bench
+    from paper_1810_02612_b200.synth import SyntheticPRM
+
+    T = SyntheticPRM(seed=5, depth=14).words(0, 20_000)
+    off = T.offsets.astype(np.int64)
+    med = T.words[off[:-1] + (off[1:] - off[:-1]) // 2]
+    for world in (1, 2, 3, 8):
+        parts = [bench.spatial_shard(T.offsets, T.words, T.masks, r, world) for r in range(world)]
+        ids = np.concatenate([p[0] for p in parts])
+        assert np.array_equal(np.sort(ids), np.arange(20_000))  # every row exactly once
+        nwords = [int(p[1][-1]) for p in parts]
+        assert sum(nwords) == len(T.words)
+        assert max(nwords) - min(nwords) <= 2 * int((off[1:] - off[:-1]).max())  # word-balanced
+        for i, (rows, so, w, m) in enumerate(parts):  # each part's arrays are its rows' own
+            for k in (0, len(rows) // 2, len(rows) - 1):
+                r = rows[k]
+                assert np.array_equal(w[so[k]:so[k + 1]], T.words[off[r]:off[r + 1]])
+                assert np.array_equal(m[so[k]:so[k + 1]], T.masks[off[r]:off[r + 1]])
+            if i:  # contiguous ranges of the median-word order
+                assert med[parts[i - 1][0]].max() <= med[rows].min()
 
 
 def test_synthetic_rows_are_row_addressable():
