@@ -551,12 +551,12 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
 
     if rank == 0:
-        # gpu_launches: our kernels per step = pl_summary, pl_scan, pl_fill, label_pl
+        # gpu_launches: our kernels per step = pl_build (the prop-lane summary) and label_pl
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32", "data": "synthetic", "config": cfg_json(world), "clocks": clk.summary(),
-            "gpu_launches": 4 * K, "roofline": roofline, "latency": lat, "e2e": e2e, "cpu_baseline": cpu,
+            "gpu_launches": 2 * K, "roofline": roofline, "latency": lat, "e2e": e2e, "cpu_baseline": cpu,
             "shape": {"W32": W32, "rows": rows_all, "t_bytes_device": int(info.t_bytes)},
         }
         print(json.dumps(line), flush=True)

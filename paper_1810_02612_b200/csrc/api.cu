@@ -120,6 +120,7 @@ struct Shard {
     DevBuf<uint8_t> t64;          // single-frame 64-cell-word copy
     DevBuf<uint64_t> mask_b64, tpair_b64, pb64;  // multi-frame 64-cell-word copy, its Pb table
     DevBuf<uint32_t> word_b64;
+    DevBuf<uint32_t> touched64;  // PackedShard::touched64
     DevBuf<uint64_t> tbyte64;
     DevBuf<uint32_t> tn64;
     DevBuf<uint32_t> perm, trow_s, trow_b;
@@ -229,6 +230,7 @@ ltlg_status upload_shard(ltlg_ctx* ctx, Shard& s, const PackedShard& p) {
     if ((st = put(s.mask_b64, p.mask_b64, "upload T pairs")) != LTLG_OK) return st;
     if ((st = put(s.word_b64, p.word_b64, "upload T pairs")) != LTLG_OK) return st;
     if ((st = put(s.tpair_b64, p.task_pair_b64, "upload tasks")) != LTLG_OK) return st;
+    if ((st = put(s.touched64, p.touched64, "upload word map")) != LTLG_OK) return st;
     if ((st = put(s.perm, p.perm, "upload row permutation")) != LTLG_OK) return st;
     if ((st = put(s.trow_s, p.task_row_stream, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.tpair_s, p.task_pair_stream, "upload tasks")) != LTLG_OK) return st;
@@ -419,6 +421,13 @@ ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
     return LTLG_OK;
 }
 
+// A/B knob LTLG_PL_TOUCHED=0: the prop-lane summary over every word of the
+// grid instead of only the words the shard's pairs are on.
+static bool pl_touched_on() {
+    static const bool on = !getenv("LTLG_PL_TOUCHED") || atoi(getenv("LTLG_PL_TOUCHED")) != 0;
+    return on;
+}
+
 // split: one launch per read-back block (submits whose labels are expected
 // to go back to the host: host-memory P); otherwise one launch.
 ltlg_status run_label(ltlg_ctx* ctx, bool split) {
@@ -499,7 +508,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
                "summary kernel");
         else if (pl)
             CK(launch_pl(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.sf.ptr,
-                         s.sf.bytes, s.ctr.ptr, nctr, s.stream),
+                         s.sf.bytes, s.ctr.ptr, nctr, s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (wide_b)
             CK(launch_summary_b64(s.Pdev(), props, frames, nw64, ctx->cells, s.sf.ptr, nullptr, s.s_only.ptr,
@@ -713,6 +722,7 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.tn64.release();
         s.mask_b64.release();
         s.word_b64.release();
+        s.touched64.release();
         s.tpair_b64.release();
         s.pb64.release();
         s.perm.release();

@@ -49,6 +49,9 @@ struct PackedShard {
     std::vector<uint64_t> mask_b64;
     std::vector<uint32_t> word_b64;
     std::vector<uint64_t> task_pair_b64;  // ntasks + 1
+    // bit w: some pair of the multi-frame copy is on 64-cell word w (the
+    // sentinel word included); the prop-lane summary skips the other words
+    std::vector<uint32_t> touched64;
     uint64_t n_pairs = 0;                 // meaningful pairs (incl. sentinels)
     std::vector<uint32_t> perm;           // sorted position -> local original row
     // warp tasks: [row_begin, row_end) in sorted positions, pairs [pair_begin, pair_end)

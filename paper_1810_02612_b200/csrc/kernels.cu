@@ -1836,7 +1836,7 @@ __global__ void __launch_bounds__(256) pl_summary_kernel(const uint64_t* __restr
                                                          uint32_t nw64, uint64_t cells, uint64_t* __restrict__ ffr,
                                                          uint64_t* __restrict__ sfr, uint32_t* __restrict__ cnt,
                                                          uint32_t* __restrict__ wcnt, uint32_t* __restrict__ task_ctr,
-                                                         int nctr, int pshift) {
+                                                         int nctr, int pshift, const uint32_t* __restrict__ touched64) {
     const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (t < static_cast<uint64_t>(nctr)) task_ctr[t] = 0;
     // consecutive threads take consecutive words of one prop: coalesced rows of P
@@ -1844,6 +1844,13 @@ __global__ void __launch_bounds__(256) pl_summary_kernel(const uint64_t* __restr
     const uint32_t j = static_cast<uint32_t>(t / nwp), w = static_cast<uint32_t>(t - static_cast<uint64_t>(j) * nwp);
     if (j >= (1u << pshift)) return;
     const uint64_t o = (static_cast<uint64_t>(w) << pshift) | j;  // ffr / sfr / cnt index
+    // a word no pair of this shard is on is never looked up: skip its P reads
+    // (a spatial row shard touches a fraction of the grid); the fill kernel
+    // sees no records for it
+    if (touched64 && !(__ldg(touched64 + (w >> 5)) >> (w & 31) & 1u)) {
+        cnt[o] = 0;
+        return;
+    }
     uint64_t full = 0, any = 0;
     uint32_t n = 0;
     const uint64_t lo = static_cast<uint64_t>(w) * 64;
@@ -1901,6 +1908,73 @@ __global__ void __launch_bounds__(256) pl_fill_kernel(const uint64_t* __restrict
     const uint64_t* base = P64 + static_cast<uint64_t>(j) * nw64 + w;
     for (int f = 0; f < frames; ++f) {
         const uint64_t x = base[static_cast<uint64_t>(f) * props * nw64] & valid;
+        if (x != 0 && x != valid)  // smem label accumulator word f + 64 (j / 32), bit j % 32
+            rec[pos++] = make_uint4(static_cast<uint32_t>(x), static_cast<uint32_t>(x >> 32),
+                                    4u * (static_cast<uint32_t>(f) + 64u * (j >> 5)), 1u << (j & 31));
+    }
+}
+
+// The three passes above in one kernel.  A CTA owns WPB consecutive words x
+// all 1 << pshift prop slots (thread j * WPB + wl: consecutive threads read
+// consecutive words of one prop, coalesced).  Per word, the partial-record
+// counts of its props are prefix-summed in shared memory and the word's
+// record segment is taken from one global cursor (segments land in any word
+// order; records stay grouped by prop, in prop order).  Each thread then
+// re-reads its P words (now in L1/L2) and writes its records.
+template <int PSHIFT, int NT>
+__global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict__ P64, int props, int frames,
+                                                        uint32_t nw64, uint64_t cells, uint64_t* __restrict__ ffr,
+                                                        uint64_t* __restrict__ sfr, uint2* __restrict__ rec_se,
+                                                        uint32_t* __restrict__ rec_cursor, uint4* __restrict__ rec,
+                                                        uint32_t* __restrict__ task_ctr, int nctr,
+                                                        const uint32_t* __restrict__ touched64) {
+    constexpr int NP = 1 << PSHIFT, WPB = NT / NP;
+    __shared__ uint32_t s_cnt[NP][WPB];
+    __shared__ uint32_t s_base[WPB];
+    const uint32_t gt = blockIdx.x * static_cast<uint32_t>(NT) + threadIdx.x;
+    if (gt < static_cast<uint32_t>(nctr)) task_ctr[gt] = 0;
+    const uint32_t j = threadIdx.x / WPB, wl = threadIdx.x % WPB;
+    const uint32_t w = blockIdx.x * WPB + wl;
+    const bool in = w <= nw64;  // word nw64 is the zero sentinel
+    const bool live = in && w < nw64 && static_cast<uint64_t>(w) * 64 < cells && j < static_cast<uint32_t>(props) &&
+                      !(touched64 && !(__ldg(touched64 + (w >> 5)) >> (w & 31) & 1u));
+    const uint64_t lo = static_cast<uint64_t>(w) * 64;
+    const uint64_t valid = !live ? 0ull : (cells - lo >= 64) ? ~0ull : ((1ull << (cells - lo)) - 1ull);
+    const uint64_t* base = P64 + static_cast<uint64_t>(j) * nw64 + w;
+    const uint64_t fstride = static_cast<uint64_t>(props) * nw64;
+    uint64_t full = 0, any = 0;
+    uint32_t n = 0;
+    if (live) {
+        for (int f = 0; f < frames; ++f) {
+            const uint64_t x = base[static_cast<uint64_t>(f) * fstride] & valid;
+            any |= static_cast<uint64_t>(x != 0) << f;
+            full |= static_cast<uint64_t>(x == valid) << f;
+            n += (x != 0 && x != valid);
+        }
+    }
+    if (in) {
+        const uint64_t o = (static_cast<uint64_t>(w) << PSHIFT) | j;
+        ffr[o] = full;
+        sfr[o] = any;
+    }
+    s_cnt[j][wl] = n;
+    __syncthreads();
+    if (j == 0 && in) {  // per word: exclusive prefix over props, then its segment
+        uint32_t run = 0;
+        for (int k = 0; k < NP; ++k) {
+            const uint32_t c = s_cnt[k][wl];
+            s_cnt[k][wl] = run;
+            run += c;
+        }
+        const uint32_t b = run ? atomicAdd(rec_cursor, run) : 0u;
+        s_base[wl] = b;
+        rec_se[w] = make_uint2(b, b + run);
+    }
+    __syncthreads();
+    if (!n) return;
+    uint32_t pos = s_base[wl] + s_cnt[j][wl];
+    for (int f = 0; f < frames; ++f) {
+        const uint64_t x = base[static_cast<uint64_t>(f) * fstride] & valid;
         if (x != 0 && x != valid)  // smem label accumulator word f + 64 (j / 32), bit j % 32
             rec[pos++] = make_uint4(static_cast<uint32_t>(x), static_cast<uint32_t>(x >> 32),
                                     4u * (static_cast<uint32_t>(f) + 64u * (j >> 5)), 1u << (j & 31));
@@ -2038,7 +2112,7 @@ struct PlLayout {
 };
 
 cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* work,
-                      size_t work_bytes, uint32_t* task_ctr, int nctr, cudaStream_t st) {
+                      size_t work_bytes, uint32_t* task_ctr, int nctr, cudaStream_t st, const uint32_t* touched64) {
     if (props > 64 || frames > 64) return cudaErrorInvalidValue;
     const int pshift = props > 32 ? 6 : 5;
     const PlLayout L(props, frames, nw64);
@@ -2050,12 +2124,32 @@ cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64,
     uint32_t* wcnt = reinterpret_cast<uint32_t*>(wb + L.wcnt);
     uint32_t* cursor = reinterpret_cast<uint32_t*>(wb + L.cursor);
     uint2* rec_se = reinterpret_cast<uint2*>(wb + L.rec_se);
+    static const bool fused = !getenv("LTLG_PL_FUSED") || atoi(getenv("LTLG_PL_FUSED")) != 0;  // A/B knob
+    if (fused) {
+        cudaError_t e = cudaMemsetAsync(cursor, 0, 4, st);
+        if (e != cudaSuccess) return e;
+        // 32 (16) words x 32 (64) prop slots per CTA.  256-thread CTAs fill the
+        // GPU better (summary 40 -> 43 us anyway) but scatter the word segments
+        // more, and the labelling kernel lost 60 us to record locality.
+        constexpr int kNT = 1024;
+        const int wpb = kNT >> pshift;
+        const uint64_t gw = (static_cast<uint64_t>(nw64) + 1 + wpb - 1) / wpb, gc = (static_cast<uint64_t>(nctr) + kNT - 1) / kNT;
+        const unsigned grid = static_cast<unsigned>(gw > gc ? gw : gc);
+        uint4* rec = reinterpret_cast<uint4*>(wb + L.rec);
+        if (pshift == 5)
+            pl_build_kernel<5, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
+                                                      task_ctr, nctr, touched64);
+        else
+            pl_build_kernel<6, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
+                                                      task_ctr, nctr, touched64);
+        return cudaGetLastError();
+    }
     cudaError_t e = cudaMemsetAsync(wcnt, 0, (nw64 + 2) * 4, st);
     if (e != cudaSuccess) return e;
     const uint64_t nt = L.nt;
     const uint64_t nthreads = nt > static_cast<uint64_t>(nctr) ? nt : static_cast<uint64_t>(nctr);
     pl_summary_kernel<<<static_cast<unsigned>((nthreads + 255) / 256), 256, 0, st>>>(
-        P64, props, frames, nw64, cells, ffr, sfr, cnt, wcnt, task_ctr, nctr, pshift);
+        P64, props, frames, nw64, cells, ffr, sfr, cnt, wcnt, task_ctr, nctr, pshift, touched64);
     pl_scan_kernel<<<1, 1024, 0, st>>>(wcnt, nw64 + 1, rec_se, cursor);
     pl_fill_kernel<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(
         P64, props, frames, nw64, cells, cnt, cursor, reinterpret_cast<uint4*>(wb + L.rec), pshift);

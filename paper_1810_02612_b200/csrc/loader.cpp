@@ -675,6 +675,11 @@ void build_batch64_layout(const WordCsr& t, uint64_t row_begin, uint32_t sentine
             }
         }
     });
+    out->touched64.assign(sentinel64 / 32 + 1, 0u);
+    for (const uint32_t wh : out->word_b64) {
+        const uint32_t w = wh & kWordMask;
+        if (w <= sentinel64) out->touched64[w >> 5] |= 1u << (w & 31);
+    }
     const size_t nt = out->task_row_batch.size() - 1;
     out->task_pair_b64.resize(nt + 1);
     for (size_t k = 0; k <= nt; ++k) out->task_pair_b64[k] = off[out->task_row_batch[k]];
