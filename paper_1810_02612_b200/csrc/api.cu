@@ -373,6 +373,13 @@ ltlg_status run_guards(ltlg_ctx* ctx, Shard& s) {
        "guard kernel");
     return LTLG_OK;
 }
+// A/B knob LTLG_PL_TOUCHED=0: the summaries (prop-lane and single-frame) over
+// every word of the grid instead of only the words the shard's pairs are on.
+static bool pl_touched_on() {
+    static const bool on = !getenv("LTLG_PL_TOUCHED") || atoi(getenv("LTLG_PL_TOUCHED")) != 0;
+    return on;
+}
+
 
 constexpr int kSmallFrames = 16;  // sweep_frames: per-frame single-frame launches win up to ~16 frames (<= 16 props)
 
@@ -388,7 +395,8 @@ ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
     const size_t pw = static_cast<size_t>(props) * nw64;  // u64 words of one frame's P
     for (int f = 0; f < frames; ++f) {
         CK(launch_summary64(s.Pdev() + f * pw, props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr, s.ctr.ptr,
-                            static_cast<int>(kCtrStride), s.stream, nullptr),
+                            static_cast<int>(kCtrStride), s.stream, nullptr,
+                            pl_touched_on() ? s.touched64.ptr : nullptr),
            "summary kernel");
         if (prof && f == 0) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
@@ -419,13 +427,6 @@ ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
     if (prof) CK(cudaEventRecord(s.ev[3], s.stream), "event");
     s.have_times = prof;
     return LTLG_OK;
-}
-
-// A/B knob LTLG_PL_TOUCHED=0: the prop-lane summary over every word of the
-// grid instead of only the words the shard's pairs are on.
-static bool pl_touched_on() {
-    static const bool on = !getenv("LTLG_PL_TOUCHED") || atoi(getenv("LTLG_PL_TOUCHED")) != 0;
-    return on;
 }
 
 // split: one launch per read-back block (submits whose labels are expected
@@ -504,7 +505,8 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         const int f0 = frames * sl / nslice, nf = pl ? frames * (sl + 1) / nslice - f0 : frames;
         if (wide)
             CK(launch_summary64(s.P_host ? s.P_host : s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr,
-                                s.ctr.ptr, nctr, s.stream, s.P_host ? s.P.ptr : nullptr),
+                                s.ctr.ptr, nctr, s.stream, s.P_host ? s.P.ptr : nullptr,
+                                pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (pl)
             CK(launch_pl(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.sf.ptr,

@@ -294,7 +294,8 @@ template <int FMT>
 __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restrict__ P64, int props, uint32_t nw64,
                                                         uint64_t cells, uint8_t* __restrict__ tab,
                                                         void* __restrict__ s_only_g, uint32_t* __restrict__ task_ctr,
-                                                        int nctr, uint64_t* __restrict__ P_copy) {
+                                                        int nctr, uint64_t* __restrict__ P_copy,
+                                                        const uint32_t* __restrict__ touched64) {
     // CTA = 32 consecutive words x 8 warps: warp g reads props g, g+8, ...
     // (coalesced 256-B rows of P), lane = word; the eight partial masks meet
     // in shared memory and warp 0 assembles the entries (first <= 2 / 4
@@ -311,7 +312,9 @@ __global__ void __launch_bounds__(256) summary64_kernel(const uint64_t* __restri
     const uint32_t w = blockIdx.x * 32 + lane;
     uint64_t any = 0, full = 0, part = 0;
     const uint64_t lo = static_cast<uint64_t>(w) * 64;
-    if (w < nw64 && lo < cells) {
+    // words no pair of the shard is on are never looked up: no read of P
+    // (over PCIe when P comes through the host mapping), a zero entry
+    if (w < nw64 && lo < cells && !(touched64 && !(__ldg(touched64 + (w >> 5)) >> (w & 31) & 1u))) {
         const uint64_t valid = (cells - lo >= 64) ? ~0ull : ((1ull << (cells - lo)) - 1ull);
         uint64_t x[8];
 #pragma unroll
@@ -1493,15 +1496,15 @@ cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t 
 }
 
 cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
-                             uint32_t* task_ctr, int nctr, cudaStream_t st, uint64_t* P_copy) {
+                             uint32_t* task_ctr, int nctr, cudaStream_t st, uint64_t* P_copy, const uint32_t* touched64) {
     // 32 words per CTA (word nw64 is the zero sentinel entry); enough CTAs to
     // reset the nctr task counters too
     const uint32_t nblk_w = (nw64 + 1 + 31) / 32, nblk_c = (static_cast<uint32_t>(nctr) + 255) / 256;
     const unsigned grid = nblk_w > nblk_c ? nblk_w : nblk_c;
     switch (entry_format(props)) {
-        case 16: summary64_kernel<16><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr, P_copy); break;
-        case 32: summary64_kernel<32><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr, P_copy); break;
-        default: summary64_kernel<64><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr, P_copy); break;
+        case 16: summary64_kernel<16><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr, P_copy, touched64); break;
+        case 32: summary64_kernel<32><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr, P_copy, touched64); break;
+        default: summary64_kernel<64><<<grid, 256, 0, st>>>(P64, props, nw64, cells, static_cast<uint8_t*>(tab), s_only, task_ctr, nctr, P_copy, touched64); break;
     }
     return cudaGetLastError();
 }

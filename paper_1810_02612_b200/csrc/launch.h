@@ -57,7 +57,8 @@ cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64,
                       const uint32_t* touched64 = nullptr);
 size_t pl_work_bytes(int props, int frames, uint32_t nw64);
 cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
-                             uint32_t* task_ctr, int nctr, cudaStream_t st, uint64_t* P_copy);
+                             uint32_t* task_ctr, int nctr, cudaStream_t st, uint64_t* P_copy,
+                             const uint32_t* touched64 = nullptr);
 bool stream_table_in_smem(int props, uint32_t nw32);
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st);
 cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, int frames, int frame,
