@@ -164,7 +164,11 @@ def spatial_shard(offsets, words, masks, rank: int, world: int):
     if world == 1:
         return np.arange(E, dtype=np.int64), offsets, words, masks
     cnt = off[1:] - off[:-1]
-    med = np.asarray(words)[off[:-1] + cnt // 2] if len(words) else np.zeros(E, np.uint32)
+    # empty rows sort as word 0 (the engine's own key, loader.cpp); their
+    # offset may be len(words), so never index with it
+    w = np.asarray(words)
+    med = (np.where(cnt > 0, w[np.minimum(off[:-1] + cnt // 2, len(w) - 1)], 0) if len(w)
+           else np.zeros(E, np.uint32))
     order = np.argsort(med, kind="stable")
     cum = np.cumsum(cnt[order])
     total = int(cum[-1]) if E else 0

@@ -252,6 +252,25 @@ ltlg_status ltlg_wait(ltlg_ctx* ctx);
  * (rows x ceil(props/64) u64).  Synchronous. */
 ltlg_status ltlg_get_labels(ltlg_ctx* ctx, int frame, uint64_t* out);
 
+/* apply_labels (reference label.cpp:191-210, label.hpp:107-114): the labels of
+ * one frame as per-edge AlphabetSymbol bits (alphabet.hpp:39-46) -- the
+ * EdgeLabeling hand-off a planner / monitor consumes (planner.cpp:56).
+ * num_edges is the TransitionSystem's num_edges(), alphabet_size the
+ * Alphabet's size(); the reference's two checks run in its order with its
+ * messages ("label matrix rows R vs edges E", "label matrix props P vs
+ * alphabet size A"; LTLG_EINVAL).  symbols = num_edges u64 (zeros when
+ * props == 0).  Synchronous. */
+ltlg_status ltlg_apply_labels(ltlg_ctx* ctx, int frame, uint64_t num_edges, int alphabet_size,
+                              uint64_t* symbols);
+
+/* label_edge_counting (reference label.cpp:140-148, the Eq. 14 diagnostic of
+ * bernoulli_experiment, scenario.cpp:232-255) for EVERY resident edge against
+ * one (frame, prop) column of the last submit, on the device: hit[i] = label
+ * bit, examined[i] = number of the row's stored indices a linear scan
+ * examines (first witness position + 1, or the row's nnz).  hit: rows bytes,
+ * examined: rows u64 (either may be NULL).  Synchronous. */
+ltlg_status ltlg_edge_counting(ltlg_ctx* ctx, int frame, int prop, uint8_t* hit, uint64_t* examined);
+
 /* Copy all frames' packed labels: edge-major rows x frames words of
  * ltlg_info.label_bytes each (bit j = prop j).  out_bytes must be >=
  * rows * frames * label_bytes.  Synchronous. */

@@ -20,7 +20,8 @@
 #include <string>
 #include <vector>
 
-#include "ltlgrid/abstraction.hpp"  // TransitionSystem / FootprintSpec (swept_volume_matrix)
+#include "ltlgrid/abstraction.hpp"  // TransitionSystem / FootprintSpec (swept_volume_matrix, apply_labels)
+#include "ltlgrid/alphabet.hpp"     // Alphabet / AlphabetSymbol (apply_labels)
 #include "ltlgrid/grid.hpp"
 #include "ltlgrid/label.hpp"  // the reference's CsrBoolMatrix / DensePropMatrix / LabelMatrix
 #include "ltlgrid_gpu.h"
@@ -97,6 +98,18 @@ public:
         std::vector<std::uint64_t> words(info.rows * static_cast<std::uint64_t>(info.label_words));
         check(ltlg_get_labels(ctx_, frame, words.empty() ? nullptr : words.data()), ctx_);
         return to_label_matrix<Labels>(info.rows, info.props, words);
+    }
+    // Drop-in for ltlgrid::apply_labels (label.cpp:191-210) over this engine's
+    // labels of `frame`: same checks, order, exception type and messages.
+    EdgeLabeling apply_labels(const TransitionSystem& s, const Alphabet& alphabet, int frame = 0) {
+        std::vector<std::uint64_t> sym(s.num_edges());
+        check(ltlg_apply_labels(ctx_, frame, s.num_edges(), alphabet.size(), sym.empty() ? nullptr : sym.data()),
+              ctx_);
+        EdgeLabeling out;
+        out.alphabet_size = alphabet.size();
+        out.labels.resize(sym.size());
+        for (std::size_t i = 0; i < sym.size(); ++i) out.labels[i].bits = sym[i];
+        return out;
     }
     ltlg_ctx* handle() const { return ctx_; }
 

@@ -90,6 +90,35 @@ int main() {
             eng.submit(p);
             expect(eng.labels<LabelMatrix>() == label_all(csr, p), "engine frame " + std::to_string(f));
         }
+        // apply_labels (label.cpp:191-210): the EdgeLabeling hand-off
+        std::vector<std::string> names;
+        for (int j = 0; j < 20; ++j) names.push_back("p" + std::to_string(j));
+        const Alphabet alphabet(names);
+        TransitionSystem ts;
+        ts.edges.resize(700);
+        auto cols = random_rows(rng, 20, 16384, 0.004);
+        DensePropMatrix p(16384, cols);
+        eng.submit(p);
+        const EdgeLabeling want = apply_labels(ts, label_all(csr, p), alphabet);
+        const EdgeLabeling got = eng.apply_labels(ts, alphabet);
+        expect(got.alphabet_size == want.alphabet_size && got.labels == want.labels, "apply_labels");
+        for (int which = 0; which < 2; ++which) {  // row mismatch, then alphabet mismatch
+            TransitionSystem t2;
+            t2.edges.resize(which ? 700 : 699);
+            const Alphabet a2(std::vector<std::string>(names.begin(), names.end() - 1));
+            std::string ra, ga;
+            try {
+                apply_labels(t2, label_all(csr, p), a2);
+            } catch (const std::invalid_argument& e) {
+                ra = e.what();
+            }
+            try {
+                eng.apply_labels(t2, a2);
+            } catch (const std::invalid_argument& e) {
+                ga = e.what();
+            }
+            expect(!ra.empty() && ra == ga, "apply_labels error: " + ra);
+        }
     }
     // swept_volume_matrix (label.cpp:75-116) vs ltlgrid::gpu::swept_volume_matrix on the
     // reference's own build_abstraction output (test_label.cpp:212-235 configuration)

@@ -318,7 +318,49 @@ class RefCore:
         L.ref_guard_admits.restype = None
         L.ref_save_bitset.argtypes = [C.c_char_p, i32, i32, P64]
         L.ref_save_bitset.restype = i32
+        L.ref_label_load.argtypes = [C.c_char_p, P64, C.POINTER(i32), P64, u64]
+        L.ref_label_load.restype = i32
+        L.ref_label_to_csv.argtypes = [u64, i32, P64, C.c_char_p, C.c_char_p, u64]
+        L.ref_label_to_csv.restype = C.c_int64
+        L.ref_to_csr.argtypes = [u64, u64, P64, P64, P32, u64]
+        L.ref_to_csr.restype = C.c_int64
         self.lib = L
+
+    def label_load(self, path):
+        """LabelMatrix::load (label.cpp:311-326) -> (rows, props, words) or raises RuntimeError/ValueError."""
+        rows, props = C.c_uint64(0), C.c_int(0)
+        if self.lib.ref_label_load(str(path).encode(), C.byref(rows), C.byref(props), None, 0):
+            raise RuntimeError(self.error())
+        n = rows.value * ((props.value + 63) // 64)
+        out = np.zeros(max(n, 1), np.uint64)
+        self.lib.ref_label_load(str(path).encode(), C.byref(rows), C.byref(props), _p(out, C.c_uint64), out.size)
+        return rows.value, props.value, out[:n]
+
+    def label_to_csv(self, rows, props, words, names):
+        """LabelMatrix::to_csv (label.cpp:328-344) with Alphabet(names)."""
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        if w.size == 0:
+            w = np.zeros(1, np.uint64)
+        nm = "".join(n + "\n" for n in names).encode()
+        n = self.lib.ref_label_to_csv(rows, props, _p(w, C.c_uint64), nm, None, 0)
+        if n < 0:
+            raise ValueError(self.error())
+        buf = C.create_string_buffer(n + 1)
+        self.lib.ref_label_to_csv(rows, props, _p(w, C.c_uint64), nm, buf, n + 1)
+        return buf.raw[:n].decode()
+
+    def to_csr(self, rows, cols, words):
+        """to_csr (label.cpp:42-57) of dense bitset rows (ceil(cols/64) u64 words each)."""
+        w = np.ascontiguousarray(words, dtype=np.uint64).reshape(-1)
+        if w.size == 0:
+            w = np.zeros(1, np.uint64)
+        off = np.zeros(rows + 1, np.uint64)
+        n = self.lib.ref_to_csr(rows, cols, _p(w, C.c_uint64), _p(off, C.c_uint64), None, 0)
+        if n < 0:
+            raise ValueError(self.error())
+        idx = np.zeros(max(n, 1), np.uint32)
+        self.lib.ref_to_csr(rows, cols, _p(w, C.c_uint64), _p(off, C.c_uint64), _p(idx, C.c_uint32), idx.size)
+        return off, idx[:n]
 
     def error(self) -> str:
         return self.lib.ref_last_error().decode()

@@ -221,6 +221,78 @@ int ref_label_save(const char* path, std::uint64_t rows, int props, const std::u
     }
 }
 
+// LabelMatrix::load (label.cpp:311-326): shape into rows/props; words into
+// out when cap (u64 words) suffices. Returns 0 ok, 1 error (ref_last_error).
+int ref_label_load(const char* path, std::uint64_t* rows, int* props, std::uint64_t* out, std::uint64_t cap) {
+    try {
+        const ltlgrid::LabelMatrix l = ltlgrid::LabelMatrix::load(path);
+        *rows = l.rows();
+        *props = l.props();
+        const std::uint64_t n = l.rows() * static_cast<std::uint64_t>((l.props() + 63) / 64);
+        if (out && n <= cap) export_labels(l, out);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// LabelMatrix::to_csv (label.cpp:328-344) with an Alphabet of `names`
+// ('\n'-separated). Returns the CSV length (written to out if cap suffices),
+// or -1 on error.
+std::int64_t ref_label_to_csv(std::uint64_t rows, int props, const std::uint64_t* words, const char* names,
+                              char* out, std::uint64_t cap) {
+    try {
+        ltlgrid::LabelMatrix l(rows, props);
+        const int wpr = (props + 63) / 64;
+        for (std::uint64_t i = 0; i < rows; ++i)
+            for (int j = 0; j < props; ++j) {
+                const std::uint64_t bit = i * static_cast<std::uint64_t>(wpr) * 64 + j;
+                if ((words[bit >> 6] >> (bit & 63)) & 1u) l.set(i, j);
+            }
+        std::vector<std::string> nm;
+        std::string cur;
+        for (const char* c = names; *c; ++c) {
+            if (*c == '\n') {
+                nm.push_back(cur);
+                cur.clear();
+            } else {
+                cur.push_back(*c);
+            }
+        }
+        if (!cur.empty()) nm.push_back(cur);
+        const ltlgrid::Alphabet a(nm);
+        const std::string csv = l.to_csv(a);
+        if (out && csv.size() <= cap) std::memcpy(out, csv.data(), csv.size());
+        return static_cast<std::int64_t>(csv.size());
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1;
+    }
+}
+
+// to_csr (label.cpp:42-57) of `rows` dense bitset rows of `cols` bits each
+// (u64 words, ceil(cols/64) per row). Returns nnz, or -1 on error; offsets /
+// indices written when nnz <= cap.
+std::int64_t ref_to_csr(std::uint64_t rows, std::uint64_t cols, const std::uint64_t* words, std::uint64_t* offsets,
+                        std::uint32_t* indices, std::uint64_t cap) {
+    try {
+        const std::uint64_t wpr = (cols + 63) / 64;
+        std::vector<ltlgrid::OccupancyBitset> r;
+        for (std::uint64_t i = 0; i < rows; ++i)
+            r.push_back(ltlgrid::OccupancyBitset::from_words(
+                cols, std::vector<std::uint64_t>(words + i * wpr, words + (i + 1) * wpr)));
+        const ltlgrid::CsrBoolMatrix m = ltlgrid::to_csr(r);
+        if (m.col_indices.size() <= cap) {
+            std::copy(m.row_offsets.begin(), m.row_offsets.end(), offsets);
+            std::copy(m.col_indices.begin(), m.col_indices.end(), indices);
+        }
+        return static_cast<std::int64_t>(m.col_indices.size());
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1;
+    }
+}
+
 std::uint64_t ref_z_index(int k, int depth, const double* lo, const double* hi, const double* p) {
     try {
         std::vector<std::pair<double, double>> b;

@@ -6,11 +6,11 @@ abstractions -- a drop-in for the reference's labeling path
   label.label_all     one-shot drop-in for ltlgrid::label_all
   synth               synthetic T / P of the BASELINE configs
 """
-from .label import (CsrBoolMatrix, DensePropMatrix, DomainError, FootprintSpec, LabelEngine,  # noqa: F401
+from .label import (CsrBoolMatrix, DensePropMatrix, DomainError, EdgeLabeling, FootprintSpec, LabelEngine,  # noqa: F401
                     LabelMatrix, LtlgError, OccupancyBitset, ScenarioConfig, SweptVolume, generate_scenario,
                     label_all, rasterize_boxes,
                     read_csb1_shape, read_zobv, swept_volume, swept_volume_matrix, to_csr)
 
-__all__ = ["CsrBoolMatrix", "DensePropMatrix", "DomainError", "FootprintSpec", "LabelEngine", "LabelMatrix",
+__all__ = ["CsrBoolMatrix", "DensePropMatrix", "DomainError", "EdgeLabeling", "FootprintSpec", "LabelEngine", "LabelMatrix",
            "LtlgError", "OccupancyBitset", "ScenarioConfig", "SweptVolume", "generate_scenario", "label_all", "rasterize_boxes", "read_csb1_shape",
            "read_zobv", "swept_volume", "swept_volume_matrix", "to_csr"]

@@ -28,7 +28,7 @@ EXPORTS = [
     "ltlg_submit_grid_device_ex",
     "ltlg_swept_volume", "ltlg_csr_rows", "ltlg_csr_cols", "ltlg_csr_nnz", "ltlg_csr_build_ms", "ltlg_csr_copy",
     "ltlg_load_csr", "ltlg_csr_free", "ltlg_set_profiling", "ltlg_generate_scenario", "ltlg_submit_scenario",
-    "ltlg_csr_save",
+    "ltlg_csr_save", "ltlg_apply_labels", "ltlg_edge_counting",
 ]
 
 
@@ -103,6 +103,8 @@ def lib() -> C.CDLL:
         "ltlg_submit_world_grid": ([ctxp, C.POINTER(Grid2), C.POINTER(Grid2), i32, vp, i32, vp, i32, i32], i32),
         "ltlg_wait": ([ctxp], i32),
         "ltlg_get_labels": ([ctxp, i32, vp], i32),
+        "ltlg_apply_labels": ([ctxp, i32, u64, i32, vp], i32),
+        "ltlg_edge_counting": ([ctxp, i32, i32, vp, vp], i32),
         "ltlg_get_labels_packed": ([ctxp, vp, C.c_size_t], i32),
         "ltlg_device_labels": ([ctxp, i32, C.POINTER(vp), P64, P64, C.POINTER(i32)], i32),
         "ltlg_get_info": ([ctxp, C.POINTER(Info)], i32),

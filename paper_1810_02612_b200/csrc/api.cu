@@ -128,12 +128,17 @@ struct Shard {
     DevBuf<uint64_t> P;  // frames x props x nw64
     const uint64_t* P_in = nullptr;  // caller's device P used in place (single device)
     // caller's pinned host P, device-mapped: the single-frame summary kernel
-    // reads it over PCIe and writes the device copy as it goes (no separate H2D)
+    // reads it over PCIe and writes the device copy as it goes (no separate H2D).
+    // That copy is PARTIAL: only the words some pair of this shard is on are
+    // written (touched64), which are the only words the labeling kernel reads.
+    // Any other reader of s.P after a fused submit must not assume the rest.
+    // Consumed (reset) by run_label on every path.
     const uint64_t* P_host = nullptr;
     const uint64_t* Pdev() const { return P_in ? P_in : P.ptr; }
     DevBuf<uint8_t> sf;
     DevBuf<uint8_t> labels;
     DevBuf<uint64_t> stage;
+    DevBuf<uint8_t> stage_hit;  // ltlg_edge_counting
     DevBuf<uint64_t> world;
     DevBuf<uint8_t> poses;
     DevBuf<uint64_t> poses_off;  // box offsets of ltlg_submit_boxes
@@ -436,6 +441,11 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
     const int props = ctx->props, frames = ctx->frames;
     for (Shard& s : ctx->shards) {
         CK(cudaSetDevice(s.device), "cudaSetDevice");
+        // the caller's pinned P mapping is good for this submit only: consume it
+        // here on every path, so no later submit (world grid, boxes, scenario)
+        // can read a stale host buffer
+        const uint64_t* const P_host = s.P_host;
+        s.P_host = nullptr;
         const size_t lab = s.rows() * static_cast<size_t>(frames) * static_cast<size_t>(ctx->label_bytes);
         CK(s.labels.reserve(lab ? lab : 8), "allocate labels");
         if (props == 0 || s.rows() == 0) {
@@ -452,12 +462,10 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // 64-cell-word single-frame path (dev knob LTLG_STREAM64=0 selects the 32-cell copy for A/B runs)
         static const bool wide_ok = !getenv("LTLG_STREAM64") || atoi(getenv("LTLG_STREAM64")) != 0;
         const bool wide = wide_ok && frames == 1;
-        if (s.P_host && !wide) {  // the fused upload only exists on the single-frame 64-cell path
-            CK(cudaMemcpyAsync(s.P.ptr, s.P_host, static_cast<size_t>(frames) * props * nw64 * 8,
+        if (P_host && !wide)  // the fused upload only exists on the single-frame 64-cell path
+            CK(cudaMemcpyAsync(s.P.ptr, P_host, static_cast<size_t>(frames) * props * nw64 * 8,
                                cudaMemcpyHostToDevice, s.stream),
                "upload P");
-            s.P_host = nullptr;
-        }
         // Few frames: the frame-per-lane multi-frame kernel would leave most
         // lanes idle (its cost is ~flat for frames <= 32), so label frame by
         // frame with the single-frame kernel, each launch writing one column
@@ -504,8 +512,8 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // balanced slices (65 frames -> 33 + 32, not 64 + 1)
         const int f0 = frames * sl / nslice, nf = pl ? frames * (sl + 1) / nslice - f0 : frames;
         if (wide)
-            CK(launch_summary64(s.P_host ? s.P_host : s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr,
-                                s.ctr.ptr, nctr, s.stream, s.P_host ? s.P.ptr : nullptr,
+            CK(launch_summary64(P_host ? P_host : s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr,
+                                s.ctr.ptr, nctr, s.stream, P_host ? s.P.ptr : nullptr,
                                 pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (pl)
@@ -1281,6 +1289,53 @@ ltlg_status ltlg_device_admitted(ltlg_ctx* ctx, int shard, void** dev_ptr) {
 ltlg_status ltlg_wait(ltlg_ctx* ctx) {
     DeviceGuard device_guard;  // the caller's current device is restored on return
     if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    return sync_all(ctx);
+}
+
+ltlg_status ltlg_apply_labels(ltlg_ctx* ctx, int frame, uint64_t num_edges, int alphabet_size, uint64_t* symbols) {
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
+    // label.cpp:193-200, in the reference's order and words
+    if (ctx->rows != num_edges)
+        return set_err(ctx, LTLG_EINVAL,
+                       "label matrix rows " + std::to_string(ctx->rows) + " vs edges " + std::to_string(num_edges));
+    if (ctx->props != alphabet_size)
+        return set_err(ctx, LTLG_EINVAL,
+                       "label matrix props " + std::to_string(ctx->props) + " vs alphabet size " +
+                           std::to_string(alphabet_size));
+    if (frame < 0 || frame >= ctx->frames) return set_err(ctx, LTLG_EINVAL, "frame out of range");
+    if (num_edges && !symbols) return set_err(ctx, LTLG_EINVAL, "null output");
+    if (ctx->props == 0) {  // every AlphabetSymbol is empty (label.cpp:205-208)
+        if (num_edges) std::memset(symbols, 0, num_edges * 8);
+        return sync_all(ctx);
+    }
+    // props <= 64: one LabelMatrix word per edge == AlphabetSymbol::bits
+    return ltlg_get_labels(ctx, frame, symbols);
+}
+
+ltlg_status ltlg_edge_counting(ltlg_ctx* ctx, int frame, int prop, uint8_t* hit, uint64_t* examined) {
+    DeviceGuard device_guard;
+    if (!ctx) return set_err(nullptr, LTLG_EINVAL, "null context");
+    if (!ctx->submitted) return set_err(ctx, LTLG_ESTATE, "no grid submitted");
+    if (frame < 0 || frame >= ctx->frames) return set_err(ctx, LTLG_EINVAL, "frame out of range");
+    if (prop < 0 || prop >= ctx->props) return set_err(ctx, LTLG_EINVAL, "prop out of range");
+    const uint64_t nw64 = (ctx->cells + 63) / 64;
+    const size_t colw = (static_cast<size_t>(frame) * ctx->props + static_cast<size_t>(prop)) * nw64;
+    for (Shard& s : ctx->shards) {
+        if (s.rows() == 0) continue;
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        CK(s.stage.reserve(s.rows() * 8), "allocate staging");
+        CK(s.stage_hit.reserve(s.rows()), "allocate staging");
+        CK(launch_edge_count(s.mask_b64.ptr, s.word_b64.ptr, s.tpair_b64.ptr, s.trow_b.ptr, s.ntask_batch, s.perm.ptr,
+                             s.Pdev() + colw, s.stage_hit.ptr, s.stage.ptr, s.stream),
+           "edge counting kernel");
+        if (hit)
+            CK(cudaMemcpyAsync(hit + s.row_begin, s.stage_hit.ptr, s.rows(), cudaMemcpyDeviceToHost, s.stream),
+               "download");
+        if (examined)
+            CK(cudaMemcpyAsync(examined + s.row_begin, s.stage.ptr, s.rows() * 8, cudaMemcpyDeviceToHost, s.stream),
+               "download");
+    }
     return sync_all(ctx);
 }
 

@@ -2244,6 +2244,59 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// label_edge_counting (label.cpp:140-148) for every row against one P column:
+// a thread walks one batch task's 64-cell pairs in order.  Within a row the
+// words ascend and a word's bit b is cell 64 w + b, so the reference's linear
+// scan over ascending cell indices examines, for the first pair with a hit,
+// the cells of the earlier pairs plus the mask bits below the lowest hit bit,
+// plus the witness itself; with no hit it examines all of the row's cells.
+__global__ void __launch_bounds__(256) edge_count_kernel(const uint64_t* __restrict__ masks,
+                                                         const uint32_t* __restrict__ words,
+                                                         const uint64_t* __restrict__ task_pair,
+                                                         const uint32_t* __restrict__ task_row, uint32_t ntasks,
+                                                         const uint32_t* __restrict__ perm,
+                                                         const uint64_t* __restrict__ col, uint8_t* __restrict__ hit,
+                                                         uint64_t* __restrict__ examined) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntasks) return;
+    int64_t row = static_cast<int64_t>(task_row[t]) - 1;
+    uint64_t before = 0, at = 0;
+    bool found = false;
+    auto close = [&]() {
+        const uint32_t r = perm[row];
+        if (hit) hit[r] = found ? 1 : 0;
+        if (examined) examined[r] = found ? at : before;
+    };
+    for (uint64_t q = task_pair[t]; q < task_pair[t + 1]; ++q) {
+        const uint32_t wh = words[q];
+        const uint64_t m = masks[q];
+        if (wh & kHead) {
+            if (row >= static_cast<int64_t>(task_row[t])) close();
+            ++row;
+            before = 0;
+            found = false;
+        }
+        if (found || !m) continue;  // (the empty row's sentinel pair has mask 0)
+        const uint64_t x = m & __ldg(col + (wh & kWordMask));
+        if (x) {
+            at = before + __popcll(m & ((x & (~x + 1)) - 1)) + 1;
+            found = true;
+        } else {
+            before += __popcll(m);
+        }
+    }
+    if (row >= static_cast<int64_t>(task_row[t])) close();
+}
+
+cudaError_t launch_edge_count(const uint64_t* masks, const uint32_t* words, const uint64_t* task_pair,
+                              const uint32_t* task_row, uint32_t ntasks, const uint32_t* perm, const uint64_t* col,
+                              uint8_t* hit, uint64_t* examined, cudaStream_t st) {
+    if (ntasks == 0) return cudaSuccess;
+    edge_count_kernel<<<(ntasks + 255) / 256, 256, 0, st>>>(masks, words, task_pair, task_row, ntasks, perm, col, hit,
+                                                            examined);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, int frames, int frame,
                            uint64_t* out, cudaStream_t st) {
     if (rows == 0) return cudaSuccess;

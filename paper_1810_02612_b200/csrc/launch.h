@@ -63,6 +63,9 @@ bool stream_table_in_smem(int props, uint32_t nw32);
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st);
 cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, int frames, int frame,
                            uint64_t* out, cudaStream_t st);
+cudaError_t launch_edge_count(const uint64_t* masks, const uint32_t* words, const uint64_t* task_pair,
+                              const uint32_t* task_row, uint32_t ntasks, const uint32_t* perm, const uint64_t* col,
+                              uint8_t* hit, uint64_t* examined, cudaStream_t st);
 cudaError_t launch_guards(const void* labels, int label_bytes, uint64_t n, const uint64_t* lut, uint64_t always,
                           uint64_t all_guards, uint64_t* admitted, cudaStream_t st);
 cudaError_t launch_lane(int depth, const uint64_t* flags, int ncols, int col0, int col_step, uint64_t* out,

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+from dataclasses import dataclass
 from typing import Iterable, Optional, Sequence
 
 import numpy as np
@@ -317,6 +318,14 @@ class LabelMatrix:
 # The engine (load abstraction -> submit grid -> get labels)
 # ---------------------------------------------------------------------------
 
+@dataclass
+class EdgeLabeling:
+    """label.hpp:107-110: per-edge label sets (AlphabetSymbol::bits, one u64
+    per edge, bit j = proposition j)."""
+    alphabet_size: int
+    labels: np.ndarray
+
+
 class LabelEngine:
     """One ltlg_ctx: T resident in HBM (sharded over `devices`), per-frame P
     submissions, labels resident per shard (include/ltlgrid_gpu.h)."""
@@ -469,6 +478,24 @@ class LabelEngine:
         buf = l.bits if l.bits.size else None
         self._ck(self._L.ltlg_get_labels(self._h, frame, _ptr(buf)))
         return l
+
+    def apply_labels(self, num_edges: int, alphabet_size: int, frame: int = 0) -> "EdgeLabeling":
+        """ltlg_apply_labels: apply_labels (label.cpp:191-210) -- one frame's
+        labels as per-edge AlphabetSymbol bits, with the reference's row /
+        alphabet-size checks and messages (ValueError)."""
+        out = np.zeros(max(int(num_edges), 1), np.uint64)
+        self._ck(self._L.ltlg_apply_labels(self._h, frame, int(num_edges), int(alphabet_size), _ptr(out)))
+        return EdgeLabeling(int(alphabet_size), out[: int(num_edges)])
+
+    def edge_counting(self, frame: int = 0, prop: int = 0):
+        """ltlg_edge_counting: label_edge_counting (label.cpp:140-148) of every
+        edge against column `prop` of frame `frame`, on the device.  Returns
+        (hit bool[rows], examined uint64[rows])."""
+        i = self.info()
+        hit = np.zeros(max(i.rows, 1), np.uint8)
+        ex = np.zeros(max(i.rows, 1), np.uint64)
+        self._ck(self._L.ltlg_edge_counting(self._h, frame, prop, _ptr(hit), _ptr(ex)))
+        return hit[: i.rows].astype(bool), ex[: i.rows]
 
     def get_labels_packed(self, out=None):
         """All frames, edge-major [rows, frames] of the packed label word

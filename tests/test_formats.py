@@ -148,3 +148,102 @@ def test_zobv_errors(refcore, tmp_path):
         read_zobv(str(trunc), 256)
     with pytest.raises(RuntimeError, match="cannot open"):
         read_zobv(str(tmp_path / "missing.zobv"), 256)
+
+
+# ---------------------------------------------------------------------------
+# LBM1 load / to_csv (label.cpp:311-344) and to_csr (label.cpp:42-57): the
+# package's LabelMatrix / to_csr against the unmodified reference core.
+# ---------------------------------------------------------------------------
+
+def _labels(seed, rows, props):
+    from paper_1810_02612_b200 import LabelMatrix
+
+    rng = np.random.default_rng(seed)
+    l = LabelMatrix(rows, props)
+    if rows and props:
+        l.bits[:] = rng.integers(0, 2**63, size=l.bits.size, dtype=np.uint64)
+        if props < 64:
+            l.bits &= np.uint64((1 << props) - 1)
+    return l
+
+
+@pytest.mark.parametrize("rows,props", [(0, 0), (0, 5), (7, 0), (13, 1), (100, 17), (33, 63), (50, 64)])
+def test_lbm1_load_roundtrip_vs_reference(refcore, tmp_path, rows, props):
+    from paper_1810_02612_b200 import LabelMatrix
+
+    l = _labels(rows * 64 + props, rows, props)
+    ours = tmp_path / "ours.lbm1"
+    l.save(str(ours))
+    ref = tmp_path / "ref.lbm1"
+    refcore.label_save(str(ref), rows, props, l.bits)
+    assert ours.read_bytes() == ref.read_bytes()
+    r, p, w = refcore.label_load(str(ours))
+    got = LabelMatrix.load(str(ref))
+    assert (got.rows(), got.props()) == (r, p) == (rows, props)
+    assert np.array_equal(got.bits, w) and got == l
+
+
+def test_lbm1_load_errors_match_reference(refcore, tmp_path):
+    from paper_1810_02612_b200 import LabelMatrix
+
+    good = tmp_path / "good.lbm1"
+    _labels(5, 40, 20).save(str(good))
+    data = good.read_bytes()
+    cases = {
+        "magic": b"LBMX" + data[4:],
+        "short_magic": data[:3],
+        "version": data[:4] + struct.pack("<I", 2) + data[8:],
+        "words": data[:-1],            # truncated inside the label words
+        "no_words": data[:20],         # header only
+        "props65": data[:16] + struct.pack("<I", 65) + data[20:],
+    }
+    for name, blob in cases.items():
+        p = tmp_path / (name + ".lbm1")
+        p.write_bytes(blob)
+        try:
+            refcore.label_load(str(p))
+            want = None
+        except RuntimeError as e:
+            want = str(e)
+        with pytest.raises((RuntimeError, ValueError)) as ei:
+            LabelMatrix.load(str(p))
+        assert want is not None and str(ei.value) == want, name
+    with pytest.raises(RuntimeError) as ei:
+        LabelMatrix.load(str(tmp_path / "missing.lbm1"))
+    try:
+        refcore.label_load(str(tmp_path / "missing.lbm1"))
+    except RuntimeError as e:
+        assert str(ei.value) == str(e)
+
+
+@pytest.mark.parametrize("rows,props", [(0, 3), (9, 0), (25, 4), (60, 64)])
+def test_to_csv_vs_reference(refcore, rows, props):
+    l = _labels(rows + 7 * props, rows, props)
+    names = [f"p{j}_{'x' * (j % 3)}" for j in range(props)]
+    assert l.to_csv(names) == refcore.label_to_csv(rows, props, l.bits, names)
+    other = names[:-1] if props == 64 else names + ["extra"]  # (an Alphabet holds <= 64 names)
+    with pytest.raises(ValueError, match="^alphabet size mismatch$"):
+        l.to_csv(other)
+    with pytest.raises(ValueError, match="^alphabet size mismatch$"):
+        refcore.label_to_csv(rows, props, l.bits, other)
+
+
+@pytest.mark.parametrize("rows,cols,density", [(0, 10, 0.1), (1, 1, 1.0), (40, 63, 0.1), (40, 64, 0.3),
+                                               (77, 1000, 0.01), (5, 130, 0.0)])
+def test_to_csr_vs_reference(refcore, rows, cols, density):
+    from oracle.oracle import bits_to_words
+    from paper_1810_02612_b200 import OccupancyBitset, to_csr as pkg_to_csr
+
+    dense = random_rows(SplitMix64(rows * 1000 + cols), rows, cols, density)
+    words = bits_to_words(dense) if rows else np.zeros((0, (cols + 63) // 64), np.uint64)
+    m = pkg_to_csr([OccupancyBitset.from_words(cols, words[i]) for i in range(rows)])
+    off, idx = refcore.to_csr(rows, cols, words)
+    assert m.rows == rows and m.cols == (cols if rows else 0)
+    assert np.array_equal(m.row_offsets, off) and np.array_equal(m.col_indices, idx)
+
+
+def test_to_csr_length_mismatch_vs_reference():
+    from paper_1810_02612_b200 import OccupancyBitset, to_csr as pkg_to_csr
+
+    with pytest.raises(ValueError, match="^row length mismatch$"):
+        pkg_to_csr([OccupancyBitset(10), OccupancyBitset(11)])

@@ -217,7 +217,29 @@ def test_synthetic_configs_full(cfg):
     eng.close()
 
 
+def _sampled_csr(prm, row_ids, chunk=100_000):
+    """Reference CSR arrays of the given (sorted) rows only, generated chunk by
+    chunk (row i of the synthetic PRM depends only on (seed, i))."""
+    row_ids = np.asarray(row_ids, dtype=np.int64)
+    offs, idxs, base = [np.zeros(1, np.uint64)], [], 0
+    for c0 in range(0, int(row_ids[-1]) + 1, chunk):
+        sel = row_ids[(row_ids >= c0) & (row_ids < c0 + chunk)] - c0
+        if not sel.size:
+            continue
+        off, idx = prm.csr(c0, min(c0 + chunk, int(row_ids[-1]) + 1))
+        cnt = (off[sel + 1] - off[sel]).astype(np.int64)
+        take = np.concatenate([np.arange(int(off[i]), int(off[i + 1])) for i in sel]) if cnt.sum() else np.zeros(0, int)
+        idxs.append(idx[take])
+        offs.append(base + np.cumsum(cnt).astype(np.uint64))
+        base += int(cnt.sum())
+    return np.concatenate(offs), (np.concatenate(idxs) if idxs else np.zeros(0, np.uint32))
+
+
 def test_config4_batched_frames():
+    """BASELINE config 4 (the bench's `value` workload: 2M edges x 64 frames,
+    512^2, 32 props) through the prop-lane kernel, against the oracle:
+    every one of the 64 frames on a row sample (every 97th row), plus three
+    frames on all 2M rows."""
     c = CONFIGS[4]
     depth, E, props, F = c["depth"], c["edges"], c["props"], c["frames"]
     prm = SyntheticPRM(seed=1, depth=depth)
@@ -227,19 +249,74 @@ def test_config4_batched_frames():
     eng.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
     eng.submit_grid(1 << depth, props, P, F)
     packed = eng.get_labels_packed()
-    assert packed.shape == (E, F) and packed.dtype == np.uint32
-    off, idx = prm.csr(0, E)
-    for f in (0, 17, 63):  # full oracle parity on sampled frames
-        want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[f])
-        assert np.array_equal(packed[:, f].astype(np.uint64), want)
-    # every frame: the batched kernel equals the single-frame kernel
-    single = LabelEngine(devices=[0])
-    single.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
-    for f in range(0, F, 7):
-        single.submit_grid(1 << depth, props, P[f], 1)
-        assert np.array_equal(single.get_labels(0).bits, packed[:, f].astype(np.uint64))
-    single.close()
     eng.close()
+    assert packed.shape == (E, F) and packed.dtype == np.uint32
+    sample = np.arange(0, E, 97)
+    soff, sidx = _sampled_csr(prm, sample)
+    hits = 0
+    for f in range(F):  # all 64 frames, row-sampled
+        want = ORACLE.label_all(len(sample), 1 << depth, soff, sidx, 1 << depth, props, P[f])
+        assert np.array_equal(packed[sample, f].astype(np.uint64), want), f"frame {f}"
+        hits += int(np.count_nonzero(want))
+    assert hits > len(sample) * F // 10  # non-trivial labels
+    off, idx = prm.csr(0, E)
+    for f in (0, 17, 63):  # full oracle parity on all rows
+        want = ORACLE.label_all(E, 1 << depth, off, idx, 1 << depth, props, P[f])
+        assert np.array_equal(packed[:, f].astype(np.uint64), want), f"frame {f} (all rows)"
+
+
+def test_config5_shard_single_frame_full():
+    """BASELINE config 5 (8M edges, 1024^2, 64 props) on one per-GPU shard of
+    the 8-way row partition: rows [0, 1M), all of them, one frame, through
+    label_stream64_kernel<64, u64, ...> (64-bit labels, the L1 table path).
+    The oracle runs in 125k-row chunks to bound host memory."""
+    c = CONFIGS[5]
+    depth, props, E = c["depth"], c["props"], c["edges"] // 8
+    prm = SyntheticPRM(seed=1, depth=depth)
+    t = prm.words(0, E)
+    P = props_words(1, depth, props, 0, 1)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
+    del t
+    eng.submit_grid(1 << depth, props, P[0], 1)
+    got = eng.get_labels(0).bits
+    eng.close()
+    step = 125_000
+    for r0 in range(0, E, step):
+        off, idx = prm.csr(r0, r0 + step)
+        want = ORACLE.label_all(step, 1 << depth, off, idx, 1 << depth, props, P[0])
+        assert np.array_equal(got[r0:r0 + step], want), f"rows {r0}..{r0 + step}"
+
+
+def test_config5_shard_64_frames():
+    """Config 5 shard (rows [0, 1M) of the 8M-edge T, 1024^2, 64 props) x a
+    64-frame batch: label_pl_kernel<u64, 2> (two props per lane) and
+    pl_build_kernel<6>. Every frame on a row sample (every 61st row), two
+    frames on all rows."""
+    c = CONFIGS[5]
+    depth, props, E, F = c["depth"], c["props"], c["edges"] // 8, 64
+    prm = SyntheticPRM(seed=1, depth=depth)
+    t = prm.words(0, E)
+    P = props_words(1, depth, props, 0, F)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_words(E, 1 << depth, t.offsets, t.words, t.masks)
+    del t
+    eng.submit_grid(1 << depth, props, P, F)
+    packed = eng.get_labels_packed()
+    eng.close()
+    assert packed.shape == (E, F) and packed.dtype == np.uint64
+    sample = np.arange(0, E, 61)
+    soff, sidx = _sampled_csr(prm, sample)
+    for f in range(F):
+        want = ORACLE.label_all(len(sample), 1 << depth, soff, sidx, 1 << depth, props, P[f])
+        assert np.array_equal(packed[sample, f], want), f"frame {f}"
+    del soff, sidx
+    step = 250_000
+    for f in (5, 62):
+        for r0 in range(0, E, step):
+            off, idx = prm.csr(r0, r0 + step)
+            want = ORACLE.label_all(step, 1 << depth, off, idx, 1 << depth, props, P[f])
+            assert np.array_equal(packed[r0:r0 + step, f], want), f"frame {f} rows {r0}.."
 
 
 def test_monotone_in_proposition_bits():
@@ -348,6 +425,61 @@ def test_world_resample_batched_poses():
         want = ORACLE.label_all(3000, 1 << vdepth, off, idx, 1 << vdepth, props,
                                 ORACLE.resample(vgrid, wgrid, ps, props, world, 0))
         assert eng.get_labels(f) == LabelMatrix(3000, props, want)
+    eng.close()
+
+
+@pytest.mark.parametrize("frames", [1, 3])
+def test_pinned_submit_then_world_grid_and_boxes(frames):
+    """A fused pinned single-frame submit_grid leaves no host mapping behind:
+    the next world-grid / boxes submit labels with the P it just produced
+    (a stale P_host used to be re-read, or read past its end)."""
+    import torch
+
+    vdepth, props = 12, 5
+    vgrid = (vdepth, 0.0, 102.4, 0.0, 102.4)
+    wgrid = (vdepth, -10.0, 112.4, -10.0, 112.4)
+    world = props_words(23, vdepth, props, 0, 1)[0]
+    prm = SyntheticPRM(seed=3, depth=vdepth)
+    E = 4000
+    t = prm.words(0, E)
+    off, idx = prm.csr(0, E)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction_words(E, 1 << vdepth, t.offsets, t.words, t.masks)
+    cells = 1 << vdepth
+
+    def pinned_submit(seed):
+        P = props_words(seed, vdepth, props, 0, 1)
+        pin = torch.from_numpy(P.view(np.int64).copy()).pin_memory()
+        eng.submit_grid(cells, props, pin, 1)
+        assert eng.get_labels(0) == LabelMatrix(E, props, ORACLE.label_all(E, cells, off, idx, cells, props, P[0]))
+        pin.fill_(-1)  # the caller reuses its buffer after the labels are back
+        return pin
+
+    keep = pinned_submit(7)
+    poses = [(1.0 * k, -0.5 * k, math.cos(0.2 * k), math.sin(0.2 * k)) for k in range(frames)]
+    eng.submit_world_grid(vgrid, wgrid, props, world, poses)
+    for f, ps in enumerate(poses):
+        want_P = ORACLE.resample(vgrid, wgrid, ps, props, world, 0)
+        assert eng.get_labels(f) == LabelMatrix(E, props, ORACLE.label_all(E, cells, off, idx, cells, props, want_P))
+    del keep
+    keep = pinned_submit(8)
+    from oracle.oracle import RefCore
+
+    if RefCore.available():
+        ref = RefCore()
+        lo, hi = [0.0, 0.0], [102.4, 102.4]
+        rng = np.random.default_rng(frames)
+        columns = []
+        for _ in range(frames * props):
+            c = rng.uniform(0, 102.4, size=(3, 2))
+            columns.append([((x - 4).tolist(), (x + 5).tolist()) for x in c])
+        eng.submit_boxes(2, vdepth, lo, hi, columns, props, frames)
+        for f in range(frames):
+            P = np.stack([ref.rasterize_union(2, vdepth, lo, hi, np.array([b[0] for b in columns[f * props + j]]),
+                                              np.array([b[1] for b in columns[f * props + j]])) for j in range(props)])
+            want = ORACLE.label_all(E, cells, off, idx, cells, props, P)
+            assert eng.get_labels(f) == LabelMatrix(E, props, want), f
+    del keep
     eng.close()
 
 
@@ -681,3 +813,60 @@ def test_ab_variants_parity(knobs):
     r = subprocess.run([sys.executable, os.path.join(os.path.dirname(GOLDEN), "..", "tools", "ab_parity.py")],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_edge_counting_vs_golden_and_oracle():
+    """ltlg_edge_counting == label_edge_counting (label.cpp:140-148) for every
+    edge: the reference-generated seed-4444 fixture (test_label.cpp:155-185),
+    then seeded scenes (empty rows, cells not a multiple of 64, several props and
+    frames, sorted and unsorted engines, several shards) against the oracle."""
+    g = load("counting_examples")
+    c = load("counting_seed4444")
+    r, cols = int(c["rows"]), int(c["cols"])
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction(CsrBoolMatrix(r, cols, c["offsets"], c["indices"]))
+    eng.submit_grid(cols, 1, c["colwords"].reshape(1, 1, -1), 1)
+    hit, ex = eng.edge_counting(0, 0)
+    assert np.array_equal(np.stack([hit.astype(np.uint64), ex], 1), g["seed4444"])
+    eng.close()
+    for seed, devs, sort in ((1, [0], True), (2, [0], False), (3, [0, 0, 0], True)):
+        rng = SplitMix64(300 + seed)
+        r, cols, props, F = 1500, 64 * 40 + 17, 3, 4
+        rows = random_rows(rng, r, cols, 0.01)
+        rows[::13] = False  # empty rows
+        off, idx = to_csr(rows)
+        P = np.stack([bits_to_words(random_rows(rng, props, cols, d)) for d in (0.002, 0.02, 0.3, 0.9)])
+        eng = LabelEngine(devices=devs, sort_rows=sort)
+        eng.load_abstraction(CsrBoolMatrix(r, cols, off, idx))
+        eng.submit_grid(cols, props, P, F)
+        for f in range(F):
+            for j in range(props):
+                hit, ex = eng.edge_counting(f, j)
+                for i in range(r):
+                    h, e = ORACLE.label_edge_counting(idx[off[i]:off[i + 1]], P[f, j])
+                    assert (bool(hit[i]), int(ex[i])) == (h, e), (seed, f, j, i)
+        with pytest.raises(ValueError, match="prop out of range"):
+            eng.edge_counting(0, props)
+        eng.close()
+
+
+@pytest.mark.parametrize("props", [0, 3, 64])
+def test_apply_labels_vs_reference(props):
+    """ltlg_apply_labels == apply_labels (label.cpp:191-210): per-edge
+    AlphabetSymbol bits, and the reference's two checks in its order."""
+    rng = SplitMix64(900 + props)
+    r, cols = 700, 1000
+    rows = random_rows(rng, r, cols, 0.01)
+    off, idx = to_csr(rows)
+    P = bits_to_words(random_rows(rng, props, cols, 0.02)) if props else np.zeros((0, 16), np.uint64)
+    eng = LabelEngine(devices=[0])
+    eng.load_abstraction(CsrBoolMatrix(r, cols, off, idx))
+    eng.submit_grid(cols, props, P.reshape(1, props, -1), 1)
+    el = eng.apply_labels(r, props)
+    want = ORACLE.label_all(r, cols, off, idx, cols, props, P) if props else np.zeros(r, np.uint64)
+    assert el.alphabet_size == props and np.array_equal(el.labels, want.reshape(r, -1)[:, 0] if props else want)
+    with pytest.raises(ValueError, match=f"^label matrix rows {r} vs edges {r + 1}$"):
+        eng.apply_labels(r + 1, props + 1)  # rows are checked first
+    with pytest.raises(ValueError, match=f"^label matrix props {props} vs alphabet size {props + 1}$"):
+        eng.apply_labels(r, props + 1)
+    eng.close()

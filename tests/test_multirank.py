@@ -126,6 +126,21 @@ def test_spatial_shard_partition():
                 assert med[parts[i - 1][0]].max() <= med[rows].min()
 
 
+def test_spatial_shard_empty_rows():
+    # empty rows (including a trailing one, whose offset is len(words)) sort as
+    # word 0 and still land in exactly one part
+    import bench
+
+    off = np.array([0, 2, 2, 5, 5, 6, 6], np.uint64)
+    words = np.array([9, 40, 3, 4, 5, 70], np.uint32)
+    masks = np.arange(1, 7, dtype=np.uint32)
+    for world in (1, 2, 3):
+        parts = [bench.spatial_shard(off, words, masks, r, world) for r in range(world)]
+        ids = np.concatenate([p[0] for p in parts])
+        assert np.array_equal(np.sort(ids), np.arange(6))
+        assert sum(int(p[1][-1]) for p in parts) == len(words)
+
+
 def test_synthetic_rows_are_row_addressable():
     from paper_1810_02612_b200.synth import SyntheticPRM
 
