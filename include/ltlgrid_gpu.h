@@ -62,7 +62,9 @@ typedef struct ltlg_options {
                              submits of host-memory P label them with separate launches, so
                              ltlg_get_labels_packed copies block c to the host while later blocks
                              are still being labelled (0/1 = off) */
-    int reserved[6];
+    int task_rows;        /* rows per warp task of the word-major multi-frame kernel (0 = default 32,
+                             at most 256); its shared memory per warp grows with it */
+    int reserved[5];
 } ltlg_options;
 
 /* Shape / layout facts about the loaded abstraction and the last submit. */

@@ -34,7 +34,7 @@ EXPORTS = [
 
 class Options(C.Structure):
     _fields_ = [("sort_rows", C.c_int), ("stream_task_pairs", C.c_int), ("batch_task_pairs", C.c_int),
-                ("profile", C.c_int), ("readback_chunks", C.c_int), ("reserved", C.c_int * 6)]
+                ("profile", C.c_int), ("readback_chunks", C.c_int), ("task_rows", C.c_int), ("reserved", C.c_int * 5)]
 
 
 class GridK(C.Structure):

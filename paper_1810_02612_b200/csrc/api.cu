@@ -121,6 +121,12 @@ struct Shard {
     DevBuf<uint64_t> mask_b64, tpair_b64, pb64;  // multi-frame 64-cell-word copy, its Pb table
     DevBuf<uint32_t> word_b64;
     DevBuf<uint32_t> touched64;  // PackedShard::touched64
+    // word-major multi-frame copy (PackedShard::wm_*)
+    DevBuf<uint64_t> wm_mask;
+    DevBuf<uint8_t> wm_row;
+    DevBuf<uint32_t> wm_gword, wm_gstart, wm_task_row, wm_task_grp;
+    std::vector<uint32_t> block_task_wm;
+    int wm_rows = 0;
     DevBuf<uint64_t> tbyte64;
     DevBuf<uint32_t> tn64;
     DevBuf<uint32_t> perm, trow_s, trow_b;
@@ -208,6 +214,10 @@ ltlg_status upload_shard(ltlg_ctx* ctx, Shard& s, const PackedShard& p) {
     s.block_row = p.block_row;
     s.block_task_s = p.block_task_stream;
     s.block_task_b = p.block_task_batch;
+    s.block_task_wm = p.block_task_wm;
+    s.wm_rows = 0;
+    for (size_t k = 0; k + 1 < p.wm_task_row.size(); ++k)
+        s.wm_rows = std::max(s.wm_rows, static_cast<int>(p.wm_task_row[k + 1] - p.wm_task_row[k]));
     const size_t nb = p.block_row.size() - 1;
     while (s.block_done.size() < nb) {
         cudaEvent_t ev;
@@ -236,13 +246,20 @@ ltlg_status upload_shard(ltlg_ctx* ctx, Shard& s, const PackedShard& p) {
     if ((st = put(s.word_b64, p.word_b64, "upload T pairs")) != LTLG_OK) return st;
     if ((st = put(s.tpair_b64, p.task_pair_b64, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.touched64, p.touched64, "upload word map")) != LTLG_OK) return st;
+    if ((st = put(s.wm_mask, p.wm_mask, "upload T pairs")) != LTLG_OK) return st;
+    if ((st = put(s.wm_row, p.wm_row, "upload T pairs")) != LTLG_OK) return st;
+    if ((st = put(s.wm_gword, p.wm_gword, "upload T groups")) != LTLG_OK) return st;
+    if ((st = put(s.wm_gstart, p.wm_gstart, "upload T groups")) != LTLG_OK) return st;
+    if ((st = put(s.wm_task_row, p.wm_task_row, "upload tasks")) != LTLG_OK) return st;
+    if ((st = put(s.wm_task_grp, p.wm_task_grp, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.perm, p.perm, "upload row permutation")) != LTLG_OK) return st;
     if ((st = put(s.trow_s, p.task_row_stream, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.tpair_s, p.task_pair_stream, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.trow_b, p.task_row_batch, "upload tasks")) != LTLG_OK) return st;
     if ((st = put(s.tpair_b, p.task_pair_batch, "upload tasks")) != LTLG_OK) return st;
     ctx->t_bytes += (p.pairs.size() + p.pairs_stream.size()) * sizeof(Pair) + p.stream64.size() + p.perm.size() * 4 +
-                    p.mask_b64.size() * 8 + p.word_b64.size() * 4;
+                    p.mask_b64.size() * 8 + p.word_b64.size() * 4 + p.wm_mask.size() * 9 +
+                    (p.wm_gword.size() + p.wm_gstart.size()) * 4;
     return LTLG_OK;
 }
 
@@ -275,7 +292,7 @@ ltlg_status load_words(ltlg_ctx* ctx, WordCsr& t) {
         build_shard(t, b[i], b[i + 1], ctx->opts.sort_rows != 0, sentinel, stream_pairs,
                     ctx->opts.batch_task_pairs > 0 ? ctx->opts.batch_task_pairs : 256,
                     ctx->opts.readback_chunks > 1 ? (ctx->opts.readback_chunks < 64 ? ctx->opts.readback_chunks : 64) : 1,
-                    &p);
+                    &p, ctx->opts.task_rows > 0 ? std::min(ctx->opts.task_rows, 256) : kWmRows);
         ltlg_status st = upload_shard(ctx, ctx->shards[static_cast<size_t>(i)], p);
         if (st != LTLG_OK) return st;
         pairs += p.n_pairs;
@@ -495,6 +512,10 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         const uint64_t pl_worst = static_cast<uint64_t>(nw64 + 1) * (props > 32 ? 64u : 32u) *
                                   static_cast<uint64_t>(std::min(frames, 64));
         const bool pl = wide_b_ok && pl_ok && frames > 1 && props <= 64 && pl_worst < (uint64_t(1) << 31);
+        // word-major kernel (label_wm_kernel) over the prop-lane summary; dev knob
+        // LTLG_WORDMAJOR=0: the pair-major label_pl_kernel, for A/B runs
+        static const bool wm_ok = !getenv("LTLG_WORDMAJOR") || atoi(getenv("LTLG_WORDMAJOR")) != 0;
+        const bool wm = wm_ok && s.wm_rows > 0;
         const int nslice = pl ? (frames + 63) / 64 : 1;
         CK(s.sf.reserve(pl ? pl_work_bytes(props, std::min(frames, 64), nw64)
                         : wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32
@@ -554,6 +575,16 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
             a.task_pair_b64 = s.tpair_b64.ptr;
             a.nw64 = nw64;
         }
+        if (pl && wm) {
+            a.word_major = 1;
+            a.wm_mask = s.wm_mask.ptr;
+            a.wm_row = s.wm_row.ptr;
+            a.wm_gword = s.wm_gword.ptr;
+            a.wm_gstart = s.wm_gstart.ptr;
+            a.wm_task_row = s.wm_task_row.ptr;
+            a.wm_task_grp = s.wm_task_grp.ptr;
+            a.wm_rows = s.wm_rows;
+        }
         if (wide) {
             a.t64 = s.t64.ptr;
             a.task_byte64 = s.tbyte64.ptr;
@@ -565,7 +596,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // one launch per read-back block for multi-frame submits (their labels are
         // large: rows x frames words); a single frame's labels are small, so it
         // runs as one launch over all tasks (tasks are listed block by block)
-        const std::vector<uint32_t>& bt = single ? s.block_task_s : s.block_task_b;
+        const std::vector<uint32_t>& bt = single ? s.block_task_s : (pl && wm) ? s.block_task_wm : s.block_task_b;
         const int nb = single || !split ? 1 : static_cast<int>(bt.size() - 1);
         for (int c = 0; c < nb; ++c) {
             a.task_begin = bt[static_cast<size_t>(c)];

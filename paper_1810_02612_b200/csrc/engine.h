@@ -52,6 +52,20 @@ struct PackedShard {
     // bit w: some pair of the multi-frame copy is on 64-cell word w (the
     // sentinel word included); the prop-lane summary skips the other words
     std::vector<uint32_t> touched64;
+    // word-major multi-frame copy (the prop-lane path's default kernel,
+    // label_wm_kernel): tasks of <= wm_rows consecutive rows of the batch row
+    // order (never crossing a read-back block); a task's 64-cell pairs are
+    // grouped by word, so the word's per-frame summary and partial records
+    // are read once per task and tested against every pair on it.
+    //   task t: rows [wm_task_row[t], wm_task_row[t+1]) (batch positions),
+    //           groups [wm_task_grp[t], wm_task_grp[t+1])
+    //   group g: word wm_gword[g], entries [wm_gstart[g], wm_gstart[g+1])
+    //   entry e: mask wm_mask[e] (64 cells), row wm_row[e] - task's first row
+    std::vector<uint64_t> wm_mask;
+    std::vector<uint8_t> wm_row;
+    std::vector<uint32_t> wm_gword, wm_gstart;         // ngroups (+1 for gstart)
+    std::vector<uint32_t> wm_task_row, wm_task_grp;    // ntasks + 1
+    std::vector<uint32_t> block_task_wm;               // per read-back block (+1)
     uint64_t n_pairs = 0;                 // meaningful pairs (incl. sentinels)
     std::vector<uint32_t> perm;           // sorted position -> local original row
     // warp tasks: [row_begin, row_end) in sorted positions, pairs [pair_begin, pair_end)
@@ -65,6 +79,7 @@ struct PackedShard {
 };
 
 constexpr uint64_t kPairPad = 512;  // tail padding so vector loads never leave the array
+constexpr int kWmRows = 32;  // rows per word-major task (label_wm_kernel: shared memory per warp ~ rows)
 
 // Single-frame layout.  The stream kernel gives each lane kStreamK consecutive
 // pairs of a warp chunk of 32*kStreamK pairs and reads them as 16-byte pieces.
@@ -108,7 +123,7 @@ bool write_csb1(const char* path, uint64_t rows, uint64_t cols, const uint64_t* 
 std::vector<uint64_t> shard_bounds(const WordCsr& t, int n);
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
                  uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs, int blocks,
-                 PackedShard* out);
+                 PackedShard* out, int wm_rows = kWmRows);
 int host_threads();
 
 }  // namespace ltlg

@@ -1835,89 +1835,7 @@ cudaError_t launch_summary_b64(const uint64_t* P64, int props, int frames, uint3
 // the prop-major ffr masks into frame-major ones (lane f holds frame f and
 // f + 32) and ORs in acc[f].
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) pl_summary_kernel(const uint64_t* __restrict__ P64, int props, int frames,
-                                                         uint32_t nw64, uint64_t cells, uint64_t* __restrict__ ffr,
-                                                         uint64_t* __restrict__ sfr, uint32_t* __restrict__ cnt,
-                                                         uint32_t* __restrict__ wcnt, uint32_t* __restrict__ task_ctr,
-                                                         int nctr, int pshift, const uint32_t* __restrict__ touched64) {
-    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    if (t < static_cast<uint64_t>(nctr)) task_ctr[t] = 0;
-    // consecutive threads take consecutive words of one prop: coalesced rows of P
-    const uint64_t nwp = nw64 + 1;
-    const uint32_t j = static_cast<uint32_t>(t / nwp), w = static_cast<uint32_t>(t - static_cast<uint64_t>(j) * nwp);
-    if (j >= (1u << pshift)) return;
-    const uint64_t o = (static_cast<uint64_t>(w) << pshift) | j;  // ffr / sfr / cnt index
-    // a word no pair of this shard is on is never looked up: skip its P reads
-    // (a spatial row shard touches a fraction of the grid); the fill kernel
-    // sees no records for it
-    if (touched64 && !(__ldg(touched64 + (w >> 5)) >> (w & 31) & 1u)) {
-        cnt[o] = 0;
-        return;
-    }
-    uint64_t full = 0, any = 0;
-    uint32_t n = 0;
-    const uint64_t lo = static_cast<uint64_t>(w) * 64;
-    if (w < nw64 && lo < cells && j < static_cast<uint32_t>(props)) {
-        const uint64_t valid = (cells - lo >= 64) ? ~0ull : ((1ull << (cells - lo)) - 1ull);
-        const uint64_t* base = P64 + static_cast<uint64_t>(j) * nw64 + w;
-        for (int f = 0; f < frames; ++f) {
-            const uint64_t x = base[static_cast<uint64_t>(f) * props * nw64] & valid;
-            any |= static_cast<uint64_t>(x != 0) << f;
-            full |= static_cast<uint64_t>(x == valid) << f;
-            n += (x != 0 && x != valid);
-        }
-    }
-    ffr[o] = full;
-    sfr[o] = any;
-    cnt[o] = n;
-    if (n) atomicAdd(wcnt + w, n);
-}
-
-// rec_off = exclusive scan of wcnt (one CTA); cursor = rec_off
-__global__ void __launch_bounds__(1024) pl_scan_kernel(const uint32_t* __restrict__ wcnt, uint32_t n,
-                                                       uint2* __restrict__ rec_se, uint32_t* __restrict__ cursor) {
-    __shared__ uint32_t part[1024];
-    const uint32_t per = (n + 1023) / 1024, b = threadIdx.x * per, e = b + per < n ? b + per : n;
-    uint32_t sum = 0;
-    for (uint32_t i = b; i < e; ++i) sum += wcnt[i];
-    part[threadIdx.x] = sum;
-    __syncthreads();
-    for (uint32_t d = 1; d < 1024; d <<= 1) {
-        const uint32_t v = threadIdx.x >= d ? part[threadIdx.x - d] : 0;
-        __syncthreads();
-        part[threadIdx.x] += v;
-        __syncthreads();
-    }
-    uint32_t acc = part[threadIdx.x] - sum;
-    for (uint32_t i = b; i < e; ++i) {
-        rec_se[i] = make_uint2(acc, acc + wcnt[i]);
-        cursor[i] = acc;
-        acc += wcnt[i];
-    }
-}
-
-__global__ void __launch_bounds__(256) pl_fill_kernel(const uint64_t* __restrict__ P64, int props, int frames,
-                                                      uint32_t nw64, uint64_t cells, const uint32_t* __restrict__ cnt,
-                                                      uint32_t* __restrict__ cursor, uint4* __restrict__ rec, int pshift) {
-    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-    const uint64_t nwp = nw64 + 1;
-    const uint32_t j = static_cast<uint32_t>(t / nwp), w = static_cast<uint32_t>(t - static_cast<uint64_t>(j) * nwp);
-    if (j >= (1u << pshift) || w >= nw64) return;
-    const uint32_t n = cnt[(static_cast<uint64_t>(w) << pshift) | j];
-    if (!n) return;
-    uint32_t pos = atomicAdd(cursor + w, n);  // record order within a word is irrelevant (OR)
-    const uint64_t lo = static_cast<uint64_t>(w) * 64;
-    const uint64_t valid = (cells - lo >= 64) ? ~0ull : ((1ull << (cells - lo)) - 1ull);
-    const uint64_t* base = P64 + static_cast<uint64_t>(j) * nw64 + w;
-    for (int f = 0; f < frames; ++f) {
-        const uint64_t x = base[static_cast<uint64_t>(f) * props * nw64] & valid;
-        if (x != 0 && x != valid)  // smem label accumulator word f + 64 (j / 32), bit j % 32
-            rec[pos++] = make_uint4(static_cast<uint32_t>(x), static_cast<uint32_t>(x >> 32),
-                                    4u * (static_cast<uint32_t>(f) + 64u * (j >> 5)), 1u << (j & 31));
-    }
-}
-
-// The three passes above in one kernel.  A CTA owns WPB consecutive words x
+// The prop-lane summary in one kernel.  A CTA owns WPB consecutive words x
 // all 1 << pshift prop slots (thread j * WPB + wl: consecutive threads read
 // consecutive words of one prop, coalesced).  Per word, the partial-record
 // counts of its props are prefix-summed in shared memory and the word's
@@ -1930,10 +1848,17 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
                                                         uint64_t* __restrict__ sfr, uint2* __restrict__ rec_se,
                                                         uint32_t* __restrict__ rec_cursor, uint4* __restrict__ rec,
                                                         uint32_t* __restrict__ task_ctr, int nctr,
-                                                        const uint32_t* __restrict__ touched64) {
+                                                        const uint32_t* __restrict__ touched64,
+                                                        uint32_t* __restrict__ ffrT, uint32_t* __restrict__ sfrT) {
     constexpr int NP = 1 << PSHIFT, WPB = NT / NP;
+    constexpr int TW = 64 * (NP / 32);  // frame-major u32 words per grid word: [prop half][frame]
     __shared__ uint32_t s_cnt[NP][WPB];
     __shared__ uint32_t s_base[WPB];
+    __shared__ uint32_t s_fT[WPB][TW], s_sT[WPB][TW];
+    for (int k = threadIdx.x; k < WPB * TW; k += NT) {
+        (&s_fT[0][0])[k] = 0;
+        (&s_sT[0][0])[k] = 0;
+    }
     const uint32_t gt = blockIdx.x * static_cast<uint32_t>(NT) + threadIdx.x;
     if (gt < static_cast<uint32_t>(nctr)) task_ctr[gt] = 0;
     const uint32_t j = threadIdx.x / WPB, wl = threadIdx.x % WPB;
@@ -1961,7 +1886,13 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
         sfr[o] = any;
     }
     s_cnt[j][wl] = n;
-    __syncthreads();
+    __syncthreads();  // (also orders the s_fT / s_sT zeroing before the ORs)
+    // frame-major copies for the word-major kernel: word f + 64 (j / 32) of
+    // grid word w holds bit j % 32 for every prop j full / non-zero in frame f
+    for (uint64_t x = full; x; x &= x - 1)
+        atomicOr(&s_fT[wl][__ffsll(static_cast<long long>(x)) - 1 + 64 * (j >> 5)], 1u << (j & 31));
+    for (uint64_t x = any; x; x &= x - 1)
+        atomicOr(&s_sT[wl][__ffsll(static_cast<long long>(x)) - 1 + 64 * (j >> 5)], 1u << (j & 31));
     if (j == 0 && in) {  // per word: exclusive prefix over props, then its segment
         uint32_t run = 0;
         for (int k = 0; k < NP; ++k) {
@@ -1974,6 +1905,13 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
         rec_se[w] = make_uint2(b, b + run);
     }
     __syncthreads();
+    for (int k = threadIdx.x; k < WPB * TW; k += NT) {  // coalesced rows of TW words per grid word
+        const uint32_t ww = blockIdx.x * WPB + static_cast<uint32_t>(k / TW);
+        if (ww <= nw64) {
+            ffrT[static_cast<uint64_t>(ww) * TW + k % TW] = (&s_fT[0][0])[k];
+            sfrT[static_cast<uint64_t>(ww) * TW + k % TW] = (&s_sT[0][0])[k];
+        }
+    }
     if (!n) return;
     uint32_t pos = s_base[wl] + s_cnt[j][wl];
     for (int f = 0; f < frames; ++f) {
@@ -2094,21 +2032,132 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Word-major multi-frame labelling (<= 64 frames per launch, <= 64 props).
+//
+// A warp task is a run of <= R consecutive rows of the batch order (z-sorted,
+// so they sweep a compact region of the grid), with the rows' 64-cell pairs
+// grouped by word (PackedShard::wm_*).  Per word group the warp reads the
+// word's frame-major summary once -- lane f holds ffrT / sfrT of frames f and
+// f + 32 (bit j = prop j full / non-zero) -- and the word's partial records
+// once, into registers (lane k holds records k, k + 32, ...), then streams the
+// group's pairs (broadcast one at a time by shuffle) past them:
+//   * every pair ORs its word's full props (any non-zero prop when the pair
+//     sweeps all 64 cells) into acc[row][f], lane f  (red.shared.or, distinct
+//     consecutive words);
+//   * a partial pair tests every record  m & P_record != 0  and ORs hits into
+//     acc[row][f_record] bit j_record.
+// acc is the warp's shared-memory label block, frame-major per row, so the
+// row-end stores are coalesced 4-byte words (lane f = frame f) and need no
+// bit transpose.  The pair-major label_pl_kernel re-read each pair's word
+// summary (256 B) and records (~600 B) from L1 for every pair; here a word's
+// ~850 B are read once per task and amortised over its pairs.
+// ---------------------------------------------------------------------------
+constexpr int kWmThreads = 128;
+constexpr int kWmRecSets = 4;  // records (x 32) held in registers per word; more are re-read per pair
+
+template <typename SW, int PW>
+__global__ void __launch_bounds__(kWmThreads)
+    label_wm_kernel(const uint64_t* __restrict__ emask, const uint8_t* __restrict__ erow,
+                    const uint32_t* __restrict__ gword, const uint32_t* __restrict__ gstart,
+                    const uint32_t* __restrict__ task_row, const uint32_t* __restrict__ task_grp,
+                    uint32_t task_begin, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
+                    const uint32_t* __restrict__ ffrT, const uint32_t* __restrict__ sfrT,
+                    const uint2* __restrict__ rec_se, const uint4* __restrict__ rec, int frames,
+                    const uint32_t* __restrict__ perm, SW* __restrict__ out, uint32_t ostride, int rows_per_task) {
+    extern __shared__ uint32_t wm_acc[];
+    constexpr int RW = 64 * PW;  // accumulator words per row: [prop half][frame]
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint32_t* acc = wm_acc + static_cast<size_t>(wib) * static_cast<size_t>(rows_per_task) * RW;
+    const uint32_t acc_s = smem_u32(acc);
+    for (int k = lane; k < rows_per_task * RW; k += 32) acc[k] = 0;
+    __syncwarp();
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntasks) break;
+        const uint32_t r0 = task_row[t], nr = task_row[t + 1] - r0;
+        const uint32_t g1 = task_grp[t + 1];
+        for (uint32_t g = task_grp[t]; g < g1; ++g) {
+            const uint32_t w = gword[g];
+            const uint32_t e0 = gstart[g], e1 = gstart[g + 1];
+            uint32_t fv[2 * PW], sv[2 * PW];
+#pragma unroll
+            for (int k = 0; k < 2 * PW; ++k) {
+                fv[k] = __ldg(ffrT + static_cast<uint64_t>(w) * RW + lane + 32 * k);
+                sv[k] = __ldg(sfrT + static_cast<uint64_t>(w) * RW + lane + 32 * k);
+            }
+            const uint2 se = __ldg(rec_se + w);
+            const uint32_t nrec = se.y - se.x;
+            uint4 rc[kWmRecSets];
+#pragma unroll
+            for (int k = 0; k < kWmRecSets; ++k)
+                rc[k] = (32u * k + lane < nrec) ? __ldg(rec + se.x + 32u * k + lane) : make_uint4(0u, 0u, 0u, 0u);
+            for (uint32_t c = e0; c < e1; c += 32) {
+                const uint2 cm = __ldg(reinterpret_cast<const uint2*>(emask + c + lane));
+                const uint32_t cr = __ldg(erow + c + lane);
+                const int n = static_cast<int>(e1 - c < 32u ? e1 - c : 32u);
+                for (int i = 0; i < n; ++i) {
+                    const uint32_t mlo = __shfl_sync(0xffffffffu, cm.x, i), mhi = __shfl_sync(0xffffffffu, cm.y, i);
+                    const uint32_t base = acc_s + __shfl_sync(0xffffffffu, cr, i) * (RW * 4u);
+                    const bool full = (mlo & mhi) == 0xffffffffu;  // warp-uniform
+#pragma unroll
+                    for (int k = 0; k < 2 * PW; ++k) {
+                        const uint32_t v = full ? sv[k] : fv[k];
+                        if (v) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + 4u * (lane + 32 * k)), "r"(v) : "memory");
+                    }
+                    if (full) continue;
+#pragma unroll
+                    for (int k = 0; k < kWmRecSets; ++k) {
+                        if (32u * k >= nrec) break;  // warp-uniform
+                        if ((mlo & rc[k].x) | (mhi & rc[k].y))
+                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + rc[k].z), "r"(rc[k].w) : "memory");
+                    }
+                    // words with more partial records than the register sets hold
+                    for (uint32_t q = se.x + 32u * kWmRecSets; q < se.y; q += 32) {
+                        const uint4 r = __ldg(rec + q + lane);  // (the record array is padded by 32)
+                        if ((q + lane < se.y) && ((mlo & r.x) | (mhi & r.y)))
+                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + r.z), "r"(r.w) : "memory");
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        // the task's rows: lane f stores frames f and f + 32, then clears them
+        for (uint32_t r = 0; r < nr; ++r) {
+            SW* o = out + static_cast<uint64_t>(perm[r0 + r]) * ostride;
+            uint32_t* a = acc + r * RW;
+            uint64_t lo = a[lane], hi = a[lane + 32];
+            if constexpr (PW == 2) {
+                lo |= static_cast<uint64_t>(a[lane + 64]) << 32;
+                hi |= static_cast<uint64_t>(a[lane + 96]) << 32;
+            }
+            if (lane < frames) o[lane] = static_cast<SW>(lo);
+            if (lane + 32 < frames) o[lane + 32] = static_cast<SW>(hi);
+#pragma unroll
+            for (int k = 0; k < 2 * PW; ++k) a[lane + 32 * k] = 0;
+        }
+        __syncwarp();
+    }
+}
+
 // Byte layout of the prop-lane work buffer: summary masks (pw prop slots per
-// word), counts, record ranges, then the records (worst case: every (word,
-// prop, frame) partial) + 32 records of padding for the last probe round.
+// word; prop-major for label_pl_kernel, frame-major for label_wm_kernel), the
+// record cursor and ranges, then the records (worst case: every (word, prop,
+// frame) partial) + 32 records of padding for the last probe round.
 struct PlLayout {
     uint64_t nt;  // (nw64 + 1) * pw
-    size_t ffr, sfr, cnt, wcnt, cursor, rec_se, rec, total;
+    size_t ffr, sfr, ffrT, sfrT, cursor, rec_se, rec, total;
     PlLayout(int props, int frames, uint32_t nw64) {
         nt = static_cast<uint64_t>(nw64 + 1) * (props > 32 ? 64u : 32u);
         auto up = [](size_t x, size_t a) { return (x + a - 1) & ~(a - 1); };
         ffr = 0;
         sfr = ffr + nt * 8;
-        cnt = sfr + nt * 8;
-        wcnt = cnt + nt * 4;
-        cursor = wcnt + (nw64 + 2) * 4;
-        rec_se = up(cursor + (nw64 + 2) * 4, 8);
+        ffrT = sfr + nt * 8;  // frame-major: (nw64 + 1) x 64 x pw/32 u32 = nt * 8 bytes
+        sfrT = ffrT + nt * 8;
+        cursor = sfrT + nt * 8;
+        rec_se = up(cursor + 4, 8);
         rec = up(rec_se + (nw64 + 2) * 8, 16);
         total = rec + (nt * static_cast<uint64_t>(frames) + 32) * 16;
     }
@@ -2123,39 +2172,26 @@ cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64,
     uint8_t* wb = static_cast<uint8_t*>(work);
     uint64_t* ffr = reinterpret_cast<uint64_t*>(wb + L.ffr);
     uint64_t* sfr = reinterpret_cast<uint64_t*>(wb + L.sfr);
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(wb + L.cnt);
-    uint32_t* wcnt = reinterpret_cast<uint32_t*>(wb + L.wcnt);
+    uint32_t* ffrT = reinterpret_cast<uint32_t*>(wb + L.ffrT);
+    uint32_t* sfrT = reinterpret_cast<uint32_t*>(wb + L.sfrT);
     uint32_t* cursor = reinterpret_cast<uint32_t*>(wb + L.cursor);
     uint2* rec_se = reinterpret_cast<uint2*>(wb + L.rec_se);
-    static const bool fused = !getenv("LTLG_PL_FUSED") || atoi(getenv("LTLG_PL_FUSED")) != 0;  // A/B knob
-    if (fused) {
-        cudaError_t e = cudaMemsetAsync(cursor, 0, 4, st);
-        if (e != cudaSuccess) return e;
-        // 32 (16) words x 32 (64) prop slots per CTA.  256-thread CTAs fill the
-        // GPU better (summary 40 -> 43 us anyway) but scatter the word segments
-        // more, and the labelling kernel lost 60 us to record locality.
-        constexpr int kNT = 1024;
-        const int wpb = kNT >> pshift;
-        const uint64_t gw = (static_cast<uint64_t>(nw64) + 1 + wpb - 1) / wpb, gc = (static_cast<uint64_t>(nctr) + kNT - 1) / kNT;
-        const unsigned grid = static_cast<unsigned>(gw > gc ? gw : gc);
-        uint4* rec = reinterpret_cast<uint4*>(wb + L.rec);
-        if (pshift == 5)
-            pl_build_kernel<5, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
-                                                      task_ctr, nctr, touched64);
-        else
-            pl_build_kernel<6, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
-                                                      task_ctr, nctr, touched64);
-        return cudaGetLastError();
-    }
-    cudaError_t e = cudaMemsetAsync(wcnt, 0, (nw64 + 2) * 4, st);
+    uint4* rec = reinterpret_cast<uint4*>(wb + L.rec);
+    cudaError_t e = cudaMemsetAsync(cursor, 0, 4, st);
     if (e != cudaSuccess) return e;
-    const uint64_t nt = L.nt;
-    const uint64_t nthreads = nt > static_cast<uint64_t>(nctr) ? nt : static_cast<uint64_t>(nctr);
-    pl_summary_kernel<<<static_cast<unsigned>((nthreads + 255) / 256), 256, 0, st>>>(
-        P64, props, frames, nw64, cells, ffr, sfr, cnt, wcnt, task_ctr, nctr, pshift, touched64);
-    pl_scan_kernel<<<1, 1024, 0, st>>>(wcnt, nw64 + 1, rec_se, cursor);
-    pl_fill_kernel<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(
-        P64, props, frames, nw64, cells, cnt, cursor, reinterpret_cast<uint4*>(wb + L.rec), pshift);
+    // 32 (16) words x 32 (64) prop slots per CTA.  256-thread CTAs fill the
+    // GPU better (summary 40 -> 43 us anyway) but scatter the word segments
+    // more, and the prop-lane labelling kernel lost 60 us to record locality.
+    constexpr int kNT = 1024;
+    const int wpb = kNT >> pshift;
+    const uint64_t gw = (static_cast<uint64_t>(nw64) + 1 + wpb - 1) / wpb, gc = (static_cast<uint64_t>(nctr) + kNT - 1) / kNT;
+    const unsigned grid = static_cast<unsigned>(gw > gc ? gw : gc);
+    if (pshift == 5)
+        pl_build_kernel<5, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
+                                                  task_ctr, nctr, touched64, ffrT, sfrT);
+    else
+        pl_build_kernel<6, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
+                                                  task_ctr, nctr, touched64, ffrT, sfrT);
     return cudaGetLastError();
 }
 
@@ -2177,6 +2213,31 @@ static void launch_pl_label(const LaunchArgs& a, cudaStream_t st) {
                                               reinterpret_cast<const uint2*>(wb + L.rec_se),
                                               reinterpret_cast<const uint4*>(wb + L.rec), a.frames, a.perm,
                                               static_cast<SW*>(a.out), a.ostride ? a.ostride : static_cast<uint32_t>(a.frames));
+}
+
+template <typename SW, int PW>
+static void launch_wm_label(const LaunchArgs& a, cudaStream_t st) {
+    const PlLayout L(a.props, a.frames, a.nw64);
+    const uint8_t* wb = static_cast<const uint8_t*>(a.sf);
+    auto kern = label_wm_kernel<SW, PW>;
+    const size_t smem = static_cast<size_t>(kWmThreads / 32) * static_cast<size_t>(a.wm_rows) * 64 * PW * 4;
+    static size_t smem_set = 0;
+    static int per_sm = 0;
+    static size_t per_sm_smem = ~size_t(0);
+    if (smem > smem_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        smem_set = smem;
+    }
+    if (per_sm_smem != smem) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWmThreads, smem);
+        if (per_sm <= 0) per_sm = 1;
+        per_sm_smem = smem;
+    }
+    kern<<<sm_count() * per_sm, kWmThreads, smem, st>>>(
+        a.wm_mask, a.wm_row, a.wm_gword, a.wm_gstart, a.wm_task_row, a.wm_task_grp, a.task_begin, a.ntasks,
+        a.task_ctr, reinterpret_cast<const uint32_t*>(wb + L.ffrT), reinterpret_cast<const uint32_t*>(wb + L.sfrT),
+        reinterpret_cast<const uint2*>(wb + L.rec_se), reinterpret_cast<const uint4*>(wb + L.rec), a.frames, a.perm,
+        static_cast<SW*>(a.out), a.ostride ? a.ostride : static_cast<uint32_t>(a.frames), a.wm_rows);
 }
 
 template <int FMT, typename SW, int FPL, bool FULL>
@@ -2205,7 +2266,14 @@ static void launch_batch_fpl(const LaunchArgs& a, cudaStream_t st) {
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
     if (a.ntasks <= a.task_begin) return cudaSuccess;
     cudaError_t e = cudaSuccess;
-    if (a.mask_b64 && a.prop_lane) {  // prop-lane multi-frame path (<= 64 props, a slice of <= 64 frames)
+    if (a.prop_lane && a.word_major) {  // word-major multi-frame path (<= 64 props, a slice of <= 64 frames)
+        switch (a.label_bytes) {
+            case 1: launch_wm_label<uint8_t, 1>(a, st); break;
+            case 2: launch_wm_label<uint16_t, 1>(a, st); break;
+            case 4: launch_wm_label<uint32_t, 1>(a, st); break;
+            default: launch_wm_label<uint64_t, 2>(a, st); break;
+        }
+    } else if (a.mask_b64 && a.prop_lane) {  // pair-major prop-lane kernel (A/B: LTLG_WORDMAJOR=0)
         switch (a.label_bytes) {
             case 1: launch_pl_label<uint8_t, 1>(a, st); break;
             case 2: launch_pl_label<uint16_t, 1>(a, st); break;

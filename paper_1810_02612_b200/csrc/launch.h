@@ -41,6 +41,15 @@ struct LaunchArgs {
     const uint64_t* pb64;  // Pb table of summary_b64_kernel
     int prop_lane;         // multi-frame: the prop-lane kernel (sf = its launch_pl work buffer)
     int pdl;               // single frame: launch as a programmatic dependent of the summary kernel
+    // word-major multi-frame copy (PackedShard::wm_*): label_wm_kernel
+    int word_major;
+    const uint64_t* wm_mask;
+    const uint8_t* wm_row;
+    const uint32_t* wm_gword;
+    const uint32_t* wm_gstart;
+    const uint32_t* wm_task_row;
+    const uint32_t* wm_task_grp;
+    int wm_rows;
 };
 
 cudaError_t launch_summary(const uint32_t* P32, int props, int frames, uint32_t nw32, uint64_t cells,

@@ -685,9 +685,91 @@ void build_batch64_layout(const WordCsr& t, uint64_t row_begin, uint32_t sentine
     for (size_t k = 0; k <= nt; ++k) out->task_pair_b64[k] = off[out->task_row_batch[k]];
 }
 
+// The word-major copy (engine.h): per task of <= wm_rows batch rows, its
+// 64-cell pairs sorted by (word, row).
+void build_wm_layout(const WordCsr& t, uint64_t row_begin, int wm_rows, PackedShard* out) {
+    const uint64_t R = out->perm.size();
+    const uint64_t rows_per = static_cast<uint64_t>(std::max(1, std::min(wm_rows, 256)));
+    out->wm_task_row.clear();
+    out->block_task_wm.clear();
+    const size_t nb = out->block_row.size() - 1;
+    for (size_t c = 0; c < nb; ++c) {
+        out->block_task_wm.push_back(static_cast<uint32_t>(out->wm_task_row.size()));
+        for (uint64_t r = out->block_row[c]; r < out->block_row[c + 1]; r += rows_per)
+            out->wm_task_row.push_back(static_cast<uint32_t>(r));
+    }
+    const size_t nt = out->wm_task_row.size();
+    out->block_task_wm.push_back(static_cast<uint32_t>(nt));
+    out->wm_task_row.push_back(static_cast<uint32_t>(R));
+    // pass 1: 64-cell pairs per task and distinct words per task
+    std::vector<uint64_t> n_ent(nt + 1, 0), n_grp(nt + 1, 0);
+    auto task_entries = [&](size_t k, std::vector<uint64_t>* key, std::vector<uint64_t>* msk) {
+        key->clear();
+        msk->clear();
+        const uint64_t r0 = out->wm_task_row[k], r1 = out->wm_task_row[k + 1];
+        for (uint64_t s = r0; s < r1; ++s) {
+            const uint64_t r = row_begin + out->perm[s];
+            for (uint64_t q = t.offsets[r]; q < t.offsets[r + 1]; ++q) {
+                const uint64_t w64 = t.word[q] >> 1;
+                const uint64_t m = static_cast<uint64_t>(t.mask[q]) << (32 * (t.word[q] & 1));
+                if (q > t.offsets[r] && !key->empty() && (key->back() >> 8) == w64 && (key->back() & 255) == s - r0) {
+                    msk->back() |= m;  // the other 32-cell half of the same 64-cell word
+                } else {
+                    key->push_back((w64 << 8) | (s - r0));
+                    msk->push_back(m);
+                }
+            }
+        }
+    };
+    parallel_chunks(nt, 256, [&](uint64_t b, uint64_t e, int) {
+        std::vector<uint64_t> key, msk;
+        for (uint64_t k = b; k < e; ++k) {
+            task_entries(k, &key, &msk);
+            std::sort(key.begin(), key.end());
+            uint64_t g = 0;
+            for (size_t i = 0; i < key.size(); ++i) g += (i == 0 || (key[i] >> 8) != (key[i - 1] >> 8));
+            n_ent[k + 1] = key.size();
+            n_grp[k + 1] = g;
+        }
+    });
+    for (size_t k = 0; k < nt; ++k) {
+        n_ent[k + 1] += n_ent[k];
+        n_grp[k + 1] += n_grp[k];
+    }
+    out->wm_mask.assign(n_ent[nt] + 32, 0);  // (+32: a warp loads whole 32-entry chunks)
+    out->wm_row.assign(n_ent[nt] + 32, 0);
+    out->wm_gword.assign(n_grp[nt], 0);
+    out->wm_gstart.assign(n_grp[nt] + 1, static_cast<uint32_t>(n_ent[nt]));
+    out->wm_task_grp.assign(nt + 1, 0);
+    for (size_t k = 0; k <= nt; ++k) out->wm_task_grp[k] = static_cast<uint32_t>(n_grp[k]);
+    // pass 2: fill, sorted by (word, row)
+    parallel_chunks(nt, 256, [&](uint64_t b, uint64_t e, int) {
+        std::vector<uint64_t> key, msk;
+        std::vector<uint32_t> ord;
+        for (uint64_t k = b; k < e; ++k) {
+            task_entries(k, &key, &msk);
+            ord.resize(key.size());
+            for (size_t i = 0; i < ord.size(); ++i) ord[i] = static_cast<uint32_t>(i);
+            std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t c) { return key[a] < key[c]; });
+            uint64_t en = n_ent[k], gn = n_grp[k];
+            for (size_t i = 0; i < ord.size(); ++i) {
+                const uint64_t kk = key[ord[i]];
+                if (i == 0 || (kk >> 8) != (key[ord[i - 1]] >> 8)) {
+                    out->wm_gword[gn] = static_cast<uint32_t>(kk >> 8);
+                    out->wm_gstart[gn] = static_cast<uint32_t>(en);
+                    ++gn;
+                }
+                out->wm_mask[en] = msk[ord[i]];
+                out->wm_row[en] = static_cast<uint8_t>(kk & 255);
+                ++en;
+            }
+        }
+    });
+}
+
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
                  uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs, int blocks,
-                 PackedShard* out) {
+                 PackedShard* out, int wm_rows) {
     const uint64_t R = row_end - row_begin;
     out->row_begin = row_begin;
     out->row_end = row_end;
@@ -743,6 +825,7 @@ void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool so
     build_stream_layout(t, row_begin, row_end, sentinel_word, stream_task_pairs, out);
     build_stream64_layout(t, row_begin, sentinel_word / 2, out);  // sentinel_word = nw32 = 2 * nw64
     build_batch64_layout(t, row_begin, sentinel_word / 2, out);
+    build_wm_layout(t, row_begin, wm_rows, out);
 }
 
 }  // namespace ltlg

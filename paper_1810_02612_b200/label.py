@@ -332,7 +332,7 @@ class LabelEngine:
 
     def __init__(self, devices: Optional[Sequence[int]] = None, sort_rows: bool = True,
                  stream_task_pairs: int = 0, batch_task_pairs: int = 0, profile: bool = False,
-                 readback_chunks: int = 0):
+                 readback_chunks: int = 0, task_rows: int = 0):
         self._L = N.lib()
         opts = N.Options()
         opts.sort_rows = 1 if sort_rows else 0
@@ -340,6 +340,7 @@ class LabelEngine:
         opts.batch_task_pairs = batch_task_pairs
         opts.profile = 1 if profile else 0
         opts.readback_chunks = readback_chunks
+        opts.task_rows = task_rows
         h = C.c_void_p()
         if devices is None:
             st = self._L.ltlg_create_ex(None, 1, C.byref(opts), C.byref(h))

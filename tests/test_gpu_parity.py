@@ -861,7 +861,7 @@ def test_apply_labels_vs_reference(props):
     P = bits_to_words(random_rows(rng, props, cols, 0.02)) if props else np.zeros((0, 16), np.uint64)
     eng = LabelEngine(devices=[0])
     eng.load_abstraction(CsrBoolMatrix(r, cols, off, idx))
-    eng.submit_grid(cols, props, P.reshape(1, props, -1), 1)
+    eng.submit_grid(cols, props, P.reshape(1, props, 16), 1)
     el = eng.apply_labels(r, props)
     want = ORACLE.label_all(r, cols, off, idx, cols, props, P) if props else np.zeros(r, np.uint64)
     assert el.alphabet_size == props and np.array_equal(el.labels, want.reshape(r, -1)[:, 0] if props else want)
