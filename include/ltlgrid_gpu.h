@@ -62,8 +62,8 @@ typedef struct ltlg_options {
                              submits of host-memory P label them with separate launches, so
                              ltlg_get_labels_packed copies block c to the host while later blocks
                              are still being labelled (0/1 = off) */
-    int task_rows;        /* rows per warp task of the word-major multi-frame kernel (0 = default 32,
-                             at most 256); its shared memory per warp grows with it */
+    int task_rows;        /* rows per CTA task of the word-major multi-frame kernel (0 = default 128,
+                             at most 256); its shared memory per CTA grows with it */
     int reserved[5];
 } ltlg_options;
 

@@ -517,7 +517,8 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         static const bool wm_ok = !getenv("LTLG_WORDMAJOR") || atoi(getenv("LTLG_WORDMAJOR")) != 0;
         const bool wm = wm_ok && s.wm_rows > 0;
         const int nslice = pl ? (frames + 63) / 64 : 1;
-        CK(s.sf.reserve(pl ? pl_work_bytes(props, std::min(frames, 64), nw64)
+        CK(s.sf.reserve(pl && wm ? wm_work_bytes(props, nw64)
+                        : pl ? pl_work_bytes(props, std::min(frames, 64), nw64)
                         : wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32
                         : wide ? split64_table_bytes(props, nw64)
                              : frames == 1 && props <= 32
@@ -536,6 +537,10 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
             CK(launch_summary64(P_host ? P_host : s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr,
                                 s.ctr.ptr, nctr, s.stream, P_host ? s.P.ptr : nullptr,
                                 pl_touched_on() ? s.touched64.ptr : nullptr),
+               "summary kernel");
+        else if (pl && wm)
+            CK(launch_wm_build(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.sf.ptr,
+                               s.sf.bytes, s.ctr.ptr, nctr, s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (pl)
             CK(launch_pl(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.sf.ptr,

@@ -53,7 +53,7 @@ struct PackedShard {
     // sentinel word included); the prop-lane summary skips the other words
     std::vector<uint32_t> touched64;
     // word-major multi-frame copy (the prop-lane path's default kernel,
-    // label_wm_kernel): tasks of <= wm_rows consecutive rows of the batch row
+    // label_wm_kernel): CTA tasks of <= wm_rows consecutive rows of the batch row
     // order (never crossing a read-back block); a task's 64-cell pairs are
     // grouped by word, so the word's per-frame summary and partial records
     // are read once per task and tested against every pair on it.
@@ -79,7 +79,7 @@ struct PackedShard {
 };
 
 constexpr uint64_t kPairPad = 512;  // tail padding so vector loads never leave the array
-constexpr int kWmRows = 32;  // rows per word-major task (label_wm_kernel: shared memory per warp ~ rows)
+constexpr int kWmRows = 128;  // rows per word-major CTA task (label_wm_kernel: 256 B of shared memory per row and 32 props)
 
 // Single-frame layout.  The stream kernel gives each lane kStreamK consecutive
 // pairs of a warp chunk of 32*kStreamK pairs and reads them as 16-byte pieces.

@@ -1848,17 +1848,10 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
                                                         uint64_t* __restrict__ sfr, uint2* __restrict__ rec_se,
                                                         uint32_t* __restrict__ rec_cursor, uint4* __restrict__ rec,
                                                         uint32_t* __restrict__ task_ctr, int nctr,
-                                                        const uint32_t* __restrict__ touched64,
-                                                        uint32_t* __restrict__ ffrT, uint32_t* __restrict__ sfrT) {
+                                                        const uint32_t* __restrict__ touched64) {
     constexpr int NP = 1 << PSHIFT, WPB = NT / NP;
-    constexpr int TW = 64 * (NP / 32);  // frame-major u32 words per grid word: [prop half][frame]
     __shared__ uint32_t s_cnt[NP][WPB];
     __shared__ uint32_t s_base[WPB];
-    __shared__ uint32_t s_fT[WPB][TW], s_sT[WPB][TW];
-    for (int k = threadIdx.x; k < WPB * TW; k += NT) {
-        (&s_fT[0][0])[k] = 0;
-        (&s_sT[0][0])[k] = 0;
-    }
     const uint32_t gt = blockIdx.x * static_cast<uint32_t>(NT) + threadIdx.x;
     if (gt < static_cast<uint32_t>(nctr)) task_ctr[gt] = 0;
     const uint32_t j = threadIdx.x / WPB, wl = threadIdx.x % WPB;
@@ -1886,13 +1879,7 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
         sfr[o] = any;
     }
     s_cnt[j][wl] = n;
-    __syncthreads();  // (also orders the s_fT / s_sT zeroing before the ORs)
-    // frame-major copies for the word-major kernel: word f + 64 (j / 32) of
-    // grid word w holds bit j % 32 for every prop j full / non-zero in frame f
-    for (uint64_t x = full; x; x &= x - 1)
-        atomicOr(&s_fT[wl][__ffsll(static_cast<long long>(x)) - 1 + 64 * (j >> 5)], 1u << (j & 31));
-    for (uint64_t x = any; x; x &= x - 1)
-        atomicOr(&s_sT[wl][__ffsll(static_cast<long long>(x)) - 1 + 64 * (j >> 5)], 1u << (j & 31));
+    __syncthreads();
     if (j == 0 && in) {  // per word: exclusive prefix over props, then its segment
         uint32_t run = 0;
         for (int k = 0; k < NP; ++k) {
@@ -1905,13 +1892,6 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
         rec_se[w] = make_uint2(b, b + run);
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < WPB * TW; k += NT) {  // coalesced rows of TW words per grid word
-        const uint32_t ww = blockIdx.x * WPB + static_cast<uint32_t>(k / TW);
-        if (ww <= nw64) {
-            ffrT[static_cast<uint64_t>(ww) * TW + k % TW] = (&s_fT[0][0])[k];
-            sfrT[static_cast<uint64_t>(ww) * TW + k % TW] = (&s_sT[0][0])[k];
-        }
-    }
     if (!n) return;
     uint32_t pos = s_base[wl] + s_cnt[j][wl];
     for (int f = 0; f < frames; ++f) {
@@ -1919,6 +1899,144 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
         if (x != 0 && x != valid)  // smem label accumulator word f + 64 (j / 32), bit j % 32
             rec[pos++] = make_uint4(static_cast<uint32_t>(x), static_cast<uint32_t>(x >> 32),
                                     4u * (static_cast<uint32_t>(f) + 64u * (j >> 5)), 1u << (j & 31));
+    }
+}
+
+// The word-major kernel's per-submit summary, one pass (label_wm_kernel).
+// A CTA owns WPB consecutive grid words x all 1 << PSHIFT prop slots (thread
+// j * WPB + wl: consecutive threads read consecutive words of one prop).  Per
+// grid word w and prop half h (props 32 h .. 32 h + 31) it writes
+//   ffrT[w][h][f]         bit j % 32 for every prop j of the half that is
+//                         full on w in frame f (frame-major);
+//   wpair[w][h][k]        the two frames lane k of the labelling warp owns,
+//                         fa | fb << 8.  Frames f and f + 32 go to different
+//                         lanes' (fa and fb) sides, so a warp's 32 fa (and 32
+//                         fb) accumulator words are distinct banks; the sides
+//                         are paired busiest-with-idlest by partial-record
+//                         count, which evens the records per lane;
+//   lane records          one 16-B record {P lo, P hi, wlo, whi} per partial
+//                         (frame f, prop j), in the lane that owns f, at slot
+//                         row (records of fa first, then of fb); wlo = 1 << j % 32
+//                         if f = fa, whi if f = fb.  Half h fills ns[h] slot
+//                         rows of 32 records (ns = the largest per-lane count;
+//                         holes are zero records, which never hit);
+//   whdr[w]               {first slot row, ns[0] | ns[1] << 16}.
+template <int PSHIFT, int NT>
+__global__ void __launch_bounds__(NT) wm_build_kernel(const uint64_t* __restrict__ P64, int props, int frames,
+                                                        uint32_t nw64, uint64_t cells, uint32_t* __restrict__ ffrT,
+                                                        uint2* __restrict__ whdr,
+                                                        uint16_t* __restrict__ wpair, uint32_t* __restrict__ row_cursor,
+                                                        uint4* __restrict__ lrec, uint32_t* __restrict__ task_ctr,
+                                                        int nctr, const uint32_t* __restrict__ touched64) {
+    constexpr int NP = 1 << PSHIFT, WPB = NT / NP, NH = NP / 32;
+    constexpr int TW = 64 * NH;  // frame-major u32 words per grid word: [prop half][frame]
+    __shared__ uint32_t s_fT[WPB][TW];
+    __shared__ uint32_t s_cnt[WPB][NH][64];  // partial records per frame, then the frame's next slot
+    __shared__ uint16_t s_own[WPB][NH][64];   // frame -> owning lane | first slot << 8
+    __shared__ uint32_t s_row[WPB][NH];       // first slot row of each (word, half)
+    __shared__ uint32_t s_nrows[WPB];         // slot rows of each word
+    for (int k = threadIdx.x; k < WPB * TW; k += NT) {
+        (&s_fT[0][0])[k] = 0;
+        (&s_cnt[0][0][0])[k] = 0;
+    }
+    const uint32_t gt = blockIdx.x * static_cast<uint32_t>(NT) + threadIdx.x;
+    if (gt < static_cast<uint32_t>(nctr)) task_ctr[gt] = 0;
+    const uint32_t j = threadIdx.x / WPB, wl = threadIdx.x % WPB, h = j >> 5;
+    const uint32_t w = blockIdx.x * WPB + wl;
+    const bool in = w <= nw64;  // word nw64 is the zero sentinel
+    const bool live = in && w < nw64 && static_cast<uint64_t>(w) * 64 < cells && j < static_cast<uint32_t>(props) &&
+                      !(touched64 && !(__ldg(touched64 + (w >> 5)) >> (w & 31) & 1u));
+    const uint64_t lo = static_cast<uint64_t>(w) * 64;
+    const uint64_t valid = !live ? 0ull : (cells - lo >= 64) ? ~0ull : ((1ull << (cells - lo)) - 1ull);
+    const uint64_t* base = P64 + static_cast<uint64_t>(j) * nw64 + w;
+    const uint64_t fstride = static_cast<uint64_t>(props) * nw64;
+    __syncthreads();  // (the zeroing before the ORs)
+    uint64_t part = 0;
+    if (live) {
+        const uint32_t bit = 1u << (j & 31);
+        for (int f = 0; f < frames; ++f) {
+            const uint64_t x = base[static_cast<uint64_t>(f) * fstride] & valid;
+            if (x == valid) atomicOr(&s_fT[wl][64 * h + f], bit);
+            if (x != 0 && x != valid) {
+                part |= 1ull << f;
+                atomicAdd(&s_cnt[wl][h][f], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    static_assert(WPB * NH == NT / 32, "one warp per (word, prop half)");
+    {  // warp q * NH + hh: the frame pairing of (word q, half hh); lane r holds residue r
+        const uint32_t wq = threadIdx.x >> 5, r = threadIdx.x & 31;
+        const uint32_t q = wq / NH, hh = wq % NH;
+        uint32_t* c = s_cnt[q][hh];
+        // side a = the busier of frames (r, r + 32), side b the other
+        const uint32_t c0 = c[r], c1 = c[r + 32];
+        const uint32_t fa = c1 > c0 ? r + 32 : r, fb = c1 > c0 ? r : r + 32;
+        const uint32_t ca = max(c0, c1), cb = min(c0, c1);
+        // ranks: a by count descending, b ascending (ties by residue)
+        uint32_t ra = 0, rb = 0;
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t xa = __shfl_sync(0xffffffffu, ca, k), xb = __shfl_sync(0xffffffffu, cb, k);
+            ra += (xa > ca) || (xa == ca && static_cast<uint32_t>(k) < r);
+            rb += (xb < cb) || (xb == cb && static_cast<uint32_t>(k) < r);
+        }
+        uint16_t* own = s_own[q][hh];  // (scratch first: own[rank] = a frame, own[32 + rank] = b frame)
+        own[ra] = static_cast<uint16_t>(fa);
+        own[32 + rb] = static_cast<uint16_t>(fb);
+        __syncwarp();
+        const uint32_t ka = own[r], kb = own[32 + r];  // lane r's pair: a of rank r, b of rank r
+        const uint32_t na = c[ka], nb = c[kb];
+        __syncwarp();
+        own[ka] = static_cast<uint16_t>(r);                   // lane | side << 5 | first slot << 8
+        own[kb] = static_cast<uint16_t>(r | 32u | na << 8);
+        c[ka] = 0;  // the frame's next slot
+        c[kb] = na;
+        uint32_t ns = na + nb;
+        for (int d = 16; d; d >>= 1) ns = max(ns, __shfl_xor_sync(0xffffffffu, ns, d));
+        const uint32_t ww = blockIdx.x * WPB + q;
+        if (ww <= nw64) wpair[(static_cast<uint64_t>(ww) * NH + hh) * 32 + r] = static_cast<uint16_t>(ka | kb << 8);
+        if (r == 0) s_row[q][hh] = ns;  // (counts for now)
+    }
+    __syncthreads();
+    if (threadIdx.x < WPB) {  // per word: its segment of slot rows
+        const uint32_t ww = blockIdx.x * WPB + threadIdx.x;
+        uint32_t ns[NH], run = 0;
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) {
+            ns[hh] = s_row[threadIdx.x][hh];
+            run += ns[hh];
+        }
+        const uint32_t r0 = run ? atomicAdd(row_cursor, run) : 0u;
+        s_nrows[threadIdx.x] = run;
+        uint32_t acc = r0;
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) {
+            s_row[threadIdx.x][hh] = acc;
+            acc += ns[hh];
+        }
+        if (ww <= nw64) whdr[ww] = make_uint2(r0, ns[0] | (NH > 1 ? ns[NH - 1] << 16 : 0u));
+    }
+    __syncthreads();
+    // the frame-major summary (coalesced rows of TW words per grid word), and
+    // zero records over every slot row of the CTA's words (the holes)
+    for (int k = threadIdx.x; k < WPB * TW; k += NT) {
+        const uint32_t ww = blockIdx.x * WPB + static_cast<uint32_t>(k / TW);
+        if (ww <= nw64) ffrT[static_cast<uint64_t>(ww) * TW + k % TW] = (&s_fT[0][0])[k];
+    }
+    for (int q = 0; q < WPB; ++q) {
+        if (blockIdx.x * WPB + q > nw64) break;
+        for (uint32_t k = threadIdx.x; k < s_nrows[q] * 32; k += NT)
+            lrec[static_cast<uint64_t>(s_row[q][0]) * 32 + k] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    __syncthreads();
+    const uint32_t bit = 1u << (j & 31);
+    for (uint64_t x = part; x; x &= x - 1) {
+        const int f = __ffsll(static_cast<long long>(x)) - 1;
+        const uint64_t p = base[static_cast<uint64_t>(f) * fstride] & valid;
+        const uint32_t o = s_own[wl][h][f], side_b = o & 32u;
+        const uint32_t slot = atomicAdd(&s_cnt[wl][h][f], 1u);
+        lrec[(static_cast<uint64_t>(s_row[wl][h]) + slot) * 32 + (o & 31u)] =
+            make_uint4(static_cast<uint32_t>(p), static_cast<uint32_t>(p >> 32), side_b ? 0u : bit, side_b ? bit : 0u);
     }
 }
 
@@ -2035,26 +2153,88 @@ __global__ void __launch_bounds__(256)
 // ---------------------------------------------------------------------------
 // Word-major multi-frame labelling (<= 64 frames per launch, <= 64 props).
 //
-// A warp task is a run of <= R consecutive rows of the batch order (z-sorted,
+// A CTA task is a run of <= R consecutive rows of the batch order (z-sorted,
 // so they sweep a compact region of the grid), with the rows' 64-cell pairs
-// grouped by word (PackedShard::wm_*).  Per word group the warp reads the
-// word's frame-major summary once -- lane f holds ffrT / sfrT of frames f and
-// f + 32 (bit j = prop j full / non-zero) -- and the word's partial records
-// once, into registers (lane k holds records k, k + 32, ...), then streams the
-// group's pairs (broadcast one at a time by shuffle) past them:
-//   * every pair ORs its word's full props (any non-zero prop when the pair
-//     sweeps all 64 cells) into acc[row][f], lane f  (red.shared.or, distinct
-//     consecutive words);
-//   * a partial pair tests every record  m & P_record != 0  and ORs hits into
-//     acc[row][f_record] bit j_record.
-// acc is the warp's shared-memory label block, frame-major per row, so the
-// row-end stores are coalesced 4-byte words (lane f = frame f) and need no
-// bit transpose.  The pair-major label_pl_kernel re-read each pair's word
-// summary (256 B) and records (~600 B) from L1 for every pair; here a word's
-// ~850 B are read once per task and amortised over its pairs.
+// grouped by word (PackedShard::wm_*).  The CTA's warps take the task's word
+// groups from a shared-memory counter.  Lane k owns two frames of the word,
+// fa and fb (wm_build_kernel's wpair), and two accumulator words per row and
+// prop half.  Per group a warp reads, once, the word's full-prop masks of the
+// lane's frames (ffrT) and the lane's partial records (slot rows of 32: each
+// lane's own records of fa / fb, {P lo, P hi, bit if fa, bit if fb}), into
+// registers, then streams the group's pairs (broadcast one at a time by
+// shuffle) past them: v_fa = full props | bits of the records with m & P != 0
+// (likewise v_fb), and one red.shared.or per accumulator word.  Every lane
+// ORs into its own frame's word, so the 32 lanes hit 32 distinct banks.
+// acc is the CTA's shared-memory label block, frame-major per row (several
+// warps may OR into one row: the reductions are atomic), so the row-end
+// stores are coalesced 4-byte words (lane f = frame f) with no bit transpose.
+// The pair-major label_pl_kernel re-read each pair's word summary (256 B)
+// and records (~600 B) from L1 for every pair and scattered its record hits
+// with bank-conflicting atomics; here a word's data is read once per task and
+// amortised over its pairs (~26 per group at R = 128 on config 4).
 // ---------------------------------------------------------------------------
-constexpr int kWmThreads = 128;
-constexpr int kWmRecSets = 4;  // records (x 32) held in registers per word; more are re-read per pair
+constexpr int kWmThreads = 256;
+constexpr int kWmSlots = 4;  // slot rows (per prop half) held in registers per word; more are re-read per pair
+
+// v0 |= z and v1 |= w if (mlo & x) | (mhi & y) != 0: a record test with
+// predicated ORs (plain C++ compiles to SELs, two more instructions)
+__device__ __forceinline__ void rec_test(uint32_t mlo, uint32_t mhi, const uint4& r, uint32_t& v0, uint32_t& v1) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t, u;\n\t"
+        "and.b32 t, %2, %4;\n\tand.b32 u, %3, %5;\n\tor.b32 t, t, u;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t@p or.b32 %0, %0, %6;\n\t@p or.b32 %1, %1, %7;\n\t}"
+        : "+r"(v0), "+r"(v1)
+        : "r"(mlo), "r"(mhi), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w));
+}
+
+// The pairs [e0, e1) of one word group against the word's summary (fv / sv:
+// lane's frames fa, fb of each prop half) and its lane records: NS slot rows
+// per half in registers (r0: half 0, r1: half 1); MORE: more rows than that,
+// re-read per pair from lrec (rows [m0, m0 + mn0) of half 0, [m1, m1 + mn1)
+// of half 1).  One red.shared.or per accumulator word (oa / ob: the lane's
+// frames' byte offsets in a row) and pair.
+template <int PW, int NS, bool MORE>
+__device__ __forceinline__ void wm_group(const uint64_t* __restrict__ emask, const uint8_t* __restrict__ erow,
+                                         uint32_t e0, uint32_t e1, const uint32_t (&fv)[2 * PW],
+                                         const uint32_t (&off)[2 * PW],
+                                         const uint4 (&r0)[kWmSlots], const uint4 (&r1)[kWmSlots], uint32_t ns0,
+                                         uint32_t ns1, const uint4* __restrict__ lrec, uint32_t m0, uint32_t mn0,
+                                         uint32_t m1, uint32_t mn1, uint32_t acc_s, int lane) {
+    constexpr uint32_t RB = 64 * PW * 4;  // accumulator bytes per row
+    for (uint32_t c = e0; c < e1; c += 32) {
+        const uint2 cm = __ldg(reinterpret_cast<const uint2*>(emask + c + lane));
+        const uint32_t cr = __ldg(erow + c + lane);
+        const int n = static_cast<int>(e1 - c < 32u ? e1 - c : 32u);
+        for (int i = 0; i < n; ++i) {
+            const uint32_t mlo = __shfl_sync(0xffffffffu, cm.x, i), mhi = __shfl_sync(0xffffffffu, cm.y, i);
+            const uint32_t base = acc_s + __shfl_sync(0xffffffffu, cr, i) * RB;
+            // full props hit any pair; a partial prop hits iff one of its
+            // records does (for a pair sweeping the whole word every record
+            // hits, so no special case for it)
+            uint32_t v[2 * PW];
+#pragma unroll
+            for (int k = 0; k < 2 * PW; ++k) v[k] = fv[k];
+            {
+                // (slot rows past a half's count hold zero records: no hit)
+#pragma unroll
+                for (int k = 0; k < NS; ++k) rec_test(mlo, mhi, r0[k], v[0], v[1]);
+                if constexpr (PW == 2) {
+#pragma unroll
+                    for (int k = 0; k < NS; ++k) rec_test(mlo, mhi, r1[k], v[2], v[3]);
+                }
+                if constexpr (MORE) {
+                    for (uint32_t q = 0; q < mn0; ++q)
+                        rec_test(mlo, mhi, __ldg(lrec + static_cast<uint64_t>(m0 + q) * 32 + lane), v[0], v[1]);
+                    if constexpr (PW == 2)
+                        for (uint32_t q = 0; q < mn1; ++q)
+                            rec_test(mlo, mhi, __ldg(lrec + static_cast<uint64_t>(m1 + q) * 32 + lane), v[2], v[3]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 2 * PW; ++k)  // (an OR of 0 is a no-op: no branch around it)
+                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + off[k]), "r"(v[k]) : "memory");
+        }
+    }
+}
 
 template <typename SW, int PW>
 __global__ void __launch_bounds__(kWmThreads)
@@ -2062,72 +2242,72 @@ __global__ void __launch_bounds__(kWmThreads)
                     const uint32_t* __restrict__ gword, const uint32_t* __restrict__ gstart,
                     const uint32_t* __restrict__ task_row, const uint32_t* __restrict__ task_grp,
                     uint32_t task_begin, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
-                    const uint32_t* __restrict__ ffrT, const uint32_t* __restrict__ sfrT,
-                    const uint2* __restrict__ rec_se, const uint4* __restrict__ rec, int frames,
-                    const uint32_t* __restrict__ perm, SW* __restrict__ out, uint32_t ostride, int rows_per_task) {
+                    const uint32_t* __restrict__ ffrT, const uint2* __restrict__ whdr, const uint16_t* __restrict__ wpair,
+                    const uint4* __restrict__ lrec, int frames, const uint32_t* __restrict__ perm,
+                    SW* __restrict__ out, uint32_t ostride, int rows_per_task) {
     extern __shared__ uint32_t wm_acc[];
+    __shared__ uint32_t s_task, s_group;
     constexpr int RW = 64 * PW;  // accumulator words per row: [prop half][frame]
+    constexpr int NW = kWmThreads / 32;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    uint32_t* acc = wm_acc + static_cast<size_t>(wib) * static_cast<size_t>(rows_per_task) * RW;
-    const uint32_t acc_s = smem_u32(acc);
-    for (int k = lane; k < rows_per_task * RW; k += 32) acc[k] = 0;
-    __syncwarp();
+    const uint32_t acc_s = smem_u32(wm_acc);
+    for (int k = threadIdx.x; k < rows_per_task * RW; k += kWmThreads) wm_acc[k] = 0;
     for (;;) {
-        uint32_t t = 0;
-        if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
-        t = __shfl_sync(0xffffffffu, t, 0);
+        if (threadIdx.x == 0) {
+            s_task = task_begin + atomicAdd(task_ctr, 1u);
+            s_group = 0;
+        }
+        __syncthreads();
+        const uint32_t t = s_task;
         if (t >= ntasks) break;
         const uint32_t r0 = task_row[t], nr = task_row[t + 1] - r0;
-        const uint32_t g1 = task_grp[t + 1];
-        for (uint32_t g = task_grp[t]; g < g1; ++g) {
+        const uint32_t g0 = task_grp[t], ng = task_grp[t + 1] - g0;
+        for (;;) {
+            uint32_t gi = 0;
+            if (lane == 0) gi = atomicAdd(&s_group, 1u);
+            gi = __shfl_sync(0xffffffffu, gi, 0);
+            if (gi >= ng) break;
+            const uint32_t g = g0 + gi;
             const uint32_t w = gword[g];
             const uint32_t e0 = gstart[g], e1 = gstart[g + 1];
-            uint32_t fv[2 * PW], sv[2 * PW];
+            uint32_t fv[2 * PW], off[2 * PW];
 #pragma unroll
-            for (int k = 0; k < 2 * PW; ++k) {
-                fv[k] = __ldg(ffrT + static_cast<uint64_t>(w) * RW + lane + 32 * k);
-                sv[k] = __ldg(sfrT + static_cast<uint64_t>(w) * RW + lane + 32 * k);
+            for (int hh = 0; hh < PW; ++hh) {  // the lane's two frames of each prop half
+                const uint32_t pr = __ldg(wpair + (static_cast<uint64_t>(w) * PW + hh) * 32 + lane);
+                off[2 * hh] = 4u * (64u * hh + (pr & 0xffu));
+                off[2 * hh + 1] = 4u * (64u * hh + (pr >> 8));
             }
-            const uint2 se = __ldg(rec_se + w);
-            const uint32_t nrec = se.y - se.x;
-            uint4 rc[kWmRecSets];
 #pragma unroll
-            for (int k = 0; k < kWmRecSets; ++k)
-                rc[k] = (32u * k + lane < nrec) ? __ldg(rec + se.x + 32u * k + lane) : make_uint4(0u, 0u, 0u, 0u);
-            for (uint32_t c = e0; c < e1; c += 32) {
-                const uint2 cm = __ldg(reinterpret_cast<const uint2*>(emask + c + lane));
-                const uint32_t cr = __ldg(erow + c + lane);
-                const int n = static_cast<int>(e1 - c < 32u ? e1 - c : 32u);
-                for (int i = 0; i < n; ++i) {
-                    const uint32_t mlo = __shfl_sync(0xffffffffu, cm.x, i), mhi = __shfl_sync(0xffffffffu, cm.y, i);
-                    const uint32_t base = acc_s + __shfl_sync(0xffffffffu, cr, i) * (RW * 4u);
-                    const bool full = (mlo & mhi) == 0xffffffffu;  // warp-uniform
+            for (int k = 0; k < 2 * PW; ++k) fv[k] = __ldg(ffrT + static_cast<uint64_t>(w) * RW + off[k] / 4);
+            const uint2 hd = __ldg(whdr + w);
+            const uint32_t ns0 = hd.y & 0xffffu, ns1 = hd.y >> 16;
+            uint4 ra[kWmSlots], rb[kWmSlots];
+            const uint4* l0 = lrec + static_cast<uint64_t>(hd.x) * 32 + lane;
+            const uint4* l1 = l0 + static_cast<uint64_t>(ns0) * 32;
 #pragma unroll
-                    for (int k = 0; k < 2 * PW; ++k) {
-                        const uint32_t v = full ? sv[k] : fv[k];
-                        if (v) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + 4u * (lane + 32 * k)), "r"(v) : "memory");
-                    }
-                    if (full) continue;
-#pragma unroll
-                    for (int k = 0; k < kWmRecSets; ++k) {
-                        if (32u * k >= nrec) break;  // warp-uniform
-                        if ((mlo & rc[k].x) | (mhi & rc[k].y))
-                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + rc[k].z), "r"(rc[k].w) : "memory");
-                    }
-                    // words with more partial records than the register sets hold
-                    for (uint32_t q = se.x + 32u * kWmRecSets; q < se.y; q += 32) {
-                        const uint4 r = __ldg(rec + q + lane);  // (the record array is padded by 32)
-                        if ((q + lane < se.y) && ((mlo & r.x) | (mhi & r.y)))
-                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + r.z), "r"(r.w) : "memory");
-                    }
+            for (int k = 0; k < kWmSlots; ++k) {
+                ra[k] = k < ns0 ? __ldg(l0 + 32 * k) : make_uint4(0u, 0u, 0u, 0u);
+                rb[k] = (PW == 2 && k < ns1) ? __ldg(l1 + 32 * k) : make_uint4(0u, 0u, 0u, 0u);
+            }
+            const uint32_t mn0 = ns0 > kWmSlots ? ns0 - kWmSlots : 0u, mn1 = ns1 > kWmSlots ? ns1 - kWmSlots : 0u;
+            const uint32_t m0 = hd.x + kWmSlots, m1 = hd.x + ns0 + kWmSlots;
+            if (mn0 | mn1)
+                wm_group<PW, kWmSlots, true>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, mn0, m1, mn1, acc_s, lane);
+            else
+                switch (ns0 > ns1 ? ns0 : ns1) {  // warp-uniform: one specialised pair loop per slot-row count
+                    case 0: wm_group<PW, 0, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
+                    case 1: wm_group<PW, 1, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
+                    case 2: wm_group<PW, 2, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
+                    case 3: wm_group<PW, 3, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
+                    default: wm_group<PW, 4, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
                 }
-            }
         }
-        __syncwarp();
-        // the task's rows: lane f stores frames f and f + 32, then clears them
-        for (uint32_t r = 0; r < nr; ++r) {
+        __syncthreads();
+        // the task's rows: warp wib stores rows wib, wib + NW, ...; lane f
+        // frames f and f + 32; then clears them
+        for (uint32_t r = wib; r < nr; r += NW) {
             SW* o = out + static_cast<uint64_t>(perm[r0 + r]) * ostride;
-            uint32_t* a = acc + r * RW;
+            uint32_t* a = wm_acc + r * RW;
             uint64_t lo = a[lane], hi = a[lane + 32];
             if constexpr (PW == 2) {
                 lo |= static_cast<uint64_t>(a[lane + 64]) << 32;
@@ -2138,25 +2318,71 @@ __global__ void __launch_bounds__(kWmThreads)
 #pragma unroll
             for (int k = 0; k < 2 * PW; ++k) a[lane + 32 * k] = 0;
         }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
-// Byte layout of the prop-lane work buffer: summary masks (pw prop slots per
-// word; prop-major for label_pl_kernel, frame-major for label_wm_kernel), the
-// record cursor and ranges, then the records (worst case: every (word, prop,
-// frame) partial) + 32 records of padding for the last probe round.
+// Byte layout of the word-major work buffer: frame-major summaries, word
+// headers, the slot-row cursor, then the lane records (worst case: every
+// (word, prop, frame) partial, one per slot row) + 1 row of padding.
+struct WmLayout {
+    uint64_t nt;  // (nw64 + 1) * prop slots
+    size_t ffrT, whdr, wpair, cursor, lrec, total;
+    WmLayout(int props, uint32_t nw64) {
+        nt = static_cast<uint64_t>(nw64 + 1) * (props > 32 ? 64u : 32u);
+        auto up = [](size_t x, size_t a) { return (x + a - 1) & ~(a - 1); };
+        ffrT = 0;
+        whdr = ffrT + nt * 8;  // ffrT: (nw64 + 1) x 64 frames x prop halves u32
+        wpair = whdr + (nw64 + 1) * 8;  // (nw64 + 1) x prop halves x 32 lanes u16 = nt * 2 bytes
+        cursor = up(wpair + nt * 2, 8);
+        lrec = up(cursor + 4, 16);
+        total = lrec + (nt * 64 + 32) * 16;
+    }
+};
+
+size_t wm_work_bytes(int props, uint32_t nw64) { return WmLayout(props, nw64).total; }
+
+cudaError_t launch_wm_build(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* work,
+                            size_t work_bytes, uint32_t* task_ctr, int nctr, cudaStream_t st,
+                            const uint32_t* touched64) {
+    if (props > 64 || frames > 64) return cudaErrorInvalidValue;
+    const WmLayout L(props, nw64);
+    if (L.total > work_bytes) return cudaErrorInvalidValue;
+    uint8_t* wb = static_cast<uint8_t*>(work);
+    cudaError_t e = cudaMemsetAsync(wb + L.cursor, 0, 4, st);
+    if (e != cudaSuccess) return e;
+    constexpr int kNT = 1024;
+    const int pshift = props > 32 ? 6 : 5;
+    const int wpb = kNT >> pshift;
+    const uint64_t gw = (static_cast<uint64_t>(nw64) + 1 + wpb - 1) / wpb, gc = (static_cast<uint64_t>(nctr) + kNT - 1) / kNT;
+    const unsigned grid = static_cast<unsigned>(gw > gc ? gw : gc);
+    auto* ffrT = reinterpret_cast<uint32_t*>(wb + L.ffrT);
+    auto* whdr = reinterpret_cast<uint2*>(wb + L.whdr);
+    auto* cur = reinterpret_cast<uint32_t*>(wb + L.cursor);
+    auto* lrec = reinterpret_cast<uint4*>(wb + L.lrec);
+    auto* wpair = reinterpret_cast<uint16_t*>(wb + L.wpair);
+    if (pshift == 5)
+        wm_build_kernel<5, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffrT, whdr, wpair, cur,
+                                                      lrec, task_ctr, nctr, touched64);
+    else
+        wm_build_kernel<6, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffrT, whdr, wpair, cur,
+                                                      lrec, task_ctr, nctr, touched64);
+    return cudaGetLastError();
+}
+
+// Byte layout of the prop-lane work buffer (label_pl_kernel): summary masks
+// (pw prop slots per word), the record cursor and ranges, then the records
+// (worst case: every (word, prop, frame) partial) + 32 records of padding for
+// the last probe round.
 struct PlLayout {
     uint64_t nt;  // (nw64 + 1) * pw
-    size_t ffr, sfr, ffrT, sfrT, cursor, rec_se, rec, total;
+    size_t ffr, sfr, cursor, rec_se, rec, total;
     PlLayout(int props, int frames, uint32_t nw64) {
         nt = static_cast<uint64_t>(nw64 + 1) * (props > 32 ? 64u : 32u);
         auto up = [](size_t x, size_t a) { return (x + a - 1) & ~(a - 1); };
         ffr = 0;
         sfr = ffr + nt * 8;
-        ffrT = sfr + nt * 8;  // frame-major: (nw64 + 1) x 64 x pw/32 u32 = nt * 8 bytes
-        sfrT = ffrT + nt * 8;
-        cursor = sfrT + nt * 8;
+        cursor = sfr + nt * 8;
         rec_se = up(cursor + 4, 8);
         rec = up(rec_se + (nw64 + 2) * 8, 16);
         total = rec + (nt * static_cast<uint64_t>(frames) + 32) * 16;
@@ -2172,8 +2398,6 @@ cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64,
     uint8_t* wb = static_cast<uint8_t*>(work);
     uint64_t* ffr = reinterpret_cast<uint64_t*>(wb + L.ffr);
     uint64_t* sfr = reinterpret_cast<uint64_t*>(wb + L.sfr);
-    uint32_t* ffrT = reinterpret_cast<uint32_t*>(wb + L.ffrT);
-    uint32_t* sfrT = reinterpret_cast<uint32_t*>(wb + L.sfrT);
     uint32_t* cursor = reinterpret_cast<uint32_t*>(wb + L.cursor);
     uint2* rec_se = reinterpret_cast<uint2*>(wb + L.rec_se);
     uint4* rec = reinterpret_cast<uint4*>(wb + L.rec);
@@ -2188,10 +2412,10 @@ cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64,
     const unsigned grid = static_cast<unsigned>(gw > gc ? gw : gc);
     if (pshift == 5)
         pl_build_kernel<5, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
-                                                  task_ctr, nctr, touched64, ffrT, sfrT);
+                                                  task_ctr, nctr, touched64);
     else
         pl_build_kernel<6, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
-                                                  task_ctr, nctr, touched64, ffrT, sfrT);
+                                                  task_ctr, nctr, touched64);
     return cudaGetLastError();
 }
 
@@ -2217,10 +2441,10 @@ static void launch_pl_label(const LaunchArgs& a, cudaStream_t st) {
 
 template <typename SW, int PW>
 static void launch_wm_label(const LaunchArgs& a, cudaStream_t st) {
-    const PlLayout L(a.props, a.frames, a.nw64);
+    const WmLayout L(a.props, a.nw64);
     const uint8_t* wb = static_cast<const uint8_t*>(a.sf);
     auto kern = label_wm_kernel<SW, PW>;
-    const size_t smem = static_cast<size_t>(kWmThreads / 32) * static_cast<size_t>(a.wm_rows) * 64 * PW * 4;
+    const size_t smem = static_cast<size_t>(a.wm_rows) * 64 * PW * 4;  // the CTA's label block
     static size_t smem_set = 0;
     static int per_sm = 0;
     static size_t per_sm_smem = ~size_t(0);
@@ -2235,8 +2459,9 @@ static void launch_wm_label(const LaunchArgs& a, cudaStream_t st) {
     }
     kern<<<sm_count() * per_sm, kWmThreads, smem, st>>>(
         a.wm_mask, a.wm_row, a.wm_gword, a.wm_gstart, a.wm_task_row, a.wm_task_grp, a.task_begin, a.ntasks,
-        a.task_ctr, reinterpret_cast<const uint32_t*>(wb + L.ffrT), reinterpret_cast<const uint32_t*>(wb + L.sfrT),
-        reinterpret_cast<const uint2*>(wb + L.rec_se), reinterpret_cast<const uint4*>(wb + L.rec), a.frames, a.perm,
+        a.task_ctr, reinterpret_cast<const uint32_t*>(wb + L.ffrT),
+        reinterpret_cast<const uint2*>(wb + L.whdr), reinterpret_cast<const uint16_t*>(wb + L.wpair),
+        reinterpret_cast<const uint4*>(wb + L.lrec), a.frames, a.perm,
         static_cast<SW*>(a.out), a.ostride ? a.ostride : static_cast<uint32_t>(a.frames), a.wm_rows);
 }
 

@@ -65,6 +65,11 @@ cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64,
                       size_t work_bytes, uint32_t* task_ctr, int nctr, cudaStream_t st,
                       const uint32_t* touched64 = nullptr);
 size_t pl_work_bytes(int props, int frames, uint32_t nw64);
+// the word-major kernel's summary (label_wm_kernel): frame-major masks + lane records
+cudaError_t launch_wm_build(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* work,
+                            size_t work_bytes, uint32_t* task_ctr, int nctr, cudaStream_t st,
+                            const uint32_t* touched64 = nullptr);
+size_t wm_work_bytes(int props, uint32_t nw64);
 cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
                              uint32_t* task_ctr, int nctr, cudaStream_t st, uint64_t* P_copy,
                              const uint32_t* touched64 = nullptr);

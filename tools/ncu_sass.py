@@ -1,7 +1,7 @@
 """Summarise an ncu report's SASS page: instructions executed per opcode and
 the hottest instructions by stall samples (dev helper).
 
-  python tools/ncu_sass.py gpurun_out/r01_stream.ncu-rep [top]
+  python tools/ncu_sass.py gpurun_out/r01_stream.ncu-rep [top] [kernel-regex]
 """
 import collections
 import csv
@@ -11,7 +11,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+kfilter = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+txt = subprocess.run(["ncu", "-i", rep, *kfilter, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 hdr = rows[1]

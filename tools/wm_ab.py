@@ -51,7 +51,7 @@ if __name__ == "__main__":
         sys.exit(0)
     import numpy as np
 
-    variants = [("wm32", {"ROWS": "32"}), ("wm16", {"ROWS": "16"}), ("wm64", {"ROWS": "64"}),
+    variants = [("wm128", {"ROWS": "128"}), ("wm64", {"ROWS": "64"}), ("wm256", {"ROWS": "256"}),
                 ("pl", {"LTLG_WORDMAJOR": "0"})]
     ref = None
     for name, env in variants:
