@@ -2174,6 +2174,7 @@ __global__ void __launch_bounds__(256)
 // amortised over its pairs (~26 per group at R = 128 on config 4).
 // ---------------------------------------------------------------------------
 constexpr int kWmThreads = 256;
+constexpr int kWmMaxRows = 256;  // rows per task at most (PackedShard::wm_row is a byte)
 constexpr int kWmSlots = 4;  // slot rows (per prop half) held in registers per word; more are re-read per pair
 
 // v0 |= z and v1 |= w if (mlo & x) | (mhi & y) != 0: a record test with
@@ -2247,6 +2248,7 @@ __global__ void __launch_bounds__(kWmThreads)
                     SW* __restrict__ out, uint32_t ostride, int rows_per_task) {
     extern __shared__ uint32_t wm_acc[];
     __shared__ uint32_t s_task, s_group;
+    __shared__ uint32_t s_perm[kWmMaxRows];  // the task's output rows (cp.async during the task)
     constexpr int RW = 64 * PW;  // accumulator words per row: [prop half][frame]
     constexpr int NW = kWmThreads / 32;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -2262,6 +2264,11 @@ __global__ void __launch_bounds__(kWmThreads)
         if (t >= ntasks) break;
         const uint32_t r0 = task_row[t], nr = task_row[t + 1] - r0;
         const uint32_t g0 = task_grp[t], ng = task_grp[t + 1] - g0;
+        if (threadIdx.x < nr)  // the store's row ids, fetched in the background (no register held)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s_perm + threadIdx.x)),
+                         "l"(perm + r0 + threadIdx.x)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
         for (;;) {
             uint32_t gi = 0;
             if (lane == 0) gi = atomicAdd(&s_group, 1u);
@@ -2302,11 +2309,12 @@ __global__ void __launch_bounds__(kWmThreads)
                     default: wm_group<PW, 4, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
                 }
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         // the task's rows: warp wib stores rows wib, wib + NW, ...; lane f
         // frames f and f + 32; then clears them
         for (uint32_t r = wib; r < nr; r += NW) {
-            SW* o = out + static_cast<uint64_t>(perm[r0 + r]) * ostride;
+            SW* o = out + static_cast<uint64_t>(s_perm[r]) * ostride;
             uint32_t* a = wm_acc + r * RW;
             uint64_t lo = a[lane], hi = a[lane + 32];
             if constexpr (PW == 2) {

@@ -746,22 +746,31 @@ void build_wm_layout(const WordCsr& t, uint64_t row_begin, int wm_rows, PackedSh
     parallel_chunks(nt, 256, [&](uint64_t b, uint64_t e, int) {
         std::vector<uint64_t> key, msk;
         std::vector<uint32_t> ord;
+        std::vector<std::pair<size_t, size_t>> grp;  // (first in ord, entries)
         for (uint64_t k = b; k < e; ++k) {
             task_entries(k, &key, &msk);
             ord.resize(key.size());
             for (size_t i = 0; i < ord.size(); ++i) ord[i] = static_cast<uint32_t>(i);
             std::sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t c) { return key[a] < key[c]; });
+            // the word groups, largest first: the CTA's warps take them in
+            // this order, so the task ends on small groups (less waiting at
+            // the task's barrier)
+            grp.clear();
+            for (size_t i = 0; i < ord.size(); ++i)
+                if (i == 0 || (key[ord[i]] >> 8) != (key[ord[i - 1]] >> 8)) grp.push_back({i, 0});
+            for (size_t g = 0; g < grp.size(); ++g)
+                grp[g].second = (g + 1 < grp.size() ? grp[g + 1].first : ord.size()) - grp[g].first;
+            std::stable_sort(grp.begin(), grp.end(), [](const auto& a, const auto& c) { return a.second > c.second; });
             uint64_t en = n_ent[k], gn = n_grp[k];
-            for (size_t i = 0; i < ord.size(); ++i) {
-                const uint64_t kk = key[ord[i]];
-                if (i == 0 || (kk >> 8) != (key[ord[i - 1]] >> 8)) {
-                    out->wm_gword[gn] = static_cast<uint32_t>(kk >> 8);
-                    out->wm_gstart[gn] = static_cast<uint32_t>(en);
-                    ++gn;
+            for (const auto& gr : grp) {
+                out->wm_gword[gn] = static_cast<uint32_t>(key[ord[gr.first]] >> 8);
+                out->wm_gstart[gn] = static_cast<uint32_t>(en);
+                ++gn;
+                for (size_t i = gr.first; i < gr.first + gr.second; ++i) {
+                    out->wm_mask[en] = msk[ord[i]];
+                    out->wm_row[en] = static_cast<uint8_t>(key[ord[i]] & 255);
+                    ++en;
                 }
-                out->wm_mask[en] = msk[ord[i]];
-                out->wm_row[en] = static_cast<uint8_t>(kk & 255);
-                ++en;
             }
         }
     });
