@@ -127,17 +127,6 @@ def ncu_traffic(kernel: str):
         return None
 
 
-def lop3_peak(sm_clk_hz: float) -> float:
-    """Integer roofline: the measured LOP3 throughput (tools/micro/lop3_peak.cu,
-    profiles/lop3_peak.json) at this run's SM clock, else 64 LOP3/clk/SM."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "lop3_peak.json")) as f:
-            d = json.load(f)
-        return d["lop3_per_clk_per_sm_at_max_clock"] * d["sms"] * sm_clk_hz
-    except Exception:
-        return 148 * 64 * sm_clk_hz
-
-
 def ncu_limiter(kernel: str):
     """Pipe utilisations of `kernel` from the committed ncu capture (profiles/limiters.json)."""
     try:
@@ -145,6 +134,44 @@ def ncu_limiter(kernel: str):
             return json.load(f).get(kernel)
     except Exception:
         return None
+
+
+def pairs64(offsets, words) -> int:
+    """64-cell (word, mask) pairs of a word-CSR: its 32-cell words minus the
+    ones that share a 64-cell word with their predecessor in the same row."""
+    w = np.asarray(words) >> 1
+    if len(w) < 2:
+        return len(w)
+    same = w[1:] == w[:-1]
+    head = np.zeros(len(w), bool)
+    off = np.asarray(offsets, dtype=np.int64)[:-1]
+    head[off[off < len(w)]] = True
+    return int(len(w) - np.count_nonzero(same & ~head[1:]))
+
+
+def binding_roofline(kernel: str, kernel_ms: float, sm_clk_hz: float, sms: int = 148, pairs: int = 0):
+    """The roofline of the algorithm as it runs, for an issue / L1-bound
+    kernel: the committed ncu --set full capture's per-launch counts
+    (profiles/limiters.json: warp instructions executed, L1TEX data-pipe
+    wavefronts) over this run's event-timed launch duration, against the
+    SM's peaks at this run's clock -- 4 warp instructions issued per cycle
+    (one per SMSP) and 1 data-pipe wavefront per cycle."""
+    lim = ncu_limiter(kernel) or {}
+    out = {"source": "profiles/limiters.json (" + str(lim.get("source")) + ") counts / this run's kernel time",
+           "sm_clock_hz": sm_clk_hz}
+    sec = kernel_ms / 1e3
+    if lim.get("warp_insts"):
+        a = lim["warp_insts"] / sec
+        out["issue"] = {"achieved": a, "peak": 4.0 * sms * sm_clk_hz, "unit": "warp-inst/s",
+                        "frac": a / (4.0 * sms * sm_clk_hz), "per_launch": lim["warp_insts"],
+                        "per_pair": lim["warp_insts"] / pairs if pairs else None}
+    if lim.get("l1_data_pipe_wavefronts"):
+        a = lim["l1_data_pipe_wavefronts"] / sec
+        out["l1tex_data_pipe"] = {"achieved": a, "peak": 1.0 * sms * sm_clk_hz, "unit": "wavefronts/s",
+                                  "frac": a / (1.0 * sms * sm_clk_hz), "per_launch": lim["l1_data_pipe_wavefronts"],
+                                  "per_pair": lim["l1_data_pipe_wavefronts"] / pairs if pairs else None}
+    out["ncu"] = {k: v for k, v in lim.items() if k.endswith("_pct")}
+    return out
 
 
 def shard_rows(E: int, rank: int, world: int):
@@ -182,68 +209,213 @@ def spatial_shard(offsets, words, masks, rank: int, world: int):
     return ids, so.astype(np.uint64), np.asarray(words)[idx], np.asarray(masks)[idx]
 
 
-def cpu_reference_sample(depth: int, props: int, rows: int, frames: int, workers: int = 0):
-    """Time the reference CPU label_all (oracle/_ref, or the C port) on rows
-    [0, rows) of the same synthetic T, `frames` frames, best of 2 per frame
-    (time_label_ms protocol, scenario.cpp:154-165).  Returns (edge-labels/s,
-    kind, cores, sample description)."""
-    from oracle.oracle import Oracle, RefCore  # checker / baseline only
-    from paper_1810_02612_b200.synth import SyntheticPRM, props_words
+def host_cpu():
+    """The CPU-baseline core count and model: nproc (the
+    affinity mask), std::thread::hardware_concurrency() as label.cpp:66 sees it,
+    and the lscpu model name."""
+    from oracle.oracle import RefCore  # checker / baseline only
 
-    prm = SyntheticPRM(seed=SEED_T, depth=depth)
-    off, idx = prm.csr(0, rows)
-    P = props_words(SEED_P, depth, props, 0, frames)
-    cells = 1 << depth
-    if RefCore.available():
-        ref = RefCore()
-        kind = "reference"
-        cores = workers or ref.hardware_concurrency()
-        m = ref.csr_handle(rows, cells, off, idx)
-        total = 0.0
-        for f in range(frames):
-            p = ref.props_handle(cells, props, P[f])
-            total += ref.time_label_ms(m, p, workers, 2) / 1e3
-            ref.free(p=p)
-        ref.free(m=m)
-    else:
-        o = Oracle()
-        kind = "port"
-        cores = o.effective_workers(workers, rows)
-        total = 0.0
-        for f in range(frames):
-            best = 1e30
-            for _ in range(2):
-                t0 = time.perf_counter()
-                o.label_all(rows, cells, off, idx, cells, props, P[f], workers)
-                best = min(best, time.perf_counter() - t0)
-            total += best
-    sample = f"rows [0,{rows}) of the {CFG4['edges']}-edge T, {frames} frames x {props} props, best of 2 per frame"
-    return rows * frames / total, kind, cores, sample
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        model = next((l.split(":", 1)[1].strip() for l in out.splitlines() if l.startswith("Model name")), None)
+    except Exception:
+        pass
+    if model is None:
+        try:
+            model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+        except Exception:
+            model = "unknown"
+    nproc = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    hc = RefCore().hardware_concurrency() if RefCore.available() else os.cpu_count()
+    return {"nproc": nproc, "hardware_concurrency": hc, "lscpu_model": model}
+
+
+class RefSlice:
+    """Rows [0, rows) of the synthetic T (depth), as the unmodified reference
+    core's CsrBoolMatrix (oracle/_ref), or the C port when the reference was
+    not built.  The generator is the one linked into oracle/_ref, so the
+    reference arm loads no other library of the repo."""
+
+    def __init__(self, depth: int, rows: int):
+        from oracle.oracle import REF_SO, Oracle, RefCore  # checker / baseline only
+        import workload.synth as ws
+
+        if RefCore.available():
+            ws.use_library(REF_SO)
+            self.ref, self.kind = RefCore(), "reference"
+        else:
+            self.ref, self.kind = Oracle(), "port"
+        self.depth, self.rows, self.cells = depth, rows, 1 << depth
+        prm = ws.SyntheticPRM(seed=SEED_T, depth=depth)
+        self.off, self.idx = prm.csr(0, rows)
+        self.m = self.ref.csr_handle(rows, self.cells, self.off, self.idx) if self.kind == "reference" else None
+
+    def query_ms(self, props: int, frame: int, workers: int, seed: int = SEED_P) -> float:
+        """time_label_ms (scenario.cpp:154-165): best of 2 label_all calls on
+        frame `frame`'s P."""
+        import workload.synth as ws
+
+        P = ws.props_words(seed, self.depth, props, frame, 1)[0]
+        if self.kind == "reference":
+            p = self.ref.props_handle(self.cells, props, P)
+            try:
+                return self.ref.time_label_ms(self.m, p, workers, 2)
+            finally:
+                self.ref.free(p=p)
+        best = 1e30
+        for _ in range(2):
+            t0 = time.perf_counter()
+            self.ref.label_all(self.rows, self.cells, self.off, self.idx, self.cells, props, P, workers)
+            best = min(best, (time.perf_counter() - t0) * 1e3)
+        return best
+
+    def protocol(self, props: int, queries: int, workers: int, seed: int = SEED_P):
+        """run_benchmark's protocol (scenario.cpp:176-216): query -1 is a
+        timed-but-discarded warm-up, then `queries` queries, best of 2 each;
+        p50 / mean of the per-query times."""
+        ts = [self.query_ms(props, q + 1, workers, seed) for q in range(-1, queries)][1:]
+        return {"p50_ms": statistics.median(ts), "mean_ms": statistics.mean(ts), "min_ms": min(ts),
+                "queries": queries, "rows": self.rows, "props": props, "workers": workers,
+                "edge_labels_per_s_p50": self.rows / (statistics.median(ts) / 1e3)}
+
+    def close(self):
+        if self.m is not None:
+            self.ref.free(m=self.m)
+            self.m = None
+
+
+def cpu_baseline(quick: bool):
+    """the unmodified reference label_all on the host cores, on
+    bounded slices of the bench's own T (rows [0, n) of the same synthetic
+    PRM), reference protocol, workers = nproc and workers = 1.  Config 4: a
+    500k-row slice, 32 props, one frame per query (the reference has no
+    batching: a 64-frame step is 64 such calls); config 3: the same slice at 16
+    props, its p50 scaled x4 to the 2M rows (linear in rows).
+    workers = 1 runs on a 16k-row slice."""
+    host = host_cpu()
+    q = 5 if quick else 15
+    big = RefSlice(CFG4["depth"], 100_000 if quick else 500_000)
+    c4 = big.protocol(CFG4["props"], q, 0)
+    c3 = big.protocol(CFG3_PROPS, q, 0, seed=SEED_P + 3)
+    big.close()
+    small = RefSlice(CFG4["depth"], 16_000)
+    c4_1 = small.protocol(CFG4["props"], q, 1)
+    small.close()
+    scale3 = CFG4["edges"] / big.rows
+    return {
+        "value": c4["edge_labels_per_s_p50"], "unit": UNIT, "cores": host["hardware_concurrency"], "kind": big.kind,
+        "sample": f"config 4: rows [0,{big.rows}) of the {CFG4['edges']}-edge T, 32 props, p50 over {q} queries "
+                  f"(1 frame each, best of 2, 1 warm-up discarded), workers = nproc",
+        "host": host, "config4": c4, "config4_workers1": c4_1,
+        "config3": dict(c3, p50_ms_2M_extrapolated=c3["p50_ms"] * scale3,
+                        note=f"{big.rows}-row slice; p50 x{scale3:g} for the 2M rows is extrapolated (linear in rows)"),
+    }
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU label_all (oracle/_ref, all
+    host threads) on the bench's workload.  One step = one query of config 4
+    (one frame of 32 props) on a 500k-row slice of the 2M-edge T, best of 2
+    (time_label_ms); value = p50 edge-labels/s over the K steps."""
     if rank != 0:
         return
-    rows, frames = 100_000, 1
-    vals = []
-    for _ in range(args.warmup):
-        cpu_reference_sample(CFG4["depth"], CFG4["props"], 20_000, 1)
+    sl = RefSlice(CFG4["depth"], 500_000)
+    for w in range(args.warmup):
+        sl.query_ms(CFG4["props"], 1000 + w, 0)
     t_all = time.perf_counter()
-    kind = cores = sample = None
-    for _ in range(args.steps):
-        v, kind, cores, sample = cpu_reference_sample(CFG4["depth"], CFG4["props"], rows, frames)
-        vals.append(v)
+    ts = [sl.query_ms(CFG4["props"], k, 0) for k in range(args.steps)]
     wall = time.perf_counter() - t_all
-    value = statistics.median(vals)
+    sl.close()
+    value = sl.rows / (statistics.median(ts) / 1e3)
+    host = host_cpu()
+    sample = (f"config 4: rows [0,{sl.rows}) of the {CFG4['edges']}-edge T, 32 props, one frame per step, best of 2 "
+              f"label_all calls (time_label_ms), p50 over the steps; workers = 0 (hardware_concurrency)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / max(args.steps, 1) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic", "config": cfg_json(world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": host["hardware_concurrency"], "kind": sl.kind,
+                         "sample": sample, "host": host, "p50_query_ms": statistics.median(ts)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def config5_shard(local: int, hbm: float, src: str, quick: bool):
+    """BASELINE config 5 (8M edges, 1024^2 grid, 64 props) on one GPU's shard
+    of the 8-way edge-row partition: rows [0, 1M).  Single-frame p50 latency
+    (pinned host P -> labels in HBM, 150 frames after a warm-up) with the
+    labelling kernel's HBM roofline, and a 64-frame batch (P resident) with
+    the multi-frame kernel's binding roofline; host pack + upload time of the
+    shard."""
+    import torch
+
+    from paper_1810_02612_b200 import LabelEngine
+    from workload.synth import SyntheticPRM, props_words
+
+    depth, props, E = 20, 64, 1_000_000
+    cells, nw = 1 << depth, (1 << depth) // 64
+    T = SyntheticPRM(seed=SEED_T, depth=depth).words(0, E)
+    np64 = pairs64(T.offsets, T.words)
+    eng = LabelEngine(devices=[local], profile=False)
+    t0 = time.perf_counter()
+    eng.load_abstraction_words(E, cells, T.offsets, T.words, T.masks)
+    load_s = time.perf_counter() - t0
+    info = eng.info()
+    del T
+    n = 30 if quick else 150
+    frames = torch.empty((n + 1, props, nw), dtype=torch.int64, pin_memory=True)
+    props_words(SEED_P, depth, props, 0, n + 1, out=frames)
+    lat = []
+    for q in range(-1, n):
+        t0 = time.perf_counter()
+        eng.submit_grid(cells, props, frames[q + 1], 1)
+        eng.wait()
+        if q >= 0:
+            lat.append((time.perf_counter() - t0) * 1e3)
+    eng.set_profiling(True)
+    lab = []
+    for q in range(-1, min(n, 50)):
+        eng.submit_grid(cells, props, frames[q + 1], 1)
+        eng.wait()
+        if q >= 0:
+            lab.append(eng.stage_times(0, 0)[2])
+    k = statistics.median(lab)
+    alg1 = 8 * int(info.words) + 4 * (E + 1) + cells * props // 8 + E * 8
+    single = {"p50_ms": statistics.median(lat), "p99_ms": sorted(lat)[int(0.99 * (len(lat) - 1))], "frames": n,
+              "what": "pinned host P (8 MB) -> labels resident in HBM (host steady clock)", "kernel_p50_ms": k,
+              "roofline": {"bound": "hbm", "achieved": alg1 / (k / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                           "frac": alg1 / (k / 1e3) / 1e9 / hbm, "alg_bytes_per_launch": alg1, "peak_source": src,
+                           "traffic": ncu_traffic("label_stream64_kernel<64>"),
+                           "limiter": ncu_limiter("label_stream64_kernel<64>"),
+                           "kernel": "label_stream64_kernel<64,u64,L1,768>"}}
+    del frames
+    F = 64
+    P = torch.empty((F, props, nw), dtype=torch.int64, device="cuda")
+    Ph = torch.empty((F, props, nw), dtype=torch.int64, pin_memory=True)
+    props_words(SEED_P, depth, props, 0, F, out=Ph)
+    P.copy_(Ph)
+    steps = []
+    for it in range(3 + (3 if quick else 8)):
+        eng.submit_grid_device(cells, props, P.data_ptr(), F)
+        eng.wait()
+        if it >= 3:
+            st = eng.stage_times(0, 0)
+            steps.append((st[1], st[2]))
+    sm = statistics.median(x[0] for x in steps)
+    lm = statistics.median(x[1] for x in steps)
+    algF = 8 * int(info.words) + 4 * (E + 1) + F * (cells * props // 8 + E * 8)
+    batch = {"frames": F, "summary_ms": sm, "label_ms": lm, "edge_labels_per_s": E * F / ((sm + lm) / 1e3),
+             "roofline": {"bound": "hbm", "achieved": algF / (lm / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                          "frac": algF / (lm / 1e3) / 1e9 / hbm, "alg_bytes_per_launch": algF,
+                          "kernel": "label_wm_kernel<u64,2> (word-major, two prop halves)",
+                          "binding": binding_roofline("label_wm_kernel<u64,2>", lm, 1965e6, pairs=np64)}}
+    eng.close()
+    return {"config": "config5-dense-grid-stress, one GPU's shard of 8: rows [0, 1M) of the 8M-edge T, 1024x1024 "
+                      "grid (2^20 cells), 64 props", "rows": E, "W32": int(info.words),
+            "t_bytes_device": int(info.t_bytes), "load_s": load_s, "single_frame": single, "batch64": batch}
 
 
 def cfg_json(world):
@@ -261,6 +433,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 shard block")
     ap.add_argument("--quick", action="store_true", help="short run for profilers")
     ap.add_argument("--dump-labels", default="", help="(tests) write a row sample of each rank's labels "
                     "after the timed steps to <prefix>_rank<r>.npz")
@@ -292,7 +465,7 @@ def main():
         else:
             dist.init_process_group(backend)
     from paper_1810_02612_b200 import LabelEngine
-    from paper_1810_02612_b200.synth import SyntheticPRM, props_words
+    from workload.synth import SyntheticPRM, props_words
 
     E, depth, props, F = CFG4["edges"], CFG4["depth"], CFG4["props"], CFG4["frames"]
     cells = 1 << depth
@@ -305,7 +478,9 @@ def main():
     del T
     rows_local = len(row_ids)
     eng = LabelEngine(devices=[local], profile=True)  # device-resident labels: one block, global z-sort
+    t_load = time.perf_counter()
     eng.load_abstraction_words(rows_local, cells, T_off, T_words, T_masks)
+    load_s = time.perf_counter() - t_load  # host pack of every device layout + upload
     info = eng.info()
     W32_all = torch.tensor([int(info.words), rows_local], dtype=torch.int64, device="cuda")
     if world > 1:
@@ -403,25 +578,18 @@ def main():
     hbm, src = peaks()
     alg_bytes = 8 * int(info.words) + 4 * (rows_local + 1) + F * (cells * props // 8 + rows_local * 4)
     achieved = alg_bytes / (label_ms / 1e3) / 1e9
-    traffic = ncu_traffic("label_pl_kernel")
     sm_clk = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
-    lop3 = float(info.words) * F * props  # one AND-OR per stored T word per prop per frame
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "peak_source": src, "kernel": "label_pl_kernel<u32> (prop-lane multi-frame)",
+                "traffic": ncu_traffic("label_wm_kernel"), "peak_source": src,
+                "kernel": "label_wm_kernel<u32,1> (word-major multi-frame)",
                 "alg_bytes_per_launch": alg_bytes, "kernel_ms": label_ms, "summary_kernel_ms": summary_ms,
-                "note": "algorithmic bytes = 8*W32 + 4*(E+1) + F*(cells*props/8 + E*4); traffic = dram read+write "
-                        "bytes per launch from the committed ncu --set full capture (profiles/traffic.json). The "
-                        "multi-frame kernel is not HBM-bound: ncu shows the L1TEX pipe (record gathers + shared-"
-                        "memory OR reductions) and issue saturated (see int_ops)",
-                "limiter": ncu_limiter("label_pl_kernel"),
-                "int_ops": {"alg_and_or_per_launch": lop3, "achieved_per_s": lop3 / (label_ms / 1e3),
-                            "peak_per_s": lop3_peak(sm_clk),
-                            "peak_source": "profiles/lop3_peak.json (tools/micro/lop3_peak.cu on this B200 model)"
-                            if os.path.exists(os.path.join(ROOT, "profiles", "lop3_peak.json"))
-                            else "assumed 64 LOP3/clk/SM",
-                            "frac": lop3 / (label_ms / 1e3) / lop3_peak(sm_clk),
-                            "note": "SURVEY 8(d) integer roofline W32*F*props AND-ORs at the measured LOP3 rate; > 1 because one "
-                                    "summary entry answers every prop of a (T word, frame) at once"}}
+                "note": "algorithmic bytes = 8*W32 + 4*(E+1) + F*(cells*props/8 + E*4) (SURVEY 8(d)); traffic = dram "
+                        "read+write bytes per launch from the committed ncu --set full capture (profiles/traffic.json). "
+                        "The multi-frame kernel is not HBM-bound; `binding` is the roofline of the algorithm as it "
+                        "runs: the issue slots and the L1TEX data pipe, from the committed capture's per-launch "
+                        "counts over this run's kernel time",
+                "binding": binding_roofline("label_wm_kernel", label_ms, sm_clk, pairs=pairs64(T_off, T_words)),
+                "pairs64": pairs64(T_off, T_words)}
 
     # ---- p50 single-frame latency, config 3 (16 props), host P -> labels in HBM
     lat = None
@@ -501,7 +669,7 @@ def main():
         streams = [torch.cuda.ExternalStream(e.stream()) for e in engs]
         outs = [torch.empty((rows_local, F), dtype=torch.int32, pin_memory=True) for _ in engs]
         Pd = [P_dev, torch.empty_like(P_dev)] if world > 1 else None
-        Ke = max(2, min(K, 6))
+        Ke = max(2, K)  # as many steps as the device-timed `value`
 
         def e2e_submit(k):
             e, st = engs[k % 2], streams[k % 2]
@@ -549,19 +717,25 @@ def main():
                        "later blocks are labelled); two engines alternate steps, so step k+1's upload and "
                        "labelling overlap step k's read-back" % args.readback_chunks}
 
+    cfg5 = None
+    if rank == 0 and world == 1 and not args.no_cfg5:
+        eng.close()  # (the e2e engines and this one are done: free HBM for the config-5 shard)
+        eng = None
+        cfg5 = config5_shard(local, hbm, src, args.quick)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, kind, cores, sample = cpu_reference_sample(depth, props, 20_000 if args.quick else 100_000, 2)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+        cpu = cpu_baseline(args.quick)
 
     if rank == 0:
-        # gpu_launches: our kernels per step = pl_build (the prop-lane summary) and label_pl
+        # gpu_launches: our kernels per step = wm_build (the word-major summary) and label_wm
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u32", "data": "synthetic", "config": cfg_json(world), "clocks": clk.summary(),
             "gpu_launches": 2 * K, "roofline": roofline, "latency": lat, "e2e": e2e, "cpu_baseline": cpu,
-            "shape": {"W32": W32, "rows": rows_all, "t_bytes_device": int(info.t_bytes)},
+            "config5_shard": cfg5,
+            "shape": {"W32": W32, "rows": rows_all, "t_bytes_device": int(info.t_bytes), "load_s": load_s},
         }
         print(json.dumps(line), flush=True)
     # tear the process group down before the engine (and its stream) goes away
@@ -569,7 +743,8 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-    eng.close()
+    if eng is not None:
+        eng.close()
 
 
 if __name__ == "__main__":

@@ -4,7 +4,7 @@ abstractions -- a drop-in for the reference's labeling path
 
   label.LabelEngine   load abstraction -> submit grid -> get labels (C ABI)
   label.label_all     one-shot drop-in for ltlgrid::label_all
-  synth               synthetic T / P of the BASELINE configs
+  (workload.synth     synthetic T / P of the BASELINE configs: not part of the product)
 """
 from .label import (CsrBoolMatrix, DensePropMatrix, DomainError, EdgeLabeling, FootprintSpec, LabelEngine,  # noqa: F401
                     LabelMatrix, LtlgError, OccupancyBitset, ScenarioConfig, SweptVolume, generate_scenario,

@@ -12,7 +12,6 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "_lib")
 GPU_SO = os.path.join(LIB_DIR, "libltlgrid_gpu.so")
-SYNTH_SO = os.path.join(LIB_DIR, "libltlgrid_synth.so")
 
 LTLG_OK, LTLG_EINVAL, LTLG_EFORMAT, LTLG_EIO, LTLG_ECUDA, LTLG_ENCCL, LTLG_ENOMEM, LTLG_ESTATE, LTLG_EDOMAIN = range(9)
 
@@ -73,7 +72,6 @@ class NativeMissing(ImportError):
 
 
 _lib = None
-_synth = None
 
 
 def lib() -> C.CDLL:
@@ -141,23 +139,3 @@ def lib() -> C.CDLL:
     del P32
     _lib = L
     return L
-
-
-def synth() -> C.CDLL:
-    global _synth
-    if _synth is not None:
-        return _synth
-    if not os.path.exists(SYNTH_SO):
-        raise NativeMissing(f"{SYNTH_SO} is not built; run __graft_entry__.build()")
-    S = C.CDLL(SYNTH_SO)
-    u64, i32, vp = C.c_uint64, C.c_int, C.c_void_p
-    S.synth_prm_create.argtypes = [u64, i32, C.c_double, i32]
-    S.synth_prm_create.restype = vp
-    S.synth_prm_free.argtypes = [vp]
-    S.synth_prm_row_words.argtypes = [vp, u64, u64, vp]
-    S.synth_prm_row_cells.argtypes = [vp, u64, u64, vp]
-    S.synth_prm_fill_words.argtypes = [vp, u64, u64, vp, vp, vp]
-    S.synth_prm_fill_cells.argtypes = [vp, u64, u64, vp, vp]
-    S.synth_props.argtypes = [u64, i32, i32, u64, i32, vp]
-    _synth = S
-    return S

@@ -263,6 +263,15 @@ ltlg_status upload_shard(ltlg_ctx* ctx, Shard& s, const PackedShard& p) {
     return LTLG_OK;
 }
 
+// Whether a multi-frame submit may take a 32-cell kernel that reads the
+// shard's 32-cell pair copy: the A/B knobs, or a grid whose worst-case
+// prop-lane / word-major summary needs 32-bit+ record indices (run_label).
+bool env_off(const char* k) { return getenv(k) && atoi(getenv(k)) == 0; }
+bool need_pairs32(uint64_t cols) {
+    const uint64_t nw64 = (cols + 63) / 64;
+    return env_off("LTLG_BATCH64") || env_off("LTLG_PROPLANE") || (nw64 + 1) * 64 * 64 >= (uint64_t(1) << 31);
+}
+
 ltlg_status load_words(ltlg_ctx* ctx, WordCsr& t) {
     ctx->loaded = false;
     ctx->submitted = false;
@@ -292,7 +301,7 @@ ltlg_status load_words(ltlg_ctx* ctx, WordCsr& t) {
         build_shard(t, b[i], b[i + 1], ctx->opts.sort_rows != 0, sentinel, stream_pairs,
                     ctx->opts.batch_task_pairs > 0 ? ctx->opts.batch_task_pairs : 256,
                     ctx->opts.readback_chunks > 1 ? (ctx->opts.readback_chunks < 64 ? ctx->opts.readback_chunks : 64) : 1,
-                    &p, ctx->opts.task_rows > 0 ? std::min(ctx->opts.task_rows, 256) : kWmRows);
+                    &p, ctx->opts.task_rows > 0 ? std::min(ctx->opts.task_rows, 256) : kWmRows, need_pairs32(t.cols));
         ltlg_status st = upload_shard(ctx, ctx->shards[static_cast<size_t>(i)], p);
         if (st != LTLG_OK) return st;
         pairs += p.n_pairs;

@@ -778,7 +778,7 @@ void build_wm_layout(const WordCsr& t, uint64_t row_begin, int wm_rows, PackedSh
 
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
                  uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs, int blocks,
-                 PackedShard* out, int wm_rows) {
+                 PackedShard* out, int wm_rows, bool need_pairs32) {
     const uint64_t R = row_end - row_begin;
     out->row_begin = row_begin;
     out->row_end = row_end;
@@ -813,8 +813,15 @@ void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool so
         pair_off[s + 1] = pair_off[s] + (n ? n : 1);
     }
     out->n_pairs = pair_off[R];
+    // The 32-cell multi-frame copy is read only by the 32-cell kernels: the
+    // A/B knobs (LTLG_BATCH64=0, LTLG_PROPLANE=0) and grids too large for the
+    // prop-lane / word-major summaries (33..64 props).  Otherwise only its
+    // padding is kept (518 MB less HBM and host packing at config 4).
     // padding: no-op head pairs, so the pair after any task is a head (the
     // single-frame kernel closes a task's last row on it)
+    if (!need_pairs32) {
+        out->pairs.assign(kPairPad, Pair{0, sentinel_word | kHead});
+    } else {
     out->pairs.assign(out->n_pairs + kPairPad, Pair{0, sentinel_word | kHead});
     parallel_chunks(R, 1 << 14, [&](uint64_t b, uint64_t e, int) {
         for (uint64_t s = b; s < e; ++s) {
@@ -829,6 +836,7 @@ void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool so
             dst[0].word |= kHead;
         }
     });
+    }
     make_tasks(pair_off, out->block_row, batch_task_pairs, &out->task_row_batch, &out->task_pair_batch,
                &out->block_task_batch);
     build_stream_layout(t, row_begin, row_end, sentinel_word, stream_task_pairs, out);

@@ -26,7 +26,7 @@ if not has_gpu():  # pragma: no cover - collected on CPU-only hosts
 
 from paper_1810_02612_b200 import (CsrBoolMatrix, DensePropMatrix, LabelEngine, LabelMatrix,  # noqa: E402
                                    LtlgError, label_all)
-from paper_1810_02612_b200.synth import CONFIGS, SyntheticPRM, props_words  # noqa: E402
+from workload.synth import CONFIGS, SyntheticPRM, props_words  # noqa: E402
 
 ORACLE = Oracle()
 LABEL_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))

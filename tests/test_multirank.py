@@ -44,7 +44,7 @@ def _worker(rank, world, port, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import bench
     from oracle.oracle import Oracle
-    from paper_1810_02612_b200.synth import SyntheticPRM, props_words
+    from workload.synth import SyntheticPRM, props_words
 
     E, depth, props, F = 9_001, 12, 6, 3
     cells = 1 << depth
@@ -80,7 +80,7 @@ def _worker(rank, world, port, out_dir):
 def test_sharded_labels_equal_single_process(tmp_path, world):
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     from oracle.oracle import Oracle
-    from paper_1810_02612_b200.synth import SyntheticPRM, props_words
+    from workload.synth import SyntheticPRM, props_words
 
     E, depth, props, F = 9_001, 12, 6, 3
     cells = 1 << depth
@@ -105,7 +105,7 @@ def test_shard_rows_partition():
 
 def test_spatial_shard_partition():
     import bench
-    from paper_1810_02612_b200.synth import SyntheticPRM
+    from workload.synth import SyntheticPRM
 
     T = SyntheticPRM(seed=5, depth=14).words(0, 20_000)
     off = T.offsets.astype(np.int64)
@@ -142,7 +142,7 @@ def test_spatial_shard_empty_rows():
 
 
 def test_synthetic_rows_are_row_addressable():
-    from paper_1810_02612_b200.synth import SyntheticPRM
+    from workload.synth import SyntheticPRM
 
     prm = SyntheticPRM(seed=5, depth=14)
     whole = prm.words(0, 3000)

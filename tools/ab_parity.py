@@ -11,7 +11,7 @@ import numpy as np  # noqa: E402
 
 from oracle.oracle import Oracle  # noqa: E402  (checker only)
 from paper_1810_02612_b200 import LabelEngine, LabelMatrix  # noqa: E402
-from paper_1810_02612_b200.synth import SyntheticPRM, props_words  # noqa: E402
+from workload.synth import SyntheticPRM, props_words  # noqa: E402
 
 O = Oracle()
 bad = 0

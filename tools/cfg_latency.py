@@ -18,7 +18,7 @@ def main():
     import torch
 
     from paper_1810_02612_b200 import LabelEngine
-    from paper_1810_02612_b200.synth import CONFIGS, SyntheticPRM, props_words
+    from workload.synth import CONFIGS, SyntheticPRM, props_words
 
     for cfg in [int(x) for x in (sys.argv[1:] or ["1", "2", "3"])]:
         c = CONFIGS[cfg]

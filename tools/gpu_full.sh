@@ -14,10 +14,14 @@ python tools/bench_summary.py $out/${tag}_bench.json
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $out/${tag}_bench_ref.json 2> $out/${tag}_bench_ref.err; echo "ref rc=$?"; cat $out/${tag}_bench_ref.json
 # launch list (cold-cache, serialised): shares only
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/${tag}_launches.csv \
-    python bench.py --quick --steps 3 --warmup 3 --no-cpu-baseline > $out/${tag}_ncu_bench.log 2>&1; echo "ncu launches rc=$?"
-# full capture of the top kernels
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"label_pl|label_batch" -s 2 -c 1 \
-    -o $out/${tag}_batch python bench.py --quick --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $out/${tag}_ncu_batch.log 2>&1; echo "ncu batch rc=$?"
+    python bench.py --quick --steps 3 --warmup 3 --no-cpu-baseline --no-cfg5 > $out/${tag}_ncu_bench.log 2>&1; echo "ncu launches rc=$?"
+# full captures of the labeling kernels (tools/wm_ab.py child mode: the bench's inputs, P resident)
+timeout 900 env WM_CHILD=1 OUT=/tmp/wm.npy ncu --set full --clock-control none --import-source on -k regex:"label_wm|label_pl" -s 2 -c 1 \
+    -o $out/${tag}_batch python tools/wm_ab.py > $out/${tag}_ncu_batch.log 2>&1; echo "ncu batch rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:label_stream -s 5 -c 1 \
     -o $out/${tag}_stream python tools/sweep_stream.py > $out/${tag}_ncu_stream.log 2>&1; echo "ncu stream rc=$?"
+timeout 900 env WM_CHILD=1 CFG=5 OUT=/tmp/wm.npy ncu --set full --clock-control none --import-source on -k regex:"label_wm" -s 2 -c 1 \
+    -o $out/${tag}_cfg5batch python tools/wm_ab.py > $out/${tag}_ncu_cfg5batch.log 2>&1; echo "ncu cfg5 batch rc=$?"
+timeout 900 env WM_CHILD=1 CFG=5 SINGLE=1 OUT=/tmp/wm.npy ncu --set full --clock-control none --import-source on -k regex:"label_stream" -s 3 -c 1 \
+    -o $out/${tag}_cfg5stream python tools/wm_ab.py > $out/${tag}_ncu_cfg5stream.log 2>&1; echo "ncu cfg5 stream rc=$?"
 ls -la $out

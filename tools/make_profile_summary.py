@@ -31,11 +31,14 @@ traffic_path = os.path.join(os.path.dirname(dst), "traffic.json")
 traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
 lim_path = os.path.join(os.path.dirname(dst), "limiters.json")
 limiters = json.load(open(lim_path)) if os.path.exists(lim_path) else {}
-for kind in ("batch", "stream"):
+TITLES = {"batch": "config 4, multi-frame labeling kernel", "stream": "config 3, single-frame labeling kernel",
+          "cfg5batch": "config 5 shard (1M rows, 1024^2, 64 props), 64-frame labeling kernel",
+          "cfg5stream": "config 5 shard (1M rows, 1024^2, 64 props), single-frame labeling kernel"}
+for kind in ("batch", "stream", "cfg5batch", "cfg5stream"):
     rep = f"{src}_{kind}.ncu-rep"
     if not os.path.exists(rep):
         continue
-    lines.append(f"\n## `ncu --set full`: {kind} labeling kernel\n```")
+    lines.append(f"\n## `ncu --set full`: {TITLES[kind]}\n```")
     lines.append(run("python", os.path.join(here, "ncu_brief.py"), rep).rstrip())
     raw = list(csv.reader(io.StringIO(run("ncu", "-i", rep, "--page", "raw", "--csv"))))
     d = dict(zip(raw[0], raw[2]))
@@ -48,7 +51,10 @@ for kind in ("batch", "stream"):
         lines.append(f"  {k:60s} {d.get(k)}")
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     tb = sum(float(d[k]) * scale.get(u[k], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-    name = d["Kernel Name"].split("<")[0].replace("void ", "").split("::")[-1]
+    full_name = d["Kernel Name"]
+    name = full_name.split("<")[0].replace("void ", "").split("::")[-1]
+    if "unsigned long" in full_name:  # the 64-prop instantiations
+        name += "<u64,2>" if "label_wm" in name else "<64>"
     traffic[name] = tb
 
     def pct(k):
@@ -57,7 +63,15 @@ for kind in ("batch", "stream"):
         except (KeyError, ValueError):
             return None
     # what binds the kernel, from the same capture (bench.py reports it next to the roofline)
+    def cnt(k):
+        try:
+            return float(d[k])
+        except (KeyError, ValueError):
+            return None
     limiters[name] = {
+        "warp_insts": cnt("smsp__inst_executed.sum"),
+        "l1_data_pipe_wavefronts": (cnt("l1tex__data_pipe_lsu_wavefronts.avg") or 0) * 148 or None,
+        "kernel_ms_under_ncu": cnt("gpu__time_duration.sum"),
         "l1tex_data_pipe_pct": pct("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
         "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "dram_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),

@@ -13,7 +13,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1810_02612_b200 import LabelEngine  # noqa: E402
-from paper_1810_02612_b200.synth import SyntheticPRM, props_words  # noqa: E402
+from workload.synth import SyntheticPRM, props_words  # noqa: E402
 
 depth, E, props, F = 18, 2_000_000, 32, 64
 prm = SyntheticPRM(1, depth)

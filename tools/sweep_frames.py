@@ -5,7 +5,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1810_02612_b200 import LabelEngine  # noqa: E402
-from paper_1810_02612_b200.synth import SyntheticPRM, props_words  # noqa: E402
+from workload.synth import SyntheticPRM, props_words  # noqa: E402
 
 depth, E, props = 18, 2_000_000, int(os.environ.get("PROPS", "16"))
 prm = SyntheticPRM(1, depth)

@@ -6,6 +6,7 @@ variant's labels.
 
   python tools/wm_ab.py            # all variants, one process each
   CFG=5 python tools/wm_ab.py      # config-5 shard (1M rows, 1024^2, 64 props)
+  WM_CHILD=1 OUT=x.npy [CFG=5] [SINGLE=1] python tools/wm_ab.py   # one variant (profilers)
 """
 import json
 import os
@@ -22,7 +23,7 @@ def run_one():
     import torch
 
     from paper_1810_02612_b200 import LabelEngine
-    from paper_1810_02612_b200.synth import SyntheticPRM, props_words
+    from workload.synth import SyntheticPRM, props_words
 
     cfg = int(os.environ.get("CFG", "4"))
     depth, E, props, F = (18, 2_000_000, 32, 64) if cfg == 4 else (20, 1_000_000, 64, 64)
@@ -32,6 +33,12 @@ def run_one():
     eng = LabelEngine(devices=[0], profile=True, task_rows=int(os.environ.get("ROWS", "0")))
     eng.load_abstraction_words(E, 1 << depth, T.offsets, T.words, T.masks)
     ts, ss = [], []
+    if os.environ.get("SINGLE"):  # single frames (the single-frame kernel), for profilers
+        for it in range(8):
+            eng.submit_grid_device(1 << depth, props, P[it % F].data_ptr(), 1)
+            eng.wait()
+        eng.close()
+        return
     for it in range(12):
         eng.submit_grid_device(1 << depth, props, P.data_ptr(), F)
         eng.wait()

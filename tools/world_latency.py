@@ -26,7 +26,7 @@ def main():
     import torch
 
     from paper_1810_02612_b200 import LabelEngine
-    from paper_1810_02612_b200.synth import SyntheticPRM, props_words
+    from workload.synth import SyntheticPRM, props_words
 
     depth, E, props = 18, 2_000_000, 16
     prm = SyntheticPRM(seed=1, depth=depth)

@@ -1,6 +1,8 @@
-"""Synthetic workloads (libltlgrid_synth.so): the BASELINE configs' T and P.
+"""Synthetic workloads (workload/libltlgrid_synth.so): the BASELINE configs' T and P.
 
-See csrc/synth.cpp for the generator definitions.
+Neither product nor checker: the input generator that the GPU engine, the CPU
+oracle and the reference core all consume, so every arm sees identical T and
+P.  See synth.cpp for the generator definitions.
 Row i of the synthetic PRM depends only on (seed, i), so any row range can be
 regenerated bit-identically -- the CPU oracle / reference time a bounded row
 sample of exactly the rows the GPU labels.
@@ -11,7 +13,40 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _native as N
+import ctypes as C
+import os
+
+SYNTH_SO = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libltlgrid_synth.so")
+_synth = None
+
+
+def use_library(path: str) -> None:
+    """Take the generator from another library that links synth.cpp (the
+    reference arm uses oracle/_ref/libltlgrid_ref.so, so it loads nothing else
+    of the repo).  Call before the first use."""
+    global _synth, SYNTH_SO
+    _synth = None
+    SYNTH_SO = path
+
+
+def _lib() -> C.CDLL:
+    global _synth
+    if _synth is not None:
+        return _synth
+    if not os.path.exists(SYNTH_SO):
+        raise RuntimeError(f"{SYNTH_SO} is not built; run __graft_entry__.build()")
+    S = C.CDLL(SYNTH_SO)
+    u64, i32, vp = C.c_uint64, C.c_int, C.c_void_p
+    S.synth_prm_create.argtypes = [u64, i32, C.c_double, i32]
+    S.synth_prm_create.restype = vp
+    S.synth_prm_free.argtypes = [vp]
+    S.synth_prm_row_words.argtypes = [vp, u64, u64, vp]
+    S.synth_prm_row_cells.argtypes = [vp, u64, u64, vp]
+    S.synth_prm_fill_words.argtypes = [vp, u64, u64, vp, vp, vp]
+    S.synth_prm_fill_cells.argtypes = [vp, u64, u64, vp, vp]
+    S.synth_props.argtypes = [u64, i32, i32, u64, i32, vp]
+    _synth = S
+    return S
 
 # BASELINE.json configs (SURVEY 8(d)): k = 2 grids over 102.4 m x 102.4 m.
 CONFIGS = {
@@ -38,7 +73,7 @@ class SyntheticPRM:
     """Handle on the primitive library of one (seed, depth)."""
 
     def __init__(self, seed: int = 1, depth: int = 18, extent: float = EXTENT, nprim: int = NPRIM):
-        self._S = N.synth()
+        self._S = _lib()
         self.depth = depth
         self.cells = 1 << depth
         self._h = self._S.synth_prm_create(seed, depth, extent, nprim)
@@ -81,5 +116,5 @@ def props_words(seed: int, depth: int, props: int, frame0: int = 0, frames: int 
     if out is None:
         out = np.zeros((frames, props, nw), np.uint64)
     ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
-    N.synth().synth_props(seed, depth, props, frame0, frames, ptr)
+    _lib().synth_props(seed, depth, props, frame0, frames, ptr)
     return out
