@@ -53,7 +53,7 @@ for kind in ("batch", "stream", "cfg5batch", "cfg5stream"):
     tb = sum(float(d[k]) * scale.get(u[k], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     full_name = d["Kernel Name"]
     name = full_name.split("<")[0].replace("void ", "").split("::")[-1]
-    if "unsigned long" in full_name:  # the 64-prop instantiations
+    if "unsigned long" in full_name.split("(")[0]:  # the 64-prop instantiations (template arguments)
         name += "<u64,2>" if "label_wm" in name else "<64>"
     traffic[name] = tb
 
@@ -70,8 +70,10 @@ for kind in ("batch", "stream", "cfg5batch", "cfg5stream"):
             return None
     limiters[name] = {
         "warp_insts": cnt("smsp__inst_executed.sum"),
-        "l1_data_pipe_wavefronts": (cnt("l1tex__data_pipe_lsu_wavefronts.avg") or 0) * 148 or None,
-        "kernel_ms_under_ncu": cnt("gpu__time_duration.sum"),
+        "l1_data_pipe_wavefronts": (cnt("SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg")
+                                    or cnt("l1tex__data_pipe_lsu_wavefronts.avg") or 0) * 148 or None,
+        "kernel_ms_under_ncu": (cnt("gpu__time_duration.sum") or 0) * {"msecond": 1.0, "usecond": 1e-3,
+                                                                       "nsecond": 1e-6}.get(u.get("gpu__time_duration.sum"), 1.0),
         "l1tex_data_pipe_pct": pct("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
         "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "dram_pct": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
