@@ -140,6 +140,7 @@ struct Shard {
     // Any other reader of s.P after a fused submit must not assume the rest.
     // Consumed (reset) by run_label on every path.
     const uint64_t* P_host = nullptr;
+    bool P_resident = true;  // Pdev() holds the last submit's P (not after a fused word-major upload)
     const uint64_t* Pdev() const { return P_in ? P_in : P.ptr; }
     DevBuf<uint8_t> sf;
     DevBuf<uint8_t> labels;
@@ -272,6 +273,21 @@ bool need_pairs32(uint64_t cols) {
     return env_off("LTLG_BATCH64") || env_off("LTLG_PROPLANE") || (nw64 + 1) * 64 * 64 >= (uint64_t(1) << 31);
 }
 
+// One frame: the word-major single-frame kernel, or the stream64 kernel (see run_label).
+bool use_wm1(int props, uint32_t nw64) {
+    const char* k = getenv("LTLG_WM1");
+    if (k) return atoi(k) != 0;
+    return stream64_table_loc(props, nw64) != 1;
+}
+
+// The single-frame 64-cell copy is read only where some prop count takes the
+// stream64 kernel: its smallest (1-prop) split table fits in shared memory,
+// or a dev knob asks for it.
+bool need_stream64(uint64_t cols) {
+    const uint32_t nw64 = static_cast<uint32_t>((cols + 63) / 64);
+    return getenv("LTLG_WM1") || env_off("LTLG_WORDMAJOR") || !use_wm1(1, nw64);
+}
+
 ltlg_status load_words(ltlg_ctx* ctx, WordCsr& t) {
     ctx->loaded = false;
     ctx->submitted = false;
@@ -301,7 +317,8 @@ ltlg_status load_words(ltlg_ctx* ctx, WordCsr& t) {
         build_shard(t, b[i], b[i + 1], ctx->opts.sort_rows != 0, sentinel, stream_pairs,
                     ctx->opts.batch_task_pairs > 0 ? ctx->opts.batch_task_pairs : 256,
                     ctx->opts.readback_chunks > 1 ? (ctx->opts.readback_chunks < 64 ? ctx->opts.readback_chunks : 64) : 1,
-                    &p, ctx->opts.task_rows > 0 ? std::min(ctx->opts.task_rows, 256) : kWmRows, need_pairs32(t.cols));
+                    &p, ctx->opts.task_rows > 0 ? std::min(ctx->opts.task_rows, 256) : kWmRows, need_pairs32(t.cols),
+                    need_stream64(t.cols));
         ltlg_status st = upload_shard(ctx, ctx->shards[static_cast<size_t>(i)], p);
         if (st != LTLG_OK) return st;
         pairs += p.n_pairs;
@@ -424,11 +441,19 @@ ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
     const bool prof = ctx->opts.profile != 0;
     if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
     const size_t pw = static_cast<size_t>(props) * nw64;  // u64 words of one frame's P
+    static const bool wm_ok = !env_off("LTLG_WORDMAJOR");
+    const bool wm1 = wm_ok && s.wm_rows > 0 && use_wm1(props, nw64);  // (as for one frame, frame by frame)
+    if (wm1) CK(s.sf.reserve(pl_work_bytes(props, 1, nw64)), "allocate summary");
     for (int f = 0; f < frames; ++f) {
-        CK(launch_summary64(s.Pdev() + f * pw, props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr, s.ctr.ptr,
-                            static_cast<int>(kCtrStride), s.stream, nullptr,
-                            pl_touched_on() ? s.touched64.ptr : nullptr),
-           "summary kernel");
+        if (wm1)
+            CK(launch_pl(s.Pdev() + f * pw, props, 1, nw64, ctx->cells, s.sf.ptr, s.sf.bytes, s.ctr.ptr,
+                         static_cast<int>(kCtrStride), s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
+               "summary kernel");
+        else
+            CK(launch_summary64(s.Pdev() + f * pw, props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr, s.ctr.ptr,
+                                static_cast<int>(kCtrStride), s.stream, nullptr,
+                                pl_touched_on() ? s.touched64.ptr : nullptr),
+               "summary kernel");
         if (prof && f == 0) CK(cudaEventRecord(s.ev[2], s.stream), "event");
         LaunchArgs a{};
         a.sf = s.sf.ptr;
@@ -448,6 +473,18 @@ ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
         a.task_begin = 0;
         a.ntasks = s.block_task_s.back();
         a.task_ctr = s.ctr.ptr;
+        if (wm1) {
+            a.word_major = 1;
+            a.wm_mask = s.wm_mask.ptr;
+            a.wm_row = s.wm_row.ptr;
+            a.wm_gword = s.wm_gword.ptr;
+            a.wm_gstart = s.wm_gstart.ptr;
+            a.wm_task_row = s.wm_task_row.ptr;
+            a.wm_task_grp = s.wm_task_grp.ptr;
+            a.wm_rows = s.wm_rows;
+            a.perm = s.perm.ptr;
+            a.ntasks = s.block_task_wm.back();
+        }
         CK(launch_label(a, s.stream), "label kernel");
     }
     s.blocks_last = 1;
@@ -472,6 +509,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // can read a stale host buffer
         const uint64_t* const P_host = s.P_host;
         s.P_host = nullptr;
+        s.P_resident = true;
         const size_t lab = s.rows() * static_cast<size_t>(frames) * static_cast<size_t>(ctx->label_bytes);
         CK(s.labels.reserve(lab ? lab : 8), "allocate labels");
         if (props == 0 || s.rows() == 0) {
@@ -525,8 +563,19 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // LTLG_WORDMAJOR=0: the pair-major label_pl_kernel, for A/B runs
         static const bool wm_ok = !getenv("LTLG_WORDMAJOR") || atoi(getenv("LTLG_WORDMAJOR")) != 0;
         const bool wm = wm_ok && s.wm_rows > 0;
+        // one frame: the word-major single-frame kernel (label_wm1_kernel) over
+        // the one-frame prop-lane summary where the stream64 kernel's split
+        // table outgrows shared memory (its per-pair gathers then go to L1 /
+        // L2: cfg-5 shard 0.273 ms vs 0.226 ms); the stream64 kernel otherwise
+        // (cfg 3: 0.094 ms vs 0.141 ms).  Dev knob LTLG_WM1=0/1 forces it.
+        const bool wm1 = wide && wm && props <= 64 && use_wm1(props, nw64);
+        // the fused upload (summary reading pinned P through the mapping) leaves
+        // no device copy of P on the word-major path: the summary holds all the
+        // labelling needs (ltlg_edge_counting then asks for a resubmit)
+        s.P_resident = !(wm1 && P_host);
         const int nslice = pl ? (frames + 63) / 64 : 1;
         CK(s.sf.reserve(pl && wm ? wm_work_bytes(props, nw64)
+                        : wm1 ? pl_work_bytes(props, 1, nw64)
                         : pl ? pl_work_bytes(props, std::min(frames, 64), nw64)
                         : wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32
                         : wide ? split64_table_bytes(props, nw64)
@@ -542,7 +591,11 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         for (int sl = 0; sl < nslice; ++sl) {  // (frame slices: prop-lane path only)
         // balanced slices (65 frames -> 33 + 32, not 64 + 1)
         const int f0 = frames * sl / nslice, nf = pl ? frames * (sl + 1) / nslice - f0 : frames;
-        if (wide)
+        if (wm1)
+            CK(launch_pl(P_host ? P_host : s.Pdev(), props, 1, nw64, ctx->cells, s.sf.ptr, s.sf.bytes, s.ctr.ptr, nctr,
+                         s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
+               "summary kernel");
+        else if (wide)
             CK(launch_summary64(P_host ? P_host : s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr,
                                 s.ctr.ptr, nctr, s.stream, P_host ? s.P.ptr : nullptr,
                                 pl_touched_on() ? s.touched64.ptr : nullptr),
@@ -589,7 +642,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
             a.task_pair_b64 = s.tpair_b64.ptr;
             a.nw64 = nw64;
         }
-        if (pl && wm) {
+        if ((pl && wm) || wm1) {
             a.word_major = 1;
             a.wm_mask = s.wm_mask.ptr;
             a.wm_row = s.wm_row.ptr;
@@ -610,7 +663,8 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // one launch per read-back block for multi-frame submits (their labels are
         // large: rows x frames words); a single frame's labels are small, so it
         // runs as one launch over all tasks (tasks are listed block by block)
-        const std::vector<uint32_t>& bt = single ? s.block_task_s : (pl && wm) ? s.block_task_wm : s.block_task_b;
+        const std::vector<uint32_t>& bt = single ? (wm1 ? s.block_task_wm : s.block_task_s)
+                                          : (pl && wm) ? s.block_task_wm : s.block_task_b;
         const int nb = single || !split ? 1 : static_cast<int>(bt.size() - 1);
         for (int c = 0; c < nb; ++c) {
             a.task_begin = bt[static_cast<size_t>(c)];
@@ -1366,6 +1420,11 @@ ltlg_status ltlg_edge_counting(ltlg_ctx* ctx, int frame, int prop, uint8_t* hit,
     if (prop < 0 || prop >= ctx->props) return set_err(ctx, LTLG_EINVAL, "prop out of range");
     const uint64_t nw64 = (ctx->cells + 63) / 64;
     const size_t colw = (static_cast<size_t>(frame) * ctx->props + static_cast<size_t>(prop)) * nw64;
+    for (Shard& s : ctx->shards)
+        if (!s.P_resident)
+            return set_err(ctx, LTLG_ESTATE,
+                           "the last submit read its pinned P in place and kept no device copy: resubmit the frame "
+                           "from pageable or device memory for edge counting");
     for (Shard& s : ctx->shards) {
         if (s.rows() == 0) continue;
         CK(cudaSetDevice(s.device), "cudaSetDevice");

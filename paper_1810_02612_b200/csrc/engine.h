@@ -123,7 +123,7 @@ bool write_csb1(const char* path, uint64_t rows, uint64_t cols, const uint64_t* 
 std::vector<uint64_t> shard_bounds(const WordCsr& t, int n);
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
                  uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs, int blocks,
-                 PackedShard* out, int wm_rows = kWmRows, bool need_pairs32 = true);
+                 PackedShard* out, int wm_rows = kWmRows, bool need_pairs32 = true, bool need_stream64 = true);
 int host_threads();
 
 }  // namespace ltlg

@@ -1848,10 +1848,16 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
                                                         uint64_t* __restrict__ sfr, uint2* __restrict__ rec_se,
                                                         uint32_t* __restrict__ rec_cursor, uint4* __restrict__ rec,
                                                         uint32_t* __restrict__ task_ctr, int nctr,
-                                                        const uint32_t* __restrict__ touched64) {
+                                                        const uint32_t* __restrict__ touched64,
+                                                        uint64_t* __restrict__ fullw) {
     constexpr int NP = 1 << PSHIFT, WPB = NT / NP;
+    // a programmatically dependent labeling launch may get resident now; it
+    // waits for this grid's completion before reading our outputs
+    asm volatile("griddepcontrol.launch_dependents;");
     __shared__ uint32_t s_cnt[NP][WPB];
     __shared__ uint32_t s_base[WPB];
+    __shared__ uint32_t s_full[WPB][2];  // (fullw) props full in frame 0, per word
+    if (threadIdx.x < 2 * WPB) (&s_full[0][0])[threadIdx.x] = 0;
     const uint32_t gt = blockIdx.x * static_cast<uint32_t>(NT) + threadIdx.x;
     if (gt < static_cast<uint32_t>(nctr)) task_ctr[gt] = 0;
     const uint32_t j = threadIdx.x / WPB, wl = threadIdx.x % WPB;
@@ -1879,7 +1885,12 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
         sfr[o] = any;
     }
     s_cnt[j][wl] = n;
-    __syncthreads();
+    __syncthreads();  // (also orders the s_full zeroing before the ORs)
+    if (fullw) {  // one frame: the word's full-prop mask in one u64 (label_wm1_kernel)
+        if (full & 1u) atomicOr(&s_full[wl][j >> 5], 1u << (j & 31));
+        __syncthreads();
+        if (j == 0 && in) fullw[w] = s_full[wl][0] | static_cast<uint64_t>(s_full[wl][1]) << 32;
+    }
     if (j == 0 && in) {  // per word: exclusive prefix over props, then its segment
         uint32_t run = 0;
         for (int k = 0; k < NP; ++k) {
@@ -2330,6 +2341,120 @@ __global__ void __launch_bounds__(kWmThreads)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Word-major single-frame labelling (<= 64 props), dev knob LTLG_WM1=1: the
+// word-major copy of T (PackedShard::wm_*) against the one-frame prop-lane
+// summary (pl_build_kernel with frames = 1: fullw[w] = the props whose P
+// covers word w, and one record {P lo, P hi, 4 * 64 * (j / 32), 1 << j % 32}
+// per partial prop).  A warp owns a task (<= R rows; its label words in the
+// warp's slice of shared memory) and takes the task's word groups 32 at a
+// time: lane k fetches group k's full mask, record range and first record.
+// The batch's pairs are one contiguous range of T, streamed flat in chunks of
+// 32 (kWm1U chunks in flight); lane i of a chunk finds its pair's group from
+// the group starts in the chunk (one redux.sync.or + popc) and its word data
+// by shuffle: v = full | the bits of the records whose P word meets the
+// pair's mask, ORed into the row's label word(s).
+// ---------------------------------------------------------------------------
+constexpr int kWm1Warps = 8;
+constexpr int kWm1U = 8;  // 32-pair chunks in flight per warp
+
+template <typename SW, int PW>
+__global__ void __launch_bounds__(kWm1Warps * 32)
+    label_wm1_kernel(const uint64_t* __restrict__ emask, const uint8_t* __restrict__ erow,
+                     const uint32_t* __restrict__ gword, const uint32_t* __restrict__ gstart,
+                     const uint32_t* __restrict__ task_row, const uint32_t* __restrict__ task_grp,
+                     uint32_t task_begin, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
+                     const uint64_t* __restrict__ fullw, const uint2* __restrict__ rec_se,
+                     const uint4* __restrict__ rec, const uint32_t* __restrict__ perm, SW* __restrict__ out,
+                     uint32_t ostride) {
+    __shared__ uint32_t s_acc[kWm1Warps][kWmMaxRows * PW];
+    __shared__ uint32_t s_perm[kWm1Warps][kWmMaxRows];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint32_t* acc = s_acc[wib];
+    for (int k = lane; k < kWmMaxRows * PW; k += 32) acc[k] = 0;
+    const uint32_t acc_s = smem_u32(acc);
+    const uint32_t le = 0xffffffffu >> (31 - lane);  // lanes 0..lane
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // (a programmatic dependent of the summary)
+    for (;;) {
+        uint32_t t = 0;
+        if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= ntasks) break;
+        const uint32_t r0 = __ldg(task_row + t), nr = __ldg(task_row + t + 1) - r0;
+        const uint32_t g0 = __ldg(task_grp + t), ng = __ldg(task_grp + t + 1) - g0;
+        for (uint32_t r = lane; r < nr; r += 32)  // the store's row ids, in the background
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s_perm[wib] + r)),
+                         "l"(perm + r0 + r)
+                         : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        for (uint32_t gb = 0; gb < ng; gb += 32) {
+            // lane k: group gb + k's word-level data
+            const uint32_t k = gb + lane;
+            const bool gv = k < ng;
+            const uint32_t wk = gv ? __ldg(gword + g0 + k) : 0u;
+            const uint32_t ek0 = gv ? __ldg(gstart + g0 + k) : 0xffffffffu;
+            const uint64_t fk = gv ? __ldg(fullw + wk) : 0ull;
+            const uint2 sek = gv ? __ldg(rec_se + wk) : make_uint2(0u, 0u);
+            const uint4 rk = sek.y > sek.x ? __ldg(rec + sek.x) : make_uint4(0u, 0u, 0u, 0u);
+            const uint32_t n = ng - gb < 32u ? ng - gb : 32u;
+            const uint32_t E0 = __shfl_sync(0xffffffffu, ek0, 0);
+            const uint32_t E1 = __ldg(gstart + g0 + gb + n);
+            uint32_t gcount = 0;  // groups of the batch started before the chunk
+            for (uint32_t c = E0; c < E1; c += 32 * kWm1U) {
+                uint2 m[kWm1U];
+                uint32_t row[kWm1U];
+#pragma unroll
+                for (int u = 0; u < kWm1U; ++u) {  // kWm1U chunks of T in flight
+                    const uint32_t e = c + 32u * u + lane;
+                    m[u] = e < E1 ? __ldg(reinterpret_cast<const uint2*>(emask + e)) : make_uint2(0u, 0u);
+                    row[u] = e < E1 ? __ldg(erow + e) : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < kWm1U; ++u) {
+                    const uint32_t cu = c + 32u * u;
+                    if (cu >= E1) break;  // (warp-uniform)
+                    const uint32_t d = ek0 - cu;  // lane k's group starts in this chunk iff d < 32
+                    const uint32_t starts = __reduce_or_sync(0xffffffffu, d < 32u ? 1u << d : 0u);
+                    const int gi = static_cast<int>(gcount + __popc(starts & le)) - 1;
+                    gcount += __popc(starts);
+                    uint32_t v0 = __shfl_sync(0xffffffffu, static_cast<uint32_t>(fk), gi);
+                    uint32_t v1 = PW == 2 ? __shfl_sync(0xffffffffu, static_cast<uint32_t>(fk >> 32), gi) : 0u;
+                    const uint32_t px = __shfl_sync(0xffffffffu, rk.x, gi), py = __shfl_sync(0xffffffffu, rk.y, gi);
+                    const uint32_t pz = __shfl_sync(0xffffffffu, rk.z, gi), pw = __shfl_sync(0xffffffffu, rk.w, gi);
+                    const uint32_t s0 = __shfl_sync(0xffffffffu, sek.x, gi), s1 = __shfl_sync(0xffffffffu, sek.y, gi);
+                    if ((m[u].x & px) | (m[u].y & py)) {  // the group's first partial record (zero: none)
+                        if (PW == 1 || pz == 0) v0 |= pw;
+                        else v1 |= pw;
+                    }
+                    for (uint32_t q = s0 + 1; q < s1; ++q) {  // (rare) more partial props on the word
+                        const uint4 r = __ldg(rec + q);
+                        if ((m[u].x & r.x) | (m[u].y & r.y)) {
+                            if (PW == 1 || r.z == 0) v0 |= r.w;
+                            else v1 |= r.w;
+                        }
+                    }
+                    if (cu + lane < E1) {  // (a task's rows are this warp's alone; rows of a group are distinct)
+                        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * row[u] * PW), "r"(v0) : "memory");
+                        if constexpr (PW == 2)
+                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * (row[u] * PW + 1)), "r"(v1)
+                                         : "memory");
+                    }
+                }
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        for (uint32_t r = lane; r < nr; r += 32) {  // lane r stores row r's label
+            uint64_t l = acc[r * PW];
+            if constexpr (PW == 2) l |= static_cast<uint64_t>(acc[r * PW + 1]) << 32;
+            out[static_cast<uint64_t>(s_perm[wib][r]) * ostride] = static_cast<SW>(l);
+#pragma unroll
+            for (int h = 0; h < PW; ++h) acc[r * PW + h] = 0;
+        }
+        __syncwarp();
+    }
+}
+
 // Byte layout of the word-major work buffer: frame-major summaries, word
 // headers, the slot-row cursor, then the lane records (worst case: every
 // (word, prop, frame) partial, one per slot row) + 1 row of padding.
@@ -2384,13 +2509,14 @@ cudaError_t launch_wm_build(const uint64_t* P64, int props, int frames, uint32_t
 // the last probe round.
 struct PlLayout {
     uint64_t nt;  // (nw64 + 1) * pw
-    size_t ffr, sfr, cursor, rec_se, rec, total;
+    size_t ffr, sfr, fullw, cursor, rec_se, rec, total;
     PlLayout(int props, int frames, uint32_t nw64) {
         nt = static_cast<uint64_t>(nw64 + 1) * (props > 32 ? 64u : 32u);
         auto up = [](size_t x, size_t a) { return (x + a - 1) & ~(a - 1); };
         ffr = 0;
         sfr = ffr + nt * 8;
-        cursor = sfr + nt * 8;
+        fullw = sfr + nt * 8;  // one frame: (nw64 + 1) u64 full-prop masks
+        cursor = fullw + (static_cast<size_t>(nw64) + 1) * 8;
         rec_se = up(cursor + 4, 8);
         rec = up(rec_se + (nw64 + 2) * 8, 16);
         total = rec + (nt * static_cast<uint64_t>(frames) + 32) * 16;
@@ -2418,12 +2544,13 @@ cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64,
     const int wpb = kNT >> pshift;
     const uint64_t gw = (static_cast<uint64_t>(nw64) + 1 + wpb - 1) / wpb, gc = (static_cast<uint64_t>(nctr) + kNT - 1) / kNT;
     const unsigned grid = static_cast<unsigned>(gw > gc ? gw : gc);
+    uint64_t* fullw = frames == 1 ? reinterpret_cast<uint64_t*>(wb + L.fullw) : nullptr;
     if (pshift == 5)
         pl_build_kernel<5, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
-                                                  task_ctr, nctr, touched64);
+                                                  task_ctr, nctr, touched64, fullw);
     else
         pl_build_kernel<6, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
-                                                  task_ctr, nctr, touched64);
+                                                  task_ctr, nctr, touched64, fullw);
     return cudaGetLastError();
 }
 
@@ -2473,6 +2600,35 @@ static void launch_wm_label(const LaunchArgs& a, cudaStream_t st) {
         static_cast<SW*>(a.out), a.ostride ? a.ostride : static_cast<uint32_t>(a.frames), a.wm_rows);
 }
 
+template <typename SW, int PW>
+static cudaError_t launch_wm1_label(const LaunchArgs& a, cudaStream_t st) {
+    const PlLayout L(a.props, 1, a.nw64);
+    const uint8_t* wb = static_cast<const uint8_t*>(a.sf);
+    auto kern = label_wm1_kernel<SW, PW>;
+    constexpr size_t smem = 0;
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWm1Warps * 32, smem);
+        if (per_sm <= 0) per_sm = 1;
+    }
+    // programmatic dependent launch: the CTAs get resident while the summary
+    // kernel finishes (label_wm1_kernel waits on it first)
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = a.pdl ? 1 : 0;
+    cfg.gridDim = dim3(static_cast<unsigned>(sm_count() * per_sm));
+    cfg.blockDim = dim3(kWm1Warps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a.wm_mask, a.wm_row, a.wm_gword, a.wm_gstart, a.wm_task_row, a.wm_task_grp,
+                              a.task_begin, a.ntasks, a.task_ctr, reinterpret_cast<const uint64_t*>(wb + L.fullw),
+                              reinterpret_cast<const uint2*>(wb + L.rec_se), reinterpret_cast<const uint4*>(wb + L.rec),
+                              a.perm, static_cast<SW*>(a.out), a.ostride ? a.ostride : 1u);
+}
+
 template <int FMT, typename SW, int FPL, bool FULL>
 static void launch_batch_t(const LaunchArgs& a, cudaStream_t st) {
     static int per_sm = 0;
@@ -2499,7 +2655,14 @@ static void launch_batch_fpl(const LaunchArgs& a, cudaStream_t st) {
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
     if (a.ntasks <= a.task_begin) return cudaSuccess;
     cudaError_t e = cudaSuccess;
-    if (a.prop_lane && a.word_major) {  // word-major multi-frame path (<= 64 props, a slice of <= 64 frames)
+    if (a.frames == 1 && a.word_major) {  // word-major single-frame path (<= 64 props)
+        switch (a.label_bytes) {
+            case 1: e = launch_wm1_label<uint8_t, 1>(a, st); break;
+            case 2: e = launch_wm1_label<uint16_t, 1>(a, st); break;
+            case 4: e = launch_wm1_label<uint32_t, 1>(a, st); break;
+            default: e = launch_wm1_label<uint64_t, 2>(a, st); break;
+        }
+    } else if (a.prop_lane && a.word_major) {  // word-major multi-frame path (<= 64 props, a slice of <= 64 frames)
         switch (a.label_bytes) {
             case 1: launch_wm_label<uint8_t, 1>(a, st); break;
             case 2: launch_wm_label<uint16_t, 1>(a, st); break;

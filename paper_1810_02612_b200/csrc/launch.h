@@ -74,6 +74,9 @@ cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint
                              uint32_t* task_ctr, int nctr, cudaStream_t st, uint64_t* P_copy,
                              const uint32_t* touched64 = nullptr);
 bool stream_table_in_smem(int props, uint32_t nw32);
+// where label_stream64_kernel keeps its split table: 1 = all in shared
+// memory, 2 = M in shared memory / X through L1, 0 = all through L1
+int stream64_table_loc(int props, uint32_t nw64);
 cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st);
 cudaError_t launch_extract(const void* labels, int label_bytes, uint64_t rows, int frames, int frame,
                            uint64_t* out, cudaStream_t st);

@@ -778,7 +778,7 @@ void build_wm_layout(const WordCsr& t, uint64_t row_begin, int wm_rows, PackedSh
 
 void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool sort_rows,
                  uint32_t sentinel_word, int stream_task_pairs, int batch_task_pairs, int blocks,
-                 PackedShard* out, int wm_rows, bool need_pairs32) {
+                 PackedShard* out, int wm_rows, bool need_pairs32, bool need_stream64) {
     const uint64_t R = row_end - row_begin;
     out->row_begin = row_begin;
     out->row_end = row_end;
@@ -840,7 +840,14 @@ void build_shard(const WordCsr& t, uint64_t row_begin, uint64_t row_end, bool so
     make_tasks(pair_off, out->block_row, batch_task_pairs, &out->task_row_batch, &out->task_pair_batch,
                &out->block_task_batch);
     build_stream_layout(t, row_begin, row_end, sentinel_word, stream_task_pairs, out);
-    build_stream64_layout(t, row_begin, sentinel_word / 2, out);  // sentinel_word = nw32 = 2 * nw64
+    if (need_stream64) {
+        build_stream64_layout(t, row_begin, sentinel_word / 2, out);  // sentinel_word = nw32 = 2 * nw64
+    } else {  // (no prop count takes the stream64 kernel on this grid: padding only)
+        const size_t nt = out->task_row_stream.size() - 1;
+        out->task_n64.assign(nt, 0);
+        out->task_byte64.assign(nt + 1, 0);
+        out->stream64.assign(kPad64Bytes, 0);
+    }
     build_batch64_layout(t, row_begin, sentinel_word / 2, out);
     build_wm_layout(t, row_begin, wm_rows, out);
 }

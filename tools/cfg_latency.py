@@ -2,7 +2,7 @@
 events off) of BASELINE configs 1-3 (host clock, 150 frames after a warm-up),
 plus the stage breakdown from a profiled pass.
 
-  python tools/cfg_latency.py [1 2 3]
+  python tools/cfg_latency.py [1 2 3 5]     (5: the 1M-row per-GPU shard)
 """
 import os
 import statistics
@@ -23,6 +23,8 @@ def main():
     for cfg in [int(x) for x in (sys.argv[1:] or ["1", "2", "3"])]:
         c = CONFIGS[cfg]
         depth, E, props = c["depth"], c["edges"], c["props"]
+        if cfg == 5:
+            E //= 8  # one GPU's shard of the 8-way row partition
         prm = SyntheticPRM(seed=1, depth=depth)
         T = prm.words(0, E)
         eng = LabelEngine(devices=[0], profile=False)
