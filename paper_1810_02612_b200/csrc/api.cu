@@ -131,7 +131,18 @@ struct Shard {
     DevBuf<uint32_t> tn64;
     DevBuf<uint32_t> perm, trow_s, trow_b;
     DevBuf<uint64_t> tpair_s, tpair_b;
-    DevBuf<uint64_t> P;  // frames x props x nw64
+    // P (frames x props x nw64) is double-buffered: each submit takes the
+    // buffer the previous submit did not read (rotate_P), so the upload /
+    // broadcast of submit k+1 on the comm stream overlaps the labelling of
+    // submit k; a buffer's read_done event (recorded after the labelling that
+    // read it) gates its refill.
+    struct PBuf {
+        DevBuf<uint64_t> b;
+        cudaEvent_t read_done = nullptr;
+    };
+    PBuf pb, pb_alt;               // pb = this submit's P
+    cudaStream_t comm = nullptr;   // P upload (shard 0) and broadcast
+    cudaEvent_t src_ready = nullptr, p_ready = nullptr;
     const uint64_t* P_in = nullptr;  // caller's device P used in place (single device)
     // caller's pinned host P, device-mapped: the single-frame summary kernel
     // reads it over PCIe and writes the device copy as it goes (no separate H2D).
@@ -141,7 +152,7 @@ struct Shard {
     // Consumed (reset) by run_label on every path.
     const uint64_t* P_host = nullptr;
     bool P_resident = true;  // Pdev() holds the last submit's P (not after a fused word-major upload)
-    const uint64_t* Pdev() const { return P_in ? P_in : P.ptr; }
+    const uint64_t* Pdev() const { return P_in ? P_in : pb.b.ptr; }
     DevBuf<uint8_t> sf;
     DevBuf<uint8_t> labels;
     DevBuf<uint64_t> stage;
@@ -346,44 +357,66 @@ ltlg_status check_grid(ltlg_ctx* ctx, uint64_t cells, int num_props, int frames)
     return LTLG_OK;
 }
 
-// Broadcast shard 0's P to the other devices (NCCL over NVLink when loaded).
-ltlg_status broadcast_P(ltlg_ctx* ctx, size_t words) {
+// Every submit: take the P buffer the previous submit did not read, sized
+// for `bytes` (the caller then fills shard 0's, and broadcast_P the others).
+ltlg_status rotate_P(ltlg_ctx* ctx, size_t bytes) {
+    for (Shard& s : ctx->shards) {
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        std::swap(s.pb, s.pb_alt);
+        if (bytes) CK(s.pb.b.reserve(bytes), "allocate P");
+    }
+    return LTLG_OK;
+}
+
+// Shard 0's P (written on stream `src` of device 0) to every shard's P
+// buffer, on the comm streams: NCCL broadcast over NVLink when the devices
+// are distinct, peer copies otherwise.  Each comm stream first waits for the
+// labelling that last read its buffer (read_done); each shard's labelling
+// stream then waits for its broadcast (p_ready).  So the broadcast of
+// submit k+1 runs while submit k labels.
+ltlg_status broadcast_P(ltlg_ctx* ctx, size_t words, cudaStream_t src) {
     const int n = static_cast<int>(ctx->shards.size());
-    if (n == 1 || words == 0) return LTLG_OK;
     Shard& s0 = ctx->shards[0];
+    if (words == 0 || (n == 1 && src == s0.stream)) return LTLG_OK;
     CK(cudaSetDevice(s0.device), "cudaSetDevice");
-    cudaEvent_t ready;
-    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
-    CK(cudaEventRecord(ready, s0.stream), "event");
-    for (int i = 1; i < n; ++i) {
+    CK(cudaEventRecord(s0.src_ready, src), "event");
+    for (int i = 0; i < n; ++i) {
         Shard& s = ctx->shards[static_cast<size_t>(i)];
         CK(cudaSetDevice(s.device), "cudaSetDevice");
-        CK(cudaStreamWaitEvent(s.stream, ready, 0), "stream wait");
+        if (src != s.comm) CK(cudaStreamWaitEvent(s.comm, s0.src_ready, 0), "stream wait");
+        CK(cudaStreamWaitEvent(s.comm, s.pb.read_done, 0), "stream wait");
     }
-    if (!ctx->comms.empty()) {
-        Nccl& N = nccl();
-        N.GroupStart();
-        for (int i = 0; i < n; ++i) {
-            Shard& s = ctx->shards[static_cast<size_t>(i)];
-            cudaSetDevice(s.device);
-            ncclResult_t r = N.Broadcast(s0.P.ptr, s.P.ptr, words, ncclUint64, 0, ctx->comms[static_cast<size_t>(i)],
-                                         s.stream);
-            if (r != ncclSuccess) {
-                N.GroupEnd();
-                return set_err(ctx, LTLG_ENCCL, std::string("ncclBroadcast: ") + N.GetErrorString(r));
+    if (n > 1) {
+        if (!ctx->comms.empty()) {
+            Nccl& N = nccl();
+            N.GroupStart();
+            for (int i = 0; i < n; ++i) {
+                Shard& s = ctx->shards[static_cast<size_t>(i)];
+                cudaSetDevice(s.device);
+                ncclResult_t r = N.Broadcast(s0.pb.b.ptr, s.pb.b.ptr, words, ncclUint64, 0,
+                                             ctx->comms[static_cast<size_t>(i)], s.comm);
+                if (r != ncclSuccess) {
+                    N.GroupEnd();
+                    return set_err(ctx, LTLG_ENCCL, std::string("ncclBroadcast: ") + N.GetErrorString(r));
+                }
+            }
+            ncclResult_t r = N.GroupEnd();
+            if (r != ncclSuccess) return set_err(ctx, LTLG_ENCCL, std::string("ncclGroupEnd: ") + N.GetErrorString(r));
+        } else {
+            for (int i = 1; i < n; ++i) {
+                Shard& s = ctx->shards[static_cast<size_t>(i)];
+                CK(cudaSetDevice(s.device), "cudaSetDevice");
+                CK(cudaMemcpyPeerAsync(s.pb.b.ptr, s.device, s0.pb.b.ptr, s0.device, words * 8, s.comm), "peer copy");
             }
         }
-        ncclResult_t r = N.GroupEnd();
-        if (r != ncclSuccess) return set_err(ctx, LTLG_ENCCL, std::string("ncclGroupEnd: ") + N.GetErrorString(r));
-    } else {
-        for (int i = 1; i < n; ++i) {
-            Shard& s = ctx->shards[static_cast<size_t>(i)];
-            CK(cudaSetDevice(s.device), "cudaSetDevice");
-            CK(cudaMemcpyPeerAsync(s.P.ptr, s.device, s0.P.ptr, s0.device, words * 8, s.stream), "peer copy");
-        }
+    }
+    for (int i = 0; i < n; ++i) {
+        Shard& s = ctx->shards[static_cast<size_t>(i)];
+        CK(cudaSetDevice(s.device), "cudaSetDevice");
+        CK(cudaEventRecord(s.p_ready, s.comm), "event");
+        CK(cudaStreamWaitEvent(s.stream, s.p_ready, 0), "stream wait");
     }
     cudaSetDevice(s0.device);
-    cudaEventDestroy(ready);
     return LTLG_OK;
 }
 
@@ -520,6 +553,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
                 const ltlg_status gst = run_guards(ctx, s);
                 if (gst != LTLG_OK) return gst;
             }
+            CK(cudaEventRecord(s.pb.read_done, s.stream), "event");
             continue;
         }
         const uint32_t nw64 = nw32 / 2;
@@ -527,7 +561,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         static const bool wide_ok = !getenv("LTLG_STREAM64") || atoi(getenv("LTLG_STREAM64")) != 0;
         const bool wide = wide_ok && frames == 1;
         if (P_host && !wide)  // the fused upload only exists on the single-frame 64-cell path
-            CK(cudaMemcpyAsync(s.P.ptr, P_host, static_cast<size_t>(frames) * props * nw64 * 8,
+            CK(cudaMemcpyAsync(s.pb.b.ptr, P_host, static_cast<size_t>(frames) * props * nw64 * 8,
                                cudaMemcpyHostToDevice, s.stream),
                "upload P");
         // Few frames: the frame-per-lane multi-frame kernel would leave most
@@ -546,6 +580,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         if (wide_ok && frames > 1 && frames <= small_frames) {
             const ltlg_status fst = run_label_per_frame(ctx, s, nw64);
             if (fst != LTLG_OK) return fst;
+            CK(cudaEventRecord(s.pb.read_done, s.stream), "event");  // (the labelling is done with this P buffer)
             continue;
         }
         static const bool wide_b_ok = !getenv("LTLG_BATCH64") || atoi(getenv("LTLG_BATCH64")) != 0;
@@ -597,7 +632,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
                "summary kernel");
         else if (wide)
             CK(launch_summary64(P_host ? P_host : s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr,
-                                s.ctr.ptr, nctr, s.stream, P_host ? s.P.ptr : nullptr,
+                                s.ctr.ptr, nctr, s.stream, P_host ? s.pb.b.ptr : nullptr,
                                 pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (pl && wm)
@@ -681,6 +716,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         }
         if (prof) CK(cudaEventRecord(s.ev[3], s.stream), "event");
         s.have_times = prof;
+        CK(cudaEventRecord(s.pb.read_done, s.stream), "event");  // (the labelling is done with this P buffer)
     }
     ctx->submitted = true;
     return LTLG_OK;
@@ -699,10 +735,7 @@ ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t*
     // A single-device engine reads a device-resident P in place (no copy);
     // the caller keeps it alive and unmodified until the labels are ready.
     const bool in_place = on_device && ctx->shards.size() == 1;
-    for (Shard& s : ctx->shards) {
-        CK(cudaSetDevice(s.device), "cudaSetDevice");
-        if (!in_place) CK(s.P.reserve(nwords * 8 + 16), "allocate P");
-    }
+    if ((st = rotate_P(ctx, in_place ? 0 : nwords * 8 + 16)) != LTLG_OK) return st;
     if (ctx->opts.profile)
         for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
     Shard& s0 = ctx->shards[0];
@@ -722,11 +755,15 @@ ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t*
         else
             cudaGetLastError();  // pageable memory: not an error, just no mapping
     }
-    if (nwords && !in_place && !s0.P_host)
-        CK(cudaMemcpyAsync(s0.P.ptr, words, nwords * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                           s0.stream),
+    cudaStream_t src = s0.stream;
+    if (nwords && !in_place && !s0.P_host) {  // the upload on the comm stream, once the buffer is free
+        src = s0.comm;
+        CK(cudaStreamWaitEvent(src, s0.pb.read_done, 0), "stream wait");
+        CK(cudaMemcpyAsync(s0.pb.b.ptr, words, nwords * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           src),
            "upload P");
-    if ((st = broadcast_P(ctx, nwords)) != LTLG_OK) return st;
+    }
+    if ((st = broadcast_P(ctx, nwords, src)) != LTLG_OK) return st;
     if (ctx->opts.profile)
         for (size_t i = 1; i < ctx->shards.size(); ++i) {
             cudaSetDevice(ctx->shards[i].device);
@@ -779,6 +816,11 @@ ltlg_status ltlg_create_ex(const int* devices, int n_devices, const ltlg_options
             return set_err(nullptr, LTLG_ECUDA, "device " + std::to_string(d) + " is not sm_100 (built for B200 only)");
         if ((e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking)) != cudaSuccess)
             return cuda_fail(nullptr, e, "stream");
+        if ((e = cudaStreamCreateWithFlags(&s.comm, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(nullptr, e, "stream");
+        for (cudaEvent_t* ev : {&s.pb.read_done, &s.pb_alt.read_done, &s.src_ready, &s.p_ready})
+            if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(nullptr, e, "event");
         if (ctx->opts.profile) {
             s.ring.assign(Shard::kRing * 4, nullptr);
             for (auto& ev : s.ring)
@@ -839,7 +881,11 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.trow_b.release();
         s.tpair_s.release();
         s.tpair_b.release();
-        s.P.release();
+        s.pb.b.release();
+        s.pb_alt.b.release();
+        for (cudaEvent_t ev : {s.pb.read_done, s.pb_alt.read_done, s.src_ready, s.p_ready})
+            if (ev) cudaEventDestroy(ev);
+        if (s.comm) cudaStreamDestroy(s.comm);
         s.sf.release();
         s.labels.release();
         s.stage.release();
@@ -942,10 +988,7 @@ ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, con
     const size_t wwords = static_cast<size_t>(num_props) * ((wcells + 63) / 64);
     const size_t vwords = static_cast<size_t>(frames) * num_props * ((cells + 63) / 64);
     if (wwords && !world_words) return set_err(ctx, LTLG_EINVAL, "null world_words");
-    for (Shard& s : ctx->shards) {
-        CK(cudaSetDevice(s.device), "cudaSetDevice");
-        CK(s.P.reserve(vwords * 8 + 16), "allocate P");
-    }
+    if ((st = rotate_P(ctx, vwords * 8 + 16)) != LTLG_OK) return st;
     if (ctx->opts.profile)
         for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
     Shard& s0 = ctx->shards[0];
@@ -965,11 +1008,11 @@ ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, con
     CK(launch_resample(vehicle->depth, vehicle->lo0, vehicle->hi0, vehicle->lo1, vehicle->hi1, world->depth, world->lo0,
                        world->hi0, world->lo1, world->hi1, s0.poses.ptr, frames, num_props,
                        reinterpret_cast<const uint32_t*>(wsrc), nw32_of(wcells), outside ? 1 : 0, nw32_of(cells),
-                       reinterpret_cast<uint32_t*>(s0.P.ptr), s0.stream),
+                       reinterpret_cast<uint32_t*>(s0.pb.b.ptr), s0.stream),
        "resample kernel");
     // pageable pose upload must complete before the caller's buffer may change
     CK(cudaStreamSynchronize(s0.stream), "resample");
-    if ((st = broadcast_P(ctx, vwords)) != LTLG_OK) return st;
+    if ((st = broadcast_P(ctx, vwords, s0.stream)) != LTLG_OK) return st;
     return run_label(ctx, !words_on_device);
 }
 
@@ -1127,14 +1170,14 @@ ltlg_status ltlg_rasterize_boxes(const ltlg_gridk* grid, int num_cols, const uin
     std::unique_ptr<ltlg_ctx, void (*)(ltlg_ctx*)> hold(ctx, ltlg_destroy);
     Shard& s0 = ctx->shards[0];
     const size_t nw = ((uint64_t(1) << grid->depth) + 63) / 64;
-    CK(s0.P.reserve(static_cast<size_t>(num_cols) * nw * 8 + 8), "allocate P");
-    st = rasterize_on(ctx, grid, num_cols, box_offsets, box_lo, box_hi, s0.poses_off, s0.box_rng, s0.P.ptr, s0.stream);
+    CK(s0.world.reserve(static_cast<size_t>(num_cols) * nw * 8 + 8), "allocate P");  // (scratch: not a submit's P)
+    st = rasterize_on(ctx, grid, num_cols, box_offsets, box_lo, box_hi, s0.poses_off, s0.box_rng, s0.world.ptr, s0.stream);
     if (st != LTLG_OK) {
         g_error = ctx->err;
         return st;
     }
     if (num_cols) {
-        cudaError_t e = cudaMemcpy(out_words, s0.P.ptr, static_cast<size_t>(num_cols) * nw * 8, cudaMemcpyDeviceToHost);
+        cudaError_t e = cudaMemcpy(out_words, s0.world.ptr, static_cast<size_t>(num_cols) * nw * 8, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) return cuda_fail(nullptr, e, "download P");
     }
     return LTLG_OK;
@@ -1156,20 +1199,17 @@ ltlg_status ltlg_submit_boxes(ltlg_ctx* ctx, const ltlg_gridk* grid, int num_pro
     ctx->frames = frames;
     ctx->label_bytes = label_bytes_for(num_props);
     const size_t nwords = static_cast<size_t>(cols) * ((cells + 63) / 64);
-    for (Shard& s : ctx->shards) {
-        CK(cudaSetDevice(s.device), "cudaSetDevice");
-        CK(s.P.reserve(nwords * 8 + 16), "allocate P");
-    }
+    if ((st = rotate_P(ctx, nwords * 8 + 16)) != LTLG_OK) return st;
     if (ctx->opts.profile)
         for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
     Shard& s0 = ctx->shards[0];
     CK(cudaSetDevice(s0.device), "cudaSetDevice");
     s0.P_in = nullptr;
     if (ctx->opts.profile) CK(cudaEventRecord(s0.ev[0], s0.stream), "event");
-    if ((st = rasterize_on(ctx, grid, cols, box_offsets, box_lo, box_hi, s0.poses_off, s0.box_rng, s0.P.ptr, s0.stream)) !=
+    if ((st = rasterize_on(ctx, grid, cols, box_offsets, box_lo, box_hi, s0.poses_off, s0.box_rng, s0.pb.b.ptr, s0.stream)) !=
         LTLG_OK)
         return st;
-    if ((st = broadcast_P(ctx, nwords)) != LTLG_OK) return st;
+    if ((st = broadcast_P(ctx, nwords, s0.stream)) != LTLG_OK) return st;
     return run_label(ctx, false);
 }
 
@@ -1307,12 +1347,12 @@ ltlg_status ltlg_generate_scenario(const ltlg_scenario* cfg, const ltlg_gridk* g
     std::unique_ptr<ltlg_ctx, void (*)(ltlg_ctx*)> hold(ctx, ltlg_destroy);
     Shard& s0 = ctx->shards[0];
     const size_t nw = ((uint64_t(1) << grid->depth) + 63) / 64;
-    CK(s0.P.reserve(2 * nw * 8 + 8), "allocate P");
-    if ((st = scenario_on(ctx, cfg, grid, query_index, 1, s0, s0.P.ptr)) != LTLG_OK) {
+    CK(s0.world.reserve(2 * nw * 8 + 8), "allocate P");  // (scratch: not a submit's P)
+    if ((st = scenario_on(ctx, cfg, grid, query_index, 1, s0, s0.world.ptr)) != LTLG_OK) {
         g_error = ctx->err;
         return st;
     }
-    cudaError_t e = cudaMemcpy(out_words, s0.P.ptr, 2 * nw * 8, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(out_words, s0.world.ptr, 2 * nw * 8, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(nullptr, e, "download P");
     return LTLG_OK;
 }
@@ -1331,10 +1371,7 @@ ltlg_status ltlg_submit_scenario(ltlg_ctx* ctx, const ltlg_scenario* cfg, const 
     ctx->frames = frames;
     ctx->label_bytes = label_bytes_for(2);
     const size_t nwords = static_cast<size_t>(frames) * 2 * ((cells + 63) / 64);
-    for (Shard& s : ctx->shards) {
-        CK(cudaSetDevice(s.device), "cudaSetDevice");
-        CK(s.P.reserve(nwords * 8 + 16), "allocate P");
-    }
+    if ((st = rotate_P(ctx, nwords * 8 + 16)) != LTLG_OK) return st;
     if (ctx->opts.profile)
         for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
     Shard& s0 = ctx->shards[0];
@@ -1342,8 +1379,8 @@ ltlg_status ltlg_submit_scenario(ltlg_ctx* ctx, const ltlg_scenario* cfg, const 
     s0.P_in = nullptr;
     s0.P_host = nullptr;
     if (ctx->opts.profile) CK(cudaEventRecord(s0.ev[0], s0.stream), "event");
-    if ((st = scenario_on(ctx, cfg, grid, query_index0, frames, s0, s0.P.ptr)) != LTLG_OK) return st;
-    if ((st = broadcast_P(ctx, nwords)) != LTLG_OK) return st;
+    if ((st = scenario_on(ctx, cfg, grid, query_index0, frames, s0, s0.pb.b.ptr)) != LTLG_OK) return st;
+    if ((st = broadcast_P(ctx, nwords, s0.stream)) != LTLG_OK) return st;
     return run_label(ctx, false);
 }
 

@@ -870,3 +870,44 @@ def test_apply_labels_vs_reference(props):
     with pytest.raises(ValueError, match=f"^label matrix props {props} vs alphabet size {props + 1}$"):
         eng.apply_labels(r, props + 1)
     eng.close()
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+def test_double_buffered_P_bursts(devices):
+    """P is double-buffered per shard (rotate_P): a submit's upload /
+    broadcast runs on the comm stream while the previous submit labels, gated
+    by the read_done event of the buffer it refills.  Bursts of submits
+    without a wait in between (pageable, pinned and device P, several frame
+    counts) must leave exactly the last submit's labels."""
+    import torch
+
+    rng = np.random.default_rng(len(devices))
+    r, c = 4000, 64 * 70 + 5
+    rows = rng.random((r, c)) < 0.01
+    off, idx = to_csr(rows)
+    eng = LabelEngine(devices=devices)
+    eng.load_abstraction(CsrBoolMatrix(r, c, off, idx))
+    nw = (c + 63) // 64
+    for burst in range(6):
+        props = int(rng.choice([3, 17, 40]))
+        Ps = []
+        for k in range(int(rng.integers(2, 5))):
+            frames = int(rng.choice([1, 3, 20]))
+            P = rng.integers(0, 2**63, size=(frames, props, nw), dtype=np.uint64)
+            P[:, :, ::4] &= np.uint64(0x0101010101010101)
+            P[:, :, 1::7] = np.uint64(0xFFFFFFFFFFFFFFFF)
+            kind = (burst + k) % 3
+            if kind == 0:
+                eng.submit_grid(c, props, P, frames)
+            elif kind == 1:
+                eng.submit_grid(c, props, torch.from_numpy(P.view(np.int64).copy()).pin_memory(), frames)
+            else:
+                dev = torch.from_numpy(P.view(np.int64).copy()).cuda()
+                eng.submit_grid_device(c, props, dev.data_ptr(), frames)
+                Ps.append(dev)  # (kept alive until the labels are read)
+            Ps.append(P)
+        P = Ps[-1] if isinstance(Ps[-1], np.ndarray) else Ps[-2]
+        for f in range(P.shape[0]):
+            want = ORACLE.label_all(r, c, off, idx, c, props, P[f])
+            assert eng.get_labels(f) == LabelMatrix(r, props, want), (burst, f)
+    eng.close()
