@@ -609,7 +609,12 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // labelling needs (ltlg_edge_counting then asks for a resubmit)
         s.P_resident = !(wm1 && P_host);
         const int nslice = pl ? (frames + 63) / 64 : 1;
-        CK(s.sf.reserve(pl && wm ? wm_work_bytes(props, nw64)
+        // dev knob LTLG_TC=1: the tcgen05 kind::i8 formulation (tc_i8.cu) on
+        // the word-major copy instead of label_wm_kernel (measured, not kept)
+        static const bool tc_on = getenv("LTLG_TC") && atoi(getenv("LTLG_TC")) != 0;
+        const bool tc = pl && wm && tc_on && s.wm_rows <= 128;
+        CK(s.sf.reserve(tc ? tc_work_bytes(nw64)
+                        : pl && wm ? wm_work_bytes(props, nw64)
                         : wm1 ? pl_work_bytes(props, 1, nw64)
                         : pl ? pl_work_bytes(props, std::min(frames, 64), nw64)
                         : wide_b ? static_cast<size_t>(nw64 + 1) * frames * 32
@@ -634,6 +639,10 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
             CK(launch_summary64(P_host ? P_host : s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr,
                                 s.ctr.ptr, nctr, s.stream, P_host ? s.pb.b.ptr : nullptr,
                                 pl_touched_on() ? s.touched64.ptr : nullptr),
+               "summary kernel");
+        else if (tc)
+            CK(launch_tc_build(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.sf.ptr,
+                               s.ctr.ptr, nctr, s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (pl && wm)
             CK(launch_wm_build(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.sf.ptr,
@@ -679,6 +688,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         }
         if ((pl && wm) || wm1) {
             a.word_major = 1;
+            a.tc = tc ? 1 : 0;
             a.wm_mask = s.wm_mask.ptr;
             a.wm_row = s.wm_row.ptr;
             a.wm_gword = s.wm_gword.ptr;

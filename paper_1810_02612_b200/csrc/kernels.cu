@@ -2662,6 +2662,8 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
             case 4: e = launch_wm1_label<uint32_t, 1>(a, st); break;
             default: e = launch_wm1_label<uint64_t, 2>(a, st); break;
         }
+    } else if (a.prop_lane && a.word_major && a.tc) {  // dev knob LTLG_TC=1: tcgen05 kind::i8
+        e = launch_tc_label(a, st);
     } else if (a.prop_lane && a.word_major) {  // word-major multi-frame path (<= 64 props, a slice of <= 64 frames)
         switch (a.label_bytes) {
             case 1: launch_wm_label<uint8_t, 1>(a, st); break;

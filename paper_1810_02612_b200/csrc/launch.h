@@ -43,6 +43,7 @@ struct LaunchArgs {
     int pdl;               // single frame: launch as a programmatic dependent of the summary kernel
     // word-major multi-frame copy (PackedShard::wm_*): label_wm_kernel
     int word_major;
+    int tc;  // (word_major, multi-frame) the tcgen05 kind::i8 kernel (tc_i8.cu)
     const uint64_t* wm_mask;
     const uint8_t* wm_row;
     const uint32_t* wm_gword;
@@ -70,6 +71,11 @@ cudaError_t launch_wm_build(const uint64_t* P64, int props, int frames, uint32_t
                             size_t work_bytes, uint32_t* task_ctr, int nctr, cudaStream_t st,
                             const uint32_t* touched64 = nullptr);
 size_t wm_work_bytes(int props, uint32_t nw64);
+// the tcgen05 kind::i8 formulation (tc_i8.cu, dev knob LTLG_TC=1)
+size_t tc_work_bytes(uint32_t nw64);
+cudaError_t launch_tc_build(const uint64_t* P64, int props, int frames, uint32_t nw64, uint64_t cells, void* work,
+                            uint32_t* task_ctr, int nctr, cudaStream_t st, const uint32_t* touched64);
+cudaError_t launch_tc_label(const LaunchArgs& a, cudaStream_t st);
 cudaError_t launch_summary64(const uint64_t* P64, int props, uint32_t nw64, uint64_t cells, void* tab, void* s_only,
                              uint32_t* task_ctr, int nctr, cudaStream_t st, uint64_t* P_copy,
                              const uint32_t* touched64 = nullptr);

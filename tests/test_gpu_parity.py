@@ -803,6 +803,10 @@ def test_config5_dense_grid_slice():
     {"LTLG_NT64": "512"},                                                   # 64-prop kernel, 16 warps
     {"LTLG_NT64": "1024"},                                                  # 64-prop kernel, 32 warps
     {"LTLG_PROPLANE": "0"},                                                 # frame-per-lane 64-cell kernel
+    {"LTLG_WORDMAJOR": "0"},                                                # pair-major prop-lane kernel
+    {"LTLG_WM1": "1"},                                                      # word-major single frame everywhere
+    {"LTLG_WM1": "0"},                                                      # stream64 single frame everywhere
+    {"LTLG_TC": "1"},                                                       # tcgen05 kind::i8 multi-frame
 ])
 def test_ab_variants_parity(knobs):
     # the A/B kernel variants (env knobs, read once per process) stay bit-exact

@@ -1,5 +1,6 @@
 """Parity of the labeling path under the current environment's A/B knobs
-(LTLG_STREAM64, LTLG_BATCH64, LTLG_STREAM_CFG, LTLG_STREAM_TABLE): run by
+(LTLG_STREAM64, LTLG_BATCH64, LTLG_STREAM_CFG, LTLG_STREAM_TABLE, LTLG_PROPLANE,
+LTLG_WORDMAJOR, LTLG_WM1, LTLG_TC): run by
 tests/test_gpu_parity.py in subprocesses, since the knobs are read once per
 process.  Exits 0 iff every case is bit-exact against the CPU oracle."""
 import os

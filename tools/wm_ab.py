@@ -58,8 +58,9 @@ if __name__ == "__main__":
         sys.exit(0)
     import numpy as np
 
-    variants = [("wm128", {"ROWS": "128"}), ("wm64", {"ROWS": "64"}), ("wm256", {"ROWS": "256"}),
-                ("pl", {"LTLG_WORDMAJOR": "0"})]
+    variants = [("wm128", {"ROWS": "128"}), ("pl", {"LTLG_WORDMAJOR": "0"}), ("tc", {"LTLG_TC": "1"})]
+    if os.environ.get("VARIANTS"):
+        variants = [v for v in variants if v[0] in os.environ["VARIANTS"].split(",")]
     ref = None
     for name, env in variants:
         out = f"/tmp/wm_ab_{name}.npy"
