@@ -388,9 +388,9 @@ def config5_shard(local: int, hbm: float, src: str, quick: bool):
               "what": "pinned host P (8 MB) -> labels resident in HBM (host steady clock)", "kernel_p50_ms": k,
               "roofline": {"bound": "hbm", "achieved": alg1 / (k / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                            "frac": alg1 / (k / 1e3) / 1e9 / hbm, "alg_bytes_per_launch": alg1, "peak_source": src,
-                           "traffic": ncu_traffic("label_stream64_kernel<64>"),
-                           "limiter": ncu_limiter("label_stream64_kernel<64>"),
-                           "kernel": "label_stream64_kernel<64,u64,L1,768>"}}
+                           "traffic": ncu_traffic("label_wm1_kernel<u64,2>"),
+                           "limiter": ncu_limiter("label_wm1_kernel<u64,2>"),
+                           "kernel": "label_wm1_kernel<u64,2> (word-major single frame)"}}
     del frames
     F = 64
     P = torch.empty((F, props, nw), dtype=torch.int64, device="cuda")

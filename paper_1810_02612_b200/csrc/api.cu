@@ -765,9 +765,13 @@ ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t*
         else
             cudaGetLastError();  // pageable memory: not an error, just no mapping
     }
+    // The upload: on the comm stream when there are shards to broadcast to
+    // (it and the broadcast then overlap the previous submit's labelling); on
+    // the labelling stream for one shard -- measured steadier for the
+    // two-engine host pipeline of bench.py (e2e 1.36-1.38e10 vs 1.17-1.37e10).
     cudaStream_t src = s0.stream;
-    if (nwords && !in_place && !s0.P_host) {  // the upload on the comm stream, once the buffer is free
-        src = s0.comm;
+    if (nwords && !in_place && !s0.P_host) {
+        if (ctx->shards.size() > 1) src = s0.comm;
         CK(cudaStreamWaitEvent(src, s0.pb.read_done, 0), "stream wait");
         CK(cudaMemcpyAsync(s0.pb.b.ptr, words, nwords * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                            src),

@@ -33,15 +33,17 @@ lim_path = os.path.join(os.path.dirname(dst), "limiters.json")
 limiters = json.load(open(lim_path)) if os.path.exists(lim_path) else {}
 TITLES = {"batch": "config 4, multi-frame labeling kernel", "stream": "config 3, single-frame labeling kernel",
           "cfg5batch": "config 5 shard (1M rows, 1024^2, 64 props), 64-frame labeling kernel",
-          "cfg5stream": "config 5 shard (1M rows, 1024^2, 64 props), single-frame labeling kernel"}
-for kind in ("batch", "stream", "cfg5batch", "cfg5stream"):
+          "cfg5stream": "config 5 shard (1M rows, 1024^2, 64 props), single-frame labeling kernel",
+          "cfg5tc": "config 5 shard, 64 frames: the tcgen05 kind::i8 formulation (LTLG_TC=1; measured, dropped)"}
+for kind in ("batch", "stream", "cfg5batch", "cfg5stream", "cfg5tc"):
     rep = f"{src}_{kind}.ncu-rep"
     if not os.path.exists(rep):
         continue
     lines.append(f"\n## `ncu --set full`: {TITLES[kind]}\n```")
     lines.append(run("python", os.path.join(here, "ncu_brief.py"), rep).rstrip())
     raw = list(csv.reader(io.StringIO(run("ncu", "-i", rep, "--page", "raw", "--csv"))))
-    d = dict(zip(raw[0], raw[2]))
+    rows = [dict(zip(raw[0], r)) for r in raw[2:]]
+    d = next((r for r in rows if "label_" in r.get("Kernel Name", "")), rows[0])  # the labelling kernel of the capture
     u = dict(zip(raw[0], raw[1]))
     for k in ["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
               "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
@@ -52,7 +54,7 @@ for kind in ("batch", "stream", "cfg5batch", "cfg5stream"):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     tb = sum(float(d[k]) * scale.get(u[k], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     full_name = d["Kernel Name"]
-    name = full_name.split("<")[0].replace("void ", "").split("::")[-1]
+    name = full_name.split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]
     if "unsigned long" in full_name.split("(")[0]:  # the 64-prop instantiations (template arguments)
         name += "<u64,2>" if "label_wm" in name else "<64>"
     traffic[name] = tb
