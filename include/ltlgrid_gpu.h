@@ -139,6 +139,17 @@ ltlg_status ltlg_submit_grid_device(ltlg_ctx* ctx, uint64_t cells, int num_props
 ltlg_status ltlg_submit_grid_device_ex(ltlg_ctx* ctx, uint64_t cells, int num_props,
                                        const uint64_t* device_column_words, int frames, int readback);
 
+/* Same as ltlg_submit_grid_device_ex, for a pipelining caller: P (on the
+ * first device) is ready when `ready_event` (a cudaEvent_t, as void*,
+ * recorded by the caller) completes -- the engine orders its reads of P after
+ * that event only, not after the engine's own earlier work.  The multi-frame
+ * summary then runs on the shard's comm stream and overlaps the previous
+ * submit's labelling; the labelling still follows the previous one.  P must
+ * stay unmodified until the labels are ready, as for the device form. */
+ltlg_status ltlg_submit_grid_device_async(ltlg_ctx* ctx, uint64_t cells, int num_props,
+                                          const uint64_t* device_column_words, int frames, int readback,
+                                          void* ready_event);
+
 /* World-frame perception grid -> vehicle-frame P resample, then label
  * (north_star subsystem 2; transform convention of translate_system,
  * abstraction.cpp:396-404).  Grids are k=2 z-order grids; world_words is

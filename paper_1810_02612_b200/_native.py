@@ -27,7 +27,7 @@ EXPORTS = [
     "ltlg_submit_grid_device_ex",
     "ltlg_swept_volume", "ltlg_csr_rows", "ltlg_csr_cols", "ltlg_csr_nnz", "ltlg_csr_build_ms", "ltlg_csr_copy",
     "ltlg_load_csr", "ltlg_csr_free", "ltlg_set_profiling", "ltlg_generate_scenario", "ltlg_submit_scenario",
-    "ltlg_csr_save", "ltlg_apply_labels", "ltlg_edge_counting",
+    "ltlg_csr_save", "ltlg_apply_labels", "ltlg_edge_counting", "ltlg_submit_grid_device_async",
 ]
 
 
@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         "ltlg_submit_grid": ([ctxp, u64, i32, vp, i32], i32),
         "ltlg_submit_grid_device": ([ctxp, u64, i32, vp, i32], i32),
         "ltlg_submit_grid_device_ex": ([ctxp, u64, i32, vp, i32, i32], i32),
+        "ltlg_submit_grid_device_async": ([ctxp, u64, i32, vp, i32, i32, vp], i32),
         "ltlg_submit_world_grid": ([ctxp, C.POINTER(Grid2), C.POINTER(Grid2), i32, vp, i32, vp, i32, i32], i32),
         "ltlg_wait": ([ctxp], i32),
         "ltlg_get_labels": ([ctxp, i32, vp], i32),

@@ -104,9 +104,13 @@ struct DevBuf {
 struct Shard {
     int device = 0;
     cudaStream_t stream = nullptr;
-    // profiling: a ring of kRing event quadruples (upload, summary, label, end)
+    // profiling: a ring of kRing event quintuples (submit, summary start,
+    // summary end, labelling start, end); the summary may run on the comm
+    // stream (ltlg_submit_grid_device_async), so its end and the labelling's
+    // start are separate events
     static constexpr int kRing = 256;
-    std::vector<cudaEvent_t> ring;  // kRing * 4 when profiling
+    static constexpr int kEv = 5;
+    std::vector<cudaEvent_t> ring;  // kRing * kEv when profiling
     uint64_t submits = 0;           // profiled submits recorded so far
     cudaEvent_t* ev = nullptr;      // the quadruple of the current submit
     uint64_t row_begin = 0, row_end = 0, n_pairs = 0, words = 0;
@@ -138,11 +142,14 @@ struct Shard {
     // read it) gates its refill.
     struct PBuf {
         DevBuf<uint64_t> b;
+        DevBuf<uint8_t> sf;    // the submit's summary (work buffer of the summary kernels)
+        DevBuf<uint32_t> ctr;  // its persistent-kernel task counters (reset by the summary kernels)
         cudaEvent_t read_done = nullptr;
     };
     PBuf pb, pb_alt;               // pb = this submit's P
     cudaStream_t comm = nullptr;   // P upload (shard 0) and broadcast
     cudaEvent_t src_ready = nullptr, p_ready = nullptr;
+    cudaEvent_t sum_done = nullptr;  // a summary built on the comm stream (ltlg_submit_grid_device_async)
     const uint64_t* P_in = nullptr;  // caller's device P used in place (single device)
     // caller's pinned host P, device-mapped: the single-frame summary kernel
     // reads it over PCIe and writes the device copy as it goes (no separate H2D).
@@ -153,7 +160,6 @@ struct Shard {
     const uint64_t* P_host = nullptr;
     bool P_resident = true;  // Pdev() holds the last submit's P (not after a fused word-major upload)
     const uint64_t* Pdev() const { return P_in ? P_in : pb.b.ptr; }
-    DevBuf<uint8_t> sf;
     DevBuf<uint8_t> labels;
     DevBuf<uint64_t> stage;
     DevBuf<uint8_t> stage_hit;  // ltlg_edge_counting
@@ -165,7 +171,6 @@ struct Shard {
     DevBuf<uint64_t> lane_flags;  // ltlg_submit_scenario: per-(x, y) not-nominal-lane flags
     uint64_t guard_lut_key = ~0ull;  // (guard epoch, props) the uploaded table is for
     DevBuf<uint8_t> box_rng;     // and their per-axis cell ranges
-    DevBuf<uint32_t> ctr;  // persistent-kernel task counter
     DevBuf<uint8_t> s_only;  // S mask per (word, frame)
     bool have_times = false;
     uint64_t rows() const { return row_end - row_begin; }
@@ -184,6 +189,11 @@ struct ltlg_ctx {
     std::vector<uint64_t> guard_pos, guard_neg;  // monitor guards (ltlg_set_guards)
     uint64_t guard_epoch = 0;                    // bumped by every ltlg_set_guards
     uint64_t cells = 0;
+    // this submit's P is ready when this caller event completes
+    // (ltlg_submit_grid_device_async): the engine does not order P's reads
+    // after its own earlier work, so the summary can overlap the previous
+    // submit's labelling on the comm stream
+    cudaEvent_t ready_ev = nullptr;
 };
 
 namespace {
@@ -468,28 +478,31 @@ constexpr int kSmallFrames = 16;  // sweep_frames: per-frame single-frame launch
 // single-frame launch writing labels[row * frames + f].
 ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
     const int props = ctx->props, frames = ctx->frames;
-    CK(s.sf.reserve(split64_table_bytes(props, nw64)), "allocate summary");
-    CK(s.ctr.reserve(64 * kCtrStride * sizeof(uint32_t)), "allocate task counters");
+    CK(s.pb.sf.reserve(split64_table_bytes(props, nw64)), "allocate summary");
+    CK(s.pb.ctr.reserve(64 * kCtrStride * sizeof(uint32_t)), "allocate task counters");
     CK(s.s_only.reserve(static_cast<size_t>(nw64 + 1) * s_only_bytes(props)), "allocate summary");
     const bool prof = ctx->opts.profile != 0;
     if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
     const size_t pw = static_cast<size_t>(props) * nw64;  // u64 words of one frame's P
     static const bool wm_ok = !env_off("LTLG_WORDMAJOR");
     const bool wm1 = wm_ok && s.wm_rows > 0 && use_wm1(props, nw64);  // (as for one frame, frame by frame)
-    if (wm1) CK(s.sf.reserve(pl_work_bytes(props, 1, nw64)), "allocate summary");
+    if (wm1) CK(s.pb.sf.reserve(pl_work_bytes(props, 1, nw64)), "allocate summary");
     for (int f = 0; f < frames; ++f) {
         if (wm1)
-            CK(launch_pl(s.Pdev() + f * pw, props, 1, nw64, ctx->cells, s.sf.ptr, s.sf.bytes, s.ctr.ptr,
+            CK(launch_pl(s.Pdev() + f * pw, props, 1, nw64, ctx->cells, s.pb.sf.ptr, s.pb.sf.bytes, s.pb.ctr.ptr,
                          static_cast<int>(kCtrStride), s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else
-            CK(launch_summary64(s.Pdev() + f * pw, props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr, s.ctr.ptr,
+            CK(launch_summary64(s.Pdev() + f * pw, props, nw64, ctx->cells, s.pb.sf.ptr, s.s_only.ptr, s.pb.ctr.ptr,
                                 static_cast<int>(kCtrStride), s.stream, nullptr,
                                 pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
-        if (prof && f == 0) CK(cudaEventRecord(s.ev[2], s.stream), "event");
+        if (prof && f == 0) {
+            CK(cudaEventRecord(s.ev[2], s.stream), "event");
+            CK(cudaEventRecord(s.ev[3], s.stream), "event");
+        }
         LaunchArgs a{};
-        a.sf = s.sf.ptr;
+        a.sf = s.pb.sf.ptr;
         a.P32 = reinterpret_cast<const uint32_t*>(s.Pdev() + f * pw);
         a.nw32 = 2 * nw64;
         a.props = props;
@@ -505,7 +518,7 @@ ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
         a.task_row = s.trow_s.ptr;
         a.task_begin = 0;
         a.ntasks = s.block_task_s.back();
-        a.task_ctr = s.ctr.ptr;
+        a.task_ctr = s.pb.ctr.ptr;
         if (wm1) {
             a.word_major = 1;
             a.wm_mask = s.wm_mask.ptr;
@@ -525,7 +538,7 @@ ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
         const ltlg_status gst = run_guards(ctx, s);
         if (gst != LTLG_OK) return gst;
     }
-    if (prof) CK(cudaEventRecord(s.ev[3], s.stream), "event");
+    if (prof) CK(cudaEventRecord(s.ev[4], s.stream), "event");
     s.have_times = prof;
     return LTLG_OK;
 }
@@ -613,7 +626,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         // the word-major copy instead of label_wm_kernel (measured, not kept)
         static const bool tc_on = getenv("LTLG_TC") && atoi(getenv("LTLG_TC")) != 0;
         const bool tc = pl && wm && tc_on && s.wm_rows <= 128;
-        CK(s.sf.reserve(tc ? tc_work_bytes(nw64)
+        CK(s.pb.sf.reserve(tc ? tc_work_bytes(nw64)
                         : pl && wm ? wm_work_bytes(props, nw64)
                         : wm1 ? pl_work_bytes(props, 1, nw64)
                         : pl ? pl_work_bytes(props, std::min(frames, 64), nw64)
@@ -623,44 +636,61 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
                                    ? split_table_bytes(props, nw32)
                                    : static_cast<size_t>(nw32 + 1) * frames * summary_entry_bytes(props)),
            "allocate summary");
-        CK(s.ctr.reserve(64 * kCtrStride * sizeof(uint32_t)), "allocate task counters");
+        CK(s.pb.ctr.reserve(64 * kCtrStride * sizeof(uint32_t)), "allocate task counters");
         CK(s.s_only.reserve(static_cast<size_t>(nw32 + 1) * frames * s_only_bytes(props)), "allocate summary");
         const bool prof = ctx->opts.profile != 0;
-        if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
+        // the word-major summary of an async submit runs on the comm stream,
+        // after the caller's ready event and the labelling that last used this
+        // summary buffer, so it overlaps the previous submit's labelling
+        const bool async_sum = ctx->ready_ev && pl && wm && !tc && nslice == 1;
+        const cudaStream_t sst = async_sum ? s.comm : s.stream;
+        if (async_sum) {
+            if (&s == &ctx->shards[0] && ctx->shards.size() == 1)
+                CK(cudaStreamWaitEvent(s.comm, ctx->ready_ev, 0), "stream wait");
+            CK(cudaStreamWaitEvent(s.comm, s.pb.read_done, 0), "stream wait");
+        } else if (ctx->ready_ev && ctx->shards.size() == 1) {
+            CK(cudaStreamWaitEvent(s.stream, ctx->ready_ev, 0), "stream wait");
+        }
+        if (prof) CK(cudaEventRecord(s.ev[1], sst), "event");
         const int nctr = static_cast<int>((s.block_row.size() - 1) * kCtrStride);
         for (int sl = 0; sl < nslice; ++sl) {  // (frame slices: prop-lane path only)
         // balanced slices (65 frames -> 33 + 32, not 64 + 1)
         const int f0 = frames * sl / nslice, nf = pl ? frames * (sl + 1) / nslice - f0 : frames;
         if (wm1)
-            CK(launch_pl(P_host ? P_host : s.Pdev(), props, 1, nw64, ctx->cells, s.sf.ptr, s.sf.bytes, s.ctr.ptr, nctr,
+            CK(launch_pl(P_host ? P_host : s.Pdev(), props, 1, nw64, ctx->cells, s.pb.sf.ptr, s.pb.sf.bytes, s.pb.ctr.ptr, nctr,
                          s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (wide)
-            CK(launch_summary64(P_host ? P_host : s.Pdev(), props, nw64, ctx->cells, s.sf.ptr, s.s_only.ptr,
-                                s.ctr.ptr, nctr, s.stream, P_host ? s.pb.b.ptr : nullptr,
+            CK(launch_summary64(P_host ? P_host : s.Pdev(), props, nw64, ctx->cells, s.pb.sf.ptr, s.s_only.ptr,
+                                s.pb.ctr.ptr, nctr, s.stream, P_host ? s.pb.b.ptr : nullptr,
                                 pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (tc)
-            CK(launch_tc_build(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.sf.ptr,
-                               s.ctr.ptr, nctr, s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
+            CK(launch_tc_build(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.pb.sf.ptr,
+                               s.pb.ctr.ptr, nctr, s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (pl && wm)
-            CK(launch_wm_build(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.sf.ptr,
-                               s.sf.bytes, s.ctr.ptr, nctr, s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
+            CK(launch_wm_build(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.pb.sf.ptr,
+                               s.pb.sf.bytes, s.pb.ctr.ptr, nctr, sst, pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (pl)
-            CK(launch_pl(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.sf.ptr,
-                         s.sf.bytes, s.ctr.ptr, nctr, s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
+            CK(launch_pl(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.pb.sf.ptr,
+                         s.pb.sf.bytes, s.pb.ctr.ptr, nctr, s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
         else if (wide_b)
-            CK(launch_summary_b64(s.Pdev(), props, frames, nw64, ctx->cells, s.sf.ptr, nullptr, s.s_only.ptr,
-                                  s.ctr.ptr, nctr, s.stream),
+            CK(launch_summary_b64(s.Pdev(), props, frames, nw64, ctx->cells, s.pb.sf.ptr, nullptr, s.s_only.ptr,
+                                  s.pb.ctr.ptr, nctr, s.stream),
                "summary kernel");
         else
-            CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.sf.ptr,
-                              s.s_only.ptr, s.ctr.ptr, nctr, s.stream),
+            CK(launch_summary(reinterpret_cast<const uint32_t*>(s.Pdev()), props, frames, nw32, ctx->cells, s.pb.sf.ptr,
+                              s.s_only.ptr, s.pb.ctr.ptr, nctr, s.stream),
                "summary kernel");
-        if (prof && sl == 0) CK(cudaEventRecord(s.ev[2], s.stream), "event");
+        if (prof && sl == 0) CK(cudaEventRecord(s.ev[2], sst), "event");
+        if (async_sum) {  // the labelling waits for its summary
+            CK(cudaEventRecord(s.sum_done, s.comm), "event");
+            CK(cudaStreamWaitEvent(s.stream, s.sum_done, 0), "stream wait");
+        }
+        if (prof && sl == 0) CK(cudaEventRecord(s.ev[3], s.stream), "event");
         LaunchArgs a{};
         // single frame: the labeling kernel is a programmatic dependent of the
         // summary kernel (not when profiling: the event between them would
@@ -668,7 +698,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         a.pdl = wide && !prof ? 1 : 0;
         a.pairs = s.pairs.ptr;
         a.perm = s.perm.ptr;
-        a.sf = s.sf.ptr;
+        a.sf = s.pb.sf.ptr;
         a.P32 = reinterpret_cast<const uint32_t*>(s.Pdev());
         a.nw32 = nw32;
         a.props = props;
@@ -714,7 +744,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         for (int c = 0; c < nb; ++c) {
             a.task_begin = bt[static_cast<size_t>(c)];
             a.ntasks = nb == 1 ? bt.back() : bt[static_cast<size_t>(c) + 1];
-            a.task_ctr = s.ctr.ptr + static_cast<size_t>(c) * kCtrStride;
+            a.task_ctr = s.pb.ctr.ptr + static_cast<size_t>(c) * kCtrStride;
             CK(launch_label(a, s.stream), "label kernel");
             if (nb > 1 && sl == nslice - 1) CK(cudaEventRecord(s.block_done[static_cast<size_t>(c)], s.stream), "event");
         }
@@ -724,7 +754,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
             const ltlg_status gst = run_guards(ctx, s);
             if (gst != LTLG_OK) return gst;
         }
-        if (prof) CK(cudaEventRecord(s.ev[3], s.stream), "event");
+        if (prof) CK(cudaEventRecord(s.ev[4], s.stream), "event");
         s.have_times = prof;
         CK(cudaEventRecord(s.pb.read_done, s.stream), "event");  // (the labelling is done with this P buffer)
     }
@@ -733,7 +763,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
 }
 
 ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* words, int frames,
-                   bool on_device, bool readback) {
+                   bool on_device, bool readback, cudaEvent_t ready = nullptr) {
     ltlg_status st = check_grid(ctx, cells, num_props, frames);
     if (st != LTLG_OK) return st;
     ctx->cells = cells;
@@ -747,7 +777,7 @@ ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t*
     const bool in_place = on_device && ctx->shards.size() == 1;
     if ((st = rotate_P(ctx, in_place ? 0 : nwords * 8 + 16)) != LTLG_OK) return st;
     if (ctx->opts.profile)
-        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
+        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * Shard::kEv];
     Shard& s0 = ctx->shards[0];
     CK(cudaSetDevice(s0.device), "cudaSetDevice");
     if (ctx->opts.profile) CK(cudaEventRecord(s0.ev[0], s0.stream), "event");
@@ -773,6 +803,7 @@ ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t*
     if (nwords && !in_place && !s0.P_host) {
         if (ctx->shards.size() > 1) src = s0.comm;
         CK(cudaStreamWaitEvent(src, s0.pb.read_done, 0), "stream wait");
+        if (ready) CK(cudaStreamWaitEvent(src, ready, 0), "stream wait");
         CK(cudaMemcpyAsync(s0.pb.b.ptr, words, nwords * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                            src),
            "upload P");
@@ -783,7 +814,10 @@ ltlg_status submit(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t*
             cudaSetDevice(ctx->shards[i].device);
             cudaEventRecord(ctx->shards[i].ev[0], ctx->shards[i].stream);
         }
-    return run_label(ctx, readback);
+    ctx->ready_ev = ready;
+    st = run_label(ctx, readback);
+    ctx->ready_ev = nullptr;
+    return st;
 }
 
 ltlg_status sync_all(ltlg_ctx* ctx) {
@@ -832,11 +866,11 @@ ltlg_status ltlg_create_ex(const int* devices, int n_devices, const ltlg_options
             return cuda_fail(nullptr, e, "stream");
         if ((e = cudaStreamCreateWithFlags(&s.comm, cudaStreamNonBlocking)) != cudaSuccess)
             return cuda_fail(nullptr, e, "stream");
-        for (cudaEvent_t* ev : {&s.pb.read_done, &s.pb_alt.read_done, &s.src_ready, &s.p_ready})
+        for (cudaEvent_t* ev : {&s.pb.read_done, &s.pb_alt.read_done, &s.src_ready, &s.p_ready, &s.sum_done})
             if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
                 return cuda_fail(nullptr, e, "event");
         if (ctx->opts.profile) {
-            s.ring.assign(Shard::kRing * 4, nullptr);
+            s.ring.assign(Shard::kRing * Shard::kEv, nullptr);
             for (auto& ev : s.ring)
                 if ((e = cudaEventCreate(&ev)) != cudaSuccess) return cuda_fail(nullptr, e, "event");
         }
@@ -895,12 +929,15 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.trow_b.release();
         s.tpair_s.release();
         s.tpair_b.release();
-        s.pb.b.release();
-        s.pb_alt.b.release();
-        for (cudaEvent_t ev : {s.pb.read_done, s.pb_alt.read_done, s.src_ready, s.p_ready})
+        for (Shard::PBuf* q : {&s.pb, &s.pb_alt}) {
+            q->b.release();
+            q->sf.release();
+            q->ctr.release();
+        }
+        for (cudaEvent_t ev : {s.pb.read_done, s.pb_alt.read_done, s.src_ready, s.p_ready, s.sum_done})
             if (ev) cudaEventDestroy(ev);
         if (s.comm) cudaStreamDestroy(s.comm);
-        s.sf.release();
+        s.pb.sf.release();
         s.labels.release();
         s.stage.release();
         s.world.release();
@@ -910,7 +947,7 @@ void ltlg_destroy(ltlg_ctx* ctx) {
         s.guard_lut.release();
         s.lane_flags.release();
         s.box_rng.release();
-        s.ctr.release();
+        s.pb.ctr.release();
         s.s_only.release();
         for (auto& ev : s.ring)
             if (ev) cudaEventDestroy(ev);
@@ -980,6 +1017,13 @@ ltlg_status ltlg_submit_grid_device_ex(ltlg_ctx* ctx, uint64_t cells, int num_pr
     return submit(ctx, cells, num_props, dev_words, frames, true, readback != 0);
 }
 
+ltlg_status ltlg_submit_grid_device_async(ltlg_ctx* ctx, uint64_t cells, int num_props, const uint64_t* dev_words,
+                                          int frames, int readback, void* ready_event) {
+    DeviceGuard device_guard;  // the caller's current device is restored on return
+    if (!ready_event) return set_err(ctx, LTLG_EINVAL, "null ready event");
+    return submit(ctx, cells, num_props, dev_words, frames, true, readback != 0, static_cast<cudaEvent_t>(ready_event));
+}
+
 ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, const ltlg_grid2* world, int num_props,
                                    const uint64_t* world_words, int words_on_device, const ltlg_pose2* poses,
                                    int frames, int outside) {
@@ -1004,7 +1048,7 @@ ltlg_status ltlg_submit_world_grid(ltlg_ctx* ctx, const ltlg_grid2* vehicle, con
     if (wwords && !world_words) return set_err(ctx, LTLG_EINVAL, "null world_words");
     if ((st = rotate_P(ctx, vwords * 8 + 16)) != LTLG_OK) return st;
     if (ctx->opts.profile)
-        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
+        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * Shard::kEv];
     Shard& s0 = ctx->shards[0];
     CK(cudaSetDevice(s0.device), "cudaSetDevice");
     s0.P_in = nullptr;
@@ -1215,7 +1259,7 @@ ltlg_status ltlg_submit_boxes(ltlg_ctx* ctx, const ltlg_gridk* grid, int num_pro
     const size_t nwords = static_cast<size_t>(cols) * ((cells + 63) / 64);
     if ((st = rotate_P(ctx, nwords * 8 + 16)) != LTLG_OK) return st;
     if (ctx->opts.profile)
-        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
+        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * Shard::kEv];
     Shard& s0 = ctx->shards[0];
     CK(cudaSetDevice(s0.device), "cudaSetDevice");
     s0.P_in = nullptr;
@@ -1387,7 +1431,7 @@ ltlg_status ltlg_submit_scenario(ltlg_ctx* ctx, const ltlg_scenario* cfg, const 
     const size_t nwords = static_cast<size_t>(frames) * 2 * ((cells + 63) / 64);
     if ((st = rotate_P(ctx, nwords * 8 + 16)) != LTLG_OK) return st;
     if (ctx->opts.profile)
-        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * 4];
+        for (Shard& s : ctx->shards) s.ev = &s.ring[static_cast<size_t>(s.submits++ % Shard::kRing) * Shard::kEv];
     Shard& s0 = ctx->shards[0];
     CK(cudaSetDevice(s0.device), "cudaSetDevice");
     s0.P_in = nullptr;
@@ -1594,7 +1638,7 @@ ltlg_status ltlg_set_profiling(ltlg_ctx* ctx, int on) {
         for (Shard& s : ctx->shards) {
             if (!s.ring.empty()) continue;
             CK(cudaSetDevice(s.device), "cudaSetDevice");
-            s.ring.assign(Shard::kRing * 4, nullptr);
+            s.ring.assign(Shard::kRing * Shard::kEv, nullptr);
             for (auto& ev : s.ring) CK(cudaEventCreate(&ev), "event");
         }
     } else {
@@ -1614,12 +1658,12 @@ ltlg_status ltlg_stage_times(ltlg_ctx* ctx, int shard, int back, float* upload_m
     if (back < 0 || back >= Shard::kRing || static_cast<uint64_t>(back) >= s.submits)
         return set_err(ctx, LTLG_EINVAL, "profiled submit out of range");
     CK(cudaSetDevice(s.device), "cudaSetDevice");
-    cudaEvent_t* q = &s.ring[static_cast<size_t>((s.submits - 1 - static_cast<uint64_t>(back)) % Shard::kRing) * 4];
-    CK(cudaEventSynchronize(q[3]), "sync");
+    cudaEvent_t* q = &s.ring[static_cast<size_t>((s.submits - 1 - static_cast<uint64_t>(back)) % Shard::kRing) * Shard::kEv];
+    CK(cudaEventSynchronize(q[4]), "sync");
     float a = 0, b = 0, c = 0;
     CK(cudaEventElapsedTime(&a, q[0], q[1]), "event time");
     CK(cudaEventElapsedTime(&b, q[1], q[2]), "event time");
-    CK(cudaEventElapsedTime(&c, q[2], q[3]), "event time");
+    CK(cudaEventElapsedTime(&c, q[3], q[4]), "event time");
     if (upload_ms) *upload_ms = a;
     if (summary_ms) *summary_ms = b;
     if (label_ms) *label_ms = c;

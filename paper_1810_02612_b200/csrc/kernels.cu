@@ -1952,8 +1952,14 @@ __global__ void __launch_bounds__(NT) wm_build_kernel(const uint64_t* __restrict
     }
     const uint32_t gt = blockIdx.x * static_cast<uint32_t>(NT) + threadIdx.x;
     if (gt < static_cast<uint32_t>(nctr)) task_ctr[gt] = 0;
+    const uint32_t w0 = blockIdx.x * WPB;
+    if (touched64 && w0 < nw64) {  // no pair of the shard is on any of this CTA's words: nothing reads them
+        static_assert(32 % WPB == 0, "a CTA's words in one touched64 word");
+        const uint32_t tw = __ldg(touched64 + (w0 >> 5)) >> (w0 & 31);
+        if ((WPB == 32 ? tw : tw & ((1u << (WPB & 31)) - 1u)) == 0u) return;
+    }
     const uint32_t j = threadIdx.x / WPB, wl = threadIdx.x % WPB, h = j >> 5;
-    const uint32_t w = blockIdx.x * WPB + wl;
+    const uint32_t w = w0 + wl;
     const bool in = w <= nw64;  // word nw64 is the zero sentinel
     const bool live = in && w < nw64 && static_cast<uint64_t>(w) * 64 < cells && j < static_cast<uint32_t>(props) &&
                       !(touched64 && !(__ldg(touched64 + (w >> 5)) >> (w & 31) & 1u));
@@ -1965,12 +1971,20 @@ __global__ void __launch_bounds__(NT) wm_build_kernel(const uint64_t* __restrict
     uint64_t part = 0;
     if (live) {
         const uint32_t bit = 1u << (j & 31);
-        for (int f = 0; f < frames; ++f) {
-            const uint64_t x = base[static_cast<uint64_t>(f) * fstride] & valid;
-            if (x == valid) atomicOr(&s_fT[wl][64 * h + f], bit);
-            if (x != 0 && x != valid) {
-                part |= 1ull << f;
-                atomicAdd(&s_cnt[wl][h][f], 1u);
+        for (int f0 = 0; f0 < frames; f0 += 16) {  // 16 loads in flight, then their updates
+            uint64_t xs[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                xs[u] = f0 + u < frames ? __ldg(base + static_cast<uint64_t>(f0 + u) * fstride) & valid : 0ull;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int f = f0 + u;
+                if (f >= frames) break;
+                if (xs[u] == valid) atomicOr(&s_fT[wl][64 * h + f], bit);
+                if (xs[u] != 0 && xs[u] != valid) {
+                    part |= 1ull << f;
+                    atomicAdd(&s_cnt[wl][h][f], 1u);
+                }
             }
         }
     }
@@ -2041,13 +2055,24 @@ __global__ void __launch_bounds__(NT) wm_build_kernel(const uint64_t* __restrict
     }
     __syncthreads();
     const uint32_t bit = 1u << (j & 31);
-    for (uint64_t x = part; x; x &= x - 1) {
-        const int f = __ffsll(static_cast<long long>(x)) - 1;
-        const uint64_t p = base[static_cast<uint64_t>(f) * fstride] & valid;
-        const uint32_t o = s_own[wl][h][f], side_b = o & 32u;
-        const uint32_t slot = atomicAdd(&s_cnt[wl][h][f], 1u);
-        lrec[(static_cast<uint64_t>(s_row[wl][h]) + slot) * 32 + (o & 31u)] =
-            make_uint4(static_cast<uint32_t>(p), static_cast<uint32_t>(p >> 32), side_b ? 0u : bit, side_b ? bit : 0u);
+    for (uint64_t x = part; x;) {  // the partial frames, 4 loads in flight at a time
+        int fs[4];
+        uint64_t ps[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            fs[u] = x ? __ffsll(static_cast<long long>(x)) - 1 : -1;
+            x &= x - 1;
+            ps[u] = fs[u] >= 0 ? __ldg(base + static_cast<uint64_t>(fs[u]) * fstride) & valid : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (fs[u] < 0) break;
+            const uint32_t o = s_own[wl][h][fs[u]], side_b = o & 32u;
+            const uint32_t slot = atomicAdd(&s_cnt[wl][h][fs[u]], 1u);
+            lrec[(static_cast<uint64_t>(s_row[wl][h]) + slot) * 32 + (o & 31u)] =
+                make_uint4(static_cast<uint32_t>(ps[u]), static_cast<uint32_t>(ps[u] >> 32), side_b ? 0u : bit,
+                           side_b ? bit : 0u);
+        }
     }
 }
 
@@ -2484,7 +2509,9 @@ cudaError_t launch_wm_build(const uint64_t* P64, int props, int frames, uint32_t
     uint8_t* wb = static_cast<uint8_t*>(work);
     cudaError_t e = cudaMemsetAsync(wb + L.cursor, 0, 4, st);
     if (e != cudaSuccess) return e;
-    constexpr int kNT = 1024;
+    // 8 (4) words x 32 (64) prop slots per CTA: many small CTAs (the kernel is
+    // a chain of dependent phases), and CTAs whose words no pair is on exit
+    constexpr int kNT = 256;
     const int pshift = props > 32 ? 6 : 5;
     const int wpb = kNT >> pshift;
     const uint64_t gw = (static_cast<uint64_t>(nw64) + 1 + wpb - 1) / wpb, gc = (static_cast<uint64_t>(nctr) + kNT - 1) / kNT;

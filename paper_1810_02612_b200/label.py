@@ -447,11 +447,18 @@ class LabelEngine:
         self._ck(self._L.ltlg_save_labels(self._h, frame, os.fsencode(path)))
 
     def submit_grid_device(self, cells: int, num_props: int, device_words, frames: int = 1,
-                           readback: bool = False) -> None:
+                           readback: bool = False, ready_event=None) -> None:
         """P already in HBM; readback=True declares a following host read of
-        the labels (block-wise labelling overlapped with the copy)."""
-        self._ck(self._L.ltlg_submit_grid_device_ex(self._h, cells, num_props, _ptr(device_words), frames,
-                                                    1 if readback else 0))
+        the labels (block-wise labelling overlapped with the copy).
+        ready_event (a recorded CUDA event handle, e.g. torch.cuda.Event's
+        `cuda_event`): P is ready when it completes (ltlg_submit_grid_device_async),
+        so the multi-frame summary overlaps the previous submit's labelling."""
+        if ready_event is None:
+            self._ck(self._L.ltlg_submit_grid_device_ex(self._h, cells, num_props, _ptr(device_words), frames,
+                                                        1 if readback else 0))
+        else:
+            self._ck(self._L.ltlg_submit_grid_device_async(self._h, cells, num_props, _ptr(device_words), frames,
+                                                           1 if readback else 0, C.c_void_p(int(ready_event))))
 
     def submit_world_grid(self, vehicle, world, num_props: int, world_words, poses, outside: int = 0,
                           words_on_device: bool = False) -> None:

@@ -880,9 +880,11 @@ def test_apply_labels_vs_reference(props):
 def test_double_buffered_P_bursts(devices):
     """P is double-buffered per shard (rotate_P): a submit's upload /
     broadcast runs on the comm stream while the previous submit labels, gated
-    by the read_done event of the buffer it refills.  Bursts of submits
-    without a wait in between (pageable, pinned and device P, several frame
-    counts) must leave exactly the last submit's labels."""
+    by the read_done event of the buffer it refills; an async device submit
+    builds its summary on the comm stream after the caller's event.  Bursts of
+    submits without a wait in between (pageable, pinned, device and async
+    device P, several frame counts) must leave exactly the last submit's
+    labels."""
     import torch
 
     rng = np.random.default_rng(len(devices))
@@ -900,17 +902,26 @@ def test_double_buffered_P_bursts(devices):
             P = rng.integers(0, 2**63, size=(frames, props, nw), dtype=np.uint64)
             P[:, :, ::4] &= np.uint64(0x0101010101010101)
             P[:, :, 1::7] = np.uint64(0xFFFFFFFFFFFFFFFF)
-            kind = (burst + k) % 3
+            kind = (burst + k) % 4
             if kind == 0:
                 eng.submit_grid(c, props, P, frames)
             elif kind == 1:
                 eng.submit_grid(c, props, torch.from_numpy(P.view(np.int64).copy()).pin_memory(), frames)
-            else:
+            elif kind == 2:
                 dev = torch.from_numpy(P.view(np.int64).copy()).cuda()
                 eng.submit_grid_device(c, props, dev.data_ptr(), frames)
                 Ps.append(dev)  # (kept alive until the labels are read)
+            else:  # async: P written on a side stream, ready when its event completes
+                side = torch.cuda.Stream()
+                with torch.cuda.stream(side):
+                    dev = torch.empty((frames, props, nw), dtype=torch.int64, device="cuda")
+                    dev.copy_(torch.from_numpy(P.view(np.int64).copy()).pin_memory(), non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                eng.submit_grid_device(c, props, dev.data_ptr(), frames, ready_event=ev.cuda_event)
+                Ps.extend([dev, ev, side])
             Ps.append(P)
-        P = Ps[-1] if isinstance(Ps[-1], np.ndarray) else Ps[-2]
+        P = [q for q in Ps if isinstance(q, np.ndarray)][-1]
         for f in range(P.shape[0]):
             want = ORACLE.label_all(r, c, off, idx, c, props, P[f])
             assert eng.get_labels(f) == LabelMatrix(r, props, want), (burst, f)
