@@ -744,6 +744,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.quick)
+        if lat is not None:  # the reference's config-3 p50 beside ours
+            lat["cpu_reference_p50_ms"] = cpu["config3"]["p50_ms_2M_extrapolated"]
+            lat["cpu_reference_what"] = cpu["config3"]["note"] + f"; {cpu['cores']} threads"
 
     if rank == 0:
         # gpu_launches: our kernels per step = wm_build (the word-major summary) and label_wm
