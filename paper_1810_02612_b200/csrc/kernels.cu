@@ -2243,7 +2243,7 @@ __device__ __forceinline__ void wm_group(const uint64_t* __restrict__ emask, con
         const int n = static_cast<int>(e1 - c < 32u ? e1 - c : 32u);
         for (int i = 0; i < n; ++i) {
             const uint32_t mlo = __shfl_sync(0xffffffffu, cm.x, i), mhi = __shfl_sync(0xffffffffu, cm.y, i);
-            const uint32_t base = acc_s + __shfl_sync(0xffffffffu, cr, i) * RB;
+            const uint32_t rowi = __shfl_sync(0xffffffffu, cr, i);
             // full props hit any pair; a partial prop hits iff one of its
             // records does (for a pair sweeping the whole word every record
             // hits, so no special case for it)
@@ -2268,7 +2268,7 @@ __device__ __forceinline__ void wm_group(const uint64_t* __restrict__ emask, con
             }
 #pragma unroll
             for (int k = 0; k < 2 * PW; ++k)  // (an OR of 0 is a no-op: no branch around it)
-                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + off[k]), "r"(v[k]) : "memory");
+                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(rowi * RB + off[k]), "r"(v[k]) : "memory");
         }
     }
 }
@@ -2317,11 +2317,11 @@ __global__ void __launch_bounds__(kWmThreads)
 #pragma unroll
             for (int hh = 0; hh < PW; ++hh) {  // the lane's two frames of each prop half
                 const uint32_t pr = __ldg(wpair + (static_cast<uint64_t>(w) * PW + hh) * 32 + lane);
-                off[2 * hh] = 4u * (64u * hh + (pr & 0xffu));
-                off[2 * hh + 1] = 4u * (64u * hh + (pr >> 8));
+                off[2 * hh] = acc_s + 4u * (64u * hh + (pr & 0xffu));  // (shared-memory addresses in row 0)
+                off[2 * hh + 1] = acc_s + 4u * (64u * hh + (pr >> 8));
             }
 #pragma unroll
-            for (int k = 0; k < 2 * PW; ++k) fv[k] = __ldg(ffrT + static_cast<uint64_t>(w) * RW + off[k] / 4);
+            for (int k = 0; k < 2 * PW; ++k) fv[k] = __ldg(ffrT + static_cast<uint64_t>(w) * RW + (off[k] - acc_s) / 4);
             const uint2 hd = __ldg(whdr + w);
             const uint32_t ns0 = hd.y & 0xffffu, ns1 = hd.y >> 16;
             uint4 ra[kWmSlots], rb[kWmSlots];
