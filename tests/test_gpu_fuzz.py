@@ -1,7 +1,7 @@
 """Randomised end-to-end parity (GPU): random shapes, proposition counts,
 frame counts across every dispatch path (single frame, per-frame, prop-lane
 slices, > 64 frames), shard counts, row sorting, read-back blocks, task
-sizes, pageable or pinned P -- against the oracle."""
+sizes, word-major task rows, pageable or pinned P -- against the oracle."""
 import random
 
 import numpy as np
@@ -37,7 +37,8 @@ def test_randomised_engine_configs(chunk):
             P[::3, :, ::4] = np.uint64(0xFFFFFFFFFFFFFFFF)
         devs = rnd.choice([[0], [0], [0, 0], [0, 0, 0]])
         eng = LabelEngine(devices=devs, sort_rows=rnd.random() < 0.5, readback_chunks=rnd.choice([0, 1, 3, 8]),
-                          stream_task_pairs=rnd.choice([0, 1, 50, 4096]), batch_task_pairs=rnd.choice([0, 1, 7, 300]))
+                          stream_task_pairs=rnd.choice([0, 1, 50, 4096]), batch_task_pairs=rnd.choice([0, 1, 7, 300]),
+                          task_rows=rnd.choice([0, 1, 5, 33, 128, 256]))
         eng.load_abstraction(CsrBoolMatrix(r, c, off, idx))
         src = P
         if rnd.random() < 0.4 and P.size:
