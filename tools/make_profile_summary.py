@@ -74,7 +74,7 @@ for kind in ("batch", "stream", "cfg5batch", "cfg5stream", "cfg5tc"):
         "warp_insts": cnt("smsp__inst_executed.sum"),
         "l1_data_pipe_wavefronts": (cnt("SM_A.TriageCompute.l1tex__data_pipe_lsu_wavefronts.avg")
                                     or cnt("l1tex__data_pipe_lsu_wavefronts.avg") or 0) * 148 or None,
-        "kernel_ms_under_ncu": (cnt("gpu__time_duration.sum") or 0) * {"msecond": 1.0, "usecond": 1e-3,
+        "kernel_ms_under_ncu": (cnt("gpu__time_duration.sum") or 0) * {"msecond": 1.0, "ms": 1.0, "usecond": 1e-3, "us": 1e-3, "ns": 1e-6,
                                                                        "nsecond": 1e-6}.get(u.get("gpu__time_duration.sum"), 1.0),
         "l1tex_data_pipe_pct": pct("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
         "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
