@@ -2394,6 +2394,7 @@ __global__ void __launch_bounds__(kWm1Warps * 32)
                      uint32_t ostride) {
     __shared__ uint32_t s_acc[kWm1Warps][kWmMaxRows * PW];
     __shared__ uint32_t s_perm[kWm1Warps][kWmMaxRows];
+    __shared__ uint4 s_grp[kWm1Warps][32][2];  // the batch's word data: {full lo, full hi, s0, s1}, first record
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint32_t* acc = s_acc[wib];
     for (int k = lane; k < kWmMaxRows * PW; k += 32) acc[k] = 0;
@@ -2421,6 +2422,10 @@ __global__ void __launch_bounds__(kWm1Warps * 32)
             const uint64_t fk = gv ? __ldg(fullw + wk) : 0ull;
             const uint2 sek = gv ? __ldg(rec_se + wk) : make_uint2(0u, 0u);
             const uint4 rk = sek.y > sek.x ? __ldg(rec + sek.x) : make_uint4(0u, 0u, 0u, 0u);
+            __syncwarp();  // (the previous batch's readers are done)
+            s_grp[wib][lane][0] = make_uint4(static_cast<uint32_t>(fk), static_cast<uint32_t>(fk >> 32), sek.x, sek.y);
+            s_grp[wib][lane][1] = rk;
+            __syncwarp();
             const uint32_t n = ng - gb < 32u ? ng - gb : 32u;
             const uint32_t E0 = __shfl_sync(0xffffffffu, ek0, 0);
             const uint32_t E1 = __ldg(gstart + g0 + gb + n);
@@ -2442,11 +2447,12 @@ __global__ void __launch_bounds__(kWm1Warps * 32)
                     const uint32_t starts = __reduce_or_sync(0xffffffffu, d < 32u ? 1u << d : 0u);
                     const int gi = static_cast<int>(gcount + __popc(starts & le)) - 1;
                     gcount += __popc(starts);
-                    uint32_t v0 = __shfl_sync(0xffffffffu, static_cast<uint32_t>(fk), gi);
-                    uint32_t v1 = PW == 2 ? __shfl_sync(0xffffffffu, static_cast<uint32_t>(fk >> 32), gi) : 0u;
-                    const uint32_t px = __shfl_sync(0xffffffffu, rk.x, gi), py = __shfl_sync(0xffffffffu, rk.y, gi);
-                    const uint32_t pz = __shfl_sync(0xffffffffu, rk.z, gi), pw = __shfl_sync(0xffffffffu, rk.w, gi);
-                    const uint32_t s0 = __shfl_sync(0xffffffffu, sek.x, gi), s1 = __shfl_sync(0xffffffffu, sek.y, gi);
+                    // the pair's word data: two 16-byte shared-memory reads (broadcast within a group)
+                    const uint4 ga = s_grp[wib][gi][0], gr = s_grp[wib][gi][1];
+                    uint32_t v0 = ga.x;
+                    uint32_t v1 = PW == 2 ? ga.y : 0u;
+                    const uint32_t px = gr.x, py = gr.y, pz = gr.z, pw = gr.w;
+                    const uint32_t s0 = ga.z, s1 = ga.w;
                     if ((m[u].x & px) | (m[u].y & py)) {  // the group's first partial record (zero: none)
                         if (PW == 1 || pz == 0) v0 |= pw;
                         else v1 |= pw;
