@@ -2235,15 +2235,25 @@ __device__ __forceinline__ void wm_group(const uint64_t* __restrict__ emask, con
                                          const uint32_t (&off)[2 * PW],
                                          const uint4 (&r0)[kWmSlots], const uint4 (&r1)[kWmSlots], uint32_t ns0,
                                          uint32_t ns1, const uint4* __restrict__ lrec, uint32_t m0, uint32_t mn0,
-                                         uint32_t m1, uint32_t mn1, uint32_t acc_s, int lane) {
+                                         uint32_t m1, uint32_t mn1, uint32_t acc_s, uint32_t sp, int lane) {
     constexpr uint32_t RB = 64 * PW * 4;  // accumulator bytes per row
     for (uint32_t c = e0; c < e1; c += 32) {
         const uint2 cm = __ldg(reinterpret_cast<const uint2*>(emask + c + lane));
         const uint32_t cr = __ldg(erow + c + lane);
         const int n = static_cast<int>(e1 - c < 32u ? e1 - c : 32u);
+        // the chunk's pairs {mask lo, mask hi, row byte offset} through the
+        // warp's shared-memory slice: one broadcast 16-B read per pair
+        __syncwarp();
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sp + 16u * lane), "r"(cm.x), "r"(cm.y),
+                     "r"(cr * RB), "r"(0u)
+                     : "memory");
+        __syncwarp();
         for (int i = 0; i < n; ++i) {
-            const uint32_t mlo = __shfl_sync(0xffffffffu, cm.x, i), mhi = __shfl_sync(0xffffffffu, cm.y, i);
-            const uint32_t rowi = __shfl_sync(0xffffffffu, cr, i);
+            uint32_t mlo, mhi, rowb, pad;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(mlo), "=r"(mhi), "=r"(rowb), "=r"(pad)
+                         : "r"(sp + 16u * i)
+                         : "memory");
             // full props hit any pair; a partial prop hits iff one of its
             // records does (for a pair sweeping the whole word every record
             // hits, so no special case for it)
@@ -2268,7 +2278,7 @@ __device__ __forceinline__ void wm_group(const uint64_t* __restrict__ emask, con
             }
 #pragma unroll
             for (int k = 0; k < 2 * PW; ++k)  // (an OR of 0 is a no-op: no branch around it)
-                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(rowi * RB + off[k]), "r"(v[k]) : "memory");
+                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(rowb + off[k]), "r"(v[k]) : "memory");
         }
     }
 }
@@ -2287,8 +2297,9 @@ __global__ void __launch_bounds__(kWmThreads)
     __shared__ uint32_t s_perm[kWmMaxRows];  // the task's output rows (cp.async during the task)
     constexpr int RW = 64 * PW;  // accumulator words per row: [prop half][frame]
     constexpr int NW = kWmThreads / 32;
+    __shared__ uint4 s_pair[NW][32];  // each warp's current chunk of pairs
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint32_t acc_s = smem_u32(wm_acc);
+    const uint32_t acc_s = smem_u32(wm_acc), sp = smem_u32(&s_pair[wib][0]);
     for (int k = threadIdx.x; k < rows_per_task * RW; k += kWmThreads) wm_acc[k] = 0;
     for (;;) {
         if (threadIdx.x == 0) {
@@ -2335,14 +2346,14 @@ __global__ void __launch_bounds__(kWmThreads)
             const uint32_t mn0 = ns0 > kWmSlots ? ns0 - kWmSlots : 0u, mn1 = ns1 > kWmSlots ? ns1 - kWmSlots : 0u;
             const uint32_t m0 = hd.x + kWmSlots, m1 = hd.x + ns0 + kWmSlots;
             if (mn0 | mn1)
-                wm_group<PW, kWmSlots, true>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, mn0, m1, mn1, acc_s, lane);
+                wm_group<PW, kWmSlots, true>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, mn0, m1, mn1, acc_s, sp, lane);
             else
                 switch (ns0 > ns1 ? ns0 : ns1) {  // warp-uniform: one specialised pair loop per slot-row count
-                    case 0: wm_group<PW, 0, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
-                    case 1: wm_group<PW, 1, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
-                    case 2: wm_group<PW, 2, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
-                    case 3: wm_group<PW, 3, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
-                    default: wm_group<PW, 4, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, lane); break;
+                    case 0: wm_group<PW, 0, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, lane); break;
+                    case 1: wm_group<PW, 1, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, lane); break;
+                    case 2: wm_group<PW, 2, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, lane); break;
+                    case 3: wm_group<PW, 3, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, lane); break;
+                    default: wm_group<PW, 4, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, lane); break;
                 }
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
