@@ -2235,7 +2235,8 @@ __device__ __forceinline__ void wm_group(const uint64_t* __restrict__ emask, con
                                          const uint32_t (&off)[2 * PW],
                                          const uint4 (&r0)[kWmSlots], const uint4 (&r1)[kWmSlots], uint32_t ns0,
                                          uint32_t ns1, const uint4* __restrict__ lrec, uint32_t m0, uint32_t mn0,
-                                         uint32_t m1, uint32_t mn1, uint32_t acc_s, uint32_t sp, int lane) {
+                                         uint32_t m1, uint32_t mn1, uint32_t acc_s, uint32_t sp,
+                                         const uint4* spp, int lane) {
     constexpr uint32_t RB = 64 * PW * 4;  // accumulator bytes per row
     for (uint32_t c = e0; c < e1; c += 32) {
         const uint2 cm = __ldg(reinterpret_cast<const uint2*>(emask + c + lane));
@@ -2249,11 +2250,8 @@ __device__ __forceinline__ void wm_group(const uint64_t* __restrict__ emask, con
                      : "memory");
         __syncwarp();
         for (int i = 0; i < n; ++i) {
-            uint32_t mlo, mhi, rowb, pad;
-            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(mlo), "=r"(mhi), "=r"(rowb), "=r"(pad)
-                         : "r"(sp + 16u * i)
-                         : "memory");
+            const uint4 pq = spp[i];
+            const uint32_t mlo = pq.x, mhi = pq.y, rowb = pq.z;
             // full props hit any pair; a partial prop hits iff one of its
             // records does (for a pair sweeping the whole word every record
             // hits, so no special case for it)
@@ -2277,8 +2275,10 @@ __device__ __forceinline__ void wm_group(const uint64_t* __restrict__ emask, con
                 }
             }
 #pragma unroll
-            for (int k = 0; k < 2 * PW; ++k)  // (an OR of 0 is a no-op: no branch around it)
-                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(rowb + off[k]), "r"(v[k]) : "memory");
+            for (int k = 0; k < 2 * PW; ++k)  // (an OR of 0 is a no-op: no branch around it; the
+                // accumulator block and the pair slice are disjoint, and __syncthreads
+                // orders the reductions against the row stores)
+                asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(rowb + off[k]), "r"(v[k]));
         }
     }
 }
@@ -2346,14 +2346,14 @@ __global__ void __launch_bounds__(kWmThreads)
             const uint32_t mn0 = ns0 > kWmSlots ? ns0 - kWmSlots : 0u, mn1 = ns1 > kWmSlots ? ns1 - kWmSlots : 0u;
             const uint32_t m0 = hd.x + kWmSlots, m1 = hd.x + ns0 + kWmSlots;
             if (mn0 | mn1)
-                wm_group<PW, kWmSlots, true>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, mn0, m1, mn1, acc_s, sp, lane);
+                wm_group<PW, kWmSlots, true>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, mn0, m1, mn1, acc_s, sp, s_pair[wib], lane);
             else
                 switch (ns0 > ns1 ? ns0 : ns1) {  // warp-uniform: one specialised pair loop per slot-row count
-                    case 0: wm_group<PW, 0, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, lane); break;
-                    case 1: wm_group<PW, 1, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, lane); break;
-                    case 2: wm_group<PW, 2, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, lane); break;
-                    case 3: wm_group<PW, 3, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, lane); break;
-                    default: wm_group<PW, 4, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, lane); break;
+                    case 0: wm_group<PW, 0, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, s_pair[wib], lane); break;
+                    case 1: wm_group<PW, 1, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, s_pair[wib], lane); break;
+                    case 2: wm_group<PW, 2, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, s_pair[wib], lane); break;
+                    case 3: wm_group<PW, 3, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, s_pair[wib], lane); break;
+                    default: wm_group<PW, 4, false>(emask, erow, e0, e1, fv, off, ra, rb, ns0, ns1, lrec, m0, 0, m1, 0, acc_s, sp, s_pair[wib], lane); break;
                 }
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
