@@ -2213,12 +2213,15 @@ constexpr int kWmThreads = 256;
 constexpr int kWmMaxRows = 256;  // rows per task at most (PackedShard::wm_row is a byte)
 constexpr int kWmSlots = 4;  // slot rows (per prop half) held in registers per word; more are re-read per pair
 
-// v0 |= z and v1 |= w if (mlo & x) | (mhi & y) != 0: a record test with
-// predicated ORs (plain C++ compiles to SELs, two more instructions)
+// v0 |= z and v1 |= w if (mlo & x) | (mhi & y) != 0: a record test.  A
+// lane's records of one frame are distinct props, none of them full, so the
+// bit z (w) is never already in v0 (v1) and the OR is an ADD: predicated
+// adds, which ptxas issues as IMAD.IADD on the FMA pipe, leaving the ALU pipe
+// (the kernel's binding one) the two LOP3s of the test
 __device__ __forceinline__ void rec_test(uint32_t mlo, uint32_t mhi, const uint4& r, uint32_t& v0, uint32_t& v1) {
     asm("{\n\t.reg .pred p;\n\t.reg .b32 t, u;\n\t"
         "and.b32 t, %2, %4;\n\tand.b32 u, %3, %5;\n\tor.b32 t, t, u;\n\t"
-        "setp.ne.u32 p, t, 0;\n\t@p or.b32 %0, %0, %6;\n\t@p or.b32 %1, %1, %7;\n\t}"
+        "setp.ne.u32 p, t, 0;\n\t@p add.u32 %0, %0, %6;\n\t@p add.u32 %1, %1, %7;\n\t}"
         : "+r"(v0), "+r"(v1)
         : "r"(mlo), "r"(mhi), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w));
 }
