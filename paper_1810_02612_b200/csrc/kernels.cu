@@ -1849,14 +1849,14 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
                                                         uint32_t* __restrict__ rec_cursor, uint4* __restrict__ rec,
                                                         uint32_t* __restrict__ task_ctr, int nctr,
                                                         const uint32_t* __restrict__ touched64,
-                                                        uint64_t* __restrict__ fullw) {
+                                                        uint4* __restrict__ wdat) {
     constexpr int NP = 1 << PSHIFT, WPB = NT / NP;
     // a programmatically dependent labeling launch may get resident now; it
     // waits for this grid's completion before reading our outputs
     asm volatile("griddepcontrol.launch_dependents;");
     __shared__ uint32_t s_cnt[NP][WPB];
     __shared__ uint32_t s_base[WPB];
-    __shared__ uint32_t s_full[WPB][2];  // (fullw) props full in frame 0, per word
+    __shared__ uint32_t s_full[WPB][2];  // (wdat) props full in frame 0, per word
     if (threadIdx.x < 2 * WPB) (&s_full[0][0])[threadIdx.x] = 0;
     const uint32_t gt = blockIdx.x * static_cast<uint32_t>(NT) + threadIdx.x;
     if (gt < static_cast<uint32_t>(nctr)) task_ctr[gt] = 0;
@@ -1886,10 +1886,9 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
     }
     s_cnt[j][wl] = n;
     __syncthreads();  // (also orders the s_full zeroing before the ORs)
-    if (fullw) {  // one frame: the word's full-prop mask in one u64 (label_wm1_kernel)
+    if (wdat) {  // one frame: the word's full-prop mask (label_wm1_kernel)
         if (full & 1u) atomicOr(&s_full[wl][j >> 5], 1u << (j & 31));
         __syncthreads();
-        if (j == 0 && in) fullw[w] = s_full[wl][0] | static_cast<uint64_t>(s_full[wl][1]) << 32;
     }
     if (j == 0 && in) {  // per word: exclusive prefix over props, then its segment
         uint32_t run = 0;
@@ -1901,15 +1900,22 @@ __global__ void __launch_bounds__(NT) pl_build_kernel(const uint64_t* __restrict
         const uint32_t b = run ? atomicAdd(rec_cursor, run) : 0u;
         s_base[wl] = b;
         rec_se[w] = make_uint2(b, b + run);
+        if (wdat) {  // {full lo, full hi, record range}, then the first record (below; none: zero)
+            wdat[2 * static_cast<uint64_t>(w)] = make_uint4(s_full[wl][0], s_full[wl][1], b, b + run);
+            if (!run) wdat[2 * static_cast<uint64_t>(w) + 1] = make_uint4(0u, 0u, 0u, 0u);
+        }
     }
     __syncthreads();
     if (!n) return;
     uint32_t pos = s_base[wl] + s_cnt[j][wl];
     for (int f = 0; f < frames; ++f) {
         const uint64_t x = base[static_cast<uint64_t>(f) * fstride] & valid;
-        if (x != 0 && x != valid)  // smem label accumulator word f + 64 (j / 32), bit j % 32
-            rec[pos++] = make_uint4(static_cast<uint32_t>(x), static_cast<uint32_t>(x >> 32),
-                                    4u * (static_cast<uint32_t>(f) + 64u * (j >> 5)), 1u << (j & 31));
+        if (x != 0 && x != valid) {  // smem label accumulator word f + 64 (j / 32), bit j % 32
+            const uint4 r = make_uint4(static_cast<uint32_t>(x), static_cast<uint32_t>(x >> 32),
+                                       4u * (static_cast<uint32_t>(f) + 64u * (j >> 5)), 1u << (j & 31));
+            if (wdat && pos == s_base[wl]) wdat[2 * static_cast<uint64_t>(w) + 1] = r;  // (one frame: the word's first)
+            rec[pos++] = r;
+        }
     }
 }
 
@@ -2381,34 +2387,52 @@ __global__ void __launch_bounds__(kWmThreads)
 }
 
 // ---------------------------------------------------------------------------
-// Word-major single-frame labelling (<= 64 props), dev knob LTLG_WM1=1: the
-// word-major copy of T (PackedShard::wm_*) against the one-frame prop-lane
-// summary (pl_build_kernel with frames = 1: fullw[w] = the props whose P
-// covers word w, and one record {P lo, P hi, 4 * 64 * (j / 32), 1 << j % 32}
-// per partial prop).  A warp owns a task (<= R rows; its label words in the
-// warp's slice of shared memory) and takes the task's word groups 32 at a
-// time: lane k fetches group k's full mask, record range and first record.
-// The batch's pairs are one contiguous range of T, streamed flat in chunks of
-// 32 (kWm1U chunks in flight); lane i of a chunk finds its pair's group from
-// the group starts in the chunk (one redux.sync.or + popc) and its word data
-// by shuffle: v = full | the bits of the records whose P word meets the
-// pair's mask, ORed into the row's label word(s).
+// Word-major single-frame labelling (<= 64 props): the word-major copy of T
+// (PackedShard::wm_*) against the one-frame prop-lane summary (pl_build_kernel
+// with frames = 1: wdat[w] = {full-prop mask lo, hi, record range}, then the
+// word's first partial record {P lo, P hi, 4 * 64 * (j / 32), 1 << j % 32} or
+// zeros).  A warp owns a task (<= R rows; its label words in the warp's slice
+// of shared memory) and takes the task's word groups 32 at a time.  The
+// batches' group starts and word data come by cp.async into two shared-memory
+// buffers, one batch ahead (the next batch's word ids two ahead), so no
+// dependent load chain sits between batches.  The batch's pairs are one
+// contiguous range of T, streamed flat in chunks of 32 (kWm1U chunks in
+// flight); lane i of a chunk finds its pair's group from the group starts in
+// the chunk (one redux.sync.or + popc) and reads the word data from the
+// buffer: v = full | the bits of the records whose P word meets the pair's
+// mask, ORed into the row's label word(s).
 // ---------------------------------------------------------------------------
 constexpr int kWm1Warps = 8;
-constexpr int kWm1U = 8;  // 32-pair chunks in flight per warp
+#ifndef WM1_U
+#define WM1_U 8
+#endif
+#ifdef WM1_MINB
+#define WM1_BOUNDS __launch_bounds__(kWm1Warps * 32, WM1_MINB)
+#else
+#define WM1_BOUNDS __launch_bounds__(kWm1Warps * 32)
+#endif
+constexpr int kWm1U = WM1_U;  // 32-pair chunks in flight per warp
+
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 
 template <typename SW, int PW>
-__global__ void __launch_bounds__(kWm1Warps * 32)
+__global__ void WM1_BOUNDS
     label_wm1_kernel(const uint64_t* __restrict__ emask, const uint8_t* __restrict__ erow,
                      const uint32_t* __restrict__ gword, const uint32_t* __restrict__ gstart,
                      const uint32_t* __restrict__ task_row, const uint32_t* __restrict__ task_grp,
                      uint32_t task_begin, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
-                     const uint64_t* __restrict__ fullw, const uint2* __restrict__ rec_se,
-                     const uint4* __restrict__ rec, const uint32_t* __restrict__ perm, SW* __restrict__ out,
-                     uint32_t ostride) {
+                     const uint4* __restrict__ wdat, const uint4* __restrict__ rec,
+                     const uint32_t* __restrict__ perm, SW* __restrict__ out, uint32_t ostride) {
     __shared__ uint32_t s_acc[kWm1Warps][kWmMaxRows * PW];
     __shared__ uint32_t s_perm[kWm1Warps][kWmMaxRows];
-    __shared__ uint4 s_grp[kWm1Warps][32][2];  // the batch's word data: {full lo, full hi, s0, s1}, first record
+    __shared__ __align__(16) uint4 s_grp[kWm1Warps][2][32][2];  // per batch buffer: word data, first record
+    __shared__ uint32_t s_gw[kWm1Warps][2][32];                 // word ids
+    __shared__ uint32_t s_ge[kWm1Warps][2][33];                 // group starts + the batch's end
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint32_t* acc = s_acc[wib];
     for (int k = lane; k < kWmMaxRows * PW; k += 32) acc[k] = 0;
@@ -2423,26 +2447,43 @@ __global__ void __launch_bounds__(kWm1Warps * 32)
         const uint32_t r0 = __ldg(task_row + t), nr = __ldg(task_row + t + 1) - r0;
         const uint32_t g0 = __ldg(task_grp + t), ng = __ldg(task_grp + t + 1) - g0;
         for (uint32_t r = lane; r < nr; r += 32)  // the store's row ids, in the background
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(s_perm[wib] + r)),
-                         "l"(perm + r0 + r)
-                         : "memory");
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        for (uint32_t gb = 0; gb < ng; gb += 32) {
-            // lane k: group gb + k's word-level data
-            const uint32_t k = gb + lane;
-            const bool gv = k < ng;
-            const uint32_t wk = gv ? __ldg(gword + g0 + k) : 0u;
-            const uint32_t ek0 = gv ? __ldg(gstart + g0 + k) : 0xffffffffu;
-            const uint64_t fk = gv ? __ldg(fullw + wk) : 0ull;
-            const uint2 sek = gv ? __ldg(rec_se + wk) : make_uint2(0u, 0u);
-            const uint4 rk = sek.y > sek.x ? __ldg(rec + sek.x) : make_uint4(0u, 0u, 0u, 0u);
-            __syncwarp();  // (the previous batch's readers are done)
-            s_grp[wib][lane][0] = make_uint4(static_cast<uint32_t>(fk), static_cast<uint32_t>(fk >> 32), sek.x, sek.y);
-            s_grp[wib][lane][1] = rk;
-            __syncwarp();
+            cp_async4(smem_u32(s_perm[wib] + r), perm + r0 + r);
+        // batch gb's word ids and group starts into buffer bf
+        auto fetch_starts = [&](int bf, uint32_t gb) {
             const uint32_t n = ng - gb < 32u ? ng - gb : 32u;
-            const uint32_t E0 = __shfl_sync(0xffffffffu, ek0, 0);
-            const uint32_t E1 = __ldg(gstart + g0 + gb + n);
+            if (static_cast<uint32_t>(lane) < n) {
+                cp_async4(smem_u32(&s_gw[wib][bf][lane]), gword + g0 + gb + lane);
+                cp_async4(smem_u32(&s_ge[wib][bf][lane]), gstart + g0 + gb + lane);
+            }
+            if (lane == 0) cp_async4(smem_u32(&s_ge[wib][bf][n]), gstart + g0 + gb + n);
+        };
+        // batch gb's word data into buffer bf (its word ids have landed)
+        auto fetch_words = [&](int bf, uint32_t gb) {
+            const uint32_t n = ng - gb < 32u ? ng - gb : 32u;
+            if (static_cast<uint32_t>(lane) < n) {
+                const uint4* src = wdat + 2 * static_cast<uint64_t>(s_gw[wib][bf][lane]);
+                cp_async16(smem_u32(&s_grp[wib][bf][lane][0]), src);
+                cp_async16(smem_u32(&s_grp[wib][bf][lane][1]), src + 1);
+            }
+        };
+        fetch_starts(0, 0);
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        fetch_words(0, 0);
+        if (ng > 32) fetch_starts(1, 32);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        int bf = 0;
+        for (uint32_t gb = 0; gb < ng; gb += 32, bf ^= 1) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();  // batch gb's starts and word data, batch gb + 32's starts
+            const uint32_t n = ng - gb < 32u ? ng - gb : 32u;
+            const uint32_t ek0 = static_cast<uint32_t>(lane) < n ? s_ge[wib][bf][lane] : 0xffffffffu;
+            const uint32_t E0 = s_ge[wib][bf][0], E1 = s_ge[wib][bf][n];
+            __syncwarp();  // (buffer bf's starts are in registers before batch gb + 64's land there)
+            if (gb + 32 < ng) fetch_words(bf ^ 1, gb + 32);
+            if (gb + 64 < ng) fetch_starts(bf, gb + 64);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            const uint4(*grp)[2] = s_grp[wib][bf];
             uint32_t gcount = 0;  // groups of the batch started before the chunk
             for (uint32_t c = E0; c < E1; c += 32 * kWm1U) {
                 uint2 m[kWm1U];
@@ -2462,14 +2503,13 @@ __global__ void __launch_bounds__(kWm1Warps * 32)
                     const int gi = static_cast<int>(gcount + __popc(starts & le)) - 1;
                     gcount += __popc(starts);
                     // the pair's word data: two 16-byte shared-memory reads (broadcast within a group)
-                    const uint4 ga = s_grp[wib][gi][0], gr = s_grp[wib][gi][1];
+                    const uint4 ga = grp[gi][0], gr = grp[gi][1];
                     uint32_t v0 = ga.x;
                     uint32_t v1 = PW == 2 ? ga.y : 0u;
-                    const uint32_t px = gr.x, py = gr.y, pz = gr.z, pw = gr.w;
                     const uint32_t s0 = ga.z, s1 = ga.w;
-                    if ((m[u].x & px) | (m[u].y & py)) {  // the group's first partial record (zero: none)
-                        if (PW == 1 || pz == 0) v0 |= pw;
-                        else v1 |= pw;
+                    if ((m[u].x & gr.x) | (m[u].y & gr.y)) {  // the group's first partial record (zero: none)
+                        if (PW == 1 || gr.z == 0) v0 |= gr.w;
+                        else v1 |= gr.w;
                     }
                     for (uint32_t q = s0 + 1; q < s1; ++q) {  // (rare) more partial props on the word
                         const uint4 r = __ldg(rec + q);
@@ -2556,14 +2596,14 @@ cudaError_t launch_wm_build(const uint64_t* P64, int props, int frames, uint32_t
 // the last probe round.
 struct PlLayout {
     uint64_t nt;  // (nw64 + 1) * pw
-    size_t ffr, sfr, fullw, cursor, rec_se, rec, total;
+    size_t ffr, sfr, wdat, cursor, rec_se, rec, total;
     PlLayout(int props, int frames, uint32_t nw64) {
         nt = static_cast<uint64_t>(nw64 + 1) * (props > 32 ? 64u : 32u);
         auto up = [](size_t x, size_t a) { return (x + a - 1) & ~(a - 1); };
         ffr = 0;
         sfr = ffr + nt * 8;
-        fullw = sfr + nt * 8;  // one frame: (nw64 + 1) u64 full-prop masks
-        cursor = fullw + (static_cast<size_t>(nw64) + 1) * 8;
+        wdat = up(sfr + nt * 8, 16);  // one frame: (nw64 + 1) x 32 B word data (pl_build_kernel)
+        cursor = wdat + (static_cast<size_t>(nw64) + 1) * 32;
         rec_se = up(cursor + 4, 8);
         rec = up(rec_se + (nw64 + 2) * 8, 16);
         total = rec + (nt * static_cast<uint64_t>(frames) + 32) * 16;
@@ -2591,13 +2631,13 @@ cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64,
     const int wpb = kNT >> pshift;
     const uint64_t gw = (static_cast<uint64_t>(nw64) + 1 + wpb - 1) / wpb, gc = (static_cast<uint64_t>(nctr) + kNT - 1) / kNT;
     const unsigned grid = static_cast<unsigned>(gw > gc ? gw : gc);
-    uint64_t* fullw = frames == 1 ? reinterpret_cast<uint64_t*>(wb + L.fullw) : nullptr;
+    uint4* wdat = frames == 1 ? reinterpret_cast<uint4*>(wb + L.wdat) : nullptr;
     if (pshift == 5)
         pl_build_kernel<5, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
-                                                  task_ctr, nctr, touched64, fullw);
+                                                  task_ctr, nctr, touched64, wdat);
     else
         pl_build_kernel<6, kNT><<<grid, kNT, 0, st>>>(P64, props, frames, nw64, cells, ffr, sfr, rec_se, cursor, rec,
-                                                  task_ctr, nctr, touched64, fullw);
+                                                  task_ctr, nctr, touched64, wdat);
     return cudaGetLastError();
 }
 
@@ -2671,8 +2711,8 @@ static cudaError_t launch_wm1_label(const LaunchArgs& a, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, a.wm_mask, a.wm_row, a.wm_gword, a.wm_gstart, a.wm_task_row, a.wm_task_grp,
-                              a.task_begin, a.ntasks, a.task_ctr, reinterpret_cast<const uint64_t*>(wb + L.fullw),
-                              reinterpret_cast<const uint2*>(wb + L.rec_se), reinterpret_cast<const uint4*>(wb + L.rec),
+                              a.task_begin, a.ntasks, a.task_ctr, reinterpret_cast<const uint4*>(wb + L.wdat),
+                              reinterpret_cast<const uint4*>(wb + L.rec),
                               a.perm, static_cast<SW*>(a.out), a.ostride ? a.ostride : 1u);
 }
 
