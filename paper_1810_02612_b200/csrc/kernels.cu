@@ -2433,6 +2433,7 @@ __global__ void WM1_BOUNDS
     __shared__ __align__(16) uint4 s_grp[kWm1Warps][2][32][2];  // per batch buffer: word data, first record
     __shared__ uint32_t s_gw[kWm1Warps][2][32];                 // word ids
     __shared__ uint32_t s_ge[kWm1Warps][2][33];                 // group starts + the batch's end
+    __shared__ uint64_t s_rows[kWm1Warps][33];                  // the iteration's row bytes
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint32_t* acc = s_acc[wib];
     for (int k = lane; k < kWmMaxRows * PW; k += 32) acc[k] = 0;
@@ -2487,17 +2488,27 @@ __global__ void WM1_BOUNDS
             uint32_t gcount = 0;  // groups of the batch started before the chunk
             for (uint32_t c = E0; c < E1; c += 32 * kWm1U) {
                 uint2 m[kWm1U];
-                uint32_t row[kWm1U];
 #pragma unroll
                 for (int u = 0; u < kWm1U; ++u) {  // kWm1U chunks of T in flight
                     const uint32_t e = c + 32u * u + lane;
                     m[u] = e < E1 ? __ldg(reinterpret_cast<const uint2*>(emask + e)) : make_uint2(0u, 0u);
-                    row[u] = e < E1 ? __ldg(erow + e) : 0u;
                 }
+                // the iteration's row bytes: one 8-byte load per lane over the
+                // 8-aligned window (lane 0 also its 33rd word), through shared memory
+                const uint32_t cb = c & ~7u;
+                const uint64_t* rw = reinterpret_cast<const uint64_t*>(erow + cb);
+                const uint64_t rlo = cb + 8u * lane < E1 ? __ldg(rw + lane) : 0ull;
+                const uint64_t rhi = lane == 0 && cb + 256u < E1 ? __ldg(rw + 32) : 0ull;
+                __syncwarp();  // (the previous iteration's row reads are done)
+                s_rows[wib][lane] = rlo;
+                if (lane == 0) s_rows[wib][32] = rhi;
+                __syncwarp();
+                const uint8_t* rows_b = reinterpret_cast<const uint8_t*>(s_rows[wib]) + (c - cb) + lane;
 #pragma unroll
                 for (int u = 0; u < kWm1U; ++u) {
                     const uint32_t cu = c + 32u * u;
                     if (cu >= E1) break;  // (warp-uniform)
+                    const uint32_t rowu = rows_b[32 * u];
                     const uint32_t d = ek0 - cu;  // lane k's group starts in this chunk iff d < 32
                     const uint32_t starts = __reduce_or_sync(0xffffffffu, d < 32u ? 1u << d : 0u);
                     const int gi = static_cast<int>(gcount + __popc(starts & le)) - 1;
@@ -2519,9 +2530,9 @@ __global__ void WM1_BOUNDS
                         }
                     }
                     if (cu + lane < E1) {  // (a task's rows are this warp's alone; rows of a group are distinct)
-                        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * row[u] * PW), "r"(v0) : "memory");
+                        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * rowu * PW), "r"(v0) : "memory");
                         if constexpr (PW == 2)
-                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * (row[u] * PW + 1)), "r"(v1)
+                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * (rowu * PW + 1)), "r"(v1)
                                          : "memory");
                     }
                 }
