@@ -2412,6 +2412,7 @@ constexpr int kWm1Warps = 8;
 #define WM1_BOUNDS __launch_bounds__(kWm1Warps * 32)
 #endif
 constexpr int kWm1U = WM1_U;  // 32-pair chunks in flight per warp
+constexpr int kWm1Rw = 4 * kWm1U + 1;  // u64 words of an iteration's row-byte window
 
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
@@ -2433,7 +2434,7 @@ __global__ void WM1_BOUNDS
     __shared__ __align__(16) uint4 s_grp[kWm1Warps][2][32][2];  // per batch buffer: word data, first record
     __shared__ uint32_t s_gw[kWm1Warps][2][32];                 // word ids
     __shared__ uint32_t s_ge[kWm1Warps][2][33];                 // group starts + the batch's end
-    __shared__ uint64_t s_rows[kWm1Warps][33];                  // the iteration's row bytes
+    __shared__ uint64_t s_rows[kWm1Warps][kWm1Rw];              // the iteration's row bytes
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint32_t* acc = s_acc[wib];
     for (int k = lane; k < kWmMaxRows * PW; k += 32) acc[k] = 0;
@@ -2493,15 +2494,20 @@ __global__ void WM1_BOUNDS
                     const uint32_t e = c + 32u * u + lane;
                     m[u] = e < E1 ? __ldg(reinterpret_cast<const uint2*>(emask + e)) : make_uint2(0u, 0u);
                 }
-                // the iteration's row bytes: one 8-byte load per lane over the
-                // 8-aligned window (lane 0 also its 33rd word), through shared memory
+                // the iteration's row bytes: 8-byte loads over the 8-aligned
+                // window (kWm1Rw words), through shared memory
                 const uint32_t cb = c & ~7u;
                 const uint64_t* rw = reinterpret_cast<const uint64_t*>(erow + cb);
-                const uint64_t rlo = cb + 8u * lane < E1 ? __ldg(rw + lane) : 0ull;
-                const uint64_t rhi = lane == 0 && cb + 256u < E1 ? __ldg(rw + 32) : 0ull;
+                uint64_t rwv[(kWm1Rw + 31) / 32];
+#pragma unroll
+                for (int k = 0; k < (kWm1Rw + 31) / 32; ++k) {
+                    const uint32_t i = 32u * k + lane;
+                    rwv[k] = i < static_cast<uint32_t>(kWm1Rw) && cb + 8u * i < E1 ? __ldg(rw + i) : 0ull;
+                }
                 __syncwarp();  // (the previous iteration's row reads are done)
-                s_rows[wib][lane] = rlo;
-                if (lane == 0) s_rows[wib][32] = rhi;
+#pragma unroll
+                for (int k = 0; k < (kWm1Rw + 31) / 32; ++k)
+                    if (32 * k + lane < kWm1Rw) s_rows[wib][32 * k + lane] = rwv[k];
                 __syncwarp();
                 const uint8_t* rows_b = reinterpret_cast<const uint8_t*>(s_rows[wib]) + (c - cb) + lane;
 #pragma unroll
