@@ -2536,9 +2536,9 @@ __global__ void WM1_BOUNDS
                         }
                     }
                     if (cu + lane < E1) {  // (a task's rows are this warp's alone; rows of a group are distinct)
-                        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * rowu * PW), "r"(v0) : "memory");
+                        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * rowu), "r"(v0) : "memory");
                         if constexpr (PW == 2)
-                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * (rowu * PW + 1)), "r"(v1)
+                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * (kWmMaxRows + rowu)), "r"(v1)
                                          : "memory");
                     }
                 }
@@ -2547,11 +2547,11 @@ __global__ void WM1_BOUNDS
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         for (uint32_t r = lane; r < nr; r += 32) {  // lane r stores row r's label
-            uint64_t l = acc[r * PW];
-            if constexpr (PW == 2) l |= static_cast<uint64_t>(acc[r * PW + 1]) << 32;
+            uint64_t l = acc[r];  // (prop halves in two planes: a row's two words are the same bank)
+            if constexpr (PW == 2) l |= static_cast<uint64_t>(acc[kWmMaxRows + r]) << 32;
             out[static_cast<uint64_t>(s_perm[wib][r]) * ostride] = static_cast<SW>(l);
 #pragma unroll
-            for (int h = 0; h < PW; ++h) acc[r * PW + h] = 0;
+            for (int h = 0; h < PW; ++h) acc[kWmMaxRows * h + r] = 0;
         }
         __syncwarp();
     }
