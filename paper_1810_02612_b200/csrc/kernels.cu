@@ -2404,14 +2404,14 @@ __global__ void __launch_bounds__(kWmThreads)
 // ---------------------------------------------------------------------------
 constexpr int kWm1Warps = 8;
 #ifndef WM1_U
-#define WM1_U 8
+#define WM1_U 4
 #endif
 #ifdef WM1_MINB
 #define WM1_BOUNDS __launch_bounds__(kWm1Warps * 32, WM1_MINB)
 #else
 #define WM1_BOUNDS __launch_bounds__(kWm1Warps * 32)
 #endif
-constexpr int kWm1U = WM1_U;  // 32-pair chunks in flight per warp
+constexpr int kWm1U = WM1_U;  // 32-pair chunks per iteration (two iterations in flight per warp)
 constexpr int kWm1Rw = 4 * kWm1U + 1;  // u64 words of an iteration's row-byte window
 
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
@@ -2487,26 +2487,40 @@ __global__ void WM1_BOUNDS
             asm volatile("cp.async.commit_group;" ::: "memory");
             const uint4(*grp)[2] = s_grp[wib][bf];
             uint32_t gcount = 0;  // groups of the batch started before the chunk
-            for (uint32_t c = E0; c < E1; c += 32 * kWm1U) {
-                uint2 m[kWm1U];
+            constexpr int RWL = (kWm1Rw + 31) / 32;  // row-window words per lane
+            // an iteration's T: kWm1U chunks of masks, and its row bytes as
+            // 8-byte loads over the 8-aligned window (kWm1Rw words)
+            auto load_it = [&](uint32_t c, uint2 (&m)[kWm1U], uint64_t (&rwv)[RWL]) {
 #pragma unroll
-                for (int u = 0; u < kWm1U; ++u) {  // kWm1U chunks of T in flight
+                for (int u = 0; u < kWm1U; ++u) {
                     const uint32_t e = c + 32u * u + lane;
                     m[u] = e < E1 ? __ldg(reinterpret_cast<const uint2*>(emask + e)) : make_uint2(0u, 0u);
                 }
-                // the iteration's row bytes: 8-byte loads over the 8-aligned
-                // window (kWm1Rw words), through shared memory
                 const uint32_t cb = c & ~7u;
                 const uint64_t* rw = reinterpret_cast<const uint64_t*>(erow + cb);
-                uint64_t rwv[(kWm1Rw + 31) / 32];
 #pragma unroll
-                for (int k = 0; k < (kWm1Rw + 31) / 32; ++k) {
+                for (int k = 0; k < RWL; ++k) {
                     const uint32_t i = 32u * k + lane;
                     rwv[k] = i < static_cast<uint32_t>(kWm1Rw) && cb + 8u * i < E1 ? __ldg(rw + i) : 0ull;
                 }
+            };
+            // software pipeline: the next iteration's loads are in flight
+            // during this one's processing
+            uint2 mn[kWm1U];
+            uint64_t rn[RWL];
+            load_it(E0, mn, rn);
+            for (uint32_t c = E0; c < E1; c += 32 * kWm1U) {
+                uint2 m[kWm1U];
+                uint64_t rwv[RWL];
+#pragma unroll
+                for (int u = 0; u < kWm1U; ++u) m[u] = mn[u];
+#pragma unroll
+                for (int k = 0; k < RWL; ++k) rwv[k] = rn[k];
+                if (c + 32 * kWm1U < E1) load_it(c + 32 * kWm1U, mn, rn);
+                const uint32_t cb = c & ~7u;
                 __syncwarp();  // (the previous iteration's row reads are done)
 #pragma unroll
-                for (int k = 0; k < (kWm1Rw + 31) / 32; ++k)
+                for (int k = 0; k < RWL; ++k)
                     if (32 * k + lane < kWm1Rw) s_rows[wib][32 * k + lane] = rwv[k];
                 __syncwarp();
                 const uint8_t* rows_b = reinterpret_cast<const uint8_t*>(s_rows[wib]) + (c - cb) + lane;

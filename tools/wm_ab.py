@@ -27,6 +27,7 @@ def run_one():
 
     cfg = int(os.environ.get("CFG", "4"))
     depth, E, props, F = (18, 2_000_000, 32, 64) if cfg == 4 else (20, 1_000_000, 64, 64)
+    props = int(os.environ.get("PROPS", props))
     prm = SyntheticPRM(1, depth)
     P = torch.from_numpy(props_words(1, depth, props, 0, F).view("int64")).cuda()
     T = prm.words(0, E)
