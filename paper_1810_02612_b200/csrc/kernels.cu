@@ -2474,6 +2474,28 @@ __global__ void WM1_BOUNDS
         fetch_words(0, 0);
         if (ng > 32) fetch_starts(1, 32);
         asm volatile("cp.async.commit_group;" ::: "memory");
+        constexpr int RWL = (kWm1Rw + 31) / 32;  // row-window words per lane
+        // an iteration's T: kWm1U chunks of masks, and its row bytes as
+        // 8-byte loads over the 8-aligned window (kWm1Rw words)
+        auto load_it = [&](uint32_t c, uint32_t E1, uint2 (&m)[kWm1U], uint64_t (&rwv)[RWL]) {
+#pragma unroll
+            for (int u = 0; u < kWm1U; ++u) {
+                const uint32_t e = c + 32u * u + lane;
+                m[u] = e < E1 ? __ldg(reinterpret_cast<const uint2*>(emask + e)) : make_uint2(0u, 0u);
+            }
+            const uint32_t cb = c & ~7u;
+            const uint64_t* rw = reinterpret_cast<const uint64_t*>(erow + cb);
+#pragma unroll
+            for (int k = 0; k < RWL; ++k) {
+                const uint32_t i = 32u * k + lane;
+                rwv[k] = i < static_cast<uint32_t>(kWm1Rw) && cb + 8u * i < E1 ? __ldg(rw + i) : 0ull;
+            }
+        };
+        // software pipeline: the next iteration's loads are in flight
+        // during this one's processing (across batches too: a task's
+        // batches are consecutive ranges of T)
+        uint2 mn[kWm1U];
+        uint64_t rn[RWL];
         int bf = 0;
         for (uint32_t gb = 0; gb < ng; gb += 32, bf ^= 1) {
             asm volatile("cp.async.wait_all;" ::: "memory");
@@ -2481,34 +2503,14 @@ __global__ void WM1_BOUNDS
             const uint32_t n = ng - gb < 32u ? ng - gb : 32u;
             const uint32_t ek0 = static_cast<uint32_t>(lane) < n ? s_ge[wib][bf][lane] : 0xffffffffu;
             const uint32_t E0 = s_ge[wib][bf][0], E1 = s_ge[wib][bf][n];
+            const uint32_t F1 = gb + 32 < ng ? s_ge[wib][bf ^ 1][ng - gb - 32 < 32u ? ng - gb - 32 : 32u] : E1;  // next batch's end
+            if (gb == 0) load_it(E0, E1, mn, rn);
             __syncwarp();  // (buffer bf's starts are in registers before batch gb + 64's land there)
             if (gb + 32 < ng) fetch_words(bf ^ 1, gb + 32);
             if (gb + 64 < ng) fetch_starts(bf, gb + 64);
             asm volatile("cp.async.commit_group;" ::: "memory");
             const uint4(*grp)[2] = s_grp[wib][bf];
             uint32_t gcount = 0;  // groups of the batch started before the chunk
-            constexpr int RWL = (kWm1Rw + 31) / 32;  // row-window words per lane
-            // an iteration's T: kWm1U chunks of masks, and its row bytes as
-            // 8-byte loads over the 8-aligned window (kWm1Rw words)
-            auto load_it = [&](uint32_t c, uint2 (&m)[kWm1U], uint64_t (&rwv)[RWL]) {
-#pragma unroll
-                for (int u = 0; u < kWm1U; ++u) {
-                    const uint32_t e = c + 32u * u + lane;
-                    m[u] = e < E1 ? __ldg(reinterpret_cast<const uint2*>(emask + e)) : make_uint2(0u, 0u);
-                }
-                const uint32_t cb = c & ~7u;
-                const uint64_t* rw = reinterpret_cast<const uint64_t*>(erow + cb);
-#pragma unroll
-                for (int k = 0; k < RWL; ++k) {
-                    const uint32_t i = 32u * k + lane;
-                    rwv[k] = i < static_cast<uint32_t>(kWm1Rw) && cb + 8u * i < E1 ? __ldg(rw + i) : 0ull;
-                }
-            };
-            // software pipeline: the next iteration's loads are in flight
-            // during this one's processing
-            uint2 mn[kWm1U];
-            uint64_t rn[RWL];
-            load_it(E0, mn, rn);
             for (uint32_t c = E0; c < E1; c += 32 * kWm1U) {
                 uint2 m[kWm1U];
                 uint64_t rwv[RWL];
@@ -2516,7 +2518,11 @@ __global__ void WM1_BOUNDS
                 for (int u = 0; u < kWm1U; ++u) m[u] = mn[u];
 #pragma unroll
                 for (int k = 0; k < RWL; ++k) rwv[k] = rn[k];
-                if (c + 32 * kWm1U < E1) load_it(c + 32 * kWm1U, mn, rn);
+                {  // the next iteration: this batch's, else the next batch's first
+                    const bool in = c + 32 * kWm1U < E1;
+                    const uint32_t nc = in ? c + 32 * kWm1U : E1, nb = in ? E1 : F1;
+                    if (nc < nb) load_it(nc, nb, mn, rn);
+                }
                 const uint32_t cb = c & ~7u;
                 __syncwarp();  // (the previous iteration's row reads are done)
 #pragma unroll
