@@ -2421,7 +2421,8 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
-template <typename SW, int PW>
+// MAXR: rows per task at most (128 or 256: the label block's size)
+template <typename SW, int PW, int MAXR>
 __global__ void WM1_BOUNDS
     label_wm1_kernel(const uint64_t* __restrict__ emask, const uint8_t* __restrict__ erow,
                      const uint32_t* __restrict__ gword, const uint32_t* __restrict__ gstart,
@@ -2429,15 +2430,15 @@ __global__ void WM1_BOUNDS
                      uint32_t task_begin, uint32_t ntasks, uint32_t* __restrict__ task_ctr,
                      const uint4* __restrict__ wdat, const uint4* __restrict__ rec,
                      const uint32_t* __restrict__ perm, SW* __restrict__ out, uint32_t ostride) {
-    __shared__ uint32_t s_acc[kWm1Warps][kWmMaxRows * PW];
-    __shared__ uint32_t s_perm[kWm1Warps][kWmMaxRows];
+    __shared__ uint32_t s_acc[kWm1Warps][MAXR * PW];
+    __shared__ uint32_t s_perm[kWm1Warps][MAXR];
     __shared__ __align__(16) uint4 s_grp[kWm1Warps][2][32][2];  // per batch buffer: word data, first record
     __shared__ uint32_t s_gw[kWm1Warps][2][32];                 // word ids
     __shared__ uint32_t s_ge[kWm1Warps][2][33];                 // group starts + the batch's end
     __shared__ uint64_t s_rows[kWm1Warps][kWm1Rw];              // the iteration's row bytes
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     uint32_t* acc = s_acc[wib];
-    for (int k = lane; k < kWmMaxRows * PW; k += 32) acc[k] = 0;
+    for (int k = lane; k < MAXR * PW; k += 32) acc[k] = 0;
     const uint32_t acc_s = smem_u32(acc);
     const uint32_t le = 0xffffffffu >> (31 - lane);  // lanes 0..lane
     asm volatile("griddepcontrol.wait;" ::: "memory");  // (a programmatic dependent of the summary)
@@ -2558,7 +2559,7 @@ __global__ void WM1_BOUNDS
                     if (cu + lane < E1) {  // (a task's rows are this warp's alone; rows of a group are distinct)
                         asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * rowu), "r"(v0) : "memory");
                         if constexpr (PW == 2)
-                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * (kWmMaxRows + rowu)), "r"(v1)
+                            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(acc_s + 4u * (MAXR + rowu)), "r"(v1)
                                          : "memory");
                     }
                 }
@@ -2568,10 +2569,10 @@ __global__ void WM1_BOUNDS
         __syncwarp();
         for (uint32_t r = lane; r < nr; r += 32) {  // lane r stores row r's label
             uint64_t l = acc[r];  // (prop halves in two planes: a row's two words are the same bank)
-            if constexpr (PW == 2) l |= static_cast<uint64_t>(acc[kWmMaxRows + r]) << 32;
+            if constexpr (PW == 2) l |= static_cast<uint64_t>(acc[MAXR + r]) << 32;
             out[static_cast<uint64_t>(s_perm[wib][r]) * ostride] = static_cast<SW>(l);
 #pragma unroll
-            for (int h = 0; h < PW; ++h) acc[kWmMaxRows * h + r] = 0;
+            for (int h = 0; h < PW; ++h) acc[MAXR * h + r] = 0;
         }
         __syncwarp();
     }
@@ -2724,11 +2725,11 @@ static void launch_wm_label(const LaunchArgs& a, cudaStream_t st) {
         static_cast<SW*>(a.out), a.ostride ? a.ostride : static_cast<uint32_t>(a.frames), a.wm_rows);
 }
 
-template <typename SW, int PW>
-static cudaError_t launch_wm1_label(const LaunchArgs& a, cudaStream_t st) {
+template <typename SW, int PW, int MAXR>
+static cudaError_t launch_wm1_label_r(const LaunchArgs& a, cudaStream_t st) {
     const PlLayout L(a.props, 1, a.nw64);
     const uint8_t* wb = static_cast<const uint8_t*>(a.sf);
-    auto kern = label_wm1_kernel<SW, PW>;
+    auto kern = label_wm1_kernel<SW, PW, MAXR>;
     constexpr size_t smem = 0;
     static int per_sm = 0;
     if (!per_sm) {
@@ -2751,6 +2752,12 @@ static cudaError_t launch_wm1_label(const LaunchArgs& a, cudaStream_t st) {
                               a.task_begin, a.ntasks, a.task_ctr, reinterpret_cast<const uint4*>(wb + L.wdat),
                               reinterpret_cast<const uint4*>(wb + L.rec),
                               a.perm, static_cast<SW*>(a.out), a.ostride ? a.ostride : 1u);
+}
+
+// (tasks of <= 128 rows -- the default -- take the smaller label block: more CTAs per SM)
+template <typename SW, int PW>
+static cudaError_t launch_wm1_label(const LaunchArgs& a, cudaStream_t st) {
+    return a.wm_rows <= 128 ? launch_wm1_label_r<SW, PW, 128>(a, st) : launch_wm1_label_r<SW, PW, kWmMaxRows>(a, st);
 }
 
 template <int FMT, typename SW, int FPL, bool FULL>
