@@ -11,7 +11,10 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "_lib")
-GPU_SO = os.environ.get("LTLG_DEV_SO") or os.path.join(LIB_DIR, "libltlgrid_gpu.so")  # (dev A/B builds)
+# the A/B build: the product library plus the variants reached only through
+# dev knobs (csrc/Makefile); tests and dev tools load it with LTLG_DEV_SO
+AB_SO = os.path.join(LIB_DIR, "libltlgrid_gpu_ab.so")
+GPU_SO = os.environ.get("LTLG_DEV_SO") or os.path.join(LIB_DIR, "libltlgrid_gpu.so")
 
 LTLG_OK, LTLG_EINVAL, LTLG_EFORMAT, LTLG_EIO, LTLG_ECUDA, LTLG_ENCCL, LTLG_ENOMEM, LTLG_ESTATE, LTLG_EDOMAIN = range(9)
 

@@ -23,6 +23,13 @@
 #include "engine.h"
 #include "launch.h"
 
+// The dev knobs that select A/B-only kernels (kernels.cu LTLG_AB_BUILD) act
+// in the A/B build only; the product library always takes the default path.
+#ifndef LTLG_AB_BUILD
+#define LTLG_AB_BUILD 0
+#endif
+#define AB_KNOB(expr, product_value) (LTLG_AB_BUILD ? (expr) : (product_value))
+
 
 using namespace ltlg;
 
@@ -306,7 +313,7 @@ bool use_wm1(int props, uint32_t nw64) {
 // or a dev knob asks for it.
 bool need_stream64(uint64_t cols) {
     const uint32_t nw64 = static_cast<uint32_t>((cols + 63) / 64);
-    return getenv("LTLG_WM1") || env_off("LTLG_WORDMAJOR") || !use_wm1(1, nw64);
+    return getenv("LTLG_WM1") || AB_KNOB(env_off("LTLG_WORDMAJOR"), false) || !use_wm1(1, nw64);
 }
 
 ltlg_status load_words(ltlg_ctx* ctx, WordCsr& t) {
@@ -484,7 +491,7 @@ ltlg_status run_label_per_frame(ltlg_ctx* ctx, Shard& s, uint32_t nw64) {
     const bool prof = ctx->opts.profile != 0;
     if (prof) CK(cudaEventRecord(s.ev[1], s.stream), "event");
     const size_t pw = static_cast<size_t>(props) * nw64;  // u64 words of one frame's P
-    static const bool wm_ok = !env_off("LTLG_WORDMAJOR");
+    static const bool wm_ok = AB_KNOB(!env_off("LTLG_WORDMAJOR"), true);
     const bool wm1 = wm_ok && s.wm_rows > 0 && use_wm1(props, nw64);  // (as for one frame, frame by frame)
     if (wm1) CK(s.pb.sf.reserve(pl_work_bytes(props, 1, nw64)), "allocate summary");
     for (int f = 0; f < frames; ++f) {
@@ -571,7 +578,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         }
         const uint32_t nw64 = nw32 / 2;
         // 64-cell-word single-frame path (dev knob LTLG_STREAM64=0 selects the 32-cell copy for A/B runs)
-        static const bool wide_ok = !getenv("LTLG_STREAM64") || atoi(getenv("LTLG_STREAM64")) != 0;
+        static const bool wide_ok = AB_KNOB(!getenv("LTLG_STREAM64") || atoi(getenv("LTLG_STREAM64")) != 0, true);
         const bool wide = wide_ok && frames == 1;
         if (P_host && !wide)  // the fused upload only exists on the single-frame 64-cell path
             CK(cudaMemcpyAsync(s.pb.b.ptr, P_host, static_cast<size_t>(frames) * props * nw64 * 8,
@@ -609,7 +616,7 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         const bool pl = wide_b_ok && pl_ok && frames > 1 && props <= 64 && pl_worst < (uint64_t(1) << 31);
         // word-major kernel (label_wm_kernel) over the prop-lane summary; dev knob
         // LTLG_WORDMAJOR=0: the pair-major label_pl_kernel, for A/B runs
-        static const bool wm_ok = !getenv("LTLG_WORDMAJOR") || atoi(getenv("LTLG_WORDMAJOR")) != 0;
+        static const bool wm_ok = AB_KNOB(!getenv("LTLG_WORDMAJOR") || atoi(getenv("LTLG_WORDMAJOR")) != 0, true);
         const bool wm = wm_ok && s.wm_rows > 0;
         // one frame: the word-major single-frame kernel (label_wm1_kernel) over
         // the one-frame prop-lane summary where the stream64 kernel's split
@@ -624,9 +631,14 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
         const int nslice = pl ? (frames + 63) / 64 : 1;
         // dev knob LTLG_TC=1: the tcgen05 kind::i8 formulation (tc_i8.cu) on
         // the word-major copy instead of label_wm_kernel (measured, not kept)
-        static const bool tc_on = getenv("LTLG_TC") && atoi(getenv("LTLG_TC")) != 0;
+        static const bool tc_on = AB_KNOB(getenv("LTLG_TC") && atoi(getenv("LTLG_TC")) != 0, false);
         const bool tc = pl && wm && tc_on && s.wm_rows <= 128;
-        CK(s.pb.sf.reserve(tc ? tc_work_bytes(nw64)
+#if LTLG_AB_BUILD
+        const size_t tc_bytes = tc ? tc_work_bytes(nw64) : 0;
+#else
+        const size_t tc_bytes = 0;
+#endif
+        CK(s.pb.sf.reserve(tc ? tc_bytes
                         : pl && wm ? wm_work_bytes(props, nw64)
                         : wm1 ? pl_work_bytes(props, 1, nw64)
                         : pl ? pl_work_bytes(props, std::min(frames, 64), nw64)
@@ -665,10 +677,12 @@ ltlg_status run_label(ltlg_ctx* ctx, bool split) {
                                 s.pb.ctr.ptr, nctr, s.stream, P_host ? s.pb.b.ptr : nullptr,
                                 pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
+#if LTLG_AB_BUILD
         else if (tc)
             CK(launch_tc_build(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.pb.sf.ptr,
                                s.pb.ctr.ptr, nctr, s.stream, pl_touched_on() ? s.touched64.ptr : nullptr),
                "summary kernel");
+#endif
         else if (pl && wm)
             CK(launch_wm_build(s.Pdev() + static_cast<size_t>(f0) * props * nw64, props, nf, nw64, ctx->cells, s.pb.sf.ptr,
                                s.pb.sf.bytes, s.pb.ctr.ptr, nctr, sst, pl_touched_on() ? s.touched64.ptr : nullptr),

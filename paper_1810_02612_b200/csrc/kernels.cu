@@ -68,6 +68,13 @@ struct Fmt<64> {
     using E = SF<uint64_t>;
 };
 
+// LTLG_AB_BUILD=1 (libltlgrid_gpu_ab.so, tests and dev tools only): also the
+// A/B variants the dispatch reaches only through dev knobs -- the 32-cell
+// single-frame kernels, the pair-major prop-lane kernel, the tcgen05 kind::i8
+// formulation.  The product library leaves them out.
+#ifndef LTLG_AB_BUILD
+#define LTLG_AB_BUILD 0
+#endif
 constexpr uint32_t kOver16 = 0x80000000u;
 constexpr uint32_t kOver32 = 0x10000u;
 
@@ -754,6 +761,7 @@ __device__ __forceinline__ void stage_table(uint8_t* dst, const void* src, uint3
     __syncthreads();
 }
 
+#if LTLG_AB_BUILD  // 32-cell single-frame kernel (A/B knob LTLG_STREAM64=0)
 // Register-prefetch variant (tables in L1 / 64-prop entries, or A/B runs):
 // the next chunk is loaded in place (IP) half by half, or double-buffered.
 template <int FMT, typename SW, bool SMEM, int K, int NT, bool IP>
@@ -846,6 +854,7 @@ __global__ void __launch_bounds__(NT)
 // -- 41% fewer pairs per row than 32-cell words at 512^2 --
 // against the 64-cell split summary (summary64_kernel).  Same lane
 // ownership, in-place prefetch and row segmentation as label_stream_kernel.
+#endif  // LTLG_AB_BUILD
 // TABLOC: 0 = split table read through L1, 1 = all of it in shared memory,
 // 2 = M (every pair) in shared memory and X (partial-prop lanes only) through
 // L1 -- for grids whose full table exceeds shared memory.
@@ -1077,6 +1086,7 @@ __global__ void __launch_bounds__(NT)
     }
 }
 
+#if LTLG_AB_BUILD  // 32-cell single-frame TMA-ring kernel (A/B knob LTLG_STREAM_CFG=4)
 // TMA-ring variant (split table in shared memory): every warp streams its
 // chunks through a 2-slot ring of 32*K-pair buffers filled by
 // cp.async.bulk (TMA) with one mbarrier per slot.  A chunk is copied into
@@ -1200,6 +1210,7 @@ __global__ void __launch_bounds__(NT)
     if (ct != ~0u) stream_close_task(sc, rs);
 }
 
+#endif  // LTLG_AB_BUILD
 // ---------------------------------------------------------------------------
 // F frames.  Persistent warps pull tasks; lane l owns frames l, l+32, ...
 // (FPL of them; FULL = every lane owns exactly FPL frames).  Each T pair is
@@ -1528,6 +1539,7 @@ static int env_int(const char* name, int dflt) {
     return v && *v ? atoi(v) : dflt;
 }
 
+#if LTLG_AB_BUILD  // launchers of the 32-cell single-frame kernels
 bool stream_table_in_smem(int props, uint32_t nw32) {
     static const int want = env_int("LTLG_STREAM_TABLE", -1);
     if (want == 0 || entry_format(props) == 64) return false;
@@ -1601,6 +1613,7 @@ static cudaError_t launch_stream_t(const LaunchArgs& a, cudaStream_t st) {
     }
     return launch_stream_v<FMT, SW, false, kStreamK, 256, true>(a, st);
 }
+#endif  // LTLG_AB_BUILD
 
 // Where the 64-cell single-frame kernel keeps its split table (TABLOC).
 int stream64_table_loc(int props, uint32_t nw64) {
@@ -2082,6 +2095,7 @@ __global__ void __launch_bounds__(NT) wm_build_kernel(const uint64_t* __restrict
     }
 }
 
+#if LTLG_AB_BUILD  // pair-major prop-lane kernel (A/B knob LTLG_WORDMAJOR=0)
 // 32x32 bit transpose across the warp: in, lane l holds row l; out, lane l
 // holds column l (bit r = row r's bit l).
 __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
@@ -2192,6 +2206,7 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+#endif  // LTLG_AB_BUILD
 // ---------------------------------------------------------------------------
 // Word-major multi-frame labelling (<= 64 frames per launch, <= 64 props).
 //
@@ -2681,6 +2696,7 @@ cudaError_t launch_pl(const uint64_t* P64, int props, int frames, uint32_t nw64,
 
 size_t pl_work_bytes(int props, int frames, uint32_t nw64) { return PlLayout(props, frames, nw64).total; }
 
+#if LTLG_AB_BUILD
 template <typename SW, int PW>
 static void launch_pl_label(const LaunchArgs& a, cudaStream_t st) {
     const PlLayout L(a.props, a.frames, a.nw64);
@@ -2698,6 +2714,7 @@ static void launch_pl_label(const LaunchArgs& a, cudaStream_t st) {
                                               reinterpret_cast<const uint4*>(wb + L.rec), a.frames, a.perm,
                                               static_cast<SW*>(a.out), a.ostride ? a.ostride : static_cast<uint32_t>(a.frames));
 }
+#endif  // LTLG_AB_BUILD
 
 template <typename SW, int PW>
 static void launch_wm_label(const LaunchArgs& a, cudaStream_t st) {
@@ -2793,8 +2810,10 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
             case 4: e = launch_wm1_label<uint32_t, 1>(a, st); break;
             default: e = launch_wm1_label<uint64_t, 2>(a, st); break;
         }
+#if LTLG_AB_BUILD
     } else if (a.prop_lane && a.word_major && a.tc) {  // dev knob LTLG_TC=1: tcgen05 kind::i8
         e = launch_tc_label(a, st);
+#endif
     } else if (a.prop_lane && a.word_major) {  // word-major multi-frame path (<= 64 props, a slice of <= 64 frames)
         switch (a.label_bytes) {
             case 1: launch_wm_label<uint8_t, 1>(a, st); break;
@@ -2802,6 +2821,7 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
             case 4: launch_wm_label<uint32_t, 1>(a, st); break;
             default: launch_wm_label<uint64_t, 2>(a, st); break;
         }
+#if LTLG_AB_BUILD
     } else if (a.mask_b64 && a.prop_lane) {  // pair-major prop-lane kernel (A/B: LTLG_WORDMAJOR=0)
         switch (a.label_bytes) {
             case 1: launch_pl_label<uint8_t, 1>(a, st); break;
@@ -2809,6 +2829,7 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
             case 4: launch_pl_label<uint32_t, 1>(a, st); break;
             default: launch_pl_label<uint64_t, 2>(a, st); break;
         }
+#endif
     } else if (a.frames == 1 && a.t64) {  // 64-cell-word single-frame path (<= 32 props)
         switch (a.label_bytes) {
             case 1: e = launch_stream64_t<16, uint8_t>(a, st); break;
@@ -2817,12 +2838,16 @@ cudaError_t launch_label(const LaunchArgs& a, cudaStream_t st) {
             default: e = launch_stream64_t<64, uint64_t>(a, st); break;
         }
     } else if (a.frames == 1) {
+#if LTLG_AB_BUILD
         switch (a.label_bytes) {
             case 1: e = launch_stream_t<16, uint8_t>(a, st); break;
             case 2: e = launch_stream_t<16, uint16_t>(a, st); break;
             case 4: e = launch_stream_t<32, uint32_t>(a, st); break;
             default: e = launch_stream_t<64, uint64_t>(a, st); break;
         }
+#else
+        e = cudaErrorNotSupported;  // (the 32-cell single-frame kernels are in the A/B build only)
+#endif
     } else if (a.mask_b64) {  // 64-cell-word multi-frame path (<= 32 props)
         switch (a.label_bytes) {
             case 1: launch_batch64_fpl<uint8_t>(a, st); break;

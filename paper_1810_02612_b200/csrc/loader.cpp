@@ -17,6 +17,11 @@
 
 #include "engine.h"
 
+#ifndef LTLG_AB_BUILD
+#define LTLG_AB_BUILD 0
+#endif
+
+
 namespace ltlg {
 
 int host_threads() {
@@ -526,7 +531,11 @@ void build_stream_layout(const WordCsr& t, uint64_t row_begin, uint64_t row_end,
     }
     // The 32-cell single-frame copy is only streamed by the A/B knob
     // LTLG_STREAM64=0 (every prop count runs the 64-cell copy by default).
+#if LTLG_AB_BUILD  // (the 32-cell single-frame kernels exist in the A/B build only)
     const char* knob = std::getenv("LTLG_STREAM64");
+#else
+    const char* knob = nullptr;
+#endif
     if (!knob || std::atoi(knob) != 0) {
         out->pairs_stream.assign(kPairPad, Pair{0, sentinel_word | kHead});
         out->task_pair_stream = dst_off;

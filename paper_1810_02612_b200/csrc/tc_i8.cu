@@ -1,7 +1,8 @@
 // tc_i8.cu -- the tcgen05 kind::i8 formulation of the multi-frame labelling
 // (north_star: "a tcgen05 kind::i8 dense-contraction variant (threshold > 0)
-// is kept only if ncu shows it beating the bit-packed path").  Dev knob
-// LTLG_TC=1; measured against label_wm_kernel in DESIGN.md (N1).
+// is kept only if ncu shows it beating the bit-packed path").  In the A/B
+// build only (libltlgrid_gpu_ab.so, dev knob LTLG_TC=1); measured against
+// label_wm_kernel in DESIGN.md (N1).
 //
 // Per word group of the word-major copy (rows sharing 64-cell word w):
 //   A (M = 128 rows x K = 64 cells, u8 0/1): the group's pair masks, expanded

@@ -42,6 +42,21 @@ def test_library_is_sm100a_only():
     assert "sm_90" not in out and "sm_80" not in out
 
 
+def test_product_library_leaves_out_the_ab_variants():
+    # the A/B-only kernels (dev knobs) live in libltlgrid_gpu_ab.so; the product
+    # library carries the default dispatch's kernels only
+    def kernels(so):
+        out = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+        return set(re.findall(r"Function : \S*?(label_\w+?_kernel|tc_build_kernel)", out))
+    if subprocess.run(["which", "cuobjdump"], capture_output=True).returncode:
+        pytest.skip("cuobjdump not on PATH")
+    prod, ab = kernels(N.GPU_SO), kernels(N.AB_SO)
+    dev_only = {"label_stream_kernel", "label_stream_tma_kernel", "label_pl_kernel", "label_tc_kernel", "tc_build_kernel"}
+    assert {"label_wm_kernel", "label_wm1_kernel", "label_stream64_kernel"} <= prod
+    assert not prod & dev_only
+    assert dev_only <= ab and prod <= ab
+
+
 def test_no_cpu_fallback_without_device():
     if has_gpu():
         pytest.skip("a GPU is present")

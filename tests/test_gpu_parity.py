@@ -809,11 +809,14 @@ def test_config5_dense_grid_slice():
     {"LTLG_TC": "1"},                                                       # tcgen05 kind::i8 multi-frame
 ])
 def test_ab_variants_parity(knobs):
-    # the A/B kernel variants (env knobs, read once per process) stay bit-exact
+    # the A/B kernel variants (env knobs, read once per process) stay bit-exact;
+    # they run on the A/B build of the library (the product one leaves them out)
     import subprocess
     import sys
 
-    env = dict(os.environ, **knobs)
+    from paper_1810_02612_b200._native import AB_SO
+
+    env = dict(os.environ, LTLG_DEV_SO=AB_SO, **knobs)
     r = subprocess.run([sys.executable, os.path.join(os.path.dirname(GOLDEN), "..", "tools", "ab_parity.py")],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr

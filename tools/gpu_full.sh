@@ -24,6 +24,6 @@ timeout 900 env WM_CHILD=1 CFG=5 OUT=/tmp/wm.npy ncu --set full --clock-control 
     -o $out/${tag}_cfg5batch python tools/wm_ab.py > $out/${tag}_ncu_cfg5batch.log 2>&1; echo "ncu cfg5 batch rc=$?"
 timeout 900 env WM_CHILD=1 CFG=5 SINGLE=1 OUT=/tmp/wm.npy ncu --set full --clock-control none --import-source on -k regex:"label_wm1|label_stream" -s 3 -c 1 \
     -o $out/${tag}_cfg5stream python tools/wm_ab.py > $out/${tag}_ncu_cfg5stream.log 2>&1; echo "ncu cfg5 stream rc=$?"
-timeout 900 env WM_CHILD=1 CFG=5 LTLG_TC=1 OUT=/tmp/wm.npy ncu --set full --clock-control none --import-source on -k regex:"label_tc" -s 1 -c 1 \
+timeout 900 env WM_CHILD=1 CFG=5 LTLG_TC=1 LTLG_DEV_SO=paper_1810_02612_b200/_lib/libltlgrid_gpu_ab.so OUT=/tmp/wm.npy ncu --set full --clock-control none --import-source on -k regex:"label_tc" -s 1 -c 1 \
     -o $out/${tag}_cfg5tc python tools/wm_ab.py > $out/${tag}_ncu_cfg5tc.log 2>&1; echo "ncu cfg5 tc rc=$?"
 ls -la $out

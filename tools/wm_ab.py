@@ -64,7 +64,10 @@ if __name__ == "__main__":
         sys.exit(0)
     import numpy as np
 
-    variants = [("wm128", {"ROWS": "128"}), ("pl", {"LTLG_WORDMAJOR": "0"}), ("tc", {"LTLG_TC": "1"})]
+    from paper_1810_02612_b200._native import AB_SO  # (pl, tc: A/B build only)
+
+    variants = [("wm128", {"ROWS": "128"}), ("pl", {"LTLG_WORDMAJOR": "0", "LTLG_DEV_SO": AB_SO}),
+                ("tc", {"LTLG_TC": "1", "LTLG_DEV_SO": AB_SO})]
     if os.environ.get("VARIANTS"):
         variants = [v for v in variants if v[0] in os.environ["VARIANTS"].split(",")]
     ref = None
