@@ -14,6 +14,26 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("chunk", range(5))
 def test_randomised_engine_configs(chunk):
+    run_chunk(chunk)
+
+
+@pytest.mark.parametrize("chunk", range(5, 8))
+def test_randomised_engine_configs_word_major_single_frame(chunk):
+    # the same with every single frame on label_wm1_kernel (LTLG_WM1=1, read
+    # once per process: a child process) -- the fuzz grids are small enough for
+    # the stream64 kernel otherwise; task_rows 256 takes its 256-row label block
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = f"import sys; sys.path[:0] = [{os.path.dirname(here)!r}, {here!r}]; import test_gpu_fuzz as t; t.run_chunk({chunk})"
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LTLG_WM1="1"), capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def run_chunk(chunk):
     import torch
 
     from paper_1810_02612_b200 import CsrBoolMatrix, LabelEngine, LabelMatrix
