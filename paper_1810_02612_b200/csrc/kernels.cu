@@ -2407,15 +2407,17 @@ __global__ void __launch_bounds__(kWmThreads)
 // with frames = 1: wdat[w] = {full-prop mask lo, hi, record range}, then the
 // word's first partial record {P lo, P hi, 4 * 64 * (j / 32), 1 << j % 32} or
 // zeros).  A warp owns a task (<= R rows; its label words in the warp's slice
-// of shared memory) and takes the task's word groups 32 at a time.  The
-// batches' group starts and word data come by cp.async into two shared-memory
-// buffers, one batch ahead (the next batch's word ids two ahead), so no
-// dependent load chain sits between batches.  The batch's pairs are one
-// contiguous range of T, streamed flat in chunks of 32 (kWm1U chunks in
-// flight); lane i of a chunk finds its pair's group from the group starts in
-// the chunk (one redux.sync.or + popc) and reads the word data from the
-// buffer: v = full | the bits of the records whose P word meets the pair's
-// mask, ORed into the row's label word(s).
+// of shared memory, one plane per prop half) and takes the task's word groups
+// 32 at a time.  The batches' group starts and word data come by cp.async into
+// two shared-memory buffers, one batch ahead (the next batch's word ids two
+// ahead), so no dependent load chain sits between batches.  A task's batches
+// are consecutive ranges of T, streamed as a software pipeline of iterations
+// of kWm1U chunks of 32 pairs: the next iteration's masks and row-byte window
+// (8-byte loads, staged through shared memory) are in flight while this one
+// is processed, across batch boundaries too.  Lane i of a chunk finds its
+// pair's group from the group starts in the chunk (one redux.sync.or + popc)
+// and reads the word data from the buffer: v = full | the bits of the records
+// whose P word meets the pair's mask, ORed into the row's label word(s).
 // ---------------------------------------------------------------------------
 constexpr int kWm1Warps = 8;
 #ifndef WM1_U
