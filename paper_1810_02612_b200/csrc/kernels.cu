@@ -2207,6 +2207,7 @@ __global__ void __launch_bounds__(256)
 }
 
 #endif  // LTLG_AB_BUILD
+
 // ---------------------------------------------------------------------------
 // Word-major multi-frame labelling (<= 64 frames per launch, <= 64 props).
 //
@@ -2218,8 +2219,10 @@ __global__ void __launch_bounds__(256)
 // prop half.  Per group a warp reads, once, the word's full-prop masks of the
 // lane's frames (ffrT) and the lane's partial records (slot rows of 32: each
 // lane's own records of fa / fb, {P lo, P hi, bit if fa, bit if fb}), into
-// registers, then streams the group's pairs (broadcast one at a time by
-// shuffle) past them: v_fa = full props | bits of the records with m & P != 0
+// registers, then streams the group's pairs (staged 32 at a time in the
+// warp's shared-memory slice, one broadcast 16-B read each) past them:
+// v_fa = full props | bits of the records with m & P != 0 (two LOP3s and a
+// predicated add per record: see rec_test)
 // (likewise v_fb), and one red.shared.or per accumulator word.  Every lane
 // ORs into its own frame's word, so the 32 lanes hit 32 distinct banks.
 // acc is the CTA's shared-memory label block, frame-major per row (several
