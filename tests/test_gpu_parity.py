@@ -822,6 +822,20 @@ def test_ab_variants_parity(knobs):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("knobs", [{"LTLG_TC": "1"}, {"LTLG_WORDMAJOR": "0"}, {"LTLG_STREAM64": "0"}])
+def test_product_library_ignores_ab_knobs(knobs):
+    # the product library has no A/B kernels: their knobs leave the default
+    # dispatch in place (and the labels bit-exact)
+    import subprocess
+    import sys
+
+    env = {k: v for k, v in os.environ.items() if k != "LTLG_DEV_SO"}
+    env.update(knobs)
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(GOLDEN), "..", "tools", "ab_parity.py")],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 def test_edge_counting_vs_golden_and_oracle():
     """ltlg_edge_counting == label_edge_counting (label.cpp:140-148) for every
     edge: the reference-generated seed-4444 fixture (test_label.cpp:155-185),
