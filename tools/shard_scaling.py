@@ -5,7 +5,7 @@ hold, N = 1, 2, 4, 8 -- the compute side of strong scaling, measured on one GPU
 (P resident; the per-step NCCL broadcast of P is not included).  Prints the
 max over the ranks (what bench.py's max-over-ranks timing sees) and the mean.
 
-  python tools/shard_scaling.py
+  python tools/shard_scaling.py            (NS="1 8" ROWS=113: ranks, word-major task rows)
 """
 import os
 import statistics
@@ -28,7 +28,7 @@ for n in [int(x) for x in os.environ.get("NS", "1 2 4 8").split()]:
     per, summ, pipe = [], [], []
     for r in range(n):
         ids, so, w, m = bench.spatial_shard(T.offsets, T.words, T.masks, r, n)
-        eng = LabelEngine(devices=[0], profile=True)
+        eng = LabelEngine(devices=[0], profile=True, task_rows=int(os.environ.get("ROWS", "0")))
         eng.load_abstraction_words(len(ids), 1 << depth, so, w, m)
         ts, ss = [], []
         for it in range(10):
