@@ -302,6 +302,12 @@ def cpu_baseline(quick: bool):
     small = RefSlice(CFG4["depth"], 16_000)
     c4_1 = small.protocol(CFG4["props"], q, 1)
     small.close()
+    # config 5 (1024^2, 64 props): a 10k-row slice of the same T the GPU's
+    # 1M-row shard starts with, scaled to the shard (slice + scale)
+    c5s = RefSlice(20, 2_000 if quick else 10_000)
+    c5 = c5s.protocol(64, q, 0, seed=SEED_P)
+    c5s.close()
+    scale5 = 1_000_000 / c5s.rows
     scale3 = CFG4["edges"] / big.rows
     return {
         "value": c4["edge_labels_per_s_p50"], "unit": UNIT, "cores": host["hardware_concurrency"], "kind": big.kind,
@@ -310,6 +316,9 @@ def cpu_baseline(quick: bool):
         "host": host, "config4": c4, "config4_workers1": c4_1,
         "config3": dict(c3, p50_ms_2M_extrapolated=c3["p50_ms"] * scale3,
                         note=f"{big.rows}-row slice; p50 x{scale3:g} for the 2M rows is extrapolated (linear in rows)"),
+        "config5": dict(c5, p50_ms_1M_shard_extrapolated=c5["p50_ms"] * scale5,
+                        note=f"{c5s.rows}-row slice of the 8M-edge T (1024^2, 64 props); p50 x{scale5:g} for the "
+                             f"1M-row shard is extrapolated (linear in rows)"),
     }
 
 
@@ -747,6 +756,9 @@ def main():
         if lat is not None:  # the reference's config-3 p50 beside ours
             lat["cpu_reference_p50_ms"] = cpu["config3"]["p50_ms_2M_extrapolated"]
             lat["cpu_reference_what"] = cpu["config3"]["note"] + f"; {cpu['cores']} threads"
+        if cfg5 is not None and cfg5.get("single_frame"):  # and its config-5 shard p50 beside ours
+            cfg5["single_frame"]["cpu_reference_p50_ms"] = cpu["config5"]["p50_ms_1M_shard_extrapolated"]
+            cfg5["single_frame"]["cpu_reference_what"] = cpu["config5"]["note"] + f"; {cpu['cores']} threads"
 
     if rank == 0:
         # gpu_launches: our kernels per step = wm_build (the word-major summary) and label_wm
