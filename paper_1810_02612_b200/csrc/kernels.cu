@@ -2461,11 +2461,17 @@ __global__ void WM1_BOUNDS
     for (int k = lane; k < MAXR * PW; k += 32) acc[k] = 0;
     const uint32_t acc_s = smem_u32(acc);
     const uint32_t le = 0xffffffffu >> (31 - lane);  // lanes 0..lane
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // (a programmatic dependent of the summary)
-    for (;;) {
-        uint32_t t = 0;
-        if (lane == 0) t = task_begin + atomicAdd(task_ctr, 1u);
-        t = __shfl_sync(0xffffffffu, t, 0);
+    // a warp's first task is static (task_begin + its grid-wide warp index), so
+    // its T-side data (row ids, group starts and word ids) is fetched before
+    // the summary this kernel depends on is complete (programmatic dependent
+    // launch); later tasks come from the counter the summary resets
+    const uint32_t nwarps = gridDim.x * kWm1Warps;
+    uint32_t t = task_begin + blockIdx.x * kWm1Warps + wib;
+    for (bool first = true;; first = false) {
+        if (!first) {
+            if (lane == 0) t = task_begin + nwarps + atomicAdd(task_ctr, 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+        }
         if (t >= ntasks) break;
         const uint32_t r0 = __ldg(task_row + t), nr = __ldg(task_row + t + 1) - r0;
         const uint32_t g0 = __ldg(task_grp + t), ng = __ldg(task_grp + t + 1) - g0;
@@ -2490,7 +2496,9 @@ __global__ void WM1_BOUNDS
             }
         };
         fetch_starts(0, 0);
-        asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (first) asm volatile("griddepcontrol.wait;" ::: "memory");  // (the summary's outputs from here on)
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
         fetch_words(0, 0);
         if (ng > 32) fetch_starts(1, 32);
