@@ -877,6 +877,12 @@ __global__ void __launch_bounds__(NT)
     const uint32_t xoff = split64_x_offset(FMT, nw64);
     const uint8_t* tab = static_cast<const uint8_t*>(tab_g);
     const uint8_t* xg = static_cast<const uint8_t*>(tab_g) + xoff;  // X in global memory
+    {  // the warp's static first task (below): its first chunk of T into L2
+       // while the summary is still running
+        const uint32_t t0 = task_begin + blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+        if (t0 < ntasks && __ldg(task_n + t0) >= CH && static_cast<uint32_t>(lane) * 128u < kChunk64Bytes)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(t64 + __ldg(task_byte + t0) + lane * 128u));
+    }
     // launched as a programmatic dependent of the summary kernel: its table,
     // S words and the reset task counter are ready after this
     asm volatile("griddepcontrol.wait;" ::: "memory");
